@@ -1,0 +1,418 @@
+// Stage GEMM for the AMDP executor: C = epi(alpha * A * B^T), bf16 in, fp32 accumulate.
+//
+// sm_100a design (no mma.sync / wgmma):
+//   * persistent CTAs (grid <= #SMs), one 128x256 output tile at a time,
+//   * warp 0 / lane 0: TMA producer into a 4-stage smem ring (SWIZZLE_128B),
+//   * warp 1 / lane 0: tcgen05.mma issuer (M=128, N=256, K=16 per instruction),
+//     accumulating in TMEM; two 256-column accumulators so the epilogue of tile i
+//     overlaps the main loop of tile i+1,
+//   * warps 4..7: epilogue (tcgen05.ld -> registers -> fused op -> global).
+// Operands may be K-major or MN-major independently, so forward (X W^T),
+// activation-gradient (dY W) and weight-gradient (dY^T X) all run without
+// transposes. Epilogues: plain bf16 store, GELU (stores pre-activation too),
+// residual add, fp32 accumulate (weight-gradient accumulation across the
+// minibatches of one AMDP window), GELU-backward.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "amdp_kernels.h"
+#include "sm100_ptx.cuh"
+
+namespace amdp {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KiB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int NUM_THREADS = 256;
+constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
+constexpr int GROUP_M = 8;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+
+struct EpiParams {
+  int M, N, K;
+  void* C;
+  int ldc;
+  const __nv_bfloat16* aux;
+  int ld_aux;
+  __nv_bfloat16* C2;
+  int ldc2;
+  float alpha;
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * x * (1.f + t);
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  const int in_group = GROUP_M * tiles_n;
+  const int g = t / in_group;
+  const int first_m = g * GROUP_M;
+  const int gsz = min(tiles_m - first_m, GROUP_M);
+  const int r = t % in_group;
+  tm = first_m + r % gsz;
+  tn = r / gsz;
+}
+
+// 32 consecutive output columns of one row: apply the fused epilogue and store.
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& p, int row, int col0,
+                                               const uint32_t (&raw)[32]) {
+  if (row >= p.M) return;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * p.alpha;
+  const bool full = (col0 + 32) <= p.N;
+
+  if constexpr (EPI == AMDP_EPI_ACCUM_F32 || EPI == AMDP_EPI_STORE_F32) {
+    float* c = static_cast<float*>(p.C) + static_cast<size_t>(row) * p.ldc + col0;
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if constexpr (EPI == AMDP_EPI_ACCUM_F32) {
+          float4 old = *reinterpret_cast<const float4*>(c + j);
+          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+        }
+        *reinterpret_cast<float4*>(c + j) = o;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < p.N) c[j] = (EPI == AMDP_EPI_ACCUM_F32) ? c[j] + v[j] : v[j];
+    }
+    return;
+  } else {
+    // bf16 outputs
+    if constexpr (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD) {
+      const __nv_bfloat16* a = p.aux + static_cast<size_t>(row) * p.ld_aux + col0;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 q = *reinterpret_cast<const uint4*>(a + j);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(h[e]);
+            if constexpr (EPI == AMDP_EPI_RESIDUAL) {
+              v[j + 2 * e] += f.x;
+              v[j + 2 * e + 1] += f.y;
+            } else {
+              v[j + 2 * e] *= gelu_tanh_grad(f.x);
+              v[j + 2 * e + 1] *= gelu_tanh_grad(f.y);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (col0 + j >= p.N) continue;
+          float f = __bfloat162float(a[j]);
+          if constexpr (EPI == AMDP_EPI_RESIDUAL) v[j] += f;
+          else v[j] *= gelu_tanh_grad(f);
+        }
+      }
+    }
+    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc + col0;
+    __nv_bfloat16* c2 = nullptr;
+    if constexpr (EPI == AMDP_EPI_GELU) {
+      c2 = p.C2 + static_cast<size_t>(row) * p.ldc2 + col0;
+    }
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        uint4 q, q2;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&q2);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float x0 = v[j + 2 * e], x1 = v[j + 2 * e + 1];
+          if constexpr (EPI == AMDP_EPI_GELU) {
+            h2[e] = __floats2bfloat162_rn(x0, x1);
+            x0 = gelu_tanh(x0);
+            x1 = gelu_tanh(x1);
+          }
+          h[e] = __floats2bfloat162_rn(x0, x1);
+        }
+        *reinterpret_cast<uint4*>(c + j) = q;
+        if constexpr (EPI == AMDP_EPI_GELU) *reinterpret_cast<uint4*>(c2 + j) = q2;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col0 + j >= p.N) continue;
+        float x = v[j];
+        if constexpr (EPI == AMDP_EPI_GELU) {
+          c2[j] = __float2bfloat16_rn(x);
+          x = gelu_tanh(x);
+        }
+        c[j] = __float2bfloat16_rn(x);
+      }
+    }
+  }
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b, const EpiParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int tiles_m = (p.M + BM - 1) / BM;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = p.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&map_a);
+    ptx::tma_prefetch(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tm, tn;
+        tile_coords(t, tiles_m, tiles_n, tm, tn);
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem_a + stage * A_STAGE_BYTES;
+          uint8_t* sb = smem_b + stage * B_STAGE_BYTES;
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              ptx::tma_load_2d(sa + i * (64 * BK * 2), &map_a, &full_bar[stage], m0 + 64 * i, k0);
+          } else {
+            ptx::tma_load_2d(sa, &map_a, &full_bar[stage], k0, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              ptx::tma_load_2d(sb + i * (64 * BK * 2), &map_b, &full_bar[stage], n0 + 64 * i, k0);
+          } else {
+            ptx::tma_load_2d(sb, &map_b, &full_bar[stage], k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * A_STAGE_BYTES);
+          const uint32_t b_addr = ptx::smem_u32(smem_b + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t a_desc, b_desc;
+            if constexpr (A_MN)  // 16 K-rows of 128 B per instruction
+              a_desc = ptx::umma_desc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024);
+            else  // 16 bf16 = 32 B along the swizzled K row
+              a_desc = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            if constexpr (B_MN)
+              b_desc = ptx::umma_desc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024);
+            else
+              b_desc = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: warp (4+q) owns TMEM lanes [32q, 32q+32)
+    const int q = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int tm, tn;
+      tile_coords(t, tiles_m, tiles_n, tm, tn);
+      const int row = tm * BM + q * 32 + lane;
+      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      const int n_valid = min(BN, p.N - tn * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        if (c * 32 >= n_valid) break;  // warp-uniform
+        uint32_t raw[32];
+        ptx::tmem_ld_32x32b_x32(t_row + c * 32, raw);
+        ptx::tmem_ld_wait();
+        epilogue_chunk<EPI>(p, row, tn * BN + c * 32, raw);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qres;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) !=
+            cudaSuccess ||
+        qres != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner dimension `inner` (contiguous), outer `outer` with
+// leading dimension `ld` elements; box = {64, box_outer}, 128-byte swizzle.
+bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+              uint32_t box_outer) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+
+template <bool A_MN, bool B_MN, int EPI>
+int launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p, cudaStream_t s) {
+  auto kern = gemm_bf16_tcgen05<A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN>
+int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p,
+                 cudaStream_t s) {
+  switch (epi) {
+    case AMDP_EPI_STORE_BF16: return launch<A_MN, B_MN, AMDP_EPI_STORE_BF16>(ma, mb, p, s);
+    case AMDP_EPI_GELU: return launch<A_MN, B_MN, AMDP_EPI_GELU>(ma, mb, p, s);
+    case AMDP_EPI_RESIDUAL: return launch<A_MN, B_MN, AMDP_EPI_RESIDUAL>(ma, mb, p, s);
+    case AMDP_EPI_ACCUM_F32: return launch<A_MN, B_MN, AMDP_EPI_ACCUM_F32>(ma, mb, p, s);
+    case AMDP_EPI_GELU_BWD: return launch<A_MN, B_MN, AMDP_EPI_GELU_BWD>(ma, mb, p, s);
+    case AMDP_EPI_STORE_F32: return launch<A_MN, B_MN, AMDP_EPI_STORE_F32>(ma, mb, p, s);
+  }
+  return AMDP_ERR_INVALID;
+}
+
+}  // namespace
+}  // namespace amdp
+
+extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
+  using namespace amdp;
+  if (!a || a->M <= 0 || a->N <= 0 || a->K <= 0 || a->K % BK != 0) return AMDP_ERR_INVALID;
+  if (a->N % 8 != 0 || a->ldc % 4 != 0) return AMDP_ERR_INVALID;
+  if (a->epilogue < 0 || a->epilogue > AMDP_EPI_STORE_F32) return AMDP_ERR_INVALID;
+  if ((a->epilogue == AMDP_EPI_RESIDUAL || a->epilogue == AMDP_EPI_GELU_BWD) && !a->aux)
+    return AMDP_ERR_INVALID;
+  if (a->epilogue == AMDP_EPI_GELU && !a->C2) return AMDP_ERR_INVALID;
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) return AMDP_ERR_CUDA;
+  }
+  CUtensorMap ma, mb;
+  bool ok;
+  if (a->a_mn_major)  // A stored [K][lda], M contiguous
+    ok = make_map(&ma, a->A, a->M, a->K, a->lda, BK);
+  else  // A stored [M][lda], K contiguous
+    ok = make_map(&ma, a->A, a->K, a->M, a->lda, BM);
+  if (!ok) return AMDP_ERR_TMA;
+  if (a->b_mn_major)
+    ok = make_map(&mb, a->B, a->N, a->K, a->ldb, BK);
+  else
+    ok = make_map(&mb, a->B, a->K, a->N, a->ldb, BN);
+  if (!ok) return AMDP_ERR_TMA;
+  EpiParams p{a->M, a->N, a->K, a->C, a->ldc,
+              static_cast<const __nv_bfloat16*>(a->aux), a->ld_aux,
+              static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha};
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int am = a->a_mn_major ? 1 : 0, bm = a->b_mn_major ? 1 : 0;
+  if (!am && !bm) return dispatch_epi<false, false>(a->epilogue, ma, mb, p, s);
+  if (!am && bm) return dispatch_epi<false, true>(a->epilogue, ma, mb, p, s);
+  if (am && !bm) return dispatch_epi<true, false>(a->epilogue, ma, mb, p, s);
+  return dispatch_epi<true, true>(a->epilogue, ma, mb, p, s);
+}

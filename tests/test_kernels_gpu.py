@@ -1,0 +1,223 @@
+"""GPU parity of every sm_100a kernel against a plain PyTorch fp32 restatement of the same op.
+
+Tolerances are stated per test: bf16 outputs carry ~2^-8 relative rounding, fp32
+accumulation order differs from torch's.
+"""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2605_29664_b200 import kernels
+    return kernels
+
+
+@pytest.fixture(scope="module")
+def N():
+    from paper_2605_29664_b200 import _native
+    return _native
+
+
+def _rel(a, b):
+    a = a.double()
+    b = b.double()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+GEMM_SHAPES = [(256, 384, 128), (1000, 520, 192), (4096, 3072, 1024), (384, 50304, 256)]
+
+
+@pytest.mark.parametrize("M,N_,K_", GEMM_SHAPES)
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_store(K, N, M, N_, K_, a_mn, b_mn):
+    torch.manual_seed(0)
+    A = torch.randn(M, K_, device="cuda").bfloat16()
+    B = torch.randn(N_, K_, device="cuda").bfloat16()
+    ref = A.float() @ B.float().T
+    As = A.T.contiguous() if a_mn else A
+    Bs = B.T.contiguous() if b_mn else B
+    C = K.gemm(As, Bs, M=M, N_=N_, K=K_, a_mn=a_mn, b_mn=b_mn)
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < 8e-3
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, True)])
+def test_gemm_accum_f32(K, N, a_mn, b_mn):
+    torch.manual_seed(1)
+    M, N_, K_ = 768, 1024, 512
+    A = torch.randn(M, K_, device="cuda").bfloat16()
+    B = torch.randn(N_, K_, device="cuda").bfloat16()
+    C0 = torch.randn(M, N_, device="cuda")
+    ref = C0 + 0.5 * (A.float() @ B.float().T)
+    As = A.T.contiguous() if a_mn else A
+    Bs = B.T.contiguous() if b_mn else B
+    C = C0.clone()
+    K.gemm(As, Bs, M=M, N_=N_, K=K_, a_mn=a_mn, b_mn=b_mn, C=C, epilogue=N.EPI_ACCUM_F32,
+           alpha=0.5)
+    torch.cuda.synchronize()
+    assert _rel(C, ref) < 1e-5
+
+
+def _gelu(x):
+    return 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def test_gemm_gelu_residual_gelubwd(K, N):
+    torch.manual_seed(2)
+    M, N_, K_ = 512, 768, 256
+    A = (0.1 * torch.randn(M, K_, device="cuda")).bfloat16()
+    B = torch.randn(N_, K_, device="cuda").bfloat16()
+    acc = A.float() @ B.float().T
+    pre = torch.empty(M, N_, dtype=torch.bfloat16, device="cuda")
+    C = K.gemm(A, B, M=M, N_=N_, K=K_, epilogue=N.EPI_GELU, C2=pre, ldc2=N_)
+    torch.cuda.synchronize()
+    assert _rel(pre, acc) < 8e-3
+    assert _rel(C, _gelu(acc)) < 1e-2
+    R = torch.randn(M, N_, device="cuda").bfloat16()
+    C = K.gemm(A, B, M=M, N_=N_, K=K_, epilogue=N.EPI_RESIDUAL, aux=R, ld_aux=N_)
+    torch.cuda.synchronize()
+    assert _rel(C, acc + R.float()) < 8e-3
+    U = torch.randn(M, N_, device="cuda").bfloat16()
+    x = U.float().requires_grad_()
+    _gelu(x).backward(acc)
+    C = K.gemm(A, B, M=M, N_=N_, K=K_, epilogue=N.EPI_GELU_BWD, aux=U, ld_aux=N_)
+    torch.cuda.synchronize()
+    assert _rel(C, x.grad) < 1e-2
+
+
+def _attn_ref(qkv, B, S, H, D, causal):
+    q, k, v = qkv.float().view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
+    s = q @ k.transpose(-1, -2) / math.sqrt(D)
+    if causal:
+        mask = torch.ones(S, S, dtype=torch.bool, device=qkv.device).triu(1)
+        s = s.masked_fill(mask, float("-inf"))
+    p = s.softmax(-1)
+    o = p @ v  # B H S D
+    return o.permute(0, 2, 1, 3).reshape(B * S, H * D)
+
+
+@pytest.mark.parametrize("B,S,H,D", [(2, 128, 4, 32), (2, 256, 3, 64), (1, 192, 2, 80),
+                                     (2, 256, 2, 128), (4, 2048, 2, 128)])
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_fwd_bwd(K, B, S, H, D, causal):
+    torch.manual_seed(3)
+    qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
+    dout = torch.randn(B * S, H * D, device="cuda").bfloat16()
+    out, lse = K.attention_fwd(qkv, B, S, H, D, causal)
+    x = qkv.float().requires_grad_()
+    ref = _attn_ref(x, B, S, H, D, causal)
+    ref.backward(dout.float())
+    torch.cuda.synchronize()
+    assert _rel(out, ref) < 1e-2
+    dqkv = K.attention_bwd(qkv, out, dout, lse, B, S, H, D, causal)
+    torch.cuda.synchronize()
+    g = x.grad
+    hd = H * D
+    for part in range(3):
+        assert _rel(dqkv[:, part * hd:(part + 1) * hd], g[:, part * hd:(part + 1) * hd]) < 2e-2
+
+
+@pytest.mark.parametrize("rows,cols", [(256, 128), (1000, 1024), (4096, 2048), (512, 2560)])
+def test_layernorm(K, rows, cols):
+    torch.manual_seed(4)
+    x = (torch.randn(rows, cols, device="cuda") * 2 + 0.5).bfloat16()
+    gamma = 1 + 0.1 * torch.randn(cols, device="cuda")
+    beta = 0.1 * torch.randn(cols, device="cuda")
+    y, mean, rstd = K.layernorm_fwd(x, gamma, beta)
+    xf = x.float().requires_grad_()
+    g = gamma.clone().requires_grad_()
+    b = beta.clone().requires_grad_()
+    ref = torch.nn.functional.layer_norm(xf, (cols,), g, b, 1e-5)
+    dy = torch.randn(rows, cols, device="cuda").bfloat16()
+    ref.backward(dy.float())
+    torch.cuda.synchronize()
+    assert _rel(y, ref) < 8e-3
+    resid = torch.randn(rows, cols, device="cuda").bfloat16()
+    dg = torch.ones(cols, device="cuda")
+    db = torch.zeros(cols, device="cuda")
+    dx = K.layernorm_bwd(dy, x, gamma, mean, rstd, resid, dg, db)
+    torch.cuda.synchronize()
+    assert _rel(dx, xf.grad + resid.float()) < 1e-2
+    assert _rel(dg - 1, g.grad) < 1e-3
+    assert _rel(db, b.grad) < 1e-3
+
+
+def test_embedding(K):
+    torch.manual_seed(5)
+    V, S, Bn, Hd = 1000, 64, 4, 256
+    wte = torch.randn(V, Hd, device="cuda").bfloat16()
+    wpe = torch.randn(S, Hd, device="cuda").bfloat16()
+    tok = torch.randint(0, V, (Bn * S,), device="cuda", dtype=torch.int32)
+    x = K.embedding_fwd(tok, wte, wpe, S)
+    pos = torch.arange(Bn * S, device="cuda") % S
+    ref = wte.float()[tok.long()] + wpe.float()[pos]
+    torch.cuda.synchronize()
+    assert _rel(x, ref) < 4e-3
+    dx = torch.randn(Bn * S, Hd, device="cuda").bfloat16()
+    dwte = torch.zeros(V, Hd, device="cuda")
+    dwpe = torch.zeros(S, Hd, device="cuda")
+    K.embedding_bwd(tok, dx, dwte, dwpe, S)
+    rte = torch.zeros(V, Hd, device="cuda").index_add_(0, tok.long(), dx.float())
+    rpe = dx.float().view(Bn, S, Hd).sum(0)
+    torch.cuda.synchronize()
+    assert _rel(dwte, rte) < 1e-5
+    assert _rel(dwpe, rpe) < 1e-5
+
+
+@pytest.mark.parametrize("ntok,V", [(256, 1024), (512, 50304), (64, 30528)])
+def test_xent(K, ntok, V):
+    torch.manual_seed(6)
+    logits = (3 * torch.randn(ntok, V, device="cuda")).bfloat16()
+    labels = torch.randint(0, V, (ntok,), device="cuda", dtype=torch.int32)
+    labels[::7] = -1
+    lf = logits.float().requires_grad_()
+    valid = labels >= 0
+    ref = torch.nn.functional.cross_entropy(lf[valid], labels[valid].long(), reduction="sum")
+    scale = 1.0 / ntok
+    (ref * scale).backward()
+    loss = torch.zeros(1, device="cuda")
+    lg = logits.clone()
+    K.xent_fwd_bwd(lg, labels, loss, scale)
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref.item()) / ref.item() < 1e-4
+    assert _rel(lg, lf.grad) < 1e-2
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+def test_optimizer(K, N, kind):
+    torch.manual_seed(7)
+    n = 100003
+    th = torch.randn(n, device="cuda")
+    m = 0.01 * torch.randn(n, device="cuda")
+    v = 0.01 * torch.rand(n, device="cuda")
+    g = torch.randn(n, device="cuda")
+    w = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    T, M_, V_, G = th.double(), m.double(), v.double(), g.double() * 0.5
+    lr, b1, b2, eps, wd = 0.01, 0.9, 0.999, 1e-3, 0.1
+    if kind == 0:
+        T = T - lr * G
+    elif kind == 1:
+        M_ = b1 * M_ + (1 - b1) * G
+        T = T - lr * M_
+    elif kind == 2:
+        M_ = b1 * M_ + (1 - b1) * G
+        V_ = b2 * V_ + (1 - b2) * G * G
+        P = (1 / (V_.sqrt() + eps)).clamp(1e-8, 1e6)
+        T = T - lr * P * M_
+    else:
+        step = 3
+        M_ = b1 * M_ + (1 - b1) * G
+        V_ = b2 * V_ + (1 - b2) * G * G
+        mh, vh = M_ / (1 - b1 ** step), V_ / (1 - b2 ** step)
+        T = T - lr * (mh / (vh.sqrt() + eps) + wd * T)
+    K.optimizer_step(kind, th, m, v, g, w, lr=lr, beta1=b1, beta2=b2, eps=eps,
+                     weight_decay=wd if kind == 3 else 0.0, grad_scale=0.5, step=3)
+    torch.cuda.synchronize()
+    assert torch.allclose(th.double(), T, rtol=1e-5, atol=1e-6)
+    assert torch.equal(w, th.bfloat16())
+    assert torch.count_nonzero(g).item() == 0
