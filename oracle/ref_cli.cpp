@@ -62,7 +62,12 @@ int main(int argc, char** argv) {
       auto tl = simulate(build(cfg, cl), cl);
       ordered_json j;
       j["makespan"] = rat_json(tl.makespan);
-      j["bubble_ratio"] = bubble_ratio(tl, warm).str();
+      try {
+        j["bubble_ratio"] = bubble_ratio(tl, warm).str();
+      } catch (const std::exception& e) {
+        j["bubble_ratio"] = nullptr;
+      }
+      j["bubble_w0"] = bubble_ratio(tl, 0).str();
       auto mm = mismatch_report(tl);
       j["mismatch"] = mismatch_json(mm);
       j["windows"] = window_json(window_mismatch(tl, cl.depth));
