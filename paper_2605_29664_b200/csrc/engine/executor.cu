@@ -1,0 +1,972 @@
+// AMDP stage executor: replays the reference dispatch order (ppsim::simulate_with_order on
+// the declared ClusterSpec) on this process's GPU, one CUDA compute stream plus one NCCL
+// communication stream, and returns the measured Timeline.
+//
+//  * Planning (host, once): stage hosting per rank (logical devices folded contiguously,
+//    depth/world per GPU), activation-slot assignment per (stage, minibatch) from the
+//    order, boundary buffers for stage-to-stage activations/gradients with exact
+//    liveness, the communication program (send/recv at the producer's position in the
+//    global order on both ranks, so NCCL pairs match and no wait can form a cycle), and
+//    the replica groups of every stage (owner = logical device i, H/builder.hpp:273).
+//  * Execution: Forward/Backward -> GptStage task bodies; Reduce -> ncclReduce of the
+//    stage's fp32 window gradient to the owner (no-op when every replica is on this
+//    GPU: co-resident replicas accumulate into one buffer); Broadcast -> fused optimizer
+//    step on the owner + ncclBroadcast of the fp32 weights + bf16 refresh on replicas.
+//    Parameter versions are therefore exactly the trace's (F sees w - preloaded, B sees
+//    w): a device-side counter per stage records what each task actually read.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "amdp_engine.h"
+#include "../kernels/common.cuh"
+#include "../sched/sched_handle.hpp"
+#include "gpt_stage.hpp"
+#include "ppsim/ppsim.hpp"
+
+namespace amdp {
+
+namespace {
+
+__global__ void record_version_kernel(const int* ver, int stage, int* trace, int idx) {
+  trace[idx] = ver[stage];
+}
+__global__ void bump_version_kernel(int* ver, int stage) { ver[stage] += 1; }
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+#define CUDA_OK(x)                                                                 \
+  do {                                                                             \
+    cudaError_t _e = (x);                                                          \
+    if (_e != cudaSuccess)                                                         \
+      throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+#define NCCL_OK(x)                                                                 \
+  do {                                                                             \
+    ncclResult_t _r = (x);                                                         \
+    if (_r != ncclSuccess)                                                         \
+      throw std::runtime_error(std::string(#x) + ": " + ncclGetErrorString(_r));   \
+  } while (0)
+
+uint64_t tensor_seed(uint64_t model_seed, int gidx) {
+  return model_seed * 1000003ull + static_cast<uint64_t>(gidx);
+}
+
+// Balanced contiguous partition of L layers over `depth` stages, costing the LM head as
+// (V / (6 h)) layer-equivalents on the last stage (2hV vs 12h^2 flops per token).
+std::vector<int> balance_layers(int L, int depth, int h, int V) {
+  const double head = static_cast<double>(V) / (6.0 * h);
+  std::vector<int> best;
+  double best_max = 1e300;
+  // last stage gets k layers, the rest spread as evenly as possible
+  for (int k = 0; k <= L; ++k) {
+    const int rest = L - k;
+    if (depth > 1 && rest < depth - 1) continue;
+    std::vector<int> p(static_cast<size_t>(depth), 0);
+    if (depth == 1) {
+      p[0] = L;
+    } else {
+      for (int i = 0; i < depth - 1; ++i) p[static_cast<size_t>(i)] = rest / (depth - 1) + (i < rest % (depth - 1) ? 1 : 0);
+      p[static_cast<size_t>(depth - 1)] = k;
+    }
+    double mx = 0;
+    for (int i = 0; i < depth; ++i) mx = std::max(mx, p[static_cast<size_t>(i)] + (i == depth - 1 ? head : 0.0));
+    if (k >= 1 && mx < best_max - 1e-9) {
+      best_max = mx;
+      best = p;
+    }
+  }
+  return best;
+}
+
+struct BoundaryBuf {
+  uint16_t* ptr = nullptr;
+  cudaEvent_t comm_done = nullptr;  // last communication use (send) of this buffer
+  bool comm_pending = false;
+};
+
+struct TaskPlan {
+  int slot = -1;            // activation slot (F/B)
+  int in_buf = -1;          // F: boundary buffer holding the stage input (stages > 0)
+  int out_buf = -1;         // F: boundary buffer receiving the stage output (stages < d-1)
+  int gin_buf = -1;         // B: incoming gradient buffer (stages < d-1)
+  int gout_buf = -1;        // B: outgoing gradient buffer (stages > 0)
+  int send_to = -1;         // rank to send out/gout to after this task (-1: none)
+  bool local = false;       // executed by this rank
+};
+
+struct CommOp {           // executed on the comm stream at a position in the global order
+  enum Kind { Send, Recv, Reduce, Bcast } kind;
+  int peer = -1;          // send/recv peer rank
+  int buf = -1;           // boundary buffer (send/recv)
+  int stage = -1;         // reduce/bcast stage
+  int after_task = -1;    // order position whose compute it must follow (send/reduce)
+};
+
+}  // namespace
+
+class Engine {
+ public:
+  Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uint8_t* nccl_id);
+  ~Engine();
+  void run(const int32_t* inputs, const int32_t* labels, float* losses_out);
+  std::string plan_json() const;
+  std::string version_csv() const;
+  int64_t stage_numel(int stage) const;
+  void copy_params(int stage, float* host, int64_t n, bool to_host);
+
+  // results
+  amdp_run_stats stats{};
+  std::vector<ppsim::TaskEvent> events;  // measured, this rank's logical devices
+  std::vector<int> version_seen;         // per task id (-1 if not local)
+  SchedHandle sched;                     // declared graph + timeline + order
+  std::vector<std::unique_ptr<GptStage>> stages;
+  std::vector<bool> hosted, owned;
+  std::vector<int> slots_per_stage;
+  int nbuf = 0;
+  Dims dm{};
+  std::vector<int> part;
+
+ private:
+  amdp_model_config mc_;
+  amdp_run_config rc_;
+  int depth_ = 0, world_ = 1, rank_ = 0, per_rank_ = 1, M_ = 0, thr_ = 1, W_ = 1;
+  std::vector<TaskPlan> plan_;               // per order position
+  std::vector<std::vector<CommOp>> comm_at_; // per order position
+  std::vector<std::vector<uint8_t*>> slot_mem_;
+  std::vector<std::vector<SlotActs>> slot_acts_;
+  std::vector<BoundaryBuf> bufs_;
+  std::vector<std::vector<int>> group_ranks_; // per stage: ranks hosting it
+  std::vector<ncclComm_t> group_comm_;        // per stage (null if single-rank group)
+  ncclComm_t world_comm_ = nullptr;
+  cudaStream_t cs_ = nullptr, ms_ = nullptr;  // compute, communication
+  uint8_t* ws_ = nullptr;
+  int32_t *d_inputs_ = nullptr, *d_labels_ = nullptr;
+  float* d_loss_ = nullptr;
+  int *d_ver_ = nullptr, *d_trace_ = nullptr;
+  std::vector<cudaEvent_t> ev_start_, ev_end_;
+  cudaEvent_t run_begin_ = nullptr, run_end_ = nullptr;
+  std::vector<cudaEvent_t> stage_ready_;      // weights of stage i usable (after bcast)
+  size_t slot_total_ = 0;
+
+  int rank_of_dev(int dev) const { return dev / per_rank_; }
+  int owner_rank(int stage) const { return rank_of_dev(stage); }
+  void make_plan();
+  void allocate();
+  void init_weights();
+  void exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::vector<int>& window_tokens_loaded,
+                 std::vector<int>& window_last_left, float* losses_out);
+  void exec_comm(int pos);
+};
+
+Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uint8_t* nccl_id)
+    : mc_(mc), rc_(rc) {
+  depth_ = rc.policy.num_pipelines * 2;
+  world_ = std::max(1, rc.world_size);
+  rank_ = rc.rank;
+  if (rc.policy.policy != 0) throw std::invalid_argument("engine: only the AMDP policy executes on GPUs");
+  if (!rc.policy.zero_enabled)
+    throw std::invalid_argument("engine: AMDP execution needs zero_enabled (sharded Reduce/Broadcast); "
+                                "replicated updates would need one weight copy per pipeline replica");
+  if (depth_ % world_ != 0) throw std::invalid_argument("engine: depth must be a multiple of world_size");
+  per_rank_ = depth_ / world_;
+  M_ = rc.policy.num_minibatches;
+  thr_ = rc.policy.accumulation_threshold;
+  if (M_ % thr_ != 0) throw std::invalid_argument("engine: num_minibatches must be a multiple of accumulation_threshold");
+  W_ = M_ / thr_;
+
+  dm.L = mc.layers;
+  dm.h = mc.hidden;
+  dm.heads = mc.heads;
+  dm.hd = mc.hidden / mc.heads;
+  dm.ffn = mc.ffn;
+  dm.V = mc.vocab;
+  dm.S = mc.seq;
+  dm.B = mc.seqs_per_minibatch;
+  dm.T = dm.B * dm.S;
+  dm.causal = mc.causal != 0;
+  dm.ln_eps = mc.ln_eps > 0 ? mc.ln_eps : 1e-5f;
+  if (dm.h % dm.heads != 0) throw std::invalid_argument("engine: hidden must divide into heads");
+
+  // schedule: build + order on the declared cost model
+  ppsim::ClusterSpec cl = ppsim::ClusterSpec::uniform(depth_, depth_, from_c(rc.declared_fwd),
+                                                      from_c(rc.declared_bwd));
+  ppsim::PolicyConfig pc = policy_from_c(&rc.policy);
+  sched.cl = cl;
+  sched.cfg = pc;
+  sched.g = ppsim::build(pc, cl);
+  sched.tl = ppsim::simulate_with_order(sched.g, cl, &sched.order);
+  sched.has_graph = sched.has_timeline = true;
+
+  // partition
+  if (mc.layers_per_stage) {
+    part.assign(mc.layers_per_stage, mc.layers_per_stage + depth_);
+    int s = 0;
+    for (int x : part) s += x;
+    if (s != dm.L) throw std::invalid_argument("engine: layers_per_stage must sum to layers");
+  } else {
+    part = balance_layers(dm.L, depth_, dm.h, dm.V);
+    if (part.empty()) throw std::invalid_argument("engine: cannot partition layers over stages");
+  }
+  int l = 0;
+  for (int i = 0; i < depth_; ++i) {
+    stages.emplace_back(new GptStage(dm, i, depth_, l, l + part[static_cast<size_t>(i)]));
+    l += part[static_cast<size_t>(i)];
+  }
+
+  // hosting
+  hosted.assign(static_cast<size_t>(depth_), false);
+  owned.assign(static_cast<size_t>(depth_), false);
+  group_ranks_.assign(static_cast<size_t>(depth_), {});
+  for (int i = 0; i < depth_; ++i) {
+    for (int p = 0; p < depth_ / 2; ++p) {
+      const int r = rank_of_dev(ppsim::map_stage_to_device(p, i, depth_));
+      if (std::find(group_ranks_[static_cast<size_t>(i)].begin(), group_ranks_[static_cast<size_t>(i)].end(), r) ==
+          group_ranks_[static_cast<size_t>(i)].end())
+        group_ranks_[static_cast<size_t>(i)].push_back(r);
+    }
+    std::sort(group_ranks_[static_cast<size_t>(i)].begin(), group_ranks_[static_cast<size_t>(i)].end());
+    hosted[static_cast<size_t>(i)] = std::count(group_ranks_[static_cast<size_t>(i)].begin(),
+                                                group_ranks_[static_cast<size_t>(i)].end(), rank_) > 0;
+    owned[static_cast<size_t>(i)] = owner_rank(i) == rank_;
+  }
+
+  CUDA_OK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+  CUDA_OK(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
+  if (world_ > 1) {
+    if (!nccl_id) throw std::invalid_argument("engine: nccl_id required when world_size > 1");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    NCCL_OK(ncclCommInitRank(&world_comm_, world_, id, rank_));
+  }
+  group_comm_.assign(static_cast<size_t>(depth_), nullptr);
+  if (world_ > 1) {
+    for (int i = 0; i < depth_; ++i) {
+      const auto& gr = group_ranks_[static_cast<size_t>(i)];
+      const int color = hosted[static_cast<size_t>(i)] ? i : NCCL_SPLIT_NOCOLOR;
+      ncclComm_t c = nullptr;
+      NCCL_OK(ncclCommSplit(world_comm_, color, rank_, &c, nullptr));  // collective over all ranks
+      group_comm_[static_cast<size_t>(i)] = (gr.size() > 1 && hosted[static_cast<size_t>(i)]) ? c : nullptr;
+      if (c && !(gr.size() > 1 && hosted[static_cast<size_t>(i)])) ncclCommDestroy(c);
+    }
+  }
+  make_plan();
+  allocate();
+  init_weights();
+}
+
+Engine::~Engine() {
+  cudaStreamSynchronize(cs_);
+  cudaStreamSynchronize(ms_);
+  for (auto& s : stages) {
+    cudaFree(s->master);
+    cudaFree(s->m);
+    cudaFree(s->v);
+    cudaFree(s->grad);
+    cudaFree(s->w);
+  }
+  for (auto& v : slot_mem_)
+    for (auto* p : v) cudaFree(p);
+  for (auto& b : bufs_) {
+    cudaFree(b.ptr);
+    if (b.comm_done) cudaEventDestroy(b.comm_done);
+  }
+  cudaFree(ws_);
+  cudaFree(d_inputs_);
+  cudaFree(d_labels_);
+  cudaFree(d_loss_);
+  cudaFree(d_ver_);
+  cudaFree(d_trace_);
+  for (auto e : ev_start_) cudaEventDestroy(e);
+  for (auto e : ev_end_) cudaEventDestroy(e);
+  for (auto e : stage_ready_) cudaEventDestroy(e);
+  if (run_begin_) cudaEventDestroy(run_begin_);
+  if (run_end_) cudaEventDestroy(run_end_);
+  for (auto c : group_comm_)
+    if (c) ncclCommDestroy(c);
+  if (world_comm_) ncclCommDestroy(world_comm_);
+  cudaStreamDestroy(cs_);
+  cudaStreamDestroy(ms_);
+}
+
+void Engine::make_plan() {
+  const auto& g = sched.g;
+  const auto& order = sched.order;
+  const int N = static_cast<int>(order.size());
+  plan_.assign(static_cast<size_t>(N), TaskPlan{});
+  comm_at_.assign(static_cast<size_t>(N), {});
+  std::vector<int> pos_of(g.tasks.size());
+  for (int k = 0; k < N; ++k) pos_of[static_cast<size_t>(order[static_cast<size_t>(k)])] = k;
+  // task ids of F(i,j) / B(i,j)
+  std::map<std::pair<int, int>, int> F, B;
+  for (std::size_t t = 0; t < g.tasks.size(); ++t) {
+    const auto& k = g.tasks[t];
+    if (k.kind == ppsim::Kind::Forward) F[{k.stage, k.minibatch}] = static_cast<int>(t);
+    if (k.kind == ppsim::Kind::Backward) B[{k.stage, k.minibatch}] = static_cast<int>(t);
+  }
+  auto rank_of_task = [&](int t) { return rank_of_dev(g.tasks[static_cast<size_t>(t)].device); };
+
+  // activation slots per stage (local tasks only)
+  slots_per_stage.assign(static_cast<size_t>(depth_), 0);
+  std::vector<std::vector<int>> free_slots(static_cast<size_t>(depth_));
+  std::map<std::pair<int, int>, int> slot_of;
+  // boundary buffers: interval allocation over positions on this rank
+  std::vector<int> free_bufs;
+  std::vector<std::vector<int>> release_at(static_cast<size_t>(N));  // buffers freed after position
+  auto alloc_buf = [&]() {
+    if (!free_bufs.empty()) {
+      const int b = free_bufs.back();
+      free_bufs.pop_back();
+      return b;
+    }
+    return nbuf++;
+  };
+  // F boundary (i -> i+1, j): receiver buffer lives [pos F(i,j), pos B(i+1,j)];
+  //   on the producer rank (if different) a send buffer lives [pos F(i,j), pos F(i,j)].
+  // B boundary (i+1 -> i, j): [pos B(i+1,j), pos B(i,j)] likewise.
+  std::map<std::pair<int, int>, int> fbuf_recv, bbuf_recv;  // key (boundary stage i, j)
+  for (int k = 0; k < N; ++k) {
+    const int t = order[static_cast<size_t>(k)];
+    const auto& task = g.tasks[static_cast<size_t>(t)];
+    TaskPlan& tp = plan_[static_cast<size_t>(k)];
+    const int me = rank_of_task(t);
+    tp.local = me == rank_;
+    // release buffers whose last use was an earlier position
+    if (task.kind == ppsim::Kind::Forward) {
+      const int i = task.stage, j = task.minibatch;
+      if (tp.local) {
+        auto& fl = free_slots[static_cast<size_t>(i)];
+        int s;
+        if (!fl.empty()) {
+          s = fl.back();
+          fl.pop_back();
+        } else {
+          s = slots_per_stage[static_cast<size_t>(i)]++;
+        }
+        slot_of[{i, j}] = s;
+        tp.slot = s;
+        if (i > 0) tp.in_buf = fbuf_recv.at({i - 1, j});
+      }
+      if (i + 1 < depth_) {
+        const int cons = F.at({i + 1, j});
+        const int cr = rank_of_task(cons);
+        const int last_use = pos_of[static_cast<size_t>(B.at({i + 1, j}))];
+        if (tp.local) {
+          const int b = alloc_buf();
+          tp.out_buf = b;
+          if (cr == rank_) {
+            fbuf_recv[{i, j}] = b;
+            release_at[static_cast<size_t>(last_use)].push_back(b);
+          } else {
+            tp.send_to = cr;
+            comm_at_[static_cast<size_t>(k)].push_back({CommOp::Send, cr, b, -1, k});
+            release_at[static_cast<size_t>(k)].push_back(b);
+          }
+        } else if (cr == rank_) {
+          const int b = alloc_buf();
+          fbuf_recv[{i, j}] = b;
+          comm_at_[static_cast<size_t>(k)].push_back({CommOp::Recv, me, b, -1, -1});
+          release_at[static_cast<size_t>(last_use)].push_back(b);
+        }
+      }
+    } else if (task.kind == ppsim::Kind::Backward) {
+      const int i = task.stage, j = task.minibatch;
+      if (tp.local) {
+        tp.slot = slot_of.at({i, j});
+        free_slots[static_cast<size_t>(i)].push_back(tp.slot);
+        if (i > 0) tp.in_buf = fbuf_recv.at({i - 1, j});
+        if (i + 1 < depth_) tp.gin_buf = bbuf_recv.at({i, j});
+      }
+      if (i > 0) {
+        const int cons = B.at({i - 1, j});
+        const int cr = rank_of_task(cons);
+        const int last_use = pos_of[static_cast<size_t>(cons)];
+        if (tp.local) {
+          const int b = alloc_buf();
+          tp.gout_buf = b;
+          if (cr == rank_) {
+            bbuf_recv[{i - 1, j}] = b;
+            release_at[static_cast<size_t>(last_use)].push_back(b);
+          } else {
+            tp.send_to = cr;
+            comm_at_[static_cast<size_t>(k)].push_back({CommOp::Send, cr, b, -1, k});
+            release_at[static_cast<size_t>(k)].push_back(b);
+          }
+        } else if (cr == rank_) {
+          const int b = alloc_buf();
+          bbuf_recv[{i - 1, j}] = b;
+          comm_at_[static_cast<size_t>(k)].push_back({CommOp::Recv, me, b, -1, -1});
+          release_at[static_cast<size_t>(last_use)].push_back(b);
+        }
+      }
+    } else if (task.kind == ppsim::Kind::Reduce) {
+      const int i = task.stage;
+      if (hosted[static_cast<size_t>(i)] && group_comm_.size() > static_cast<size_t>(i) &&
+          group_ranks_[static_cast<size_t>(i)].size() > 1)
+        comm_at_[static_cast<size_t>(k)].push_back({CommOp::Reduce, -1, -1, i, k});
+    } else if (task.kind == ppsim::Kind::Broadcast) {
+      const int i = task.stage;
+      if (hosted[static_cast<size_t>(i)] && group_ranks_[static_cast<size_t>(i)].size() > 1)
+        comm_at_[static_cast<size_t>(k)].push_back({CommOp::Bcast, -1, -1, i, k});
+    }
+    for (int b : release_at[static_cast<size_t>(k)]) free_bufs.push_back(b);
+  }
+}
+
+void Engine::allocate() {
+  const size_t T = static_cast<size_t>(dm.T), h = static_cast<size_t>(dm.h);
+  for (int i = 0; i < depth_; ++i) {
+    if (!hosted[static_cast<size_t>(i)]) continue;
+    GptStage& st = *stages[static_cast<size_t>(i)];
+    const size_t n = static_cast<size_t>(st.numel());
+    CUDA_OK(cudaMalloc(&st.master, n * sizeof(float)));
+    CUDA_OK(cudaMalloc(&st.grad, n * sizeof(float)));
+    CUDA_OK(cudaMalloc(&st.w, n * sizeof(uint16_t)));
+    CUDA_OK(cudaMemsetAsync(st.grad, 0, n * sizeof(float), cs_));
+    if (owned[static_cast<size_t>(i)]) {
+      CUDA_OK(cudaMalloc(&st.m, n * sizeof(float)));
+      CUDA_OK(cudaMalloc(&st.v, n * sizeof(float)));
+      CUDA_OK(cudaMemsetAsync(st.m, 0, n * sizeof(float), cs_));
+      CUDA_OK(cudaMemsetAsync(st.v, 0, n * sizeof(float), cs_));
+    }
+  }
+  slot_mem_.assign(static_cast<size_t>(depth_), {});
+  slot_acts_.assign(static_cast<size_t>(depth_), {});
+  for (int i = 0; i < depth_; ++i) {
+    const size_t bytes = stages[static_cast<size_t>(i)]->slot_bytes();
+    for (int s = 0; s < slots_per_stage[static_cast<size_t>(i)]; ++s) {
+      uint8_t* p = nullptr;
+      CUDA_OK(cudaMalloc(&p, bytes));
+      slot_total_ += bytes;
+      slot_mem_[static_cast<size_t>(i)].push_back(p);
+      slot_acts_[static_cast<size_t>(i)].push_back(stages[static_cast<size_t>(i)]->carve_slot(p));
+    }
+  }
+  bufs_.resize(static_cast<size_t>(nbuf));
+  for (auto& b : bufs_) {
+    CUDA_OK(cudaMalloc(&b.ptr, T * h * sizeof(uint16_t)));
+    CUDA_OK(cudaEventCreateWithFlags(&b.comm_done, cudaEventDisableTiming));
+  }
+  CUDA_OK(cudaMalloc(&ws_, GptStage::workspace_bytes(dm)));
+  CUDA_OK(cudaMalloc(&d_inputs_, static_cast<size_t>(M_) * T * sizeof(int32_t)));
+  CUDA_OK(cudaMalloc(&d_labels_, static_cast<size_t>(M_) * T * sizeof(int32_t)));
+  CUDA_OK(cudaMalloc(&d_loss_, static_cast<size_t>(M_) * sizeof(float)));
+  CUDA_OK(cudaMalloc(&d_ver_, static_cast<size_t>(depth_) * sizeof(int)));
+  CUDA_OK(cudaMalloc(&d_trace_, sched.g.tasks.size() * sizeof(int)));
+  stage_ready_.resize(static_cast<size_t>(depth_));
+  for (auto& e : stage_ready_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CUDA_OK(cudaEventCreate(&run_begin_));
+  CUDA_OK(cudaEventCreate(&run_end_));
+}
+
+void Engine::init_weights() {
+  for (int i = 0; i < depth_; ++i) {
+    if (!hosted[static_cast<size_t>(i)]) continue;
+    GptStage& st = *stages[static_cast<size_t>(i)];
+    CUDA_OK(cudaMemsetAsync(st.master, 0, static_cast<size_t>(st.numel()) * sizeof(float), cs_));
+    for (const auto& p : st.params()) {
+      float* dst = st.master + p.off;
+      int rc = 0;
+      if (p.init == 0)
+        rc = amdp_fill_normal_bf16_f32(nullptr, dst, p.numel(), tensor_seed(mc_.seed, p.global_index), p.std,
+                                       reinterpret_cast<amdp_stream_t>(cs_));
+      else
+        rc = amdp_fill_const_f32(dst, p.numel(), p.init == 1 ? 1.0f : 0.0f, reinterpret_cast<amdp_stream_t>(cs_));
+      if (rc != 0) throw std::runtime_error("weight init failed");
+    }
+    const int64_t n = st.numel();
+    cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
+        st.master, reinterpret_cast<bf16*>(st.w), n);
+    CUDA_OK(cudaGetLastError());
+  }
+  CUDA_OK(cudaStreamSynchronize(cs_));
+}
+
+void Engine::exec_comm(int pos) {
+  for (const CommOp& op : comm_at_[static_cast<size_t>(pos)]) {
+    const size_t T = static_cast<size_t>(dm.T), h = static_cast<size_t>(dm.h);
+    switch (op.kind) {
+      case CommOp::Send: {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_OK(cudaEventRecord(e, cs_));
+        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
+        cudaEventDestroy(e);
+        NCCL_OK(ncclSend(bufs_[static_cast<size_t>(op.buf)].ptr, T * h, ncclBfloat16, op.peer, world_comm_, ms_));
+        CUDA_OK(cudaEventRecord(bufs_[static_cast<size_t>(op.buf)].comm_done, ms_));
+        bufs_[static_cast<size_t>(op.buf)].comm_pending = true;
+        stats.p2p_bytes_sent += static_cast<int64_t>(T * h * 2);
+        break;
+      }
+      case CommOp::Recv: {
+        BoundaryBuf& b = bufs_[static_cast<size_t>(op.buf)];
+        // the buffer's previous compute use must be finished before it is overwritten
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_OK(cudaEventRecord(e, cs_));
+        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
+        cudaEventDestroy(e);
+        NCCL_OK(ncclRecv(b.ptr, T * h, ncclBfloat16, op.peer, world_comm_, ms_));
+        CUDA_OK(cudaEventRecord(b.comm_done, ms_));
+        b.comm_pending = true;
+        break;
+      }
+      case CommOp::Reduce: {
+        GptStage& st = *stages[static_cast<size_t>(op.stage)];
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_OK(cudaEventRecord(e, cs_));
+        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
+        cudaEventDestroy(e);
+        const auto& gr = group_ranks_[static_cast<size_t>(op.stage)];
+        const int root = static_cast<int>(std::find(gr.begin(), gr.end(), owner_rank(op.stage)) - gr.begin());
+        NCCL_OK(ncclReduce(st.grad, st.grad, static_cast<size_t>(st.numel()), ncclFloat32, ncclSum, root,
+                           group_comm_[static_cast<size_t>(op.stage)], ms_));
+        stats.collective_bytes += st.numel() * 4;
+        break;
+      }
+      case CommOp::Bcast:
+        break;  // issued from exec_task (needs the owner's optimizer step first)
+    }
+  }
+}
+
+void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::vector<int>& loaded,
+                       std::vector<int>& last_left, float* losses_out) {
+  const auto& g = sched.g;
+  const int t = sched.order[static_cast<size_t>(pos)];
+  const auto& task = g.tasks[static_cast<size_t>(t)];
+  const TaskPlan& tp = plan_[static_cast<size_t>(pos)];
+  const size_t T = static_cast<size_t>(dm.T);
+  auto st = reinterpret_cast<amdp_stream_t>(cs_);
+  int rc = 0;
+
+  if (task.kind == ppsim::Kind::Forward || task.kind == ppsim::Kind::Backward) {
+    if (!tp.local) {
+      exec_comm(pos);
+      return;
+    }
+    const int i = task.stage, j = task.minibatch;
+    GptStage& S = *stages[static_cast<size_t>(i)];
+    const SlotActs& A = slot_acts_[static_cast<size_t>(i)][static_cast<size_t>(tp.slot)];
+    const int w = j / thr_;
+    if (task.kind == ppsim::Kind::Forward && !loaded[static_cast<size_t>(w)]) {
+      const size_t off = static_cast<size_t>(w) * thr_ * T;
+      CUDA_OK(cudaMemcpyAsync(d_inputs_ + off, h_in + off, thr_ * T * sizeof(int32_t), cudaMemcpyHostToDevice, cs_));
+      CUDA_OK(cudaMemcpyAsync(d_labels_ + off, h_lab + off, thr_ * T * sizeof(int32_t), cudaMemcpyHostToDevice, cs_));
+      stats.h2d_bytes += static_cast<int64_t>(2 * thr_ * T * sizeof(int32_t));
+      loaded[static_cast<size_t>(w)] = 1;
+    }
+    auto wait_buf = [&](int b) {
+      if (b >= 0 && bufs_[static_cast<size_t>(b)].comm_pending) {
+        CUDA_OK(cudaStreamWaitEvent(cs_, bufs_[static_cast<size_t>(b)].comm_done, 0));
+      }
+    };
+    wait_buf(tp.in_buf);
+    wait_buf(tp.gin_buf);
+    wait_buf(tp.out_buf);
+    wait_buf(tp.gout_buf);
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    record_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i, d_trace_, t);
+    stats.kernels_launched += 1;
+    const int32_t* tok = d_inputs_ + static_cast<size_t>(j) * T;
+    const int32_t* lab = d_labels_ + static_cast<size_t>(j) * T;
+    const uint16_t* in = tp.in_buf >= 0 ? bufs_[static_cast<size_t>(tp.in_buf)].ptr : nullptr;
+    int launched;
+    if (task.kind == ppsim::Kind::Forward) {
+      uint16_t* out = tp.out_buf >= 0 ? bufs_[static_cast<size_t>(tp.out_buf)].ptr : nullptr;
+      launched = S.forward(A, tok, lab, in, out, d_loss_ + j, ws_, cs_, &rc);
+    } else {
+      const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
+      uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
+      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, &rc);
+    }
+    stats.kernels_launched += launched;
+    if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    stats.tasks_executed += 1;
+    exec_comm(pos);  // sends of this task's output, recvs placed at this position
+    // D2H of a window's losses once its last-stage forwards are all issued
+    if (task.kind == ppsim::Kind::Forward && S.last() && losses_out) {
+      if (--last_left[static_cast<size_t>(w)] == 0) {
+        CUDA_OK(cudaMemcpyAsync(losses_out + static_cast<size_t>(w) * thr_, d_loss_ + static_cast<size_t>(w) * thr_,
+                                thr_ * sizeof(float), cudaMemcpyDeviceToHost, cs_));
+        stats.d2h_bytes += thr_ * static_cast<int64_t>(sizeof(float));
+      }
+    }
+    return;
+  }
+
+  // window machinery
+  const int i = task.stage;
+  if (!hosted[static_cast<size_t>(i)]) {
+    exec_comm(pos);
+    return;
+  }
+  GptStage& S = *stages[static_cast<size_t>(i)];
+  if (task.kind == ppsim::Kind::Reduce) {
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    exec_comm(pos);  // ncclReduce on the comm stream after this position's compute
+    if (group_ranks_[static_cast<size_t>(i)].size() > 1 && owned[static_cast<size_t>(i)]) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(e, ms_));
+      CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
+      cudaEventDestroy(e);
+    }
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    stats.tasks_executed += 1;
+    return;
+  }
+  if (task.kind == ppsim::Kind::Broadcast) {
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    const bool multi = group_ranks_[static_cast<size_t>(i)].size() > 1;
+    if (owned[static_cast<size_t>(i)]) {
+      amdp_opt_args o = rc_.optimizer;
+      o.step = task.window + 1;
+      o.grad_scale = rc_.optimizer.grad_scale * (1.0f / static_cast<float>(thr_));
+      rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), st);
+      if (rc != 0) throw std::runtime_error("optimizer step failed");
+      stats.kernels_launched += 1;
+    } else {
+      // the reduce on the comm stream read this replica's gradient: wait, then clear it
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(e, ms_));
+      CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
+      cudaEventDestroy(e);
+      CUDA_OK(cudaMemsetAsync(S.grad, 0, static_cast<size_t>(S.numel()) * sizeof(float), cs_));
+    }
+    if (multi) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CUDA_OK(cudaEventRecord(e, cs_));
+      CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
+      cudaEventDestroy(e);
+      const auto& gr = group_ranks_[static_cast<size_t>(i)];
+      const int root = static_cast<int>(std::find(gr.begin(), gr.end(), owner_rank(i)) - gr.begin());
+      NCCL_OK(ncclBroadcast(S.master, S.master, static_cast<size_t>(S.numel()), ncclFloat32, root,
+                            group_comm_[static_cast<size_t>(i)], ms_));
+      stats.collective_bytes += S.numel() * 4;
+      CUDA_OK(cudaEventRecord(stage_ready_[static_cast<size_t>(i)], ms_));
+      if (!owned[static_cast<size_t>(i)]) {
+        CUDA_OK(cudaStreamWaitEvent(cs_, stage_ready_[static_cast<size_t>(i)], 0));
+        const int64_t n = S.numel();
+        cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
+            S.master, reinterpret_cast<bf16*>(S.w), n);
+        stats.kernels_launched += 1;
+      }
+    }
+    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i);
+    stats.kernels_launched += 1;
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    stats.tasks_executed += 1;
+    return;
+  }
+  exec_comm(pos);
+}
+
+void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out) {
+  const int N = static_cast<int>(sched.order.size());
+  const auto& g = sched.g;
+  stats = amdp_run_stats{};
+  if (rc_.record_events && ev_start_.empty()) {
+    ev_start_.resize(static_cast<size_t>(N));
+    ev_end_.resize(static_cast<size_t>(N));
+    for (int k = 0; k < N; ++k) {
+      CUDA_OK(cudaEventCreate(&ev_start_[static_cast<size_t>(k)]));
+      CUDA_OK(cudaEventCreate(&ev_end_[static_cast<size_t>(k)]));
+    }
+  }
+  CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_) * sizeof(int), cs_));
+  CUDA_OK(cudaMemsetAsync(d_loss_, 0, static_cast<size_t>(M_) * sizeof(float), cs_));
+  CUDA_OK(cudaMemsetAsync(d_trace_, 0xff, g.tasks.size() * sizeof(int), cs_));
+  std::vector<int> loaded(static_cast<size_t>(W_), 0), last_left(static_cast<size_t>(W_), 0);
+  for (int k = 0; k < N; ++k) {
+    const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
+    if (t.kind == ppsim::Kind::Forward && t.stage == depth_ - 1 && plan_[static_cast<size_t>(k)].local)
+      ++last_left[static_cast<size_t>(t.window)];
+  }
+  CUDA_OK(cudaEventRecord(run_begin_, cs_));
+  for (int k = 0; k < N; ++k) exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
+  {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_OK(cudaEventRecord(e, ms_));
+    CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
+    cudaEventDestroy(e);
+  }
+  CUDA_OK(cudaEventRecord(run_end_, cs_));
+  CUDA_OK(cudaStreamSynchronize(cs_));
+  float ms = 0.f;
+  CUDA_OK(cudaEventElapsedTime(&ms, run_begin_, run_end_));
+  stats.device_ms = ms;
+  if (losses_out)
+    for (int j = 0; j < M_; ++j) losses_out[j] /= static_cast<float>(dm.T);
+
+  // measured timeline + observed versions
+  std::vector<int> trace(g.tasks.size());
+  CUDA_OK(cudaMemcpy(trace.data(), d_trace_, trace.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  version_seen = trace;
+  events.clear();
+  double busy = 0;
+  if (rc_.record_events) {
+    for (int k = 0; k < N; ++k) {
+      const TaskPlan& tp = plan_[static_cast<size_t>(k)];
+      const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
+      const bool fb = t.kind == ppsim::Kind::Forward || t.kind == ppsim::Kind::Backward;
+      if (fb ? !tp.local : !hosted[static_cast<size_t>(t.stage)] || rank_of_dev(t.device) != rank_) continue;
+      float a = 0.f, b = 0.f;
+      CUDA_OK(cudaEventElapsedTime(&a, run_begin_, ev_start_[static_cast<size_t>(k)]));
+      CUDA_OK(cudaEventElapsedTime(&b, run_begin_, ev_end_[static_cast<size_t>(k)]));
+      const int64_t s_ns = std::llround(static_cast<double>(a) * 1e6);
+      int64_t e_ns = std::llround(static_cast<double>(b) * 1e6);
+      if (e_ns < s_ns) e_ns = s_ns;
+      ppsim::TaskEvent ev;
+      ev.kind = t.kind;
+      ev.stage = t.stage;
+      ev.minibatch = t.minibatch;
+      ev.pipeline = t.pipeline;
+      ev.device = t.device;
+      ev.window = t.window;
+      ev.preloaded = t.preloaded;
+      ev.start = ppsim::Rat(s_ns);
+      ev.duration = ppsim::Rat(e_ns - s_ns);
+      busy += static_cast<double>(e_ns - s_ns) * 1e-6;
+      events.push_back(ev);
+    }
+  }
+  stats.busy_ms = busy;
+}
+
+std::string Engine::plan_json() const {
+  std::string s = "{\"depth\":" + std::to_string(depth_) + ",\"world_size\":" + std::to_string(world_) +
+                  ",\"rank\":" + std::to_string(rank_) + ",\"tokens_per_minibatch\":" + std::to_string(dm.T) +
+                  ",\"partition\":[";
+  for (size_t i = 0; i < part.size(); ++i) s += (i ? "," : "") + std::to_string(part[i]);
+  s += "],\"stages\":[";
+  for (int i = 0; i < depth_; ++i) {
+    const GptStage& st = *stages[static_cast<size_t>(i)];
+    s += std::string(i ? ",{" : "{") + "\"stage\":" + std::to_string(i) + ",\"hosted\":" +
+         (hosted[static_cast<size_t>(i)] ? "true" : "false") + ",\"owner\":" +
+         (owned[static_cast<size_t>(i)] ? "true" : "false") + ",\"numel\":" + std::to_string(st.numel()) +
+         ",\"slots\":" + std::to_string(slots_per_stage[static_cast<size_t>(i)]) +
+         ",\"slot_bytes\":" + std::to_string(st.slot_bytes()) + ",\"group\":[";
+    const auto& gr = group_ranks_[static_cast<size_t>(i)];
+    for (size_t k = 0; k < gr.size(); ++k) s += (k ? "," : "") + std::to_string(gr[k]);
+    s += "],\"params\":[";
+    const auto& ps = st.params();
+    for (size_t k = 0; k < ps.size(); ++k)
+      s += std::string(k ? ",{" : "{") + "\"name\":\"" + ps[k].name + "\",\"offset\":" + std::to_string(ps[k].off) +
+           ",\"rows\":" + std::to_string(ps[k].rows) + ",\"cols\":" + std::to_string(ps[k].cols) +
+           ",\"global_index\":" + std::to_string(ps[k].global_index) + ",\"init\":" + std::to_string(ps[k].init) +
+           ",\"std\":" + std::to_string(ps[k].std) + "}";
+    s += "]}";
+  }
+  s += "],\"boundary_buffers\":" + std::to_string(nbuf) + ",\"activation_bytes\":" + std::to_string(slot_total_) +
+       ",\"workspace_bytes\":" + std::to_string(GptStage::workspace_bytes(dm)) + ",\"comm_ops\":[";
+  bool first = true;
+  for (size_t k = 0; k < comm_at_.size(); ++k)
+    for (const CommOp& op : comm_at_[k]) {
+      static const char* names[] = {"send", "recv", "reduce", "bcast"};
+      s += std::string(first ? "[" : ",[") + std::to_string(k) + ",\"" + names[op.kind] + "\"," +
+           std::to_string(op.peer) + "," + std::to_string(op.stage) + "]";
+      first = false;
+    }
+  return s + "]}";
+}
+
+std::string Engine::version_csv() const {
+  std::string s = "device,kind,stage,minibatch,pipeline,window,preloaded,version\n";
+  std::vector<std::vector<int>> per_dev(static_cast<size_t>(depth_));
+  for (size_t k = 0; k < sched.order.size(); ++k) {
+    const int t = sched.order[k];
+    const auto& task = sched.g.tasks[static_cast<size_t>(t)];
+    if ((task.kind == ppsim::Kind::Forward || task.kind == ppsim::Kind::Backward) && plan_[k].local)
+      per_dev[static_cast<size_t>(task.device)].push_back(t);
+  }
+  for (int d = 0; d < depth_; ++d)
+    for (int t : per_dev[static_cast<size_t>(d)]) {
+      const auto& e = sched.g.tasks[static_cast<size_t>(t)];
+      s += std::to_string(d) + ',' + ppsim::kind_name(e.kind) + ',' + std::to_string(e.stage) + ',' +
+           std::to_string(e.minibatch) + ',' + std::to_string(e.pipeline) + ',' + std::to_string(e.window) + ',' +
+           (e.preloaded ? '1' : '0') + ',' +
+           std::to_string(version_seen.empty() ? -1 : version_seen[static_cast<size_t>(t)]) + '\n';
+    }
+  return s;
+}
+
+int64_t Engine::stage_numel(int stage) const { return stages.at(static_cast<size_t>(stage))->numel(); }
+
+void Engine::copy_params(int stage, float* host, int64_t n, bool to_host) {
+  GptStage& st = *stages.at(static_cast<size_t>(stage));
+  if (!hosted[static_cast<size_t>(stage)]) throw std::invalid_argument("stage not hosted on this rank");
+  if (n != st.numel()) throw std::invalid_argument("parameter count mismatch");
+  CUDA_OK(cudaStreamSynchronize(cs_));
+  if (to_host) {
+    CUDA_OK(cudaMemcpy(host, st.master, static_cast<size_t>(n) * sizeof(float), cudaMemcpyDeviceToHost));
+  } else {
+    CUDA_OK(cudaMemcpy(st.master, host, static_cast<size_t>(n) * sizeof(float), cudaMemcpyHostToDevice));
+    cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
+        st.master, reinterpret_cast<bf16*>(st.w), n);
+    CUDA_OK(cudaStreamSynchronize(cs_));
+  }
+}
+
+}  // namespace amdp
+
+// ====================================================================== C-ABI
+namespace {
+void put_err(char* err, size_t len, const std::string& m) {
+  if (!err || !len) return;
+  const size_t n = std::min(len - 1, m.size());
+  std::memcpy(err, m.data(), n);
+  err[n] = 0;
+}
+size_t put_text(const std::string& s, char* buf, size_t len) {
+  if (buf && len) {
+    const size_t n = std::min(len - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return s.size();
+}
+}  // namespace
+
+using amdp::Engine;
+
+extern "C" {
+
+int amdp_nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return AMDP_ERR_CUDA;
+  std::memcpy(out, &id, sizeof(id));
+  return 0;
+}
+
+amdp_engine* amdp_engine_create(const amdp_model_config* model, const amdp_run_config* run,
+                                const uint8_t* nccl_id, char* err, size_t errlen) {
+  try {
+    return reinterpret_cast<amdp_engine*>(new Engine(*model, *run, nccl_id));
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return nullptr;
+  }
+}
+
+void amdp_engine_destroy(amdp_engine* e) { delete reinterpret_cast<Engine*>(e); }
+
+void* amdp_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+void amdp_host_free(void* p) { cudaFreeHost(p); }
+
+int amdp_synthetic_tokens(const amdp_model_config* m, uint64_t seed, int first, int count, int32_t* inputs,
+                          int32_t* labels) {
+  const int S = m->seq, B = m->seqs_per_minibatch, V = m->vocab;
+  if (S <= 0 || B <= 0 || V <= 0 || count < 0) return AMDP_ERR_INVALID;
+  const size_t T = static_cast<size_t>(S) * B;
+  for (int j = 0; j < count; ++j) {
+    const uint64_t mb = static_cast<uint64_t>(first + j);
+    for (int b = 0; b < B; ++b) {
+      const uint64_t r = amdp::splitmix64(seed * 0x100000001B3ull + mb * 1024ull + static_cast<uint64_t>(b));
+      const uint64_t start = r % static_cast<uint64_t>(V);
+      const uint64_t stride = 1 + (r >> 32) % 7;
+      for (int p = 0; p <= S; ++p) {
+        const uint64_t nz = amdp::splitmix64(r + static_cast<uint64_t>(p) + 1);
+        const int32_t tok = static_cast<int32_t>((nz & 7) == 0 ? (nz >> 8) % static_cast<uint64_t>(V)
+                                                               : (start + static_cast<uint64_t>(p) * stride) %
+                                                                     static_cast<uint64_t>(V));
+        const size_t base = static_cast<size_t>(j) * T + static_cast<size_t>(b) * S;
+        if (p < S) inputs[base + static_cast<size_t>(p)] = tok;
+        if (p > 0) labels[base + static_cast<size_t>(p) - 1] = tok;
+      }
+    }
+  }
+  return 0;
+}
+
+int amdp_engine_run(amdp_engine* e, const int32_t* inputs, const int32_t* labels, float* losses_out, char* err,
+                    size_t errlen) {
+  try {
+    reinterpret_cast<Engine*>(e)->run(inputs, labels, losses_out);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(err, errlen, ex.what());
+    return AMDP_ERR_CUDA;
+  }
+}
+
+int amdp_engine_stats(const amdp_engine* e, amdp_run_stats* out) {
+  *out = reinterpret_cast<const Engine*>(e)->stats;
+  return 0;
+}
+
+int amdp_engine_num_events(const amdp_engine* e) {
+  return static_cast<int>(reinterpret_cast<const Engine*>(e)->events.size());
+}
+
+int amdp_engine_events(const amdp_engine* e, amdp_event* out, int cap) {
+  const auto& ev = reinterpret_cast<const Engine*>(e)->events;
+  const int n = std::min(cap, static_cast<int>(ev.size()));
+  for (int i = 0; i < n; ++i) {
+    const auto& x = ev[static_cast<size_t>(i)];
+    out[i] = amdp_event{static_cast<int>(x.kind), x.stage, x.minibatch, x.pipeline, x.device, x.window,
+                        x.preloaded ? 1 : 0, amdp_rat{x.start.num(), x.start.den()},
+                        amdp_rat{x.duration.num(), x.duration.den()}};
+  }
+  return n;
+}
+
+size_t amdp_engine_version_trace(const amdp_engine* e, char* buf, size_t len) {
+  return put_text(reinterpret_cast<const Engine*>(e)->version_csv(), buf, len);
+}
+
+amdp_schedule* amdp_engine_schedule(const amdp_engine* e) {
+  return reinterpret_cast<amdp_schedule*>(new amdp::SchedHandle(reinterpret_cast<const Engine*>(e)->sched));
+}
+
+int64_t amdp_engine_stage_numel(const amdp_engine* e, int stage) {
+  try {
+    return reinterpret_cast<const Engine*>(e)->stage_numel(stage);
+  } catch (...) {
+    return -1;
+  }
+}
+
+int amdp_engine_get_stage_params(const amdp_engine* e, int stage, float* out, int64_t n) {
+  try {
+    const_cast<Engine*>(reinterpret_cast<const Engine*>(e))->copy_params(stage, out, n, true);
+    return 0;
+  } catch (...) {
+    return AMDP_ERR_INVALID;
+  }
+}
+
+int amdp_engine_set_stage_params(amdp_engine* e, int stage, const float* in, int64_t n) {
+  try {
+    reinterpret_cast<Engine*>(e)->copy_params(stage, const_cast<float*>(in), n, false);
+    return 0;
+  } catch (...) {
+    return AMDP_ERR_INVALID;
+  }
+}
+
+size_t amdp_engine_plan_json(const amdp_engine* e, char* buf, size_t len) {
+  return put_text(reinterpret_cast<const Engine*>(e)->plan_json(), buf, len);
+}
+
+}  // extern "C"

@@ -1,0 +1,276 @@
+// GPT stage forward/backward as kernel sequences (see gpt_stage.hpp).
+#include <cmath>
+
+#include "gpt_stage.hpp"
+
+namespace amdp {
+
+namespace {
+constexpr int64_t kAlign = 64;  // elements; keeps every tensor 128-B aligned for TMA
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Carver {
+  uint8_t* p;
+  size_t used = 0;
+  template <class T>
+  T* take(size_t n) {
+    T* r = reinterpret_cast<T*>(p ? p + used : nullptr);
+    used += (n * sizeof(T) + 255) & ~static_cast<size_t>(255);
+    return r;
+  }
+};
+
+int gemm(int M, int N, int K, const void* A, int lda, bool amn, const void* B, int ldb, bool bmn,
+         void* C, int ldc, int epi, cudaStream_t s, const void* aux = nullptr, int ld_aux = 0,
+         void* C2 = nullptr, int ldc2 = 0) {
+  amdp_gemm_args a{M, N, K, A, lda, amn ? 1 : 0, B, ldb, bmn ? 1 : 0, C, ldc, aux, ld_aux, C2, ldc2,
+                   epi, 1.0f};
+  return amdp_gemm(&a, reinterpret_cast<amdp_stream_t>(s));
+}
+}  // namespace
+
+GptStage::GptStage(const Dims& d, int stage, int depth, int l0, int l1)
+    : d_(d), stage_(stage), depth_(depth), l0_(l0), l1_(l1) {
+  const float std = 0.02f;
+  const float proj_std = std / std::sqrt(2.0f * static_cast<float>(d.L));
+  if (first()) {
+    wte_ = add("wte", d.V, d.h, 0, 0, std);
+    wpe_ = add("wpe", d.S, d.h, 1, 0, std);
+  }
+  for (int l = l0; l < l1; ++l) {
+    const int g = 16 + 8 * l;
+    const std::string p = "layer" + std::to_string(l) + ".";
+    LayerParams lp;
+    lp.ln1_g = add(p + "ln1.gamma", 1, d.h, g + 0, 1, 0.f);
+    lp.ln1_b = add(p + "ln1.beta", 1, d.h, g + 1, 2, 0.f);
+    lp.qkv = add(p + "attn.qkv", 3 * d.h, d.h, g + 2, 0, std);
+    lp.o = add(p + "attn.out", d.h, d.h, g + 3, 0, proj_std);
+    lp.ln2_g = add(p + "ln2.gamma", 1, d.h, g + 4, 1, 0.f);
+    lp.ln2_b = add(p + "ln2.beta", 1, d.h, g + 5, 2, 0.f);
+    lp.fc1 = add(p + "mlp.fc1", d.ffn, d.h, g + 6, 0, std);
+    lp.fc2 = add(p + "mlp.fc2", d.h, d.ffn, g + 7, 0, proj_std);
+    layers_.push_back(lp);
+  }
+  if (last()) {
+    lnf_g_ = add("lnf.gamma", 1, d.h, 2, 1, 0.f);
+    lnf_b_ = add("lnf.beta", 1, d.h, 3, 2, 0.f);
+    head_ = add("head", d.V, d.h, 4, 0, std);
+  }
+}
+
+ParamRef GptStage::add(const std::string& name, int rows, int cols, int gidx, int init, float std) {
+  ParamRef r;
+  r.name = name;
+  r.off = numel_;
+  r.rows = rows;
+  r.cols = cols;
+  r.global_index = gidx;
+  r.init = init;
+  r.std = std;
+  numel_ = round_up(numel_ + r.numel(), kAlign);
+  all_.push_back(r);
+  return r;
+}
+
+size_t GptStage::slot_bytes() const {
+  Carver c{nullptr};
+  SlotActs a;
+  (void)a;
+  const size_t T = static_cast<size_t>(d_.T), h = static_cast<size_t>(d_.h);
+  if (first()) c.take<uint16_t>(T * h);
+  for (int l = l0_; l < l1_; ++l) {
+    if (l > l0_) c.take<uint16_t>(T * h);  // x
+    c.take<uint16_t>(T * h);               // ln1
+    c.take<uint16_t>(T * 3 * h);           // qkv
+    c.take<uint16_t>(T * h);               // o
+    c.take<uint16_t>(T * h);               // hmid
+    c.take<uint16_t>(T * h);               // ln2
+    c.take<uint16_t>(T * d_.ffn);          // u
+    c.take<uint16_t>(T * d_.ffn);          // f
+    c.take<float>(T);
+    c.take<float>(T);
+    c.take<float>(T);
+    c.take<float>(T);
+    c.take<float>(static_cast<size_t>(d_.B) * d_.heads * d_.S);  // lse
+  }
+  if (last()) {
+    c.take<uint16_t>(T * h);
+    c.take<uint16_t>(T * h);
+    c.take<float>(T);
+    c.take<float>(T);
+    c.take<uint16_t>(T * static_cast<size_t>(d_.V));
+  }
+  return c.used;
+}
+
+SlotActs GptStage::carve_slot(uint8_t* base) const {
+  Carver c{base};
+  SlotActs a;
+  const size_t T = static_cast<size_t>(d_.T), h = static_cast<size_t>(d_.h);
+  if (first()) a.x0 = c.take<uint16_t>(T * h);
+  for (int l = l0_; l < l1_; ++l) {
+    LayerActs la;
+    if (l > l0_) la.x = c.take<uint16_t>(T * h);
+    la.ln1 = c.take<uint16_t>(T * h);
+    la.qkv = c.take<uint16_t>(T * 3 * h);
+    la.o = c.take<uint16_t>(T * h);
+    la.hmid = c.take<uint16_t>(T * h);
+    la.ln2 = c.take<uint16_t>(T * h);
+    la.u = c.take<uint16_t>(T * d_.ffn);
+    la.f = c.take<uint16_t>(T * d_.ffn);
+    la.ln1_mean = c.take<float>(T);
+    la.ln1_rstd = c.take<float>(T);
+    la.ln2_mean = c.take<float>(T);
+    la.ln2_rstd = c.take<float>(T);
+    la.lse = c.take<float>(static_cast<size_t>(d_.B) * d_.heads * d_.S);
+    a.layers.push_back(la);
+  }
+  if (last()) {
+    a.xf = c.take<uint16_t>(T * h);
+    a.lnf = c.take<uint16_t>(T * h);
+    a.lnf_mean = c.take<float>(T);
+    a.lnf_rstd = c.take<float>(T);
+    a.logits = c.take<uint16_t>(T * static_cast<size_t>(d_.V));
+  }
+  return a;
+}
+
+namespace {
+struct Ws {
+  uint16_t *g0, *g1, *dU, *dqkv, *dtmp, *dhmid;
+  float* attn;
+  uint8_t* ln;
+};
+Ws carve_ws(const Dims& d, uint8_t* base) {
+  Carver c{base};
+  const size_t T = static_cast<size_t>(d.T), h = static_cast<size_t>(d.h);
+  Ws w;
+  w.g0 = c.take<uint16_t>(T * h);
+  w.g1 = c.take<uint16_t>(T * h);
+  w.dU = c.take<uint16_t>(T * d.ffn);
+  w.dqkv = c.take<uint16_t>(T * 3 * h);
+  w.dtmp = c.take<uint16_t>(T * h);
+  w.dhmid = c.take<uint16_t>(T * h);
+  w.attn = c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
+  w.ln = c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
+  return w;
+}
+}  // namespace
+
+size_t GptStage::workspace_bytes(const Dims& d) {
+  Carver c{nullptr};
+  const size_t T = static_cast<size_t>(d.T), h = static_cast<size_t>(d.h);
+  c.take<uint16_t>(T * h);
+  c.take<uint16_t>(T * h);
+  c.take<uint16_t>(T * d.ffn);
+  c.take<uint16_t>(T * 3 * h);
+  c.take<uint16_t>(T * h);
+  c.take<uint16_t>(T * h);
+  c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
+  c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
+  return c.used;
+}
+
+#define AMDP_TRY(expr, nk)      \
+  do {                          \
+    const int _r = (expr);      \
+    if (_r != 0) {              \
+      *rc = _r;                 \
+      return launched;          \
+    }                           \
+    launched += (nk);           \
+  } while (0)
+
+int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
+                      const uint16_t* in, uint16_t* out, float* loss_sum, uint8_t* /*ws*/,
+                      cudaStream_t s, int* rc) const {
+  int launched = 0;
+  *rc = 0;
+  auto st = reinterpret_cast<amdp_stream_t>(s);
+  const int T = d_.T, h = d_.h;
+  const uint16_t* x = in;
+  if (first()) {
+    AMDP_TRY(amdp_embedding_fwd(tokens, w + wte_.off, w + wpe_.off, a.x0, T, d_.S, h, st), 1);
+    x = a.x0;
+  }
+  for (int li = 0; li < l1_ - l0_; ++li) {
+    const LayerParams& P = layers_[static_cast<size_t>(li)];
+    const LayerActs& A = a.layers[static_cast<size_t>(li)];
+    AMDP_TRY(amdp_layernorm_fwd(x, master + P.ln1_g.off, master + P.ln1_b.off, A.ln1, A.ln1_mean,
+                                A.ln1_rstd, T, h, d_.ln_eps, st), 1);
+    AMDP_TRY(gemm(T, 3 * h, h, A.ln1, h, false, w + P.qkv.off, h, false, A.qkv, 3 * h,
+                  AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_TRY(amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, st), 1);
+    AMDP_TRY(gemm(T, h, h, A.o, h, false, w + P.o.off, h, false, A.hmid, h, AMDP_EPI_RESIDUAL, s, x, h), 1);
+    AMDP_TRY(amdp_layernorm_fwd(A.hmid, master + P.ln2_g.off, master + P.ln2_b.off, A.ln2, A.ln2_mean,
+                                A.ln2_rstd, T, h, d_.ln_eps, st), 1);
+    AMDP_TRY(gemm(T, d_.ffn, h, A.ln2, h, false, w + P.fc1.off, h, false, A.f, d_.ffn, AMDP_EPI_GELU, s,
+                  nullptr, 0, A.u, d_.ffn), 1);
+    uint16_t* nx;
+    if (li + 1 < l1_ - l0_) nx = a.layers[static_cast<size_t>(li) + 1].x;
+    else nx = last() ? a.xf : out;
+    AMDP_TRY(gemm(T, h, d_.ffn, A.f, d_.ffn, false, w + P.fc2.off, d_.ffn, false, nx, h, AMDP_EPI_RESIDUAL,
+                  s, A.hmid, h), 1);
+    x = nx;
+  }
+  if (last()) {
+    AMDP_TRY(amdp_layernorm_fwd(a.xf, master + lnf_g_.off, master + lnf_b_.off, a.lnf, a.lnf_mean,
+                                a.lnf_rstd, T, h, d_.ln_eps, st), 1);
+    AMDP_TRY(gemm(T, d_.V, h, a.lnf, h, false, w + head_.off, h, false, a.logits, d_.V,
+                  AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_TRY(amdp_xent_fwd_bwd(a.logits, labels, loss_sum, T, d_.V, d_.V, 1.0f / static_cast<float>(T), st), 1);
+  }
+  return launched;
+}
+
+int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in, const uint16_t* gin,
+                       uint16_t* gout, uint8_t* wsb, cudaStream_t s, int* rc) const {
+  int launched = 0;
+  *rc = 0;
+  auto st = reinterpret_cast<amdp_stream_t>(s);
+  const int T = d_.T, h = d_.h, F = d_.ffn;
+  const Ws ws = carve_ws(d_, wsb);
+  const uint16_t* g = gin;
+  if (last()) {
+    // a.logits already holds dloss/dlogits (scale 1/T), written by the forward's CE pass
+    AMDP_TRY(gemm(T, h, d_.V, a.logits, d_.V, false, w + head_.off, h, true, ws.dtmp, h,
+                  AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_TRY(gemm(d_.V, h, T, a.logits, d_.V, true, a.lnf, h, true, grad + head_.off, h,
+                  AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_TRY(amdp_layernorm_bwd(ws.dtmp, a.xf, master + lnf_g_.off, a.lnf_mean, a.lnf_rstd, nullptr, ws.g0,
+                                grad + lnf_g_.off, grad + lnf_b_.off, ws.ln, T, h, st), 2);
+    g = ws.g0;
+  }
+  for (int li = l1_ - l0_ - 1; li >= 0; --li) {
+    const LayerParams& P = layers_[static_cast<size_t>(li)];
+    const LayerActs& A = a.layers[static_cast<size_t>(li)];
+    const uint16_t* x = li > 0 ? A.x : (first() ? a.x0 : in);
+    // y = hmid + f W2^T
+    AMDP_TRY(gemm(T, F, h, g, h, false, w + P.fc2.off, F, true, ws.dU, F, AMDP_EPI_GELU_BWD, s, A.u, F), 1);
+    AMDP_TRY(gemm(h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, s), 1);
+    // f = gelu(ln2 W1^T)
+    AMDP_TRY(gemm(T, h, F, ws.dU, F, false, w + P.fc1.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_TRY(gemm(F, h, T, ws.dU, F, true, A.ln2, h, true, grad + P.fc1.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    // ln2 = LN(hmid); dhmid = g + LN'(dln2)
+    AMDP_TRY(amdp_layernorm_bwd(ws.dtmp, A.hmid, master + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g, ws.dhmid,
+                                grad + P.ln2_g.off, grad + P.ln2_b.off, ws.ln, T, h, st), 2);
+    // hmid = x + o Wo^T
+    AMDP_TRY(gemm(T, h, h, ws.dhmid, h, false, w + P.o.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_TRY(gemm(h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_TRY(amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
+                                d_.causal ? 1 : 0, st), 3);
+    // qkv = ln1 Wqkv^T
+    AMDP_TRY(gemm(T, h, 3 * h, ws.dqkv, 3 * h, false, w + P.qkv.off, h, true, ws.dtmp, h,
+                  AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_TRY(gemm(3 * h, h, T, ws.dqkv, 3 * h, true, A.ln1, h, true, grad + P.qkv.off, h,
+                  AMDP_EPI_ACCUM_F32, s), 1);
+    uint16_t* gn = (li == 0 && !first()) ? gout : (g == ws.g0 ? ws.g1 : ws.g0);
+    AMDP_TRY(amdp_layernorm_bwd(ws.dtmp, x, master + P.ln1_g.off, A.ln1_mean, A.ln1_rstd, ws.dhmid, gn,
+                                grad + P.ln1_g.off, grad + P.ln1_b.off, ws.ln, T, h, st), 2);
+    g = gn;
+  }
+  if (first()) AMDP_TRY(amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, T, d_.S, h, st), 2);
+  return launched;
+}
+
+}  // namespace amdp

@@ -1,0 +1,99 @@
+// GPT stage model for the AMDP executor: parameter layout of one pipeline stage (a
+// contiguous range of transformer layers, plus the embedding on the first stage and the
+// final LayerNorm + LM head on the last), its activation slot layout, and the forward /
+// backward task bodies as sequences of sm_100a kernel launches (include/amdp_kernels.h).
+//
+// The reference models a stage only as an opaque cost (ppsim types.hpp:63-64); the
+// arithmetic here is this repository's (pre-LN GPT, no linear biases, untied LM head),
+// restated on the CPU by oracle/gpt_oracle.py for the loss/weight parity tests.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "amdp_kernels.h"
+
+namespace amdp {
+
+struct Dims {
+  int L, h, heads, hd, ffn, V, S, B, T;  // T = B * S tokens per minibatch
+  bool causal;
+  float ln_eps;
+};
+
+struct ParamRef {
+  std::string name;
+  int64_t off = 0;  // element offset in the stage's flat buffers
+  int rows = 0, cols = 0;
+  int global_index = 0;  // model-wide tensor id (init seeding, partition-independent)
+  int init = 0;          // 0 normal(std), 1 ones, 2 zeros
+  float std = 0.f;
+  int64_t numel() const { return static_cast<int64_t>(rows) * cols; }
+};
+
+struct LayerParams {
+  ParamRef ln1_g, ln1_b, qkv, o, ln2_g, ln2_b, fc1, fc2;
+};
+
+// Activations of one (stage, minibatch) between its Forward and Backward.
+struct LayerActs {
+  uint16_t *x = nullptr, *ln1 = nullptr, *qkv = nullptr, *o = nullptr, *hmid = nullptr,
+           *ln2 = nullptr, *u = nullptr, *f = nullptr;
+  float *ln1_mean = nullptr, *ln1_rstd = nullptr, *ln2_mean = nullptr, *ln2_rstd = nullptr,
+        *lse = nullptr;
+};
+struct SlotActs {
+  std::vector<LayerActs> layers;
+  uint16_t* x0 = nullptr;      // stage 0: embedding output (layer-0 input)
+  uint16_t* xf = nullptr;      // last stage: final residual stream
+  uint16_t* lnf = nullptr;     // last stage: final LayerNorm output
+  float *lnf_mean = nullptr, *lnf_rstd = nullptr;
+  uint16_t* logits = nullptr;  // last stage: [T][V] logits, overwritten by dlogits
+};
+
+class GptStage {
+ public:
+  GptStage(const Dims& d, int stage, int depth, int l0, int l1);
+
+  int stage() const { return stage_; }
+  bool first() const { return stage_ == 0; }
+  bool last() const { return stage_ == depth_ - 1; }
+  int64_t numel() const { return numel_; }
+  const std::vector<ParamRef>& params() const { return all_; }
+  size_t slot_bytes() const;
+  SlotActs carve_slot(uint8_t* base) const;
+  // Workspace shared by all tasks on one stream.
+  static size_t workspace_bytes(const Dims& d);
+
+  // Buffers of this stage on this GPU.
+  float* master = nullptr;  // fp32 weights (owner: updated by the optimizer)
+  float* m = nullptr;
+  float* v = nullptr;
+  float* grad = nullptr;    // fp32 window-accumulated gradient
+  uint16_t* w = nullptr;    // bf16 working weights read by the kernels
+
+  // Task bodies (stream-ordered).  `in`: stage input [T][h] (stages > 0); `out`: stage
+  // output [T][h] (stages < depth-1).  Backward: `gin` incoming grad [T][h] (stages <
+  // depth-1), `gout` grad w.r.t. the stage input (stages > 0).  Returns the number of
+  // kernels launched (>= 0) or a negative/positive error code via `rc`.
+  int forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
+              const uint16_t* in, uint16_t* out, float* loss_sum, uint8_t* ws,
+              cudaStream_t s, int* rc) const;
+  int backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in,
+               const uint16_t* gin, uint16_t* gout, uint8_t* ws, cudaStream_t s,
+               int* rc) const;
+
+ private:
+  Dims d_;
+  int stage_, depth_, l0_, l1_;
+  int64_t numel_ = 0;
+  std::vector<LayerParams> layers_;
+  ParamRef wte_, wpe_, lnf_g_, lnf_b_, head_;
+  std::vector<ParamRef> all_;
+  ParamRef add(const std::string& name, int rows, int cols, int gidx, int init, float std);
+};
+
+}  // namespace amdp
