@@ -82,6 +82,26 @@ int amdp_synthetic_tokens(const amdp_model_config* model, uint64_t data_seed,
  * (valid on the rank hosting the last stage).  Returns when the device work is done. */
 int amdp_engine_run(amdp_engine* e, const int32_t* inputs, const int32_t* labels,
                     float* losses_out, char* err, size_t errlen);
+/* Runs the tasks of windows [0, num_windows) of the schedule in dispatch order (a window
+ * prefix: the pipeline starts empty and drains at the end; the next window's preloaded
+ * forwards are not run).  resident != 0: the token arrays were already copied to the
+ * device by amdp_engine_stage_tokens and no host->device copy happens inside the run. */
+int amdp_engine_run_windows(amdp_engine* e, int num_windows, const int32_t* inputs,
+                            const int32_t* labels, float* losses_out, int resident,
+                            char* err, size_t errlen);
+/* Copies all token arrays to the device now (synchronously). */
+int amdp_engine_stage_tokens(amdp_engine* e, const int32_t* inputs, const int32_t* labels);
+
+/* Per-kernel-class CUDA-event timing inside runs (adds two events per launch). */
+typedef struct amdp_kernel_class_stats {
+  char name[24];
+  int64_t launches;
+  double total_ms;
+  double flops; /* algorithmic (tensor-pipe work) */
+  double bytes; /* algorithmic HBM bytes (memory-bound classes) */
+} amdp_kernel_class_stats;
+int amdp_engine_set_kernel_timing(amdp_engine* e, int enable);
+int amdp_engine_kernel_stats(const amdp_engine* e, amdp_kernel_class_stats* out, int cap);
 
 /* Stats of the last run: device-timed milliseconds from the first task to the last,
  * tasks / kernels launched by this rank, bytes copied H2D / D2H. */

@@ -30,6 +30,7 @@
 #include "../kernels/common.cuh"
 #include "../sched/sched_handle.hpp"
 #include "gpt_stage.hpp"
+#include "ktimer.hpp"
 #include "ppsim/ppsim.hpp"
 
 namespace amdp {
@@ -64,9 +65,9 @@ uint64_t tensor_seed(uint64_t model_seed, int gidx) {
 }
 
 // Balanced contiguous partition of L layers over `depth` stages, costing the LM head as
-// (V / (6 h)) layer-equivalents on the last stage (2hV vs 12h^2 flops per token).
+// V / (12 h) layer-equivalents on the last stage (2hV vs 24h^2 forward flops per token).
 std::vector<int> balance_layers(int L, int depth, int h, int V) {
-  const double head = static_cast<double>(V) / (6.0 * h);
+  const double head = static_cast<double>(V) / (12.0 * h);
   std::vector<int> best;
   double best_max = 1e300;
   // last stage gets k layers, the rest spread as evenly as possible
@@ -120,7 +121,14 @@ class Engine {
  public:
   Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uint8_t* nccl_id);
   ~Engine();
-  void run(const int32_t* inputs, const int32_t* labels, float* losses_out);
+  void run(const int32_t* inputs, const int32_t* labels, float* losses_out, int max_window = -1,
+           bool resident = false);
+  void stage_tokens(const int32_t* inputs, const int32_t* labels);
+  void set_kernel_timing(bool on) {
+    ktimer_.enabled = on;
+    for (auto& s : stages) s->kt = on ? &ktimer_ : nullptr;
+  }
+  KTimer ktimer_;
   std::string plan_json() const;
   std::string version_csv() const;
   int64_t stage_numel(int stage) const;
@@ -636,7 +644,9 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       amdp_opt_args o = rc_.optimizer;
       o.step = task.window + 1;
       o.grad_scale = rc_.optimizer.grad_scale * (1.0f / static_cast<float>(thr_));
+      ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), cs_);
       rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), st);
+      ktimer_.end(cs_);
       if (rc != 0) throw std::runtime_error("optimizer step failed");
       stats.kernels_launched += 1;
     } else {
@@ -677,10 +687,18 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
   exec_comm(pos);
 }
 
-void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out) {
+void Engine::stage_tokens(const int32_t* h_in, const int32_t* h_lab) {
+  const size_t n = static_cast<size_t>(M_) * static_cast<size_t>(dm.T) * sizeof(int32_t);
+  CUDA_OK(cudaMemcpy(d_inputs_, h_in, n, cudaMemcpyHostToDevice));
+  CUDA_OK(cudaMemcpy(d_labels_, h_lab, n, cudaMemcpyHostToDevice));
+}
+
+void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, int max_window, bool resident) {
   const int N = static_cast<int>(sched.order.size());
   const auto& g = sched.g;
+  if (max_window < 0 || max_window > W_) max_window = W_;
   stats = amdp_run_stats{};
+  ktimer_.reset();
   if (rc_.record_events && ev_start_.empty()) {
     ev_start_.resize(static_cast<size_t>(N));
     ev_end_.resize(static_cast<size_t>(N));
@@ -692,14 +710,16 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out) {
   CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_) * sizeof(int), cs_));
   CUDA_OK(cudaMemsetAsync(d_loss_, 0, static_cast<size_t>(M_) * sizeof(float), cs_));
   CUDA_OK(cudaMemsetAsync(d_trace_, 0xff, g.tasks.size() * sizeof(int), cs_));
-  std::vector<int> loaded(static_cast<size_t>(W_), 0), last_left(static_cast<size_t>(W_), 0);
+  std::vector<int> loaded(static_cast<size_t>(W_), resident ? 1 : 0), last_left(static_cast<size_t>(W_), 0);
   for (int k = 0; k < N; ++k) {
     const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
     if (t.kind == ppsim::Kind::Forward && t.stage == depth_ - 1 && plan_[static_cast<size_t>(k)].local)
       ++last_left[static_cast<size_t>(t.window)];
   }
   CUDA_OK(cudaEventRecord(run_begin_, cs_));
-  for (int k = 0; k < N; ++k) exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
+  for (int k = 0; k < N; ++k)
+    if (g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])].window < max_window)
+      exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
   {
     cudaEvent_t e;
     CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -712,8 +732,9 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out) {
   float ms = 0.f;
   CUDA_OK(cudaEventElapsedTime(&ms, run_begin_, run_end_));
   stats.device_ms = ms;
+  ktimer_.collect();
   if (losses_out)
-    for (int j = 0; j < M_; ++j) losses_out[j] /= static_cast<float>(dm.T);
+    for (int j = 0; j < max_window * thr_; ++j) losses_out[j] /= static_cast<float>(dm.T);
 
   // measured timeline + observed versions
   std::vector<int> trace(g.tasks.size());
@@ -726,6 +747,7 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out) {
       const TaskPlan& tp = plan_[static_cast<size_t>(k)];
       const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
       const bool fb = t.kind == ppsim::Kind::Forward || t.kind == ppsim::Kind::Backward;
+      if (t.window >= max_window) continue;
       if (fb ? !tp.local : !hosted[static_cast<size_t>(t.stage)] || rank_of_dev(t.device) != rank_) continue;
       float a = 0.f, b = 0.f;
       CUDA_OK(cudaEventElapsedTime(&a, run_begin_, ev_start_[static_cast<size_t>(k)]));
@@ -908,6 +930,45 @@ int amdp_engine_run(amdp_engine* e, const int32_t* inputs, const int32_t* labels
     put_err(err, errlen, ex.what());
     return AMDP_ERR_CUDA;
   }
+}
+
+int amdp_engine_run_windows(amdp_engine* e, int num_windows, const int32_t* inputs, const int32_t* labels,
+                            float* losses_out, int resident, char* err, size_t errlen) {
+  try {
+    reinterpret_cast<Engine*>(e)->run(inputs, labels, losses_out, num_windows, resident != 0);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(err, errlen, ex.what());
+    return AMDP_ERR_CUDA;
+  }
+}
+
+int amdp_engine_stage_tokens(amdp_engine* e, const int32_t* inputs, const int32_t* labels) {
+  try {
+    reinterpret_cast<Engine*>(e)->stage_tokens(inputs, labels);
+    return 0;
+  } catch (...) {
+    return AMDP_ERR_CUDA;
+  }
+}
+
+int amdp_engine_set_kernel_timing(amdp_engine* e, int enable) {
+  reinterpret_cast<Engine*>(e)->set_kernel_timing(enable != 0);
+  return 0;
+}
+
+int amdp_engine_kernel_stats(const amdp_engine* e, amdp_kernel_class_stats* out, int cap) {
+  const auto& kt = reinterpret_cast<const Engine*>(e)->ktimer_;
+  const int n = std::min(cap, static_cast<int>(amdp::K_NUM));
+  for (int c = 0; c < n; ++c) {
+    std::memset(out[c].name, 0, sizeof(out[c].name));
+    std::strncpy(out[c].name, amdp::kclass_name(c), sizeof(out[c].name) - 1);
+    out[c].launches = kt.launches[static_cast<size_t>(c)];
+    out[c].total_ms = kt.ms[static_cast<size_t>(c)];
+    out[c].flops = kt.flops[static_cast<size_t>(c)];
+    out[c].bytes = kt.bytes[static_cast<size_t>(c)];
+  }
+  return n;
 }
 
 int amdp_engine_stats(const amdp_engine* e, amdp_run_stats* out) {

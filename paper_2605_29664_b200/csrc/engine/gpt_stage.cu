@@ -2,6 +2,7 @@
 #include <cmath>
 
 #include "gpt_stage.hpp"
+#include "ktimer.hpp"
 
 namespace amdp {
 
@@ -20,12 +21,18 @@ struct Carver {
   }
 };
 
-int gemm(int M, int N, int K, const void* A, int lda, bool amn, const void* B, int ldb, bool bmn,
-         void* C, int ldc, int epi, cudaStream_t s, const void* aux = nullptr, int ld_aux = 0,
-         void* C2 = nullptr, int ldc2 = 0) {
+// One stage contraction; timed by class (forward / activation-gradient / weight-gradient)
+// when the executor's kernel timer is on.
+int gemm_t(KTimer* kt, int M, int N, int K, const void* A, int lda, bool amn, const void* B, int ldb,
+           bool bmn, void* C, int ldc, int epi, cudaStream_t s, const void* aux = nullptr,
+           int ld_aux = 0, void* C2 = nullptr, int ldc2 = 0) {
   amdp_gemm_args a{M, N, K, A, lda, amn ? 1 : 0, B, ldb, bmn ? 1 : 0, C, ldc, aux, ld_aux, C2, ldc2,
                    epi, 1.0f};
-  return amdp_gemm(&a, reinterpret_cast<amdp_stream_t>(s));
+  const int cls = epi == AMDP_EPI_ACCUM_F32 ? K_GEMM_WGRAD : (bmn ? K_GEMM_DGRAD : K_GEMM_FWD);
+  if (kt) kt->begin(cls, 2.0 * M * N * static_cast<double>(K), 0, s);
+  const int rc = amdp_gemm(&a, reinterpret_cast<amdp_stream_t>(s));
+  if (kt) kt->end(s);
+  return rc;
 }
 }  // namespace
 
@@ -171,14 +178,26 @@ size_t GptStage::workspace_bytes(const Dims& d) {
   return c.used;
 }
 
-#define AMDP_TRY(expr, nk)      \
-  do {                          \
-    const int _r = (expr);      \
-    if (_r != 0) {              \
-      *rc = _r;                 \
-      return launched;          \
-    }                           \
-    launched += (nk);           \
+#define AMDP_TRY(cls, fl, by, expr, nk)   \
+  do {                                    \
+    if (kt) kt->begin((cls), (fl), (by), s); \
+    const int _r = (expr);                \
+    if (kt) kt->end(s);                   \
+    if (_r != 0) {                        \
+      *rc = _r;                           \
+      return launched;                    \
+    }                                     \
+    launched += (nk);                     \
+  } while (0)
+
+#define AMDP_GEMM(call, nk)   \
+  do {                        \
+    const int _r = (call);    \
+    if (_r != 0) {            \
+      *rc = _r;               \
+      return launched;        \
+    }                         \
+    launched += (nk);         \
   } while (0)
 
 int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
@@ -190,35 +209,35 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
   const int T = d_.T, h = d_.h;
   const uint16_t* x = in;
   if (first()) {
-    AMDP_TRY(amdp_embedding_fwd(tokens, w + wte_.off, w + wpe_.off, a.x0, T, d_.S, h, st), 1);
+    AMDP_TRY(K_EMBED, 0, 6.0 * T * h, amdp_embedding_fwd(tokens, w + wte_.off, w + wpe_.off, a.x0, T, d_.S, h, st), 1);
     x = a.x0;
   }
   for (int li = 0; li < l1_ - l0_; ++li) {
     const LayerParams& P = layers_[static_cast<size_t>(li)];
     const LayerActs& A = a.layers[static_cast<size_t>(li)];
-    AMDP_TRY(amdp_layernorm_fwd(x, master + P.ln1_g.off, master + P.ln1_b.off, A.ln1, A.ln1_mean,
+    AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * h, amdp_layernorm_fwd(x, master + P.ln1_g.off, master + P.ln1_b.off, A.ln1, A.ln1_mean,
                                 A.ln1_rstd, T, h, d_.ln_eps, st), 1);
-    AMDP_TRY(gemm(T, 3 * h, h, A.ln1, h, false, w + P.qkv.off, h, false, A.qkv, 3 * h,
+    AMDP_GEMM(gemm_t(kt, T, 3 * h, h, A.ln1, h, false, w + P.qkv.off, h, false, A.qkv, 3 * h,
                   AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, st), 1);
-    AMDP_TRY(gemm(T, h, h, A.o, h, false, w + P.o.off, h, false, A.hmid, h, AMDP_EPI_RESIDUAL, s, x, h), 1);
-    AMDP_TRY(amdp_layernorm_fwd(A.hmid, master + P.ln2_g.off, master + P.ln2_b.off, A.ln2, A.ln2_mean,
+    AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, st), 1);
+    AMDP_GEMM(gemm_t(kt, T, h, h, A.o, h, false, w + P.o.off, h, false, A.hmid, h, AMDP_EPI_RESIDUAL, s, x, h), 1);
+    AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * h, amdp_layernorm_fwd(A.hmid, master + P.ln2_g.off, master + P.ln2_b.off, A.ln2, A.ln2_mean,
                                 A.ln2_rstd, T, h, d_.ln_eps, st), 1);
-    AMDP_TRY(gemm(T, d_.ffn, h, A.ln2, h, false, w + P.fc1.off, h, false, A.f, d_.ffn, AMDP_EPI_GELU, s,
+    AMDP_GEMM(gemm_t(kt, T, d_.ffn, h, A.ln2, h, false, w + P.fc1.off, h, false, A.f, d_.ffn, AMDP_EPI_GELU, s,
                   nullptr, 0, A.u, d_.ffn), 1);
     uint16_t* nx;
     if (li + 1 < l1_ - l0_) nx = a.layers[static_cast<size_t>(li) + 1].x;
     else nx = last() ? a.xf : out;
-    AMDP_TRY(gemm(T, h, d_.ffn, A.f, d_.ffn, false, w + P.fc2.off, d_.ffn, false, nx, h, AMDP_EPI_RESIDUAL,
+    AMDP_GEMM(gemm_t(kt, T, h, d_.ffn, A.f, d_.ffn, false, w + P.fc2.off, d_.ffn, false, nx, h, AMDP_EPI_RESIDUAL,
                   s, A.hmid, h), 1);
     x = nx;
   }
   if (last()) {
-    AMDP_TRY(amdp_layernorm_fwd(a.xf, master + lnf_g_.off, master + lnf_b_.off, a.lnf, a.lnf_mean,
+    AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * h, amdp_layernorm_fwd(a.xf, master + lnf_g_.off, master + lnf_b_.off, a.lnf, a.lnf_mean,
                                 a.lnf_rstd, T, h, d_.ln_eps, st), 1);
-    AMDP_TRY(gemm(T, d_.V, h, a.lnf, h, false, w + head_.off, h, false, a.logits, d_.V,
+    AMDP_GEMM(gemm_t(kt, T, d_.V, h, a.lnf, h, false, w + head_.off, h, false, a.logits, d_.V,
                   AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(amdp_xent_fwd_bwd(a.logits, labels, loss_sum, T, d_.V, d_.V, 1.0f / static_cast<float>(T), st), 1);
+    AMDP_TRY(K_XENT, 0, 6.0 * T * d_.V, amdp_xent_fwd_bwd(a.logits, labels, loss_sum, T, d_.V, d_.V, 1.0f / static_cast<float>(T), st), 1);
   }
   return launched;
 }
@@ -233,11 +252,11 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
   const uint16_t* g = gin;
   if (last()) {
     // a.logits already holds dloss/dlogits (scale 1/T), written by the forward's CE pass
-    AMDP_TRY(gemm(T, h, d_.V, a.logits, d_.V, false, w + head_.off, h, true, ws.dtmp, h,
+    AMDP_GEMM(gemm_t(kt, T, h, d_.V, a.logits, d_.V, false, w + head_.off, h, true, ws.dtmp, h,
                   AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(gemm(d_.V, h, T, a.logits, d_.V, true, a.lnf, h, true, grad + head_.off, h,
+    AMDP_GEMM(gemm_t(kt, d_.V, h, T, a.logits, d_.V, true, a.lnf, h, true, grad + head_.off, h,
                   AMDP_EPI_ACCUM_F32, s), 1);
-    AMDP_TRY(amdp_layernorm_bwd(ws.dtmp, a.xf, master + lnf_g_.off, a.lnf_mean, a.lnf_rstd, nullptr, ws.g0,
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, a.xf, master + lnf_g_.off, a.lnf_mean, a.lnf_rstd, nullptr, ws.g0,
                                 grad + lnf_g_.off, grad + lnf_b_.off, ws.ln, T, h, st), 2);
     g = ws.g0;
   }
@@ -246,30 +265,30 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     const LayerActs& A = a.layers[static_cast<size_t>(li)];
     const uint16_t* x = li > 0 ? A.x : (first() ? a.x0 : in);
     // y = hmid + f W2^T
-    AMDP_TRY(gemm(T, F, h, g, h, false, w + P.fc2.off, F, true, ws.dU, F, AMDP_EPI_GELU_BWD, s, A.u, F), 1);
-    AMDP_TRY(gemm(h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_GEMM(gemm_t(kt, T, F, h, g, h, false, w + P.fc2.off, F, true, ws.dU, F, AMDP_EPI_GELU_BWD, s, A.u, F), 1);
+    AMDP_GEMM(gemm_t(kt, h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, s), 1);
     // f = gelu(ln2 W1^T)
-    AMDP_TRY(gemm(T, h, F, ws.dU, F, false, w + P.fc1.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(gemm(F, h, T, ws.dU, F, true, A.ln2, h, true, grad + P.fc1.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_GEMM(gemm_t(kt, T, h, F, ws.dU, F, false, w + P.fc1.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_GEMM(gemm_t(kt, F, h, T, ws.dU, F, true, A.ln2, h, true, grad + P.fc1.off, h, AMDP_EPI_ACCUM_F32, s), 1);
     // ln2 = LN(hmid); dhmid = g + LN'(dln2)
-    AMDP_TRY(amdp_layernorm_bwd(ws.dtmp, A.hmid, master + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g, ws.dhmid,
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, A.hmid, master + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g, ws.dhmid,
                                 grad + P.ln2_g.off, grad + P.ln2_b.off, ws.ln, T, h, st), 2);
     // hmid = x + o Wo^T
-    AMDP_TRY(gemm(T, h, h, ws.dhmid, h, false, w + P.o.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(gemm(h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, s), 1);
-    AMDP_TRY(amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
+    AMDP_GEMM(gemm_t(kt, T, h, h, ws.dhmid, h, false, w + P.o.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
                                 d_.causal ? 1 : 0, st), 3);
     // qkv = ln1 Wqkv^T
-    AMDP_TRY(gemm(T, h, 3 * h, ws.dqkv, 3 * h, false, w + P.qkv.off, h, true, ws.dtmp, h,
+    AMDP_GEMM(gemm_t(kt, T, h, 3 * h, ws.dqkv, 3 * h, false, w + P.qkv.off, h, true, ws.dtmp, h,
                   AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(gemm(3 * h, h, T, ws.dqkv, 3 * h, true, A.ln1, h, true, grad + P.qkv.off, h,
+    AMDP_GEMM(gemm_t(kt, 3 * h, h, T, ws.dqkv, 3 * h, true, A.ln1, h, true, grad + P.qkv.off, h,
                   AMDP_EPI_ACCUM_F32, s), 1);
     uint16_t* gn = (li == 0 && !first()) ? gout : (g == ws.g0 ? ws.g1 : ws.g0);
-    AMDP_TRY(amdp_layernorm_bwd(ws.dtmp, x, master + P.ln1_g.off, A.ln1_mean, A.ln1_rstd, ws.dhmid, gn,
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, x, master + P.ln1_g.off, A.ln1_mean, A.ln1_rstd, ws.dhmid, gn,
                                 grad + P.ln1_g.off, grad + P.ln1_b.off, ws.ln, T, h, st), 2);
     g = gn;
   }
-  if (first()) AMDP_TRY(amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, T, d_.S, h, st), 2);
+  if (first()) AMDP_TRY(K_EMBED, 0, 10.0 * T * h, amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, T, d_.S, h, st), 2);
   return launched;
 }
 

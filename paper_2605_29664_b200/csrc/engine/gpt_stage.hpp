@@ -18,6 +18,8 @@
 
 namespace amdp {
 
+class KTimer;
+
 struct Dims {
   int L, h, heads, hd, ffn, V, S, B, T;  // T = B * S tokens per minibatch
   bool causal;
@@ -74,6 +76,11 @@ class GptStage {
   float* v = nullptr;
   float* grad = nullptr;    // fp32 window-accumulated gradient
   uint16_t* w = nullptr;    // bf16 working weights read by the kernels
+  KTimer* kt = nullptr;     // optional per-kernel-class timing
+  double attn_fwd_flops() const {  // algorithmic: QK^T + PV, causal half
+    const double f = 4.0 * d_.B * d_.heads * static_cast<double>(d_.S) * d_.S * d_.hd;
+    return d_.causal ? f / 2 : f;
+  }
 
   // Task bodies (stream-ordered).  `in`: stage input [T][h] (stages > 0); `out`: stage
   // output [T][h] (stages < depth-1).  Backward: `gin` incoming grad [T][h] (stages <

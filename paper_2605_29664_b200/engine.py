@@ -57,6 +57,17 @@ _sig("amdp_host_free", None, [c_void_p])
 _sig("amdp_synthetic_tokens", c_int, [POINTER(_Model), c_uint64, c_int, c_int, c_void_p, c_void_p])
 _sig("amdp_engine_run", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_char_p, c_size_t])
 _sig("amdp_engine_stats", c_int, [c_void_p, POINTER(_Stats)])
+_sig("amdp_engine_run_windows", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_char_p, c_size_t])
+_sig("amdp_engine_stage_tokens", c_int, [c_void_p, c_void_p, c_void_p])
+_sig("amdp_engine_set_kernel_timing", c_int, [c_void_p, c_int])
+
+
+class _KStat(Structure):
+    _fields_ = [("name", ctypes.c_char * 24), ("launches", c_int64), ("total_ms", c_double),
+                ("flops", c_double), ("bytes", c_double)]
+
+
+_sig("amdp_engine_kernel_stats", c_int, [c_void_p, POINTER(_KStat), c_int])
 _sig("amdp_engine_num_events", c_int, [c_void_p])
 _sig("amdp_engine_events", c_int, [c_void_p, POINTER(P._Event), c_int])
 _sig("amdp_engine_version_trace", c_size_t, [c_void_p, c_char_p, c_size_t])
@@ -234,6 +245,31 @@ class Engine:
         if rc != 0:
             raise RuntimeError("amdp_engine_run: " + err.value.decode())
         return losses
+
+    def run_windows(self, num_windows: int, inputs: np.ndarray, labels: np.ndarray,
+                    losses: Optional[np.ndarray] = None, resident: bool = False) -> np.ndarray:
+        """Windows [0, num_windows) of the schedule, pipeline starting empty (one bench 'run')."""
+        if losses is None:
+            losses = np.zeros(self.runcfg.num_minibatches, np.float32)
+        err = ctypes.create_string_buffer(4096)
+        rc = lib.amdp_engine_run_windows(self._h, num_windows, inputs.ctypes.data, labels.ctypes.data,
+                                         losses.ctypes.data, int(resident), err, len(err))
+        if rc != 0:
+            raise RuntimeError("amdp_engine_run_windows: " + err.value.decode())
+        return losses
+
+    def stage_tokens(self, inputs: np.ndarray, labels: np.ndarray) -> None:
+        N.check(lib.amdp_engine_stage_tokens(self._h, inputs.ctypes.data, labels.ctypes.data),
+                "amdp_engine_stage_tokens")
+
+    def set_kernel_timing(self, on: bool) -> None:
+        lib.amdp_engine_set_kernel_timing(self._h, int(on))
+
+    def kernel_stats(self) -> dict:
+        arr = (_KStat * 16)()
+        n = lib.amdp_engine_kernel_stats(self._h, arr, 16)
+        return {a.name.decode(): dict(launches=a.launches, ms=a.total_ms, flops=a.flops, bytes=a.bytes)
+                for a in arr[:n]}
 
     def stats(self) -> dict:
         s = _Stats()
