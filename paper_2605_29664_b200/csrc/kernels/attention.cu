@@ -525,6 +525,11 @@ int launch_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* 
 }  // namespace
 }  // namespace amdp
 
+namespace amdp {
+int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int D, int causal,
+                     cudaStream_t st);
+}
+
 using namespace amdp;
 
 extern "C" int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse, int batch,
@@ -534,6 +539,8 @@ extern "C" int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse
   auto q = reinterpret_cast<const bf16*>(qkv);
   auto o = reinterpret_cast<bf16*>(out);
   auto s = reinterpret_cast<cudaStream_t>(stream);
+  if ((head_dim == 64 || head_dim == 128) && seq % 128 == 0)  // tcgen05 path
+    return attention_fwd_tc(q, o, lse, batch, seq, heads, head_dim, causal, s);
   switch (head_dim) {
     case 32: return launch_fwd<32>(q, o, lse, batch, seq, heads, causal, s);
     case 64: return launch_fwd<64>(q, o, lse, batch, seq, heads, causal, s);
