@@ -528,6 +528,8 @@ int launch_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* 
 namespace amdp {
 int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int D, int causal,
                      cudaStream_t st);
+int attention_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
+                     int S, int H, int D, int causal, cudaStream_t st);
 }
 
 using namespace amdp;
@@ -566,6 +568,11 @@ extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, cons
   auto dq = reinterpret_cast<bf16*>(dqkv);
   auto w = static_cast<float*>(workspace);
   auto s = reinterpret_cast<cudaStream_t>(stream);
+  if ((head_dim == 64 || head_dim == 128) && seq % 128 == 0) {  // tcgen05 path
+    const int ntok = batch * seq;
+    attn_bwd_delta_kernel<<<(ntok * heads + 7) / 8, 256, 0, s>>>(o, d, w, ntok, seq, heads, head_dim);
+    return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, s);
+  }
   switch (head_dim) {
     case 32: return launch_bwd<32>(q, o, d, lse, dq, w, batch, seq, heads, causal, s);
     case 64: return launch_bwd<64>(q, o, d, lse, dq, w, batch, seq, heads, causal, s);

@@ -69,43 +69,34 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
 }
 
 // ---------------------------------------------------------------- LayerNorm backward
-// Each CTA handles a strided set of rows; per-column dgamma/dbeta partials are kept in
-// registers per lane, reduced across the CTA's warps in shared memory and written to
-// workspace[block][2*cols]; a second kernel folds the partials into dgamma/dbeta.
-__global__ void __launch_bounds__(256) layernorm_bwd_kernel(
+// Two fully parallel kernels (no serial fold):
+//  dx  : one warp per row: s1 = mean(dy*g), s2 = mean(dy*g*xhat), then
+//        dx = resid + rstd * (dy*g - s1 - xhat*s2)   (second pass re-reads the row from L1)
+//  dg/db: a CTA owns 256 columns x 64 rows; each lane accumulates 8 columns over its
+//        warp's rows, the 8 warps combine in smem and add into the fp32 gradient buffer.
+__global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
     const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ gamma,
-    const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-    const bf16* resid_grad, bf16* dx, float* __restrict__ partial, int rows, int cols) {
-  extern __shared__ float red[];  // [warps][2*cols]: per-warp dgamma | dbeta partials
+    const float* __restrict__ mean_in, const float* __restrict__ rstd_in, const bf16* resid_grad,
+    bf16* dx, int rows, int cols) {
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   const int warps = blockDim.x >> 5;
-  float* mine = red + static_cast<size_t>(warp) * 2 * cols;
-  for (int c = lane; c < 2 * cols; c += 32) mine[c] = 0.f;
-  __syncwarp();
-
-  for (int row = blockIdx.x * warps + warp; row < rows; row += gridDim.x * warps) {
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const size_t off = static_cast<size_t>(row) * cols;
     const float mean = mean_in[row], rstd = rstd_in[row];
     float s1 = 0.f, s2 = 0.f;
-    // pass 1: row statistics of dxhat = dy*gamma, column partials into smem
     for (int c = lane * 8; c < cols; c += 256) {
       float xv[8], dv[8];
       load8(x + off + c, xv);
       load8(dy + off + c, dv);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float xh = (xv[e] - mean) * rstd;
         const float dxh = dv[e] * gamma[c + e];
         s1 += dxh;
-        s2 += dxh * xh;
-        mine[c + e] += dv[e] * xh;
-        mine[cols + c + e] += dv[e];
+        s2 += dxh * (xv[e] - mean) * rstd;
       }
     }
     s1 = warp_sum(s1) / cols;
     s2 = warp_sum(s2) / cols;
-    // pass 2: dx (row re-read hits L1)
     for (int c = lane * 8; c < cols; c += 256) {
       float xv[8], dv[8], o[8];
       float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -115,34 +106,50 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const float xh = (xv[e] - mean) * rstd;
-        const float dxh = dv[e] * gamma[c + e];
-        o[e] = r[e] + rstd * (dxh - s1 - xh * s2);
+        o[e] = r[e] + rstd * (dv[e] * gamma[c + e] - s1 - xh * s2);
       }
       store8(dx + off + c, o);
     }
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
-    float s = 0.f;
-    for (int w = 0; w < warps; ++w) s += red[static_cast<size_t>(w) * 2 * cols + c];
-    partial[static_cast<size_t>(blockIdx.x) * 2 * cols + c] = s;
+}
+
+constexpr int LN_DG_ROWS = 64;
+__global__ void __launch_bounds__(256) layernorm_bwd_dgb_kernel(
+    const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean_in,
+    const float* __restrict__ rstd_in, float* dgamma, float* dbeta, int rows, int cols) {
+  __shared__ float red[8][2][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 256 + lane * 8;
+  const int r0 = blockIdx.y * LN_DG_ROWS;
+  float g[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (c < cols) {
+    for (int row = r0 + warp; row < min(rows, r0 + LN_DG_ROWS); row += 8) {
+      const size_t off = static_cast<size_t>(row) * cols + c;
+      const float mean = mean_in[row], rstd = rstd_in[row];
+      float xv[8], dv[8];
+      load8(x + off, xv);
+      load8(dy + off, dv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        g[e] += dv[e] * (xv[e] - mean) * rstd;
+        bb[e] += dv[e];
+      }
+    }
   }
-}
-
-__global__ void layernorm_bwd_fold(const float* __restrict__ partial, int nblocks, int cols,
-                                   float* dgamma, float* dbeta) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * cols) return;
-  float s = 0.f;
-  for (int b = 0; b < nblocks; ++b) s += partial[static_cast<size_t>(b) * 2 * cols + c];
-  if (c < cols) dgamma[c] += s;
-  else dbeta[c - cols] += s;
-}
-
-int ln_bwd_blocks(int rows) {
-  const int want = (rows + 7) / 8;  // 8 warps per CTA, >= 1 row per warp
-  const int cap = 2 * num_sms();
-  return want < cap ? want : cap;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    red[warp][0][lane * 8 + e] = g[e];
+    red[warp][1][lane * 8 + e] = bb[e];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 512; i += 256) {
+    const int which = i >> 8, col = i & 255;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][which][col];
+    const int gc = blockIdx.x * 256 + col;
+    if (gc < cols) atomicAdd((which ? dbeta : dgamma) + gc, s);
+  }
 }
 
 // ---------------------------------------------------------------- embedding
@@ -288,7 +295,9 @@ extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const f
 }
 
 extern "C" size_t amdp_layernorm_bwd_workspace(int rows, int cols) {
-  return static_cast<size_t>(ln_bwd_blocks(rows)) * 2 * cols * sizeof(float);
+  (void)rows;
+  (void)cols;
+  return 16;  // no workspace needed any more; kept for ABI stability
 }
 
 extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const float* gamma,
@@ -296,23 +305,18 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
                                   const uint16_t* resid_grad, uint16_t* dx, float* dgamma,
                                   float* dbeta, void* workspace, int rows, int cols,
                                   amdp_stream_t stream) {
-  if (rows <= 0 || cols <= 0 || cols % 8 != 0 || cols > LN_MAX_VEC * 256 || !workspace)
-    return AMDP_ERR_INVALID;
+  (void)workspace;
+  if (rows <= 0 || cols <= 0 || cols % 8 != 0) return AMDP_ERR_INVALID;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int blocks = ln_bwd_blocks(rows);
-  const size_t smem = static_cast<size_t>(8) * 2 * cols * sizeof(float);
-  static int smem_attr = 0;
-  if (smem > 48 * 1024 && static_cast<int>(smem) > smem_attr) {
-    cudaFuncSetAttribute(layernorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    smem_attr = static_cast<int>(smem);
-  }
-  layernorm_bwd_kernel<<<blocks, 256, smem, s>>>(
+  int blocks = (rows + 7) / 8;
+  if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
+  layernorm_bwd_dx_kernel<<<blocks, 256, 0, s>>>(
       reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(x), gamma, mean, rstd,
-      reinterpret_cast<const bf16*>(resid_grad), reinterpret_cast<bf16*>(dx),
-      static_cast<float*>(workspace), rows, cols);
-  layernorm_bwd_fold<<<(2 * cols + 255) / 256, 256, 0, s>>>(static_cast<float*>(workspace),
-                                                           blocks, cols, dgamma, dbeta);
+      reinterpret_cast<const bf16*>(resid_grad), reinterpret_cast<bf16*>(dx), rows, cols);
+  dim3 g((cols + 255) / 256, (rows + LN_DG_ROWS - 1) / LN_DG_ROWS);
+  layernorm_bwd_dgb_kernel<<<g, 256, 0, s>>>(reinterpret_cast<const bf16*>(dy),
+                                             reinterpret_cast<const bf16*>(x), mean, rstd, dgamma,
+                                             dbeta, rows, cols);
   return cudaGetLastError();
 }
 
