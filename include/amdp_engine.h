@@ -51,6 +51,8 @@ typedef struct amdp_run_config {
   int world_size, rank;        /* GPUs in the job and this process's rank        */
   int record_events;           /* 1 = per-task CUDA events (measured Timeline)   */
   uint64_t data_seed;
+  int plan_only;               /* 1 = plan (hosting/slots/comm program) without  */
+                               /*     touching CUDA or NCCL; see plan_json       */
 } amdp_run_config;
 
 typedef struct amdp_engine amdp_engine;

@@ -1,0 +1,43 @@
+// ppsim::execute — the GPU counterpart of ppsim::simulate (engine.hpp:28).
+//
+//   auto g  = ppsim::build(cfg, declared);          // unchanged reference API
+//   auto tl = ppsim::simulate(g, declared);         // declared-cost order (the trace)
+//   auto run = ppsim::execute(cfg, declared, opts, inputs, labels);  // same order on B200s
+//   ppsim::bubble_ratio(run.timeline, 1);           // analyses apply unchanged
+//
+// execute() builds the same TaskGraph from (cfg, declared), replays its simulate() dispatch
+// order on this process's GPU (logical devices folded world_size ways), and returns the
+// measured Timeline (integer nanoseconds as Rat) plus the per-minibatch losses.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "amdp_engine.h"
+#include "ppsim/ppsim.hpp"
+
+namespace ppsim {
+
+struct ExecuteOptions {
+  amdp_model_config model{};
+  amdp_opt_args optimizer{AMDP_OPT_ADAMW, 3e-4f, 0.9f, 0.95f, 1e-8f, 0.f, 1e-8f, 1e6f, 1.f, 1};
+  int world_size = 1;
+  int rank = 0;
+  const uint8_t* nccl_id = nullptr;  // amdp_nccl_unique_id() from rank 0 when world_size > 1
+  uint64_t data_seed = 1234;
+};
+
+struct ExecuteResult {
+  Timeline timeline;          // measured, this rank's logical devices
+  std::vector<float> losses;  // per minibatch (valid on the rank hosting the last stage)
+  amdp_run_stats stats{};
+};
+
+// Throws std::invalid_argument for configurations the executor does not run (non-AMDP
+// policy, ZeRO disabled, depth not divisible by world_size) and std::runtime_error for
+// CUDA/NCCL failures.  inputs/labels: host [num_minibatches][tokens_per_minibatch].
+PPSIM_API ExecuteResult execute(const PolicyConfig& cfg, const ClusterSpec& declared,
+                                const ExecuteOptions& opt, const int32_t* inputs,
+                                const int32_t* labels);
+
+}  // namespace ppsim

@@ -167,6 +167,7 @@ class Engine {
   cudaEvent_t run_begin_ = nullptr, run_end_ = nullptr;
   std::vector<cudaEvent_t> stage_ready_;      // weights of stage i usable (after bcast)
   size_t slot_total_ = 0;
+  bool plan_only_ = false;
 
   int rank_of_dev(int dev) const { return dev / per_rank_; }
   int owner_rank(int stage) const { return rank_of_dev(stage); }
@@ -250,6 +251,12 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     owned[static_cast<size_t>(i)] = owner_rank(i) == rank_;
   }
 
+  if (rc.plan_only) {  // host-side planning only (multi-rank consistency tests on CPU)
+    group_comm_.assign(static_cast<size_t>(depth_), nullptr);
+    make_plan();
+    plan_only_ = true;
+    return;
+  }
   CUDA_OK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
   if (world_ > 1) {
@@ -275,6 +282,7 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
 }
 
 Engine::~Engine() {
+  if (plan_only_) return;
   cudaStreamSynchronize(cs_);
   cudaStreamSynchronize(ms_);
   for (auto& s : stages) {
@@ -1031,3 +1039,48 @@ size_t amdp_engine_plan_json(const amdp_engine* e, char* buf, size_t len) {
 }
 
 }  // extern "C"
+
+// ====================================================================== C++ API
+#include "ppsim/execute.hpp"
+
+namespace ppsim {
+
+ExecuteResult execute(const PolicyConfig& cfg, const ClusterSpec& declared, const ExecuteOptions& opt,
+                      const int32_t* inputs, const int32_t* labels) {
+  if (cfg.policy != Policy::AMDP) throw std::invalid_argument("execute: only the AMDP policy runs on GPUs");
+  if (declared.fwd_cost.empty() || declared.bwd_cost.empty())
+    throw std::invalid_argument("execute: declared cluster needs per-stage costs");
+  for (std::size_t i = 1; i < declared.fwd_cost.size(); ++i)
+    if (declared.fwd_cost[i] != declared.fwd_cost[0] || declared.bwd_cost[i] != declared.bwd_cost[0])
+      throw std::invalid_argument("execute: the executor replays uniform declared costs");
+  if (declared.comm_cost != Rat(0) || declared.update_cost != Rat(0))
+    throw std::invalid_argument("execute: declared comm/update costs must be 0 (they change the order)");
+  amdp_run_config rc{};
+  rc.policy = amdp_policy_config{static_cast<int>(cfg.policy), cfg.injection_limit, cfg.num_pipelines,
+                                 cfg.accumulation_threshold, cfg.num_minibatches, cfg.zero_enabled ? 1 : 0,
+                                 cfg.injection_override ? 1 : 0};
+  rc.declared_fwd = amdp_rat{declared.fwd_cost[0].num(), declared.fwd_cost[0].den()};
+  rc.declared_bwd = amdp_rat{declared.bwd_cost[0].num(), declared.bwd_cost[0].den()};
+  rc.optimizer = opt.optimizer;
+  rc.world_size = opt.world_size;
+  rc.rank = opt.rank;
+  rc.record_events = 1;
+  rc.data_seed = opt.data_seed;
+  amdp::Engine eng(opt.model, rc, opt.nccl_id);
+  ExecuteResult out;
+  out.losses.assign(static_cast<std::size_t>(cfg.num_minibatches), 0.f);
+  eng.run(inputs, labels, out.losses.data());
+  out.stats = eng.stats;
+  out.timeline.policy = Policy::AMDP;
+  out.timeline.depth = declared.depth;
+  out.timeline.devices = declared.devices;
+  out.timeline.threshold = cfg.accumulation_threshold;
+  out.timeline.per_device.assign(static_cast<std::size_t>(declared.devices), {});
+  for (const auto& e : eng.events) {
+    out.timeline.makespan = max(out.timeline.makespan, e.finish());
+    out.timeline.per_device[static_cast<std::size_t>(e.device)].push_back(e);
+  }
+  return out;
+}
+
+}  // namespace ppsim

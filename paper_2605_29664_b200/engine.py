@@ -35,7 +35,7 @@ class _Model(Structure):
 class _Run(Structure):
     _fields_ = [("policy", P._Policy), ("declared_fwd", P._Rat), ("declared_bwd", P._Rat),
                 ("optimizer", N.OptArgs), ("world_size", c_int), ("rank", c_int),
-                ("record_events", c_int), ("data_seed", c_uint64)]
+                ("record_events", c_int), ("data_seed", c_uint64), ("plan_only", c_int)]
 
 
 class _Stats(Structure):
@@ -162,6 +162,7 @@ class RunConfig:
     rank: int = 0
     record_events: bool = True
     data_seed: int = 1234
+    plan_only: bool = False   # host-side plan without CUDA/NCCL (multi-rank tests on CPU)
 
     @property
     def num_minibatches(self) -> int:
@@ -177,7 +178,7 @@ class RunConfig:
     def _c(self):
         return _Run(self.policy()._c(), P._r(self.declared_fwd), P._r(self.declared_bwd),
                     self.optimizer._c(), self.world_size, self.rank, int(self.record_events),
-                    self.data_seed)
+                    self.data_seed, int(self.plan_only))
 
 
 def nccl_unique_id() -> bytes:
