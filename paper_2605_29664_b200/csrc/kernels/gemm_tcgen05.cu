@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "amdp_kernels.h"
 #include "sm100_ptx.cuh"
@@ -314,6 +315,169 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair kernel
+// cta_group::2 variant: a cluster of two CTAs computes a 256 x BNP tile with one
+// tcgen05.mma (M=256) per K=16 step, issued by the even CTA.  CTA r loads A rows
+// [m0 + 128 r, +128) and B rows [n0 + r BNP/2, +BNP/2) into its own smem; both CTAs' TMA
+// bytes land on the even CTA's `full` barrier; each CTA's TMEM holds its 128 rows x BNP
+// columns.  Per SM the tensor core reads 4 KiB of A and BNP/8 KiB of B per instruction,
+// and a 256 x 128 pair tile keeps the N=2048 stage GEMMs at ~7 waves on 148 SMs.
+constexpr int PAIR_THREADS = 256;
+
+template <int BNP>
+struct PairCfg {
+  static constexpr int B_HALF = BNP / 2;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = B_HALF * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int NSTAGE = BNP == 256 ? 4 : 6;
+  static constexpr size_t SMEM = 1024 + NSTAGE * STAGE + 256;
+  static constexpr uint32_t TMEM = 2 * BNP <= 256 ? 256 : 512;
+};
+
+template <bool A_MN, bool B_MN, int EPI, int BNP>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
+    gemm_bf16_tc_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                      const EpiParams p) {
+  using C = PairCfg<BNP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + C::NSTAGE * C::A_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::NSTAGE * C::STAGE);
+  uint64_t* empty_bar = full_bar + C::NSTAGE;
+  uint64_t* tfull_bar = empty_bar + C::NSTAGE;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_rank();
+  const int tiles_m = (p.M + 255) / 256;
+  const int tiles_n = (p.N + BNP - 1) / BNP;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = p.K / BK;
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&map_a);
+    ptx::tma_prefetch(&map_b);
+    for (int s = 0; s < C::NSTAGE; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], 2 * 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc_pair<C::TMEM>(tmem_slot);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        int tm, tn;
+        tile_coords(t, tiles_m, tiles_n, tm, tn);
+        const int ma = tm * 256 + 128 * static_cast<int>(rank);
+        const int nb = tn * BNP + C::B_HALF * static_cast<int>(rank);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE);
+          uint8_t* sa = smem_a + stage * C::A_BYTES;
+          uint8_t* sb = smem_b + stage * C::B_BYTES;
+          const int k0 = kb * BK;
+          if constexpr (A_MN) {
+            ptx::tma_load_2d_pair(sa, &map_a, fb, ma, k0);
+            ptx::tma_load_2d_pair(sa + 64 * BK * 2, &map_a, fb, ma + 64, k0);
+          } else {
+            ptx::tma_load_2d_pair(sa, &map_a, fb, k0, ma);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int i = 0; i < C::B_HALF / 64; ++i)
+              ptx::tma_load_2d_pair(sb + i * 64 * BK * 2, &map_b, fb, nb + 64 * i, k0);
+          } else {
+            ptx::tma_load_2d_pair(sb, &map_b, fb, k0, nb);
+          }
+          if (++stage == C::NSTAGE) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BNP, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BNP;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * C::A_BYTES);
+          const uint32_t b_addr = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t a_desc = A_MN ? ptx::umma_desc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024)
+                                         : ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t b_desc = B_MN ? ptx::umma_desc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024)
+                                         : ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma_bf16_ss_pair(d_tmem, a_desc, b_desc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit_pair(&empty_bar[stage], 0x3);
+          if (++stage == C::NSTAGE) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit_pair(&tfull_bar[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty_bar[0]), 0);
+    const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty_bar[1]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters) {
+      int tm, tn;
+      tile_coords(t, tiles_m, tiles_n, tm, tn);
+      const int row = tm * 256 + 128 * static_cast<int>(rank) + q * 32 + lane;
+      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BNP;
+      const int n_valid = min(BNP, p.N - tn * BNP);
+#pragma unroll 1
+      for (int c = 0; c < BNP / 32; ++c) {
+        if (c * 32 >= n_valid) break;  // warp-uniform
+        uint32_t raw[32];
+        ptx::tmem_ld_32x32b_x32(t_row + c * 32, raw);
+        ptx::tmem_ld_wait();
+        epilogue_chunk<EPI>(p, row, tn * BNP + c * 32, raw);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_pair<C::TMEM>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -347,34 +511,73 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
 
 int g_num_sms = 0;
 
-template <bool A_MN, bool B_MN, int EPI>
+// MODE 0: single-CTA 128x256 tiles; MODE 128 / 256: CTA-pair 256 x MODE tiles.
+template <bool A_MN, bool B_MN, int EPI, int MODE>
 int launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p, cudaStream_t s) {
-  auto kern = gemm_bf16_tcgen05<A_MN, B_MN, EPI>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(SMEM_BYTES));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+  if constexpr (MODE == 0) {
+    auto kern = gemm_bf16_tcgen05<A_MN, B_MN, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(SMEM_BYTES));
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+    const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+    kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  } else {
+    auto kern = gemm_bf16_tc_pair<A_MN, B_MN, EPI, MODE>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(PairCfg<MODE>::SMEM));
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    const int tiles = ((p.M + 255) / 256) * ((p.N + MODE - 1) / MODE);
+    const int pairs = g_num_sms / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    kern<<<grid, PAIR_THREADS, PairCfg<MODE>::SMEM, s>>>(ma, mb, p);
   }
-  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
   return cudaGetLastError();
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int MODE>
 int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p,
                  cudaStream_t s) {
   switch (epi) {
-    case AMDP_EPI_STORE_BF16: return launch<A_MN, B_MN, AMDP_EPI_STORE_BF16>(ma, mb, p, s);
-    case AMDP_EPI_GELU: return launch<A_MN, B_MN, AMDP_EPI_GELU>(ma, mb, p, s);
-    case AMDP_EPI_RESIDUAL: return launch<A_MN, B_MN, AMDP_EPI_RESIDUAL>(ma, mb, p, s);
-    case AMDP_EPI_ACCUM_F32: return launch<A_MN, B_MN, AMDP_EPI_ACCUM_F32>(ma, mb, p, s);
-    case AMDP_EPI_GELU_BWD: return launch<A_MN, B_MN, AMDP_EPI_GELU_BWD>(ma, mb, p, s);
-    case AMDP_EPI_STORE_F32: return launch<A_MN, B_MN, AMDP_EPI_STORE_F32>(ma, mb, p, s);
+    case AMDP_EPI_STORE_BF16: return launch<A_MN, B_MN, AMDP_EPI_STORE_BF16, MODE>(ma, mb, p, s);
+    case AMDP_EPI_GELU: return launch<A_MN, B_MN, AMDP_EPI_GELU, MODE>(ma, mb, p, s);
+    case AMDP_EPI_RESIDUAL: return launch<A_MN, B_MN, AMDP_EPI_RESIDUAL, MODE>(ma, mb, p, s);
+    case AMDP_EPI_ACCUM_F32: return launch<A_MN, B_MN, AMDP_EPI_ACCUM_F32, MODE>(ma, mb, p, s);
+    case AMDP_EPI_GELU_BWD: return launch<A_MN, B_MN, AMDP_EPI_GELU_BWD, MODE>(ma, mb, p, s);
+    case AMDP_EPI_STORE_F32: return launch<A_MN, B_MN, AMDP_EPI_STORE_F32, MODE>(ma, mb, p, s);
   }
   return AMDP_ERR_INVALID;
+}
+
+template <bool A_MN, bool B_MN>
+int dispatch_mode(int mode, int epi, const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p,
+                  cudaStream_t s) {
+  if (mode == 128) return dispatch_epi<A_MN, B_MN, 128>(epi, ma, mb, p, s);
+  if (mode == 256) return dispatch_epi<A_MN, B_MN, 256>(epi, ma, mb, p, s);
+  return dispatch_epi<A_MN, B_MN, 0>(epi, ma, mb, p, s);
+}
+
+// Tile shape per problem: CTA pairs with 256 x 256 tiles whenever M >= 256.  Measured at
+// the 1.3B shapes (profiles/r01_gemm_modes.txt) the pair-256 kernel matches or beats the
+// single-CTA 128x256 kernel everywhere (+5-13% on QKV / fc1 / head / 8192^3); the
+// pair-128 width loses 20-35% and is only reachable through AMDP_GEMM_MODE=128.
+int choose_mode(int M, int N) {
+  (void)N;
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("AMDP_GEMM_MODE");
+    forced = e ? atoi(e) : -1;
+  }
+  if (forced == 0 || forced == 128 || forced == 256) return forced;
+  return M >= 256 ? 256 : 0;
 }
 
 }  // namespace
@@ -394,25 +597,26 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) return AMDP_ERR_CUDA;
   }
+  const int mode = choose_mode(a->M, a->N);
   CUtensorMap ma, mb;
   bool ok;
   if (a->a_mn_major)  // A stored [K][lda], M contiguous
     ok = make_map(&ma, a->A, a->M, a->K, a->lda, BK);
-  else  // A stored [M][lda], K contiguous
+  else  // A stored [M][lda], K contiguous (128 rows per CTA in both kernels)
     ok = make_map(&ma, a->A, a->K, a->M, a->lda, BM);
   if (!ok) return AMDP_ERR_TMA;
   if (a->b_mn_major)
     ok = make_map(&mb, a->B, a->N, a->K, a->ldb, BK);
-  else
-    ok = make_map(&mb, a->B, a->K, a->N, a->ldb, BN);
+  else  // B rows per CTA: 256 (single) or mode / 2 (pair)
+    ok = make_map(&mb, a->B, a->K, a->N, a->ldb, mode == 0 ? BN : mode / 2);
   if (!ok) return AMDP_ERR_TMA;
   EpiParams p{a->M, a->N, a->K, a->C, a->ldc,
               static_cast<const __nv_bfloat16*>(a->aux), a->ld_aux,
               static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int am = a->a_mn_major ? 1 : 0, bm = a->b_mn_major ? 1 : 0;
-  if (!am && !bm) return dispatch_epi<false, false>(a->epilogue, ma, mb, p, s);
-  if (!am && bm) return dispatch_epi<false, true>(a->epilogue, ma, mb, p, s);
-  if (am && !bm) return dispatch_epi<true, false>(a->epilogue, ma, mb, p, s);
-  return dispatch_epi<true, true>(a->epilogue, ma, mb, p, s);
+  if (!am && !bm) return dispatch_mode<false, false>(mode, a->epilogue, ma, mb, p, s);
+  if (!am && bm) return dispatch_mode<false, true>(mode, a->epilogue, ma, mb, p, s);
+  if (am && !bm) return dispatch_mode<true, false>(mode, a->epilogue, ma, mb, p, s);
+  return dispatch_mode<true, true>(mode, a->epilogue, ma, mb, p, s);
 }
