@@ -140,6 +140,11 @@ int amdp_fill_normal_bf16_f32(uint16_t* w_bf16, float* w_f32, int64_t n, uint64_
                               float stddev, amdp_stream_t stream);
 int amdp_fill_const_f32(float* x, int64_t n, float value, amdp_stream_t stream);
 
+/* Diagnostics: CTA 0 of the tensor-core attention forward records clock64() at each
+ * pipeline hand-off into device_buf (>= 11*64 int64; NULL disables). */
+int amdp_debug_attention_trace(long long* device_buf);
+int amdp_debug_attention_bwd_trace(long long* device_buf); /* CTA 0 of the dQ kernel */
+
 /* Library identification (for the loader's sanity check). */
 const char* amdp_version(void);
 

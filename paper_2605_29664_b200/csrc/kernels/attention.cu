@@ -244,6 +244,29 @@ __global__ void attn_bwd_delta_kernel(const bf16* __restrict__ out, const bf16* 
   }
 }
 
+// Vectorised variant for D in {32, 64, 128}: one thread per 8-element chunk, D/8 lanes per
+// (token, head) reduce with shuffles (groups never straddle a warp).
+__global__ void attn_bwd_delta_vec_kernel(const bf16* __restrict__ out, const bf16* __restrict__ dout,
+                                          float* __restrict__ delta, int ntok, int seq, int H, int D) {
+  const int G = D / 8;
+  const int64_t chunks = static_cast<int64_t>(ntok) * H * G;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < chunks;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float o[8], d[8];
+    load8(out + i * 8, o);
+    load8(dout + i * 8, d);
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += o[e] * d[e];
+    for (int m = G >> 1; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+    if (i % G == 0) {
+      const int64_t th = i / G;  // token * H + head
+      const int tok = static_cast<int>(th / H), h = static_cast<int>(th % H);
+      delta[(static_cast<size_t>(tok / seq) * H + h) * seq + tok % seq] = s;
+    }
+  }
+}
+
 // ================================================================== backward dQ
 template <int D>
 __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
@@ -570,7 +593,10 @@ extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, cons
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if ((head_dim == 64 || head_dim == 128) && seq % 128 == 0) {  // tcgen05 path
     const int ntok = batch * seq;
-    attn_bwd_delta_kernel<<<(ntok * heads + 7) / 8, 256, 0, s>>>(o, d, w, ntok, seq, heads, head_dim);
+    const int64_t chunks = static_cast<int64_t>(ntok) * heads * (head_dim / 8);
+    int64_t blocks = (chunks + 255) / 256;
+    if (blocks > 16 * num_sms()) blocks = 16 * num_sms();  // grid-stride; multiple of 256 threads
+    attn_bwd_delta_vec_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(o, d, w, ntok, seq, heads, head_dim);
     return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, s);
   }
   switch (head_dim) {

@@ -20,6 +20,13 @@ namespace amdp {
 namespace {
 
 constexpr uint32_t T128 = 16384;  // [128 rows][64 bf16] SW128 tile
+
+// Diagnostics (amdp_debug_attention_bwd_trace): CTA 0 of the dQ kernel records clock64().
+__device__ long long* g_bw_dbg = nullptr;
+#define BW_T(slot, j)                                                                       \
+  do {                                                                                      \
+    if (g_bw_dbg != nullptr && blockIdx.x == 0 && (j) < 64) g_bw_dbg[(slot)*64 + (j)] = clock64(); \
+  } while (0)
 constexpr uint32_t T64 = 8192;    // [64 rows][64 bf16]
 
 __device__ __forceinline__ float ex2(float x) {
@@ -261,16 +268,20 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ==================================================================== dQ
+// dS never touches shared memory: the softmax threads write it (bf16) over the TMEM
+// columns of the S tile they just read, and dQ += dS K_j reads it as the TMEM A operand
+// (tcgen05 "TS" form).  Three S/dP TMEM buffers let S_{n+1} issue while dQ_{n-1} is still
+// reading buffer n-1; the freed smem goes into a 5-deep K/V TMA ring (TMA latency on this
+// path is ~3-5k cycles, profiles/r01_attn_fwd_trace.txt).
 template <int D>
 struct QSmem {
   static constexpr int NB = D / 64;
+  static constexpr int NS = D == 128 ? 5 : 8;     // K / V ring depth
   static constexpr uint32_t Q = 0;
   static constexpr uint32_t DO = Q + NB * T128;
-  static constexpr int NS = 4;                    // K / V ring depth
   static constexpr uint32_t K = DO + NB * T128;   // NS stages of NB x T64
   static constexpr uint32_t V = K + NS * NB * T64;
-  static constexpr uint32_t DS = V + NS * NB * T64;  // 2 warpgroups x [128 q][64 keys]
-  static constexpr uint32_t BAR = DS + 2 * T128;
+  static constexpr uint32_t BAR = V + NS * NB * T64;
   static constexpr uint32_t BYTES = BAR + 256;
   static constexpr uint32_t TMEM_COLS = 512;
 };
@@ -282,19 +293,19 @@ __global__ void __launch_bounds__(384, 1)
                      const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int H, int n_qt,
                      float scale_log2, float scale, int causal) {
   using L = QSmem<D>;
+  constexpr int NS = L::NS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  constexpr int NS = L::NS;
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [NS]
-  uint64_t* kv_empty = bar + 5;  // [NS]
-  uint64_t* s_full = bar + 9;    // [2] per warpgroup
-  uint64_t* s_empty = bar + 11;  // [2]
-  uint64_t* p_full = bar + 13;   // [2]
-  uint64_t* pd_done = bar + 15;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  uint64_t* kv_full = bar + 1;        // [NS]
+  uint64_t* kv_empty = kv_full + 8;   // [NS]
+  uint64_t* s_full = kv_empty + 8;    // [3] TMEM S/dP buffers
+  uint64_t* s_empty = s_full + 3;     // [3]
+  uint64_t* p_full = s_empty + 3;     // [2] per warpgroup: dS written
+  uint64_t* dq_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qt = n_qt - 1 - static_cast<int>(blockIdx.x % n_qt);  // heavy first
@@ -312,12 +323,13 @@ __global__ void __launch_bounds__(384, 1)
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 3; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_empty[s], 128);
-      ptx::mbar_init(&p_full[s], 128);
-      ptx::mbar_init(&pd_done[s], 1);
+      ptx::mbar_init(&s_empty[s], 1);
     }
+    ptx::mbar_init(&p_full[0], 128);
+    ptx::mbar_init(&p_full[1], 128);
+    ptx::mbar_init(dq_done, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc<L::TMEM_COLS>(tmem_slot);
@@ -325,8 +337,10 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S_w at 128w, dP_w at 128w + 64, dQ at 256
-  const uint32_t t_dq = tmem + 256;
+  // TMEM: buffer b: S at 128b (dS bf16 overwrites its first 32 columns), dP at 128b + 64;
+  // dQ at 384.
+  const uint32_t t_dq = tmem + 384;
+  if (threadIdx.x == 0) BW_T(7, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -338,6 +352,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int n = 0; n < N; ++n) {
         const int st = n % NS;
         ptx::mbar_wait(&kv_empty[st], ((n / NS) & 1) ^ 1);
+        BW_T(6, n);
         ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * L::NB * T64);
         for (int c = 0; c < L::NB; ++c) {
           ptx::tma_load_2d(sm + L::K + (st * L::NB + c) * T64, &qkv64, &kv_full[st], H * D + h * D + 64 * c,
@@ -355,10 +370,12 @@ __global__ void __launch_bounds__(384, 1)
       ptx::mbar_wait(q_full, 0);
       for (int n = 0; n <= N; ++n) {
         if (n < N) {
-          const int st = n % NS, w = n & 1;
-          const uint32_t t_s = tmem + 128 * w, t_dp = t_s + 64;
+          const int st = n % NS, bf = n % 3;
+          const uint32_t t_s = tmem + 128 * bf, t_dp = t_s + 64;
           ptx::mbar_wait(&kv_full[st], (n / NS) & 1);
-          ptx::mbar_wait(&s_empty[w], ((n >> 1) & 1) ^ 1);
+          BW_T(0, n);
+          ptx::mbar_wait(&s_empty[bf], ((n / 3) & 1) ^ 1);
+          BW_T(1, n);
           ptx::tc_fence_after();
           const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * T64);
           const uint32_t sv = ptx::smem_u32(sm + L::V + st * L::NB * T64);
@@ -370,22 +387,23 @@ __global__ void __launch_bounds__(384, 1)
             ptx::mma_bf16_ss(t_dp, ptx::umma_desc_sw128(sdo + oa, 16, 1024),
                              ptx::umma_desc_sw128(sv + ob, 16, 1024), id_s, kk > 0);
           }
-          ptx::mma_commit(&s_full[w]);
+          ptx::mma_commit(&s_full[bf]);
         }
         if (n > 0) {
-          const int m = n - 1, st = m % NS, w = m & 1;
-          ptx::mbar_wait(&p_full[w], (m >> 1) & 1);
+          const int m = n - 1, st = m % NS, bf = m % 3;
+          ptx::mbar_wait(&p_full[m & 1], (m >> 1) & 1);
+          BW_T(2, m);
           ptx::tc_fence_after();
           const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * T64);
-          const uint32_t sds = ptx::smem_u32(sm + L::DS + w * T128);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // K = 64 keys
-            ptx::mma_bf16_ss(t_dq, ptx::umma_desc_sw128(sds + kk * 32, 16, 1024),
-                             ptx::umma_desc_sw128(sk + kk * 2048, T64, 1024), id_g, (m > 0 || kk > 0));
-          ptx::mma_commit(&pd_done[w]);
+          for (int kk = 0; kk < 4; ++kk)  // K = 64 keys, 16 per instruction (8 TMEM columns)
+            ptx::mma_bf16_ts(t_dq, tmem + 128 * bf + kk * 8, ptx::umma_desc_sw128(sk + kk * 2048, T64, 1024), id_g,
+                             (m > 0 || kk > 0));
+          ptx::mma_commit(&s_empty[bf]);
           ptx::mma_commit(&kv_empty[st]);
         }
       }
+      ptx::mma_commit(dq_done);
     }
   } else if (warp >= 4) {
     const int wg = (warp - 4) >> 2;
@@ -393,28 +411,28 @@ __global__ void __launch_bounds__(384, 1)
     const int r = q * 32 + lane;
     const int qrow = qt * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t t_s = tmem + 128 * wg, t_dp = t_s + 64;
     const size_t bh = (static_cast<size_t>(b) * H + h) * seq;
     const float nl = -lse[bh + qrow], dl = delta[bh + qrow];
     int it = 0;
     for (int n = wg; n < N; n += 2, ++it) {
+      const int bf = n % 3;
+      const uint32_t t_s = tmem + 128 * bf + lanes, t_dp = t_s + 64;
       const bool diag = causal && n >= 2 * qt;
-      ptx::mbar_wait(&s_full[wg], it & 1);
+      ptx::mbar_wait(&s_full[bf], (n / 3) & 1);
+      if (lane == 0 && q == 0) BW_T(3, n);
       ptx::tc_fence_after();
       uint32_t s0[32], s1[32], d0[32], d1[32];
-      ptx::tmem_ld_32x32b_x32(t_s + lanes, s0);
-      ptx::tmem_ld_32x32b_x32(t_s + lanes + 32, s1);
-      ptx::tmem_ld_32x32b_x32(t_dp + lanes, d0);
-      ptx::tmem_ld_32x32b_x32(t_dp + lanes + 32, d1);
+      ptx::tmem_ld_32x32b_x32(t_s, s0);
+      ptx::tmem_ld_32x32b_x32(t_s + 32, s1);
+      ptx::tmem_ld_32x32b_x32(t_dp, d0);
+      ptx::tmem_ld_32x32b_x32(t_dp + 32, d1);
       ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&s_empty[wg]);
       float g[64];
 #pragma unroll
       for (int cc = 0; cc < 64; ++cc) {
-        const float s = __uint_as_float(cc < 32 ? s0[cc] : s1[cc - 32]);
+        const float sv = __uint_as_float(cc < 32 ? s0[cc] : s1[cc - 32]);
         const float dp = __uint_as_float(cc < 32 ? d0[cc] : d1[cc - 32]);
-        g[cc] = ex2(fmaf(s, scale_log2, nl)) * (dp - dl);
+        g[cc] = ex2(fmaf(sv, scale_log2, nl)) * (dp - dl);
       }
       if (diag) {
 #pragma unroll
@@ -424,17 +442,14 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t gg[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) gg[c] = pack2(g[2 * c], g[2 * c + 1]);
-      if (it > 0) ptx::mbar_wait(&pd_done[wg], (it - 1) & 1);
-      uint8_t* sds = sm + L::DS + wg * T128;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        *reinterpret_cast<uint4*>(sds + ptx::sw128_offset(r, u)) =
-            make_uint4(gg[4 * u], gg[4 * u + 1], gg[4 * u + 2], gg[4 * u + 3]);
-      ptx::fence_proxy_async_smem();
+      if (lane == 0 && q == 0) BW_T(4, n);
+      ptx::tmem_st_32x32b_x32(t_s, gg);  // dS (bf16 pairs) over the S columns just read
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
       ptx::mbar_arrive(&p_full[wg]);
+      if (lane == 0 && q == 0) BW_T(5, n);
     }
-    if (it > 0) ptx::mbar_wait(&pd_done[wg], (it - 1) & 1);
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // both warpgroups drained: dQ final
+    ptx::mbar_wait(dq_done, 0);
     ptx::tc_fence_after();
     // each warpgroup writes half of the D columns
     bf16* rowq = dqkv + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(3) * H * D) + h * D;
@@ -505,3 +520,7 @@ int attention_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const 
 }
 
 }  // namespace amdp
+
+extern "C" int amdp_debug_attention_bwd_trace(long long* device_buf) {
+  return cudaMemcpyToSymbol(amdp::g_bw_dbg, &device_buf, sizeof(device_buf));
+}

@@ -25,6 +25,14 @@ namespace amdp {
 namespace {
 
 constexpr int FA_BQ = 128, FA_BKV = 128, FA_THREADS = 384;
+
+// Diagnostics: when set (amdp_debug_attention_trace), CTA 0 records clock64() at each
+// pipeline hand-off into this buffer (slot layout in scripts/attn_trace.py).
+__device__ long long* g_fa_dbg = nullptr;
+#define FA_T(slot, j)                                             \
+  do {                                                            \
+    if (g_fa_dbg != nullptr && blockIdx.x == 0) g_fa_dbg[(slot)*64 + (j)] = clock64(); \
+  } while (0)
 constexpr uint32_t TILE = 16384;  // one [128 rows][64 bf16] SW128 tile
 
 template <int D>
@@ -94,6 +102,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) FA_T(10, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -105,6 +114,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (j < nkv) {
           const int st = j & 1;
           ptx::mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+          FA_T(8, j);
           ptx::mbar_arrive_expect_tx(&k_full[st], L::NB * TILE);
           for (int c = 0; c < L::NB; ++c)
             ptx::tma_load_2d(sm + L::K + (st * L::NB + c) * TILE, &qkv_map, &k_full[st],
@@ -113,6 +123,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (j > 0) {
           const int jj = j - 1, st = jj & 1;
           ptx::mbar_wait(&v_empty[st], ((jj >> 1) & 1) ^ 1);
+          FA_T(9, jj);
           ptx::mbar_arrive_expect_tx(&v_full[st], L::NB * TILE);
           for (int c = 0; c < L::NB; ++c)
             ptx::tma_load_2d(sm + L::V + (st * L::NB + c) * TILE, &qkv_map, &v_full[st],
@@ -130,7 +141,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (j < nkv) {
           const int st = j & 1;  // K stage == S buffer == warpgroup
           ptx::mbar_wait(&k_full[st], (j >> 1) & 1);
+          FA_T(0, j);
           ptx::mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
+          FA_T(1, j);
           ptx::tc_fence_after();
           const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * TILE);
 #pragma unroll
@@ -145,7 +158,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         if (j > 0) {
           const int jj = j - 1, w = jj & 1;
           ptx::mbar_wait(&v_full[w], (jj >> 1) & 1);
+          FA_T(2, jj);
           ptx::mbar_wait(&p_full[w], (jj >> 1) & 1);
+          FA_T(3, jj);
           ptx::tc_fence_after();
           const uint32_t sv = ptx::smem_u32(sm + L::V + w * L::NB * TILE);
           const uint32_t sp = ptx::smem_u32(sm + L::P + w * 2 * TILE);
@@ -175,6 +190,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     for (int j = wg; j < nkv; j += 2, ++it) {
       const bool diag = causal && j == qt;
       ptx::mbar_wait(&s_full[wg], it & 1);
+      if (lane == 0 && (warp & 3) == 0) FA_T(4, j);
       ptx::tc_fence_after();
       // pass 1: row max of the raw scores (scale > 0 commutes with max)
       float mx = -INFINITY;
@@ -193,7 +209,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
         }
       }
       const float m_new = fmaxf(m_ref, mx * scale_log2);
+      if (lane == 0 && (warp & 3) == 0) FA_T(5, j);
       if (it > 0) ptx::mbar_wait(&pv_done[wg], (it - 1) & 1);  // P[wg] free, O[wg] settled
+      if (lane == 0 && (warp & 3) == 0) FA_T(6, j);
       if (it == 0) {
         m_ref = m_new;
       } else if (__any_sync(0xffffffffu, m_new > m_ref + 8.f)) {  // warp-collective TMEM ops
@@ -242,6 +260,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       ptx::mbar_arrive(&s_empty[wg]);
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&p_full[wg]);
+      if (lane == 0 && (warp & 3) == 0) FA_T(7, j);
     }
     // drain this warpgroup's last PV
     if (it > 0) ptx::mbar_wait(&pv_done[wg], (it - 1) & 1);
@@ -318,3 +337,8 @@ int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H
 }
 
 }  // namespace amdp
+
+// Diagnostics hook (see g_fa_dbg): device buffer of >= 11 * 64 int64, or NULL to disable.
+extern "C" int amdp_debug_attention_trace(long long* device_buf) {
+  return cudaMemcpyToSymbol(amdp::g_fa_dbg, &device_buf, sizeof(device_buf));
+}

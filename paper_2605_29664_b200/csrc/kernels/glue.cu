@@ -8,9 +8,22 @@
 namespace amdp {
 namespace {
 
-constexpr int LN_MAX_VEC = 12;  // up to 12 x 256 = 3072 columns held in registers per warp
+constexpr int LN_MAX_VEC = 12;  // up to 12 x 256 = 3072 columns per row
+
+__device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __bfloat1622float2(h[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
 
 // ---------------------------------------------------------------- LayerNorm forward
+// One warp per row; the row is held in registers as raw bf16 (4 registers per 8 columns,
+// NV = ceil(cols / 256) chunks per lane), so HBM is read once and written once.
+template <int NV>
 __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
     const bf16* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     bf16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows,
@@ -19,37 +32,43 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
   const int warps = blockDim.x >> 5;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const bf16* xr = x + static_cast<size_t>(row) * cols;
-    float v[LN_MAX_VEC][8];
+    uint4 raw[NV];
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < LN_MAX_VEC; ++i) {
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < cols) raw[i] = *reinterpret_cast<const uint4*>(xr + c);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
       const int c = (i * 32 + lane) * 8;
       if (c < cols) {
-        load8(xr + c, v[i]);
+        float v[8];
+        unpack8(raw[i], v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) s += v[i][e];
+        for (int e = 0; e < 8; ++e) s += v[e];
       }
     }
     const float mean = warp_sum(s) / cols;
     float ss = 0.f;
 #pragma unroll
-    for (int i = 0; i < LN_MAX_VEC; ++i) {
+    for (int i = 0; i < NV; ++i) {
       const int c = (i * 32 + lane) * 8;
       if (c < cols) {
+        float v[8];
+        unpack8(raw[i], v);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float d = v[i][e] - mean;
-          ss += d * d;
-        }
+        for (int e = 0; e < 8; ++e) ss += (v[e] - mean) * (v[e] - mean);
       }
     }
     const float rstd = rsqrtf(warp_sum(ss) / cols + eps);
     bf16* yr = y + static_cast<size_t>(row) * cols;
 #pragma unroll
-    for (int i = 0; i < LN_MAX_VEC; ++i) {
+    for (int i = 0; i < NV; ++i) {
       const int c = (i * 32 + lane) * 8;
       if (c < cols) {
-        float o[8];
+        float v[8], o[8];
+        unpack8(raw[i], v);
         const float4 g0 = *reinterpret_cast<const float4*>(gamma + c);
         const float4 g1 = *reinterpret_cast<const float4*>(gamma + c + 4);
         const float4 b0 = *reinterpret_cast<const float4*>(beta + c);
@@ -57,7 +76,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
         const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
         const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = (v[i][e] - mean) * rstd * g[e] + b[e];
+        for (int e = 0; e < 8; ++e) o[e] = (v[e] - mean) * rstd * g[e] + b[e];
         store8(yr + c, o);
       }
     }
@@ -74,6 +93,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
 //        dx = resid + rstd * (dy*g - s1 - xhat*s2)   (second pass re-reads the row from L1)
 //  dg/db: a CTA owns 256 columns x 64 rows; each lane accumulates 8 columns over its
 //        warp's rows, the 8 warps combine in smem and add into the fp32 gradient buffer.
+template <int NV>
 __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
     const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ gamma,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, const bf16* resid_grad,
@@ -83,32 +103,47 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
     const size_t off = static_cast<size_t>(row) * cols;
     const float mean = mean_in[row], rstd = rstd_in[row];
-    float s1 = 0.f, s2 = 0.f;
-    for (int c = lane * 8; c < cols; c += 256) {
-      float xv[8], dv[8];
-      load8(x + off + c, xv);
-      load8(dy + off + c, dv);
+    uint4 xr[NV], dr[NV];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float dxh = dv[e] * gamma[c + e];
-        s1 += dxh;
-        s2 += dxh * (xv[e] - mean) * rstd;
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < cols) {
+        xr[i] = *reinterpret_cast<const uint4*>(x + off + c);
+        dr[i] = *reinterpret_cast<const uint4*>(dy + off + c);
+      }
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < cols) {
+        float xv[8], dv[8];
+        unpack8(xr[i], xv);
+        unpack8(dr[i], dv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float dxh = dv[e] * gamma[c + e];
+          s1 += dxh;
+          s2 += dxh * (xv[e] - mean) * rstd;
+        }
       }
     }
     s1 = warp_sum(s1) / cols;
     s2 = warp_sum(s2) / cols;
-    for (int c = lane * 8; c < cols; c += 256) {
-      float xv[8], dv[8], o[8];
-      float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      load8(x + off + c, xv);
-      load8(dy + off + c, dv);
-      if (resid_grad) load8(resid_grad + off + c, r);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float xh = (xv[e] - mean) * rstd;
-        o[e] = r[e] + rstd * (dv[e] * gamma[c + e] - s1 - xh * s2);
+    for (int i = 0; i < NV; ++i) {
+      const int c = (i * 32 + lane) * 8;
+      if (c < cols) {
+        float xv[8], dv[8], o[8];
+        float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        unpack8(xr[i], xv);
+        unpack8(dr[i], dv);
+        if (resid_grad) load8(resid_grad + off + c, r);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          o[e] = r[e] + rstd * (dv[e] * gamma[c + e] - s1 - (xv[e] - mean) * rstd * s2);
+        store8(dx + off + c, o);
       }
-      store8(dx + off + c, o);
     }
   }
 }
@@ -288,9 +323,14 @@ extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const f
   int blocks = (warps_needed + 7) / 8;
   const int cap = 8 * num_sms();
   if (blocks > cap) blocks = cap;
-  layernorm_fwd_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const bf16*>(x), gamma, beta, reinterpret_cast<bf16*>(y), mean, rstd, rows,
-      cols, eps);
+  auto xs = reinterpret_cast<const bf16*>(x);
+  auto ys = reinterpret_cast<bf16*>(y);
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  const int nv = (cols + 255) / 256;
+  if (nv <= 1) layernorm_fwd_kernel<1><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+  else if (nv <= 4) layernorm_fwd_kernel<4><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+  else if (nv <= 8) layernorm_fwd_kernel<8><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+  else layernorm_fwd_kernel<LN_MAX_VEC><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
   return cudaGetLastError();
 }
 
@@ -306,13 +346,21 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
                                   float* dbeta, void* workspace, int rows, int cols,
                                   amdp_stream_t stream) {
   (void)workspace;
-  if (rows <= 0 || cols <= 0 || cols % 8 != 0) return AMDP_ERR_INVALID;
+  if (rows <= 0 || cols <= 0 || cols % 8 != 0 || cols > LN_MAX_VEC * 256) return AMDP_ERR_INVALID;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int blocks = (rows + 7) / 8;
   if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
-  layernorm_bwd_dx_kernel<<<blocks, 256, 0, s>>>(
-      reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(x), gamma, mean, rstd,
-      reinterpret_cast<const bf16*>(resid_grad), reinterpret_cast<bf16*>(dx), rows, cols);
+  {
+    auto dys = reinterpret_cast<const bf16*>(dy);
+    auto xs = reinterpret_cast<const bf16*>(x);
+    auto rs = reinterpret_cast<const bf16*>(resid_grad);
+    auto dxs = reinterpret_cast<bf16*>(dx);
+    const int nv = (cols + 255) / 256;
+    if (nv <= 1) layernorm_bwd_dx_kernel<1><<<blocks, 256, 0, s>>>(dys, xs, gamma, mean, rstd, rs, dxs, rows, cols);
+    else if (nv <= 4) layernorm_bwd_dx_kernel<4><<<blocks, 256, 0, s>>>(dys, xs, gamma, mean, rstd, rs, dxs, rows, cols);
+    else if (nv <= 8) layernorm_bwd_dx_kernel<8><<<blocks, 256, 0, s>>>(dys, xs, gamma, mean, rstd, rs, dxs, rows, cols);
+    else layernorm_bwd_dx_kernel<LN_MAX_VEC><<<blocks, 256, 0, s>>>(dys, xs, gamma, mean, rstd, rs, dxs, rows, cols);
+  }
   dim3 g((cols + 255) / 256, (rows + LN_DG_ROWS - 1) / LN_DG_ROWS);
   layernorm_bwd_dgb_kernel<<<g, 256, 0, s>>>(reinterpret_cast<const bf16*>(dy),
                                              reinterpret_cast<const bf16*>(x), mean, rstd, dgamma,
