@@ -48,8 +48,11 @@ def _sm_int(x: int) -> int:
     return int(splitmix64(np.uint64(x & M64)))
 
 
-def synthetic_tokens(seq: int, seqs: int, vocab: int, data_seed: int, first: int, count: int):
-    """Arithmetic-progression token streams with 1/8 noise (amdp_synthetic_tokens)."""
+def synthetic_tokens(seq: int, seqs: int, vocab: int, data_seed: int, first: int, count: int,
+                     causal: bool = True):
+    """amdp_synthetic_tokens: arithmetic-progression token streams with 1/8 noise; causal ->
+    next-token labels; otherwise BERT MLM (15% positions, 80/10/10 [MASK]/random/keep,
+    [MASK] = vocab - 1, label -1 elsewhere)."""
     T = seq * seqs
     inputs = np.empty((count, T), np.int32)
     labels = np.empty((count, T), np.int32)
@@ -63,9 +66,20 @@ def synthetic_tokens(seq: int, seqs: int, vocab: int, data_seed: int, first: int
                 nz = splitmix64(np.uint64(r) + p + np.uint64(1))
             noisy = (nz & np.uint64(7)) == 0
             prog = (np.uint64(start) + p * np.uint64(stride)) % np.uint64(vocab)
-            tok = np.where(noisy, (nz >> np.uint64(8)) % np.uint64(vocab), prog).astype(np.int32)
-            inputs[j, b * seq:(b + 1) * seq] = tok[:seq]
-            labels[j, b * seq:(b + 1) * seq] = tok[1:]
+            tok = np.where(noisy, (nz >> np.uint64(8)) % np.uint64(vocab), prog).astype(np.int64)
+            sl = slice(b * seq, (b + 1) * seq)
+            if causal:
+                inputs[j, sl] = tok[:seq]
+                labels[j, sl] = tok[1:]
+            else:
+                with np.errstate(over="ignore"):
+                    hm = splitmix64(np.uint64(r ^ 0xA5A5A5A5A5A5A5A5) + p[:seq])
+                masked = (hm % np.uint64(100)) < 15
+                act = (hm >> np.uint64(8)) % np.uint64(10)
+                rnd = ((hm >> np.uint64(16)) % np.uint64(vocab)).astype(np.int64)
+                inp = np.where(masked & (act < 8), vocab - 1, np.where(masked & (act == 8), rnd, tok[:seq]))
+                inputs[j, sl] = inp
+                labels[j, sl] = np.where(masked, tok[:seq], -1)
     return inputs, labels
 
 
@@ -227,10 +241,14 @@ class StageMath:
             logits = rb(lf @ W["head"].T)
             mx = logits.max(-1, keepdims=True)
             lse = (mx + np.log(np.exp(logits - mx).sum(-1, keepdims=True)))[:, 0]
-            loss = float(np.mean(lse - logits[np.arange(m.T), labels]))
+            valid = labels >= 0
+            cnt = max(1, int(valid.sum()))  # mean over labelled tokens (all for GPT)
+            rows = np.arange(m.T)[valid]
+            loss = float((lse[valid] - logits[rows, labels[valid]]).sum() / cnt)
             prob = np.exp(logits - lse[:, None])
-            prob[np.arange(m.T), labels] -= 1.0
-            cache["dlogits"] = rb(prob / m.T)
+            prob[rows, labels[valid]] -= 1.0
+            prob[~valid] = 0.0
+            cache["dlogits"] = rb(prob / cnt)
             return None, cache, loss
         return x, cache, loss
 

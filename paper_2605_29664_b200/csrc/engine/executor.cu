@@ -168,6 +168,7 @@ class Engine {
   std::vector<cudaEvent_t> stage_ready_;      // weights of stage i usable (after bcast)
   size_t slot_total_ = 0;
   bool plan_only_ = false;
+  std::vector<float> loss_scale_;  // per minibatch: 1 / number of labelled tokens
 
   int rank_of_dev(int dev) const { return dev / per_rank_; }
   int owner_rank(int stage) const { return rank_of_dev(stage); }
@@ -602,7 +603,7 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     int launched;
     if (task.kind == ppsim::Kind::Forward) {
       uint16_t* out = tp.out_buf >= 0 ? bufs_[static_cast<size_t>(tp.out_buf)].ptr : nullptr;
-      launched = S.forward(A, tok, lab, in, out, d_loss_ + j, ws_, cs_, &rc);
+      launched = S.forward(A, tok, lab, in, out, d_loss_ + j, loss_scale_[static_cast<size_t>(j)], ws_, cs_, &rc);
     } else {
       const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
       uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
@@ -706,6 +707,16 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
   const auto& g = sched.g;
   if (max_window < 0 || max_window > W_) max_window = W_;
   stats = amdp_run_stats{};
+  // loss = mean over the minibatch's labelled tokens (all of them for GPT; the masked
+  // positions for MLM), so the CE gradient and the reported loss use 1 / count
+  loss_scale_.assign(static_cast<size_t>(M_), 1.f / static_cast<float>(dm.T));
+  if (h_lab)
+    for (int j = 0; j < M_; ++j) {
+      int64_t cnt = 0;
+      const int32_t* lj = h_lab + static_cast<size_t>(j) * dm.T;
+      for (int t = 0; t < dm.T; ++t) cnt += lj[t] >= 0;
+      loss_scale_[static_cast<size_t>(j)] = 1.f / static_cast<float>(cnt > 0 ? cnt : 1);
+    }
   ktimer_.reset();
   if (rc_.record_events && ev_start_.empty()) {
     ev_start_.resize(static_cast<size_t>(N));
@@ -742,7 +753,7 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
   stats.device_ms = ms;
   ktimer_.collect();
   if (losses_out)
-    for (int j = 0; j < max_window * thr_; ++j) losses_out[j] /= static_cast<float>(dm.T);
+    for (int j = 0; j < max_window * thr_; ++j) losses_out[j] *= loss_scale_[static_cast<size_t>(j)];
 
   // measured timeline + observed versions
   std::vector<int> trace(g.tasks.size());
@@ -909,20 +920,33 @@ int amdp_synthetic_tokens(const amdp_model_config* m, uint64_t seed, int first, 
   const int S = m->seq, B = m->seqs_per_minibatch, V = m->vocab;
   if (S <= 0 || B <= 0 || V <= 0 || count < 0) return AMDP_ERR_INVALID;
   const size_t T = static_cast<size_t>(S) * B;
+  const uint64_t UV = static_cast<uint64_t>(V);
   for (int j = 0; j < count; ++j) {
     const uint64_t mb = static_cast<uint64_t>(first + j);
     for (int b = 0; b < B; ++b) {
       const uint64_t r = amdp::splitmix64(seed * 0x100000001B3ull + mb * 1024ull + static_cast<uint64_t>(b));
-      const uint64_t start = r % static_cast<uint64_t>(V);
+      const uint64_t start = r % UV;
       const uint64_t stride = 1 + (r >> 32) % 7;
+      const size_t base = static_cast<size_t>(j) * T + static_cast<size_t>(b) * S;
       for (int p = 0; p <= S; ++p) {
         const uint64_t nz = amdp::splitmix64(r + static_cast<uint64_t>(p) + 1);
-        const int32_t tok = static_cast<int32_t>((nz & 7) == 0 ? (nz >> 8) % static_cast<uint64_t>(V)
-                                                               : (start + static_cast<uint64_t>(p) * stride) %
-                                                                     static_cast<uint64_t>(V));
-        const size_t base = static_cast<size_t>(j) * T + static_cast<size_t>(b) * S;
-        if (p < S) inputs[base + static_cast<size_t>(p)] = tok;
-        if (p > 0) labels[base + static_cast<size_t>(p) - 1] = tok;
+        const int32_t tok = static_cast<int32_t>((nz & 7) == 0 ? (nz >> 8) % UV
+                                                               : (start + static_cast<uint64_t>(p) * stride) % UV);
+        if (m->causal) {  // GPT: next-token prediction
+          if (p < S) inputs[base + static_cast<size_t>(p)] = tok;
+          if (p > 0) labels[base + static_cast<size_t>(p) - 1] = tok;
+        } else if (p < S) {  // BERT MLM: 15% of positions, 80/10/10 mask/random/keep
+          const uint64_t hm = amdp::splitmix64((r ^ 0xA5A5A5A5A5A5A5A5ull) + static_cast<uint64_t>(p));
+          int32_t in = tok, lab = -1;
+          if (hm % 100 < 15) {
+            lab = tok;
+            const uint64_t act = (hm >> 8) % 10;
+            if (act < 8) in = static_cast<int32_t>(UV - 1);  // [MASK] = last vocabulary id
+            else if (act == 8) in = static_cast<int32_t>((hm >> 16) % UV);
+          }
+          inputs[base + static_cast<size_t>(p)] = in;
+          labels[base + static_cast<size_t>(p)] = lab;
+        }
       }
     }
   }

@@ -201,7 +201,7 @@ size_t GptStage::workspace_bytes(const Dims& d) {
   } while (0)
 
 int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
-                      const uint16_t* in, uint16_t* out, float* loss_sum, uint8_t* /*ws*/,
+                      const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* /*ws*/,
                       cudaStream_t s, int* rc) const {
   int launched = 0;
   *rc = 0;
@@ -237,7 +237,7 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
                                 a.lnf_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm_t(kt, T, d_.V, h, a.lnf, h, false, w + head_.off, h, false, a.logits, d_.V,
                   AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(K_XENT, 0, 6.0 * T * d_.V, amdp_xent_fwd_bwd(a.logits, labels, loss_sum, T, d_.V, d_.V, 1.0f / static_cast<float>(T), st), 1);
+    AMDP_TRY(K_XENT, 0, 6.0 * T * d_.V, amdp_xent_fwd_bwd(a.logits, labels, loss_sum, T, d_.V, d_.V, loss_scale, st), 1);
   }
   return launched;
 }

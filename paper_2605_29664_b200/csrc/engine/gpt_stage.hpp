@@ -87,7 +87,7 @@ class GptStage {
   // depth-1), `gout` grad w.r.t. the stage input (stages > 0).  Returns the number of
   // kernels launched (>= 0) or a negative/positive error code via `rc`.
   int forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
-              const uint16_t* in, uint16_t* out, float* loss_sum, uint8_t* ws,
+              const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* ws,
               cudaStream_t s, int* rc) const;
   int backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in,
                const uint16_t* gin, uint16_t* gout, uint8_t* ws, cudaStream_t s,

@@ -1,0 +1,92 @@
+"""The BASELINE.json configurations on one B200 (logical devices folded onto the GPU).
+
+  * tiny BERT-style MLM (non-causal attention, 15% masked-token loss) — parity with the CPU
+    oracle replaying the reference trace, same tolerances as the tiny GPT test;
+  * GPT-350M D=2 / D=4, BERT-large D=8, GPT-2.7B D=2 / D=4 (the depth sweep's single-GPU
+    points; D=8 needs ~210 GB of activations + states and runs 8-way) — every F/B the GPU
+    ran is in the reference's per-device order and read the parameter version the
+    reference's trace implies (F: w - preloaded, B: w), the measured timeline passes the
+    reference audits, and the loss is finite, starts near ln(V) and does not diverge.
+"""
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
+
+
+def _golden_csv(cfg):
+    for e in json.load(open(os.path.join(HERE, "golden", "sched_golden.json"))):
+        if e["config"] == cfg and "csv" in e:
+            return e["csv"]
+    raise KeyError(cfg)
+
+
+def test_tiny_bert_mlm_parity():
+    import gpt_oracle as O
+    from paper_2605_29664_b200 import engine as E
+
+    model = E.ModelConfig.tiny()
+    model.causal = False
+    model.layers_per_stage = [1, 1, 1, 1]
+    opt = E.OptimizerConfig(kind=3, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8)
+    run = E.RunConfig(depth=4, threshold=8, windows=4, optimizer=opt)
+    eng = E.Engine(model, run)
+    inputs, labels = E.synthetic_tokens(model, run.data_seed, 0, run.num_minibatches)
+    assert 0.1 < (labels >= 0).mean() < 0.2
+    losses = eng.run(inputs, labels)
+    om = O.Model(4, 128, 4, 512, 1024, 64, 4, False, model.seed)
+    trace = _golden_csv(["AMDP", 4, 4, "1", "1", "0", "0", 2, 2, 8, 32, 1])
+    ol, _, seen = O.replay(trace, om, [1, 1, 1, 1], O.Opt("adamw", 1e-3, 0.9, 0.95, 1e-8, 0.0), 8, inputs,
+                           labels)
+    rel = np.abs(losses - ol) / np.abs(ol)
+    assert rel.max() < 2e-3, rel.max()
+    for r in eng.version_trace().strip().split("\n")[1:]:
+        dev, kind, stage, mb, pipe, w, pre, ver = r.split(",")
+        assert int(ver) == seen[(kind, int(stage), int(mb))]
+    eng.close()
+
+
+CONFIGS = {
+    # name: (model factory, depth, threshold, windows)
+    "gpt350m_d2": ("gpt_350m", 2, 16, 2),
+    "gpt350m_d4": ("gpt_350m", 4, 16, 2),
+    "bert_large_d8": ("bert_large", 8, 32, 2),
+    "gpt2p7b_d2": ("gpt_2p7b", 2, 8, 1),
+    "gpt2p7b_d4": ("gpt_2p7b", 4, 16, 1),
+}
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_baseline_config_runs(name):
+    from paper_2605_29664_b200 import engine as E
+    from paper_2605_29664_b200 import ppsim as P
+
+    factory, depth, thr, windows = CONFIGS[name]
+    model = getattr(E.ModelConfig, factory)()
+    run = E.RunConfig(depth=depth, threshold=thr, windows=windows,
+                      optimizer=E.OptimizerConfig(lr=1e-4))
+    eng = E.Engine(model, run)
+    try:
+        inputs, labels = E.synthetic_tokens(model, run.data_seed, 0, run.num_minibatches)
+        losses = eng.run(inputs, labels)
+        assert np.all(np.isfinite(losses))
+        assert abs(losses[0] - math.log(model.vocab)) < 1.0  # random init ~ uniform prediction
+        assert losses[-thr:].mean() < losses[0] + 0.5
+        # per-device F/B order and versions == the reference trace (declared 1:1 costs)
+        ref = P.simulate(P.build(run.policy(), run.declared_cluster()), run.declared_cluster())
+        ref_rows = P.version_trace_csv(ref).strip().split("\n")
+        got_rows = eng.version_trace().strip().split("\n")
+        assert got_rows == ref_rows
+        rep = eng.timeline().report(run.policy(), warmup=0)
+        assert rep["causality_issues"] == [] and rep["overlap_issues"] == []
+        assert rep["mismatch"]["max_overall"] <= 1
+    finally:
+        eng.close()
