@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -169,6 +170,7 @@ class Engine {
   size_t slot_total_ = 0;
   bool plan_only_ = false;
   std::vector<float> loss_scale_;  // per minibatch: 1 / number of labelled tokens
+  SideStream side_;                // weight-gradient GEMM stream + events
 
   int rank_of_dev(int dev) const { return dev / per_rank_; }
   int owner_rank(int stage) const { return rank_of_dev(stage); }
@@ -260,6 +262,10 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   }
   CUDA_OK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   CUDA_OK(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
+  if (!getenv("AMDP_NO_SIDE_STREAM")) {
+    CUDA_OK(cudaStreamCreateWithFlags(&side_.side, cudaStreamNonBlocking));
+    for (auto& e : side_.ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   if (world_ > 1) {
     if (!nccl_id) throw std::invalid_argument("engine: nccl_id required when world_size > 1");
     ncclUniqueId id;
@@ -313,6 +319,11 @@ Engine::~Engine() {
   for (auto c : group_comm_)
     if (c) ncclCommDestroy(c);
   if (world_comm_) ncclCommDestroy(world_comm_);
+  if (side_.side) {
+    cudaStreamSynchronize(side_.side);
+    for (auto e : side_.ev) cudaEventDestroy(e);
+    cudaStreamDestroy(side_.side);
+  }
   cudaStreamDestroy(cs_);
   cudaStreamDestroy(ms_);
 }
@@ -607,7 +618,8 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     } else {
       const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
       uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
-      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, &rc);
+      // the kernel-timing run serialises the streams so per-launch event spans are exact
+      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, ktimer_.enabled ? SideStream{} : side_, &rc);
     }
     stats.kernels_launched += launched;
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));

@@ -242,20 +242,32 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
   return launched;
 }
 
+// Weight-gradient GEMMs run on `side` so they fill the wave-quantisation tails of the
+// activation-gradient chain on `s` (most stage GEMMs have N = h = 2048: 3.5 waves of
+// 256x256 pair tiles on 148 SMs).  Events order every hand-off; the task ends with `s`
+// joined to `side`, so slot activations and gradient buffers are quiescent afterwards.
 int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in, const uint16_t* gin,
-                       uint16_t* gout, uint8_t* wsb, cudaStream_t s, int* rc) const {
+                       uint16_t* gout, uint8_t* wsb, cudaStream_t s, const SideStream& ss, int* rc) const {
   int launched = 0;
   *rc = 0;
   auto st = reinterpret_cast<amdp_stream_t>(s);
   const int T = d_.T, h = d_.h, F = d_.ffn;
   const Ws ws = carve_ws(d_, wsb);
+  cudaStream_t sd = ss.side ? ss.side : s;
+  auto hand = [&](cudaEvent_t e, cudaStream_t from, cudaStream_t to) {
+    if (from == to) return;
+    cudaEventRecord(e, from);
+    cudaStreamWaitEvent(to, e, 0);
+  };
+  enum { E_G, E_DU, E_DH, E_DQ, F_G, F_DU, F_DH, F_DQ, E_HEAD, F_END };
   const uint16_t* g = gin;
   if (last()) {
     // a.logits already holds dloss/dlogits (scale 1/T), written by the forward's CE pass
-    AMDP_GEMM(gemm_t(kt, T, h, d_.V, a.logits, d_.V, false, w + head_.off, h, true, ws.dtmp, h,
-                  AMDP_EPI_STORE_BF16, s), 1);
+    hand(ss.ev[E_HEAD], s, sd);
     AMDP_GEMM(gemm_t(kt, d_.V, h, T, a.logits, d_.V, true, a.lnf, h, true, grad + head_.off, h,
-                  AMDP_EPI_ACCUM_F32, s), 1);
+                     AMDP_EPI_ACCUM_F32, sd), 1);
+    AMDP_GEMM(gemm_t(kt, T, h, d_.V, a.logits, d_.V, false, w + head_.off, h, true, ws.dtmp, h,
+                     AMDP_EPI_STORE_BF16, s), 1);
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, a.xf, master + lnf_g_.off, a.lnf_mean, a.lnf_rstd, nullptr, ws.g0,
                                 grad + lnf_g_.off, grad + lnf_b_.off, ws.ln, T, h, st), 2);
     g = ws.g0;
@@ -265,30 +277,43 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     const LayerActs& A = a.layers[static_cast<size_t>(li)];
     const uint16_t* x = li > 0 ? A.x : (first() ? a.x0 : in);
     // y = hmid + f W2^T
+    hand(ss.ev[E_G], s, sd);
+    AMDP_GEMM(gemm_t(kt, h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, sd), 1);
+    if (sd != s) cudaEventRecord(ss.ev[F_G], sd);
+    if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DU], 0);  // previous layer's dW1 done with dU
     AMDP_GEMM(gemm_t(kt, T, F, h, g, h, false, w + P.fc2.off, F, true, ws.dU, F, AMDP_EPI_GELU_BWD, s, A.u, F), 1);
-    AMDP_GEMM(gemm_t(kt, h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, s), 1);
+    hand(ss.ev[E_DU], s, sd);
     // f = gelu(ln2 W1^T)
+    AMDP_GEMM(gemm_t(kt, F, h, T, ws.dU, F, true, A.ln2, h, true, grad + P.fc1.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
+    if (sd != s) cudaEventRecord(ss.ev[F_DU], sd);
     AMDP_GEMM(gemm_t(kt, T, h, F, ws.dU, F, false, w + P.fc1.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_GEMM(gemm_t(kt, F, h, T, ws.dU, F, true, A.ln2, h, true, grad + P.fc1.off, h, AMDP_EPI_ACCUM_F32, s), 1);
     // ln2 = LN(hmid); dhmid = g + LN'(dln2)
+    if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DH], 0);  // previous layer's dWo done with dhmid
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, A.hmid, master + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g, ws.dhmid,
                                 grad + P.ln2_g.off, grad + P.ln2_b.off, ws.ln, T, h, st), 2);
+    hand(ss.ev[E_DH], s, sd);
     // hmid = x + o Wo^T
+    AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
+    if (sd != s) cudaEventRecord(ss.ev[F_DH], sd);
     AMDP_GEMM(gemm_t(kt, T, h, h, ws.dhmid, h, false, w + P.o.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DQ], 0);  // previous layer's dWqkv done with dqkv
     AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
                                 d_.causal ? 1 : 0, st), 3);
+    hand(ss.ev[E_DQ], s, sd);
     // qkv = ln1 Wqkv^T
-    AMDP_GEMM(gemm_t(kt, T, h, 3 * h, ws.dqkv, 3 * h, false, w + P.qkv.off, h, true, ws.dtmp, h,
-                  AMDP_EPI_STORE_BF16, s), 1);
     AMDP_GEMM(gemm_t(kt, 3 * h, h, T, ws.dqkv, 3 * h, true, A.ln1, h, true, grad + P.qkv.off, h,
-                  AMDP_EPI_ACCUM_F32, s), 1);
+                     AMDP_EPI_ACCUM_F32, sd), 1);
+    if (sd != s) cudaEventRecord(ss.ev[F_DQ], sd);
+    AMDP_GEMM(gemm_t(kt, T, h, 3 * h, ws.dqkv, 3 * h, false, w + P.qkv.off, h, true, ws.dtmp, h,
+                     AMDP_EPI_STORE_BF16, s), 1);
     uint16_t* gn = (li == 0 && !first()) ? gout : (g == ws.g0 ? ws.g1 : ws.g0);
+    if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_G], 0);  // dW2 of the layer that read gn's buffer
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, x, master + P.ln1_g.off, A.ln1_mean, A.ln1_rstd, ws.dhmid, gn,
                                 grad + P.ln1_g.off, grad + P.ln1_b.off, ws.ln, T, h, st), 2);
     g = gn;
   }
   if (first()) AMDP_TRY(K_EMBED, 0, 10.0 * T * h, amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, T, d_.S, h, st), 2);
+  hand(ss.ev[F_END], sd, s);  // join: weight gradients complete before the task ends
   return launched;
 }
 

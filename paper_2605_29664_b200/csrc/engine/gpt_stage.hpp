@@ -20,6 +20,12 @@ namespace amdp {
 
 class KTimer;
 
+// Second stream + events for the weight-gradient GEMMs of a backward task.
+struct SideStream {
+  cudaStream_t side = nullptr;  // nullptr: everything on the main stream
+  cudaEvent_t ev[10] = {};
+};
+
 struct Dims {
   int L, h, heads, hd, ffn, V, S, B, T;  // T = B * S tokens per minibatch
   bool causal;
@@ -91,7 +97,7 @@ class GptStage {
               cudaStream_t s, int* rc) const;
   int backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in,
                const uint16_t* gin, uint16_t* gout, uint8_t* ws, cudaStream_t s,
-               int* rc) const;
+               const SideStream& side, int* rc) const;
 
  private:
   Dims d_;
