@@ -141,8 +141,10 @@ int amdp_fill_normal_bf16_f32(uint16_t* w_bf16, float* w_f32, int64_t n, uint64_
 int amdp_fill_const_f32(float* x, int64_t n, float value, amdp_stream_t stream);
 
 /* Diagnostics: CTA 0 of the tensor-core attention forward records clock64() at each
- * pipeline hand-off into device_buf (>= 11*64 int64; NULL disables). */
+ * pipeline hand-off into device_buf (>= 16*64 int64; NULL disables). */
 int amdp_debug_attention_trace(long long* device_buf);
+/* Every CTA of the attention forward writes (start ns, end ns, smid) at 3*blockIdx. */
+int amdp_debug_attention_cta_times(long long* device_buf);
 int amdp_debug_attention_bwd_trace(long long* device_buf); /* CTA 0 of the dQ kernel */
 
 /* Library identification (for the loader's sanity check). */

@@ -564,7 +564,7 @@ extern "C" int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse
   auto q = reinterpret_cast<const bf16*>(qkv);
   auto o = reinterpret_cast<bf16*>(out);
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  if ((head_dim == 64 || head_dim == 128) && seq % 128 == 0)  // tcgen05 path
+  if ((head_dim == 64 || head_dim == 128) && seq % 256 == 0)  // tcgen05 path (256-query tiles)
     return attention_fwd_tc(q, o, lse, batch, seq, heads, head_dim, causal, s);
   switch (head_dim) {
     case 32: return launch_fwd<32>(q, o, lse, batch, seq, heads, causal, s);

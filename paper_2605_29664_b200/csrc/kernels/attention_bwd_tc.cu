@@ -25,7 +25,7 @@ constexpr uint32_t T128 = 16384;  // [128 rows][64 bf16] SW128 tile
 __device__ long long* g_bw_dbg = nullptr;
 #define BW_T(slot, j)                                                                       \
   do {                                                                                      \
-    if (g_bw_dbg != nullptr && blockIdx.x == 0 && (j) < 64) g_bw_dbg[(slot)*64 + (j)] = clock64(); \
+    if (dbg_ != nullptr && (j) < 64) dbg_[(slot)*64 + (j)] = clock64(); \
   } while (0)
 constexpr uint32_t T64 = 8192;    // [64 rows][64 bf16]
 
@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(384, 1)
                        float scale_log2, float scale, int causal) {
   using L = KvSmem<D>;
   extern __shared__ uint8_t smem_raw[];
+  long long* const dbg_ = blockIdx.x == 0 ? g_bw_dbg : nullptr;  // trace hook, read once
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(384, 1)
   using L = QSmem<D>;
   constexpr int NS = L::NS;
   extern __shared__ uint8_t smem_raw[];
+  long long* const dbg_ = blockIdx.x == 0 ? g_bw_dbg : nullptr;  // trace hook, read once
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);

@@ -1,22 +1,25 @@
 // Flash-attention forward on the 5th-generation tensor cores (sm_100a).
 //
-// One CTA per (128-query tile, head, sequence), 12 warps:
-//   warp 0     : TMA producer — Q once, K_j and V_j (128 keys) into separate 2-stage rings,
-//                straight out of the packed qkv activation rows (no repacking);
-//   warp 1     : tcgen05.mma issuer — S_j = Q K_j^T (M=128, N=128, K=D) into TMEM buffer
-//                S[j%2]; O[j%2] += P[j%2] V_j (M=128, N=D, K=128), P from swizzled smem,
-//                V consumed MN-major;
-//   warp 2     : TMEM allocator (512 columns: S0 | S1 | O0 | O1);
-//   warps 4-7  : softmax warpgroup 0 — even KV blocks;  warps 8-11 : warpgroup 1 — odd.
-// Each warpgroup runs an independent online softmax (its own running max m, sum l and
-// O accumulator) over its half of the KV blocks, so the two never synchronise per block;
-// thread t of a warpgroup owns query row t (TMEM lane t).  The halves are merged once at
-// the end: O = (O0 2^(m0-m) + O1 2^(m1-m)) / (l0 2^(m0-m) + l1 2^(m1-m)).
+// Persistent CTAs (one per SM) over (256-query pair tile, head, sequence) tiles, 12 warps:
+//   warp 0     : TMA producer — Q_A, Q_B once, then K_j / V_j (128 keys) into 2-stage rings
+//                straight out of the packed qkv activation rows;
+//   warp 1     : tcgen05.mma issuer, ping-pong order  S_A(j) | PV_B(j-1) | S_B(j) | PV_A(j):
+//                while warpgroup A turns S_A(j) into P_A(j) the tensor core runs B's work
+//                and vice versa;
+//   warp 2     : TMEM allocator (512 columns: S_A | S_B | O_A | O_B);
+//   warps 4-7  : softmax warpgroup A (query rows 0-127 of the pair tile);
+//   warps 8-11 : softmax warpgroup B (rows 128-255).
+// Each K/V tile feeds 256 queries, halving the K/V traffic of a 128-query CTA (the K/V
+// stream was the bottleneck: profiles/r01_attn_traces.md).  P never touches smem: the
+// softmax threads write it (bf16) over the first 64 TMEM columns of the S tile they just
+// read and PV reads it as the TMEM A operand (tcgen05 TS form).  tcgen05 MMAs execute in
+// issue order, so S_A(j+1) may be issued right behind PV_A(j) that reads the same columns,
+// and s_full(j) fires only after every earlier MMA (including PV(j-1)) retired, which is
+// what lets the softmax rescale O in place.
 // Per score: one FFMA (scale folded into the exponent), one ex2.approx, one FADD, half a
-// pack; the running max is only pushed into O (rescale in TMEM) when it grows by more
-// than 2^8 — exact, since P and O then share the stale reference.
-// LSE is stored in the log2 domain with the softmax scale folded in, the convention the
-// backward kernels in attention.cu consume.
+// pack; O is rescaled only when the running max grows by more than 2^8 (exact).
+// LSE is stored in the log2 domain with the softmax scale folded in (the backward's
+// convention).
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 #include "tma_host.hpp"
@@ -24,26 +27,30 @@
 namespace amdp {
 namespace {
 
-constexpr int FA_BQ = 128, FA_BKV = 128, FA_THREADS = 384;
+constexpr int FA_BQ = 256, FA_BKV = 128, FA_THREADS = 384;
+#ifndef FA_POLY_PAIRS
+#define FA_POLY_PAIRS 1  // of every 4 exponent pairs, this many are evaluated on the FMA pipe (1 measured best)
+#endif
+constexpr uint32_t TILE = 16384;  // one [128 rows][64 bf16] SW128 tile
 
 // Diagnostics: when set (amdp_debug_attention_trace), CTA 0 records clock64() at each
 // pipeline hand-off into this buffer (slot layout in scripts/attn_trace.py).
 __device__ long long* g_fa_dbg = nullptr;
-#define FA_T(slot, j)                                             \
-  do {                                                            \
-    if (g_fa_dbg != nullptr && blockIdx.x == 0) g_fa_dbg[(slot)*64 + (j)] = clock64(); \
+// Per-CTA (start ns, end ns, smid) when set (amdp_debug_attention_cta_times).
+__device__ long long* g_fa_cta = nullptr;
+#define FA_T(slot, j)                                                                        \
+  do {                                                                                       \
+    if (dbg_ != nullptr && (j) < 64) dbg_[(slot)*64 + (j)] = clock64(); \
   } while (0)
-constexpr uint32_t TILE = 16384;  // one [128 rows][64 bf16] SW128 tile
 
 template <int D>
 struct FaSmem {
-  static constexpr int NB = D / 64;  // 64-wide column blocks per row tile
-  static constexpr uint32_t Q = 0;
-  static constexpr uint32_t K = Q + NB * TILE;      // 2 stages
-  static constexpr uint32_t V = K + 2 * NB * TILE;  // 2 stages
-  static constexpr uint32_t P = V + 2 * NB * TILE;  // 2 buffers of [128 q][128 keys]
-  static constexpr uint32_t XCH = P + 4 * TILE;     // warpgroup-1 (m, l) hand-off
-  static constexpr uint32_t BAR = XCH + 2 * 128 * 4;
+  static constexpr int NB = D / 64;                 // 64-wide column blocks per row tile
+  static constexpr int KVS = D == 128 ? 2 : 4;      // K / V ring depth
+  static constexpr uint32_t Q = 0;                  // Q_A | Q_B
+  static constexpr uint32_t K = Q + 2 * NB * TILE;
+  static constexpr uint32_t V = K + KVS * NB * TILE;
+  static constexpr uint32_t BAR = V + KVS * NB * TILE;
   static constexpr uint32_t BYTES = BAR + 256;
 };
 
@@ -53,47 +60,137 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe for a pair (round-to-nearest split, degree-3 fit of 2^f on [-1/2, 1/2],
+// rel. err 7.7e-5, far below the bf16 rounding of P): takes a quarter of the exponentials off
+// the 16/clk/SM MUFU unit, which otherwise matches the tensor time at head_dim 128.
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  // f = x - (t - M) = x + (M - t), both steps exact
+  const float2 f = __fadd2_rn(x, __ffma2_rn(t, make_float2(-1.f, -1.f), make_float2(12582912.f, 12582912.f)));
+  float2 p = __ffma2_rn(f, make_float2(0.05508868f, 0.05508868f), make_float2(0.24260405f, 0.24260405f));
+  p = __ffma2_rn(p, f, make_float2(0.69327623f, 0.69327623f));
+  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+// P = 2^(S*scale - m) for one 128-column row held in registers, written as bf16 pairs over
+// the first 64 TMEM columns of the S tile; returns the row sum.  Packed f32x2 arithmetic and
+// one exponent pair in four on the FMA pipe keep issue slots and MUFU below the tensor time.
+template <bool DIAG>
+__device__ __forceinline__ float softmax_p_row(const uint32_t (&v)[FA_BKV], float scale_log2, float nm, int kbase,
+                                               int qrow, uint32_t ts) {
+  const float2 sc = make_float2(scale_log2, scale_log2), sh = make_float2(nm, nm);
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < FA_BKV / 32; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      const float2 sv = make_float2(__uint_as_float(v[c * 32 + e]), __uint_as_float(v[c * 32 + e + 1]));
+      const float2 x = __ffma2_rn(sv, sc, sh);
+      float2 p;
+      if (((e >> 1) & 3) < FA_POLY_PAIRS) {
+        p = ex2_fma2(x);
+      } else {
+        p.x = ex2(x.x);
+        p.y = ex2(x.y);
+      }
+      if (DIAG) {
+        const int k0 = kbase + c * 32 + e;
+        if (k0 > qrow) p.x = 0.f;
+        if (k0 + 1 > qrow) p.y = 0.f;
+      }
+      if ((e >> 1) & 1) acc1 = __fadd2_rn(acc1, p);
+      else acc0 = __fadd2_rn(acc0, p);
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(p.x, p.y);
+      pk[e >> 1] = *reinterpret_cast<uint32_t*>(&t2);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            ts + c * 16),
+        "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7]), "r"(pk[8]),
+        "r"(pk[9]), "r"(pk[10]), "r"(pk[11]), "r"(pk[12]), "r"(pk[13]), "r"(pk[14]), "r"(pk[15])
+        : "memory");
+  }
+  return (acc0.x + acc0.y) + (acc1.x + acc1.y);
+}
+
+// Persistent: one CTA per SM walks pair tiles in a snake order over the heavy-first tile list
+// (causal tiles late in the sequence carry more KV blocks), so the per-CTA prologue (barrier
+// init, TMEM alloc, first loads) is paid once and the next tile's Q/K loads and first S MMA
+// overlap the previous tile's epilogue.
+struct FaTile {
+  int qp, h, b, nkv, last_a;
+};
+__device__ __forceinline__ int fa_tile_index(int it) {
+  const int G = gridDim.x, c = blockIdx.x;
+  return it * G + ((it & 1) ? (G - 1 - c) : c);
+}
+__device__ __forceinline__ FaTile fa_tile(int idx, int BH, int H, int n_qt, int seq, int causal) {
+  FaTile t;
+  t.qp = n_qt - 1 - idx / BH;  // heavy first
+  const int hb = idx % BH;
+  t.h = hb % H;
+  t.b = hb / H;
+  t.nkv = causal ? 2 * t.qp + 2 : seq / FA_BKV;  // blocks warpgroup B needs
+  t.last_a = causal ? 2 * t.qp : t.nkv - 1;       // last block warpgroup A needs
+  return t;
+}
+
 template <int D>
 __global__ void __launch_bounds__(FA_THREADS, 1)
     fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap qkv_map, bf16* __restrict__ out,
-                     float* __restrict__ lse, int seq, int H, int n_qt, float scale_log2,
+                     float* __restrict__ lse, int seq, int H, int BH, int n_qt, float scale_log2,
                      int causal) {
   using L = FaSmem<D>;
+  constexpr int KVS = L::KVS;
   extern __shared__ uint8_t smem_raw[];
+  long long* const dbg_ = blockIdx.x == 0 ? g_fa_dbg : nullptr;  // trace hook, read once
+  long long* const cta_t = g_fa_cta;
+  if (cta_t != nullptr && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    cta_t[3 * blockIdx.x] = static_cast<long long>(t);
+    cta_t[3 * blockIdx.x + 2] = smid;
+  }
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;   // [2]
-  uint64_t* k_empty = bar + 3;  // [2]
-  uint64_t* v_full = bar + 5;   // [2]
-  uint64_t* v_empty = bar + 7;  // [2]
-  uint64_t* s_full = bar + 9;   // [2] per warpgroup
-  uint64_t* s_empty = bar + 11; // [2]
-  uint64_t* p_full = bar + 13;  // [2]
-  uint64_t* pv_done = bar + 15; // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
-  float* xch = reinterpret_cast<float*>(sm + L::XCH);
+  uint64_t* q_empty = bar + 1;
+  uint64_t* k_full = bar + 2;          // [KVS]
+  uint64_t* k_empty = k_full + 4;      // [KVS]
+  uint64_t* v_full = k_empty + 4;      // [KVS]
+  uint64_t* v_empty = v_full + 4;      // [KVS]
+  uint64_t* s_full = v_empty + 4;      // [2] per warpgroup
+  uint64_t* p_full = s_full + 2;       // [2]
+  uint64_t* pv_done = p_full + 2;      // [2]
+  uint64_t* o_empty = pv_done + 2;     // [2] warpgroup has read O out of TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = n_qt - 1 - static_cast<int>(blockIdx.x % n_qt);  // heavy (late) tiles first
-  const int hb = static_cast<int>(blockIdx.x / n_qt);
-  const int h = hb % H, b = hb / H;
-  const int nkv = causal ? qt + 1 : seq / FA_BKV;
-  const int row0 = b * seq;
+  const int ntiles = n_qt * BH;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&qkv_map);
     ptx::mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    ptx::mbar_init(q_empty, 1);
+    for (int s = 0; s < KVS; ++s) {
       ptx::mbar_init(&k_full[s], 1);
       ptx::mbar_init(&k_empty[s], 1);
       ptx::mbar_init(&v_full[s], 1);
       ptx::mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_empty[s], 128);
       ptx::mbar_init(&p_full[s], 128);
       ptx::mbar_init(&pv_done[s], 1);
+      ptx::mbar_init(&o_empty[s], 128);
     }
     ptx::fence_mbar_init();
   }
@@ -102,206 +199,226 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) FA_T(10, 0);
-
+  if (dbg_ != nullptr && threadIdx.x == 0) dbg_[10 * 64] = clock64();
+  // register split: the softmax warpgroups hold a whole 128-column S row in registers
+  // (setmaxnreg placed inside each role branch so it dominates that role's code)
   if (warp == 0) {
+    ptx::regs_dec<56>();
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(q_full, L::NB * TILE);
-      for (int c = 0; c < L::NB; ++c)
-        ptx::tma_load_2d(sm + L::Q + c * TILE, &qkv_map, q_full, h * D + 64 * c, row0 + qt * FA_BQ);
-      // K_j runs one block ahead of V_j: S_j needs K_j before PV_{j-1} needs V_{j-1}
-      for (int j = 0; j <= nkv; ++j) {
-        if (j < nkv) {
-          const int st = j & 1;
-          ptx::mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
-          FA_T(8, j);
-          ptx::mbar_arrive_expect_tx(&k_full[st], L::NB * TILE);
+      int kv = 0;  // KV blocks loaded by this CTA so far (ring position)
+      for (int it = 0;; ++it) {
+        const int idx = fa_tile_index(it);
+        if (idx >= ntiles) break;
+        const FaTile T = fa_tile(idx, BH, H, n_qt, seq, causal);
+        const int row0 = T.b * seq;
+        ptx::mbar_wait(q_empty, (it & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(q_full, 2 * L::NB * TILE);
+        for (int t = 0; t < 2; ++t)
           for (int c = 0; c < L::NB; ++c)
-            ptx::tma_load_2d(sm + L::K + (st * L::NB + c) * TILE, &qkv_map, &k_full[st],
-                             H * D + h * D + 64 * c, row0 + j * FA_BKV);
+            ptx::tma_load_2d(sm + L::Q + (t * L::NB + c) * TILE, &qkv_map, q_full, T.h * D + 64 * c,
+                             row0 + T.qp * FA_BQ + 128 * t);
+        // K_j runs ahead of V_j: S(j) needs K_j before PV(j) needs V_j
+        for (int j = 0; j <= T.nkv; ++j) {
+          if (j < T.nkv) {
+            const int g = kv + j, st = g % KVS;
+            ptx::mbar_wait(&k_empty[st], ((g / KVS) & 1) ^ 1);
+            if (it == 0) FA_T(8, j);
+            ptx::mbar_arrive_expect_tx(&k_full[st], L::NB * TILE);
+            for (int c = 0; c < L::NB; ++c)
+              ptx::tma_load_2d(sm + L::K + (st * L::NB + c) * TILE, &qkv_map, &k_full[st],
+                               H * D + T.h * D + 64 * c, row0 + j * FA_BKV);
+          }
+          if (j > 0) {
+            const int g = kv + j - 1, st = g % KVS;
+            ptx::mbar_wait(&v_empty[st], ((g / KVS) & 1) ^ 1);
+            if (it == 0) FA_T(9, j - 1);
+            ptx::mbar_arrive_expect_tx(&v_full[st], L::NB * TILE);
+            for (int c = 0; c < L::NB; ++c)
+              ptx::tma_load_2d(sm + L::V + (st * L::NB + c) * TILE, &qkv_map, &v_full[st],
+                               2 * H * D + T.h * D + 64 * c, row0 + (j - 1) * FA_BKV);
+          }
         }
-        if (j > 0) {
-          const int jj = j - 1, st = jj & 1;
-          ptx::mbar_wait(&v_empty[st], ((jj >> 1) & 1) ^ 1);
-          FA_T(9, jj);
-          ptx::mbar_arrive_expect_tx(&v_full[st], L::NB * TILE);
-          for (int c = 0; c < L::NB; ++c)
-            ptx::tma_load_2d(sm + L::V + (st * L::NB + c) * TILE, &qkv_map, &v_full[st],
-                             2 * H * D + h * D + 64 * c, row0 + jj * FA_BKV);
-        }
+        kv += T.nkv;
       }
     }
   } else if (warp == 1) {
+    ptx::regs_dec<56>();
     if (lane == 0) {
-      constexpr uint32_t id_s = ptx::idesc_bf16_f32(FA_BQ, FA_BKV, false, false);
-      constexpr uint32_t id_o = ptx::idesc_bf16_f32(FA_BQ, D, false, true);
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, FA_BKV, false, false);
+      constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, D, false, true);
       const uint32_t sq = ptx::smem_u32(sm + L::Q);
-      ptx::mbar_wait(q_full, 0);
-      for (int j = 0; j <= nkv; ++j) {
-        if (j < nkv) {
-          const int st = j & 1;  // K stage == S buffer == warpgroup
-          ptx::mbar_wait(&k_full[st], (j >> 1) & 1);
-          FA_T(0, j);
-          ptx::mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
-          FA_T(1, j);
-          ptx::tc_fence_after();
-          const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * TILE);
+      auto issue_s = [&](int w, int st) {  // S_w = Q_w K^T (K in ring stage st)
+        const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * TILE);
+        const uint32_t qw = sq + w * L::NB * TILE;
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * TILE + (kk & 3) * 32;
-            ptx::mma_bf16_ss(tmem + st * FA_BKV, ptx::umma_desc_sw128(sq + off, 16, 1024),
-                             ptx::umma_desc_sw128(sk + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&s_full[st]);
-          ptx::mma_commit(&k_empty[st]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * TILE + (kk & 3) * 32;
+          ptx::mma_bf16_ss(tmem + w * 128, ptx::umma_desc_sw128(qw + off, 16, 1024),
+                           ptx::umma_desc_sw128(sk + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
         }
-        if (j > 0) {
-          const int jj = j - 1, w = jj & 1;
-          ptx::mbar_wait(&v_full[w], (jj >> 1) & 1);
-          FA_T(2, jj);
-          ptx::mbar_wait(&p_full[w], (jj >> 1) & 1);
-          FA_T(3, jj);
-          ptx::tc_fence_after();
-          const uint32_t sv = ptx::smem_u32(sm + L::V + w * L::NB * TILE);
-          const uint32_t sp = ptx::smem_u32(sm + L::P + w * 2 * TILE);
+        ptx::mma_commit(&s_full[w]);
+      };
+      auto issue_pv = [&](int w, int st, bool first) {  // O_w += P_w V, P from TMEM
+        ptx::tc_fence_after();
+        const uint32_t sv = ptx::smem_u32(sm + L::V + st * L::NB * TILE);
 #pragma unroll
-          for (int kk = 0; kk < FA_BKV / 16; ++kk) {
-            ptx::mma_bf16_ss(tmem + 256 + w * 128,
-                             ptx::umma_desc_sw128(sp + (kk >> 2) * TILE + (kk & 3) * 32, 16, 1024),
-                             ptx::umma_desc_sw128(sv + kk * 2048, TILE, 1024), id_o,
-                             (jj >= 2 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < FA_BKV / 16; ++kk)
+          ptx::mma_bf16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8,
+                           ptx::umma_desc_sw128(sv + kk * 2048, TILE, 1024), id_o, (!first || kk > 0) ? 1u : 0u);
+        ptx::mma_commit(&pv_done[w]);
+      };
+      int kv = 0, na = 0, nb = 0;  // KV blocks / A blocks / B blocks issued so far
+      for (int it = 0;; ++it) {
+        const int idx = fa_tile_index(it);
+        if (idx >= ntiles) break;
+        const FaTile T = fa_tile(idx, BH, H, n_qt, seq, causal);
+        ptx::mbar_wait(q_full, it & 1);
+        for (int j = 0; j <= T.nkv; ++j) {
+          if (j < T.nkv) {
+            const int g = kv + j;
+            ptx::mbar_wait(&k_full[g % KVS], (g / KVS) & 1);
+            if (it == 0) FA_T(0, j);
+            ptx::tc_fence_after();
+            if (j <= T.last_a) issue_s(0, g % KVS);
           }
-          ptx::mma_commit(&pv_done[w]);
-          ptx::mma_commit(&v_empty[w]);
+          if (j > 0) {  // PV_B(j-1)
+            const int g = kv + j - 1;
+            ptx::mbar_wait(&v_full[g % KVS], (g / KVS) & 1);
+            if (j == 1) ptx::mbar_wait(&o_empty[1], (it & 1) ^ 1);  // O_B of the previous tile read out
+            ptx::mbar_wait(&p_full[1], (nb + j - 1) & 1);
+            if (it == 0) FA_T(4, j - 1);
+            issue_pv(1, g % KVS, j == 1);
+            ptx::mma_commit(&v_empty[g % KVS]);  // PV_A(j-1) was issued before PV_B(j-1)
+          }
+          if (j < T.nkv) {
+            const int g = kv + j;
+            // start B's first softmax only once A's is done: the two warpgroups then keep
+            // alternating between the MUFU and the tensor core instead of sharing both
+            if (j == 0) ptx::mbar_wait(&p_full[0], na & 1);
+            issue_s(1, g % KVS);
+            ptx::mma_commit(&k_empty[g % KVS]);
+            if (j == T.nkv - 1) ptx::mma_commit(q_empty);  // last read of this tile's Q
+            if (j <= T.last_a) {
+              ptx::mbar_wait(&v_full[g % KVS], (g / KVS) & 1);
+              if (j == 0) ptx::mbar_wait(&o_empty[0], (it & 1) ^ 1);
+              ptx::mbar_wait(&p_full[0], (na + j) & 1);
+              if (it == 0) FA_T(3, j);
+              issue_pv(0, g % KVS, j == 0);
+            }
+          }
         }
+        kv += T.nkv;
+        na += T.last_a + 1;
+        nb += T.nkv;
       }
     }
   } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;      // softmax warpgroup: KV blocks j = wg, wg + 2, ...
-    const int q = warp & 3;              // TMEM lane quadrant
-    const int r = q * 32 + lane;         // query row within the tile
-    const int qrow = qt * FA_BQ + r;
+    ptx::regs_inc<224>();
+    const int wg = (warp - 4) >> 2;  // 0: rows 0-127 (A), 1: rows 128-255 (B)
+    const int q = warp & 3;          // TMEM lane quadrant
+    const int r = q * 32 + lane;
     const uint32_t lanes = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const uint32_t ts = lanes + wg * FA_BKV;
+    const uint32_t ts = lanes + wg * 128;
     const uint32_t to = lanes + 256 + wg * 128;
-    uint8_t* sp = sm + L::P + wg * 2 * TILE;
-    float m_ref = -INFINITY, l = 0.f;
-    int it = 0;
-    for (int j = wg; j < nkv; j += 2, ++it) {
-      const bool diag = causal && j == qt;
-      ptx::mbar_wait(&s_full[wg], it & 1);
-      if (lane == 0 && (warp & 3) == 0) FA_T(4, j);
-      ptx::tc_fence_after();
-      // pass 1: row max of the raw scores (scale > 0 commutes with max)
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < FA_BKV / 32; ++c) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(ts + c * 32, v);
-        ptx::tmem_ld_wait();
-        if (diag) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (j * FA_BKV + c * 32 + e <= qrow) mx = fmaxf(mx, __uint_as_float(v[e]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(v[e]), __uint_as_float(v[e + 1])));
-        }
-      }
-      const float m_new = fmaxf(m_ref, mx * scale_log2);
-      if (lane == 0 && (warp & 3) == 0) FA_T(5, j);
-      if (it > 0) ptx::mbar_wait(&pv_done[wg], (it - 1) & 1);  // P[wg] free, O[wg] settled
-      if (lane == 0 && (warp & 3) == 0) FA_T(6, j);
-      if (it == 0) {
-        m_ref = m_new;
-      } else if (__any_sync(0xffffffffu, m_new > m_ref + 8.f)) {  // warp-collective TMEM ops
-        const float alpha = ex2(m_ref - m_new);
+    int nbase = 0;  // blocks this warpgroup processed in earlier tiles (barrier phases)
+    for (int it = 0;; ++it) {
+      const int idx = fa_tile_index(it);
+      if (idx >= ntiles) break;
+      const FaTile T = fa_tile(idx, BH, H, n_qt, seq, causal);
+      const int qrow = T.qp * FA_BQ + 128 * wg + r;
+      const int nblk = wg == 0 ? T.last_a + 1 : T.nkv;
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < nblk; ++j) {
+        const bool diag = causal && j == nblk - 1;
+        ptx::mbar_wait(&s_full[wg], (nbase + j) & 1);  // also implies PV_wg(j-1) retired: O settled
+        if (it == 0 && lane == 0 && q == 0) FA_T(5 + wg, j);
         ptx::tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          uint32_t o[32];
-          ptx::tmem_ld_32x32b_x32(to + c * 32, o);
-          ptx::tmem_ld_wait();
+        // one pass over S: all 128 columns of this thread's row into registers
+        uint32_t v[FA_BKV];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          ptx::tmem_st_32x32b_x32(to + c * 32, o);
-        }
-        ptx::tmem_st_wait();
-        l *= alpha;
-        m_ref = m_new;
-      }
-      const float nm = -m_ref;
-      // pass 2: P = 2^(s*scale - m) -> bf16 -> swizzled smem
-#pragma unroll
-      for (int c = 0; c < FA_BKV / 32; ++c) {
-        uint32_t v[32];
-        ptx::tmem_ld_32x32b_x32(ts + c * 32, v);
+        for (int c = 0; c < FA_BKV / 32; ++c)
+          ptx::tmem_ld_32x32b_x32(ts + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[c * 32]));
         ptx::tmem_ld_wait();
-        uint32_t pk[16];
+        float mx;
+        {  // 8 independent max chains (a single chain is 64 dependent FMNMX deep)
+          float m8[8];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p0 = ex2(fmaf(__uint_as_float(v[e]), scale_log2, nm));
-          float p1 = ex2(fmaf(__uint_as_float(v[e + 1]), scale_log2, nm));
+          for (int t = 0; t < 8; ++t) m8[t] = -INFINITY;
           if (diag) {
-            const int k0 = j * FA_BKV + c * 32 + e;
-            if (k0 > qrow) p0 = 0.f;
-            if (k0 + 1 > qrow) p1 = 0.f;
-          }
-          l += p0 + p1;
-          __nv_bfloat162 t2 = __floats2bfloat162_rn(p0, p1);
-          pk[e >> 1] = *reinterpret_cast<uint32_t*>(&t2);
-        }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          *reinterpret_cast<uint4*>(sp + (c >> 1) * TILE + ptx::sw128_offset(r, (c & 1) * 4 + u)) =
-              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            for (int e = 0; e < FA_BKV; ++e)
+              if (j * FA_BKV + e <= qrow) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(v[e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < FA_BKV; e += 16)
+#pragma unroll
+              for (int t = 0; t < 8; ++t)
+                m8[t] = fmaxf(m8[t], fmaxf(__uint_as_float(v[e + t]), __uint_as_float(v[e + 8 + t])));
+          }
+          mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        }
+        const float m_new = fmaxf(m_ref, mx * scale_log2);
+        if (it == 0 && lane == 0 && q == 0 && wg == 0) FA_T(12, j);
+        if (j == 0) {
+          m_ref = m_new;
+        } else if (__any_sync(0xffffffffu, m_new > m_ref + 8.f)) {  // warp-collective TMEM ops
+          const float alpha = ex2(m_ref - m_new);
+#pragma unroll 1
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld_32x32b_x32(to + c * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            ptx::tmem_st_32x32b_x32(to + c * 32, o);
+          }
+          l *= alpha;
+          m_ref = m_new;
+        }
+        const float nm = -m_ref;
+        if (diag) l += softmax_p_row<true>(v, scale_log2, nm, j * FA_BKV, qrow, ts);
+        else l += softmax_p_row<false>(v, scale_log2, nm, j * FA_BKV, qrow, ts);
+        if (it == 0 && lane == 0 && q == 0 && wg == 0) FA_T(13, j);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[wg]);
+        if (it == 0 && lane == 0 && q == 0) FA_T(1 + wg, j);
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&s_empty[wg]);
-      ptx::fence_proxy_async_smem();
-      ptx::mbar_arrive(&p_full[wg]);
-      if (lane == 0 && (warp & 3) == 0) FA_T(7, j);
-    }
-    // drain this warpgroup's last PV
-    if (it > 0) ptx::mbar_wait(&pv_done[wg], (it - 1) & 1);
-    ptx::tc_fence_after();
-    // merge the two halves: warpgroup 1 hands (m, l) to warpgroup 0 through smem
-    if (wg == 1) {
-      xch[r] = m_ref;
-      xch[128 + r] = l;
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (wg == 0) {
-      const bool has1 = nkv > 1;
-      const float m1 = has1 ? xch[r] : -INFINITY, l1 = has1 ? xch[128 + r] : 0.f;
-      const float m = fmaxf(m_ref, m1);
-      const float a0 = ex2(m_ref - m), a1 = has1 ? ex2(m1 - m) : 0.f;
-      const float inv = 1.f / (l * a0 + l1 * a1);
-      const float c0 = a0 * inv, c1 = a1 * inv;
-      bf16* orow = out + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(H) * D) + h * D;
+      ptx::mbar_wait(&pv_done[wg], (nbase + nblk - 1) & 1);
+      ptx::tc_fence_after();
+      const float inv = 1.f / l;
+      bf16* orow = out + (static_cast<size_t>(T.b) * seq + qrow) * (static_cast<size_t>(H) * D) + T.h * D;
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
-        uint32_t o0[32], o1[32];
-        ptx::tmem_ld_32x32b_x32(lanes + 256 + c * 32, o0);
-        ptx::tmem_ld_32x32b_x32(lanes + 384 + c * 32, o1);
+        uint32_t o[32];
+        ptx::tmem_ld_32x32b_x32(to + c * 32, o);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           float f[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            f[e] = __uint_as_float(o0[8 * u + e]) * c0 + (has1 ? __uint_as_float(o1[8 * u + e]) * c1 : 0.f);
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(o[8 * u + e]) * inv;
           store8(orow + c * 32 + 8 * u, f);
         }
       }
-      lse[(static_cast<size_t>(b) * H + h) * seq + qrow] = m + log2f(l * a0 + l1 * a1);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&o_empty[wg]);
+      lse[(static_cast<size_t>(T.b) * H + T.h) * seq + qrow] = m_ref + log2f(l);
+      nbase += nblk;
     }
+  } else {
+    ptx::regs_dec<56>();
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
+  }
+  if (cta_t != nullptr && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    cta_t[3 * blockIdx.x + 1] = static_cast<long long>(t);
   }
 }
 
@@ -321,13 +438,14 @@ int launch_fa_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, i
   }
   const int n_qt = S / FA_BQ;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
-  k<<<n_qt * H * B, FA_THREADS, smem, st>>>(map, out, lse, S, H, n_qt, scale_log2, causal);
+  const int grid = std::min(n_qt * H * B, num_sms());
+  k<<<grid, FA_THREADS, smem, st>>>(map, out, lse, S, H, H * B, n_qt, scale_log2, causal);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// Used by amdp_attention_fwd when the tensor-core path applies.
+// Used by amdp_attention_fwd when the tensor-core path applies (seq % 256 == 0).
 int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int D, int causal,
                      cudaStream_t st) {
   if (S % FA_BQ != 0) return AMDP_ERR_UNSUPPORTED;
@@ -338,7 +456,10 @@ int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H
 
 }  // namespace amdp
 
-// Diagnostics hook (see g_fa_dbg): device buffer of >= 11 * 64 int64, or NULL to disable.
+// Diagnostics hook (see g_fa_dbg): device buffer of >= 16 * 64 int64, or NULL to disable.
 extern "C" int amdp_debug_attention_trace(long long* device_buf) {
   return cudaMemcpyToSymbol(amdp::g_fa_dbg, &device_buf, sizeof(device_buf));
+}
+extern "C" int amdp_debug_attention_cta_times(long long* device_buf) {
+  return cudaMemcpyToSymbol(amdp::g_fa_cta, &device_buf, sizeof(device_buf));
 }
