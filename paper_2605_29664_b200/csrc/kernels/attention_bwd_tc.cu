@@ -1,17 +1,22 @@
 // Flash-attention backward on the 5th-generation tensor cores (sm_100a).
 //
 // Two deterministic kernels (no atomics), each with its accumulators in TMEM:
-//   dK/dV : one CTA per (128-key tile, head, sequence), looping over 64-query blocks:
-//           S^T = K Q_i^T, dP^T = V dO_i^T            (M=128 keys, N=64, K=D)
-//           P^T = 2^(S^T c - lse), dS^T = P^T (dP^T - delta)  (warps 4-7, thread = key)
-//           dV += P^T dO_i, dK += dS^T Q_i              (M=128, N=D, K=64)
-//   dQ    : one CTA per (128-query tile, head, sequence), looping over 64-key blocks:
-//           S = Q K_j^T, dP = dO V_j^T; dS = P (dP - delta); dQ += dS K_j
-// Every operand is in its natural layout: the same SWIZZLE_128B tile of Q, dO or K is
-// read K-major by one MMA and MN-major by another, P^T / dS^T / dS are written by the
-// softmax threads straight into the K-major swizzled layout the tensor core reads.
+//   dK/dV : one CTA per (128-key tile, head, sequence), looping over 64-query halves:
+//           S^T = K Q_i^T, dP^T = V dO_i^T                    (SS, M=128 keys, N=64 queries)
+//           P^T = 2^(S^T c - lse), dS^T = P^T (dP^T - delta)  (thread = key, one warpgroup
+//                                                              per half, overlapping the
+//                                                              other half's MMAs)
+//           dV += P^T dO_i, dK += dS^T Q_i                    (TS: P^T / dS^T from TMEM)
+//   dQ    : one CTA per (128-query tile, head, sequence), looping over 128-key blocks:
+//           S = Q K_j^T (TS, Q in TMEM), dP = dO V_j^T; dS = P (dP - delta); dQ += dS K_j (TS)
+//           dS goes to its own TMEM columns, so S/dP's TMEM frees as soon as the softmax
+//           threads have loaded it, letting S_{j+1} overlap the dS math of block j.
+// The backward softmax is elementwise given lse and delta, so the two softmax warpgroups
+// split each block by columns and no cross-thread reduction is needed.
+// tcgen05.mma issue blocks once ~5 MMAs are queued (the issuing thread runs at the pipe's
+// pace), so each kernel issues its MMA groups in the order their inputs become ready.
 // lse / delta use the forward's log2-domain convention (softmax scale folded in);
-// delta = rowsum(dO * O) comes from attn_bwd_delta_kernel (attention.cu).
+// delta = rowsum(dO * O) comes from attn_bwd_delta_vec_kernel (attention.cu).
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 #include "tma_host.hpp"
@@ -23,11 +28,10 @@ constexpr uint32_t T128 = 16384;  // [128 rows][64 bf16] SW128 tile
 
 // Diagnostics (amdp_debug_attention_bwd_trace): CTA 0 of the dQ kernel records clock64().
 __device__ long long* g_bw_dbg = nullptr;
-#define BW_T(slot, j)                                                                       \
-  do {                                                                                      \
+#define BW_T(slot, j)                                                   \
+  do {                                                                  \
     if (dbg_ != nullptr && (j) < 64) dbg_[(slot)*64 + (j)] = clock64(); \
   } while (0)
-constexpr uint32_t T64 = 8192;    // [64 rows][64 bf16]
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -38,275 +42,305 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&t);
 }
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+// Writes NCOLS fp32 TMEM columns of this thread's lane, times mul, as bf16 to dst.
+template <int NCOLS>
+__device__ __forceinline__ void tmem_row_to_global(uint32_t src, bf16* dst, float mul) {
+#pragma unroll 1
+  for (int c = 0; c < NCOLS / 32; ++c) {
+    uint32_t a[32];
+    ptx::tmem_ld_32x32b_x32(src + c * 32, a);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float f[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * u + e]) * mul;
+      store8(dst + c * 32 + 8 * u, f);
+    }
+  }
+}
 
 // ==================================================================== dK / dV
+// The 128-query block is processed as two 64-query halves a / b, one per softmax
+// warpgroup, with the MMAs interleaved so each half's softmax overlaps the other half's
+// tensor work:   dVdK_a(i) | S_a(i+1) | dVdK_b(i) | S_b(i+1) | ...   (S_x = S^T_x + dP^T_x)
+// Q / dO stream in half-block units through a 5-deep ring, so a unit's load starts ~3
+// half-block MMA groups ahead of its first use; lse / delta are read from L2 (broadcast).
+constexpr uint32_t T64 = 8192;  // [64 rows][64 bf16] SW128 tile
+
 template <int D>
 struct KvSmem {
   static constexpr int NB = D / 64;
+  static constexpr int NU = D == 128 ? 5 : 10;        // half-block units in flight
+  static constexpr uint32_t UNIT = 2 * NB * T64;      // Q half, dO half
   static constexpr uint32_t K = 0;
   static constexpr uint32_t V = K + NB * T128;
-  static constexpr int NS = 3;                   // Q / dO / lse / delta ring depth
-  static constexpr uint32_t Q = V + NB * T128;   // NS stages of NB x T64
-  static constexpr uint32_t DO = Q + NS * NB * T64;
-  static constexpr uint32_t PT = DO + NS * NB * T64;  // 2 warpgroups x [128 keys][64 q]
-  static constexpr uint32_t DST = PT + 2 * T128;
-  static constexpr uint32_t LD = DST + 2 * T128;  // NS stages x (64 lse + 64 delta) fp32
-  static constexpr uint32_t BAR = LD + NS * 512;
+  static constexpr uint32_t U = V + NB * T128;        // NU units
+  static constexpr uint32_t BAR = U + NU * UNIT;
   static constexpr uint32_t BYTES = BAR + 256;
-  static constexpr uint32_t TMEM_COLS = 512;
 };
 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
-    fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap qkv128, const __grid_constant__ CUtensorMap qkv64,
-                       const __grid_constant__ CUtensorMap do64, const float* __restrict__ lse,
-                       const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int H, int n_kt,
-                       float scale_log2, float scale, int causal) {
+    fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap kv_map, const __grid_constant__ CUtensorMap qkv_map,
+                       const __grid_constant__ CUtensorMap do_map, const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
+                       int seq, int H, int n_kt, float scale_log2, float scale, int causal) {
   using L = KvSmem<D>;
+  constexpr int NU = L::NU;
   extern __shared__ uint8_t smem_raw[];
-  long long* const dbg_ = blockIdx.x == 0 ? g_bw_dbg : nullptr;  // trace hook, read once
+  long long* const dbg_ = blockIdx.x == 0 && g_bw_dbg != nullptr ? g_bw_dbg + 16 * 64 : nullptr;  // trace hook
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  constexpr int NS = L::NS;
   uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;   // [NS]
-  uint64_t* q_empty = bar + 5;  // [NS]
-  uint64_t* s_full = bar + 9;   // [2] per warpgroup
-  uint64_t* s_empty = bar + 11; // [2]
-  uint64_t* p_full = bar + 13;  // [2]
-  uint64_t* pd_done = bar + 15; // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  uint64_t* u_full = bar + 1;        // [NU]
+  uint64_t* u_empty = u_full + 10;   // [NU]
+  uint64_t* s_full = u_empty + 10;   // [2] per half
+  uint64_t* p_full = s_full + 2;     // [2] 128 arrivals: P^T / dS^T of the half in TMEM
+  uint64_t* kv_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kt = static_cast<int>(blockIdx.x % n_kt);  // causal: small kt = most work, first
   const int hb = static_cast<int>(blockIdx.x / n_kt);
   const int h = hb % H, b = hb / H;
   const int row0 = b * seq;
-  const int nqb = seq / 64;
-  const int i0 = causal ? 2 * kt : 0;
-  const int N = nqb - i0;
+  const int nqb = seq / 128;
+  const int i0 = causal ? kt : 0;
+  const int N = nqb - i0;  // 128-query blocks; 2N half-block units
   const float* lse_bh = lse + (static_cast<size_t>(b) * H + h) * seq;
   const float* del_bh = delta + (static_cast<size_t>(b) * H + h) * seq;
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch(&qkv128);
-    ptx::tma_prefetch(&qkv64);
-    ptx::tma_prefetch(&do64);
+    ptx::tma_prefetch(&kv_map);
+    ptx::tma_prefetch(&qkv_map);
+    ptx::tma_prefetch(&do_map);
     ptx::mbar_init(kv_full, 1);
-    for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(&q_full[s], 1);
-      ptx::mbar_init(&q_empty[s], 1);
+    for (int s = 0; s < NU; ++s) {
+      ptx::mbar_init(&u_full[s], 1);
+      ptx::mbar_init(&u_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_empty[s], 128);
       ptx::mbar_init(&p_full[s], 128);
-      ptx::mbar_init(&pd_done[s], 1);
     }
+    ptx::mbar_init(kv_done, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S^T_w at 128w, dP^T_w at 128w + 64 (w = warpgroup), dV at 256, dK at 256 + D
+  // TMEM: S^T_a at 0, S^T_b at 64 (P^T_x bf16 pairs over their first 32 columns),
+  // dP^T_a at 128, dP^T_b at 192 (dS^T_x likewise), dV at 256, dK at 256 + D
   const uint32_t t_dv = tmem + 256, t_dk = tmem + 256 + D;
 
   if (warp == 0) {
+    ptx::regs_dec<56>();
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(kv_full, 2 * L::NB * T128);
       for (int c = 0; c < L::NB; ++c) {
-        ptx::tma_load_2d(sm + L::K + c * T128, &qkv128, kv_full, H * D + h * D + 64 * c, row0 + kt * 128);
-        ptx::tma_load_2d(sm + L::V + c * T128, &qkv128, kv_full, 2 * H * D + h * D + 64 * c, row0 + kt * 128);
+        ptx::tma_load_2d(sm + L::K + c * T128, &kv_map, kv_full, H * D + h * D + 64 * c, row0 + kt * 128);
+        ptx::tma_load_2d(sm + L::V + c * T128, &kv_map, kv_full, 2 * H * D + h * D + 64 * c, row0 + kt * 128);
       }
-      for (int n = 0; n < N; ++n) {
-        const int st = n % NS, i = i0 + n;
-        ptx::mbar_wait(&q_empty[st], ((n / NS) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&q_full[st], 2 * L::NB * T64 + 512);
+      for (int u = 0; u < 2 * N; ++u) {
+        const int st = u % NU, q0 = i0 * 128 + u * 64;
+        uint8_t* unit = sm + L::U + st * L::UNIT;
+        ptx::mbar_wait(&u_empty[st], ((u / NU) & 1) ^ 1);
+        BW_T(6, u);
+        ptx::mbar_arrive_expect_tx(&u_full[st], L::UNIT);
         for (int c = 0; c < L::NB; ++c) {
-          ptx::tma_load_2d(sm + L::Q + (st * L::NB + c) * T64, &qkv64, &q_full[st], h * D + 64 * c, row0 + i * 64);
-          ptx::tma_load_2d(sm + L::DO + (st * L::NB + c) * T64, &do64, &q_full[st], h * D + 64 * c, row0 + i * 64);
+          ptx::tma_load_2d(unit + c * T64, &qkv_map, &u_full[st], h * D + 64 * c, row0 + q0);
+          ptx::tma_load_2d(unit + (L::NB + c) * T64, &do_map, &u_full[st], h * D + 64 * c, row0 + q0);
         }
-        ptx::bulk_load(sm + L::LD + st * 512, lse_bh + i * 64, 256, &q_full[st]);
-        ptx::bulk_load(sm + L::LD + st * 512 + 256, del_bh + i * 64, 256, &q_full[st]);
       }
     }
   } else if (warp == 1) {
+    ptx::regs_dec<56>();
     if (lane == 0) {
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t id_g = ptx::idesc_bf16_f32(128, D, false, true);
       const uint32_t sk = ptx::smem_u32(sm + L::K), sv = ptx::smem_u32(sm + L::V);
+      auto unit = [&](int u) { return ptx::smem_u32(sm + L::U + (u % NU) * L::UNIT); };
+      // S^T_x, dP^T_x of half-unit u (x = u & 1) into columns 64x / 128 + 64x
+      auto issue_s = [&](int u) {
+        const int x = u & 1;
+        ptx::mbar_wait(&u_full[u % NU], (u / NU) & 1);
+        BW_T(0, u);
+        ptx::tc_fence_after();
+        const uint32_t sq = unit(u), sdo = sq + L::NB * T64;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * T128 + (kk & 3) * 32, ob = (kk >> 2) * T64 + (kk & 3) * 32;
+          ptx::mma_bf16_ss(tmem + 64 * x, ptx::umma_desc_sw128(sk + oa, 16, 1024),
+                           ptx::umma_desc_sw128(sq + ob, 16, 1024), id_s, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * T128 + (kk & 3) * 32, ob = (kk >> 2) * T64 + (kk & 3) * 32;
+          ptx::mma_bf16_ss(tmem + 128 + 64 * x, ptx::umma_desc_sw128(sv + oa, 16, 1024),
+                           ptx::umma_desc_sw128(sdo + ob, 16, 1024), id_s, kk > 0);
+        }
+        ptx::mma_commit(&s_full[x]);
+        BW_T(1, u);
+      };
+      // dV += P^T_x dO_x, dK += dS^T_x Q_x (K = 64 queries; P^T / dS^T from TMEM)
+      auto issue_g = [&](int u) {
+        const int x = u & 1;
+        ptx::mbar_wait(&p_full[x], (u >> 1) & 1);
+        BW_T(2, u);
+        ptx::tc_fence_after();
+        const uint32_t sq = unit(u), sdo = sq + L::NB * T64;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma_bf16_ts(t_dv, tmem + 64 * x + kk * 8, ptx::umma_desc_sw128(sdo + kk * 2048, T64, 1024), id_g,
+                           (u > 0 || kk > 0));
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          ptx::mma_bf16_ts(t_dk, tmem + 128 + 64 * x + kk * 8, ptx::umma_desc_sw128(sq + kk * 2048, T64, 1024), id_g,
+                           (u > 0 || kk > 0));
+        ptx::mma_commit(&u_empty[u % NU]);
+        BW_T(3, u);
+      };
       ptx::mbar_wait(kv_full, 0);
-      for (int n = 0; n <= N; ++n) {
-        if (n < N) {
-          const int st = n % NS, w = n & 1;
-          const uint32_t t_st = tmem + 128 * w, t_dpt = t_st + 64;
-          ptx::mbar_wait(&q_full[st], (n / NS) & 1);
-          ptx::mbar_wait(&s_empty[w], ((n >> 1) & 1) ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t sq = ptx::smem_u32(sm + L::Q + st * L::NB * T64);
-          const uint32_t sdo = ptx::smem_u32(sm + L::DO + st * L::NB * T64);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t oa = (kk >> 2) * T128 + (kk & 3) * 32, ob = (kk >> 2) * T64 + (kk & 3) * 32;
-            ptx::mma_bf16_ss(t_st, ptx::umma_desc_sw128(sk + oa, 16, 1024), ptx::umma_desc_sw128(sq + ob, 16, 1024),
-                             id_s, kk > 0);
-            ptx::mma_bf16_ss(t_dpt, ptx::umma_desc_sw128(sv + oa, 16, 1024),
-                             ptx::umma_desc_sw128(sdo + ob, 16, 1024), id_s, kk > 0);
-          }
-          ptx::mma_commit(&s_full[w]);
-        }
-        if (n > 0) {
-          const int m = n - 1, st = m % NS, w = m & 1;
-          ptx::mbar_wait(&p_full[w], (m >> 1) & 1);
-          ptx::tc_fence_after();
-          const uint32_t sq = ptx::smem_u32(sm + L::Q + st * L::NB * T64);
-          const uint32_t sdo = ptx::smem_u32(sm + L::DO + st * L::NB * T64);
-          const uint32_t spt = ptx::smem_u32(sm + L::PT + w * T128), sdst = ptx::smem_u32(sm + L::DST + w * T128);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // K = 64 queries
-            ptx::mma_bf16_ss(t_dv, ptx::umma_desc_sw128(spt + kk * 32, 16, 1024),
-                             ptx::umma_desc_sw128(sdo + kk * 2048, T64, 1024), id_g, (m > 0 || kk > 0));
-            ptx::mma_bf16_ss(t_dk, ptx::umma_desc_sw128(sdst + kk * 32, 16, 1024),
-                             ptx::umma_desc_sw128(sq + kk * 2048, T64, 1024), id_g, (m > 0 || kk > 0));
-          }
-          ptx::mma_commit(&pd_done[w]);
-          ptx::mma_commit(&q_empty[st]);
-        }
+      const int U = 2 * N;
+      issue_s(0);
+      if (U > 1) issue_s(1);
+      for (int u = 0; u < U; ++u) {  // dVdK(u) | S(u + 2): S(u+2) reuses the columns dVdK(u) reads
+        issue_g(u);
+        if (u + 2 < U) issue_s(u + 2);
       }
+      ptx::mma_commit(kv_done);
     }
   } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;  // blocks n = wg, wg + 2, ...
+    ptx::regs_inc<224>();
+    const int x = (warp - 4) >> 2;  // half: queries [64 x, 64 x + 64) of every block
     const int q = warp & 3;
     const int r = q * 32 + lane;  // key row within the tile
     const int key = kt * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
-    const uint32_t t_st = tmem + 128 * wg, t_dpt = t_st + 64;
-    int it = 0;
-    for (int n = wg; n < N; n += 2, ++it) {
-      const int st = n % NS, i = i0 + n;
-      const bool diag = causal && i < i0 + 2;
-      ptx::mbar_wait(&q_full[st], (n / NS) & 1);  // lse / delta of this block visible
-      ptx::mbar_wait(&s_full[wg], it & 1);
+    const uint32_t t_s = tmem + lanes + 64 * x, t_d = tmem + 128 + lanes + 64 * x;
+    const float2 c2 = make_float2(scale_log2, scale_log2);
+    for (int n = 0; n < N; ++n) {
+      const int u = 2 * n + x;
+      const int qbase = (i0 + n) * 128 + 64 * x;
+      const bool diag = causal && n == 0;
+      float4 lq4[16], dq4[16];  // this half's 64 lse / delta (same address across the warp)
+#pragma unroll
+      for (int c4 = 0; c4 < 16; ++c4) {
+        lq4[c4] = __ldg(reinterpret_cast<const float4*>(lse_bh + qbase) + c4);
+        dq4[c4] = __ldg(reinterpret_cast<const float4*>(del_bh + qbase) + c4);
+      }
+      ptx::mbar_wait(&s_full[x], n & 1);
+      if (threadIdx.x == 128) BW_T(4, u);
       ptx::tc_fence_after();
-      uint32_t s0[32], s1[32], d0[32], d1[32];
-      ptx::tmem_ld_32x32b_x32(t_st + lanes, s0);
-      ptx::tmem_ld_32x32b_x32(t_st + lanes + 32, s1);
-      ptx::tmem_ld_32x32b_x32(t_dpt + lanes, d0);
-      ptx::tmem_ld_32x32b_x32(t_dpt + lanes + 32, d1);
+      uint32_t s[64], d[64];
+      ptx::tmem_ld_32x32b_x32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      ptx::tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      ptx::tmem_ld_32x32b_x32(t_d, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
+      ptx::tmem_ld_32x32b_x32(t_d + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
       ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&s_empty[wg]);
-      const float4* ls4 = reinterpret_cast<const float4*>(sm + L::LD + st * 512);
       uint32_t pp[32], dd[32];
 #pragma unroll
       for (int c4 = 0; c4 < 16; ++c4) {
-        const float4 lq = ls4[c4], dq = ls4[16 + c4];
-        const float lv[4] = {lq.x, lq.y, lq.z, lq.w}, dv[4] = {dq.x, dq.y, dq.z, dq.w};
-        float p[4], g[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int cc = 4 * c4 + u;
-          const float s = __uint_as_float(cc < 32 ? s0[cc] : s1[cc - 32]);
-          const float dp = __uint_as_float(cc < 32 ? d0[cc] : d1[cc - 32]);
-          p[u] = ex2(fmaf(s, scale_log2, -lv[u]));
-          g[u] = dp - dv[u];
+        const float4 lq = lq4[c4], dq = dq4[c4];
+        const int cc = 4 * c4;
+        float2 x0 = __ffma2_rn(make_float2(__uint_as_float(s[cc]), __uint_as_float(s[cc + 1])), c2,
+                               make_float2(-lq.x, -lq.y));
+        float2 x1 = __ffma2_rn(make_float2(__uint_as_float(s[cc + 2]), __uint_as_float(s[cc + 3])), c2,
+                               make_float2(-lq.z, -lq.w));
+        float2 p0 = make_float2(ex2(x0.x), ex2(x0.y)), p1 = make_float2(ex2(x1.x), ex2(x1.y));
+        if (diag) {  // query < key is masked
+          if (qbase + cc < key) p0.x = 0.f;
+          if (qbase + cc + 1 < key) p0.y = 0.f;
+          if (qbase + cc + 2 < key) p1.x = 0.f;
+          if (qbase + cc + 3 < key) p1.y = 0.f;
         }
-        if (diag) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            if (i * 64 + 4 * c4 + u < key) p[u] = 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) g[u] *= p[u];
-        pp[2 * c4] = pack2(p[0], p[1]);
-        pp[2 * c4 + 1] = pack2(p[2], p[3]);
-        dd[2 * c4] = pack2(g[0], g[1]);
-        dd[2 * c4 + 1] = pack2(g[2], g[3]);
+        const float2 g0 = __fmul2_rn(
+            __fadd2_rn(make_float2(__uint_as_float(d[cc]), __uint_as_float(d[cc + 1])), make_float2(-dq.x, -dq.y)), p0);
+        const float2 g1 = __fmul2_rn(
+            __fadd2_rn(make_float2(__uint_as_float(d[cc + 2]), __uint_as_float(d[cc + 3])), make_float2(-dq.z, -dq.w)),
+            p1);
+        pp[2 * c4] = pack2(p0.x, p0.y);
+        pp[2 * c4 + 1] = pack2(p1.x, p1.y);
+        dd[2 * c4] = pack2(g0.x, g0.y);
+        dd[2 * c4 + 1] = pack2(g1.x, g1.y);
       }
-      if (it > 0) ptx::mbar_wait(&pd_done[wg], (it - 1) & 1);  // previous P^T / dS^T consumed
-      uint8_t* spt = sm + L::PT + wg * T128;
-      uint8_t* sdst = sm + L::DST + wg * T128;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const uint32_t off = ptx::sw128_offset(r, u);
-        *reinterpret_cast<uint4*>(spt + off) = make_uint4(pp[4 * u], pp[4 * u + 1], pp[4 * u + 2], pp[4 * u + 3]);
-        *reinterpret_cast<uint4*>(sdst + off) = make_uint4(dd[4 * u], dd[4 * u + 1], dd[4 * u + 2], dd[4 * u + 3]);
-      }
-      ptx::fence_proxy_async_smem();
-      ptx::mbar_arrive(&p_full[wg]);
+      if (threadIdx.x == 128) BW_T(5, u);
+      // P^T_x / dS^T_x (bf16 pairs) over the first 32 columns of this half's S^T / dP^T
+      tmem_st_x16(t_s, pp);
+      tmem_st_x16(t_s + 16, pp + 16);
+      tmem_st_x16(t_d, dd);
+      tmem_st_x16(t_d + 16, dd + 16);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&p_full[x]);
+      if (threadIdx.x == 128) BW_T(7, u);
     }
-    if (it > 0) ptx::mbar_wait(&pd_done[wg], (it - 1) & 1);
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // both warpgroups drained: dK, dV final
+    ptx::mbar_wait(kv_done, 0);
     ptx::tc_fence_after();
     // warpgroup 0 writes dK, warpgroup 1 writes dV
     const size_t ld = static_cast<size_t>(3) * H * D;
-    bf16* dst = dqkv + (static_cast<size_t>(row0) + key) * ld + (wg == 0 ? H * D : 2 * H * D) + h * D;
-    const uint32_t src = (wg == 0 ? t_dk : t_dv) + lanes;
-    const float mul = wg == 0 ? scale : 1.f;
-#pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t a[32];
-      ptx::tmem_ld_32x32b_x32(src + c * 32, a);
-      ptx::tmem_ld_wait();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float f[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * u + e]) * mul;
-        store8(dst + c * 32 + 8 * u, f);
-      }
-    }
+    bf16* dst = dqkv + (static_cast<size_t>(row0) + key) * ld + (x == 0 ? H * D : 2 * H * D) + h * D;
+    tmem_row_to_global<D>((x == 0 ? t_dk : t_dv) + lanes, dst, x == 0 ? scale : 1.f);
+  } else {
+    ptx::regs_dec<56>();
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<L::TMEM_COLS>(tmem);
+    ptx::tmem_dealloc<512>(tmem);
   }
 }
 
 // ==================================================================== dQ
-// dS never touches shared memory: the softmax threads write it (bf16) over the TMEM
-// columns of the S tile they just read, and dQ += dS K_j reads it as the TMEM A operand
-// (tcgen05 "TS" form).  Three S/dP TMEM buffers let S_{n+1} issue while dQ_{n-1} is still
-// reading buffer n-1; the freed smem goes into a 5-deep K/V TMA ring (TMA latency on this
-// path is ~3-5k cycles, profiles/r01_attn_fwd_trace.txt).
 template <int D>
 struct QSmem {
   static constexpr int NB = D / 64;
-  static constexpr int NS = D == 128 ? 5 : 8;     // K / V ring depth
-  static constexpr uint32_t Q = 0;
-  static constexpr uint32_t DO = Q + NB * T128;
-  static constexpr uint32_t K = DO + NB * T128;   // NS stages of NB x T64
-  static constexpr uint32_t V = K + NS * NB * T64;
-  static constexpr uint32_t BAR = V + NS * NB * T64;
+  // K is held from S(j) until dQ(j) (one block later), V only until dP(j): separate rings.
+  // Q lives in TMEM (S = Q K^T is a TS MMA), which frees the smem for a 4-deep K ring: K
+  // loads start ~3 blocks ahead of use, covering the ~3k-cycle TMA latency under load.
+  static constexpr int NSK = D == 128 ? 4 : 8, NSV = D == 128 ? 2 : 4;
+  static constexpr uint32_t DO = 0;
+  static constexpr uint32_t K = DO + NB * T128;   // NSK stages of NB x T128
+  static constexpr uint32_t V = K + NSK * NB * T128;
+  static constexpr uint32_t BAR = V + NSV * NB * T128;
   static constexpr uint32_t BYTES = BAR + 256;
-  static constexpr uint32_t TMEM_COLS = 512;
 };
 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
-    fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap qkv128, const __grid_constant__ CUtensorMap qkv64,
-                     const __grid_constant__ CUtensorMap do128, const float* __restrict__ lse,
-                     const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int H, int n_qt,
-                     float scale_log2, float scale, int causal) {
+    fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap qkv_map, const __grid_constant__ CUtensorMap do_map,
+                     const bf16* __restrict__ qkv, const float* __restrict__ lse, const float* __restrict__ delta,
+                     bf16* __restrict__ dqkv, int seq, int H, int n_qt, float scale_log2, float scale, int causal) {
   using L = QSmem<D>;
-  constexpr int NS = L::NS;
+  constexpr int NSK = L::NSK, NSV = L::NSV;
   extern __shared__ uint8_t smem_raw[];
   long long* const dbg_ = blockIdx.x == 0 ? g_bw_dbg : nullptr;  // trace hook, read once
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;        // [NS]
-  uint64_t* kv_empty = kv_full + 8;   // [NS]
-  uint64_t* s_full = kv_empty + 8;    // [3] TMEM S/dP buffers
-  uint64_t* s_empty = s_full + 3;     // [3]
-  uint64_t* p_full = s_empty + 3;     // [2] per warpgroup: dS written
-  uint64_t* dq_done = p_full + 2;
+  uint64_t* q_full = bar + 0;          // 256 arrivals: Q rows stored into TMEM
+  uint64_t* do_full = bar + 1;
+  uint64_t* k_full = bar + 2;          // [NSK]
+  uint64_t* k_empty = k_full + 8;      // [NSK]
+  uint64_t* v_full = k_empty + 8;      // [NSV]
+  uint64_t* v_empty = v_full + 4;      // [NSV]
+  uint64_t* s_full = v_empty + 4;
+  uint64_t* s_empty = s_full + 1;      // 256 arrivals: S / dP loaded into registers
+  uint64_t* p_full = s_empty + 1;      // 256 arrivals: dS written into TMEM
+  uint64_t* ds_empty = p_full + 1;     // dQ MMA has read dS
+  uint64_t* dq_done = ds_empty + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -314,166 +348,187 @@ __global__ void __launch_bounds__(384, 1)
   const int hb = static_cast<int>(blockIdx.x / n_qt);
   const int h = hb % H, b = hb / H;
   const int row0 = b * seq;
-  const int N = causal ? 2 * qt + 2 : seq / 64;
+  const int N = causal ? qt + 1 : seq / 128;
 
   if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch(&qkv128);
-    ptx::tma_prefetch(&qkv64);
-    ptx::tma_prefetch(&do128);
-    ptx::mbar_init(q_full, 1);
-    for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(&kv_full[s], 1);
-      ptx::mbar_init(&kv_empty[s], 1);
+    ptx::tma_prefetch(&qkv_map);
+    ptx::tma_prefetch(&do_map);
+    ptx::mbar_init(q_full, 256);
+    ptx::mbar_init(do_full, 1);
+    for (int s = 0; s < NSK; ++s) {
+      ptx::mbar_init(&k_full[s], 1);
+      ptx::mbar_init(&k_empty[s], 1);
     }
-    for (int s = 0; s < 3; ++s) {
-      ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_empty[s], 1);
+    for (int s = 0; s < NSV; ++s) {
+      ptx::mbar_init(&v_full[s], 1);
+      ptx::mbar_init(&v_empty[s], 1);
     }
-    ptx::mbar_init(&p_full[0], 128);
-    ptx::mbar_init(&p_full[1], 128);
+    ptx::mbar_init(s_full, 1);
+    ptx::mbar_init(s_empty, 256);
+    ptx::mbar_init(p_full, 256);
+    ptx::mbar_init(ds_empty, 1);
     ptx::mbar_init(dq_done, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: buffer b: S at 128b (dS bf16 overwrites its first 32 columns), dP at 128b + 64;
-  // dQ at 384.
-  const uint32_t t_dq = tmem + 384;
+  // TMEM: S at 0, dP at 128, dQ at 256, dS (bf16 pairs, 64 columns) at 256 + D,
+  // Q (bf16 pairs, D / 2 columns) at 320 + D
+  const uint32_t t_dq = tmem + 256, t_ds = tmem + 256 + D, t_q = tmem + 320 + D;
   if (threadIdx.x == 0) BW_T(7, 0);
 
   if (warp == 0) {
+    ptx::regs_dec<56>();
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(q_full, 2 * L::NB * T128);
-      for (int c = 0; c < L::NB; ++c) {
-        ptx::tma_load_2d(sm + L::Q + c * T128, &qkv128, q_full, h * D + 64 * c, row0 + qt * 128);
-        ptx::tma_load_2d(sm + L::DO + c * T128, &do128, q_full, h * D + 64 * c, row0 + qt * 128);
-      }
+      ptx::mbar_arrive_expect_tx(do_full, L::NB * T128);
+      for (int c = 0; c < L::NB; ++c)
+        ptx::tma_load_2d(sm + L::DO + c * T128, &do_map, do_full, h * D + 64 * c, row0 + qt * 128);
+      // K(j) ahead of V(j): S(j) is issued before dP(j)
       for (int n = 0; n < N; ++n) {
-        const int st = n % NS;
-        ptx::mbar_wait(&kv_empty[st], ((n / NS) & 1) ^ 1);
+        const int sk = n % NSK, sv = n % NSV;
+        ptx::mbar_wait(&k_empty[sk], ((n / NSK) & 1) ^ 1);
         BW_T(6, n);
-        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * L::NB * T64);
-        for (int c = 0; c < L::NB; ++c) {
-          ptx::tma_load_2d(sm + L::K + (st * L::NB + c) * T64, &qkv64, &kv_full[st], H * D + h * D + 64 * c,
-                           row0 + n * 64);
-          ptx::tma_load_2d(sm + L::V + (st * L::NB + c) * T64, &qkv64, &kv_full[st], 2 * H * D + h * D + 64 * c,
-                           row0 + n * 64);
-        }
+        ptx::mbar_arrive_expect_tx(&k_full[sk], L::NB * T128);
+        for (int c = 0; c < L::NB; ++c)
+          ptx::tma_load_2d(sm + L::K + (sk * L::NB + c) * T128, &qkv_map, &k_full[sk], H * D + h * D + 64 * c,
+                           row0 + n * 128);
+        ptx::mbar_wait(&v_empty[sv], ((n / NSV) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&v_full[sv], L::NB * T128);
+        for (int c = 0; c < L::NB; ++c)
+          ptx::tma_load_2d(sm + L::V + (sv * L::NB + c) * T128, &qkv_map, &v_full[sv],
+                           2 * H * D + h * D + 64 * c, row0 + n * 128);
       }
     }
   } else if (warp == 1) {
+    ptx::regs_dec<56>();
     if (lane == 0) {
-      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 64, false, false);
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t id_g = ptx::idesc_bf16_f32(128, D, false, true);
-      const uint32_t sq = ptx::smem_u32(sm + L::Q), sdo = ptx::smem_u32(sm + L::DO);
+      const uint32_t sdo = ptx::smem_u32(sm + L::DO);
       ptx::mbar_wait(q_full, 0);
+      ptx::mbar_wait(do_full, 0);
       for (int n = 0; n <= N; ++n) {
-        if (n < N) {
-          const int st = n % NS, bf = n % 3;
-          const uint32_t t_s = tmem + 128 * bf, t_dp = t_s + 64;
-          ptx::mbar_wait(&kv_full[st], (n / NS) & 1);
+        if (n < N) {  // S(n), dP(n) once the softmax threads hold S(n-1) / dP(n-1) in registers
+          const int stk = n % NSK, stv = n % NSV;
+          ptx::mbar_wait(&k_full[stk], (n / NSK) & 1);
           BW_T(0, n);
-          ptx::mbar_wait(&s_empty[bf], ((n / 3) & 1) ^ 1);
+          ptx::mbar_wait(s_empty, (n & 1) ^ 1);
           BW_T(1, n);
           ptx::tc_fence_after();
-          const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * T64);
-          const uint32_t sv = ptx::smem_u32(sm + L::V + st * L::NB * T64);
+          const uint32_t sk = ptx::smem_u32(sm + L::K + stk * L::NB * T128);
+          const uint32_t sv = ptx::smem_u32(sm + L::V + stv * L::NB * T128);
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            ptx::mma_bf16_ts(tmem, t_q + kk * 8, ptx::umma_desc_sw128(sk + (kk >> 2) * T128 + (kk & 3) * 32, 16, 1024),
+                             id_s, kk > 0);
+          ptx::mbar_wait(&v_full[stv], (n / NSV) & 1);
+          ptx::tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t oa = (kk >> 2) * T128 + (kk & 3) * 32, ob = (kk >> 2) * T64 + (kk & 3) * 32;
-            ptx::mma_bf16_ss(t_s, ptx::umma_desc_sw128(sq + oa, 16, 1024), ptx::umma_desc_sw128(sk + ob, 16, 1024),
-                             id_s, kk > 0);
-            ptx::mma_bf16_ss(t_dp, ptx::umma_desc_sw128(sdo + oa, 16, 1024),
-                             ptx::umma_desc_sw128(sv + ob, 16, 1024), id_s, kk > 0);
+            const uint32_t o = (kk >> 2) * T128 + (kk & 3) * 32;
+            ptx::mma_bf16_ss(tmem + 128, ptx::umma_desc_sw128(sdo + o, 16, 1024),
+                             ptx::umma_desc_sw128(sv + o, 16, 1024), id_s, kk > 0);
           }
-          ptx::mma_commit(&s_full[bf]);
+          ptx::mma_commit(s_full);
+          ptx::mma_commit(&v_empty[stv]);
+          BW_T(8, n);
         }
-        if (n > 0) {
-          const int m = n - 1, st = m % NS, bf = m % 3;
-          ptx::mbar_wait(&p_full[m & 1], (m >> 1) & 1);
+        if (n > 0) {  // dQ += dS(n-1) K(n-1), dS from TMEM
+          const int m = n - 1, stk = m % NSK;
+          ptx::mbar_wait(p_full, m & 1);
           BW_T(2, m);
           ptx::tc_fence_after();
-          const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * T64);
+          const uint32_t sk = ptx::smem_u32(sm + L::K + stk * L::NB * T128);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)  // K = 64 keys, 16 per instruction (8 TMEM columns)
-            ptx::mma_bf16_ts(t_dq, tmem + 128 * bf + kk * 8, ptx::umma_desc_sw128(sk + kk * 2048, T64, 1024), id_g,
+          for (int kk = 0; kk < 8; ++kk)  // K = 128 keys, 16 per MMA = 8 TMEM columns of bf16 pairs
+            ptx::mma_bf16_ts(t_dq, t_ds + kk * 8, ptx::umma_desc_sw128(sk + kk * 2048, T128, 1024), id_g,
                              (m > 0 || kk > 0));
-          ptx::mma_commit(&s_empty[bf]);
-          ptx::mma_commit(&kv_empty[st]);
+          ptx::mma_commit(ds_empty);
+          ptx::mma_commit(&k_empty[stk]);
+          BW_T(9, m);
         }
       }
       ptx::mma_commit(dq_done);
     }
   } else if (warp >= 4) {
-    const int wg = (warp - 4) >> 2;
+    ptx::regs_inc<224>();
+    const int wg = (warp - 4) >> 2;  // keys [64 wg, 64 wg + 64) of every block
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const int qrow = qt * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
+    const int c0 = 64 * wg;
     const size_t bh = (static_cast<size_t>(b) * H + h) * seq;
     const float nl = -lse[bh + qrow], dl = delta[bh + qrow];
-    int it = 0;
-    for (int n = wg; n < N; n += 2, ++it) {
-      const int bf = n % 3;
-      const uint32_t t_s = tmem + 128 * bf + lanes, t_dp = t_s + 64;
-      const bool diag = causal && n >= 2 * qt;
-      ptx::mbar_wait(&s_full[bf], (n / 3) & 1);
-      if (lane == 0 && q == 0) BW_T(3, n);
-      ptx::tc_fence_after();
-      uint32_t s0[32], s1[32], d0[32], d1[32];
-      ptx::tmem_ld_32x32b_x32(t_s, s0);
-      ptx::tmem_ld_32x32b_x32(t_s + 32, s1);
-      ptx::tmem_ld_32x32b_x32(t_dp, d0);
-      ptx::tmem_ld_32x32b_x32(t_dp + 32, d1);
-      ptx::tmem_ld_wait();
-      float g[64];
+    {  // this thread's half of its Q row -> TMEM (bf16 pairs: column j holds dims 2j, 2j+1)
+      const uint4* src = reinterpret_cast<const uint4*>(qkv + (static_cast<size_t>(row0) + qrow) * (3 * H * D) +
+                                                        h * D + wg * (D / 2));
+      uint32_t qv[D / 4];
 #pragma unroll
-      for (int cc = 0; cc < 64; ++cc) {
-        const float sv = __uint_as_float(cc < 32 ? s0[cc] : s1[cc - 32]);
-        const float dp = __uint_as_float(cc < 32 ? d0[cc] : d1[cc - 32]);
-        g[cc] = ex2(fmaf(sv, scale_log2, nl)) * (dp - dl);
+      for (int u = 0; u < D / 16; ++u) {
+        const uint4 t = src[u];
+        qv[4 * u] = t.x;
+        qv[4 * u + 1] = t.y;
+        qv[4 * u + 2] = t.z;
+        qv[4 * u + 3] = t.w;
       }
-      if (diag) {
 #pragma unroll
-        for (int cc = 0; cc < 64; ++cc)
-          if (n * 64 + cc > qrow) g[cc] = 0.f;
-      }
-      uint32_t gg[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) gg[c] = pack2(g[2 * c], g[2 * c + 1]);
-      if (lane == 0 && q == 0) BW_T(4, n);
-      ptx::tmem_st_32x32b_x32(t_s, gg);  // dS (bf16 pairs) over the S columns just read
+      for (int u = 0; u < D / 64; ++u) tmem_st_x16(t_q + lanes + wg * (D / 4) + 16 * u, qv + 16 * u);
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&p_full[wg]);
-      if (lane == 0 && q == 0) BW_T(5, n);
+      ptx::mbar_arrive(q_full);
+    }
+    for (int n = 0; n < N; ++n) {
+      const bool diag = causal && n == N - 1;
+      ptx::mbar_wait(s_full, n & 1);
+      if (lane == 0 && q == 0 && wg == 0) BW_T(3, n);
+      ptx::tc_fence_after();
+      uint32_t s[64], d[64];
+      ptx::tmem_ld_32x32b_x32(tmem + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+      ptx::tmem_ld_32x32b_x32(tmem + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
+      ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(s_empty);
+      uint32_t gg[32];
+#pragma unroll
+      for (int cc = 0; cc < 64; cc += 2) {
+        float g0 = ex2(fmaf(__uint_as_float(s[cc]), scale_log2, nl)) * (__uint_as_float(d[cc]) - dl);
+        float g1 = ex2(fmaf(__uint_as_float(s[cc + 1]), scale_log2, nl)) * (__uint_as_float(d[cc + 1]) - dl);
+        if (diag) {
+          const int k0 = n * 128 + c0 + cc;
+          if (k0 > qrow) g0 = 0.f;
+          if (k0 + 1 > qrow) g1 = 0.f;
+        }
+        gg[cc >> 1] = pack2(g0, g1);
+      }
+      if (lane == 0 && q == 0 && wg == 0) BW_T(4, n);
+      ptx::mbar_wait(ds_empty, (n & 1) ^ 1);  // dQ(n-1) has read the previous dS
+      ptx::tc_fence_after();
+      tmem_st_x16(t_ds + lanes + 32 * wg, gg);
+      tmem_st_x16(t_ds + lanes + 32 * wg + 16, gg + 16);
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+      if (lane == 0 && q == 0 && wg == 0) BW_T(5, n);
     }
     ptx::mbar_wait(dq_done, 0);
     ptx::tc_fence_after();
     // each warpgroup writes half of the D columns
-    bf16* rowq = dqkv + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(3) * H * D) + h * D;
-#pragma unroll 1
-    for (int c = wg * (D / 64); c < (wg + 1) * (D / 64); ++c) {
-      uint32_t a[32];
-      ptx::tmem_ld_32x32b_x32(t_dq + lanes + c * 32, a);
-      ptx::tmem_ld_wait();
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float f[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * u + e]) * scale;
-        store8(rowq + c * 32 + 8 * u, f);
-      }
-    }
+    bf16* rowq = dqkv + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(3) * H * D) + h * D + wg * (D / 2);
+    tmem_row_to_global<D / 2>(t_dq + lanes + wg * (D / 2), rowq, scale);
+  } else {
+    ptx::regs_dec<56>();
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<L::TMEM_COLS>(tmem);
+    ptx::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -485,11 +540,11 @@ int set_smem(K k, size_t bytes) {
 template <int D>
 int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
                   int S, int H, int causal, cudaStream_t st) {
-  CUtensorMap q128, q64, o128, o64;
+  CUtensorMap q128, o128, q64, o64;
   const uint64_t ldq = static_cast<uint64_t>(3) * H * D, ldo = static_cast<uint64_t>(H) * D;
   const uint64_t rows = static_cast<uint64_t>(B) * S;
-  if (!tma_map_bf16_2d(&q128, qkv, ldq, rows, ldq, 64, 128) || !tma_map_bf16_2d(&q64, qkv, ldq, rows, ldq, 64, 64) ||
-      !tma_map_bf16_2d(&o128, dout, ldo, rows, ldo, 64, 128) || !tma_map_bf16_2d(&o64, dout, ldo, rows, ldo, 64, 64))
+  if (!tma_map_bf16_2d(&q128, qkv, ldq, rows, ldq, 64, 128) || !tma_map_bf16_2d(&o128, dout, ldo, rows, ldo, 64, 128) ||
+      !tma_map_bf16_2d(&q64, qkv, ldq, rows, ldq, 64, 64) || !tma_map_bf16_2d(&o64, dout, ldo, rows, ldo, 64, 64))
     return AMDP_ERR_TMA;
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
@@ -503,9 +558,9 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
     attr = true;
   }
   const int nt = S / 128;
-  fa_bwd_dkdv_kernel<D><<<nt * H * B, 384, smem_kv, st>>>(q128, q64, o64, lse, delta, dqkv, S, H, nt, scale_log2,
-                                                          scale, causal);
-  fa_bwd_dq_kernel<D><<<nt * H * B, 384, smem_q, st>>>(q128, q64, o128, lse, delta, dqkv, S, H, nt, scale_log2,
+  fa_bwd_dkdv_kernel<D><<<nt * H * B, 384, smem_kv, st>>>(q128, q64, o64, lse, delta, dqkv, S, H, nt, scale_log2, scale,
+                                                          causal);
+  fa_bwd_dq_kernel<D><<<nt * H * B, 384, smem_q, st>>>(q128, o128, qkv, lse, delta, dqkv, S, H, nt, scale_log2,
                                                        scale, causal);
   return cudaGetLastError();
 }
