@@ -72,9 +72,12 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 }
 
 // 32 consecutive output columns of one row: apply the fused epilogue and store.
+constexpr int EPI_DISCARD = 6;  // experiment only: drain TMEM, store nothing (AMDP_GEMM_DISCARD)
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& p, int row, int col0,
                                                const uint32_t (&raw)[32]) {
+  if constexpr (EPI == EPI_DISCARD) return;
   if (row >= p.M) return;
   float v[32];
 #pragma unroll
@@ -316,52 +319,210 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ CTA-pair kernel
-// cta_group::2 variant: a cluster of two CTAs computes a 256 x BNP tile with one
+// cta_group::2 variant: a cluster of two CTAs computes a 256 x 256 tile with one
 // tcgen05.mma (M=256) per K=16 step, issued by the even CTA.  CTA r loads A rows
-// [m0 + 128 r, +128) and B rows [n0 + r BNP/2, +BNP/2) into its own smem; both CTAs' TMA
-// bytes land on the even CTA's `full` barrier; each CTA's TMEM holds its 128 rows x BNP
-// columns.  Per SM the tensor core reads 4 KiB of A and BNP/8 KiB of B per instruction,
-// and a 256 x 128 pair tile keeps the N=2048 stage GEMMs at ~7 waves on 148 SMs.
+// [m0 + 128 r, +128) and B rows [n0 + r W/2, +W/2) into its own smem; both CTAs' TMA
+// bytes land on the even CTA's `full` barrier; each CTA's TMEM holds its 128 rows x W
+// columns.
+//
+// Tail waves: with 74 pairs, a GEMM of T tiles runs ceil(T/74) tile-times while only
+// T/74 are busy (N=2048 stage GEMMs: 256 tiles = 3.46 waves -> 4).  The last T mod 74
+// tiles are therefore split along N into `tail_split` sub-tiles of width 256/s (one
+// tcgen05.mma of N = 256/s per K step), so the final wave takes 1/s of a tile-time.
 constexpr int PAIR_THREADS = 256;
+constexpr int PBN = 256;
 
-template <int BNP>
+template <int NST>
 struct PairCfg {
-  static constexpr int B_HALF = BNP / 2;
+  static constexpr int B_HALF = PBN / 2;
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = B_HALF * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NSTAGE = BNP == 256 ? 4 : 6;
-  static constexpr size_t SMEM = 1024 + NSTAGE * STAGE + 256;
-  static constexpr uint32_t TMEM = 2 * BNP <= 256 ? 256 : 512;
+  static constexpr int NSTAGE = NST;
+  static constexpr int STG = 4 * 2 * 4096;  // epilogue staging: 4 warps x 2 x 4 KB
+  static constexpr size_t SMEM = 1024 + NSTAGE * STAGE + STG + 256;
+  static constexpr uint32_t TMEM = 512;
 };
 
-template <bool A_MN, bool B_MN, int EPI, int BNP>
+struct PairSched {
+  int tiles_m, tiles_n;
+  int full_tiles;   // tiles before the split tail (raster order)
+  int tail_split;   // 1, 2 or 4
+  int num_work;     // full_tiles + tail_split * (tiles - full_tiles)
+};
+
+// Work item w -> output rows [m0, m0 + 256), columns [n0, n0 + width).
+__device__ __forceinline__ void pair_work(const PairSched& s, int w, int& m0, int& n0, int& width) {
+  int t = w, part = 0, split = 1;
+  if (w >= s.full_tiles) {
+    const int u = w - s.full_tiles;
+    split = s.tail_split;
+    t = s.full_tiles + u / split;
+    part = u % split;
+  }
+  int tm, tn;
+  tile_coords(t, s.tiles_m, s.tiles_n, tm, tn);
+  width = PBN / split;
+  m0 = tm * 256;
+  n0 = tn * PBN + part * width;
+}
+
+// Output tensor maps of the pair kernel's TMA epilogue: C (bf16 box {64, 32} or f32 box
+// {32, 32}), C2 (GELU pre-activation), aux (residual / pre-activation input), SWIZZLE_128B.
+struct EpiMaps {
+  CUtensorMap c, c2, aux;
+};
+
+__device__ __forceinline__ uint32_t sw_chunk(int lane, int j) {
+  return static_cast<uint32_t>(lane) * 128u + ((static_cast<uint32_t>(j) ^ (static_cast<uint32_t>(lane) & 7u)) << 4);
+}
+
+// One epilogue warp drains its 32 TMEM lanes (rows row0..row0+31) x `width` columns:
+// tcgen05.ld -> fused op in registers -> swizzled row into a 4 KB staging buffer (conflict
+// free: 8 consecutive lanes hit 8 distinct 16-byte bank groups) -> one TMA store (or
+// reduce-add for the fp32 window gradient) per 32 x 64 bf16 / 32 x 32 fp32 block.  Two
+// staging buffers per warp alternate, so a block's store overlaps the next block's math.
+// Residual / GELU' inputs arrive by TMA into the same buffer before the math.
+template <int EPI>
+__device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams& p, uint32_t t_row, int width,
+                                              int n0, int row0, uint8_t* stg, uint64_t* aux_bar,
+                                              uint32_t& aux_phase, int& bsel, int lane) {
+  constexpr bool F32 = (EPI == AMDP_EPI_ACCUM_F32 || EPI == AMDP_EPI_STORE_F32);
+  constexpr bool AUX = (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD);
+  if constexpr (F32) {
+#pragma unroll 1
+    for (int cc = 0; cc < width; cc += 32) {
+      if (n0 + cc >= p.N) break;
+      uint32_t raw[32];
+      ptx::tmem_ld_32x32b_x32(t_row + cc, raw);
+      uint8_t* buf = stg + bsel * 4096;
+      if (lane == 0) ptx::bulk_wait_read<1>();
+      __syncwarp();
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 o = make_float4(__uint_as_float(raw[4 * j]) * p.alpha, __uint_as_float(raw[4 * j + 1]) * p.alpha,
+                               __uint_as_float(raw[4 * j + 2]) * p.alpha, __uint_as_float(raw[4 * j + 3]) * p.alpha);
+        *reinterpret_cast<float4*>(buf + sw_chunk(lane, j)) = o;
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (EPI == AMDP_EPI_ACCUM_F32) ptx::tma_reduce_add_2d(&em.c, buf, n0 + cc, row0);
+        else ptx::tma_store_2d(&em.c, buf, n0 + cc, row0);
+        ptx::bulk_commit();
+      }
+      bsel ^= 1;
+    }
+  } else {
+#pragma unroll 1
+    for (int cc = 0; cc < width; cc += 64) {
+      if (n0 + cc >= p.N) break;
+      uint32_t raw[64];
+      ptx::tmem_ld_32x32b_x32(t_row + cc, *reinterpret_cast<uint32_t(*)[32]>(&raw[0]));
+      ptx::tmem_ld_32x32b_x32(t_row + cc + 32, *reinterpret_cast<uint32_t(*)[32]>(&raw[32]));
+      uint8_t* buf = stg + bsel * 4096;
+      if (lane == 0) ptx::bulk_wait_read<1>();
+      __syncwarp();
+      float v[64];
+      if constexpr (AUX) {
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(aux_bar, 4096);
+          ptx::tma_load_2d(buf, &em.aux, aux_bar, n0 + cc, row0);
+        }
+        ptx::mbar_wait(aux_bar, aux_phase);
+        aux_phase ^= 1;
+      }
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(raw[j]) * p.alpha;
+      if constexpr (AUX) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 q = *reinterpret_cast<const uint4*>(buf + sw_chunk(lane, j));
+          const __nv_bfloat162* hq = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(hq[e]);
+            if constexpr (EPI == AMDP_EPI_RESIDUAL) {
+              v[8 * j + 2 * e] += f.x;
+              v[8 * j + 2 * e + 1] += f.y;
+            } else {
+              v[8 * j + 2 * e] *= gelu_tanh_grad(f.x);
+              v[8 * j + 2 * e + 1] *= gelu_tanh_grad(f.y);
+            }
+          }
+        }
+      }
+      if constexpr (EPI == AMDP_EPI_GELU) {  // pre-activation to C2 first
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint4 q;
+          __nv_bfloat162* hq = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hq[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+          *reinterpret_cast<uint4*>(buf + sw_chunk(lane, j)) = q;
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&em.c2, buf, n0 + cc, row0);
+          ptx::bulk_commit();
+        }
+        bsel ^= 1;
+        buf = stg + bsel * 4096;
+        if (lane == 0) ptx::bulk_wait_read<1>();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 64; ++j) v[j] = gelu_tanh(v[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        uint4 q;
+        __nv_bfloat162* hq = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) hq[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+        *reinterpret_cast<uint4*>(buf + sw_chunk(lane, j)) = q;
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_2d(&em.c, buf, n0 + cc, row0);
+        ptx::bulk_commit();
+      }
+      bsel ^= 1;
+    }
+  }
+}
+
+template <bool A_MN, bool B_MN, int EPI, int NST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     gemm_bf16_tc_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                      const EpiParams p) {
-  using C = PairCfg<BNP>;
+                      const __grid_constant__ CUtensorMap map_b_tail, const __grid_constant__ EpiMaps em,
+                      const EpiParams p, const PairSched sc) {
+  using C = PairCfg<NST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + C::NSTAGE * C::A_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::NSTAGE * C::STAGE);
+  uint8_t* stg_all = smem + C::NSTAGE * C::STAGE;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg_all + C::STG);
   uint64_t* empty_bar = full_bar + C::NSTAGE;
   uint64_t* tfull_bar = empty_bar + C::NSTAGE;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar = tempty_bar + 2;  // [4], one per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_rank();
-  const int tiles_m = (p.M + 255) / 256;
-  const int tiles_n = (p.N + BNP - 1) / BNP;
-  const int num_tiles = tiles_m * tiles_n;
   const int num_kb = p.K / BK;
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&map_a);
     ptx::tma_prefetch(&map_b);
+    if (sc.tail_split > 1) ptx::tma_prefetch(&map_b_tail);
     for (int s = 0; s < C::NSTAGE; ++s) {
       ptx::mbar_init(&full_bar[s], 1);
       ptx::mbar_init(&empty_bar[s], 1);
@@ -370,7 +531,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       ptx::mbar_init(&tfull_bar[b], 1);
       ptx::mbar_init(&tempty_bar[b], 2 * 128);
     }
+    for (int q = 0; q < 4; ++q) ptx::mbar_init(&aux_bar[q], 1);
     ptx::fence_mbar_init();
+  }
+  if (warp == 3 && lane == 0) {
+    ptx::tma_prefetch(&em.c);
+    if (EPI == AMDP_EPI_GELU) ptx::tma_prefetch(&em.c2);
+    if (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD) ptx::tma_prefetch(&em.aux);
   }
   if (warp == 2) ptx::tmem_alloc_pair<C::TMEM>(tmem_slot);
   ptx::tc_fence_before();
@@ -382,15 +549,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
-        int tm, tn;
-        tile_coords(t, tiles_m, tiles_n, tm, tn);
-        const int ma = tm * 256 + 128 * static_cast<int>(rank);
-        const int nb = tn * BNP + C::B_HALF * static_cast<int>(rank);
+      for (int w = cluster; w < sc.num_work; w += nclusters) {
+        int m0, n0, width;
+        pair_work(sc, w, m0, n0, width);
+        const int ma = m0 + 128 * static_cast<int>(rank);
+        const int half = width / 2;
+        const int nb = n0 + half * static_cast<int>(rank);
+        const uint32_t bytes = 2u * (C::A_BYTES + static_cast<uint32_t>(half) * BK * 2);
+        const CUtensorMap* mb = (width == PBN || B_MN) ? &map_b : &map_b_tail;
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], bytes);
           uint8_t* sa = smem_a + stage * C::A_BYTES;
           uint8_t* sb = smem_b + stage * C::B_BYTES;
           const int k0 = kb * BK;
@@ -401,11 +571,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
             ptx::tma_load_2d_pair(sa, &map_a, fb, k0, ma);
           }
           if constexpr (B_MN) {
-#pragma unroll
-            for (int i = 0; i < C::B_HALF / 64; ++i)
+            for (int i = 0; i < half / 64; ++i)
               ptx::tma_load_2d_pair(sb + i * 64 * BK * 2, &map_b, fb, nb + 64 * i, k0);
           } else {
-            ptx::tma_load_2d_pair(sb, &map_b, fb, k0, nb);
+            ptx::tma_load_2d_pair(sb, mb, fb, k0, nb);
           }
           if (++stage == C::NSTAGE) { stage = 0; phase ^= 1; }
         }
@@ -413,15 +582,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(256, BNP, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
+      for (int w = cluster; w < sc.num_work; w += nclusters) {
+        int m0, n0, width;
+        pair_work(sc, w, m0, n0, width);
+        const uint32_t idesc = ptx::idesc_bf16_f32(256, width, A_MN, B_MN);
         ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BNP;
+        const uint32_t d_tmem = tmem_base + acc * PBN;
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
@@ -447,27 +618,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     const uint32_t tempty_leader0 = ptx::mapa(ptx::smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = ptx::mapa(ptx::smem_u32(&tempty_bar[1]), 0);
     int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = cluster; t < num_tiles; t += nclusters) {
-      int tm, tn;
-      tile_coords(t, tiles_m, tiles_n, tm, tn);
-      const int row = tm * 256 + 128 * static_cast<int>(rank) + q * 32 + lane;
+    uint32_t acc_phase = 0, aux_phase = 0;
+    int bsel = 0;
+    uint8_t* stg = stg_all + q * 8192;
+    for (int w = cluster; w < sc.num_work; w += nclusters) {
+      int m0, n0, width;
+      pair_work(sc, w, m0, n0, width);
+      const int row0 = m0 + 128 * static_cast<int>(rank) + q * 32;
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BNP;
-      const int n_valid = min(BNP, p.N - tn * BNP);
-#pragma unroll 1
-      for (int c = 0; c < BNP / 32; ++c) {
-        if (c * 32 >= n_valid) break;  // warp-uniform
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * PBN;
+      if constexpr (EPI == EPI_DISCARD) {
         uint32_t raw[32];
-        ptx::tmem_ld_32x32b_x32(t_row + c * 32, raw);
+        for (int c = 0; c < width; c += 32) ptx::tmem_ld_32x32b_x32(t_row + c, raw);
         ptx::tmem_ld_wait();
-        epilogue_chunk<EPI>(p, row, tn * BNP + c * 32, raw);
+      } else {
+        pair_epilogue<EPI>(em, p, t_row, width, n0, row0, stg, &aux_bar[q], aux_phase, bsel, lane);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) ptx::bulk_wait<0>();
   }
 
   ptx::tc_fence_before();
@@ -496,25 +668,105 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 // 2-D bf16 tensor map: inner dimension `inner` (contiguous), outer `outer` with
 // leading dimension `ld` elements; box = {64, box_outer}, 128-byte swizzle.
 bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-              uint32_t box_outer) {
+              uint32_t box_outer, bool f32 = false, uint32_t box_inner = 64) {
   auto enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_outer};
+  cuuint64_t strides[1] = {ld * (f32 ? 4 : 2)};
+  cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
 int g_num_sms = 0;
 
-// MODE 0: single-CTA 128x256 tiles; MODE 128 / 256: CTA-pair 256 x MODE tiles.
-template <bool A_MN, bool B_MN, int EPI, int MODE>
-int launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p, cudaStream_t s) {
-  if constexpr (MODE == 0) {
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// Tail split (see the pair kernel): the s in {1, 2, 4} minimising the tail's length
+// ceil(s R / P) / s tile-times (R = tiles mod P, P = pairs); s = 4 needs K-major B
+// (an MN-major B sub-tile must stay a whole 64-column swizzle atom per CTA).
+PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
+  PairSched s;
+  s.tiles_m = (M + 255) / 256;
+  s.tiles_n = (N + PBN - 1) / PBN;
+  const int T = s.tiles_m * s.tiles_n;
+  static const int forced = env_int("AMDP_GEMM_TAIL", -1);
+  const int P = pairs;
+  const int R = T % P;
+  int best = 1;
+  if (R != 0 && T > P) {
+    double best_len = 1.0;
+    for (int cand = 2; cand <= (b_mn ? 2 : 4); cand *= 2) {
+      const double len = static_cast<double>((cand * R + P - 1) / P) / cand;
+      if (len < best_len - 1e-9) { best_len = len; best = cand; }
+    }
+  }
+  if (forced == 1 || forced == 2 || (forced == 4 && !b_mn)) best = forced;
+  s.tail_split = best;
+  s.full_tiles = best == 1 ? T : T - R;
+  s.num_work = s.full_tiles + best * (T - s.full_tiles);
+  return s;
+}
+
+// Co-resident 2-CTA clusters for this smem footprint (GPC sizes can leave SMs unpaired,
+// so this may be below #SMs / 2); the persistent grid never exceeds it.
+template <int NST>
+int max_pairs() {
+  static int pairs = 0;
+  if (pairs == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.gridDim = dim3(g_num_sms, 1, 1);
+    cfg.blockDim = dim3(PAIR_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = PairCfg<NST>::SMEM;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    auto kern = gemm_bf16_tc_pair<false, false, AMDP_EPI_STORE_BF16, NST>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(PairCfg<NST>::SMEM));
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = g_num_sms / 2;
+    }
+    pairs = n < g_num_sms / 2 ? n : g_num_sms / 2;
+    if (getenv("AMDP_GEMM_DEBUG")) fprintf(stderr, "amdp_gemm: %d co-resident CTA pairs (NST=%d)\n", pairs, NST);
+  }
+  return pairs;
+}
+
+template <bool A_MN, bool B_MN, int EPI, int NST>
+int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbt, const EpiMaps& em,
+                const EpiParams& p, cudaStream_t s) {
+  auto kern = gemm_bf16_tc_pair<A_MN, B_MN, EPI, NST>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(PairCfg<NST>::SMEM));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int pairs = max_pairs<NST>();
+  const PairSched sc = pair_schedule(p.M, p.N, B_MN, pairs);
+  const int grid = 2 * (sc.num_work < pairs ? sc.num_work : pairs);
+  kern<<<grid, PAIR_THREADS, PairCfg<NST>::SMEM, s>>>(ma, mb, mbt, em, p, sc);
+  return cudaGetLastError();
+}
+
+// MODE 0: single-CTA 128x256 tiles; MODE 256: CTA-pair 256x256 tiles (+ split tail).
+template <bool A_MN, bool B_MN, int EPI>
+int launch(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbt, const EpiMaps& em,
+           const EpiParams& p, cudaStream_t s) {
+  if (mode == 0) {
     auto kern = gemm_bf16_tcgen05<A_MN, B_MN, EPI>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -526,57 +778,42 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p, cud
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
     const int grid = tiles < g_num_sms ? tiles : g_num_sms;
     kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
-  } else {
-    auto kern = gemm_bf16_tc_pair<A_MN, B_MN, EPI, MODE>;
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(PairCfg<MODE>::SMEM));
-      if (e != cudaSuccess) return e;
-      attr_set = true;
-    }
-    const int tiles = ((p.M + 255) / 256) * ((p.N + MODE - 1) / MODE);
-    const int pairs = g_num_sms / 2;
-    const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    kern<<<grid, PAIR_THREADS, PairCfg<MODE>::SMEM, s>>>(ma, mb, p);
+    return cudaGetLastError();
   }
-  return cudaGetLastError();
+  static const int nst = env_int("AMDP_GEMM_STAGES", 6);
+  if (nst == 4) return launch_pair<A_MN, B_MN, EPI, 4>(ma, mb, mbt, em, p, s);
+  return launch_pair<A_MN, B_MN, EPI, 6>(ma, mb, mbt, em, p, s);
 }
 
-template <bool A_MN, bool B_MN, int MODE>
-int dispatch_epi(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p,
-                 cudaStream_t s) {
+template <bool A_MN, bool B_MN>
+int dispatch_epi(int mode, int epi, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbt,
+                 const EpiMaps& em, const EpiParams& p, cudaStream_t s) {
   switch (epi) {
-    case AMDP_EPI_STORE_BF16: return launch<A_MN, B_MN, AMDP_EPI_STORE_BF16, MODE>(ma, mb, p, s);
-    case AMDP_EPI_GELU: return launch<A_MN, B_MN, AMDP_EPI_GELU, MODE>(ma, mb, p, s);
-    case AMDP_EPI_RESIDUAL: return launch<A_MN, B_MN, AMDP_EPI_RESIDUAL, MODE>(ma, mb, p, s);
-    case AMDP_EPI_ACCUM_F32: return launch<A_MN, B_MN, AMDP_EPI_ACCUM_F32, MODE>(ma, mb, p, s);
-    case AMDP_EPI_GELU_BWD: return launch<A_MN, B_MN, AMDP_EPI_GELU_BWD, MODE>(ma, mb, p, s);
-    case AMDP_EPI_STORE_F32: return launch<A_MN, B_MN, AMDP_EPI_STORE_F32, MODE>(ma, mb, p, s);
+    case AMDP_EPI_STORE_BF16: {
+      static const bool discard = getenv("AMDP_GEMM_DISCARD") != nullptr;
+      if (discard) return launch<A_MN, B_MN, EPI_DISCARD>(mode, ma, mb, mbt, em, p, s);
+      return launch<A_MN, B_MN, AMDP_EPI_STORE_BF16>(mode, ma, mb, mbt, em, p, s);
+    }
+    case AMDP_EPI_GELU: return launch<A_MN, B_MN, AMDP_EPI_GELU>(mode, ma, mb, mbt, em, p, s);
+    case AMDP_EPI_RESIDUAL: return launch<A_MN, B_MN, AMDP_EPI_RESIDUAL>(mode, ma, mb, mbt, em, p, s);
+    case AMDP_EPI_ACCUM_F32: return launch<A_MN, B_MN, AMDP_EPI_ACCUM_F32>(mode, ma, mb, mbt, em, p, s);
+    case AMDP_EPI_GELU_BWD: return launch<A_MN, B_MN, AMDP_EPI_GELU_BWD>(mode, ma, mb, mbt, em, p, s);
+    case AMDP_EPI_STORE_F32: return launch<A_MN, B_MN, AMDP_EPI_STORE_F32>(mode, ma, mb, mbt, em, p, s);
   }
   return AMDP_ERR_INVALID;
 }
 
-template <bool A_MN, bool B_MN>
-int dispatch_mode(int mode, int epi, const CUtensorMap& ma, const CUtensorMap& mb, const EpiParams& p,
-                  cudaStream_t s) {
-  if (mode == 128) return dispatch_epi<A_MN, B_MN, 128>(epi, ma, mb, p, s);
-  if (mode == 256) return dispatch_epi<A_MN, B_MN, 256>(epi, ma, mb, p, s);
-  return dispatch_epi<A_MN, B_MN, 0>(epi, ma, mb, p, s);
+int gemm_pairs() {
+  static const int nst = env_int("AMDP_GEMM_STAGES", 6);
+  return nst == 4 ? max_pairs<4>() : max_pairs<6>();
 }
 
-// Tile shape per problem: CTA pairs with 256 x 256 tiles whenever M >= 256.  Measured at
-// the 1.3B shapes (profiles/r01_gemm_modes.txt) the pair-256 kernel matches or beats the
-// single-CTA 128x256 kernel everywhere (+5-13% on QKV / fc1 / head / 8192^3); the
-// pair-128 width loses 20-35% and is only reachable through AMDP_GEMM_MODE=128.
+// Tile shape per problem: CTA pairs with 256 x 256 tiles whenever M >= 256 (measured at the
+// 1.3B shapes, profiles/r01_gemm_modes.txt: +5-13% over single-CTA 128x256 tiles).
 int choose_mode(int M, int N) {
   (void)N;
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = getenv("AMDP_GEMM_MODE");
-    forced = e ? atoi(e) : -1;
-  }
-  if (forced == 0 || forced == 128 || forced == 256) return forced;
+  static const int forced = env_int("AMDP_GEMM_MODE", -1);
+  if (forced == 0 || forced == 256) return forced;
   return M >= 256 ? 256 : 0;
 }
 
@@ -598,25 +835,44 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
     if (g_num_sms <= 0) return AMDP_ERR_CUDA;
   }
   const int mode = choose_mode(a->M, a->N);
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mbt;
   bool ok;
   if (a->a_mn_major)  // A stored [K][lda], M contiguous
     ok = make_map(&ma, a->A, a->M, a->K, a->lda, BK);
   else  // A stored [M][lda], K contiguous (128 rows per CTA in both kernels)
     ok = make_map(&ma, a->A, a->K, a->M, a->lda, BM);
   if (!ok) return AMDP_ERR_TMA;
-  if (a->b_mn_major)
+  if (a->b_mn_major) {
     ok = make_map(&mb, a->B, a->N, a->K, a->ldb, BK);
-  else  // B rows per CTA: 256 (single) or mode / 2 (pair)
-    ok = make_map(&mb, a->B, a->K, a->N, a->ldb, mode == 0 ? BN : mode / 2);
+    mbt = mb;
+  } else {  // B rows per CTA: 256 (single) or 128 (pair); tail sub-tiles 128 / s
+    ok = make_map(&mb, a->B, a->K, a->N, a->ldb, mode == 0 ? BN : PBN / 2);
+    if (ok && mode != 0) {
+      const PairSched sc = pair_schedule(a->M, a->N, false, gemm_pairs());
+      ok = make_map(&mbt, a->B, a->K, a->N, a->ldb, PBN / 2 / sc.tail_split);
+    } else {
+      mbt = mb;
+    }
+  }
   if (!ok) return AMDP_ERR_TMA;
+  EpiMaps em;
+  if (mode != 0) {  // pair kernel: TMA-store epilogue maps (box 32 rows x 128 bytes)
+    const bool f32 = a->epilogue == AMDP_EPI_ACCUM_F32 || a->epilogue == AMDP_EPI_STORE_F32;
+    ok = make_map(&em.c, a->C, a->N, a->M, a->ldc, 32, f32, f32 ? 32 : 64);
+    em.c2 = em.c;
+    em.aux = em.c;
+    if (ok && a->epilogue == AMDP_EPI_GELU) ok = make_map(&em.c2, a->C2, a->N, a->M, a->ldc2, 32);
+    if (ok && (a->epilogue == AMDP_EPI_RESIDUAL || a->epilogue == AMDP_EPI_GELU_BWD))
+      ok = make_map(&em.aux, a->aux, a->N, a->M, a->ld_aux, 32);
+    if (!ok) return AMDP_ERR_TMA;
+  }
   EpiParams p{a->M, a->N, a->K, a->C, a->ldc,
               static_cast<const __nv_bfloat16*>(a->aux), a->ld_aux,
               static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int am = a->a_mn_major ? 1 : 0, bm = a->b_mn_major ? 1 : 0;
-  if (!am && !bm) return dispatch_mode<false, false>(mode, a->epilogue, ma, mb, p, s);
-  if (!am && bm) return dispatch_mode<false, true>(mode, a->epilogue, ma, mb, p, s);
-  if (am && !bm) return dispatch_mode<true, false>(mode, a->epilogue, ma, mb, p, s);
-  return dispatch_mode<true, true>(mode, a->epilogue, ma, mb, p, s);
+  if (!am && !bm) return dispatch_epi<false, false>(mode, a->epilogue, ma, mb, mbt, em, p, s);
+  if (!am && bm) return dispatch_epi<false, true>(mode, a->epilogue, ma, mb, mbt, em, p, s);
+  if (am && !bm) return dispatch_epi<true, false>(mode, a->epilogue, ma, mb, mbt, em, p, s);
+  return dispatch_epi<true, true>(mode, a->epilogue, ma, mb, mbt, em, p, s);
 }

@@ -187,6 +187,201 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dgb_kernel(
   }
 }
 
+// ---------------------------------------------------------------- LayerNorm, row-group form
+// For the model widths (cols a multiple of 256, <= 8192): one thread per 8 columns, so a
+// CTA of cols/8 threads spans a whole row and handles RG rows per iteration (RG 16-byte
+// loads in flight per thread and per tensor).  Row statistics: warp shuffle, then the
+// cols/256 warp partials through shared memory (double-buffered by iteration parity, so
+// one __syncthreads per reduction).  The backward accumulates dgamma/dbeta for its 8
+// columns in registers across all its rows and adds them once per CTA, so x and dy are
+// read exactly once (dx, dgamma, dbeta fused: 4 bf16 tensors of traffic per row).
+template <int RG>
+__device__ __forceinline__ void block_sums(float (&v)[RG], float* red, int nw) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < RG; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < RG; ++i) red[i * 32 + w] = v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < RG; ++i) {
+    float t = 0.f;
+    for (int k = 0; k < nw; ++k) t += red[i * 32 + k];
+    v[i] = t;
+  }
+}
+
+template <int RG>
+__global__ void __launch_bounds__(512) layernorm_fwd_rows_kernel(
+    const bf16* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
+    bf16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows,
+    int cols, float eps) {
+  __shared__ float red[4][RG * 32];
+  const int nw = blockDim.x >> 5;
+  const int c = threadIdx.x * 8;
+  float g[8], b[8];
+  {
+    const float4 g0 = *reinterpret_cast<const float4*>(gamma + c), g1 = *reinterpret_cast<const float4*>(gamma + c + 4);
+    const float4 b0 = *reinterpret_cast<const float4*>(beta + c), b1 = *reinterpret_cast<const float4*>(beta + c + 4);
+    g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+    b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+  }
+  const float inv = 1.f / static_cast<float>(cols);
+  int it = 0;
+  for (int r0 = blockIdx.x * RG; r0 < rows; r0 += gridDim.x * RG, it ^= 1) {
+    uint4 raw[RG];
+#pragma unroll
+    for (int i = 0; i < RG; ++i)
+      raw[i] = (r0 + i < rows) ? *reinterpret_cast<const uint4*>(x + static_cast<size_t>(r0 + i) * cols + c)
+                               : make_uint4(0, 0, 0, 0);
+    float m[RG], v[RG];
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      float f[8];
+      unpack8(raw[i], f);
+      m[i] = ((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7]));
+    }
+    block_sums<RG>(m, red[2 * it], nw);
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      m[i] *= inv;
+      float f[8];
+      unpack8(raw[i], f);
+      float q = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) q += (f[e] - m[i]) * (f[e] - m[i]);
+      v[i] = q;
+    }
+    block_sums<RG>(v, red[2 * it + 1], nw);
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      if (r0 + i >= rows) break;
+      const float rs = rsqrtf(v[i] * inv + eps);
+      float f[8], o[8];
+      unpack8(raw[i], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = (f[e] - m[i]) * rs * g[e] + b[e];
+      store8(y + static_cast<size_t>(r0 + i) * cols + c, o);
+      if (threadIdx.x == 0) {
+        mean_out[r0 + i] = m[i];
+        rstd_out[r0 + i] = rs;
+      }
+    }
+  }
+}
+
+template <int RG>
+struct LnBwdRows {
+  uint4 x[RG], d[RG], r[RG];
+  float mu[RG], rs[RG];
+  __device__ __forceinline__ void load(const bf16* __restrict__ x_, const bf16* __restrict__ dy,
+                                       const bf16* resid, const float* __restrict__ mean_in,
+                                       const float* __restrict__ rstd_in, int r0, int rows, int cols, int c) {
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      const bool ok = r0 + i < rows;
+      const size_t off = static_cast<size_t>(r0 + i) * cols + c;
+      x[i] = ok ? *reinterpret_cast<const uint4*>(x_ + off) : make_uint4(0, 0, 0, 0);
+      d[i] = ok ? *reinterpret_cast<const uint4*>(dy + off) : make_uint4(0, 0, 0, 0);
+      r[i] = (ok && resid) ? *reinterpret_cast<const uint4*>(resid + off) : make_uint4(0, 0, 0, 0);
+      mu[i] = ok ? mean_in[r0 + i] : 0.f;
+      rs[i] = ok ? rstd_in[r0 + i] : 0.f;
+    }
+  }
+};
+
+// Software-pipelined over row groups: group k+1's loads are in flight while group k is
+// reduced and written, so each CTA keeps 2 x RG rows x 3 tensors of loads outstanding.
+template <int RG>
+__global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
+    const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ gamma,
+    const float* __restrict__ mean_in, const float* __restrict__ rstd_in, const bf16* resid_grad, bf16* dx,
+    float* __restrict__ part, int rows, int cols) {
+  __shared__ float red[2][2 * RG * 32];
+  const int nw = blockDim.x >> 5;
+  const int c = threadIdx.x * 8;
+  float g[8], ag[8], ab[8];
+  {
+    const float4 g0 = *reinterpret_cast<const float4*>(gamma + c), g1 = *reinterpret_cast<const float4*>(gamma + c + 4);
+    g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) ag[e] = ab[e] = 0.f;
+  const float inv = 1.f / static_cast<float>(cols);
+  const int stride = gridDim.x * RG;
+  LnBwdRows<RG> cur, nxt;
+  int r0 = blockIdx.x * RG;
+  if (r0 < rows) cur.load(x, dy, resid_grad, mean_in, rstd_in, r0, rows, cols, c);
+  for (int it = 0; r0 < rows; r0 += stride, it ^= 1) {
+    if (r0 + stride < rows) nxt.load(x, dy, resid_grad, mean_in, rstd_in, r0 + stride, rows, cols, c);
+    float sv[2 * RG];
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      float xv[8], dv[8];
+      unpack8(cur.x[i], xv);
+      unpack8(cur.d[i], dv);
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (xv[e] - cur.mu[i]) * cur.rs[i];
+        const float dxh = dv[e] * g[e];
+        s1 += dxh;
+        s2 += dxh * xh;
+        ag[e] += dv[e] * xh;
+        ab[e] += dv[e];
+      }
+      sv[2 * i] = s1;
+      sv[2 * i + 1] = s2;
+    }
+    block_sums<2 * RG>(sv, red[it], nw);
+#pragma unroll
+    for (int i = 0; i < RG; ++i) {
+      if (r0 + i >= rows) break;
+      const float s1 = sv[2 * i] * inv, s2 = sv[2 * i + 1] * inv;
+      float xv[8], dv[8], r[8], o[8];
+      unpack8(cur.x[i], xv);
+      unpack8(cur.d[i], dv);
+      unpack8(cur.r[i], r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        o[e] = r[e] + cur.rs[i] * (dv[e] * g[e] - s1 - (xv[e] - cur.mu[i]) * cur.rs[i] * s2);
+      store8(dx + static_cast<size_t>(r0 + i) * cols + c, o);
+    }
+    cur = nxt;
+  }
+  // per-CTA column partials -> workspace row blockIdx.x: [dgamma cols | dbeta cols]
+  float* wrow = part + static_cast<size_t>(blockIdx.x) * 2 * cols;
+  *reinterpret_cast<float4*>(wrow + c) = make_float4(ag[0], ag[1], ag[2], ag[3]);
+  *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(ag[4], ag[5], ag[6], ag[7]);
+  *reinterpret_cast<float4*>(wrow + cols + c) = make_float4(ab[0], ab[1], ab[2], ab[3]);
+  *reinterpret_cast<float4*>(wrow + cols + c + 4) = make_float4(ab[4], ab[5], ab[6], ab[7]);
+}
+
+// dgamma, dbeta += column sums of the [nparts][2*cols] partials ([dgamma | dbeta] per row).
+// CTA = 32 columns x 8 row-lanes; fixed summation order, so the gradient is deterministic.
+__global__ void __launch_bounds__(256) layernorm_dgb_reduce_kernel(const float* __restrict__ part, int nparts,
+                                                                   int cols, float* dgamma, float* dbeta) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;  // in [0, 2*cols)
+  float s = 0.f;
+  if (col < 2 * cols) {
+#pragma unroll 4
+    for (int r = w; r < nparts; r += 8) s += part[static_cast<size_t>(r) * 2 * cols + col];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && col < 2 * cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    if (col < cols) dgamma[col] += t;
+    else dbeta[col - cols] += t;
+  }
+}
+
 // ---------------------------------------------------------------- embedding
 __global__ void embedding_fwd_kernel(const int32_t* __restrict__ tok, const bf16* __restrict__ wte,
                                      const bf16* __restrict__ wpe, bf16* __restrict__ x, int ntok,
@@ -315,6 +510,12 @@ __global__ void __launch_bounds__(512) xent_kernel(bf16* logits, const int32_t* 
 
 using namespace amdp;
 
+// The row-group LayerNorm kernels cover widths that are whole warps of 8-column threads.
+static bool ln_row_group_form(int cols) {
+  static const int off = getenv("AMDP_LN_WARP_ROWS") ? atoi(getenv("AMDP_LN_WARP_ROWS")) : 0;
+  return !off && cols % 256 == 0 && cols >= 256 && cols / 8 <= 512;
+}
+
 extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const float* beta,
                                   uint16_t* y, float* mean, float* rstd, int rows, int cols,
                                   float eps, amdp_stream_t stream) {
@@ -326,6 +527,12 @@ extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const f
   auto xs = reinterpret_cast<const bf16*>(x);
   auto ys = reinterpret_cast<bf16*>(y);
   auto st = reinterpret_cast<cudaStream_t>(stream);
+  if (ln_row_group_form(cols) && getenv("AMDP_LN_FWD_ROWS")) {
+    constexpr int RG = 8;
+    const int grid = (rows + RG - 1) / RG;
+    layernorm_fwd_rows_kernel<RG><<<grid, cols / 8, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+    return cudaGetLastError();
+  }
   const int nv = (cols + 255) / 256;
   if (nv <= 1) layernorm_fwd_kernel<1><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
   else if (nv <= 4) layernorm_fwd_kernel<4><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
@@ -334,10 +541,18 @@ extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const f
   return cudaGetLastError();
 }
 
+// Row-group backward: per-CTA dgamma/dbeta partials, [ln_bwd_ctas][2][cols] fp32.
+static int ln_bwd_ctas(int rows) {
+  constexpr int RG = 2;
+  static const int per_sm = getenv("AMDP_LN_BWD_CTAS") ? atoi(getenv("AMDP_LN_BWD_CTAS")) : 2;
+  const int grid = (rows + RG - 1) / RG;
+  const int cap = per_sm * num_sms();  // one resident wave (128 registers x cols/8 threads)
+  return grid < cap ? grid : cap;
+}
+
 extern "C" size_t amdp_layernorm_bwd_workspace(int rows, int cols) {
-  (void)rows;
-  (void)cols;
-  return 16;  // no workspace needed any more; kept for ABI stability
+  if (rows <= 0 || cols <= 0) return 16;
+  return static_cast<size_t>(ln_bwd_ctas(rows)) * 2 * cols * sizeof(float) + 16;
 }
 
 extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const float* gamma,
@@ -345,9 +560,18 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
                                   const uint16_t* resid_grad, uint16_t* dx, float* dgamma,
                                   float* dbeta, void* workspace, int rows, int cols,
                                   amdp_stream_t stream) {
-  (void)workspace;
   if (rows <= 0 || cols <= 0 || cols % 8 != 0 || cols > LN_MAX_VEC * 256) return AMDP_ERR_INVALID;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (ln_row_group_form(cols)) {
+    if (!workspace) return AMDP_ERR_INVALID;
+    const int grid = ln_bwd_ctas(rows);
+    float* part = static_cast<float*>(workspace);
+    layernorm_bwd_rows_kernel<2><<<grid, cols / 8, 0, s>>>(
+        reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(x), gamma, mean, rstd,
+        reinterpret_cast<const bf16*>(resid_grad), reinterpret_cast<bf16*>(dx), part, rows, cols);
+    layernorm_dgb_reduce_kernel<<<(2 * cols + 31) / 32, 256, 0, s>>>(part, grid, cols, dgamma, dbeta);
+    return cudaGetLastError();
+  }
   int blocks = (rows + 7) / 8;
   if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
   {

@@ -46,6 +46,34 @@ def test_gemm_store(K, N, M, N_, K_, a_mn, b_mn):
     assert _rel(C, ref) < 8e-3
 
 
+# Shapes whose last wave is split along N (tail_split 2 or 4 over 74 CTA pairs):
+# 8192x2048 = 256 tiles (R=34 -> s=2); 2560x2000 = 80 tiles (R=6 -> s=4 for K-major B,
+# partial last N tile); 6144x2048 = 192 tiles (R=44 -> s=4 K-major).  Every element is
+# checked, so a missing or misplaced sub-tile fails.
+@pytest.mark.parametrize("M,N_,K_", [(8192, 2048, 128), (2560, 2000, 128), (6144, 2048, 192)])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True)])
+@pytest.mark.parametrize("accum", [False, True])
+def test_gemm_split_tail(K, N, M, N_, K_, a_mn, b_mn, accum):
+    torch.manual_seed(3)
+    A = torch.randn(M, K_, device="cuda").bfloat16()
+    B = torch.randn(N_, K_, device="cuda").bfloat16()
+    ref = A.float() @ B.float().T
+    As = A.T.contiguous() if a_mn else A
+    Bs = B.T.contiguous() if b_mn else B
+    if accum:
+        C0 = torch.randn(M, N_, device="cuda")
+        C = C0.clone()
+        K.gemm(As, Bs, M=M, N_=N_, K=K_, a_mn=a_mn, b_mn=b_mn, C=C, epilogue=N.EPI_ACCUM_F32)
+        ref = ref + C0
+        tol = 1e-3
+    else:
+        C = K.gemm(As, Bs, M=M, N_=N_, K=K_, a_mn=a_mn, b_mn=b_mn)
+        tol = 0.02 * ref.abs().max().item()
+    torch.cuda.synchronize()
+    err = (C.float() - ref).abs().max().item()
+    assert err < tol, f"max abs err {err}"
+
+
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, True)])
 def test_gemm_accum_f32(K, N, a_mn, b_mn):
     torch.manual_seed(1)
