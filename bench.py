@@ -95,7 +95,8 @@ class ClockSampler:
                  0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
                  0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
         return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
-                "power_w_max": max(r[2] for r in rows), "samples": len(load),
+                "power_w_max": max(r[2] for r in rows), "power_w_median": statistics.median(r[2] for r in load),
+                "samples": len(load),
                 "reasons": [n for b, n in names.items() if bits & b and n != "gpu_idle"]}
 
 
@@ -246,6 +247,7 @@ def main():
         barrier()
     st = eng.stats()
     dev_ms = max_over_ranks(st["device_ms"])
+    host_issue_ms = max_over_ranks(st["host_issue_ms"])
     value = args.steps * tok_step / (dev_ms / 1e3)
     tl = eng.timeline()
     launches = int(sum_over_ranks(st["kernels_launched"]))
@@ -310,6 +312,7 @@ def main():
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": st2["h2d_bytes"] // args.steps,
                     "d2h_bytes_per_step": st2["d2h_bytes"] // args.steps},
             "gpu_launches": launches,
+            "host_issue_ms_per_step": host_issue_ms / args.steps,
             "roofline": roofline,
             "model_flops_utilization": mfu,
             "bubble": {"physical_gpu": phys_bubble, "logical_devices_bubble_ratio_w1": logical_bubble},

@@ -114,6 +114,7 @@ typedef struct amdp_run_stats {
   int64_t h2d_bytes, d2h_bytes;
   int64_t p2p_bytes_sent, collective_bytes;
   double busy_ms; /* sum of measured task durations on this GPU (record_events) */
+  double host_issue_ms; /* host wall time spent issuing the run (launches, events, NCCL) */
 } amdp_run_stats;
 int amdp_engine_stats(const amdp_engine* e, amdp_run_stats* out);
 

@@ -12,7 +12,8 @@ from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int, c_in
                     c_size_t, c_uint16, c_uint64, c_void_p)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libamdp.so")
+# AMDP_LIB: an alternative in-tree build (A/B timing of two library versions on one box).
+LIB_PATH = os.environ.get("AMDP_LIB") or os.path.join(_HERE, "libamdp.so")
 
 
 class NativeLibraryMissing(RuntimeError):

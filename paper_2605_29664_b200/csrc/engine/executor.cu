@@ -15,6 +15,8 @@
 //    Parameter versions are therefore exactly the trace's (F sees w - preloaded, B sees
 //    w): a device-side counter per stage records what each task actually read.
 #include <cuda_runtime.h>
+
+#include <chrono>
 #include <nccl.h>
 
 #include <algorithm>
@@ -748,9 +750,12 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
       ++last_left[static_cast<size_t>(t.window)];
   }
   CUDA_OK(cudaEventRecord(run_begin_, cs_));
+  const auto t_issue0 = std::chrono::steady_clock::now();
   for (int k = 0; k < N; ++k)
     if (g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])].window < max_window)
       exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
+  stats.host_issue_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_issue0).count();
   {
     cudaEvent_t e;
     CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

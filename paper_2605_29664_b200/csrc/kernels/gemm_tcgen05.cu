@@ -50,14 +50,21 @@ struct EpiParams {
   float alpha;
 };
 
+// tanh on the SFU (tanh.approx.f32, max rel. error ~2^-11): the GELU epilogues run once per
+// output element of the largest GEMMs, and their results are rounded to bf16 (2^-8).
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  float t = tanhf(k0 * (x + k1 * x * x * x));
+  float t = tanh_fast(k0 * (x + k1 * x * x * x));
   return 0.5f * x * (1.f + t);
 }
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  float t = tanhf(k0 * (x + k1 * x * x * x));
+  float t = tanh_fast(k0 * (x + k1 * x * x * x));
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
@@ -387,6 +394,8 @@ template <int EPI>
 __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams& p, uint32_t t_row, int width,
                                               int n0, int row0, uint8_t* stg, uint64_t* aux_bar,
                                               uint32_t& aux_phase, int& bsel, int lane) {
+  // aux_bar[b] / bit b of aux_phase: the residual / pre-activation block landing in staging
+  // buffer b.  Block c+1's load is issued before block c's math (one block of prefetch).
   constexpr bool F32 = (EPI == AMDP_EPI_ACCUM_F32 || EPI == AMDP_EPI_STORE_F32);
   constexpr bool AUX = (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD);
   if constexpr (F32) {
@@ -415,23 +424,33 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
       bsel ^= 1;
     }
   } else {
+    const int n_end = min(width, p.N - n0);
+    if constexpr (AUX) {  // block 0's residual / pre-activation
+      if (lane == 0) {
+        ptx::bulk_wait_read<1>();
+        ptx::mbar_arrive_expect_tx(&aux_bar[bsel], 4096);
+        ptx::tma_load_2d(stg + bsel * 4096, &em.aux, &aux_bar[bsel], n0, row0);
+      }
+    }
 #pragma unroll 1
-    for (int cc = 0; cc < width; cc += 64) {
-      if (n0 + cc >= p.N) break;
+    for (int cc = 0; cc < n_end; cc += 64) {
       uint32_t raw[64];
       ptx::tmem_ld_32x32b_x32(t_row + cc, *reinterpret_cast<uint32_t(*)[32]>(&raw[0]));
       ptx::tmem_ld_32x32b_x32(t_row + cc + 32, *reinterpret_cast<uint32_t(*)[32]>(&raw[32]));
       uint8_t* buf = stg + bsel * 4096;
-      if (lane == 0) ptx::bulk_wait_read<1>();
-      __syncwarp();
       float v[64];
       if constexpr (AUX) {
-        if (lane == 0) {
-          ptx::mbar_arrive_expect_tx(aux_bar, 4096);
-          ptx::tma_load_2d(buf, &em.aux, aux_bar, n0 + cc, row0);
+        if (lane == 0 && cc + 64 < n_end) {  // prefetch block c+1 into the other buffer
+          const int nb = bsel ^ 1;
+          ptx::bulk_wait_read<0>();  // block c-1's store has finished reading it
+          ptx::mbar_arrive_expect_tx(&aux_bar[nb], 4096);
+          ptx::tma_load_2d(stg + nb * 4096, &em.aux, &aux_bar[nb], n0 + cc + 64, row0);
         }
-        ptx::mbar_wait(aux_bar, aux_phase);
-        aux_phase ^= 1;
+        ptx::mbar_wait(&aux_bar[bsel], (aux_phase >> bsel) & 1u);
+        aux_phase ^= 1u << bsel;
+      } else {
+        if (lane == 0) ptx::bulk_wait_read<1>();
+        __syncwarp();
       }
       ptx::tmem_ld_wait();
 #pragma unroll
@@ -511,8 +530,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   uint64_t* empty_bar = full_bar + C::NSTAGE;
   uint64_t* tfull_bar = empty_bar + C::NSTAGE;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;  // [4], one per epilogue warp
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 4);
+  uint64_t* aux_bar = tempty_bar + 2;  // [4][2]: per epilogue warp, per staging buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_rank();
@@ -531,7 +550,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       ptx::mbar_init(&tfull_bar[b], 1);
       ptx::mbar_init(&tempty_bar[b], 2 * 128);
     }
-    for (int q = 0; q < 4; ++q) ptx::mbar_init(&aux_bar[q], 1);
+    for (int q = 0; q < 8; ++q) ptx::mbar_init(&aux_bar[q], 1);
     ptx::fence_mbar_init();
   }
   if (warp == 3 && lane == 0) {
@@ -633,7 +652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         for (int c = 0; c < width; c += 32) ptx::tmem_ld_32x32b_x32(t_row + c, raw);
         ptx::tmem_ld_wait();
       } else {
-        pair_epilogue<EPI>(em, p, t_row, width, n0, row0, stg, &aux_bar[q], aux_phase, bsel, lane);
+        pair_epilogue<EPI>(em, p, t_row, width, n0, row0, stg, &aux_bar[2 * q], aux_phase, bsel, lane);
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
@@ -689,8 +708,10 @@ int env_int(const char* name, int dflt) {
 }
 
 // Tail split (see the pair kernel): the s in {1, 2, 4} minimising the tail's length
-// ceil(s R / P) / s tile-times (R = tiles mod P, P = pairs); s = 4 needs K-major B
-// (an MN-major B sub-tile must stay a whole 64-column swizzle atom per CTA).
+// ceil(s R / P) / s tile-times (R = tiles mod P, P = pairs).  Only for K-major B, i.e. the
+// forward GEMMs, which run alone on the compute stream: the backward's activation- and
+// weight-gradient GEMMs (MN-major B) run concurrently on two streams and fill each other's
+// tails, where split sub-tiles measured slower (scripts/task_durations.py, B tasks).
 PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
   PairSched s;
   s.tiles_m = (M + 255) / 256;
@@ -700,14 +721,14 @@ PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
   const int P = pairs;
   const int R = T % P;
   int best = 1;
-  if (R != 0 && T > P) {
+  if (R != 0 && T > P && !b_mn) {
     double best_len = 1.0;
-    for (int cand = 2; cand <= (b_mn ? 2 : 4); cand *= 2) {
+    for (int cand = 2; cand <= 4; cand *= 2) {
       const double len = static_cast<double>((cand * R + P - 1) / P) / cand;
       if (len < best_len - 1e-9) { best_len = len; best = cand; }
     }
   }
-  if (forced == 1 || forced == 2 || (forced == 4 && !b_mn)) best = forced;
+  if (forced == 1 || ((forced == 2 || forced == 4) && !b_mn)) best = forced;
   s.tail_split = best;
   s.full_tiles = best == 1 ? T : T - R;
   s.num_work = s.full_tiles + best * (T - s.full_tiles);

@@ -41,7 +41,8 @@ class _Run(Structure):
 class _Stats(Structure):
     _fields_ = [("device_ms", c_double), ("tasks_executed", c_int64), ("kernels_launched", c_int64),
                 ("h2d_bytes", c_int64), ("d2h_bytes", c_int64), ("p2p_bytes_sent", c_int64),
-                ("collective_bytes", c_int64), ("busy_ms", c_double)]
+                ("collective_bytes", c_int64), ("busy_ms", c_double),
+                ("host_issue_ms", c_double)]
 
 
 def _sig(name, res, args):
@@ -200,6 +201,8 @@ class PinnedTokens:
         self.labels = np.ctypeslib.as_array((ctypes.c_int32 * (num_minibatches * tokens)).from_address(self._pl)).reshape(num_minibatches, tokens)
 
     def __del__(self):
+        if lib is None:  # interpreter teardown: the process exit releases the pinned pages
+            return
         for p in (getattr(self, "_pi", None), getattr(self, "_pl", None)):
             if p:
                 lib.amdp_host_free(p)

@@ -21,6 +21,10 @@ CASES = {
     "fc1_dgrad": (T, h, 4 * h, False, True, N.EPI_STORE_BF16),
     "fc1_wgrad": (4 * h, h, T, True, True, N.EPI_ACCUM_F32),
     "square8192": (8192, 8192, 8192, False, False, N.EPI_STORE_BF16),
+    "fc1_dgrad_kk": (T, h, 4 * h, False, False, N.EPI_STORE_BF16),
+    "fc1_wgrad_kk": (4 * h, h, T, False, False, N.EPI_STORE_BF16),
+    "fc1_wgrad_bf16": (4 * h, h, T, True, True, N.EPI_STORE_BF16),
+    "fc2_fwd": (T, h, 4 * h, False, False, N.EPI_STORE_BF16),
 }
 
 

@@ -40,6 +40,9 @@ CASES = [
     ("fc1_wgrad_kk", 4 * h, h, T, False, False, N.EPI_STORE_BF16),
     ("qkv_wgrad", 3 * h, h, T, True, True, N.EPI_ACCUM_F32),
     ("out_wgrad", h, h, T, True, True, N.EPI_ACCUM_F32),
+    ("fc2_dgrad_gelubwd", T, 4 * h, h, False, True, N.EPI_GELU_BWD),
+    ("fc2_fwd_residual", T, h, 4 * h, False, False, N.EPI_RESIDUAL),
+    ("fc1_fwd_gelu", T, 4 * h, h, False, False, N.EPI_GELU),
 ]
 only = set(sys.argv[1:])
 for name, M, Nn, Kk, a_mn, b_mn, epi in CASES:
@@ -49,7 +52,12 @@ for name, M, Nn, Kk, a_mn, b_mn, epi in CASES:
     B = torch.randn(Kk, Nn, device="cuda").bfloat16() if b_mn else torch.randn(Nn, Kk, device="cuda").bfloat16()
     dt = torch.float32 if epi in (N.EPI_ACCUM_F32, N.EPI_STORE_F32) else torch.bfloat16
     C = torch.zeros(M, Nn, dtype=dt, device="cuda")
-    ms = med(lambda: K.gemm(A, B, M=M, N_=Nn, K=Kk, a_mn=a_mn, b_mn=b_mn, C=C, epilogue=epi))
+    extra = {}
+    if epi in (N.EPI_GELU_BWD, N.EPI_RESIDUAL):
+        extra = dict(aux=torch.randn(M, Nn, device="cuda").bfloat16(), ld_aux=Nn)
+    if epi == N.EPI_GELU:
+        extra = dict(C2=torch.empty(M, Nn, dtype=torch.bfloat16, device="cuda"), ldc2=Nn)
+    ms = med(lambda: K.gemm(A, B, M=M, N_=Nn, K=Kk, a_mn=a_mn, b_mn=b_mn, C=C, epilogue=epi, **extra))
     Al = A.T if a_mn else A
     Bl = B if b_mn else B.T
     ms_t = med(lambda: torch.matmul(Al, Bl))
