@@ -37,7 +37,8 @@ constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
 constexpr int GROUP_M = 8;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+constexpr int STG_BYTES = 4 * 2 * 4096;  // TMA-store epilogue staging (4 warps x 2 x 4 KB)
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 256 /*barriers*/;
 
 struct EpiParams {
   int M, N, K;
@@ -48,6 +49,7 @@ struct EpiParams {
   __nv_bfloat16* C2;
   int ldc2;
   float alpha;
+  uint32_t epi_sleep_ns;  // epilogue warps' back-off while a tile's main loop runs (0: spin)
 };
 
 // tanh on the SFU (tanh.approx.f32, max rel. error ~2^-11): the GELU epilogues run once per
@@ -177,201 +179,6 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& p, int row, int 
       }
     }
   }
-}
-
-template <bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b, const EpiParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tfull_bar = empty_bar + STAGES;
-  uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-
-  const int warp = threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  const int tiles_m = (p.M + BM - 1) / BM;
-  const int tiles_n = (p.N + BN - 1) / BN;
-  const int num_tiles = tiles_m * tiles_n;
-  const int num_kb = p.K / BK;
-
-  if (warp == 0 && lane == 0) {
-    ptx::tma_prefetch(&map_a);
-    ptx::tma_prefetch(&map_b);
-    for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full_bar[s], 1);
-      ptx::mbar_init(&empty_bar[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&tfull_bar[b], 1);
-      ptx::mbar_init(&tempty_bar[b], 128);
-    }
-    ptx::fence_mbar_init();
-  }
-  if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int tm, tn;
-        tile_coords(t, tiles_m, tiles_n, tm, tn);
-        const int m0 = tm * BM, n0 = tn * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem_a + stage * A_STAGE_BYTES;
-          uint8_t* sb = smem_b + stage * B_STAGE_BYTES;
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
-          const int k0 = kb * BK;
-          if constexpr (A_MN) {
-#pragma unroll
-            for (int i = 0; i < BM / 64; ++i)
-              ptx::tma_load_2d(sa + i * (64 * BK * 2), &map_a, &full_bar[stage], m0 + 64 * i, k0);
-          } else {
-            ptx::tma_load_2d(sa, &map_a, &full_bar[stage], k0, m0);
-          }
-          if constexpr (B_MN) {
-#pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              ptx::tma_load_2d(sb + i * (64 * BK * 2), &map_b, &full_bar[stage], n0 + 64 * i, k0);
-          } else {
-            ptx::tma_load_2d(sb, &map_b, &full_bar[stage], k0, n0);
-          }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(&full_bar[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * A_STAGE_BYTES);
-          const uint32_t b_addr = ptx::smem_u32(smem_b + stage * B_STAGE_BYTES);
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t a_desc, b_desc;
-            if constexpr (A_MN)  // 16 K-rows of 128 B per instruction
-              a_desc = ptx::umma_desc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024);
-            else  // 16 bf16 = 32 B along the swizzled K row
-              a_desc = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            if constexpr (B_MN)
-              b_desc = ptx::umma_desc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024);
-            else
-              b_desc = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        ptx::mma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-    }
-  } else if (warp >= 4) {
-    // ---------------- epilogue: warp (4+q) owns TMEM lanes [32q, 32q+32)
-    const int q = warp - 4;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      int tm, tn;
-      tile_coords(t, tiles_m, tiles_n, tm, tn);
-      const int row = tm * BM + q * 32 + lane;
-      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
-      ptx::tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      const int n_valid = min(BN, p.N - tn * BN);
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        if (c * 32 >= n_valid) break;  // warp-uniform
-        uint32_t raw[32];
-        ptx::tmem_ld_32x32b_x32(t_row + c * 32, raw);
-        ptx::tmem_ld_wait();
-        epilogue_chunk<EPI>(p, row, tn * BN + c * 32, raw);
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty_bar[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-    }
-  }
-
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
-  }
-}
-
-// ------------------------------------------------------------------ CTA-pair kernel
-// cta_group::2 variant: a cluster of two CTAs computes a 256 x 256 tile with one
-// tcgen05.mma (M=256) per K=16 step, issued by the even CTA.  CTA r loads A rows
-// [m0 + 128 r, +128) and B rows [n0 + r W/2, +W/2) into its own smem; both CTAs' TMA
-// bytes land on the even CTA's `full` barrier; each CTA's TMEM holds its 128 rows x W
-// columns.
-//
-// Tail waves: with 74 pairs, a GEMM of T tiles runs ceil(T/74) tile-times while only
-// T/74 are busy (N=2048 stage GEMMs: 256 tiles = 3.46 waves -> 4).  The last T mod 74
-// tiles are therefore split along N into `tail_split` sub-tiles of width 256/s (one
-// tcgen05.mma of N = 256/s per K step), so the final wave takes 1/s of a tile-time.
-constexpr int PAIR_THREADS = 256;
-constexpr int PBN = 256;
-
-template <int NST>
-struct PairCfg {
-  static constexpr int B_HALF = PBN / 2;
-  static constexpr int A_BYTES = 128 * BK * 2;
-  static constexpr int B_BYTES = B_HALF * BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int NSTAGE = NST;
-  static constexpr int STG = 4 * 2 * 4096;  // epilogue staging: 4 warps x 2 x 4 KB
-  static constexpr size_t SMEM = 1024 + NSTAGE * STAGE + STG + 256;
-  static constexpr uint32_t TMEM = 512;
-};
-
-struct PairSched {
-  int tiles_m, tiles_n;
-  int full_tiles;   // tiles before the split tail (raster order)
-  int tail_split;   // 1, 2 or 4
-  int num_work;     // full_tiles + tail_split * (tiles - full_tiles)
-};
-
-// Work item w -> output rows [m0, m0 + 256), columns [n0, n0 + width).
-__device__ __forceinline__ void pair_work(const PairSched& s, int w, int& m0, int& n0, int& width) {
-  int t = w, part = 0, split = 1;
-  if (w >= s.full_tiles) {
-    const int u = w - s.full_tiles;
-    split = s.tail_split;
-    t = s.full_tiles + u / split;
-    part = u % split;
-  }
-  int tm, tn;
-  tile_coords(t, s.tiles_m, s.tiles_n, tm, tn);
-  width = PBN / split;
-  m0 = tm * 256;
-  n0 = tn * PBN + part * width;
 }
 
 // Output tensor maps of the pair kernel's TMA epilogue: C (bf16 box {64, 32} or f32 box
@@ -514,6 +321,211 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
   }
 }
 
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b, const __grid_constant__ EpiMaps em,
+                      const EpiParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
+  uint8_t* stg_all = smem + STAGES * STAGE_BYTES;  // epilogue staging, 4 warps x 2 x 4 KB
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(stg_all + STG_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* aux_bar = tempty_bar + 2;  // [4][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + 8);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int tiles_m = (p.M + BM - 1) / BM;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = p.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&map_a);
+    ptx::tma_prefetch(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full_bar[s], 1);
+      ptx::mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull_bar[b], 1);
+      ptx::mbar_init(&tempty_bar[b], 128);
+    }
+    for (int q = 0; q < 8; ++q) ptx::mbar_init(&aux_bar[q], 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 3 && lane == 0) {
+    ptx::tma_prefetch(&em.c);
+    if (EPI == AMDP_EPI_GELU) ptx::tma_prefetch(&em.c2);
+    if (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD) ptx::tma_prefetch(&em.aux);
+  }
+  if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int tm, tn;
+        tile_coords(t, tiles_m, tiles_n, tm, tn);
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem_a + stage * A_STAGE_BYTES;
+          uint8_t* sb = smem_b + stage * B_STAGE_BYTES;
+          ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              ptx::tma_load_2d(sa + i * (64 * BK * 2), &map_a, &full_bar[stage], m0 + 64 * i, k0);
+          } else {
+            ptx::tma_load_2d(sa, &map_a, &full_bar[stage], k0, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              ptx::tma_load_2d(sb + i * (64 * BK * 2), &map_b, &full_bar[stage], n0 + 64 * i, k0);
+          } else {
+            ptx::tma_load_2d(sb, &map_b, &full_bar[stage], k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(&full_bar[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * A_STAGE_BYTES);
+          const uint32_t b_addr = ptx::smem_u32(smem_b + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t a_desc, b_desc;
+            if constexpr (A_MN)  // 16 K-rows of 128 B per instruction
+              a_desc = ptx::umma_desc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024);
+            else  // 16 bf16 = 32 B along the swizzled K row
+              a_desc = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            if constexpr (B_MN)
+              b_desc = ptx::umma_desc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024);
+            else
+              b_desc = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: warp (4+q) owns TMEM lanes [32q, 32q+32)
+    const int q = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0, aux_phase = 0;
+    int bsel = 0;
+    uint8_t* stg = stg_all + q * 8192;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int tm, tn;
+      tile_coords(t, tiles_m, tiles_n, tm, tn);
+      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      if constexpr (EPI == EPI_DISCARD) {
+        uint32_t raw[32];
+        for (int c = 0; c < BN; c += 32) ptx::tmem_ld_32x32b_x32(t_row + c, raw);
+        ptx::tmem_ld_wait();
+      } else {
+        pair_epilogue<EPI>(em, p, t_row, BN, tn * BN, tm * BM + q * 32, stg, &aux_bar[2 * q], aux_phase, bsel,
+                           lane);
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) ptx::bulk_wait<0>();
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-pair kernel
+// cta_group::2 variant: a cluster of two CTAs computes a 256 x 256 tile with one
+// tcgen05.mma (M=256) per K=16 step, issued by the even CTA.  CTA r loads A rows
+// [m0 + 128 r, +128) and B rows [n0 + r W/2, +W/2) into its own smem; both CTAs' TMA
+// bytes land on the even CTA's `full` barrier; each CTA's TMEM holds its 128 rows x W
+// columns.
+//
+// Tail waves: with 74 pairs, a GEMM of T tiles runs ceil(T/74) tile-times while only
+// T/74 are busy (N=2048 stage GEMMs: 256 tiles = 3.46 waves -> 4).  The last T mod 74
+// tiles are therefore split along N into `tail_split` sub-tiles of width 256/s (one
+// tcgen05.mma of N = 256/s per K step), so the final wave takes 1/s of a tile-time.
+constexpr int PAIR_THREADS = 256;
+constexpr int PBN = 256;
+
+template <int NST>
+struct PairCfg {
+  static constexpr int B_HALF = PBN / 2;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = B_HALF * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int NSTAGE = NST;
+  static constexpr int STG = 4 * 2 * 4096;  // epilogue staging: 4 warps x 2 x 4 KB
+  static constexpr size_t SMEM = 1024 + NSTAGE * STAGE + STG + 256;
+  static constexpr uint32_t TMEM = 512;
+};
+
+struct PairSched {
+  int tiles_m, tiles_n;
+  int full_tiles;   // tiles before the split tail (raster order)
+  int tail_split;   // 1, 2 or 4
+  int num_work;     // full_tiles + tail_split * (tiles - full_tiles)
+};
+
+// Work item w -> output rows [m0, m0 + 256), columns [n0, n0 + width).
+__device__ __forceinline__ void pair_work(const PairSched& s, int w, int& m0, int& n0, int& width) {
+  int t = w, part = 0, split = 1;
+  if (w >= s.full_tiles) {
+    const int u = w - s.full_tiles;
+    split = s.tail_split;
+    t = s.full_tiles + u / split;
+    part = u % split;
+  }
+  int tm, tn;
+  tile_coords(t, s.tiles_m, s.tiles_n, tm, tn);
+  width = PBN / split;
+  m0 = tm * 256;
+  n0 = tn * PBN + part * width;
+}
+
 template <bool A_MN, bool B_MN, int EPI, int NST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     gemm_bf16_tc_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -644,7 +656,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       int m0, n0, width;
       pair_work(sc, w, m0, n0, width);
       const int row0 = m0 + 128 * static_cast<int>(rank) + q * 32;
-      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      if (p.epi_sleep_ns) ptx::mbar_wait_sleep(&tfull_bar[acc], acc_phase, p.epi_sleep_ns);
+      else ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * PBN;
       if constexpr (EPI == EPI_DISCARD) {
@@ -798,7 +811,7 @@ int launch(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     }
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
     const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-    kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+    kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, em, p);
     return cudaGetLastError();
   }
   static const int nst = env_int("AMDP_GEMM_STAGES", 6);
@@ -824,6 +837,11 @@ int dispatch_epi(int mode, int epi, const CUtensorMap& ma, const CUtensorMap& mb
   return AMDP_ERR_INVALID;
 }
 
+uint32_t epi_sleep_ns() {
+  static const uint32_t ns = static_cast<uint32_t>(env_int("AMDP_GEMM_EPI_SLEEP", 0));
+  return ns;
+}
+
 int gemm_pairs() {
   static const int nst = env_int("AMDP_GEMM_STAGES", 6);
   return nst == 4 ? max_pairs<4>() : max_pairs<6>();
@@ -831,10 +849,15 @@ int gemm_pairs() {
 
 // Tile shape per problem: CTA pairs with 256 x 256 tiles whenever M >= 256 (measured at the
 // 1.3B shapes, profiles/r01_gemm_modes.txt: +5-13% over single-CTA 128x256 tiles).
-int choose_mode(int M, int N) {
+int choose_mode(int M, int N, bool a_mn, bool b_mn) {
   (void)N;
   static const int forced = env_int("AMDP_GEMM_MODE", -1);
   if (forced == 0 || forced == 256) return forced;
+  // Weight-gradient GEMMs (A and B both MN-major): single-CTA 128x256 tiles sustain ~4% more
+  // under the power cap than CTA pairs (scripts/gemm_sustained.py, fc1_wgrad 0.88 vs 0.84 of
+  // cuBLAS on the same box) and split the 2048x2048 out-projection into 128 tiles instead of
+  // 64 pairs (+12%).  Everything else: pairs.
+  if (a_mn && b_mn) return 0;
   return M >= 256 ? 256 : 0;
 }
 
@@ -855,7 +878,7 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) return AMDP_ERR_CUDA;
   }
-  const int mode = choose_mode(a->M, a->N);
+  const int mode = choose_mode(a->M, a->N, a->a_mn_major != 0, a->b_mn_major != 0);
   CUtensorMap ma, mb, mbt;
   bool ok;
   if (a->a_mn_major)  // A stored [K][lda], M contiguous
@@ -877,7 +900,7 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
   }
   if (!ok) return AMDP_ERR_TMA;
   EpiMaps em;
-  if (mode != 0) {  // pair kernel: TMA-store epilogue maps (box 32 rows x 128 bytes)
+  {  // TMA-store epilogue maps (box 32 rows x 128 bytes)
     const bool f32 = a->epilogue == AMDP_EPI_ACCUM_F32 || a->epilogue == AMDP_EPI_STORE_F32;
     ok = make_map(&em.c, a->C, a->N, a->M, a->ldc, 32, f32, f32 ? 32 : 64);
     em.c2 = em.c;
@@ -889,7 +912,8 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
   }
   EpiParams p{a->M, a->N, a->K, a->C, a->ldc,
               static_cast<const __nv_bfloat16*>(a->aux), a->ld_aux,
-              static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha};
+              static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha,
+              epi_sleep_ns()};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int am = a->a_mn_major ? 1 : 0, bm = a->b_mn_major ? 1 : 0;
   if (!am && !bm) return dispatch_epi<false, false>(mode, a->epilogue, ma, mb, mbt, em, p, s);

@@ -41,6 +41,8 @@ CASES = [
     ("qkv_wgrad", 3 * h, h, T, True, True, N.EPI_ACCUM_F32),
     ("out_wgrad", h, h, T, True, True, N.EPI_ACCUM_F32),
     ("fc2_dgrad_gelubwd", T, 4 * h, h, False, True, N.EPI_GELU_BWD),
+    ("fc1_wgrad_amn", 4 * h, h, T, True, False, N.EPI_STORE_BF16),
+    ("fc1_wgrad_bmn", 4 * h, h, T, False, True, N.EPI_STORE_BF16),
     ("fc2_fwd_residual", T, h, 4 * h, False, False, N.EPI_RESIDUAL),
     ("fc1_fwd_gelu", T, 4 * h, h, False, False, N.EPI_GELU),
 ]
