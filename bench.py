@@ -258,6 +258,14 @@ def main():
     except Exception:
         logical_bubble = None
     phys_bubble = max_over_ranks(1.0 - busy_frac) if busy_frac is not None else None
+    projection = None
+    if world == 1 and args.steps > 2:
+        try:  # d-GPU projection of this measured run (static-order replay, reference bubble_ratio)
+            from paper_2605_29664_b200 import projection as PR
+            gap_ns = model.tokens_per_minibatch * model.hidden * 2 / 770e9 * 1e9
+            projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns)
+        except Exception as e:  # never let the projection break the bench line
+            projection = {"error": str(e)[:200]}
 
     # e2e through the public API with pinned host buffers
     barrier()
@@ -315,7 +323,8 @@ def main():
             "host_issue_ms_per_step": host_issue_ms / args.steps,
             "roofline": roofline,
             "model_flops_utilization": mfu,
-            "bubble": {"physical_gpu": phys_bubble, "logical_devices_bubble_ratio_w1": logical_bubble},
+            "bubble": {"physical_gpu": phys_bubble, "logical_devices_bubble_ratio_w1": logical_bubble,
+                       f"projected_d{args.depth}_gpus": projection},
             "kernels": kernels,
             "clocks": clk.summary()}
     if rank == 0:

@@ -1,0 +1,46 @@
+"""Static-order replay projection (paper_2605_29664_b200/projection.py), CPU only.
+
+With task costs equal to the declared cost model and no gap, re-timing the declared
+dispatch order must reproduce `simulate` exactly (the executor's order is a list schedule
+of those costs); with slower backward or an inter-device gap the replay can only get
+longer, and its events must satisfy the reference's causality / non-overlap validators."""
+from fractions import Fraction
+
+import pytest
+
+from paper_2605_29664_b200 import ppsim as P
+from paper_2605_29664_b200 import projection as PR
+
+
+def _pol(d, thr, windows):
+    return P.PolicyConfig(P.Policy.AMDP, 2, d // 2, thr, windows * thr, True)
+
+
+@pytest.mark.parametrize("d,thr,windows", [(4, 8, 3), (8, 32, 3), (2, 4, 4)])
+def test_replay_with_declared_costs_is_simulate(d, thr, windows):
+    pol = _pol(d, thr, windows)
+    costs = {(k, s): 1000.0 for k in (P.Kind.Forward, P.Kind.Backward) for s in range(d)}
+    rep = PR.static_order_replay(pol, d, costs, 0.0)
+    decl = P.ClusterSpec.uniform(d, d, 1, 1)
+    sim = P.simulate(P.build(pol, decl), decl)
+    a = sorted((e.device, e.kind, e.stage, e.minibatch, e.pipeline, e.start, e.duration) for e in rep.flat())
+    b = sorted((e.device, e.kind, e.stage, e.minibatch, e.pipeline, e.start * 1000, e.duration * 1000)
+               for e in sim.flat())
+    assert a == b
+    assert P.bubble_ratio(rep, 1) == P.bubble_ratio(sim, 1)
+
+
+def test_replay_slower_backward_and_gap_is_causal():
+    d, thr, windows = 8, 32, 3
+    pol = _pol(d, thr, windows)
+    costs = {}
+    for s in range(d):
+        costs[(P.Kind.Forward, s)] = 1000.0
+        costs[(P.Kind.Backward, s)] = 2100.0
+    base = PR.static_order_replay(pol, d, {k: 1000.0 for k in costs}, 0.0)
+    rep = PR.static_order_replay(pol, d, costs, 50.0)
+    cl = P.ClusterSpec(d, d, [Fraction(1000)] * d, [Fraction(2100)] * d, Fraction(0), Fraction(50))
+    assert P.validate_causality(rep, cl) == []
+    assert P.validate_non_overlap(rep) == []
+    assert max(e.finish() for e in rep.flat()) > max(e.finish() for e in base.flat())
+    assert 0 <= P.bubble_ratio(rep, 1) < 1
