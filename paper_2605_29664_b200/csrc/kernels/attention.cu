@@ -267,6 +267,26 @@ __global__ void attn_bwd_delta_vec_kernel(const bf16* __restrict__ out, const bf
   }
 }
 
+// delta for head dims whose 8-element chunk count is not a power of two (head_dim 80): one
+// thread per (token, head) row, 16-byte loads.
+__global__ void attn_bwd_delta_row_kernel(const bf16* __restrict__ out, const bf16* __restrict__ dout,
+                                          float* __restrict__ delta, int ntok, int seq, int H, int D) {
+  const int64_t rows = static_cast<int64_t>(ntok) * H;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < D; c += 8) {
+      float o[8], d[8];
+      load8(out + i * D + c, o);
+      load8(dout + i * D + c, d);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += o[e] * d[e];
+    }
+    const int tok = static_cast<int>(i / H), h = static_cast<int>(i % H);
+    delta[(static_cast<size_t>(tok / seq) * H + h) * seq + tok % seq] = s;
+  }
+}
+
 // ================================================================== backward dQ
 template <int D>
 __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
@@ -564,7 +584,7 @@ extern "C" int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse
   auto q = reinterpret_cast<const bf16*>(qkv);
   auto o = reinterpret_cast<bf16*>(out);
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  if ((head_dim == 64 || head_dim == 128) && seq % 256 == 0)  // tcgen05 path (256-query tiles)
+  if ((head_dim == 64 || head_dim == 80 || head_dim == 128) && seq % 256 == 0)  // tcgen05 path
     return attention_fwd_tc(q, o, lse, batch, seq, heads, head_dim, causal, s);
   switch (head_dim) {
     case 32: return launch_fwd<32>(q, o, lse, batch, seq, heads, causal, s);
@@ -591,12 +611,18 @@ extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, cons
   auto dq = reinterpret_cast<bf16*>(dqkv);
   auto w = static_cast<float*>(workspace);
   auto s = reinterpret_cast<cudaStream_t>(stream);
-  if ((head_dim == 64 || head_dim == 128) && seq % 128 == 0) {  // tcgen05 path
+  if ((head_dim == 64 || head_dim == 80 || head_dim == 128) && seq % 128 == 0) {  // tcgen05 path
     const int ntok = batch * seq;
     const int64_t chunks = static_cast<int64_t>(ntok) * heads * (head_dim / 8);
     int64_t blocks = (chunks + 255) / 256;
     if (blocks > 16 * num_sms()) blocks = 16 * num_sms();  // grid-stride; multiple of 256 threads
-    attn_bwd_delta_vec_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(o, d, w, ntok, seq, heads, head_dim);
+    if ((head_dim / 8) & (head_dim / 8 - 1)) {  // shuffle groups need a power-of-two chunk count
+      const int64_t rows = static_cast<int64_t>(ntok) * heads;
+      attn_bwd_delta_row_kernel<<<static_cast<int>(std::min<int64_t>((rows + 255) / 256, 16 * num_sms())), 256, 0, s>>>(
+          o, d, w, ntok, seq, heads, head_dim);
+    } else {
+      attn_bwd_delta_vec_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(o, d, w, ntok, seq, heads, head_dim);
+    }
     return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, s);
   }
   switch (head_dim) {

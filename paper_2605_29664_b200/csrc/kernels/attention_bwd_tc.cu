@@ -66,6 +66,29 @@ __device__ __forceinline__ void tmem_row_to_global(uint32_t src, bf16* dst, floa
       store8(dst + c * 32 + 8 * u, f);
     }
   }
+  constexpr int T0 = (NCOLS / 32) * 32;  // head_dim 80: 16- / 8-column tails
+  if constexpr (NCOLS % 32 >= 16) {
+    uint32_t a[16];
+    ptx::tmem_ld_32x32b_x16(src + T0, a);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      float f[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * u + e]) * mul;
+      store8(dst + T0 + 8 * u, f);
+    }
+  }
+  if constexpr (NCOLS % 16 == 8) {
+    constexpr int T1 = T0 + (NCOLS % 32 >= 16 ? 16 : 0);
+    uint32_t a[8];
+    ptx::tmem_ld_32x32b_x8(src + T1, a);
+    ptx::tmem_ld_wait();
+    float f[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[e]) * mul;
+    store8(dst + T1, f);
+  }
 }
 
 // ==================================================================== dK / dV
@@ -76,10 +99,12 @@ __device__ __forceinline__ void tmem_row_to_global(uint32_t src, bf16* dst, floa
 // half-block MMA groups ahead of its first use; lse / delta are read from L2 (broadcast).
 constexpr uint32_t T64 = 8192;  // [64 rows][64 bf16] SW128 tile
 
+// head_dim 80 uses the 128-wide layout (two SW128 boxes per row tile; see attention_tc.cu):
+// K-dim loops run D/16 steps, the D-wide outputs are N = D MMAs, TMEM keeps 128-column slots.
 template <int D>
 struct KvSmem {
-  static constexpr int NB = D / 64;
-  static constexpr int NU = D == 128 ? 5 : 10;        // half-block units in flight
+  static constexpr int NB = (D + 63) / 64;
+  static constexpr int NU = NB == 2 ? 5 : 10;         // half-block units in flight
   static constexpr uint32_t UNIT = 2 * NB * T64;      // Q half, dO half
   static constexpr uint32_t K = 0;
   static constexpr uint32_t V = K + NB * T128;
@@ -141,8 +166,8 @@ __global__ void __launch_bounds__(384, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // TMEM: S^T_a at 0, S^T_b at 64 (P^T_x bf16 pairs over their first 32 columns),
-  // dP^T_a at 128, dP^T_b at 192 (dS^T_x likewise), dV at 256, dK at 256 + D
-  const uint32_t t_dv = tmem + 256, t_dk = tmem + 256 + D;
+  // dP^T_a at 128, dP^T_b at 192 (dS^T_x likewise), dV at 256, dK at 256 + 64 NB
+  const uint32_t t_dv = tmem + 256, t_dk = tmem + 256 + 64 * L::NB;
 
   if (warp == 0) {
     ptx::regs_dec<56>();
@@ -157,6 +182,9 @@ __global__ void __launch_bounds__(384, 1)
         uint8_t* unit = sm + L::U + st * L::UNIT;
         ptx::mbar_wait(&u_empty[st], ((u / NU) & 1) ^ 1);
         BW_T(6, u);
+#ifdef FA_ABL_NOLOAD  // ablation: keep the ring's first fill, skip every later load
+        if (u >= NU) { ptx::mbar_arrive(&u_full[st]); continue; }
+#endif
         ptx::mbar_arrive_expect_tx(&u_full[st], L::UNIT);
         for (int c = 0; c < L::NB; ++c) {
           ptx::tma_load_2d(unit + c * T64, &qkv_map, &u_full[st], h * D + 64 * c, row0 + q0);
@@ -258,7 +286,11 @@ __global__ void __launch_bounds__(384, 1)
                                make_float2(-lq.x, -lq.y));
         float2 x1 = __ffma2_rn(make_float2(__uint_as_float(s[cc + 2]), __uint_as_float(s[cc + 3])), c2,
                                make_float2(-lq.z, -lq.w));
+#ifdef FA_ABL_NOSOFT
+        float2 p0 = x0, p1 = x1;
+#else
         float2 p0 = make_float2(ex2(x0.x), ex2(x0.y)), p1 = make_float2(ex2(x1.x), ex2(x1.y));
+#endif
         if (diag) {  // query < key is masked
           if (qbase + cc < key) p0.x = 0.f;
           if (qbase + cc + 1 < key) p0.y = 0.f;
@@ -306,11 +338,11 @@ __global__ void __launch_bounds__(384, 1)
 // ==================================================================== dQ
 template <int D>
 struct QSmem {
-  static constexpr int NB = D / 64;
+  static constexpr int NB = (D + 63) / 64;
   // K is held from S(j) until dQ(j) (one block later), V only until dP(j): separate rings.
   // Q lives in TMEM (S = Q K^T is a TS MMA), which frees the smem for a 4-deep K ring: K
   // loads start ~3 blocks ahead of use, covering the ~3k-cycle TMA latency under load.
-  static constexpr int NSK = D == 128 ? 4 : 8, NSV = D == 128 ? 2 : 4;
+  static constexpr int NSK = NB == 2 ? 4 : 8, NSV = NB == 2 ? 2 : 4;
   static constexpr uint32_t DO = 0;
   static constexpr uint32_t K = DO + NB * T128;   // NSK stages of NB x T128
   static constexpr uint32_t V = K + NSK * NB * T128;
@@ -375,9 +407,9 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: S at 0, dP at 128, dQ at 256, dS (bf16 pairs, 64 columns) at 256 + D,
-  // Q (bf16 pairs, D / 2 columns) at 320 + D
-  const uint32_t t_dq = tmem + 256, t_ds = tmem + 256 + D, t_q = tmem + 320 + D;
+  // TMEM: S at 0, dP at 128, dQ at 256, dS (bf16 pairs, 64 columns) at 256 + 64 NB,
+  // Q (bf16 pairs, D / 2 columns) at 320 + 64 NB
+  const uint32_t t_dq = tmem + 256, t_ds = tmem + 256 + 64 * L::NB, t_q = tmem + 320 + 64 * L::NB;
   if (threadIdx.x == 0) BW_T(7, 0);
 
   if (warp == 0) {
@@ -391,6 +423,14 @@ __global__ void __launch_bounds__(384, 1)
         const int sk = n % NSK, sv = n % NSV;
         ptx::mbar_wait(&k_empty[sk], ((n / NSK) & 1) ^ 1);
         BW_T(6, n);
+#ifdef FA_ABL_NOLOAD
+        if (n >= NSK) {
+          ptx::mbar_arrive(&k_full[sk]);
+          ptx::mbar_wait(&v_empty[sv], ((n / NSV) & 1) ^ 1);
+          ptx::mbar_arrive(&v_full[sv]);
+          continue;
+        }
+#endif
         ptx::mbar_arrive_expect_tx(&k_full[sk], L::NB * T128);
         for (int c = 0; c < L::NB; ++c)
           ptx::tma_load_2d(sm + L::K + (sk * L::NB + c) * T128, &qkv_map, &k_full[sk], H * D + h * D + 64 * c,
@@ -463,12 +503,15 @@ __global__ void __launch_bounds__(384, 1)
     const int c0 = 64 * wg;
     const size_t bh = (static_cast<size_t>(b) * H + h) * seq;
     const float nl = -lse[bh + qrow], dl = delta[bh + qrow];
-    {  // this thread's half of its Q row -> TMEM (bf16 pairs: column j holds dims 2j, 2j+1)
-      const uint4* src = reinterpret_cast<const uint4*>(qkv + (static_cast<size_t>(row0) + qrow) * (3 * H * D) +
-                                                        h * D + wg * (D / 2));
-      uint32_t qv[D / 4];
+    {  // this thread's half of its Q row -> TMEM (bf16 pairs: column j holds dims 2j, 2j+1).
+       // Warpgroup wg owns dims [32 (D/64) wg, +32 (D/64)) and, for head_dim 80, the tail dims
+       // [64 + 8 wg, +8): every TMEM access stays aligned to its own width.
+      constexpr int MAIN = 32 * (D / 64);  // dims per warpgroup in the 64-multiple part
+      const bf16* qrow_p = qkv + (static_cast<size_t>(row0) + qrow) * (3 * H * D) + h * D;
+      const uint4* src = reinterpret_cast<const uint4*>(qrow_p + wg * MAIN);
+      uint32_t qv[MAIN / 2];
 #pragma unroll
-      for (int u = 0; u < D / 16; ++u) {
+      for (int u = 0; u < MAIN / 8; ++u) {
         const uint4 t = src[u];
         qv[4 * u] = t.x;
         qv[4 * u + 1] = t.y;
@@ -476,7 +519,12 @@ __global__ void __launch_bounds__(384, 1)
         qv[4 * u + 3] = t.w;
       }
 #pragma unroll
-      for (int u = 0; u < D / 64; ++u) tmem_st_x16(t_q + lanes + wg * (D / 4) + 16 * u, qv + 16 * u);
+      for (int u = 0; u < MAIN / 32; ++u) tmem_st_x16(t_q + lanes + wg * (MAIN / 2) + 16 * u, qv + 16 * u);
+      if constexpr (D % 64 == 16) {
+        const uint4 t = *reinterpret_cast<const uint4*>(qrow_p + 2 * MAIN + 8 * wg);
+        const uint32_t tv[4] = {t.x, t.y, t.z, t.w};
+        ptx::tmem_st_32x32b_x4(t_q + lanes + MAIN + 4 * wg, tv);
+      }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       ptx::mbar_arrive(q_full);
@@ -497,8 +545,13 @@ __global__ void __launch_bounds__(384, 1)
       uint32_t gg[32];
 #pragma unroll
       for (int cc = 0; cc < 64; cc += 2) {
+#ifdef FA_ABL_NOSOFT  // ablation: no exponentials / softmax math, dS = S + dP
+        float g0 = __uint_as_float(s[cc]) + __uint_as_float(d[cc]);
+        float g1 = __uint_as_float(s[cc + 1]) + __uint_as_float(d[cc + 1]);
+#else
         float g0 = ex2(fmaf(__uint_as_float(s[cc]), scale_log2, nl)) * (__uint_as_float(d[cc]) - dl);
         float g1 = ex2(fmaf(__uint_as_float(s[cc + 1]), scale_log2, nl)) * (__uint_as_float(d[cc + 1]) - dl);
+#endif
         if (diag) {
           const int k0 = n * 128 + c0 + cc;
           if (k0 > qrow) g0 = 0.f;
@@ -518,9 +571,11 @@ __global__ void __launch_bounds__(384, 1)
     }
     ptx::mbar_wait(dq_done, 0);
     ptx::tc_fence_after();
-    // each warpgroup writes half of the D columns
-    bf16* rowq = dqkv + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(3) * H * D) + h * D + wg * (D / 2);
-    tmem_row_to_global<D / 2>(t_dq + lanes + wg * (D / 2), rowq, scale);
+    // each warpgroup writes half of the D columns (head_dim 80: 32 + 8 each, aligned as above)
+    constexpr int MAIN = 32 * (D / 64);
+    bf16* rowq = dqkv + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(3) * H * D) + h * D;
+    tmem_row_to_global<MAIN>(t_dq + lanes + wg * MAIN, rowq + wg * MAIN, scale);
+    if constexpr (D % 64 == 16) tmem_row_to_global<8>(t_dq + lanes + 2 * MAIN + 8 * wg, rowq + 2 * MAIN + 8 * wg, scale);
   } else {
     ptx::regs_dec<56>();
   }
@@ -573,6 +628,7 @@ int attention_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const 
   if (S % 128 != 0) return AMDP_ERR_UNSUPPORTED;
   if (D == 128) return launch_bwd_tc<128>(qkv, dout, lse, delta, dqkv, B, S, H, causal, st);
   if (D == 64) return launch_bwd_tc<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, st);
+  if (D == 80) return launch_bwd_tc<80>(qkv, dout, lse, delta, dqkv, B, S, H, causal, st);
   return AMDP_ERR_UNSUPPORTED;
 }
 

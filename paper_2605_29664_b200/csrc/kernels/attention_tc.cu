@@ -43,10 +43,14 @@ __device__ long long* g_fa_cta = nullptr;
     if (dbg_ != nullptr && (j) < 64) dbg_[(slot)*64 + (j)] = clock64(); \
   } while (0)
 
+// head_dim 80 (GPT-2.7B) runs on the 128-wide layout: every row tile is two 64-column SW128
+// boxes (the second box's columns 80-127 belong to the next head and are never used), the
+// S = Q K^T reduction issues D/16 = 5 K-steps, and the PV / dV / dK / dQ MMAs use N = D = 80
+// (an MN-major B operand of 64 + 16 columns across the two boxes).
 template <int D>
 struct FaSmem {
-  static constexpr int NB = D / 64;                 // 64-wide column blocks per row tile
-  static constexpr int KVS = D == 128 ? 2 : 4;      // K / V ring depth
+  static constexpr int NB = (D + 63) / 64;          // 64-wide column blocks per row tile
+  static constexpr int KVS = NB == 2 ? 2 : 4;       // K / V ring depth
   static constexpr uint32_t Q = 0;                  // Q_A | Q_B
   static constexpr uint32_t K = Q + 2 * NB * TILE;
   static constexpr uint32_t V = K + KVS * NB * TILE;
@@ -372,6 +376,14 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
             ptx::tmem_st_32x32b_x32(to + c * 32, o);
           }
+          if constexpr (D % 32 == 16) {
+            uint32_t o[16];
+            ptx::tmem_ld_32x32b_x16(to + (D / 32) * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            ptx::tmem_st_32x32b_x16(to + (D / 32) * 32, o);
+          }
           l *= alpha;
           m_ref = m_new;
         }
@@ -399,6 +411,18 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(o[8 * u + e]) * inv;
           store8(orow + c * 32 + 8 * u, f);
+        }
+      }
+      if constexpr (D % 32 == 16) {
+        uint32_t o[16];
+        ptx::tmem_ld_32x32b_x16(to + (D / 32) * 32, o);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(o[8 * u + e]) * inv;
+          store8(orow + (D / 32) * 32 + 8 * u, f);
         }
       }
       ptx::tc_fence_before();
@@ -451,6 +475,7 @@ int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H
   if (S % FA_BQ != 0) return AMDP_ERR_UNSUPPORTED;
   if (D == 128) return launch_fa_fwd<128>(qkv, out, lse, B, S, H, causal, st);
   if (D == 64) return launch_fa_fwd<64>(qkv, out, lse, B, S, H, causal, st);
+  if (D == 80) return launch_fa_fwd<80>(qkv, out, lse, B, S, H, causal, st);
   return AMDP_ERR_UNSUPPORTED;
 }
 

@@ -2,7 +2,7 @@
 import sys, os, json, statistics, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_29664_b200 import kernels as K
-B, S, H, D = 4, 2048, 16, 128
+B, S, H, D = [int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (4, 2048, 16, 128))]
 qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
 dout = torch.randn(B * S, H * D, device="cuda").bfloat16()
 out, lse = K.attention_fwd(qkv, B, S, H, D)

@@ -4,7 +4,7 @@
 #include <cuda_runtime.h>
 #include "kernels/sm100_ptx.cuh"
 using namespace amdp;
-enum { SS_KK = 0, SS_KMN = 1, TS_MN = 2, SS_KK_N256 = 3, TS_MN_N64 = 4, SS_KK_N64 = 5, DQ_MIX = 6 };
+enum { SS_KK = 0, SS_KMN = 1, TS_MN = 2, SS_KK_N256 = 3, TS_MN_N64 = 4, SS_KK_N64 = 5, DQ_MIX = 6, DQ128_MIX = 7, TS_KK = 8 };
 template <int MODE>
 __global__ void probe(int rounds, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -26,6 +26,28 @@ __global__ void probe(int rounds, long long* out) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, N, false, bmn);
     long long t0 = clock64();
     for (int r = 0; r < rounds; ++r) {
+      if (MODE == DQ128_MIX) {  // current dQ block: S (TS N128) | dP (SS N128) | dQ (TS N128, B MN-major)
+        constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, false, false);
+        constexpr uint32_t id_g = ptx::idesc_bf16_f32(128, 128, false, true);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_bf16_ts(tmem, tmem + 448 + (kk & 7) * 8, ptx::umma_desc_sw128(b + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_bf16_ss(tmem + 128, ptx::umma_desc_sw128(a + (kk & 3) * 32, 16, 1024),
+                           ptx::umma_desc_sw128(b + (kk & 3) * 32, 16, 1024), id_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_bf16_ts(tmem + 256, tmem + 384 + kk * 8, ptx::umma_desc_sw128(b + kk * 2048, 16384, 1024), id_g, 1u);
+        continue;
+      }
+      if (MODE == TS_KK) {
+        constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, false, false);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          ptx::mma_bf16_ts(tmem, tmem + 448 + (kk & 7) * 8, ptx::umma_desc_sw128(b + (kk & 3) * 32, 16, 1024), id_s, 1u);
+        continue;
+      }
       if (MODE == DQ_MIX) {  // dQ kernel block: S, dP (M128 N64 K128, SS) + dQ (M128 N128 K64, TS)
         constexpr uint32_t id64 = ptx::idesc_bf16_f32(128, 64, false, false);
         constexpr uint32_t idg = ptx::idesc_bf16_f32(128, 128, false, true);
@@ -188,5 +210,7 @@ int main() {
   run<TS_MN_N64>("TS M128 N64 B MN-major", d);
   run<SS_KK_N64>("SS M128 N64 K/K-major", d);
   run<DQ_MIX>("dQ block (16 SS N64 + 4 TS N128) per 8", d);
+  run<TS_KK>("TS M128 N128 B K-major", d);
+  run<DQ128_MIX>("dQ128 block (8 TS + 8 SS + 8 TS, N128) per 8", d);
   return 0;
 }

@@ -129,7 +129,7 @@ def _attn_ref(qkv, B, S, H, D, causal):
     return o.permute(0, 2, 1, 3).reshape(B * S, H * D)
 
 
-@pytest.mark.parametrize("B,S,H,D", [(2, 128, 4, 32), (2, 256, 3, 64), (1, 192, 2, 80),
+@pytest.mark.parametrize("B,S,H,D", [(2, 128, 4, 32), (2, 256, 3, 64), (1, 192, 2, 80), (2, 512, 3, 80), (1, 2048, 2, 80),
                                      (2, 256, 2, 128), (4, 2048, 2, 128)])
 @pytest.mark.parametrize("causal", [True, False])
 def test_attention_fwd_bwd(K, B, S, H, D, causal):
