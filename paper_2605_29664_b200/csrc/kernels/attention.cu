@@ -248,6 +248,8 @@ __global__ void attn_bwd_delta_kernel(const bf16* __restrict__ out, const bf16* 
 // (token, head) reduce with shuffles (groups never straddle a warp).
 __global__ void attn_bwd_delta_vec_kernel(const bf16* __restrict__ out, const bf16* __restrict__ dout,
                                           float* __restrict__ delta, int ntok, int seq, int H, int D) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   const int G = D / 8;
   const int64_t chunks = static_cast<int64_t>(ntok) * H * G;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < chunks;
@@ -271,6 +273,8 @@ __global__ void attn_bwd_delta_vec_kernel(const bf16* __restrict__ out, const bf
 // thread per (token, head) row, 16-byte loads.
 __global__ void attn_bwd_delta_row_kernel(const bf16* __restrict__ out, const bf16* __restrict__ dout,
                                           float* __restrict__ delta, int ntok, int seq, int H, int D) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   const int64_t rows = static_cast<int64_t>(ntok) * H;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -618,10 +622,10 @@ extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, cons
     if (blocks > 16 * num_sms()) blocks = 16 * num_sms();  // grid-stride; multiple of 256 threads
     if ((head_dim / 8) & (head_dim / 8 - 1)) {  // shuffle groups need a power-of-two chunk count
       const int64_t rows = static_cast<int64_t>(ntok) * heads;
-      attn_bwd_delta_row_kernel<<<static_cast<int>(std::min<int64_t>((rows + 255) / 256, 16 * num_sms())), 256, 0, s>>>(
+      launch_pdl(attn_bwd_delta_row_kernel, dim3(static_cast<int>(std::min<int64_t>((rows + 255) / 256, 16 * num_sms()))), dim3(256), 0, s, 
           o, d, w, ntok, seq, heads, head_dim);
     } else {
-      attn_bwd_delta_vec_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(o, d, w, ntok, seq, heads, head_dim);
+      launch_pdl(attn_bwd_delta_vec_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0, s, o, d, w, ntok, seq, heads, head_dim);
     }
     return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, s);
   }

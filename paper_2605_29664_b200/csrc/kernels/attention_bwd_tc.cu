@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
   // TMEM: S^T_a at 0, S^T_b at 64 (P^T_x bf16 pairs over their first 32 columns),
   // dP^T_a at 128, dP^T_b at 192 (dS^T_x likewise), dV at 256, dK at 256 + 64 NB
   const uint32_t t_dv = tmem + 256, t_dk = tmem + 256 + 64 * L::NB;
@@ -407,6 +409,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
   // TMEM: S at 0, dP at 128, dQ at 256, dS (bf16 pairs, 64 columns) at 256 + 64 NB,
   // Q (bf16 pairs, D / 2 columns) at 320 + 64 NB
   const uint32_t t_dq = tmem + 256, t_ds = tmem + 256 + 64 * L::NB, t_q = tmem + 320 + 64 * L::NB;
@@ -613,11 +617,12 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
     attr = true;
   }
   const int nt = S / 128;
-  fa_bwd_dkdv_kernel<D><<<nt * H * B, 384, smem_kv, st>>>(q128, q64, o64, lse, delta, dqkv, S, H, nt, scale_log2, scale,
-                                                          causal);
-  fa_bwd_dq_kernel<D><<<nt * H * B, 384, smem_q, st>>>(q128, o128, qkv, lse, delta, dqkv, S, H, nt, scale_log2,
-                                                       scale, causal);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(fa_bwd_dkdv_kernel<D>, dim3(nt * H * B), dim3(384), smem_kv, st, q128, q64, o64, lse,
+                             delta, dqkv, S, H, nt, scale_log2, scale, causal);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(fa_bwd_dq_kernel<D>, dim3(nt * H * B), dim3(384), smem_q, st, q128, o128, qkv, lse, delta, dqkv, S, H,
+                 nt, scale_log2, scale, causal);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace

@@ -203,6 +203,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();
+  ptx::pdl_trigger();
   if (dbg_ != nullptr && threadIdx.x == 0) dbg_[10 * 64] = clock64();
   // register split: the softmax warpgroups hold a whole 128-column S row in registers
   // (setmaxnreg placed inside each role branch so it dominates that role's code)
@@ -463,8 +465,9 @@ int launch_fa_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, i
   const int n_qt = S / FA_BQ;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   const int grid = std::min(n_qt * H * B, num_sms());
-  k<<<grid, FA_THREADS, smem, st>>>(map, out, lse, S, H, H * B, n_qt, scale_log2, causal);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(k, dim3(grid), dim3(FA_THREADS), smem, st, map, out, lse, S, H, H * B, n_qt, scale_log2,
+                             causal);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace

@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "amdp_kernels.h"
+#include "common.cuh"
 #include "sm100_ptx.cuh"
 
 namespace amdp {
@@ -370,6 +371,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();  // setup above overlapped the previous kernel's tail (PDL)
+  ptx::pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -575,6 +578,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ptx::pdl_wait();  // setup above overlapped the previous kernel's tail (PDL)
+  ptx::pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -792,8 +797,8 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int pairs = max_pairs<NST>();
   const PairSched sc = pair_schedule(p.M, p.N, B_MN, pairs);
   const int grid = 2 * (sc.num_work < pairs ? sc.num_work : pairs);
-  kern<<<grid, PAIR_THREADS, PairCfg<NST>::SMEM, s>>>(ma, mb, mbt, em, p, sc);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(PAIR_THREADS), PairCfg<NST>::SMEM, s, ma, mb, mbt, em, p, sc);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // MODE 0: single-CTA 128x256 tiles; MODE 256: CTA-pair 256x256 tiles (+ split tail).
@@ -811,8 +816,8 @@ int launch(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     }
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
     const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-    kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, em, p);
-    return cudaGetLastError();
+    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, s, ma, mb, em, p);
+    return e != cudaSuccess ? e : cudaGetLastError();
   }
   static const int nst = env_int("AMDP_GEMM_STAGES", 6);
   if (nst == 4) return launch_pair<A_MN, B_MN, EPI, 4>(ma, mb, mbt, em, p, s);

@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(
     const bf16* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
     bf16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows,
     int cols, float eps) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   const int lane = threadIdx.x & 31;
   const int warps = blockDim.x >> 5;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < rows; row += gridDim.x * warps) {
@@ -299,6 +301,8 @@ __global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
     const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ gamma,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, const bf16* resid_grad, bf16* dx,
     float* __restrict__ part, int rows, int cols) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   __shared__ float red[2][2 * RG * 32];
   const int nw = blockDim.x >> 5;
   const int c = threadIdx.x * 8;
@@ -363,6 +367,8 @@ __global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
 // CTA = 32 columns x 8 row-lanes; fixed summation order, so the gradient is deterministic.
 __global__ void __launch_bounds__(256) layernorm_dgb_reduce_kernel(const float* __restrict__ part, int nparts,
                                                                    int cols, float* dgamma, float* dbeta) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   __shared__ float red[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int col = blockIdx.x * 32 + lane;  // in [0, 2*cols)
@@ -386,6 +392,8 @@ __global__ void __launch_bounds__(256) layernorm_dgb_reduce_kernel(const float* 
 __global__ void embedding_fwd_kernel(const int32_t* __restrict__ tok, const bf16* __restrict__ wte,
                                      const bf16* __restrict__ wpe, bf16* __restrict__ x, int ntok,
                                      int seq, int hidden) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   const int vecs = hidden / 8;
   const int64_t total = static_cast<int64_t>(ntok) * vecs;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -404,6 +412,8 @@ __global__ void embedding_fwd_kernel(const int32_t* __restrict__ tok, const bf16
 __global__ void embedding_bwd_tok_kernel(const int32_t* __restrict__ tok,
                                          const bf16* __restrict__ dx, float* dwte, int ntok,
                                          int hidden) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   const int vecs = hidden / 8;
   const int64_t total = static_cast<int64_t>(ntok) * vecs;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -420,6 +430,8 @@ __global__ void embedding_bwd_tok_kernel(const int32_t* __restrict__ tok,
 
 __global__ void embedding_bwd_pos_kernel(const bf16* __restrict__ dx, float* dwpe, int ntok,
                                          int seq, int hidden) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   const int vecs = hidden / 8;
   const int batch = ntok / seq;
   const int total = seq * vecs;
@@ -445,6 +457,8 @@ __global__ void embedding_bwd_pos_kernel(const bf16* __restrict__ dx, float* dwp
 __global__ void __launch_bounds__(512) xent_kernel(bf16* logits, const int32_t* __restrict__ labels,
                                                    float* loss_sum, int vocab, int ld,
                                                    float scale) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   __shared__ float sm_m[16], sm_s[16];
   __shared__ float row_lse;
   const int row = blockIdx.x;
@@ -534,10 +548,10 @@ extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const f
     return cudaGetLastError();
   }
   const int nv = (cols + 255) / 256;
-  if (nv <= 1) layernorm_fwd_kernel<1><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
-  else if (nv <= 4) layernorm_fwd_kernel<4><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
-  else if (nv <= 8) layernorm_fwd_kernel<8><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
-  else layernorm_fwd_kernel<LN_MAX_VEC><<<blocks, 256, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+  if (nv <= 1) launch_pdl(layernorm_fwd_kernel<1>, dim3(blocks), dim3(256), 0, st, xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+  else if (nv <= 4) launch_pdl(layernorm_fwd_kernel<4>, dim3(blocks), dim3(256), 0, st, xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+  else if (nv <= 8) launch_pdl(layernorm_fwd_kernel<8>, dim3(blocks), dim3(256), 0, st, xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
+  else launch_pdl(layernorm_fwd_kernel<LN_MAX_VEC>, dim3(blocks), dim3(256), 0, st, xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
   return cudaGetLastError();
 }
 
@@ -566,10 +580,10 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
     if (!workspace) return AMDP_ERR_INVALID;
     const int grid = ln_bwd_ctas(rows);
     float* part = static_cast<float*>(workspace);
-    layernorm_bwd_rows_kernel<2><<<grid, cols / 8, 0, s>>>(
+    launch_pdl(layernorm_bwd_rows_kernel<2>, dim3(grid), dim3(cols / 8), 0, s, 
         reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(x), gamma, mean, rstd,
         reinterpret_cast<const bf16*>(resid_grad), reinterpret_cast<bf16*>(dx), part, rows, cols);
-    layernorm_dgb_reduce_kernel<<<(2 * cols + 31) / 32, 256, 0, s>>>(part, grid, cols, dgamma, dbeta);
+    launch_pdl(layernorm_dgb_reduce_kernel, dim3((2 * cols + 31) / 32), dim3(256), 0, s, part, grid, cols, dgamma, dbeta);
     return cudaGetLastError();
   }
   int blocks = (rows + 7) / 8;
@@ -599,7 +613,7 @@ extern "C" int amdp_embedding_fwd(const int32_t* tokens, const uint16_t* wte, co
   const int64_t work = static_cast<int64_t>(ntok) * (hidden / 8);
   int blocks = static_cast<int>((work + 255) / 256);
   if (blocks > 16 * num_sms()) blocks = 16 * num_sms();
-  embedding_fwd_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  launch_pdl(embedding_fwd_kernel, dim3(blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 
       tokens, reinterpret_cast<const bf16*>(wte), reinterpret_cast<const bf16*>(wpe),
       reinterpret_cast<bf16*>(x), ntok, seq, hidden);
   return cudaGetLastError();
@@ -613,10 +627,10 @@ extern "C" int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, flo
   const int64_t work = static_cast<int64_t>(ntok) * (hidden / 8);
   int blocks = static_cast<int>((work + 255) / 256);
   if (blocks > 16 * num_sms()) blocks = 16 * num_sms();
-  embedding_bwd_tok_kernel<<<blocks, 256, 0, s>>>(tokens, reinterpret_cast<const bf16*>(dx), dwte,
+  launch_pdl(embedding_bwd_tok_kernel, dim3(blocks), dim3(256), 0, s, tokens, reinterpret_cast<const bf16*>(dx), dwte,
                                                   ntok, hidden);
   const int pwork = seq * (hidden / 8);
-  embedding_bwd_pos_kernel<<<(pwork + 255) / 256, 256, 0, s>>>(reinterpret_cast<const bf16*>(dx),
+  launch_pdl(embedding_bwd_pos_kernel, dim3((pwork + 255) / 256), dim3(256), 0, s, reinterpret_cast<const bf16*>(dx),
                                                                dwpe, ntok, seq, hidden);
   return cudaGetLastError();
 }
@@ -624,7 +638,7 @@ extern "C" int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, flo
 extern "C" int amdp_xent_fwd_bwd(uint16_t* logits, const int32_t* labels, float* loss_sum,
                                  int ntok, int vocab, int ld, float scale, amdp_stream_t stream) {
   if (ntok <= 0 || vocab % 8 != 0 || ld % 8 != 0 || ld < vocab) return AMDP_ERR_INVALID;
-  xent_kernel<<<ntok, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  launch_pdl(xent_kernel, dim3(ntok), dim3(512), 0, reinterpret_cast<cudaStream_t>(stream), 
       reinterpret_cast<bf16*>(logits), labels, loss_sum, vocab, ld, scale);
   return cudaGetLastError();
 }

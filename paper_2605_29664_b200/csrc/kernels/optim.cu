@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(256) opt_kernel(OptK o, float* __restrict__ th
                                                   float* __restrict__ m, float* __restrict__ v,
                                                   float* __restrict__ grad, bf16* __restrict__ w,
                                                   int64_t n) {
+  grid_dep_wait();  // PDL: predecessor's outputs visible from here
+  grid_dep_trigger();
   const int64_t n4 = n / 4;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
@@ -166,7 +168,7 @@ extern "C" int amdp_optimizer_step(const amdp_opt_args* a, float* master, float*
   // SGD never touches m/v; keep the kernel branch-free on pointer validity.
   float* mm = m ? m : grad;
   float* vv = v ? v : grad;
-  opt_kernel<<<grid_for(n / 4 + 1, 8), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  launch_pdl(opt_kernel, dim3(grid_for(n / 4 + 1, 8)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 
       o, master, mm, vv, grad, reinterpret_cast<bf16*>(weight_bf16), n);
   return cudaGetLastError();
 }

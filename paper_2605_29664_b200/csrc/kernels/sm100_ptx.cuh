@@ -61,6 +61,12 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
   while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 
+// Programmatic dependent launch: the kernel may start while its predecessor in the stream
+// drains; it must not touch the predecessor's outputs (or buffers it still reads) before
+// pdl_wait().  pdl_trigger() lets the successor launch as soon as every CTA got here.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
