@@ -14,7 +14,11 @@
 // The backward softmax is elementwise given lse and delta, so the two softmax warpgroups
 // split each block by columns and no cross-thread reduction is needed.
 // tcgen05.mma issue blocks once ~5 MMAs are queued (the issuing thread runs at the pipe's
-// pace), so each kernel issues its MMA groups in the order their inputs become ready.
+// pace), so each kernel issues its MMA groups in the order their inputs become ready.  The
+// issuing warp runs converged and elect.sync picks the lane inside each MMA's asm: with a
+// single-lane branch the compiler wrapped every UTCHMMA in an ELECT / R2UR.BROADCAST /
+// BRA.U.ANY loop (~15 instructions), which made issue, not the tensor pipe, the limit for
+// the N=64 / N=128 MMAs here (dQ kernel 166 -> 146 us).
 // lse / delta use the forward's log2-domain convention (softmax scale folded in);
 // delta = rowsum(dO * O) comes from attn_bwd_delta_vec_kernel (attention.cu).
 #include "common.cuh"
@@ -196,10 +200,11 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     ptx::regs_dec<56>();
-    if (lane == 0) {
+    {  // warp-wide MMA issue (elect.sync inside the asm; see mma_bf16_*_w)
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 64, false, false);
       constexpr uint32_t id_g = ptx::idesc_bf16_f32(128, D, false, true);
-      const uint32_t sk = ptx::smem_u32(sm + L::K), sv = ptx::smem_u32(sm + L::V);
+      const uint64_t dk0 = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K), 16, 1024);
+      const uint64_t dv0 = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::V), 16, 1024);
       auto unit = [&](int u) { return ptx::smem_u32(sm + L::U + (u % NU) * L::UNIT); };
       // S^T_x, dP^T_x of half-unit u (x = u & 1) into columns 64x / 128 + 64x
       auto issue_s = [&](int u) {
@@ -207,20 +212,19 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_wait(&u_full[u % NU], (u / NU) & 1);
         BW_T(0, u);
         ptx::tc_fence_after();
-        const uint32_t sq = unit(u), sdo = sq + L::NB * T64;
+        const uint64_t dq = ptx::umma_desc_sw128(unit(u), 16, 1024);
+        const uint64_t ddo = dq + ((L::NB * T64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * T128 + (kk & 3) * 32, ob = (kk >> 2) * T64 + (kk & 3) * 32;
-          ptx::mma_bf16_ss(tmem + 64 * x, ptx::umma_desc_sw128(sk + oa, 16, 1024),
-                           ptx::umma_desc_sw128(sq + ob, 16, 1024), id_s, kk > 0);
+          const uint32_t oa = ((kk >> 2) * T128 + (kk & 3) * 32) >> 4, ob = ((kk >> 2) * T64 + (kk & 3) * 32) >> 4;
+          ptx::mma_bf16_ss_w(tmem + 64 * x, dk0 + oa, dq + ob, id_s, kk > 0);
         }
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * T128 + (kk & 3) * 32, ob = (kk >> 2) * T64 + (kk & 3) * 32;
-          ptx::mma_bf16_ss(tmem + 128 + 64 * x, ptx::umma_desc_sw128(sv + oa, 16, 1024),
-                           ptx::umma_desc_sw128(sdo + ob, 16, 1024), id_s, kk > 0);
+          const uint32_t oa = ((kk >> 2) * T128 + (kk & 3) * 32) >> 4, ob = ((kk >> 2) * T64 + (kk & 3) * 32) >> 4;
+          ptx::mma_bf16_ss_w(tmem + 128 + 64 * x, dv0 + oa, ddo + ob, id_s, kk > 0);
         }
-        ptx::mma_commit(&s_full[x]);
+        ptx::mma_commit_w(&s_full[x]);
         BW_T(1, u);
       };
       // dV += P^T_x dO_x, dK += dS^T_x Q_x (K = 64 queries; P^T / dS^T from TMEM)
@@ -229,16 +233,15 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_wait(&p_full[x], (u >> 1) & 1);
         BW_T(2, u);
         ptx::tc_fence_after();
-        const uint32_t sq = unit(u), sdo = sq + L::NB * T64;
+        const uint64_t dq = ptx::umma_desc_sw128(unit(u), T64, 1024);
+        const uint64_t ddo = dq + ((L::NB * T64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          ptx::mma_bf16_ts(t_dv, tmem + 64 * x + kk * 8, ptx::umma_desc_sw128(sdo + kk * 2048, T64, 1024), id_g,
-                           (u > 0 || kk > 0));
+          ptx::mma_bf16_ts_w(t_dv, tmem + 64 * x + kk * 8, ddo + ((kk * 2048) >> 4), id_g, (u > 0 || kk > 0));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          ptx::mma_bf16_ts(t_dk, tmem + 128 + 64 * x + kk * 8, ptx::umma_desc_sw128(sq + kk * 2048, T64, 1024), id_g,
-                           (u > 0 || kk > 0));
-        ptx::mma_commit(&u_empty[u % NU]);
+          ptx::mma_bf16_ts_w(t_dk, tmem + 128 + 64 * x + kk * 8, dq + ((kk * 2048) >> 4), id_g, (u > 0 || kk > 0));
+        ptx::mma_commit_w(&u_empty[u % NU]);
         BW_T(3, u);
       };
       ptx::mbar_wait(kv_full, 0);
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(384, 1)
         issue_g(u);
         if (u + 2 < U) issue_s(u + 2);
       }
-      ptx::mma_commit(kv_done);
+      ptx::mma_commit_w(kv_done);
     }
   } else if (warp >= 4) {
     ptx::regs_inc<224>();
@@ -448,54 +451,54 @@ __global__ void __launch_bounds__(384, 1)
     }
   } else if (warp == 1) {
     ptx::regs_dec<56>();
-    if (lane == 0) {
+    {  // warp-wide MMA issue (elect.sync inside the asm; see mma_bf16_*_w)
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t id_g = ptx::idesc_bf16_f32(128, D, false, true);
       const uint32_t sdo = ptx::smem_u32(sm + L::DO);
       ptx::mbar_wait(q_full, 0);
       ptx::mbar_wait(do_full, 0);
+      // warp-wide issue (see mma_bf16_*_w); descriptors built once per stage and advanced by
+      // adding the 16-byte-unit offset to their address field (smem < 256 KB: no carry)
+      const uint64_t dsdo = ptx::umma_desc_sw128(sdo, 16, 1024);
       for (int n = 0; n <= N; ++n) {
-        if (n < N) {  // S(n), dP(n) once the softmax threads hold S(n-1) / dP(n-1) in registers
+        if (n < N) {
           const int stk = n % NSK, stv = n % NSV;
           ptx::mbar_wait(&k_full[stk], (n / NSK) & 1);
           BW_T(0, n);
           ptx::mbar_wait(s_empty, (n & 1) ^ 1);
           BW_T(1, n);
           ptx::tc_fence_after();
-          const uint32_t sk = ptx::smem_u32(sm + L::K + stk * L::NB * T128);
-          const uint32_t sv = ptx::smem_u32(sm + L::V + stv * L::NB * T128);
+          const uint64_t dk = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K + stk * L::NB * T128), 16, 1024);
+          const uint64_t dv = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::V + stv * L::NB * T128), 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
-            ptx::mma_bf16_ts(tmem, t_q + kk * 8, ptx::umma_desc_sw128(sk + (kk >> 2) * T128 + (kk & 3) * 32, 16, 1024),
-                             id_s, kk > 0);
+            ptx::mma_bf16_ts_w(tmem, t_q + kk * 8, dk + (((kk >> 2) * T128 + (kk & 3) * 32) >> 4), id_s, kk > 0);
           ptx::mbar_wait(&v_full[stv], (n / NSV) & 1);
           ptx::tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t o = (kk >> 2) * T128 + (kk & 3) * 32;
-            ptx::mma_bf16_ss(tmem + 128, ptx::umma_desc_sw128(sdo + o, 16, 1024),
-                             ptx::umma_desc_sw128(sv + o, 16, 1024), id_s, kk > 0);
+            const uint32_t o = ((kk >> 2) * T128 + (kk & 3) * 32) >> 4;
+            ptx::mma_bf16_ss_w(tmem + 128, dsdo + o, dv + o, id_s, kk > 0);
           }
-          ptx::mma_commit(s_full);
-          ptx::mma_commit(&v_empty[stv]);
+          ptx::mma_commit_w(s_full);
+          ptx::mma_commit_w(&v_empty[stv]);
           BW_T(8, n);
         }
-        if (n > 0) {  // dQ += dS(n-1) K(n-1), dS from TMEM
+        if (n > 0) {
           const int m = n - 1, stk = m % NSK;
           ptx::mbar_wait(p_full, m & 1);
           BW_T(2, m);
           ptx::tc_fence_after();
-          const uint32_t sk = ptx::smem_u32(sm + L::K + stk * L::NB * T128);
+          const uint64_t dk = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K + stk * L::NB * T128), T128, 1024);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)  // K = 128 keys, 16 per MMA = 8 TMEM columns of bf16 pairs
-            ptx::mma_bf16_ts(t_dq, t_ds + kk * 8, ptx::umma_desc_sw128(sk + kk * 2048, T128, 1024), id_g,
-                             (m > 0 || kk > 0));
-          ptx::mma_commit(ds_empty);
-          ptx::mma_commit(&k_empty[stk]);
+          for (int kk = 0; kk < 8; ++kk)
+            ptx::mma_bf16_ts_w(t_dq, t_ds + kk * 8, dk + ((kk * 2048) >> 4), id_g, (m > 0 || kk > 0));
+          ptx::mma_commit_w(ds_empty);
+          ptx::mma_commit_w(&k_empty[stk]);
           BW_T(9, m);
         }
       }
-      ptx::mma_commit(dq_done);
+      ptx::mma_commit_w(dq_done);
     }
   } else if (warp >= 4) {
     ptx::regs_inc<224>();

@@ -249,29 +249,30 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
     }
   } else if (warp == 1) {
     ptx::regs_dec<56>();
-    if (lane == 0) {
+    {  // warp-wide MMA issue (elect.sync inside the asm; see mma_bf16_*_w)
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, FA_BKV, false, false);
       constexpr uint32_t id_o = ptx::idesc_bf16_f32(128, D, false, true);
-      const uint32_t sq = ptx::smem_u32(sm + L::Q);
+      const uint64_t dq0 = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::Q), 16, 1024);
+      const uint64_t dk0 = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K), 16, 1024);
+      const uint64_t dv0 = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::V), TILE, 1024);
       auto issue_s = [&](int w, int st) {  // S_w = Q_w K^T (K in ring stage st)
-        const uint32_t sk = ptx::smem_u32(sm + L::K + st * L::NB * TILE);
-        const uint32_t qw = sq + w * L::NB * TILE;
+        const uint64_t dk = dk0 + ((st * L::NB * TILE) >> 4);
+        const uint64_t dq = dq0 + ((w * L::NB * TILE) >> 4);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * TILE + (kk & 3) * 32;
-          ptx::mma_bf16_ss(tmem + w * 128, ptx::umma_desc_sw128(qw + off, 16, 1024),
-                           ptx::umma_desc_sw128(sk + off, 16, 1024), id_s, kk > 0 ? 1u : 0u);
+          const uint32_t off = ((kk >> 2) * TILE + (kk & 3) * 32) >> 4;
+          ptx::mma_bf16_ss_w(tmem + w * 128, dq + off, dk + off, id_s, kk > 0 ? 1u : 0u);
         }
-        ptx::mma_commit(&s_full[w]);
+        ptx::mma_commit_w(&s_full[w]);
       };
       auto issue_pv = [&](int w, int st, bool first) {  // O_w += P_w V, P from TMEM
         ptx::tc_fence_after();
-        const uint32_t sv = ptx::smem_u32(sm + L::V + st * L::NB * TILE);
+        const uint64_t dv = dv0 + ((st * L::NB * TILE) >> 4);
 #pragma unroll
         for (int kk = 0; kk < FA_BKV / 16; ++kk)
-          ptx::mma_bf16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8,
-                           ptx::umma_desc_sw128(sv + kk * 2048, TILE, 1024), id_o, (!first || kk > 0) ? 1u : 0u);
-        ptx::mma_commit(&pv_done[w]);
+          ptx::mma_bf16_ts_w(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, dv + ((kk * 2048) >> 4), id_o,
+                             (!first || kk > 0) ? 1u : 0u);
+        ptx::mma_commit_w(&pv_done[w]);
       };
       int kv = 0, na = 0, nb = 0;  // KV blocks / A blocks / B blocks issued so far
       for (int it = 0;; ++it) {
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             ptx::mbar_wait(&p_full[1], (nb + j - 1) & 1);
             if (it == 0) FA_T(4, j - 1);
             issue_pv(1, g % KVS, j == 1);
-            ptx::mma_commit(&v_empty[g % KVS]);  // PV_A(j-1) was issued before PV_B(j-1)
+            ptx::mma_commit_w(&v_empty[g % KVS]);  // PV_A(j-1) was issued before PV_B(j-1)
           }
           if (j < T.nkv) {
             const int g = kv + j;
@@ -302,8 +303,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
             // alternating between the MUFU and the tensor core instead of sharing both
             if (j == 0) ptx::mbar_wait(&p_full[0], na & 1);
             issue_s(1, g % KVS);
-            ptx::mma_commit(&k_empty[g % KVS]);
-            if (j == T.nkv - 1) ptx::mma_commit(q_empty);  // last read of this tile's Q
+            ptx::mma_commit_w(&k_empty[g % KVS]);
+            if (j == T.nkv - 1) ptx::mma_commit_w(q_empty);  // last read of this tile's Q
             if (j <= T.last_a) {
               ptx::mbar_wait(&v_full[g % KVS], (g / KVS) & 1);
               if (j == 0) ptx::mbar_wait(&o_empty[0], (it & 1) ^ 1);
