@@ -408,8 +408,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    {  // ---------------- MMA issuer (warp-converged, elect.sync inside the asm)
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
@@ -422,25 +421,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * A_STAGE_BYTES);
-          const uint32_t b_addr = ptx::smem_u32(smem_b + stage * B_STAGE_BYTES);
+          const uint64_t a0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_a + stage * A_STAGE_BYTES),
+                                                   A_MN ? 64 * BK * 2 : 16, 1024);
+          const uint64_t b0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_b + stage * B_STAGE_BYTES),
+                                                   B_MN ? 64 * BK * 2 : 16, 1024);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t a_desc, b_desc;
-            if constexpr (A_MN)  // 16 K-rows of 128 B per instruction
-              a_desc = ptx::umma_desc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024);
-            else  // 16 bf16 = 32 B along the swizzled K row
-              a_desc = ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            if constexpr (B_MN)
-              b_desc = ptx::umma_desc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024);
-            else
-              b_desc = ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::mma_bf16_ss(d_tmem, a_desc, b_desc, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+          for (int k = 0; k < BK / 16; ++k)  // MN-major: 16 K-rows of 128 B; K-major: 32 B along the row
+            ptx::mma_bf16_ss_w(d_tmem, a0 + ((A_MN ? k * 2048 : k * 32) >> 4), b0 + ((B_MN ? k * 2048 : k * 32) >> 4),
+                               idesc, (kb | k) != 0 ? 1u : 0u);
+          ptx::mma_commit_w(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        ptx::mma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        ptx::mma_commit_w(&tfull_bar[acc]);  // accumulator ready for the epilogue
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -617,7 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // warp-converged issue, elect.sync inside the asm
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -632,20 +624,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem_a + stage * C::A_BYTES);
-          const uint32_t b_addr = ptx::smem_u32(smem_b + stage * C::B_BYTES);
+          const uint64_t a0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_a + stage * C::A_BYTES),
+                                                   A_MN ? 64 * BK * 2 : 16, 1024);
+          const uint64_t b0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_b + stage * C::B_BYTES),
+                                                   B_MN ? 64 * BK * 2 : 16, 1024);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t a_desc = A_MN ? ptx::umma_desc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024)
-                                         : ptx::umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t b_desc = B_MN ? ptx::umma_desc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024)
-                                         : ptx::umma_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::mma_bf16_ss_pair(d_tmem, a_desc, b_desc, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
-          ptx::mma_commit_pair(&empty_bar[stage], 0x3);
+          for (int k = 0; k < BK / 16; ++k)
+            ptx::mma_bf16_ss_pair_w(d_tmem, a0 + ((A_MN ? k * 2048 : k * 32) >> 4),
+                                    b0 + ((B_MN ? k * 2048 : k * 32) >> 4), idesc, (kb | k) != 0 ? 1u : 0u);
+          ptx::mma_commit_pair_w(&empty_bar[stage], 0x3);
           if (++stage == C::NSTAGE) { stage = 0; phase ^= 1; }
         }
-        ptx::mma_commit_pair(&tfull_bar[acc], 0x3);
+        ptx::mma_commit_pair_w(&tfull_bar[acc], 0x3);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
