@@ -4,7 +4,7 @@
 #include <cuda_runtime.h>
 #include "kernels/sm100_ptx.cuh"
 using namespace amdp;
-enum { SS_KK = 0, SS_KMN = 1, TS_MN = 2, SS_KK_N256 = 3, TS_MN_N64 = 4, SS_KK_N64 = 5, DQ_MIX = 6, DQ128_MIX = 7, TS_KK = 8 };
+enum { SS_KK = 0, SS_KMN = 1, TS_MN = 2, SS_KK_N256 = 3, TS_MN_N64 = 4, SS_KK_N64 = 5, DQ_MIX = 6, DQ128_MIX = 7, TS_KK = 8, W_SS_N64 = 9, W_TS_N64 = 10, W_SS_N128 = 11 };
 template <int MODE>
 __global__ void probe(int rounds, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -19,7 +19,26 @@ __global__ void probe(int rounds, long long* out) {
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = slot;
-  if (threadIdx.x == 0) {
+  if (MODE >= W_SS_N64 && threadIdx.x < 32) {  // warp-converged issue (elect.sync in the asm)
+    const uint32_t a = ptx::smem_u32(sm), b = a + 32768;
+    constexpr int N = MODE == W_SS_N128 ? 128 : 64;
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, N, false, MODE == W_TS_N64);
+    const uint64_t da = ptx::umma_desc_sw128(a, 16, 1024), db = ptx::umma_desc_sw128(b, 16, 1024);
+    const uint64_t dbm = ptx::umma_desc_sw128(b, 16384, 1024);
+    long long t0 = clock64();
+    for (int r = 0; r < rounds; ++r) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (MODE == W_TS_N64)
+          ptx::mma_bf16_ts_w(tmem + 256, tmem + kk * 8, dbm + ((kk * 2048) >> 4), id, 1u);
+        else
+          ptx::mma_bf16_ss_w(tmem + 256, da + (((kk & 3) * 32) >> 4), db + (((kk & 3) * 32) >> 4), id, 1u);
+      }
+    }
+    ptx::mma_commit_w(&bar);
+    ptx::mbar_wait(&bar, 0);
+    if (threadIdx.x == 0) out[0] = clock64() - t0;
+  } else if (MODE < W_SS_N64 && threadIdx.x == 0) {
     const uint32_t a = ptx::smem_u32(sm), b = a + 32768;
     constexpr int N = MODE == SS_KK_N256 ? 256 : ((MODE == TS_MN_N64 || MODE == SS_KK_N64) ? 64 : 128);
     constexpr bool bmn = MODE == SS_KMN || MODE == TS_MN || MODE == TS_MN_N64;
@@ -212,5 +231,8 @@ int main() {
   run<DQ_MIX>("dQ block (16 SS N64 + 4 TS N128) per 8", d);
   run<TS_KK>("TS M128 N128 B K-major", d);
   run<DQ128_MIX>("dQ128 block (8 TS + 8 SS + 8 TS, N128) per 8", d);
+  run<W_SS_N64>("warp-issue SS M128 N64", d);
+  run<W_TS_N64>("warp-issue TS M128 N64", d);
+  run<W_SS_N128>("warp-issue SS M128 N128", d);
   return 0;
 }
