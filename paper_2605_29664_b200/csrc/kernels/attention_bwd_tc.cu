@@ -138,8 +138,12 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = static_cast<int>(blockIdx.x % n_kt);  // causal: small kt = most work, first
-  const int hb = static_cast<int>(blockIdx.x / n_kt);
+  // Heavy first across the whole grid (causal: key tile kt carries n_kt - kt query blocks): the
+  // block scheduler then packs the light tiles into the last wave instead of leaving a few
+  // 32-unit tiles running alone at the end (longest-processing-time-first).
+  const int BH = static_cast<int>(gridDim.x) / n_kt;
+  const int kt = static_cast<int>(blockIdx.x) / BH;
+  const int hb = static_cast<int>(blockIdx.x) % BH;
   const int h = hb % H, b = hb / H;
   const int row0 = b * seq;
   const int nqb = seq / 128;
@@ -352,7 +356,7 @@ struct QSmem {
   static constexpr uint32_t K = DO + NB * T128;   // NSK stages of NB x T128
   static constexpr uint32_t V = K + NSK * NB * T128;
   static constexpr uint32_t BAR = V + NSV * NB * T128;
-  static constexpr uint32_t BYTES = BAR + 256;
+  static constexpr uint32_t BYTES = BAR + 512;
 };
 
 template <int D>
@@ -374,15 +378,17 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_full = k_empty + 8;      // [NSV]
   uint64_t* v_empty = v_full + 4;      // [NSV]
   uint64_t* s_full = v_empty + 4;
-  uint64_t* s_empty = s_full + 1;      // 256 arrivals: S / dP loaded into registers
-  uint64_t* p_full = s_empty + 1;      // 256 arrivals: dS written into TMEM
+  uint64_t* s_empty = s_full + 1;      // 256 arrivals: S loaded into registers
+  uint64_t* d_empty = s_empty + 1;     // 256 arrivals: dP loaded into registers
+  uint64_t* p_full = d_empty + 1;      // 256 arrivals: dS written into TMEM
   uint64_t* ds_empty = p_full + 1;     // dQ MMA has read dS
   uint64_t* dq_done = ds_empty + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = n_qt - 1 - static_cast<int>(blockIdx.x % n_qt);  // heavy first
-  const int hb = static_cast<int>(blockIdx.x / n_qt);
+  const int BH = static_cast<int>(gridDim.x) / n_qt;  // heavy first across the grid (see dK/dV)
+  const int qt = n_qt - 1 - static_cast<int>(blockIdx.x) / BH;
+  const int hb = static_cast<int>(blockIdx.x) % BH;
   const int h = hb % H, b = hb / H;
   const int row0 = b * seq;
   const int N = causal ? qt + 1 : seq / 128;
@@ -402,6 +408,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     ptx::mbar_init(s_full, 1);
     ptx::mbar_init(s_empty, 256);
+    ptx::mbar_init(d_empty, 256);
     ptx::mbar_init(p_full, 256);
     ptx::mbar_init(ds_empty, 1);
     ptx::mbar_init(dq_done, 1);
@@ -474,6 +481,7 @@ __global__ void __launch_bounds__(384, 1)
           for (int kk = 0; kk < D / 16; ++kk)
             ptx::mma_bf16_ts_w(tmem, t_q + kk * 8, dk + (((kk >> 2) * T128 + (kk & 3) * 32) >> 4), id_s, kk > 0);
           ptx::mbar_wait(&v_full[stv], (n / NSV) & 1);
+          ptx::mbar_wait(d_empty, (n & 1) ^ 1);  // dP(n-1) loaded: S(n) above overlapped that load
           ptx::tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
@@ -542,13 +550,17 @@ __global__ void __launch_bounds__(384, 1)
       if (lane == 0 && q == 0 && wg == 0) BW_T(3, n);
       ptx::tc_fence_after();
       uint32_t s[64], d[64];
+      // S first, released as soon as it is in registers so S(n+1) overlaps the dP load
       ptx::tmem_ld_32x32b_x32(tmem + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
       ptx::tmem_ld_32x32b_x32(tmem + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(s_empty);
       ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
       ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(s_empty);
+      ptx::mbar_arrive(d_empty);
       uint32_t gg[32];
 #pragma unroll
       for (int cc = 0; cc < 64; cc += 2) {
