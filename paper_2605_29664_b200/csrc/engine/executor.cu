@@ -300,6 +300,7 @@ Engine::~Engine() {
     cudaFree(s->v);
     cudaFree(s->grad);
     cudaFree(s->w);
+    cudaFree(s->wt);
   }
   for (auto& v : slot_mem_)
     for (auto* p : v) cudaFree(p);
@@ -463,6 +464,7 @@ void Engine::allocate() {
     CUDA_OK(cudaMalloc(&st.master, n * sizeof(float)));
     CUDA_OK(cudaMalloc(&st.grad, n * sizeof(float)));
     CUDA_OK(cudaMalloc(&st.w, n * sizeof(uint16_t)));
+    CUDA_OK(cudaMalloc(&st.wt, n * sizeof(uint16_t)));
     CUDA_OK(cudaMemsetAsync(st.grad, 0, n * sizeof(float), cs_));
     if (owned[static_cast<size_t>(i)]) {
       CUDA_OK(cudaMalloc(&st.m, n * sizeof(float)));
@@ -519,6 +521,7 @@ void Engine::init_weights() {
     cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
         st.master, reinterpret_cast<bf16*>(st.w), n);
     CUDA_OK(cudaGetLastError());
+    if (st.refresh_transposed(cs_) < 0) throw std::runtime_error("weight transpose failed");
   }
   CUDA_OK(cudaStreamSynchronize(cs_));
 }
@@ -672,6 +675,9 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       ktimer_.end(cs_);
       if (rc != 0) throw std::runtime_error("optimizer step failed");
       stats.kernels_launched += 1;
+      const int nt = S.refresh_transposed(cs_);
+      if (nt < 0) throw std::runtime_error("weight transpose failed");
+      stats.kernels_launched += nt;
     } else {
       // the reduce on the comm stream read this replica's gradient: wait, then clear it
       cudaEvent_t e;
@@ -699,6 +705,9 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
         cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
             S.master, reinterpret_cast<bf16*>(S.w), n);
         stats.kernels_launched += 1;
+        const int nt = S.refresh_transposed(cs_);
+        if (nt < 0) throw std::runtime_error("weight transpose failed");
+        stats.kernels_launched += nt;
       }
     }
     bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i);
@@ -878,6 +887,7 @@ void Engine::copy_params(int stage, float* host, int64_t n, bool to_host) {
     CUDA_OK(cudaMemcpy(st.master, host, static_cast<size_t>(n) * sizeof(float), cudaMemcpyHostToDevice));
     cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
         st.master, reinterpret_cast<bf16*>(st.w), n);
+    if (st.refresh_transposed(cs_) < 0) throw std::runtime_error("weight transpose failed");
     CUDA_OK(cudaStreamSynchronize(cs_));
   }
 }

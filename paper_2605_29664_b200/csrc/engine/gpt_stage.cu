@@ -25,16 +25,51 @@ struct Carver {
 // when the executor's kernel timer is on.
 int gemm_t(KTimer* kt, int M, int N, int K, const void* A, int lda, bool amn, const void* B, int ldb,
            bool bmn, void* C, int ldc, int epi, cudaStream_t s, const void* aux = nullptr,
-           int ld_aux = 0, void* C2 = nullptr, int ldc2 = 0) {
+           int ld_aux = 0, void* C2 = nullptr, int ldc2 = 0, int cls = -1) {
   amdp_gemm_args a{M, N, K, A, lda, amn ? 1 : 0, B, ldb, bmn ? 1 : 0, C, ldc, aux, ld_aux, C2, ldc2,
                    epi, 1.0f};
-  const int cls = epi == AMDP_EPI_ACCUM_F32 ? K_GEMM_WGRAD : (bmn ? K_GEMM_DGRAD : K_GEMM_FWD);
+  if (cls < 0) cls = epi == AMDP_EPI_ACCUM_F32 ? K_GEMM_WGRAD : (bmn ? K_GEMM_DGRAD : K_GEMM_FWD);
   if (kt) kt->begin(cls, 2.0 * M * N * static_cast<double>(K), 0, s);
   const int rc = amdp_gemm(&a, reinterpret_cast<amdp_stream_t>(s));
   if (kt) kt->end(s);
   return rc;
 }
+// dst[c][r] = src[r][c] for a [rows][cols] bf16 matrix; 64x64 tiles through shared memory.
+__global__ void transpose_bf16_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst, int rows,
+                                      int cols) {
+  __shared__ uint16_t tile[64][66];
+  const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
+  for (int i = threadIdx.y; i < 64; i += 8)
+    for (int j = threadIdx.x; j < 64; j += 32) {
+      const int r = r0 + i, c = c0 + j;
+      tile[i][j] = (r < rows && c < cols) ? src[static_cast<size_t>(r) * cols + c] : 0;
+    }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 64; i += 8)
+    for (int j = threadIdx.x; j < 64; j += 32) {
+      const int c = c0 + i, r = r0 + j;
+      if (c < cols && r < rows) dst[static_cast<size_t>(c) * rows + r] = tile[j][i];
+    }
+}
 }  // namespace
+
+int GptStage::refresh_transposed(cudaStream_t s) const {
+  if (!wt) return 0;
+  int launched = 0;
+  auto tr = [&](const ParamRef& p) {
+    dim3 grid((p.cols + 63) / 64, (p.rows + 63) / 64);
+    transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(w + p.off, wt + p.off, p.rows, p.cols);
+    ++launched;
+  };
+  for (const LayerParams& P : layers_) {
+    tr(P.qkv);
+    tr(P.o);
+    tr(P.fc1);
+    tr(P.fc2);
+  }
+  if (last()) tr(head_);
+  return cudaGetLastError() == cudaSuccess ? launched : -1;
+}
 
 GptStage::GptStage(const Dims& d, int stage, int depth, int l0, int l1)
     : d_(d), stage_(stage), depth_(depth), l0_(l0), l1_(l1) {
@@ -266,8 +301,8 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     hand(ss.ev[E_HEAD], s, sd);
     AMDP_GEMM(gemm_t(kt, d_.V, h, T, a.logits, d_.V, true, a.lnf, h, true, grad + head_.off, h,
                      AMDP_EPI_ACCUM_F32, sd), 1);
-    AMDP_GEMM(gemm_t(kt, T, h, d_.V, a.logits, d_.V, false, w + head_.off, h, true, ws.dtmp, h,
-                     AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_GEMM(gemm_t(kt, T, h, d_.V, a.logits, d_.V, false, wt + head_.off, d_.V, false, ws.dtmp, h,
+                     AMDP_EPI_STORE_BF16, s, nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, a.xf, master + lnf_g_.off, a.lnf_mean, a.lnf_rstd, nullptr, ws.g0,
                                 grad + lnf_g_.off, grad + lnf_b_.off, ws.ln, T, h, st), 2);
     g = ws.g0;
@@ -281,12 +316,14 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     AMDP_GEMM(gemm_t(kt, h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_G], sd);
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DU], 0);  // previous layer's dW1 done with dU
-    AMDP_GEMM(gemm_t(kt, T, F, h, g, h, false, w + P.fc2.off, F, true, ws.dU, F, AMDP_EPI_GELU_BWD, s, A.u, F), 1);
+    AMDP_GEMM(gemm_t(kt, T, F, h, g, h, false, wt + P.fc2.off, h, false, ws.dU, F, AMDP_EPI_GELU_BWD, s, A.u, F,
+                     nullptr, 0, K_GEMM_DGRAD), 1);
     hand(ss.ev[E_DU], s, sd);
     // f = gelu(ln2 W1^T)
     AMDP_GEMM(gemm_t(kt, F, h, T, ws.dU, F, true, A.ln2, h, true, grad + P.fc1.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_DU], sd);
-    AMDP_GEMM(gemm_t(kt, T, h, F, ws.dU, F, false, w + P.fc1.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_GEMM(gemm_t(kt, T, h, F, ws.dU, F, false, wt + P.fc1.off, F, false, ws.dtmp, h, AMDP_EPI_STORE_BF16, s,
+                     nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
     // ln2 = LN(hmid); dhmid = g + LN'(dln2)
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DH], 0);  // previous layer's dWo done with dhmid
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, A.hmid, master + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g, ws.dhmid,
@@ -295,7 +332,8 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     // hmid = x + o Wo^T
     AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_DH], sd);
-    AMDP_GEMM(gemm_t(kt, T, h, h, ws.dhmid, h, false, w + P.o.off, h, true, ws.dtmp, h, AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_GEMM(gemm_t(kt, T, h, h, ws.dhmid, h, false, wt + P.o.off, h, false, ws.dtmp, h, AMDP_EPI_STORE_BF16, s,
+                     nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DQ], 0);  // previous layer's dWqkv done with dqkv
     AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
                                 d_.causal ? 1 : 0, st), 3);
@@ -304,8 +342,8 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     AMDP_GEMM(gemm_t(kt, 3 * h, h, T, ws.dqkv, 3 * h, true, A.ln1, h, true, grad + P.qkv.off, h,
                      AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_DQ], sd);
-    AMDP_GEMM(gemm_t(kt, T, h, 3 * h, ws.dqkv, 3 * h, false, w + P.qkv.off, h, true, ws.dtmp, h,
-                     AMDP_EPI_STORE_BF16, s), 1);
+    AMDP_GEMM(gemm_t(kt, T, h, 3 * h, ws.dqkv, 3 * h, false, wt + P.qkv.off, 3 * h, false, ws.dtmp, h,
+                     AMDP_EPI_STORE_BF16, s, nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
     uint16_t* gn = (li == 0 && !first()) ? gout : (g == ws.g0 ? ws.g1 : ws.g0);
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_G], 0);  // dW2 of the layer that read gn's buffer
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, x, master + P.ln1_g.off, A.ln1_mean, A.ln1_rstd, ws.dhmid, gn,

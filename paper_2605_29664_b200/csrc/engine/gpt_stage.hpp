@@ -82,6 +82,11 @@ class GptStage {
   float* v = nullptr;
   float* grad = nullptr;    // fp32 window-accumulated gradient
   uint16_t* w = nullptr;    // bf16 working weights read by the kernels
+  // bf16 transposed copies ([in][out], same offsets as `w`) of the matrices the
+  // activation-gradient GEMMs read, so dX = dY W runs with a K-major B operand like the
+  // forward GEMMs (refresh_transposed() after every write of `w`)
+  uint16_t* wt = nullptr;
+  int refresh_transposed(cudaStream_t s) const;
   KTimer* kt = nullptr;     // optional per-kernel-class timing
   double attn_fwd_flops() const {  // algorithmic: QK^T + PV, causal half
     const double f = 4.0 * d_.B * d_.heads * static_cast<double>(d_.S) * d_.S * d_.hd;
