@@ -25,6 +25,9 @@ CASES = {
     "fc1_wgrad_kk": (4 * h, h, T, False, False, N.EPI_STORE_BF16),
     "fc1_wgrad_bf16": (4 * h, h, T, True, True, N.EPI_STORE_BF16),
     "fc2_fwd": (T, h, 4 * h, False, False, N.EPI_STORE_BF16),
+    "fc1_wgrad_amn": (4 * h, h, T, True, False, N.EPI_ACCUM_F32),
+    "fc1_fwd_amn": (T, 4 * h, h, True, False, N.EPI_STORE_BF16),
+    "fc2_fwd_amn": (T, h, 4 * h, True, False, N.EPI_STORE_BF16),
 }
 
 
