@@ -1,17 +1,22 @@
 // Stage GEMM for the AMDP executor: C = epi(alpha * A * B^T), bf16 in, fp32 accumulate.
 //
-// sm_100a design (no mma.sync / wgmma):
-//   * persistent CTAs (grid <= #SMs), one 128x256 output tile at a time,
-//   * warp 0 / lane 0: TMA producer into a 4-stage smem ring (SWIZZLE_128B),
-//   * warp 1 / lane 0: tcgen05.mma issuer (M=128, N=256, K=16 per instruction),
-//     accumulating in TMEM; two 256-column accumulators so the epilogue of tile i
-//     overlaps the main loop of tile i+1,
-//   * warps 4..7: epilogue (tcgen05.ld -> registers -> fused op -> global).
-// Operands may be K-major or MN-major independently, so forward (X W^T),
-// activation-gradient (dY W) and weight-gradient (dY^T X) all run without
-// transposes. Epilogues: plain bf16 store, GELU (stores pre-activation too),
-// residual add, fp32 accumulate (weight-gradient accumulation across the
-// minibatches of one AMDP window), GELU-backward.
+// sm_100a design (no mma.sync / wgmma), two kernels with the same warp roles:
+//   * gemm_bf16_tc_pair: a CTA pair (cta_group::2) per 256x256 tile, 6-stage TMA ring; the
+//     forward and activation-gradient GEMMs (the last partial wave of forward GEMMs is split
+//     along N);  gemm_bf16_tcgen05: one CTA per 128x256 tile, 4-stage ring; the
+//     weight-gradient GEMMs (A and B MN-major), where it sustains more under the power cap;
+//   * persistent CTAs (grid = co-resident CTAs / pairs), launched with programmatic
+//     dependent launch so the prologue overlaps the previous kernel's tail;
+//   * warp 0: TMA producer; warp 1: tcgen05.mma issue, warp-converged with elect.sync in the
+//     asm and descriptors advanced by offset (no per-MMA single-lane loop); two TMEM
+//     accumulators so a tile's epilogue overlaps the next tile's main loop;
+//   * warps 4..7: epilogue, each owning 32 TMEM lanes: tcgen05.ld -> fused op in registers
+//     -> swizzled smem staging -> TMA store (or TMA reduce-add for the fp32 window gradient).
+// Operands may be K-major or MN-major independently, so forward (X W^T), activation-gradient
+// (dY W, via transposed weight copies) and weight-gradient (dY^T X) run without transposes
+// of the activations.  Epilogues: plain bf16 store, GELU (stores pre-activation too),
+// residual add, fp32 accumulate (weight-gradient accumulation across the minibatches of one
+// AMDP window), GELU-backward, fp32 store.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -81,106 +86,7 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   tn = r / gsz;
 }
 
-// 32 consecutive output columns of one row: apply the fused epilogue and store.
 constexpr int EPI_DISCARD = 6;  // experiment only: drain TMEM, store nothing (AMDP_GEMM_DISCARD)
-
-template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& p, int row, int col0,
-                                               const uint32_t (&raw)[32]) {
-  if constexpr (EPI == EPI_DISCARD) return;
-  if (row >= p.M) return;
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]) * p.alpha;
-  const bool full = (col0 + 32) <= p.N;
-
-  if constexpr (EPI == AMDP_EPI_ACCUM_F32 || EPI == AMDP_EPI_STORE_F32) {
-    float* c = static_cast<float*>(p.C) + static_cast<size_t>(row) * p.ldc + col0;
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        if constexpr (EPI == AMDP_EPI_ACCUM_F32) {
-          float4 old = *reinterpret_cast<const float4*>(c + j);
-          o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-        }
-        *reinterpret_cast<float4*>(c + j) = o;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (col0 + j < p.N) c[j] = (EPI == AMDP_EPI_ACCUM_F32) ? c[j] + v[j] : v[j];
-    }
-    return;
-  } else {
-    // bf16 outputs
-    if constexpr (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD) {
-      const __nv_bfloat16* a = p.aux + static_cast<size_t>(row) * p.ld_aux + col0;
-      if (full) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 q = *reinterpret_cast<const uint4*>(a + j);
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            float2 f = __bfloat1622float2(h[e]);
-            if constexpr (EPI == AMDP_EPI_RESIDUAL) {
-              v[j + 2 * e] += f.x;
-              v[j + 2 * e + 1] += f.y;
-            } else {
-              v[j + 2 * e] *= gelu_tanh_grad(f.x);
-              v[j + 2 * e + 1] *= gelu_tanh_grad(f.y);
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (col0 + j >= p.N) continue;
-          float f = __bfloat162float(a[j]);
-          if constexpr (EPI == AMDP_EPI_RESIDUAL) v[j] += f;
-          else v[j] *= gelu_tanh_grad(f);
-        }
-      }
-    }
-    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(row) * p.ldc + col0;
-    __nv_bfloat16* c2 = nullptr;
-    if constexpr (EPI == AMDP_EPI_GELU) {
-      c2 = p.C2 + static_cast<size_t>(row) * p.ldc2 + col0;
-    }
-    if (full) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        uint4 q, q2;
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&q2);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float x0 = v[j + 2 * e], x1 = v[j + 2 * e + 1];
-          if constexpr (EPI == AMDP_EPI_GELU) {
-            h2[e] = __floats2bfloat162_rn(x0, x1);
-            x0 = gelu_tanh(x0);
-            x1 = gelu_tanh(x1);
-          }
-          h[e] = __floats2bfloat162_rn(x0, x1);
-        }
-        *reinterpret_cast<uint4*>(c + j) = q;
-        if constexpr (EPI == AMDP_EPI_GELU) *reinterpret_cast<uint4*>(c2 + j) = q2;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (col0 + j >= p.N) continue;
-        float x = v[j];
-        if constexpr (EPI == AMDP_EPI_GELU) {
-          c2[j] = __float2bfloat16_rn(x);
-          x = gelu_tanh(x);
-        }
-        c[j] = __float2bfloat16_rn(x);
-      }
-    }
-  }
-}
 
 // Output tensor maps of the pair kernel's TMA epilogue: C (bf16 box {64, 32} or f32 box
 // {32, 32}), C2 (GELU pre-activation), aux (residual / pre-activation input), SWIZZLE_128B.

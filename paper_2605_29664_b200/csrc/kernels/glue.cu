@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dgb_kernel(
 }
 
 // ---------------------------------------------------------------- LayerNorm, row-group form
-// For the model widths (cols a multiple of 256, <= 8192): one thread per 8 columns, so a
+// Backward for the model widths (cols a multiple of 256, <= 4096): one thread per 8 columns, so a
 // CTA of cols/8 threads spans a whole row and handles RG rows per iteration (RG 16-byte
 // loads in flight per thread and per tensor).  Row statistics: warp shuffle, then the
 // cols/256 warp partials through shared memory (double-buffered by iteration parity, so
@@ -212,65 +212,6 @@ __device__ __forceinline__ void block_sums(float (&v)[RG], float* red, int nw) {
     float t = 0.f;
     for (int k = 0; k < nw; ++k) t += red[i * 32 + k];
     v[i] = t;
-  }
-}
-
-template <int RG>
-__global__ void __launch_bounds__(512) layernorm_fwd_rows_kernel(
-    const bf16* __restrict__ x, const float* __restrict__ gamma, const float* __restrict__ beta,
-    bf16* __restrict__ y, float* __restrict__ mean_out, float* __restrict__ rstd_out, int rows,
-    int cols, float eps) {
-  __shared__ float red[4][RG * 32];
-  const int nw = blockDim.x >> 5;
-  const int c = threadIdx.x * 8;
-  float g[8], b[8];
-  {
-    const float4 g0 = *reinterpret_cast<const float4*>(gamma + c), g1 = *reinterpret_cast<const float4*>(gamma + c + 4);
-    const float4 b0 = *reinterpret_cast<const float4*>(beta + c), b1 = *reinterpret_cast<const float4*>(beta + c + 4);
-    g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
-    b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
-  }
-  const float inv = 1.f / static_cast<float>(cols);
-  int it = 0;
-  for (int r0 = blockIdx.x * RG; r0 < rows; r0 += gridDim.x * RG, it ^= 1) {
-    uint4 raw[RG];
-#pragma unroll
-    for (int i = 0; i < RG; ++i)
-      raw[i] = (r0 + i < rows) ? *reinterpret_cast<const uint4*>(x + static_cast<size_t>(r0 + i) * cols + c)
-                               : make_uint4(0, 0, 0, 0);
-    float m[RG], v[RG];
-#pragma unroll
-    for (int i = 0; i < RG; ++i) {
-      float f[8];
-      unpack8(raw[i], f);
-      m[i] = ((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7]));
-    }
-    block_sums<RG>(m, red[2 * it], nw);
-#pragma unroll
-    for (int i = 0; i < RG; ++i) {
-      m[i] *= inv;
-      float f[8];
-      unpack8(raw[i], f);
-      float q = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) q += (f[e] - m[i]) * (f[e] - m[i]);
-      v[i] = q;
-    }
-    block_sums<RG>(v, red[2 * it + 1], nw);
-#pragma unroll
-    for (int i = 0; i < RG; ++i) {
-      if (r0 + i >= rows) break;
-      const float rs = rsqrtf(v[i] * inv + eps);
-      float f[8], o[8];
-      unpack8(raw[i], f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = (f[e] - m[i]) * rs * g[e] + b[e];
-      store8(y + static_cast<size_t>(r0 + i) * cols + c, o);
-      if (threadIdx.x == 0) {
-        mean_out[r0 + i] = m[i];
-        rstd_out[r0 + i] = rs;
-      }
-    }
   }
 }
 
@@ -545,12 +486,6 @@ extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const f
   auto xs = reinterpret_cast<const bf16*>(x);
   auto ys = reinterpret_cast<bf16*>(y);
   auto st = reinterpret_cast<cudaStream_t>(stream);
-  if (ln_row_group_form(cols) && getenv("AMDP_LN_FWD_ROWS")) {
-    constexpr int RG = 8;
-    const int grid = (rows + RG - 1) / RG;
-    layernorm_fwd_rows_kernel<RG><<<grid, cols / 8, 0, st>>>(xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
-    return cudaGetLastError();
-  }
   const int nv = (cols + 255) / 256;
   if (nv <= 1) launch_pdl(layernorm_fwd_kernel<1>, dim3(blocks), dim3(256), 0, st, xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
   else if (nv <= 4) launch_pdl(layernorm_fwd_kernel<4>, dim3(blocks), dim3(256), 0, st, xs, gamma, beta, ys, mean, rstd, rows, cols, eps);
