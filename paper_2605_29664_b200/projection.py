@@ -19,6 +19,10 @@ from typing import Dict, Tuple
 
 from . import ppsim as P
 
+# per-stage cost keys in bench.py's JSON: F3 = Forward of stage 3, BC3 = Broadcast (optimizer) ...
+KIND_TAG = {P.Kind.Forward: "F", P.Kind.Backward: "B", P.Kind.Reduce: "R", P.Kind.Broadcast: "BC",
+            P.Kind.Update: "U"}
+
 
 def measured_costs(tl: P.Timeline, min_window: int = 1) -> Dict[Tuple[P.Kind, int], float]:
     """Mean measured duration (ns) per (kind, stage) over windows >= min_window."""
@@ -30,15 +34,22 @@ def measured_costs(tl: P.Timeline, min_window: int = 1) -> Dict[Tuple[P.Kind, in
 
 
 def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple[P.Kind, int], float],
-                        gap_ns: float, declared_fwd=1, declared_bwd=1) -> P.Timeline:
-    """Re-times the declared dispatch order of `policy` on `depth` devices with measured costs."""
-    declared = P.ClusterSpec.uniform(depth, depth, declared_fwd, declared_bwd)
+                        gap_ns: float, declared_fwd=1, declared_bwd=1, devices: int = 0) -> P.Timeline:
+    """Re-times the declared dispatch order of `policy` (depth stages on `devices`, default
+    depth) with measured costs.  Update tasks (replicated-weight policies) cost what the
+    stage's measured Broadcast (fused optimizer step) cost."""
+    devices = devices or depth
+    declared = P.ClusterSpec.uniform(depth, devices, declared_fwd, declared_bwd)
     g = P.build(policy, declared)
     tl = P.simulate(g, declared)
+    costs_ns = dict(costs_ns)
+    for s in range(depth):
+        if (P.Kind.Update, s) not in costs_ns and (P.Kind.Broadcast, s) in costs_ns:
+            costs_ns[(P.Kind.Update, s)] = costs_ns[(P.Kind.Broadcast, s)]
     preds = [[] for _ in g.tasks]
     for a, b in g.deps:
         preds[b].append(a)
-    free = [0] * depth
+    free = [0] * devices
     finish = [0] * len(g.tasks)
     gap = int(round(gap_ns))
     events = []
@@ -52,7 +63,7 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
         free[task.device] = finish[t]
         events.append(P.TaskEvent(task.kind, task.stage, task.minibatch, task.pipeline, task.device,
                                   Fraction(start), Fraction(dur), task.preloaded, task.window))
-    return P.Timeline.from_events(events, policy.policy, depth, depth, policy.accumulation_threshold)
+    return P.Timeline.from_events(events, policy.policy, depth, devices, policy.accumulation_threshold)
 
 
 def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, tokens_per_minibatch: int,
@@ -74,9 +85,40 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
     return {"gpus": depth, "bubble": float(bubble),
             "tokens_per_s": (threshold * tokens_per_minibatch / (period * 1e-9)) if period else None,
             "gap_us": gap_ns / 1e3,
-            "stage_ms": {f"{k[0].name[0]}{k[1]}": round(v / 1e6, 3) for k, v in sorted(costs.items())
-                         if k[0] in (P.Kind.Forward, P.Kind.Backward)},
+            "stage_ms": {f"{KIND_TAG[k[0]]}{k[1]}": round(v / 1e6, 3) for k, v in sorted(costs.items())},
             "method": "static-order replay of the declared AMDP dispatch order on one GPU per "
                       "logical device, task costs = measured 1-GPU means (windows >= 1), "
                       "inter-device gap = activation bytes / 770 GB/s peer copy; bubble = "
                       "reference bubble_ratio(tl, 1).  A projection, not a multi-GPU measurement."}
+
+
+# Schedules of the paper's comparison (reference builder.hpp policies) on the same D stages /
+# D devices, thr minibatches per accumulation window.  Interleaved 1F1B needs
+# 2D stages (another partition) and is left out.
+COMPARE = {
+    "AMDP": lambda d, thr, m: P.PolicyConfig(P.Policy.AMDP, 2, d // 2, thr, m, True),
+    # synchronous schedules inject the whole window (validate.hpp: threshold == injection limit)
+    "DAPPLE": lambda d, thr, m: P.PolicyConfig(P.Policy.DAPPLE, thr, 1, thr, m, False),
+    "GPipe": lambda d, thr, m: P.PolicyConfig(P.Policy.GPipe, thr, 1, thr, m, False),
+    "Chimera": lambda d, thr, m: P.PolicyConfig(P.Policy.Chimera, thr, 2, thr, m, False),
+    "PipeDreamAsync": lambda d, thr, m: P.PolicyConfig(P.Policy.PipeDreamAsync, d, 1, thr, m, False),
+}
+
+
+def compare_policies(costs_ns: Dict[Tuple[P.Kind, int], float], depth: int, threshold: int, windows: int,
+                     tokens_per_minibatch: int, gap_ns: float) -> dict:
+    """Projected bubble / tokens/s / makespan of each policy from the same measured stage costs."""
+    out = {}
+    for name, mk in COMPARE.items():
+        pol = mk(depth, threshold, windows * threshold)
+        try:
+            rep = static_order_replay(pol, depth, costs_ns, gap_ns)
+        except Exception as e:  # a policy whose rules reject this shape
+            out[name] = {"error": str(e)[:160]}
+            continue
+        ev = rep.flat()
+        span = float(max(e.finish() for e in ev))
+        out[name] = {"bubble_w1": float(P.bubble_ratio(rep, 1 if windows > 2 else 0)),
+                     "tokens_per_s": windows * threshold * tokens_per_minibatch / (span * 1e-9),
+                     "makespan_ms": span / 1e6}
+    return out

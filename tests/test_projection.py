@@ -44,3 +44,19 @@ def test_replay_slower_backward_and_gap_is_causal():
     assert P.validate_non_overlap(rep) == []
     assert max(e.finish() for e in rep.flat()) > max(e.finish() for e in base.flat())
     assert 0 <= P.bubble_ratio(rep, 1) < 1
+
+
+def test_compare_policies_all_schedules_run_and_amdp_matches_project():
+    d, thr, windows = 8, 32, 3
+    costs = {}
+    for s in range(d):
+        costs[(P.Kind.Forward, s)] = 1000.0 + 100 * (s < 2)
+        costs[(P.Kind.Backward, s)] = 2200.0 + 200 * (s < 2)
+        costs[(P.Kind.Broadcast, s)] = 300.0
+    res = PR.compare_policies(costs, d, thr, windows, 8192, 40.0)
+    assert set(res) == {"AMDP", "DAPPLE", "GPipe", "Chimera", "PipeDreamAsync"}
+    for name, r in res.items():
+        assert "error" not in r, (name, r)
+        assert 0 <= r["bubble_w1"] < 1 and r["tokens_per_s"] > 0
+    rep = PR.static_order_replay(_pol(d, thr, windows), d, costs, 40.0)
+    assert abs(float(P.bubble_ratio(rep, 1)) - res["AMDP"]["bubble_w1"]) < 1e-12
