@@ -67,12 +67,18 @@ uint64_t tensor_seed(uint64_t model_seed, int gidx) {
   return model_seed * 1000003ull + static_cast<uint64_t>(gidx);
 }
 
-// Balanced contiguous partition of L layers over `depth` stages, costing the LM head as
-// V / (12 h) layer-equivalents on the last stage (2hV vs 24h^2 forward flops per token).
-std::vector<int> balance_layers(int L, int depth, int h, int V) {
-  const double head = static_cast<double>(V) / (12.0 * h);
+// Balanced contiguous partition of L layers over `depth` stages.  The LM head (+ final LN and
+// cross-entropy) on the last stage costs 6hV training flops per token against a layer's
+// 6(4h^2 + 2h ffn) + 6 s h (causal attention), i.e. ~1.9 layer-equivalents for GPT-1.3B
+// (measured on B200: 1.7).  Among partitions with the smallest maximum stage cost, take the
+// one with the fewest stages at that maximum: the AMDP projection from measured stage costs
+// (profiles/r01_sweep) gives [4,3,3,3,3,3,3,2] 9.7% bubble vs 11.5% for [4,4,3,3,3,3,3,1].
+std::vector<int> balance_layers(int L, int depth, int h, int V, int ffn, int seq, bool causal) {
+  const double layer = 6.0 * (4.0 * h * h + 2.0 * h * ffn) + (causal ? 6.0 : 12.0) * seq * h;
+  const double head = 6.0 * h * static_cast<double>(V) / layer;
   std::vector<int> best;
   double best_max = 1e300;
+  int best_at_max = 1 << 30;
   // last stage gets k layers, the rest spread as evenly as possible
   for (int k = 0; k <= L; ++k) {
     const int rest = L - k;
@@ -84,10 +90,17 @@ std::vector<int> balance_layers(int L, int depth, int h, int V) {
       for (int i = 0; i < depth - 1; ++i) p[static_cast<size_t>(i)] = rest / (depth - 1) + (i < rest % (depth - 1) ? 1 : 0);
       p[static_cast<size_t>(depth - 1)] = k;
     }
+    std::vector<double> c(static_cast<size_t>(depth));
     double mx = 0;
-    for (int i = 0; i < depth; ++i) mx = std::max(mx, p[static_cast<size_t>(i)] + (i == depth - 1 ? head : 0.0));
-    if (k >= 1 && mx < best_max - 1e-9) {
+    for (int i = 0; i < depth; ++i) {
+      c[static_cast<size_t>(i)] = p[static_cast<size_t>(i)] + (i == depth - 1 ? head : 0.0);
+      mx = std::max(mx, c[static_cast<size_t>(i)]);
+    }
+    int at_max = 0;
+    for (double x : c) at_max += x > mx - 1e-9 ? 1 : 0;
+    if (k >= 1 && (mx < best_max - 1e-9 || (mx < best_max + 1e-9 && at_max < best_at_max))) {
       best_max = mx;
+      best_at_max = at_max;
       best = p;
     }
   }
@@ -230,7 +243,7 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     for (int x : part) s += x;
     if (s != dm.L) throw std::invalid_argument("engine: layers_per_stage must sum to layers");
   } else {
-    part = balance_layers(dm.L, depth_, dm.h, dm.V);
+    part = balance_layers(dm.L, depth_, dm.h, dm.V, dm.ffn, dm.S, dm.causal);
     if (part.empty()) throw std::invalid_argument("engine: cannot partition layers over stages");
   }
   int l = 0;
