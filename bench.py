@@ -152,6 +152,11 @@ def schedule_baseline():
         return None
 
 
+def lib_numel(eng, stage):
+    from paper_2605_29664_b200 import engine as E
+    return int(E.lib.amdp_engine_stage_numel(eng._h, stage))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -263,7 +268,9 @@ def main():
         try:  # d-GPU projection of this measured run (static-order replay, reference bubble_ratio)
             from paper_2605_29664_b200 import projection as PR
             gap_ns = model.tokens_per_minibatch * model.hidden * 2 / 770e9 * 1e9
-            projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns)
+            numel = [lib_numel(eng, i) for i in range(args.depth)]
+            projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
+                                    stage_numel=numel)
         except Exception as e:  # never let the projection break the bench line
             projection = {"error": str(e)[:200]}
 

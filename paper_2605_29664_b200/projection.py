@@ -66,13 +66,35 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
     return P.Timeline.from_events(events, policy.policy, depth, devices, policy.accumulation_threshold)
 
 
+def collective_costs(stage_numel, replicas: int, link_gbs: float = 770.0) -> Dict[Tuple[P.Kind, int], float]:
+    """Window-boundary communication a 1-GPU run does not perform: per stage, the ZeRO Reduce of
+    the fp32 window gradient to the owner and the Broadcast of the fp32 weights over the
+    stage's `replicas` devices, each moving (replicas-1)/replicas of the stage's bytes per
+    device (analysis.hpp:341-346 reduce_broadcast_cost) at the measured peer bandwidth."""
+    f = (replicas - 1) / replicas if replicas > 1 else 0.0
+    out = {}
+    for s, n in enumerate(stage_numel):
+        t = f * 4.0 * n / (link_gbs * 1e9) * 1e9
+        out[(P.Kind.Reduce, s)] = t
+        out[(P.Kind.Broadcast, s)] = t
+    return out
+
+
 def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, tokens_per_minibatch: int,
-            gap_ns: float) -> dict:
-    """Projected d-GPU bubble and throughput of the AMDP schedule from a measured run."""
+            gap_ns: float, stage_numel=None) -> dict:
+    """Projected d-GPU bubble and throughput of the AMDP schedule from a measured run.  With
+    `stage_numel`, the Reduce / Broadcast tasks also carry the NVLink collective time
+    (collective_costs) on top of what was measured on one GPU (the fused optimizer)."""
     costs = measured_costs(tl_measured)
     pol = P.PolicyConfig(policy=P.Policy.AMDP, injection_limit=2, num_pipelines=depth // 2,
                          accumulation_threshold=threshold, num_minibatches=windows * threshold,
                          zero_enabled=True)
+    bubble_nc = None
+    if stage_numel is not None:
+        rep0 = static_order_replay(pol, depth, costs, gap_ns)
+        bubble_nc = float(P.bubble_ratio(rep0, 1 if windows > 2 else 0))
+        for k, v in collective_costs(stage_numel, depth // 2).items():
+            costs[k] = costs.get(k, 0.0) + v
     rep = static_order_replay(pol, depth, costs, gap_ns)
     bubble = P.bubble_ratio(rep, 1 if windows > 2 else 0)
     # steady-state window period: first F of window w to first F of window w+1, averaged
@@ -82,13 +104,14 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
             firsts[ev.window] = min(firsts.get(ev.window, ev.start), ev.start)
     ws = sorted(firsts)
     period = float(firsts[ws[-1]] - firsts[ws[1]]) / (len(ws) - 2) if len(ws) > 2 else None
-    return {"gpus": depth, "bubble": float(bubble),
+    return {"gpus": depth, "bubble": float(bubble), "bubble_without_collectives": bubble_nc,
             "tokens_per_s": (threshold * tokens_per_minibatch / (period * 1e-9)) if period else None,
             "gap_us": gap_ns / 1e3,
             "stage_ms": {f"{KIND_TAG[k[0]]}{k[1]}": round(v / 1e6, 3) for k, v in sorted(costs.items())},
             "method": "static-order replay of the declared AMDP dispatch order on one GPU per "
-                      "logical device, task costs = measured 1-GPU means (windows >= 1), "
-                      "inter-device gap = activation bytes / 770 GB/s peer copy; bubble = "
+                      "logical device, task costs = measured 1-GPU means (windows >= 1) plus the "
+                      "window Reduce/Broadcast collectives at 770 GB/s ((P-1)/P of the stage's fp32 "
+                      "bytes each), inter-device gap = activation bytes / 770 GB/s peer copy; bubble = "
                       "reference bubble_ratio(tl, 1).  A projection, not a multi-GPU measurement."}
 
 

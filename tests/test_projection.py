@@ -60,3 +60,11 @@ def test_compare_policies_all_schedules_run_and_amdp_matches_project():
         assert 0 <= r["bubble_w1"] < 1 and r["tokens_per_s"] > 0
     rep = PR.static_order_replay(_pol(d, thr, windows), d, costs, 40.0)
     assert abs(float(P.bubble_ratio(rep, 1)) - res["AMDP"]["bubble_w1"]) < 1e-12
+
+
+def test_collective_costs_follow_reduce_broadcast_cost():
+    # (P-1)/P of the stage's fp32 bytes per phase at the link bandwidth (analysis.hpp:341-346)
+    c = PR.collective_costs([1_000_000, 2_000_000], 4, link_gbs=1000.0)
+    assert abs(c[(P.Kind.Reduce, 0)] - 0.75 * 4e6 / 1e12 * 1e9) < 1e-6
+    assert c[(P.Kind.Broadcast, 1)] == 2 * c[(P.Kind.Broadcast, 0)]
+    assert PR.collective_costs([5], 1) == {(P.Kind.Reduce, 0): 0.0, (P.Kind.Broadcast, 0): 0.0}
