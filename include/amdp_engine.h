@@ -53,6 +53,9 @@ typedef struct amdp_run_config {
   uint64_t data_seed;
   int plan_only;               /* 1 = plan (hosting/slots/comm program) without  */
                                /*     touching CUDA or NCCL; see plan_json       */
+  int depth;                   /* stages = devices; 0 = 2 x num_pipelines (AMDP).  */
+                               /* Policies: AMDP (ZeRO on), or DAPPLE / GPipe with */
+                               /* one pipeline and per-window Update tasks         */
 } amdp_run_config;
 
 typedef struct amdp_engine amdp_engine;

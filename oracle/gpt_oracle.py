@@ -373,7 +373,7 @@ def replay(trace_csv: str, m: Model, partition: List[int], opt: Opt, threshold: 
             g = math_[i].backward(work[i], caches.pop((i, j)), gsend.pop((i, j), None), inputs[j], grads[i])
             if g is not None:
                 gsend[(i - 1, j)] = g
-        elif e["kind"] == "Broadcast":
+        elif e["kind"] in ("Broadcast", "Update"):  # ZeRO owner step / single-replica Update (P = 1)
             step = e["window"] + 1
             for k in master[i]:
                 apply_update(opt, master[i][k], mom[i][k], vel[i][k], grads[i][k] / threshold, step)

@@ -199,13 +199,23 @@ class Engine {
 
 Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uint8_t* nccl_id)
     : mc_(mc), rc_(rc) {
-  depth_ = rc.policy.num_pipelines * 2;
+  depth_ = rc.depth > 0 ? rc.depth : rc.policy.num_pipelines * 2;
   world_ = std::max(1, rc.world_size);
   rank_ = rc.rank;
-  if (rc.policy.policy != 0) throw std::invalid_argument("engine: only the AMDP policy executes on GPUs");
-  if (!rc.policy.zero_enabled)
-    throw std::invalid_argument("engine: AMDP execution needs zero_enabled (sharded Reduce/Broadcast); "
-                                "replicated updates would need one weight copy per pipeline replica");
+  const auto pol = static_cast<ppsim::Policy>(rc.policy.policy);
+  if (pol == ppsim::Policy::AMDP) {
+    if (!rc.policy.zero_enabled)
+      throw std::invalid_argument("engine: AMDP execution needs zero_enabled (sharded Reduce/Broadcast); "
+                                  "replicated updates would need one weight copy per pipeline replica");
+    if (depth_ != 2 * rc.policy.num_pipelines)
+      throw std::invalid_argument("engine: AMDP runs depth = 2 x num_pipelines stages");
+  } else if (pol == ppsim::Policy::DAPPLE || pol == ppsim::Policy::GPipe) {
+    // one pipeline, one replica per stage: the window's Update(w, i, 0) is the optimizer step
+    if (rc.policy.num_pipelines != 1 || rc.policy.zero_enabled)
+      throw std::invalid_argument("engine: DAPPLE / GPipe execute with one pipeline and zero_enabled off");
+  } else {
+    throw std::invalid_argument("engine: executes AMDP, DAPPLE and GPipe schedules");
+  }
   if (depth_ % world_ != 0) throw std::invalid_argument("engine: depth must be a multiple of world_size");
   per_rank_ = depth_ / world_;
   M_ = rc.policy.num_minibatches;
@@ -256,13 +266,15 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   hosted.assign(static_cast<size_t>(depth_), false);
   owned.assign(static_cast<size_t>(depth_), false);
   group_ranks_.assign(static_cast<size_t>(depth_), {});
+  // replica group of stage i: the ranks whose devices run a Forward / Backward of stage i
+  // (AMDP: map_stage_to_device over the d/2 pipelines, builder.hpp:81-88; DAPPLE/GPipe: device i)
+  for (const auto& t : sched.g.tasks) {
+    if (t.kind != ppsim::Kind::Forward && t.kind != ppsim::Kind::Backward) continue;
+    auto& gr = group_ranks_[static_cast<size_t>(t.stage)];
+    const int r = rank_of_dev(t.device);
+    if (std::find(gr.begin(), gr.end(), r) == gr.end()) gr.push_back(r);
+  }
   for (int i = 0; i < depth_; ++i) {
-    for (int p = 0; p < depth_ / 2; ++p) {
-      const int r = rank_of_dev(ppsim::map_stage_to_device(p, i, depth_));
-      if (std::find(group_ranks_[static_cast<size_t>(i)].begin(), group_ranks_[static_cast<size_t>(i)].end(), r) ==
-          group_ranks_[static_cast<size_t>(i)].end())
-        group_ranks_[static_cast<size_t>(i)].push_back(r);
-    }
     std::sort(group_ranks_[static_cast<size_t>(i)].begin(), group_ranks_[static_cast<size_t>(i)].end());
     hosted[static_cast<size_t>(i)] = std::count(group_ranks_[static_cast<size_t>(i)].begin(),
                                                 group_ranks_[static_cast<size_t>(i)].end(), rank_) > 0;
@@ -672,6 +684,23 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
       cudaEventDestroy(e);
     }
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    stats.tasks_executed += 1;
+    return;
+  }
+  if (task.kind == ppsim::Kind::Update) {  // single-replica window update (DAPPLE / GPipe)
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    amdp_opt_args o = rc_.optimizer;
+    o.step = task.window + 1;
+    o.grad_scale = rc_.optimizer.grad_scale * (1.0f / static_cast<float>(thr_));
+    ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), cs_);
+    rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), st);
+    ktimer_.end(cs_);
+    if (rc != 0) throw std::runtime_error("optimizer step failed");
+    const int nt = S.refresh_transposed(cs_);
+    if (nt < 0) throw std::runtime_error("weight transpose failed");
+    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i);
+    stats.kernels_launched += 2 + nt;
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
     stats.tasks_executed += 1;
     return;
@@ -1111,7 +1140,8 @@ namespace ppsim {
 
 ExecuteResult execute(const PolicyConfig& cfg, const ClusterSpec& declared, const ExecuteOptions& opt,
                       const int32_t* inputs, const int32_t* labels) {
-  if (cfg.policy != Policy::AMDP) throw std::invalid_argument("execute: only the AMDP policy runs on GPUs");
+  if (cfg.policy != Policy::AMDP && cfg.policy != Policy::DAPPLE && cfg.policy != Policy::GPipe)
+    throw std::invalid_argument("execute: AMDP, DAPPLE and GPipe schedules run on GPUs");
   if (declared.fwd_cost.empty() || declared.bwd_cost.empty())
     throw std::invalid_argument("execute: declared cluster needs per-stage costs");
   for (std::size_t i = 1; i < declared.fwd_cost.size(); ++i)
@@ -1130,12 +1160,13 @@ ExecuteResult execute(const PolicyConfig& cfg, const ClusterSpec& declared, cons
   rc.rank = opt.rank;
   rc.record_events = 1;
   rc.data_seed = opt.data_seed;
+  rc.depth = declared.depth;
   amdp::Engine eng(opt.model, rc, opt.nccl_id);
   ExecuteResult out;
   out.losses.assign(static_cast<std::size_t>(cfg.num_minibatches), 0.f);
   eng.run(inputs, labels, out.losses.data());
   out.stats = eng.stats;
-  out.timeline.policy = Policy::AMDP;
+  out.timeline.policy = cfg.policy;
   out.timeline.depth = declared.depth;
   out.timeline.devices = declared.devices;
   out.timeline.threshold = cfg.accumulation_threshold;

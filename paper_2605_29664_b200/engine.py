@@ -35,7 +35,8 @@ class _Model(Structure):
 class _Run(Structure):
     _fields_ = [("policy", P._Policy), ("declared_fwd", P._Rat), ("declared_bwd", P._Rat),
                 ("optimizer", N.OptArgs), ("world_size", c_int), ("rank", c_int),
-                ("record_events", c_int), ("data_seed", c_uint64), ("plan_only", c_int)]
+                ("record_events", c_int), ("data_seed", c_uint64), ("plan_only", c_int),
+                ("depth", c_int)]
 
 
 class _Stats(Structure):
@@ -164,14 +165,22 @@ class RunConfig:
     record_events: bool = True
     data_seed: int = 1234
     plan_only: bool = False   # host-side plan without CUDA/NCCL (multi-rank tests on CPU)
+    # "AMDP" (d/2 pipelines, ZeRO), or the synchronous single-pipeline baselines "DAPPLE" /
+    # "GPipe" (builder.hpp: injection = threshold, replicated weights, Update per window)
+    schedule: str = "AMDP"
 
     @property
     def num_minibatches(self) -> int:
         return self.windows * self.threshold
 
     def policy(self) -> P.PolicyConfig:
-        return P.PolicyConfig(P.Policy.AMDP, 2, self.depth // 2, self.threshold,
-                              self.num_minibatches, True)
+        if self.schedule == "AMDP":
+            return P.PolicyConfig(P.Policy.AMDP, 2, self.depth // 2, self.threshold,
+                                  self.num_minibatches, True)
+        if self.schedule in ("DAPPLE", "GPipe"):
+            return P.PolicyConfig(P.Policy[self.schedule], self.threshold, 1, self.threshold,
+                                  self.num_minibatches, False)
+        raise ValueError(f"schedule {self.schedule!r} does not execute on GPUs")
 
     def declared_cluster(self) -> P.ClusterSpec:
         return P.ClusterSpec.uniform(self.depth, self.depth, self.declared_fwd, self.declared_bwd)
@@ -179,7 +188,7 @@ class RunConfig:
     def _c(self):
         return _Run(self.policy()._c(), P._r(self.declared_fwd), P._r(self.declared_bwd),
                     self.optimizer._c(), self.world_size, self.rank, int(self.record_events),
-                    self.data_seed, int(self.plan_only))
+                    self.data_seed, int(self.plan_only), self.depth)
 
 
 def nccl_unique_id() -> bytes:

@@ -40,6 +40,8 @@ CONFIGS += [
     ("Chimera", 8, 8, "1", "1", "0", "0", 8, 2, 8, 16, 0),
     ("PipeDreamAsync", 4, 4, "1", "1", "0", "0", 2, 1, 1, 16, 0),
     ("PipeDreamAsync", 8, 8, "1", "2", "1/2", "0", 8, 1, 4, 32, 0),
+    ("DAPPLE", 4, 4, "1", "1", "0", "0", 8, 1, 8, 32, 0),     # tiny GPT on the executor (P = 1)
+    ("GPipe", 4, 4, "1", "1", "0", "0", 8, 1, 8, 32, 0),
 ]
 
 

@@ -127,3 +127,36 @@ def test_gloo_world2_plans_consistent():
     status, val = q.get(timeout=10)
     assert status == "ok", val
     assert val > 0
+
+
+@pytest.mark.parametrize("schedule", ["DAPPLE", "GPipe"])
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_synchronous_baselines_plan(schedule, world):
+    """DAPPLE / GPipe on the executor (one pipeline, stage i on device i, per-window Update):
+    every stage is hosted and owned by the rank of its device, replica groups are single
+    ranks (no collectives), and the P2P program pairs up across ranks."""
+    model = E.ModelConfig.gpt_1p3b()
+    plans = []
+    for r in range(world):
+        run = E.RunConfig(depth=8, threshold=8, windows=2, world_size=world, rank=r, plan_only=True,
+                          schedule=schedule)
+        plans.append(E.Engine(model, run).plan())
+    per = 8 // world
+    for r, pl in enumerate(plans):
+        for s in pl["stages"]:
+            assert s["hosted"] == (s["stage"] // per == r)
+            assert s["owner"] == (s["stage"] // per == r)
+            assert s["group"] == [s["stage"] // per]
+        assert all(o[1] in ("send", "recv") for o in pl["comm_ops"])
+    ops = [[tuple(o) for o in pl["comm_ops"]] for pl in plans]
+    for r in range(world):
+        for (k, kind, peer, stage) in ops[r]:
+            assert (k, "recv" if kind == "send" else "send", r, -1) in ops[peer]
+
+
+def test_unsupported_schedules_rejected():
+    model = E.ModelConfig.tiny()
+    with pytest.raises(ValueError):  # replicated multi-pipeline schedules do not execute
+        E.Engine(model, E.RunConfig(depth=4, threshold=8, windows=2, plan_only=True, schedule="Chimera"))
+    with pytest.raises(RuntimeError):  # AMDP needs an even depth (validate.hpp:60-73)
+        E.Engine(model, E.RunConfig(depth=3, threshold=8, windows=2, plan_only=True))
