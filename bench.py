@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--model", default="1p3b")
     ap.add_argument("--threshold", type=int, default=32)
     ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--schedule", default="AMDP", choices=["AMDP", "DAPPLE", "GPipe"],
+                    help="AMDP (headline) or a synchronous single-pipeline baseline on the same executor")
     ap.add_argument("--no-kernel-timing", action="store_true")
     args = ap.parse_args()
 
@@ -174,14 +176,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     model = model_cfg(args.model)
     tok_step = args.threshold * model.tokens_per_minibatch
-    cfg = {"workload": f"GPT-style {args.model} AMDP D={args.depth} ({args.depth // 2} pipelines), "
+    npipe = args.depth // 2 if args.schedule == "AMDP" else 1
+    cfg = {"workload": f"GPT-style {args.model} {args.schedule} D={args.depth} ({npipe} pipelines), "
                        f"seq {model.seq}, {model.seqs_per_minibatch} seqs/minibatch, "
                        f"{args.threshold} minibatches/step",
            "model": f"gpt-{args.model}", "layers": model.layers, "hidden": model.hidden,
            "global_batch": args.threshold * model.seqs_per_minibatch, "seq_len": model.seq,
-           "tokens_per_step": tok_step, "parallelism": f"amdp-d{args.depth}-p{args.depth // 2} folded on {args.gpus} GPU",
+           "tokens_per_step": tok_step, "parallelism": f"{args.schedule.lower()}-d{args.depth}-p{npipe} folded on {args.gpus} GPU",
            "declared_costs": "uniform fwd=1 bwd=1 (preload 1)", "l2": "working set >> L2 (no flush)"}
-    metric = "tokens/s AMDP GPT-style training"
+    metric = "tokens/s AMDP GPT-style training" if args.schedule == "AMDP" else f"tokens/s {args.schedule} GPT-style training"
 
     if args.impl == "reference":
         if rank != 0:
@@ -234,7 +237,7 @@ def main():
 
     windows = max(args.steps, args.warmup)
     opt = E.OptimizerConfig(lr=1e-4, weight_decay=0.0)
-    run = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=windows, optimizer=opt,
+    run = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=windows, optimizer=opt, schedule=args.schedule,
                       world_size=world, rank=rank)
     eng = E.Engine(model, run, nccl_id)
     M = run.num_minibatches
@@ -269,8 +272,10 @@ def main():
             from paper_2605_29664_b200 import projection as PR
             gap_ns = model.tokens_per_minibatch * model.hidden * 2 / 770e9 * 1e9
             numel = [lib_numel(eng, i) for i in range(args.depth)]
+            pol = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=args.steps,
+                              schedule=args.schedule).policy()
             projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
-                                    stage_numel=numel)
+                                    stage_numel=numel if args.schedule == "AMDP" else None, policy=pol)
         except Exception as e:  # never let the projection break the bench line
             projection = {"error": str(e)[:200]}
 

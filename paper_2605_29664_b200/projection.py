@@ -81,14 +81,14 @@ def collective_costs(stage_numel, replicas: int, link_gbs: float = 770.0) -> Dic
 
 
 def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, tokens_per_minibatch: int,
-            gap_ns: float, stage_numel=None) -> dict:
-    """Projected d-GPU bubble and throughput of the AMDP schedule from a measured run.  With
+            gap_ns: float, stage_numel=None, policy: P.PolicyConfig = None) -> dict:
+    """Projected d-GPU bubble and throughput of a measured run's schedule (default AMDP).  With
     `stage_numel`, the Reduce / Broadcast tasks also carry the NVLink collective time
     (collective_costs) on top of what was measured on one GPU (the fused optimizer)."""
     costs = measured_costs(tl_measured)
-    pol = P.PolicyConfig(policy=P.Policy.AMDP, injection_limit=2, num_pipelines=depth // 2,
-                         accumulation_threshold=threshold, num_minibatches=windows * threshold,
-                         zero_enabled=True)
+    pol = policy or P.PolicyConfig(policy=P.Policy.AMDP, injection_limit=2, num_pipelines=depth // 2,
+                                   accumulation_threshold=threshold, num_minibatches=windows * threshold,
+                                   zero_enabled=True)
     bubble_nc = None
     if stage_numel is not None:
         rep0 = static_order_replay(pol, depth, costs, gap_ns)
@@ -108,7 +108,7 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
             "tokens_per_s": (threshold * tokens_per_minibatch / (period * 1e-9)) if period else None,
             "gap_us": gap_ns / 1e3,
             "stage_ms": {f"{KIND_TAG[k[0]]}{k[1]}": round(v / 1e6, 3) for k, v in sorted(costs.items())},
-            "method": "static-order replay of the declared AMDP dispatch order on one GPU per "
+            "method": "static-order replay of the declared dispatch order on one GPU per "
                       "logical device, task costs = measured 1-GPU means (windows >= 1) plus the "
                       "window Reduce/Broadcast collectives at 770 GB/s ((P-1)/P of the stage's fp32 "
                       "bytes each), inter-device gap = activation bytes / 770 GB/s peer copy; bubble = "
