@@ -46,7 +46,7 @@ def peaks():
 def model_cfg(name):
     from paper_2605_29664_b200 import engine as E
     return {"1p3b": E.ModelConfig.gpt_1p3b, "350m": E.ModelConfig.gpt_350m,
-            "2p7b": E.ModelConfig.gpt_2p7b, "tiny": E.ModelConfig.tiny}[name]()
+            "2p7b": E.ModelConfig.gpt_2p7b, "bert": E.ModelConfig.bert_large, "tiny": E.ModelConfig.tiny}[name]()
 
 
 class ClockSampler:
