@@ -180,7 +180,7 @@ def main():
     cfg = {"workload": f"GPT-style {args.model} {args.schedule} D={args.depth} ({npipe} pipelines), "
                        f"seq {model.seq}, {model.seqs_per_minibatch} seqs/minibatch, "
                        f"{args.threshold} minibatches/step",
-           "model": f"gpt-{args.model}", "layers": model.layers, "hidden": model.hidden,
+           "model": ("bert-large" if args.model == "bert" else f"gpt-{args.model}"), "layers": model.layers, "hidden": model.hidden,
            "global_batch": args.threshold * model.seqs_per_minibatch, "seq_len": model.seq,
            "tokens_per_step": tok_step, "parallelism": f"{args.schedule.lower()}-d{args.depth}-p{npipe} folded on {args.gpus} GPU",
            "declared_costs": "uniform fwd=1 bwd=1 (preload 1)", "l2": "working set >> L2 (no flush)"}
