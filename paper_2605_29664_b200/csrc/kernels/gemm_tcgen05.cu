@@ -55,7 +55,6 @@ struct EpiParams {
   __nv_bfloat16* C2;
   int ldc2;
   float alpha;
-  uint32_t epi_sleep_ns;  // epilogue warps' back-off while a tile's main loop runs (0: spin)
 };
 
 // tanh on the SFU (tanh.approx.f32, max rel. error ~2^-11): the GELU epilogues run once per
@@ -557,8 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       int m0, n0, width;
       pair_work(sc, w, m0, n0, width);
       const int row0 = m0 + 128 * static_cast<int>(rank) + q * 32;
-      if (p.epi_sleep_ns) ptx::mbar_wait_sleep(&tfull_bar[acc], acc_phase, p.epi_sleep_ns);
-      else ptx::mbar_wait(&tfull_bar[acc], acc_phase);
+      ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * PBN;
       if constexpr (EPI == EPI_DISCARD) {
@@ -738,11 +736,6 @@ int dispatch_epi(int mode, int epi, const CUtensorMap& ma, const CUtensorMap& mb
   return AMDP_ERR_INVALID;
 }
 
-uint32_t epi_sleep_ns() {
-  static const uint32_t ns = static_cast<uint32_t>(env_int("AMDP_GEMM_EPI_SLEEP", 0));
-  return ns;
-}
-
 int gemm_pairs() {
   static const int nst = env_int("AMDP_GEMM_STAGES", 6);
   return nst == 4 ? max_pairs<4>() : max_pairs<6>();
@@ -813,8 +806,7 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
   }
   EpiParams p{a->M, a->N, a->K, a->C, a->ldc,
               static_cast<const __nv_bfloat16*>(a->aux), a->ld_aux,
-              static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha,
-              epi_sleep_ns()};
+              static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int am = a->a_mn_major ? 1 : 0, bm = a->b_mn_major ? 1 : 0;
   if (!am && !bm) return dispatch_epi<false, false>(mode, a->epilogue, ma, mb, mbt, em, p, s);

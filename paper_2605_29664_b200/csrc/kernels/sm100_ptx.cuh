@@ -42,25 +42,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Same, but backs off with nanosleep between probes: for warps that wait long (epilogue
-// warps during a tile's main loop), so they do not keep issuing try_wait probes.
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  while (!mbar_try(bar, parity)) __nanosleep(ns);
-}
-
 // Programmatic dependent launch: the kernel may start while its predecessor in the stream
 // drains; it must not touch the predecessor's outputs (or buffers it still reads) before
 // pdl_wait().  pdl_trigger() lets the successor launch as soon as every CTA got here.
