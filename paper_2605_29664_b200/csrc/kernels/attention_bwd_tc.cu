@@ -359,11 +359,17 @@ struct QSmem {
   static constexpr uint32_t BYTES = BAR + 512;
 };
 
+// Persistent: one CTA per SM walks (128-query tile, head, sequence) tiles heavy-first in a
+// snake order; the K/V ring, the S/dP/dS hand-off barriers and the dO buffer run on across
+// tiles, so the next tile's loads land during this tile's last blocks and epilogue instead of
+// behind a fresh CTA's prologue (the non-persistent version spent ~9k cycles before its
+// first MMA: profiles/r01_attn_traces.md).
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap qkv_map, const __grid_constant__ CUtensorMap do_map,
                      const bf16* __restrict__ qkv, const float* __restrict__ lse, const float* __restrict__ delta,
-                     bf16* __restrict__ dqkv, int seq, int H, int n_qt, float scale_log2, float scale, int causal) {
+                     bf16* __restrict__ dqkv, int seq, int H, int n_qt, int BH, float scale_log2, float scale,
+                     int causal) {
   using L = QSmem<D>;
   constexpr int NSK = L::NSK, NSV = L::NSV;
   extern __shared__ uint8_t smem_raw[];
@@ -383,15 +389,23 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* p_full = d_empty + 1;      // 256 arrivals: dS written into TMEM
   uint64_t* ds_empty = p_full + 1;     // dQ MMA has read dS
   uint64_t* dq_done = ds_empty + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+  uint64_t* do_empty = dq_done + 1;    // the tile's last dP MMA has read dO
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(do_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int BH = static_cast<int>(gridDim.x) / n_qt;  // heavy first across the grid (see dK/dV)
-  const int qt = n_qt - 1 - static_cast<int>(blockIdx.x) / BH;
-  const int hb = static_cast<int>(blockIdx.x) % BH;
-  const int h = hb % H, b = hb / H;
-  const int row0 = b * seq;
-  const int N = causal ? qt + 1 : seq / 128;
+  const int ntiles = n_qt * BH;
+  const int G = static_cast<int>(gridDim.x), cta = static_cast<int>(blockIdx.x);
+  // tile it of this CTA: snake over the heavy-first list (query tile n_qt-1 of every head first)
+  auto tile_of = [&](int it, int& qt, int& h, int& b) -> bool {
+    const int idx = it * G + ((it & 1) ? (G - 1 - cta) : cta);
+    if (idx >= ntiles) return false;
+    qt = n_qt - 1 - idx / BH;
+    const int hb = idx % BH;
+    h = hb % H;
+    b = hb / H;
+    return true;
+  };
+  auto nblocks = [&](int qt) { return causal ? qt + 1 : seq / 128; };
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&qkv_map);
@@ -412,6 +426,7 @@ __global__ void __launch_bounds__(384, 1)
     ptx::mbar_init(p_full, 256);
     ptx::mbar_init(ds_empty, 1);
     ptx::mbar_init(dq_done, 1);
+    ptx::mbar_init(do_empty, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -429,172 +444,180 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     ptx::regs_dec<56>();
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(do_full, L::NB * T128);
-      for (int c = 0; c < L::NB; ++c)
-        ptx::tma_load_2d(sm + L::DO + c * T128, &do_map, do_full, h * D + 64 * c, row0 + qt * 128);
-      // K(j) ahead of V(j): S(j) is issued before dP(j)
-      for (int n = 0; n < N; ++n) {
-        const int sk = n % NSK, sv = n % NSV;
-        ptx::mbar_wait(&k_empty[sk], ((n / NSK) & 1) ^ 1);
-        BW_T(6, n);
-#ifdef FA_ABL_NOLOAD
-        if (n >= NSK) {
-          ptx::mbar_arrive(&k_full[sk]);
-          ptx::mbar_wait(&v_empty[sv], ((n / NSV) & 1) ^ 1);
-          ptx::mbar_arrive(&v_full[sv]);
-          continue;
+      int g0 = 0;  // K/V blocks loaded by this CTA so far (ring position)
+      int qt, h, b;
+      for (int it = 0; tile_of(it, qt, h, b); ++it) {
+        const int row0 = b * seq, N = nblocks(qt);
+        ptx::mbar_wait(do_empty, (it & 1) ^ 1);  // previous tile's last dP MMA read dO
+        ptx::mbar_arrive_expect_tx(do_full, L::NB * T128);
+        for (int c = 0; c < L::NB; ++c)
+          ptx::tma_load_2d(sm + L::DO + c * T128, &do_map, do_full, h * D + 64 * c, row0 + qt * 128);
+        // K(j) ahead of V(j): S(j) is issued before dP(j)
+        for (int n = 0; n < N; ++n) {
+          const int g = g0 + n, sk = g % NSK, sv = g % NSV;
+          ptx::mbar_wait(&k_empty[sk], ((g / NSK) & 1) ^ 1);
+          if (it == 0) BW_T(6, n);
+          ptx::mbar_arrive_expect_tx(&k_full[sk], L::NB * T128);
+          for (int c = 0; c < L::NB; ++c)
+            ptx::tma_load_2d(sm + L::K + (sk * L::NB + c) * T128, &qkv_map, &k_full[sk], H * D + h * D + 64 * c,
+                             row0 + n * 128);
+          ptx::mbar_wait(&v_empty[sv], ((g / NSV) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&v_full[sv], L::NB * T128);
+          for (int c = 0; c < L::NB; ++c)
+            ptx::tma_load_2d(sm + L::V + (sv * L::NB + c) * T128, &qkv_map, &v_full[sv],
+                             2 * H * D + h * D + 64 * c, row0 + n * 128);
         }
-#endif
-        ptx::mbar_arrive_expect_tx(&k_full[sk], L::NB * T128);
-        for (int c = 0; c < L::NB; ++c)
-          ptx::tma_load_2d(sm + L::K + (sk * L::NB + c) * T128, &qkv_map, &k_full[sk], H * D + h * D + 64 * c,
-                           row0 + n * 128);
-        ptx::mbar_wait(&v_empty[sv], ((n / NSV) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&v_full[sv], L::NB * T128);
-        for (int c = 0; c < L::NB; ++c)
-          ptx::tma_load_2d(sm + L::V + (sv * L::NB + c) * T128, &qkv_map, &v_full[sv],
-                           2 * H * D + h * D + 64 * c, row0 + n * 128);
+        g0 += N;
       }
     }
   } else if (warp == 1) {
     ptx::regs_dec<56>();
-    {  // warp-wide MMA issue (elect.sync inside the asm; see mma_bf16_*_w)
+    {  // warp-wide MMA issue (elect.sync inside the asm; see mma_bf16_*_w); descriptors built
+       // once per stage and advanced by adding the 16-byte-unit offset to their address field
       constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128, false, false);
       constexpr uint32_t id_g = ptx::idesc_bf16_f32(128, D, false, true);
-      const uint32_t sdo = ptx::smem_u32(sm + L::DO);
-      ptx::mbar_wait(q_full, 0);
-      ptx::mbar_wait(do_full, 0);
-      // warp-wide issue (see mma_bf16_*_w); descriptors built once per stage and advanced by
-      // adding the 16-byte-unit offset to their address field (smem < 256 KB: no carry)
-      const uint64_t dsdo = ptx::umma_desc_sw128(sdo, 16, 1024);
-      for (int n = 0; n <= N; ++n) {
-        if (n < N) {
-          const int stk = n % NSK, stv = n % NSV;
-          ptx::mbar_wait(&k_full[stk], (n / NSK) & 1);
-          BW_T(0, n);
-          ptx::mbar_wait(s_empty, (n & 1) ^ 1);
-          BW_T(1, n);
-          ptx::tc_fence_after();
-          const uint64_t dk = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K + stk * L::NB * T128), 16, 1024);
-          const uint64_t dv = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::V + stv * L::NB * T128), 16, 1024);
+      const uint64_t dsdo = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::DO), 16, 1024);
+      int g0 = 0;
+      int qt, h, b;
+      for (int it = 0; tile_of(it, qt, h, b); ++it) {
+        const int N = nblocks(qt);
+        ptx::mbar_wait(q_full, it & 1);   // this tile's Q in TMEM (written after the last dQ drain)
+        ptx::mbar_wait(do_full, it & 1);
+        for (int n = 0; n <= N; ++n) {
+          if (n < N) {
+            const int g = g0 + n, stk = g % NSK, stv = g % NSV;
+            ptx::mbar_wait(&k_full[stk], (g / NSK) & 1);
+            if (it == 0) BW_T(0, n);
+            ptx::mbar_wait(s_empty, (g & 1) ^ 1);
+            if (it == 0) BW_T(1, n);
+            ptx::tc_fence_after();
+            const uint64_t dk = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K + stk * L::NB * T128), 16, 1024);
+            const uint64_t dv = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::V + stv * L::NB * T128), 16, 1024);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            ptx::mma_bf16_ts_w(tmem, t_q + kk * 8, dk + (((kk >> 2) * T128 + (kk & 3) * 32) >> 4), id_s, kk > 0);
-          ptx::mbar_wait(&v_full[stv], (n / NSV) & 1);
-          ptx::mbar_wait(d_empty, (n & 1) ^ 1);  // dP(n-1) loaded: S(n) above overlapped that load
-          ptx::tc_fence_after();
+            for (int kk = 0; kk < D / 16; ++kk)
+              ptx::mma_bf16_ts_w(tmem, t_q + kk * 8, dk + (((kk >> 2) * T128 + (kk & 3) * 32) >> 4), id_s, kk > 0);
+            ptx::mbar_wait(&v_full[stv], (g / NSV) & 1);
+            ptx::mbar_wait(d_empty, (g & 1) ^ 1);  // dP(g-1) loaded: S(g) above overlapped that load
+            ptx::tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t o = ((kk >> 2) * T128 + (kk & 3) * 32) >> 4;
-            ptx::mma_bf16_ss_w(tmem + 128, dsdo + o, dv + o, id_s, kk > 0);
+            for (int kk = 0; kk < D / 16; ++kk) {
+              const uint32_t o = ((kk >> 2) * T128 + (kk & 3) * 32) >> 4;
+              ptx::mma_bf16_ss_w(tmem + 128, dsdo + o, dv + o, id_s, kk > 0);
+            }
+            ptx::mma_commit_w(s_full);
+            ptx::mma_commit_w(&v_empty[stv]);
+            if (n == N - 1) ptx::mma_commit_w(do_empty);  // last read of this tile's dO
+            if (it == 0) BW_T(8, n);
           }
-          ptx::mma_commit_w(s_full);
-          ptx::mma_commit_w(&v_empty[stv]);
-          BW_T(8, n);
-        }
-        if (n > 0) {
-          const int m = n - 1, stk = m % NSK;
-          ptx::mbar_wait(p_full, m & 1);
-          BW_T(2, m);
-          ptx::tc_fence_after();
-          const uint64_t dk = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K + stk * L::NB * T128), T128, 1024);
+          if (n > 0) {
+            const int m = n - 1, g = g0 + m, stk = g % NSK;
+            ptx::mbar_wait(p_full, g & 1);
+            if (it == 0) BW_T(2, m);
+            ptx::tc_fence_after();
+            const uint64_t dk = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K + stk * L::NB * T128), T128, 1024);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            ptx::mma_bf16_ts_w(t_dq, t_ds + kk * 8, dk + ((kk * 2048) >> 4), id_g, (m > 0 || kk > 0));
-          ptx::mma_commit_w(ds_empty);
-          ptx::mma_commit_w(&k_empty[stk]);
-          BW_T(9, m);
+            for (int kk = 0; kk < 8; ++kk)
+              ptx::mma_bf16_ts_w(t_dq, t_ds + kk * 8, dk + ((kk * 2048) >> 4), id_g, (m > 0 || kk > 0));
+            ptx::mma_commit_w(ds_empty);
+            ptx::mma_commit_w(&k_empty[stk]);
+            if (it == 0) BW_T(9, m);
+          }
         }
+        ptx::mma_commit_w(dq_done);
+        g0 += N;
       }
-      ptx::mma_commit_w(dq_done);
     }
   } else if (warp >= 4) {
     ptx::regs_inc<224>();
     const int wg = (warp - 4) >> 2;  // keys [64 wg, 64 wg + 64) of every block
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    const int qrow = qt * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
     const int c0 = 64 * wg;
-    const size_t bh = (static_cast<size_t>(b) * H + h) * seq;
-    const float nl = -lse[bh + qrow], dl = delta[bh + qrow];
-    {  // this thread's half of its Q row -> TMEM (bf16 pairs: column j holds dims 2j, 2j+1).
-       // Warpgroup wg owns dims [32 (D/64) wg, +32 (D/64)) and, for head_dim 80, the tail dims
-       // [64 + 8 wg, +8): every TMEM access stays aligned to its own width.
-      constexpr int MAIN = 32 * (D / 64);  // dims per warpgroup in the 64-multiple part
-      const bf16* qrow_p = qkv + (static_cast<size_t>(row0) + qrow) * (3 * H * D) + h * D;
-      const uint4* src = reinterpret_cast<const uint4*>(qrow_p + wg * MAIN);
-      uint32_t qv[MAIN / 2];
+    constexpr int MAIN = 32 * (D / 64);  // dims per warpgroup in the 64-multiple part
+    int g0 = 0;
+    int qt, h, b;
+    for (int it = 0; tile_of(it, qt, h, b); ++it) {
+      const int row0 = b * seq, N = nblocks(qt);
+      const int qrow = qt * 128 + r;
+      const size_t bh = (static_cast<size_t>(b) * H + h) * seq;
+      const float nl = -lse[bh + qrow], dl = delta[bh + qrow];
+      {  // this thread's half of its Q row -> TMEM (bf16 pairs: column j holds dims 2j, 2j+1).
+         // Warpgroup wg owns dims [32 (D/64) wg, +32 (D/64)) and, for head_dim 80, the tail dims
+         // [64 + 8 wg, +8): every TMEM access stays aligned to its own width.  Written after the
+         // previous tile's dQ was drained, i.e. after all its MMAs (dq_done).
+        const bf16* qrow_p = qkv + (static_cast<size_t>(row0) + qrow) * (3 * H * D) + h * D;
+        const uint4* src = reinterpret_cast<const uint4*>(qrow_p + wg * MAIN);
+        uint32_t qv[MAIN / 2];
 #pragma unroll
-      for (int u = 0; u < MAIN / 8; ++u) {
-        const uint4 t = src[u];
-        qv[4 * u] = t.x;
-        qv[4 * u + 1] = t.y;
-        qv[4 * u + 2] = t.z;
-        qv[4 * u + 3] = t.w;
-      }
-#pragma unroll
-      for (int u = 0; u < MAIN / 32; ++u) tmem_st_x16(t_q + lanes + wg * (MAIN / 2) + 16 * u, qv + 16 * u);
-      if constexpr (D % 64 == 16) {
-        const uint4 t = *reinterpret_cast<const uint4*>(qrow_p + 2 * MAIN + 8 * wg);
-        const uint32_t tv[4] = {t.x, t.y, t.z, t.w};
-        ptx::tmem_st_32x32b_x4(t_q + lanes + MAIN + 4 * wg, tv);
-      }
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(q_full);
-    }
-    for (int n = 0; n < N; ++n) {
-      const bool diag = causal && n == N - 1;
-      ptx::mbar_wait(s_full, n & 1);
-      if (lane == 0 && q == 0 && wg == 0) BW_T(3, n);
-      ptx::tc_fence_after();
-      uint32_t s[64], d[64];
-      // S first, released as soon as it is in registers so S(n+1) overlaps the dP load
-      ptx::tmem_ld_32x32b_x32(tmem + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      ptx::tmem_ld_32x32b_x32(tmem + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(s_empty);
-      ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
-      ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(d_empty);
-      uint32_t gg[32];
-#pragma unroll
-      for (int cc = 0; cc < 64; cc += 2) {
-#ifdef FA_ABL_NOSOFT  // ablation: no exponentials / softmax math, dS = S + dP
-        float g0 = __uint_as_float(s[cc]) + __uint_as_float(d[cc]);
-        float g1 = __uint_as_float(s[cc + 1]) + __uint_as_float(d[cc + 1]);
-#else
-        float g0 = ex2(fmaf(__uint_as_float(s[cc]), scale_log2, nl)) * (__uint_as_float(d[cc]) - dl);
-        float g1 = ex2(fmaf(__uint_as_float(s[cc + 1]), scale_log2, nl)) * (__uint_as_float(d[cc + 1]) - dl);
-#endif
-        if (diag) {
-          const int k0 = n * 128 + c0 + cc;
-          if (k0 > qrow) g0 = 0.f;
-          if (k0 + 1 > qrow) g1 = 0.f;
+        for (int u = 0; u < MAIN / 8; ++u) {
+          const uint4 t = src[u];
+          qv[4 * u] = t.x;
+          qv[4 * u + 1] = t.y;
+          qv[4 * u + 2] = t.z;
+          qv[4 * u + 3] = t.w;
         }
-        gg[cc >> 1] = pack2(g0, g1);
+#pragma unroll
+        for (int u = 0; u < MAIN / 32; ++u) tmem_st_x16(t_q + lanes + wg * (MAIN / 2) + 16 * u, qv + 16 * u);
+        if constexpr (D % 64 == 16) {
+          const uint4 t = *reinterpret_cast<const uint4*>(qrow_p + 2 * MAIN + 8 * wg);
+          const uint32_t tv[4] = {t.x, t.y, t.z, t.w};
+          ptx::tmem_st_32x32b_x4(t_q + lanes + MAIN + 4 * wg, tv);
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(q_full);
       }
-      if (lane == 0 && q == 0 && wg == 0) BW_T(4, n);
-      ptx::mbar_wait(ds_empty, (n & 1) ^ 1);  // dQ(n-1) has read the previous dS
+      for (int n = 0; n < N; ++n) {
+        const int g = g0 + n;
+        const bool diag = causal && n == N - 1;
+        ptx::mbar_wait(s_full, g & 1);
+        if (it == 0 && lane == 0 && q == 0 && wg == 0) BW_T(3, n);
+        ptx::tc_fence_after();
+        uint32_t s[64], d[64];
+        // S first, released as soon as it is in registers so S(n+1) overlaps the dP load
+        ptx::tmem_ld_32x32b_x32(tmem + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        ptx::tmem_ld_32x32b_x32(tmem + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(s_empty);
+        ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
+        ptx::tmem_ld_32x32b_x32(tmem + 128 + lanes + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(d_empty);
+        uint32_t gg[32];
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 2) {
+          float g0f = ex2(fmaf(__uint_as_float(s[cc]), scale_log2, nl)) * (__uint_as_float(d[cc]) - dl);
+          float g1f = ex2(fmaf(__uint_as_float(s[cc + 1]), scale_log2, nl)) * (__uint_as_float(d[cc + 1]) - dl);
+          if (diag) {
+            const int k0 = n * 128 + c0 + cc;
+            if (k0 > qrow) g0f = 0.f;
+            if (k0 + 1 > qrow) g1f = 0.f;
+          }
+          gg[cc >> 1] = pack2(g0f, g1f);
+        }
+        if (it == 0 && lane == 0 && q == 0 && wg == 0) BW_T(4, n);
+        ptx::mbar_wait(ds_empty, (g & 1) ^ 1);  // dQ(g-1) has read the previous dS
+        ptx::tc_fence_after();
+        tmem_st_x16(t_ds + lanes + 32 * wg, gg);
+        tmem_st_x16(t_ds + lanes + 32 * wg + 16, gg + 16);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(p_full);
+        if (it == 0 && lane == 0 && q == 0 && wg == 0) BW_T(5, n);
+      }
+      ptx::mbar_wait(dq_done, it & 1);
       ptx::tc_fence_after();
-      tmem_st_x16(t_ds + lanes + 32 * wg, gg);
-      tmem_st_x16(t_ds + lanes + 32 * wg + 16, gg + 16);
-      ptx::tmem_st_wait();
+      // each warpgroup writes half of the D columns (head_dim 80: 32 + 8 each, aligned as above)
+      bf16* rowq = dqkv + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(3) * H * D) + h * D;
+      tmem_row_to_global<MAIN>(t_dq + lanes + wg * MAIN, rowq + wg * MAIN, scale);
+      if constexpr (D % 64 == 16)
+        tmem_row_to_global<8>(t_dq + lanes + 2 * MAIN + 8 * wg, rowq + 2 * MAIN + 8 * wg, scale);
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full);
-      if (lane == 0 && q == 0 && wg == 0) BW_T(5, n);
+      g0 += N;
     }
-    ptx::mbar_wait(dq_done, 0);
-    ptx::tc_fence_after();
-    // each warpgroup writes half of the D columns (head_dim 80: 32 + 8 each, aligned as above)
-    constexpr int MAIN = 32 * (D / 64);
-    bf16* rowq = dqkv + (static_cast<size_t>(row0) + qrow) * (static_cast<size_t>(3) * H * D) + h * D;
-    tmem_row_to_global<MAIN>(t_dq + lanes + wg * MAIN, rowq + wg * MAIN, scale);
-    if constexpr (D % 64 == 16) tmem_row_to_global<8>(t_dq + lanes + 2 * MAIN + 8 * wg, rowq + 2 * MAIN + 8 * wg, scale);
   } else {
     ptx::regs_dec<56>();
   }
@@ -635,8 +658,9 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   cudaError_t e = launch_pdl(fa_bwd_dkdv_kernel<D>, dim3(nt * H * B), dim3(384), smem_kv, st, q128, q64, o64, lse,
                              delta, dqkv, S, H, nt, scale_log2, scale, causal);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(fa_bwd_dq_kernel<D>, dim3(nt * H * B), dim3(384), smem_q, st, q128, o128, qkv, lse, delta, dqkv, S, H,
-                 nt, scale_log2, scale, causal);
+  const int dq_grid = std::min(nt * H * B, num_sms());  // persistent
+  e = launch_pdl(fa_bwd_dq_kernel<D>, dim3(dq_grid), dim3(384), smem_q, st, q128, o128, qkv, lse, delta, dqkv, S, H,
+                 nt, H * B, scale_log2, scale, causal);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
