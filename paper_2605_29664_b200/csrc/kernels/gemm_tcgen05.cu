@@ -1,14 +1,15 @@
 // Stage GEMM for the AMDP executor: C = epi(alpha * A * B^T), bf16 in, fp32 accumulate.
 //
 // sm_100a design (no mma.sync / wgmma), two kernels with the same warp roles:
-//   * gemm_bf16_tc_pair: a CTA pair (cta_group::2) per 256x256 tile, 6-stage TMA ring; the
-//     forward and activation-gradient GEMMs (the last partial wave of forward GEMMs is split
-//     along N);  gemm_bf16_tcgen05: one CTA per 128x256 tile, 4-stage ring; the
-//     weight-gradient GEMMs (A and B MN-major), where it sustains more under the power cap;
+//   * gemm_bf16_tc_pair: a CTA pair (cta_group::2) per 256x256 tile, 6-stage TMA ring; every
+//     stage GEMM with M >= 256 (the last partial wave of K-major-B GEMMs is split along N);
+//     gemm_bf16_tcgen05: one CTA per 128x256 tile, 4-stage ring, for M < 256;
 //   * persistent CTAs (grid = co-resident CTAs / pairs), launched with programmatic
 //     dependent launch so the prologue overlaps the previous kernel's tail;
-//   * warp 0: TMA producer; warp 1: tcgen05.mma issue, warp-converged with elect.sync in the
-//     asm and descriptors advanced by offset (no per-MMA single-lane loop); two TMEM
+//   * warp 0: TMA producer, warp 1: tcgen05.mma issue, both warp-converged with elect.sync in
+//     the asm (a single-lane branch made the compiler wrap every UTMALDG / UTCHMMA in a
+//     serialisation loop, which starved the MN-major pair main loop) and descriptors advanced
+//     by offset; two TMEM
 //     accumulators so a tile's epilogue overlaps the next tile's main loop;
 //   * warps 4..7: epilogue, each owning 32 TMEM lanes: tcgen05.ld -> fused op in registers
 //     -> swizzled smem staging -> TMA store (or TMA reduce-add for the fp32 window gradient).
@@ -280,8 +281,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::pdl_trigger();
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---------------- TMA producer
+    {  // ---------------- TMA producer (warp-converged, elect.sync in the asm)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -292,21 +292,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem_a + stage * A_STAGE_BYTES;
           uint8_t* sb = smem_b + stage * B_STAGE_BYTES;
-          ptx::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          ptx::mbar_arrive_expect_tx_w(&full_bar[stage], STAGE_BYTES);
           const int k0 = kb * BK;
           if constexpr (A_MN) {
 #pragma unroll
             for (int i = 0; i < BM / 64; ++i)
-              ptx::tma_load_2d(sa + i * (64 * BK * 2), &map_a, &full_bar[stage], m0 + 64 * i, k0);
+              ptx::tma_load_2d_w(sa + i * (64 * BK * 2), &map_a, &full_bar[stage], m0 + 64 * i, k0);
           } else {
-            ptx::tma_load_2d(sa, &map_a, &full_bar[stage], k0, m0);
+            ptx::tma_load_2d_w(sa, &map_a, &full_bar[stage], k0, m0);
           }
           if constexpr (B_MN) {
 #pragma unroll
             for (int i = 0; i < BN / 64; ++i)
-              ptx::tma_load_2d(sb + i * (64 * BK * 2), &map_b, &full_bar[stage], n0 + 64 * i, k0);
+              ptx::tma_load_2d_w(sb + i * (64 * BK * 2), &map_b, &full_bar[stage], n0 + 64 * i, k0);
           } else {
-            ptx::tma_load_2d(sb, &map_b, &full_bar[stage], k0, n0);
+            ptx::tma_load_2d_w(sb, &map_b, &full_bar[stage], k0, n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -479,7 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   ptx::pdl_trigger();
 
   if (warp == 0) {
-    if (lane == 0) {
+    {  // TMA producer (warp-converged, elect.sync in the asm)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = cluster; w < sc.num_work; w += nclusters) {
@@ -493,21 +493,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[stage], bytes);
+          if (rank == 0) ptx::mbar_arrive_expect_tx_w(&full_bar[stage], bytes);
           uint8_t* sa = smem_a + stage * C::A_BYTES;
           uint8_t* sb = smem_b + stage * C::B_BYTES;
           const int k0 = kb * BK;
           if constexpr (A_MN) {
-            ptx::tma_load_2d_pair(sa, &map_a, fb, ma, k0);
-            ptx::tma_load_2d_pair(sa + 64 * BK * 2, &map_a, fb, ma + 64, k0);
+            ptx::tma_load_2d_pair_w(sa, &map_a, fb, ma, k0);
+            ptx::tma_load_2d_pair_w(sa + 64 * BK * 2, &map_a, fb, ma + 64, k0);
           } else {
-            ptx::tma_load_2d_pair(sa, &map_a, fb, k0, ma);
+            ptx::tma_load_2d_pair_w(sa, &map_a, fb, k0, ma);
           }
           if constexpr (B_MN) {
             for (int i = 0; i < half / 64; ++i)
-              ptx::tma_load_2d_pair(sb + i * 64 * BK * 2, &map_b, fb, nb + 64 * i, k0);
+              ptx::tma_load_2d_pair_w(sb + i * 64 * BK * 2, &map_b, fb, nb + 64 * i, k0);
           } else {
-            ptx::tma_load_2d_pair(sb, mb, fb, k0, nb);
+            ptx::tma_load_2d_pair_w(sb, mb, fb, k0, nb);
           }
           if (++stage == C::NSTAGE) { stage = 0; phase ^= 1; }
         }
@@ -745,13 +745,13 @@ int gemm_pairs() {
 // 1.3B shapes, profiles/r01_gemm_modes.txt: +5-13% over single-CTA 128x256 tiles).
 int choose_mode(int M, int N, bool a_mn, bool b_mn) {
   (void)N;
+  (void)a_mn;
+  (void)b_mn;
   static const int forced = env_int("AMDP_GEMM_MODE", -1);
   if (forced == 0 || forced == 256) return forced;
-  // Weight-gradient GEMMs (A and B both MN-major): single-CTA 128x256 tiles sustain ~4% more
-  // under the power cap than CTA pairs (scripts/gemm_sustained.py, fc1_wgrad 0.88 vs 0.84 of
-  // cuBLAS on the same box) and split the 2048x2048 out-projection into 128 tiles instead of
-  // 64 pairs (+12%).  Everything else: pairs.
-  if (a_mn && b_mn) return 0;
+  // CTA pairs everywhere M allows.  (Weight-gradient GEMMs, A and B MN-major, issue four TMA
+  // boxes per stage and CTA; with a single-lane producer that issue loop starved the pair
+  // kernel, 1081 TF/s sustained vs 1136 on single-CTA tiles; warp-converged issue: 1189.)
   return M >= 256 ? 256 : 0;
 }
 
