@@ -34,22 +34,30 @@ int gemm_t(KTimer* kt, int M, int N, int K, const void* A, int lda, bool amn, co
   if (kt) kt->end(s);
   return rc;
 }
-// dst[c][r] = src[r][c] for a [rows][cols] bf16 matrix; 64x64 tiles through shared memory.
-__global__ void transpose_bf16_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst, int rows,
-                                      int cols) {
-  __shared__ uint16_t tile[64][66];
+// dst[c][r] = src[r][c] for a [rows][cols] bf16 matrix (rows, cols multiples of 8): 64x64
+// tiles through shared memory, 16-byte global loads and stores (8 bf16 per thread per access).
+__global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __restrict__ src,
+                                                             uint16_t* __restrict__ dst, int rows, int cols) {
+  __shared__ uint16_t tile[64][72];  // +8 columns: 16-byte aligned rows, fewer bank conflicts
   const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
-  for (int i = threadIdx.y; i < 64; i += 8)
-    for (int j = threadIdx.x; j < 64; j += 32) {
-      const int r = r0 + i, c = c0 + j;
-      tile[i][j] = (r < rows && c < cols) ? src[static_cast<size_t>(r) * cols + c] : 0;
-    }
+  const int t = threadIdx.x;
+  for (int i = t; i < 64 * 8; i += 256) {  // 64 rows x 8 chunks of 8 columns
+    const int r = i >> 3, c = (i & 7) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r0 + r < rows && c0 + c < cols) v = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(r0 + r) * cols + c0 + c);
+    *reinterpret_cast<uint4*>(&tile[r][c]) = v;
+  }
   __syncthreads();
-  for (int i = threadIdx.y; i < 64; i += 8)
-    for (int j = threadIdx.x; j < 64; j += 32) {
-      const int c = c0 + i, r = r0 + j;
-      if (c < cols && r < rows) dst[static_cast<size_t>(c) * rows + r] = tile[j][i];
-    }
+  for (int i = t; i < 64 * 8; i += 256) {  // 64 output rows (source columns) x 8 chunks of 8 rows
+    const int c = i >> 3, r = (i & 7) * 8;
+    if (c0 + c >= cols || r0 + r >= rows) continue;
+    uint4 o;
+    o.x = tile[r][c] | (static_cast<uint32_t>(tile[r + 1][c]) << 16);
+    o.y = tile[r + 2][c] | (static_cast<uint32_t>(tile[r + 3][c]) << 16);
+    o.z = tile[r + 4][c] | (static_cast<uint32_t>(tile[r + 5][c]) << 16);
+    o.w = tile[r + 6][c] | (static_cast<uint32_t>(tile[r + 7][c]) << 16);
+    *reinterpret_cast<uint4*>(dst + static_cast<size_t>(c0 + c) * rows + r0 + r) = o;
+  }
 }
 }  // namespace
 
@@ -58,7 +66,7 @@ int GptStage::refresh_transposed(cudaStream_t s) const {
   int launched = 0;
   auto tr = [&](const ParamRef& p) {
     dim3 grid((p.cols + 63) / 64, (p.rows + 63) / 64);
-    transpose_bf16_kernel<<<grid, dim3(32, 8), 0, s>>>(w + p.off, wt + p.off, p.rows, p.cols);
+    transpose_bf16_kernel<<<grid, 256, 0, s>>>(w + p.off, wt + p.off, p.rows, p.cols);
     ++launched;
   };
   for (const LayerParams& P : layers_) {
