@@ -76,7 +76,8 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn, int group_m = GROUP_M) {
+  const int GROUP_M = group_m;
   const int in_group = GROUP_M * tiles_n;
   const int g = t / in_group;
   const int first_m = g * GROUP_M;
@@ -408,6 +409,7 @@ struct PairSched {
   int full_tiles;   // tiles before the split tail (raster order)
   int tail_split;   // 1, 2 or 4
   int num_work;     // full_tiles + tail_split * (tiles - full_tiles)
+  int group_m;      // raster: tile rows per group (L2 reuse of B across consecutive tiles)
 };
 
 // Work item w -> output rows [m0, m0 + 256), columns [n0, n0 + width).
@@ -420,7 +422,7 @@ __device__ __forceinline__ void pair_work(const PairSched& s, int w, int& m0, in
     part = u % split;
   }
   int tm, tn;
-  tile_coords(t, s.tiles_m, s.tiles_n, tm, tn);
+  tile_coords(t, s.tiles_m, s.tiles_n, tm, tn, s.group_m);
   width = PBN / split;
   m0 = tm * 256;
   n0 = tn * PBN + part * width;
@@ -642,6 +644,8 @@ PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
   }
   if (forced == 1 || ((forced == 2 || forced == 4) && !b_mn)) best = forced;
   s.tail_split = best;
+  static const int gm = env_int("AMDP_GEMM_GROUP_M", GROUP_M);
+  s.group_m = gm > 0 ? gm : GROUP_M;
   s.full_tiles = best == 1 ? T : T - R;
   s.num_work = s.full_tiles + best * (T - s.full_tiles);
   return s;
