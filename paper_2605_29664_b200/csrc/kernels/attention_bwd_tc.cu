@@ -121,7 +121,7 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap kv_map, const __grid_constant__ CUtensorMap qkv_map,
                        const __grid_constant__ CUtensorMap do_map, const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
-                       int seq, int H, int n_kt, float scale_log2, float scale, int causal) {
+                       int seq, int H, int n_kt, int BH, float scale_log2, float scale, int causal) {
   using L = KvSmem<D>;
   constexpr int NU = L::NU;
   extern __shared__ uint8_t smem_raw[];
@@ -134,23 +134,32 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* u_empty = u_full + 10;   // [NU]
   uint64_t* s_full = u_empty + 10;   // [2] per half
   uint64_t* p_full = s_full + 2;     // [2] 128 arrivals: P^T / dS^T of the half in TMEM
-  uint64_t* kv_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(kv_done + 1);
+  uint64_t* kv_done = p_full + 2;    // the tile's last dK/dV MMA retired
+  uint64_t* kv_empty = kv_done + 1;  // the tile's last S/dP MMA has read K / V
+  uint64_t* acc_empty = kv_empty + 1;  // 256 arrivals: dK / dV drained from TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Heavy first across the whole grid (causal: key tile kt carries n_kt - kt query blocks): the
-  // block scheduler then packs the light tiles into the last wave instead of leaving a few
-  // 32-unit tiles running alone at the end (longest-processing-time-first).
-  const int BH = static_cast<int>(gridDim.x) / n_kt;
-  const int kt = static_cast<int>(blockIdx.x) / BH;
-  const int hb = static_cast<int>(blockIdx.x) % BH;
-  const int h = hb % H, b = hb / H;
-  const int row0 = b * seq;
+  // Persistent: one CTA per SM walks (128-key tile, head, sequence) tiles heavy first (causal:
+  // key tile kt carries n_kt - kt query blocks) in a snake order.  The Q/dO ring and the S/P
+  // hand-offs run on across tiles (global unit counter g = 2 * blocks done + u), so the next
+  // tile's K/V and first Q/dO units load, and its first S/dP MMAs run, while this tile's dK/dV
+  // drain from TMEM.
+  const int ntiles = n_kt * BH;
+  const int G = static_cast<int>(gridDim.x), cta = static_cast<int>(blockIdx.x);
   const int nqb = seq / 128;
-  const int i0 = causal ? kt : 0;
-  const int N = nqb - i0;  // 128-query blocks; 2N half-block units
-  const float* lse_bh = lse + (static_cast<size_t>(b) * H + h) * seq;
-  const float* del_bh = delta + (static_cast<size_t>(b) * H + h) * seq;
+  struct Tile { int kt, h, b, i0, N; };
+  auto tile_of = [&](int it, Tile& t) -> bool {
+    const int idx = it * G + ((it & 1) ? (G - 1 - cta) : cta);
+    if (idx >= ntiles) return false;
+    t.kt = idx / BH;
+    const int hb = idx % BH;
+    t.h = hb % H;
+    t.b = hb / H;
+    t.i0 = causal ? t.kt : 0;
+    t.N = nqb - t.i0;  // 128-query blocks; 2N half-block units
+    return true;
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&kv_map);
@@ -166,6 +175,8 @@ __global__ void __launch_bounds__(384, 1)
       ptx::mbar_init(&p_full[s], 128);
     }
     ptx::mbar_init(kv_done, 1);
+    ptx::mbar_init(kv_empty, 1);
+    ptx::mbar_init(acc_empty, 256);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
@@ -182,23 +193,28 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 0) {
     ptx::regs_dec<56>();
     if (lane == 0) {
-      ptx::mbar_arrive_expect_tx(kv_full, 2 * L::NB * T128);
-      for (int c = 0; c < L::NB; ++c) {
-        ptx::tma_load_2d(sm + L::K + c * T128, &kv_map, kv_full, H * D + h * D + 64 * c, row0 + kt * 128);
-        ptx::tma_load_2d(sm + L::V + c * T128, &kv_map, kv_full, 2 * H * D + h * D + 64 * c, row0 + kt * 128);
-      }
-      for (int u = 0; u < 2 * N; ++u) {
-        const int st = u % NU, q0 = i0 * 128 + u * 64;
-        uint8_t* unit = sm + L::U + st * L::UNIT;
-        ptx::mbar_wait(&u_empty[st], ((u / NU) & 1) ^ 1);
-        BW_T(6, u);
-#ifdef FA_ABL_NOLOAD  // ablation: keep the ring's first fill, skip every later load
-        if (u >= NU) { ptx::mbar_arrive(&u_full[st]); continue; }
-#endif
-        ptx::mbar_arrive_expect_tx(&u_full[st], L::UNIT);
+      Tile t;
+      for (int it = 0, g0 = 0; tile_of(it, t); g0 += 2 * t.N, ++it) {
+        const int row0 = t.b * seq, h = t.h;
+        ptx::mbar_wait(kv_empty, (it & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(kv_full, 2 * L::NB * T128);
         for (int c = 0; c < L::NB; ++c) {
-          ptx::tma_load_2d(unit + c * T64, &qkv_map, &u_full[st], h * D + 64 * c, row0 + q0);
-          ptx::tma_load_2d(unit + (L::NB + c) * T64, &do_map, &u_full[st], h * D + 64 * c, row0 + q0);
+          ptx::tma_load_2d(sm + L::K + c * T128, &kv_map, kv_full, H * D + h * D + 64 * c, row0 + t.kt * 128);
+          ptx::tma_load_2d(sm + L::V + c * T128, &kv_map, kv_full, 2 * H * D + h * D + 64 * c, row0 + t.kt * 128);
+        }
+        for (int u = 0; u < 2 * t.N; ++u) {
+          const int g = g0 + u, st = g % NU, q0 = t.i0 * 128 + u * 64;
+          uint8_t* unit = sm + L::U + st * L::UNIT;
+          ptx::mbar_wait(&u_empty[st], ((g / NU) & 1) ^ 1);
+          BW_T(6, u);
+#ifdef FA_ABL_NOLOAD  // ablation: keep the ring's first fill, skip every later load
+          if (g >= NU) { ptx::mbar_arrive(&u_full[st]); continue; }
+#endif
+          ptx::mbar_arrive_expect_tx(&u_full[st], L::UNIT);
+          for (int c = 0; c < L::NB; ++c) {
+            ptx::tma_load_2d(unit + c * T64, &qkv_map, &u_full[st], h * D + 64 * c, row0 + q0);
+            ptx::tma_load_2d(unit + (L::NB + c) * T64, &do_map, &u_full[st], h * D + 64 * c, row0 + q0);
+          }
         }
       }
     }
@@ -209,14 +225,14 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t id_g = ptx::idesc_bf16_f32(128, D, false, true);
       const uint64_t dk0 = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::K), 16, 1024);
       const uint64_t dv0 = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::V), 16, 1024);
-      auto unit = [&](int u) { return ptx::smem_u32(sm + L::U + (u % NU) * L::UNIT); };
-      // S^T_x, dP^T_x of half-unit u (x = u & 1) into columns 64x / 128 + 64x
-      auto issue_s = [&](int u) {
-        const int x = u & 1;
-        ptx::mbar_wait(&u_full[u % NU], (u / NU) & 1);
-        BW_T(0, u);
+      auto unit = [&](int g) { return ptx::smem_u32(sm + L::U + (g % NU) * L::UNIT); };
+      // S^T_x, dP^T_x of global half-unit g (x = g & 1) into columns 64x / 128 + 64x
+      auto issue_s = [&](int g) {
+        const int x = g & 1;
+        ptx::mbar_wait(&u_full[g % NU], (g / NU) & 1);
+        BW_T(0, g);
         ptx::tc_fence_after();
-        const uint64_t dq = ptx::umma_desc_sw128(unit(u), 16, 1024);
+        const uint64_t dq = ptx::umma_desc_sw128(unit(g), 16, 1024);
         const uint64_t ddo = dq + ((L::NB * T64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -229,110 +245,129 @@ __global__ void __launch_bounds__(384, 1)
           ptx::mma_bf16_ss_w(tmem + 128 + 64 * x, dv0 + oa, ddo + ob, id_s, kk > 0);
         }
         ptx::mma_commit_w(&s_full[x]);
-        BW_T(1, u);
+        BW_T(1, g);
       };
-      // dV += P^T_x dO_x, dK += dS^T_x Q_x (K = 64 queries; P^T / dS^T from TMEM)
-      auto issue_g = [&](int u) {
-        const int x = u & 1;
-        ptx::mbar_wait(&p_full[x], (u >> 1) & 1);
-        BW_T(2, u);
+      // dV += P^T_x dO_x, dK += dS^T_x Q_x (K = 64 queries; P^T / dS^T from TMEM); first = the
+      // tile's first unit (overwrites the accumulators)
+      auto issue_g = [&](int g, bool first) {
+        const int x = g & 1;
+        ptx::mbar_wait(&p_full[x], (g >> 1) & 1);
+        BW_T(2, g);
         ptx::tc_fence_after();
-        const uint64_t dq = ptx::umma_desc_sw128(unit(u), T64, 1024);
+        const uint64_t dq = ptx::umma_desc_sw128(unit(g), T64, 1024);
         const uint64_t ddo = dq + ((L::NB * T64) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          ptx::mma_bf16_ts_w(t_dv, tmem + 64 * x + kk * 8, ddo + ((kk * 2048) >> 4), id_g, (u > 0 || kk > 0));
+          ptx::mma_bf16_ts_w(t_dv, tmem + 64 * x + kk * 8, ddo + ((kk * 2048) >> 4), id_g, (!first || kk > 0));
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          ptx::mma_bf16_ts_w(t_dk, tmem + 128 + 64 * x + kk * 8, dq + ((kk * 2048) >> 4), id_g, (u > 0 || kk > 0));
-        ptx::mma_commit_w(&u_empty[u % NU]);
-        BW_T(3, u);
+          ptx::mma_bf16_ts_w(t_dk, tmem + 128 + 64 * x + kk * 8, dq + ((kk * 2048) >> 4), id_g, (!first || kk > 0));
+        ptx::mma_commit_w(&u_empty[g % NU]);
+        BW_T(3, g);
       };
-      ptx::mbar_wait(kv_full, 0);
-      const int U = 2 * N;
-      issue_s(0);
-      if (U > 1) issue_s(1);
-      for (int u = 0; u < U; ++u) {  // dVdK(u) | S(u + 2): S(u+2) reuses the columns dVdK(u) reads
-        issue_g(u);
-        if (u + 2 < U) issue_s(u + 2);
+      // Per tile: S(0) S(1) | dVdK(u) S(u + 2) ... (S(u+2) reuses the columns dVdK(u) reads).
+      // The next tile's S(0) S(1) are issued before this tile's dK/dV are drained; its first
+      // dVdK waits for the drain (acc_empty).
+      Tile t;
+      for (int it = 0, g0 = 0; tile_of(it, t); g0 += 2 * t.N, ++it) {
+        const int U = 2 * t.N;
+        ptx::mbar_wait(kv_full, it & 1);
+        issue_s(g0);
+        if (U > 1) issue_s(g0 + 1);
+        if (U <= 2) ptx::mma_commit_w(kv_empty);
+        ptx::mbar_wait(acc_empty, (it & 1) ^ 1);
+        for (int u = 0; u < U; ++u) {
+          issue_g(g0 + u, u == 0);
+          if (u + 2 < U) {
+            issue_s(g0 + u + 2);
+            if (u + 3 == U) ptx::mma_commit_w(kv_empty);
+          }
+        }
+        ptx::mma_commit_w(kv_done);
       }
-      ptx::mma_commit_w(kv_done);
     }
   } else if (warp >= 4) {
     ptx::regs_inc<224>();
     const int x = (warp - 4) >> 2;  // half: queries [64 x, 64 x + 64) of every block
     const int q = warp & 3;
     const int r = q * 32 + lane;  // key row within the tile
-    const int key = kt * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t t_s = tmem + lanes + 64 * x, t_d = tmem + 128 + lanes + 64 * x;
     const float2 c2 = make_float2(scale_log2, scale_log2);
-    for (int n = 0; n < N; ++n) {
-      const int u = 2 * n + x;
-      const int qbase = (i0 + n) * 128 + 64 * x;
-      const bool diag = causal && n == 0;
-      float4 lq4[16], dq4[16];  // this half's 64 lse / delta (same address across the warp)
+    Tile t;
+    for (int it = 0, g0 = 0; tile_of(it, t); g0 += 2 * t.N, ++it) {
+      const int key = t.kt * 128 + r;
+      const float* lse_bh = lse + (static_cast<size_t>(t.b) * H + t.h) * seq;
+      const float* del_bh = delta + (static_cast<size_t>(t.b) * H + t.h) * seq;
+      for (int n = 0; n < t.N; ++n) {
+        const int u = g0 + 2 * n + x;
+        const int qbase = (t.i0 + n) * 128 + 64 * x;
+        const bool diag = causal && n == 0;
+        float4 lq4[16], dq4[16];  // this half's 64 lse / delta (same address across the warp)
 #pragma unroll
-      for (int c4 = 0; c4 < 16; ++c4) {
-        lq4[c4] = __ldg(reinterpret_cast<const float4*>(lse_bh + qbase) + c4);
-        dq4[c4] = __ldg(reinterpret_cast<const float4*>(del_bh + qbase) + c4);
-      }
-      ptx::mbar_wait(&s_full[x], n & 1);
-      if (threadIdx.x == 128) BW_T(4, u);
-      ptx::tc_fence_after();
-      uint32_t s[64], d[64];
-      ptx::tmem_ld_32x32b_x32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-      ptx::tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-      ptx::tmem_ld_32x32b_x32(t_d, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
-      ptx::tmem_ld_32x32b_x32(t_d + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
-      ptx::tmem_ld_wait();
-      uint32_t pp[32], dd[32];
-#pragma unroll
-      for (int c4 = 0; c4 < 16; ++c4) {
-        const float4 lq = lq4[c4], dq = dq4[c4];
-        const int cc = 4 * c4;
-        float2 x0 = __ffma2_rn(make_float2(__uint_as_float(s[cc]), __uint_as_float(s[cc + 1])), c2,
-                               make_float2(-lq.x, -lq.y));
-        float2 x1 = __ffma2_rn(make_float2(__uint_as_float(s[cc + 2]), __uint_as_float(s[cc + 3])), c2,
-                               make_float2(-lq.z, -lq.w));
-#ifdef FA_ABL_NOSOFT
-        float2 p0 = x0, p1 = x1;
-#else
-        float2 p0 = make_float2(ex2(x0.x), ex2(x0.y)), p1 = make_float2(ex2(x1.x), ex2(x1.y));
-#endif
-        if (diag) {  // query < key is masked
-          if (qbase + cc < key) p0.x = 0.f;
-          if (qbase + cc + 1 < key) p0.y = 0.f;
-          if (qbase + cc + 2 < key) p1.x = 0.f;
-          if (qbase + cc + 3 < key) p1.y = 0.f;
+        for (int c4 = 0; c4 < 16; ++c4) {
+          lq4[c4] = __ldg(reinterpret_cast<const float4*>(lse_bh + qbase) + c4);
+          dq4[c4] = __ldg(reinterpret_cast<const float4*>(del_bh + qbase) + c4);
         }
-        const float2 g0 = __fmul2_rn(
-            __fadd2_rn(make_float2(__uint_as_float(d[cc]), __uint_as_float(d[cc + 1])), make_float2(-dq.x, -dq.y)), p0);
-        const float2 g1 = __fmul2_rn(
-            __fadd2_rn(make_float2(__uint_as_float(d[cc + 2]), __uint_as_float(d[cc + 3])), make_float2(-dq.z, -dq.w)),
-            p1);
-        pp[2 * c4] = pack2(p0.x, p0.y);
-        pp[2 * c4 + 1] = pack2(p1.x, p1.y);
-        dd[2 * c4] = pack2(g0.x, g0.y);
-        dd[2 * c4 + 1] = pack2(g1.x, g1.y);
+        ptx::mbar_wait(&s_full[x], (u >> 1) & 1);
+        if (threadIdx.x == 128) BW_T(4, u);
+        ptx::tc_fence_after();
+        uint32_t s[64], d[64];
+        ptx::tmem_ld_32x32b_x32(t_s, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        ptx::tmem_ld_32x32b_x32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        ptx::tmem_ld_32x32b_x32(t_d, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
+        ptx::tmem_ld_32x32b_x32(t_d + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
+        ptx::tmem_ld_wait();
+        uint32_t pp[32], dd[32];
+#pragma unroll
+        for (int c4 = 0; c4 < 16; ++c4) {
+          const float4 lq = lq4[c4], dq = dq4[c4];
+          const int cc = 4 * c4;
+          float2 x0 = __ffma2_rn(make_float2(__uint_as_float(s[cc]), __uint_as_float(s[cc + 1])), c2,
+                                 make_float2(-lq.x, -lq.y));
+          float2 x1 = __ffma2_rn(make_float2(__uint_as_float(s[cc + 2]), __uint_as_float(s[cc + 3])), c2,
+                                 make_float2(-lq.z, -lq.w));
+#ifdef FA_ABL_NOSOFT
+          float2 p0 = x0, p1 = x1;
+#else
+          float2 p0 = make_float2(ex2(x0.x), ex2(x0.y)), p1 = make_float2(ex2(x1.x), ex2(x1.y));
+#endif
+          if (diag) {  // query < key is masked
+            if (qbase + cc < key) p0.x = 0.f;
+            if (qbase + cc + 1 < key) p0.y = 0.f;
+            if (qbase + cc + 2 < key) p1.x = 0.f;
+            if (qbase + cc + 3 < key) p1.y = 0.f;
+          }
+          const float2 g0 = __fmul2_rn(
+              __fadd2_rn(make_float2(__uint_as_float(d[cc]), __uint_as_float(d[cc + 1])), make_float2(-dq.x, -dq.y)), p0);
+          const float2 g1 = __fmul2_rn(
+              __fadd2_rn(make_float2(__uint_as_float(d[cc + 2]), __uint_as_float(d[cc + 3])), make_float2(-dq.z, -dq.w)),
+              p1);
+          pp[2 * c4] = pack2(p0.x, p0.y);
+          pp[2 * c4 + 1] = pack2(p1.x, p1.y);
+          dd[2 * c4] = pack2(g0.x, g0.y);
+          dd[2 * c4 + 1] = pack2(g1.x, g1.y);
+        }
+        if (threadIdx.x == 128) BW_T(5, u);
+        // P^T_x / dS^T_x (bf16 pairs) over the first 32 columns of this half's S^T / dP^T
+        tmem_st_x16(t_s, pp);
+        tmem_st_x16(t_s + 16, pp + 16);
+        tmem_st_x16(t_d, dd);
+        tmem_st_x16(t_d + 16, dd + 16);
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[x]);
+        if (threadIdx.x == 128) BW_T(7, u);
       }
-      if (threadIdx.x == 128) BW_T(5, u);
-      // P^T_x / dS^T_x (bf16 pairs) over the first 32 columns of this half's S^T / dP^T
-      tmem_st_x16(t_s, pp);
-      tmem_st_x16(t_s + 16, pp + 16);
-      tmem_st_x16(t_d, dd);
-      tmem_st_x16(t_d + 16, dd + 16);
-      ptx::tmem_st_wait();
+      ptx::mbar_wait(kv_done, it & 1);
+      ptx::tc_fence_after();
+      // warpgroup 0 writes dK, warpgroup 1 writes dV
+      const size_t ld = static_cast<size_t>(3) * H * D;
+      bf16* dst = dqkv + (static_cast<size_t>(t.b) * seq + key) * ld + (x == 0 ? H * D : 2 * H * D) + t.h * D;
+      tmem_row_to_global<D>((x == 0 ? t_dk : t_dv) + lanes, dst, x == 0 ? scale : 1.f);
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&p_full[x]);
-      if (threadIdx.x == 128) BW_T(7, u);
+      ptx::mbar_arrive(acc_empty);
     }
-    ptx::mbar_wait(kv_done, 0);
-    ptx::tc_fence_after();
-    // warpgroup 0 writes dK, warpgroup 1 writes dV
-    const size_t ld = static_cast<size_t>(3) * H * D;
-    bf16* dst = dqkv + (static_cast<size_t>(row0) + key) * ld + (x == 0 ? H * D : 2 * H * D) + h * D;
-    tmem_row_to_global<D>((x == 0 ? t_dk : t_dv) + lanes, dst, x == 0 ? scale : 1.f);
   } else {
     ptx::regs_dec<56>();
   }
@@ -655,8 +690,9 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
     attr = true;
   }
   const int nt = S / 128;
-  cudaError_t e = launch_pdl(fa_bwd_dkdv_kernel<D>, dim3(nt * H * B), dim3(384), smem_kv, st, q128, q64, o64, lse,
-                             delta, dqkv, S, H, nt, scale_log2, scale, causal);
+  const int kv_grid = std::min(nt * H * B, num_sms());  // persistent
+  cudaError_t e = launch_pdl(fa_bwd_dkdv_kernel<D>, dim3(kv_grid), dim3(384), smem_kv, st, q128, q64, o64, lse,
+                             delta, dqkv, S, H, nt, H * B, scale_log2, scale, causal);
   if (e != cudaSuccess) return e;
   const int dq_grid = std::min(nt * H * B, num_sms());  // persistent
   e = launch_pdl(fa_bwd_dq_kernel<D>, dim3(dq_grid), dim3(384), smem_q, st, q128, o128, qkv, lse, delta, dqkv, S, H,
