@@ -337,13 +337,25 @@ def parse_timeline_csv(text: str):
 
 
 def replay(trace_csv: str, m: Model, partition: List[int], opt: Opt, threshold: int,
-           inputs: np.ndarray, labels: np.ndarray, emulate_bf16: bool = True):
+           inputs: np.ndarray, labels: np.ndarray, emulate_bf16: bool = True,
+           update_div: Optional[int] = None):
     """Executes the reference trace on the CPU.  Returns (losses[M], params per stage (fp32
-    master dicts), version trace rows {(kind, stage, minibatch): version})."""
+    master dicts), version trace rows {(kind, stage, minibatch): version}).
+
+    Window events (builder.hpp:260-338): Broadcast(w, i) (ZeRO) rewrites every replica of
+    stage i; Update(w, i, p) advances replica p only (analysis.hpp:47-52: a Forward / Backward
+    of pipeline p counts the Broadcasts of its stage and the Updates of its own pipeline).
+    Replicas apply the same all-reduced gradient, so the first Update of (stage, window) takes
+    the optimizer step and the others switch to its result.  The optimizer step number is the
+    event's minibatch field + 1 (window w, or minibatch j for PipeDreamAsync's per-backward
+    Update); the gradient is divided by `update_div` (default: the threshold; 1 for
+    PipeDreamAsync)."""
     ev = parse_timeline_csv(trace_csv)
     # zero-duration window events complete at their start: apply before compute starting then
     ev.sort(key=lambda e: (e["start"], e["dur"] > 0, e["device"], e["row"]))
+    div = threshold if update_div is None else update_div
     depth = len(partition)
+    npipe = 1 + max(e["pipeline"] for e in ev)
     bounds = np.concatenate([[0], np.cumsum(partition)]).astype(int)
     specs = [stage_param_specs(m, i, depth, bounds[i], bounds[i + 1]) for i in range(depth)]
     master = [{k: v.astype(np.float64) for k, v in init_stage(m, s).items()} for s in specs]
@@ -352,35 +364,43 @@ def replay(trace_csv: str, m: Model, partition: List[int], opt: Opt, threshold: 
     grads = [{k: np.zeros_like(v) for k, v in st.items()} for st in master]
     math_ = [StageMath(m, i, depth, bounds[i], bounds[i + 1], emulate_bf16) for i in range(depth)]
     rb = (lambda x: bf16(x).astype(np.float64)) if emulate_bf16 else (lambda x: x)
-    work = [{k: rb(v) if v.ndim == 2 else v.copy() for k, v in st.items()} for st in master]
-    version = [0] * depth
+
+    def working(st):  # the bf16 working copy the kernels read
+        return {k: rb(v.astype(np.float32)) if v.ndim == 2 else v.astype(np.float32).astype(np.float64)
+                for k, v in st.items()}
+
+    works = [[working(st)] for st in master]  # works[i][k]: stage i after k optimizer steps
+    ver = {(i, p): 0 for i in range(depth) for p in range(npipe)}  # replica -> steps it reads
+    stepped = set()
     acts, caches, gsend = {}, {}, {}
     M = inputs.shape[0]
     losses = np.zeros(M)
     seen = {}
     for e in ev:
-        i, j = e["stage"], e["minibatch"]
+        i, j, p = e["stage"], e["minibatch"], e["pipeline"]
         if e["kind"] == "Forward":
-            seen[("Forward", i, j)] = version[i]
-            out, cache, loss = math_[i].forward(work[i], acts.get((i, j)), inputs[j], labels[j])
+            seen[("Forward", i, j)] = ver[(i, p)]
+            out, cache, loss = math_[i].forward(works[i][ver[(i, p)]], acts.get((i, j)), inputs[j], labels[j])
             caches[(i, j)] = cache
             if out is not None:
                 acts[(i + 1, j)] = out
             if loss is not None:
                 losses[j] = loss
         elif e["kind"] == "Backward":
-            seen[("Backward", i, j)] = version[i]
-            g = math_[i].backward(work[i], caches.pop((i, j)), gsend.pop((i, j), None), inputs[j], grads[i])
+            seen[("Backward", i, j)] = ver[(i, p)]
+            g = math_[i].backward(works[i][ver[(i, p)]], caches.pop((i, j)), gsend.pop((i, j), None),
+                                  inputs[j], grads[i])
             if g is not None:
                 gsend[(i - 1, j)] = g
-        elif e["kind"] in ("Broadcast", "Update"):  # ZeRO owner step / single-replica Update (P = 1)
-            step = e["window"] + 1
-            for k in master[i]:
-                apply_update(opt, master[i][k], mom[i][k], vel[i][k], grads[i][k] / threshold, step)
-                grads[i][k][...] = 0
-                work[i][k] = rb(master[i][k].astype(np.float32)) if master[i][k].ndim == 2 else \
-                    master[i][k].astype(np.float32).astype(np.float64)
-            version[i] += 1
+        elif e["kind"] in ("Broadcast", "Update"):
+            if (i, j) not in stepped:  # first window event of (stage, window / minibatch)
+                stepped.add((i, j))
+                for k in master[i]:
+                    apply_update(opt, master[i][k], mom[i][k], vel[i][k], grads[i][k] / div, j + 1)
+                    grads[i][k][...] = 0
+                works[i].append(working(master[i]))
+            for q in (range(npipe) if e["kind"] == "Broadcast" else (p,)):
+                ver[(i, q)] = len(works[i]) - 1
     return losses, master, seen
 
 

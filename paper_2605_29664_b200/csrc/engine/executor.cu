@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -43,7 +44,9 @@ namespace {
 __global__ void record_version_kernel(const int* ver, int stage, int* trace, int idx) {
   trace[idx] = ver[stage];
 }
-__global__ void bump_version_kernel(int* ver, int stage) { ver[stage] += 1; }
+__global__ void bump_version_kernel(int* ver, int first, int count) {
+  for (int k = 0; k < count; ++k) ver[first + k] += 1;
+}
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -121,10 +124,11 @@ struct TaskPlan {
   int gout_buf = -1;        // B: outgoing gradient buffer (stages > 0)
   int send_to = -1;         // rank to send out/gout to after this task (-1: none)
   bool local = false;       // executed by this rank
+  bool first_update = false;  // Update: the first of its (stage, window) -> the optimizer step
 };
 
 struct CommOp {           // executed on the comm stream at a position in the global order
-  enum Kind { Send, Recv, Reduce, Bcast } kind;
+  enum Kind { Send, Recv, Reduce, Bcast, Allreduce } kind;
   int peer = -1;          // send/recv peer rank
   int buf = -1;           // boundary buffer (send/recv)
   int stage = -1;         // reduce/bcast stage
@@ -165,7 +169,24 @@ class Engine {
  private:
   amdp_model_config mc_;
   amdp_run_config rc_;
-  int depth_ = 0, world_ = 1, rank_ = 0, per_rank_ = 1, M_ = 0, thr_ = 1, W_ = 1;
+  int depth_ = 0, devices_ = 0, world_ = 1, rank_ = 0, per_rank_ = 1, M_ = 0, thr_ = 1, W_ = 1;
+  ppsim::Policy policy_ = ppsim::Policy::AMDP;
+  bool zero_ = true;  // ZeRO Reduce/Broadcast (AMDP) vs Update tasks (every other schedule)
+  int P_ = 1;         // pipelines: version counters are per (stage, pipeline replica)
+  // Update-task schedules with several pipelines (AMDP without ZeRO, Chimera): replica p of
+  // stage i advances at its own Update(w, i, p) (builder.hpp:306-336), but every replica's k-th
+  // update applies the same all-reduced window gradient, so the k-th weights are identical
+  // across replicas.  One optimizer state per rank; the first Update(w, i, .) in the global
+  // order takes the step into the other of two bf16 weight buffers, and each replica switches
+  // buffers at its own Update.  (At most two versions are live: no replica's Update(w + 1)
+  // can precede another's Update(w).)
+  bool versioned_ = false;
+  std::vector<std::array<uint16_t*, 2>> wbuf_, wtbuf_;  // per stage
+  std::vector<int> cur_buf_;                             // per stage: newest weights
+  std::vector<std::vector<int>> rep_buf_;                // per stage, pipeline
+  float update_div_ = 1.f;                               // minibatches per optimizer step
+  void use_replica_weights(int stage, int pipeline);
+  void optimizer_step(int stage, int step);
   std::vector<TaskPlan> plan_;               // per order position
   std::vector<std::vector<CommOp>> comm_at_; // per order position
   std::vector<std::vector<uint8_t*>> slot_mem_;
@@ -202,25 +223,37 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   depth_ = rc.depth > 0 ? rc.depth : rc.policy.num_pipelines * 2;
   world_ = std::max(1, rc.world_size);
   rank_ = rc.rank;
-  const auto pol = static_cast<ppsim::Policy>(rc.policy.policy);
-  if (pol == ppsim::Policy::AMDP) {
-    if (!rc.policy.zero_enabled)
-      throw std::invalid_argument("engine: AMDP execution needs zero_enabled (sharded Reduce/Broadcast); "
-                                  "replicated updates would need one weight copy per pipeline replica");
-    if (depth_ != 2 * rc.policy.num_pipelines)
-      throw std::invalid_argument("engine: AMDP runs depth = 2 x num_pipelines stages");
-  } else if (pol == ppsim::Policy::DAPPLE || pol == ppsim::Policy::GPipe) {
-    // one pipeline, one replica per stage: the window's Update(w, i, 0) is the optimizer step
-    if (rc.policy.num_pipelines != 1 || rc.policy.zero_enabled)
-      throw std::invalid_argument("engine: DAPPLE / GPipe execute with one pipeline and zero_enabled off");
-  } else {
-    throw std::invalid_argument("engine: executes AMDP, DAPPLE and GPipe schedules");
+  policy_ = static_cast<ppsim::Policy>(rc.policy.policy);
+  zero_ = rc.policy.zero_enabled != 0;
+  // logical devices: Interleaved1F1B places two stage chunks per device (validate.hpp:96-98)
+  devices_ = policy_ == ppsim::Policy::Interleaved1F1B ? depth_ / 2 : depth_;
+  switch (policy_) {
+    case ppsim::Policy::AMDP:
+      if (depth_ != 2 * rc.policy.num_pipelines)
+        throw std::invalid_argument("engine: AMDP runs depth = 2 x num_pipelines stages");
+      P_ = rc.policy.num_pipelines;
+      break;
+    case ppsim::Policy::Chimera:
+      P_ = 2;
+      break;
+    case ppsim::Policy::DAPPLE:
+    case ppsim::Policy::GPipe:
+    case ppsim::Policy::Interleaved1F1B:
+    case ppsim::Policy::PipeDreamAsync:
+      P_ = 1;
+      break;
+    default:
+      throw std::invalid_argument("engine: unknown policy");
   }
-  if (depth_ % world_ != 0) throw std::invalid_argument("engine: depth must be a multiple of world_size");
-  per_rank_ = depth_ / world_;
+  versioned_ = !zero_ && P_ > 1;
+  if (devices_ < 1 || devices_ % world_ != 0)
+    throw std::invalid_argument("engine: logical devices must be a multiple of world_size");
+  per_rank_ = devices_ / world_;
   M_ = rc.policy.num_minibatches;
   thr_ = rc.policy.accumulation_threshold;
   if (M_ % thr_ != 0) throw std::invalid_argument("engine: num_minibatches must be a multiple of accumulation_threshold");
+  // PipeDreamAsync updates after every backward (builder.hpp:260-270): one minibatch per step
+  update_div_ = policy_ == ppsim::Policy::PipeDreamAsync ? 1.f : static_cast<float>(thr_);
   W_ = M_ / thr_;
 
   dm.L = mc.layers;
@@ -237,7 +270,7 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   if (dm.h % dm.heads != 0) throw std::invalid_argument("engine: hidden must divide into heads");
 
   // schedule: build + order on the declared cost model
-  ppsim::ClusterSpec cl = ppsim::ClusterSpec::uniform(depth_, depth_, from_c(rc.declared_fwd),
+  ppsim::ClusterSpec cl = ppsim::ClusterSpec::uniform(depth_, devices_, from_c(rc.declared_fwd),
                                                       from_c(rc.declared_bwd));
   ppsim::PolicyConfig pc = policy_from_c(&rc.policy);
   sched.cl = cl;
@@ -267,7 +300,9 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   owned.assign(static_cast<size_t>(depth_), false);
   group_ranks_.assign(static_cast<size_t>(depth_), {});
   // replica group of stage i: the ranks whose devices run a Forward / Backward of stage i
-  // (AMDP: map_stage_to_device over the d/2 pipelines, builder.hpp:81-88; DAPPLE/GPipe: device i)
+  // (AMDP: map_stage_to_device over the d/2 pipelines, builder.hpp:81-88; Chimera: i and d-1-i;
+  // Interleaved1F1B: i mod devices; the others: device i).  ZeRO: the owner (device i) keeps the
+  // optimizer state; otherwise every hosting rank does (replicated update).
   for (const auto& t : sched.g.tasks) {
     if (t.kind != ppsim::Kind::Forward && t.kind != ppsim::Kind::Backward) continue;
     auto& gr = group_ranks_[static_cast<size_t>(t.stage)];
@@ -278,7 +313,7 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     std::sort(group_ranks_[static_cast<size_t>(i)].begin(), group_ranks_[static_cast<size_t>(i)].end());
     hosted[static_cast<size_t>(i)] = std::count(group_ranks_[static_cast<size_t>(i)].begin(),
                                                 group_ranks_[static_cast<size_t>(i)].end(), rank_) > 0;
-    owned[static_cast<size_t>(i)] = owner_rank(i) == rank_;
+    owned[static_cast<size_t>(i)] = zero_ ? owner_rank(i) == rank_ : hosted[static_cast<size_t>(i)];
   }
 
   if (rc.plan_only) {  // host-side planning only (multi-rank consistency tests on CPU)
@@ -327,6 +362,11 @@ Engine::~Engine() {
     cudaFree(s->w);
     cudaFree(s->wt);
   }
+  for (size_t i = 0; i < wbuf_.size(); ++i)  // the replica buffer the stage does not point at
+    for (int b = 0; b < 2; ++b) {
+      if (wbuf_[i][static_cast<size_t>(b)] != stages[i]->w) cudaFree(wbuf_[i][static_cast<size_t>(b)]);
+      if (wtbuf_[i][static_cast<size_t>(b)] != stages[i]->wt) cudaFree(wtbuf_[i][static_cast<size_t>(b)]);
+    }
   for (auto& v : slot_mem_)
     for (auto* p : v) cudaFree(p);
   for (auto& b : bufs_) {
@@ -392,6 +432,7 @@ void Engine::make_plan() {
   //   on the producer rank (if different) a send buffer lives [pos F(i,j), pos F(i,j)].
   // B boundary (i+1 -> i, j): [pos B(i+1,j), pos B(i,j)] likewise.
   std::map<std::pair<int, int>, int> fbuf_recv, bbuf_recv;  // key (boundary stage i, j)
+  std::map<std::pair<int, int>, int> updates_seen;          // key (stage, Update's window / mb)
   for (int k = 0; k < N; ++k) {
     const int t = order[static_cast<size_t>(k)];
     const auto& task = g.tasks[static_cast<size_t>(t)];
@@ -475,6 +516,15 @@ void Engine::make_plan() {
       const int i = task.stage;
       if (hosted[static_cast<size_t>(i)] && group_ranks_[static_cast<size_t>(i)].size() > 1)
         comm_at_[static_cast<size_t>(k)].push_back({CommOp::Bcast, -1, -1, i, k});
+    } else if (task.kind == ppsim::Kind::Update) {
+      // Update(w, i, p) (minibatch field = w; PipeDreamAsync: = j).  The first one in the global
+      // order steps the optimizer on every rank hosting stage i, after an all-reduce of the
+      // window gradient over the replica group (the reference's "all-reduce-equivalent
+      // barrier", builder.hpp:306-308): all of the window's backwards precede it.
+      const int i = task.stage;
+      tp.first_update = updates_seen[{i, task.minibatch}]++ == 0;
+      if (tp.first_update && hosted[static_cast<size_t>(i)] && group_ranks_[static_cast<size_t>(i)].size() > 1)
+        comm_at_[static_cast<size_t>(k)].push_back({CommOp::Allreduce, -1, -1, i, k});
     }
     for (int b : release_at[static_cast<size_t>(k)]) free_bufs.push_back(b);
   }
@@ -482,6 +532,10 @@ void Engine::make_plan() {
 
 void Engine::allocate() {
   const size_t T = static_cast<size_t>(dm.T), h = static_cast<size_t>(dm.h);
+  wbuf_.assign(static_cast<size_t>(depth_), {nullptr, nullptr});
+  wtbuf_.assign(static_cast<size_t>(depth_), {nullptr, nullptr});
+  cur_buf_.assign(static_cast<size_t>(depth_), 0);
+  rep_buf_.assign(static_cast<size_t>(depth_), std::vector<int>(static_cast<size_t>(P_), 0));
   for (int i = 0; i < depth_; ++i) {
     if (!hosted[static_cast<size_t>(i)]) continue;
     GptStage& st = *stages[static_cast<size_t>(i)];
@@ -491,6 +545,14 @@ void Engine::allocate() {
     CUDA_OK(cudaMalloc(&st.w, n * sizeof(uint16_t)));
     CUDA_OK(cudaMalloc(&st.wt, n * sizeof(uint16_t)));
     CUDA_OK(cudaMemsetAsync(st.grad, 0, n * sizeof(float), cs_));
+    if (versioned_) {
+      auto& wb = wbuf_[static_cast<size_t>(i)];
+      auto& wtb = wtbuf_[static_cast<size_t>(i)];
+      wb[0] = st.w;
+      wtb[0] = st.wt;
+      CUDA_OK(cudaMalloc(&wb[1], n * sizeof(uint16_t)));
+      CUDA_OK(cudaMalloc(&wtb[1], n * sizeof(uint16_t)));
+    }
     if (owned[static_cast<size_t>(i)]) {
       CUDA_OK(cudaMalloc(&st.m, n * sizeof(float)));
       CUDA_OK(cudaMalloc(&st.v, n * sizeof(float)));
@@ -519,7 +581,7 @@ void Engine::allocate() {
   CUDA_OK(cudaMalloc(&d_inputs_, static_cast<size_t>(M_) * T * sizeof(int32_t)));
   CUDA_OK(cudaMalloc(&d_labels_, static_cast<size_t>(M_) * T * sizeof(int32_t)));
   CUDA_OK(cudaMalloc(&d_loss_, static_cast<size_t>(M_) * sizeof(float)));
-  CUDA_OK(cudaMalloc(&d_ver_, static_cast<size_t>(depth_) * sizeof(int)));
+  CUDA_OK(cudaMalloc(&d_ver_, static_cast<size_t>(depth_ * P_) * sizeof(int)));
   CUDA_OK(cudaMalloc(&d_trace_, sched.g.tasks.size() * sizeof(int)));
   stage_ready_.resize(static_cast<size_t>(depth_));
   for (auto& e : stage_ready_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -595,7 +657,8 @@ void Engine::exec_comm(int pos) {
         break;
       }
       case CommOp::Bcast:
-        break;  // issued from exec_task (needs the owner's optimizer step first)
+      case CommOp::Allreduce:
+        break;  // issued from exec_task (ordered with the optimizer step)
     }
   }
 }
@@ -636,7 +699,8 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     wait_buf(tp.out_buf);
     wait_buf(tp.gout_buf);
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
-    record_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i, d_trace_, t);
+    record_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, d_trace_, t);
+    use_replica_weights(i, task.pipeline);
     stats.kernels_launched += 1;
     const int32_t* tok = d_inputs_ + static_cast<size_t>(j) * T;
     const int32_t* lab = d_labels_ + static_cast<size_t>(j) * T;
@@ -688,19 +752,28 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     stats.tasks_executed += 1;
     return;
   }
-  if (task.kind == ppsim::Kind::Update) {  // single-replica window update (DAPPLE / GPipe)
+  if (task.kind == ppsim::Kind::Update) {  // replicated update (every schedule but ZeRO AMDP)
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
-    amdp_opt_args o = rc_.optimizer;
-    o.step = task.window + 1;
-    o.grad_scale = rc_.optimizer.grad_scale * (1.0f / static_cast<float>(thr_));
-    ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), cs_);
-    rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), st);
-    ktimer_.end(cs_);
-    if (rc != 0) throw std::runtime_error("optimizer step failed");
-    const int nt = S.refresh_transposed(cs_);
-    if (nt < 0) throw std::runtime_error("weight transpose failed");
-    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i);
-    stats.kernels_launched += 2 + nt;
+    if (tp.first_update) {
+      if (group_ranks_[static_cast<size_t>(i)].size() > 1) {  // sum the replicas' window gradients
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_OK(cudaEventRecord(e, cs_));
+        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
+        NCCL_OK(ncclAllReduce(S.grad, S.grad, static_cast<size_t>(S.numel()), ncclFloat32, ncclSum,
+                              group_comm_[static_cast<size_t>(i)], ms_));
+        stats.collective_bytes += 2 * S.numel() * 4;
+        CUDA_OK(cudaEventRecord(e, ms_));
+        CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
+        cudaEventDestroy(e);
+      }
+      optimizer_step(i, task.minibatch + 1);  // Update's minibatch field: window (PipeDream: j)
+    }
+    if (rank_of_dev(task.device) == rank_) {  // this replica now reads the newest weights
+      if (versioned_) rep_buf_[static_cast<size_t>(i)][static_cast<size_t>(task.pipeline)] = cur_buf_[static_cast<size_t>(i)];
+      bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, 1);
+      stats.kernels_launched += 1;
+    }
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
     stats.tasks_executed += 1;
     return;
@@ -709,17 +782,7 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
     const bool multi = group_ranks_[static_cast<size_t>(i)].size() > 1;
     if (owned[static_cast<size_t>(i)]) {
-      amdp_opt_args o = rc_.optimizer;
-      o.step = task.window + 1;
-      o.grad_scale = rc_.optimizer.grad_scale * (1.0f / static_cast<float>(thr_));
-      ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), cs_);
-      rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), st);
-      ktimer_.end(cs_);
-      if (rc != 0) throw std::runtime_error("optimizer step failed");
-      stats.kernels_launched += 1;
-      const int nt = S.refresh_transposed(cs_);
-      if (nt < 0) throw std::runtime_error("weight transpose failed");
-      stats.kernels_launched += nt;
+      optimizer_step(i, task.minibatch + 1);  // Broadcast's minibatch field: the window
     } else {
       // the reduce on the comm stream read this replica's gradient: wait, then clear it
       cudaEvent_t e;
@@ -752,7 +815,7 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
         stats.kernels_launched += nt;
       }
     }
-    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i);
+    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_, P_);  // every replica of stage i
     stats.kernels_launched += 1;
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
     stats.tasks_executed += 1;
@@ -791,7 +854,7 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
       CUDA_OK(cudaEventCreate(&ev_end_[static_cast<size_t>(k)]));
     }
   }
-  CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_) * sizeof(int), cs_));
+  CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_ * P_) * sizeof(int), cs_));
   CUDA_OK(cudaMemsetAsync(d_loss_, 0, static_cast<size_t>(M_) * sizeof(float), cs_));
   CUDA_OK(cudaMemsetAsync(d_trace_, 0xff, g.tasks.size() * sizeof(int), cs_));
   std::vector<int> loaded(static_cast<size_t>(W_), resident ? 1 : 0), last_left(static_cast<size_t>(W_), 0);
@@ -888,7 +951,7 @@ std::string Engine::plan_json() const {
   bool first = true;
   for (size_t k = 0; k < comm_at_.size(); ++k)
     for (const CommOp& op : comm_at_[k]) {
-      static const char* names[] = {"send", "recv", "reduce", "bcast"};
+      static const char* names[] = {"send", "recv", "reduce", "bcast", "allreduce"};
       s += std::string(first ? "[" : ",[") + std::to_string(k) + ",\"" + names[op.kind] + "\"," +
            std::to_string(op.peer) + "," + std::to_string(op.stage) + "]";
       first = false;
@@ -898,14 +961,14 @@ std::string Engine::plan_json() const {
 
 std::string Engine::version_csv() const {
   std::string s = "device,kind,stage,minibatch,pipeline,window,preloaded,version\n";
-  std::vector<std::vector<int>> per_dev(static_cast<size_t>(depth_));
+  std::vector<std::vector<int>> per_dev(static_cast<size_t>(devices_));
   for (size_t k = 0; k < sched.order.size(); ++k) {
     const int t = sched.order[k];
     const auto& task = sched.g.tasks[static_cast<size_t>(t)];
     if ((task.kind == ppsim::Kind::Forward || task.kind == ppsim::Kind::Backward) && plan_[k].local)
       per_dev[static_cast<size_t>(task.device)].push_back(t);
   }
-  for (int d = 0; d < depth_; ++d)
+  for (int d = 0; d < devices_; ++d)
     for (int t : per_dev[static_cast<size_t>(d)]) {
       const auto& e = sched.g.tasks[static_cast<size_t>(t)];
       s += std::to_string(d) + ',' + ppsim::kind_name(e.kind) + ',' + std::to_string(e.stage) + ',' +
@@ -918,6 +981,37 @@ std::string Engine::version_csv() const {
 
 int64_t Engine::stage_numel(int stage) const { return stages.at(static_cast<size_t>(stage))->numel(); }
 
+void Engine::use_replica_weights(int stage, int pipeline) {
+  if (!versioned_) return;
+  GptStage& S = *stages[static_cast<size_t>(stage)];
+  const int b = rep_buf_[static_cast<size_t>(stage)][static_cast<size_t>(pipeline)];
+  S.w = wbuf_[static_cast<size_t>(stage)][static_cast<size_t>(b)];
+  S.wt = wtbuf_[static_cast<size_t>(stage)][static_cast<size_t>(b)];
+}
+
+// The optimizer step of stage i (detail::apply_update H/optim.hpp:234-268 / AdamW) on this
+// rank's state: g / update_div -> master, m, v; bf16 working copy + transposed copy rewritten
+// (versioned: into the buffer no replica reads yet); the gradient is zeroed.
+void Engine::optimizer_step(int stage, int step) {
+  GptStage& S = *stages[static_cast<size_t>(stage)];
+  if (versioned_) {
+    int& cur = cur_buf_[static_cast<size_t>(stage)];
+    cur ^= 1;
+    S.w = wbuf_[static_cast<size_t>(stage)][static_cast<size_t>(cur)];
+    S.wt = wtbuf_[static_cast<size_t>(stage)][static_cast<size_t>(cur)];
+  }
+  amdp_opt_args o = rc_.optimizer;
+  o.step = step;
+  o.grad_scale = rc_.optimizer.grad_scale * (1.0f / update_div_);
+  ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), cs_);
+  const int rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), reinterpret_cast<amdp_stream_t>(cs_));
+  ktimer_.end(cs_);
+  if (rc != 0) throw std::runtime_error("optimizer step failed");
+  const int nt = S.refresh_transposed(cs_);
+  if (nt < 0) throw std::runtime_error("weight transpose failed");
+  stats.kernels_launched += 1 + nt;
+}
+
 void Engine::copy_params(int stage, float* host, int64_t n, bool to_host) {
   GptStage& st = *stages.at(static_cast<size_t>(stage));
   if (!hosted[static_cast<size_t>(stage)]) throw std::invalid_argument("stage not hosted on this rank");
@@ -926,6 +1020,10 @@ void Engine::copy_params(int stage, float* host, int64_t n, bool to_host) {
   if (to_host) {
     CUDA_OK(cudaMemcpy(host, st.master, static_cast<size_t>(n) * sizeof(float), cudaMemcpyDeviceToHost));
   } else {
+    if (versioned_) {  // every replica reads the newly written weights
+      for (int& b : rep_buf_[static_cast<size_t>(stage)]) b = cur_buf_[static_cast<size_t>(stage)];
+      use_replica_weights(stage, 0);
+    }
     CUDA_OK(cudaMemcpy(st.master, host, static_cast<size_t>(n) * sizeof(float), cudaMemcpyHostToDevice));
     cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
         st.master, reinterpret_cast<bf16*>(st.w), n);
@@ -1140,8 +1238,6 @@ namespace ppsim {
 
 ExecuteResult execute(const PolicyConfig& cfg, const ClusterSpec& declared, const ExecuteOptions& opt,
                       const int32_t* inputs, const int32_t* labels) {
-  if (cfg.policy != Policy::AMDP && cfg.policy != Policy::DAPPLE && cfg.policy != Policy::GPipe)
-    throw std::invalid_argument("execute: AMDP, DAPPLE and GPipe schedules run on GPUs");
   if (declared.fwd_cost.empty() || declared.bwd_cost.empty())
     throw std::invalid_argument("execute: declared cluster needs per-stage costs");
   for (std::size_t i = 1; i < declared.fwd_cost.size(); ++i)

@@ -165,25 +165,37 @@ class RunConfig:
     record_events: bool = True
     data_seed: int = 1234
     plan_only: bool = False   # host-side plan without CUDA/NCCL (multi-rank tests on CPU)
-    # "AMDP" (d/2 pipelines, ZeRO), or the synchronous single-pipeline baselines "DAPPLE" /
-    # "GPipe" (builder.hpp: injection = threshold, replicated weights, Update per window)
+    # "AMDP" (d/2 pipelines; ZeRO Reduce/Broadcast unless zero=False: replicated per-pipeline
+    # Update), "Chimera" (two bidirectional pipelines, replicated), the synchronous
+    # single-pipeline baselines "DAPPLE" / "GPipe", "Interleaved1F1B" (two stage chunks per
+    # device: depth = 2 x devices) and "PipeDreamAsync" (an update after every backward);
+    # builder.hpp:145-338 for each policy's tasks and dependencies.
     schedule: str = "AMDP"
+    zero: bool = True
 
     @property
     def num_minibatches(self) -> int:
         return self.windows * self.threshold
 
     def policy(self) -> P.PolicyConfig:
+        M = self.num_minibatches
         if self.schedule == "AMDP":
-            return P.PolicyConfig(P.Policy.AMDP, 2, self.depth // 2, self.threshold,
-                                  self.num_minibatches, True)
-        if self.schedule in ("DAPPLE", "GPipe"):
-            return P.PolicyConfig(P.Policy[self.schedule], self.threshold, 1, self.threshold,
-                                  self.num_minibatches, False)
-        raise ValueError(f"schedule {self.schedule!r} does not execute on GPUs")
+            return P.PolicyConfig(P.Policy.AMDP, 2, self.depth // 2, self.threshold, M, bool(self.zero))
+        if self.schedule in ("DAPPLE", "GPipe", "Interleaved1F1B"):
+            return P.PolicyConfig(P.Policy[self.schedule], self.threshold, 1, self.threshold, M, False)
+        if self.schedule == "Chimera":
+            return P.PolicyConfig(P.Policy.Chimera, self.threshold, 2, self.threshold, M, False)
+        if self.schedule == "PipeDreamAsync":
+            return P.PolicyConfig(P.Policy.PipeDreamAsync, min(self.depth, self.threshold), 1,
+                                  self.threshold, M, False)
+        raise ValueError(f"unknown schedule {self.schedule!r}")
+
+    @property
+    def devices(self) -> int:
+        return self.depth // 2 if self.schedule == "Interleaved1F1B" else self.depth
 
     def declared_cluster(self) -> P.ClusterSpec:
-        return P.ClusterSpec.uniform(self.depth, self.depth, self.declared_fwd, self.declared_bwd)
+        return P.ClusterSpec.uniform(self.depth, self.devices, self.declared_fwd, self.declared_bwd)
 
     def _c(self):
         return _Run(self.policy()._c(), P._r(self.declared_fwd), P._r(self.declared_bwd),
@@ -295,8 +307,9 @@ class Engine:
         lib.amdp_engine_events(self._h, arr, n)
         evs = [P.TaskEvent(P.Kind(e.kind), e.stage, e.minibatch, e.pipeline, e.device,
                            P._f(e.start), P._f(e.duration), bool(e.preloaded), e.window) for e in arr[:n]]
-        return P.Timeline.from_events(evs, P.Policy.AMDP, self.runcfg.depth, self.runcfg.depth,
-                                      self.runcfg.threshold, self.runcfg.declared_cluster())
+        rc = self.runcfg
+        return P.Timeline.from_events(evs, rc.policy().policy, rc.depth, rc.devices, rc.threshold,
+                                      rc.declared_cluster())
 
     def declared_timeline(self) -> P.Timeline:
         h = P._Handle(lib.amdp_engine_schedule(self._h))
@@ -304,7 +317,7 @@ class Engine:
         arr = (c_int * max(1, n))()
         P.lib.amdp_schedule_order(h.h, arr, n)
         rc = self.runcfg
-        return P.Timeline(h, P.Policy.AMDP, rc.depth, rc.depth, rc.threshold, rc.declared_cluster(),
+        return P.Timeline(h, rc.policy().policy, rc.depth, rc.devices, rc.threshold, rc.declared_cluster(),
                           list(arr[:n]))
 
     def version_trace(self) -> str:

@@ -42,6 +42,9 @@ CONFIGS += [
     ("PipeDreamAsync", 8, 8, "1", "2", "1/2", "0", 8, 1, 4, 32, 0),
     ("DAPPLE", 4, 4, "1", "1", "0", "0", 8, 1, 8, 32, 0),     # tiny GPT on the executor (P = 1)
     ("GPipe", 4, 4, "1", "1", "0", "0", 8, 1, 8, 32, 0),
+    ("Chimera", 4, 4, "1", "1", "0", "0", 8, 2, 8, 32, 0),            # replicated, two pipelines
+    ("Interleaved1F1B", 4, 2, "1", "1", "0", "0", 8, 1, 8, 32, 0),    # two chunks per device
+    ("PipeDreamAsync", 4, 4, "1", "1", "0", "0", 4, 1, 8, 32, 0),     # update per backward
 ]
 
 

@@ -154,9 +154,103 @@ def test_synchronous_baselines_plan(schedule, world):
             assert (k, "recv" if kind == "send" else "send", r, -1) in ops[peer]
 
 
+@pytest.mark.parametrize("schedule,zero", [("AMDP", False), ("Chimera", False)])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_replicated_update_plans(schedule, zero, world):
+    """Replicated-update schedules with several pipelines (AMDP with ZeRO off, Chimera;
+    builder.hpp:306-336): every rank hosting a replica of stage i keeps its own optimizer state,
+    the window gradient is all-reduced over the stage's replica group at the first
+    Update(w, i, .) of the global order (issued by exactly the group, same position on every
+    member), and the joint P2P + collective program cannot deadlock."""
+    model = E.ModelConfig.gpt_1p3b()
+    thr = 8 if schedule == "Chimera" else 32
+    plans = []
+    for r in range(world):
+        run = E.RunConfig(depth=8, threshold=thr, windows=2, world_size=world, rank=r, plan_only=True,
+                          schedule=schedule, zero=zero)
+        plans.append(E.Engine(model, run).plan())
+    per = 8 // world
+    if schedule == "Chimera":
+        dev = lambda p, i: i if p == 0 else 7 - i  # noqa: E731  (builder.hpp:160)
+        pipes = 2
+    else:
+        dev = lambda p, i: P.map_stage_to_device(p, i, 8)  # noqa: E731
+        pipes = 4
+    for r, pl in enumerate(plans):
+        for s in pl["stages"]:
+            grp = sorted({dev(p, s["stage"]) // per for p in range(pipes)})
+            assert s["group"] == grp
+            assert s["hosted"] == (r in grp)
+            assert s["owner"] == s["hosted"]  # replicated optimizer state
+        kinds = {o[1] for o in pl["comm_ops"]}
+        assert kinds <= {"send", "recv", "allreduce"}
+    ops = [[tuple(o) for o in pl["comm_ops"]] for pl in plans]
+    if world == 1:
+        assert not any(ops[0])
+        return
+    n_ar = sum(o[1] == "allreduce" for o in ops[0])
+    hosted0 = [s for s in plans[0]["stages"] if s["hosted"] and len(s["group"]) > 1]
+    assert n_ar == 2 * len(hosted0)  # one per window per multi-rank hosted stage
+    assert _check_joint(plans) > 0
+
+
+def _check_joint(plans):
+    """Pairing + rendezvous simulation of the joint program (any collective kinds)."""
+    world = len(plans)
+    ops = [[tuple(o) for o in pl["comm_ops"]] for pl in plans]
+    for r in range(world):
+        for (k, kind, peer, stage) in ops[r]:
+            if kind in ("send", "recv"):
+                assert (k, "recv" if kind == "send" else "send", r, -1) in ops[peer]
+            else:
+                for m in plans[r]["stages"][stage]["group"]:
+                    assert (k, kind, -1, stage) in ops[m]
+    pos = [0] * world
+    while not all(pos[r] >= len(ops[r]) for r in range(world)):
+        progressed = False
+        for r in range(world):
+            if pos[r] >= len(ops[r]):
+                continue
+            k, kind, peer, stage = ops[r][pos[r]]
+            if kind in ("send", "recv"):
+                if pos[peer] < len(ops[peer]) and ops[peer][pos[peer]][:3] == (k, "recv" if kind == "send" else "send", r):
+                    pos[r] += 1
+                    pos[peer] += 1
+                    progressed = True
+            else:
+                members = plans[r]["stages"][stage]["group"]
+                if all(pos[m] < len(ops[m]) and ops[m][pos[m]] == (k, kind, -1, stage) for m in members):
+                    for m in members:
+                        pos[m] += 1
+                    progressed = True
+        assert progressed, f"communication deadlock at positions {pos}"
+    return sum(len(o) for o in ops)
+
+
+@pytest.mark.parametrize("schedule", ["Interleaved1F1B", "PipeDreamAsync"])
+def test_single_pipeline_schedules_plan(schedule):
+    """Interleaved1F1B folds stage chunks i and i + devices onto device i (builder.hpp:165);
+    PipeDreamAsync updates after every backward.  One replica per stage: no collectives."""
+    model = E.ModelConfig.gpt_1p3b()
+    plans = []
+    for r in range(2):
+        run = E.RunConfig(depth=8, threshold=8, windows=2, world_size=2, rank=r, plan_only=True,
+                          schedule=schedule)
+        plans.append(E.Engine(model, run).plan())
+    devices = 4 if schedule == "Interleaved1F1B" else 8
+    per = devices // 2
+    for r, pl in enumerate(plans):
+        for s in pl["stages"]:
+            d = s["stage"] % devices
+            assert s["hosted"] == (d // per == r)
+            assert s["group"] == [d // per]
+        assert all(o[1] in ("send", "recv") for o in pl["comm_ops"])
+    assert _check_joint(plans) > 0
+
+
 def test_unsupported_schedules_rejected():
     model = E.ModelConfig.tiny()
-    with pytest.raises(ValueError):  # replicated multi-pipeline schedules do not execute
-        E.Engine(model, E.RunConfig(depth=4, threshold=8, windows=2, plan_only=True, schedule="Chimera"))
+    with pytest.raises(ValueError):
+        E.Engine(model, E.RunConfig(depth=4, threshold=8, windows=2, plan_only=True, schedule="ZeroBubble"))
     with pytest.raises(RuntimeError):  # AMDP needs an even depth (validate.hpp:60-73)
         E.Engine(model, E.RunConfig(depth=3, threshold=8, windows=2, plan_only=True))

@@ -87,3 +87,34 @@ def test_bf16_rounding_is_nearest_even():
     assert r[0] == 1.0 and r[1] == 1.0  # tie -> even
     assert r[2] == np.float32(1.0 + 2 ** -7)
     assert r[3] == -2.5
+
+
+EXEC_CONFIGS = [
+    ["AMDP", 4, 4, "1", "1", "0", "0", 2, 2, 8, 32, 1],
+    ["AMDP", 4, 4, "1", "1", "0", "0", 2, 2, 8, 32, 0],
+    ["Chimera", 4, 4, "1", "1", "0", "0", 8, 2, 8, 32, 0],
+    ["DAPPLE", 4, 4, "1", "1", "0", "0", 8, 1, 8, 32, 0],
+    ["GPipe", 4, 4, "1", "1", "0", "0", 8, 1, 8, 32, 0],
+    ["Interleaved1F1B", 4, 2, "1", "1", "0", "0", 8, 1, 8, 32, 0],
+    ["PipeDreamAsync", 4, 4, "1", "1", "0", "0", 4, 1, 8, 32, 0],
+]
+
+
+@pytest.mark.parametrize("cfg", EXEC_CONFIGS, ids=lambda c: f"{c[0]}-zero{c[-1]}")
+def test_replay_versions_match_reference_mismatch_report(cfg):
+    """The replay's per-replica versions (Broadcast rewrites every replica of a stage, Update
+    only its own pipeline's) reproduce the reference's own mismatch_report: updates between
+    F finish and B start per (stage, minibatch) (analysis.hpp:28-88, fixture from the
+    unmodified reference)."""
+    e = [x for x in SCHED if x["config"] == cfg][0]
+    m = O.Model(4, 32, 2, 64, 64, 16, 1, True, 3)
+    M = cfg[10]
+    inputs, labels = O.synthetic_tokens(16, 1, 64, 1234, 0, M)
+    div = 1 if cfg[0] == "PipeDreamAsync" else cfg[9]
+    losses, _, seen = O.replay(e["csv"], m, [1, 1, 1, 1], O.Opt("adamw", 1e-3, 0.9, 0.95, 1e-8, 0.0),
+                               cfg[9], inputs, labels, update_div=div)
+    assert np.all(np.isfinite(losses))
+    nz = {(s, j): n for s, j, n in e["mismatch_nonzero"]}
+    for i in range(4):
+        for j in range(M):
+            assert seen[("Backward", i, j)] - seen[("Forward", i, j)] == nz.get((i, j), 0), (i, j)
