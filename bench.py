@@ -166,8 +166,11 @@ def main():
     ap.add_argument("--model", default="1p3b")
     ap.add_argument("--threshold", type=int, default=32)
     ap.add_argument("--depth", type=int, default=8)
-    ap.add_argument("--schedule", default="AMDP", choices=["AMDP", "DAPPLE", "GPipe"],
-                    help="AMDP (headline) or a synchronous single-pipeline baseline on the same executor")
+    ap.add_argument("--schedule", default="AMDP",
+                    choices=["AMDP", "DAPPLE", "GPipe", "Chimera", "Interleaved1F1B", "PipeDreamAsync"],
+                    help="AMDP (headline) or another reference schedule on the same executor")
+    ap.add_argument("--no-zero", action="store_true",
+                    help="AMDP with replicated per-pipeline updates instead of ZeRO reduce/broadcast")
     ap.add_argument("--no-kernel-timing", action="store_true")
     args = ap.parse_args()
 
@@ -176,13 +179,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     model = model_cfg(args.model)
     tok_step = args.threshold * model.tokens_per_minibatch
-    npipe = args.depth // 2 if args.schedule == "AMDP" else 1
+    npipe = {"AMDP": args.depth // 2, "Chimera": 2}.get(args.schedule, 1)
+    zero = args.schedule == "AMDP" and not args.no_zero
     cfg = {"workload": f"GPT-style {args.model} {args.schedule} D={args.depth} ({npipe} pipelines), "
                        f"seq {model.seq}, {model.seqs_per_minibatch} seqs/minibatch, "
                        f"{args.threshold} minibatches/step",
            "model": ("bert-large" if args.model == "bert" else f"gpt-{args.model}"), "layers": model.layers, "hidden": model.hidden,
            "global_batch": args.threshold * model.seqs_per_minibatch, "seq_len": model.seq,
-           "tokens_per_step": tok_step, "parallelism": f"{args.schedule.lower()}-d{args.depth}-p{npipe} folded on {args.gpus} GPU",
+           "tokens_per_step": tok_step, "parallelism": f"{args.schedule.lower()}{'' if zero or args.schedule != 'AMDP' else '-replicated'}-d{args.depth}-p{npipe} folded on {args.gpus} GPU",
            "declared_costs": "uniform fwd=1 bwd=1 (preload 1)", "l2": "working set >> L2 (no flush)"}
     metric = "tokens/s AMDP GPT-style training" if args.schedule == "AMDP" else f"tokens/s {args.schedule} GPT-style training"
 
@@ -238,7 +242,7 @@ def main():
     windows = max(args.steps, args.warmup)
     opt = E.OptimizerConfig(lr=1e-4, weight_decay=0.0)
     run = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=windows, optimizer=opt, schedule=args.schedule,
-                      world_size=world, rank=rank)
+                      zero=zero, world_size=world, rank=rank)
     eng = E.Engine(model, run, nccl_id)
     M = run.num_minibatches
     toks = E.PinnedTokens(M, model.tokens_per_minibatch)
@@ -273,9 +277,9 @@ def main():
             gap_ns = model.tokens_per_minibatch * model.hidden * 2 / 770e9 * 1e9
             numel = [lib_numel(eng, i) for i in range(args.depth)]
             pol = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=args.steps,
-                              schedule=args.schedule).policy()
+                              schedule=args.schedule, zero=zero).policy()
             projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
-                                    stage_numel=numel if args.schedule == "AMDP" else None, policy=pol)
+                                    stage_numel=numel, policy=pol)
         except Exception as e:  # never let the projection break the bench line
             projection = {"error": str(e)[:200]}
 

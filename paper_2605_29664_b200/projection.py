@@ -25,12 +25,15 @@ KIND_TAG = {P.Kind.Forward: "F", P.Kind.Backward: "B", P.Kind.Reduce: "R", P.Kin
 
 
 def measured_costs(tl: P.Timeline, min_window: int = 1) -> Dict[Tuple[P.Kind, int], float]:
-    """Mean measured duration (ns) per (kind, stage) over windows >= min_window."""
+    """Mean measured duration (ns) per (kind, stage) over windows >= min_window.  Update tasks
+    take the max: folded on one GPU only the first replica's Update of a window runs the
+    optimizer (the others switch weight buffers), while on one GPU per device every replica
+    steps its own optimizer state."""
     acc: Dict[Tuple[P.Kind, int], list] = {}
     for ev in tl.flat():
         if ev.window >= min_window:
             acc.setdefault((ev.kind, ev.stage), []).append(float(ev.duration))
-    return {k: statistics.mean(v) for k, v in acc.items()}
+    return {k: (max(v) if k[0] == P.Kind.Update else statistics.mean(v)) for k, v in acc.items()}
 
 
 def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple[P.Kind, int], float],
@@ -66,18 +69,30 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
     return P.Timeline.from_events(events, policy.policy, depth, devices, policy.accumulation_threshold)
 
 
-def collective_costs(stage_numel, replicas: int, link_gbs: float = 770.0) -> Dict[Tuple[P.Kind, int], float]:
+def collective_costs(stage_numel, replicas: int, link_gbs: float = 770.0,
+                     zero: bool = True) -> Dict[Tuple[P.Kind, int], float]:
     """Window-boundary communication a 1-GPU run does not perform: per stage, the ZeRO Reduce of
     the fp32 window gradient to the owner and the Broadcast of the fp32 weights over the
     stage's `replicas` devices, each moving (replicas-1)/replicas of the stage's bytes per
-    device (analysis.hpp:341-346 reduce_broadcast_cost) at the measured peer bandwidth."""
+    device (analysis.hpp:341-346 reduce_broadcast_cost) at the measured peer bandwidth; without
+    ZeRO, the all-reduce of the window gradient (reduce + broadcast volume) in every Update."""
     f = (replicas - 1) / replicas if replicas > 1 else 0.0
     out = {}
     for s, n in enumerate(stage_numel):
         t = f * 4.0 * n / (link_gbs * 1e9) * 1e9
-        out[(P.Kind.Reduce, s)] = t
-        out[(P.Kind.Broadcast, s)] = t
+        if zero:
+            out[(P.Kind.Reduce, s)] = t
+            out[(P.Kind.Broadcast, s)] = t
+        else:
+            out[(P.Kind.Update, s)] = 2 * t
     return out
+
+
+def replicas_of(policy: P.PolicyConfig) -> int:
+    """Weight replicas per stage (builder.hpp:154-156): AMDP d/2 pipelines, Chimera 2, else 1."""
+    if policy.policy == P.Policy.AMDP:
+        return policy.num_pipelines
+    return 2 if policy.policy == P.Policy.Chimera else 1
 
 
 def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, tokens_per_minibatch: int,
@@ -90,12 +105,13 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
                                    accumulation_threshold=threshold, num_minibatches=windows * threshold,
                                    zero_enabled=True)
     bubble_nc = None
-    if stage_numel is not None:
-        rep0 = static_order_replay(pol, depth, costs, gap_ns)
+    devices = depth // 2 if pol.policy == P.Policy.Interleaved1F1B else depth
+    if stage_numel is not None and replicas_of(pol) > 1:
+        rep0 = static_order_replay(pol, depth, costs, gap_ns, devices=devices)
         bubble_nc = float(P.bubble_ratio(rep0, 1 if windows > 2 else 0))
-        for k, v in collective_costs(stage_numel, depth // 2).items():
+        for k, v in collective_costs(stage_numel, replicas_of(pol), zero=pol.zero_enabled).items():
             costs[k] = costs.get(k, 0.0) + v
-    rep = static_order_replay(pol, depth, costs, gap_ns)
+    rep = static_order_replay(pol, depth, costs, gap_ns, devices=devices)
     bubble = P.bubble_ratio(rep, 1 if windows > 2 else 0)
     # steady-state window period: first F of window w to first F of window w+1, averaged
     firsts = {}
@@ -104,14 +120,14 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
             firsts[ev.window] = min(firsts.get(ev.window, ev.start), ev.start)
     ws = sorted(firsts)
     period = float(firsts[ws[-1]] - firsts[ws[1]]) / (len(ws) - 2) if len(ws) > 2 else None
-    return {"gpus": depth, "bubble": float(bubble), "bubble_without_collectives": bubble_nc,
+    return {"gpus": devices, "bubble": float(bubble), "bubble_without_collectives": bubble_nc,
             "tokens_per_s": (threshold * tokens_per_minibatch / (period * 1e-9)) if period else None,
             "gap_us": gap_ns / 1e3,
             "stage_ms": {f"{KIND_TAG[k[0]]}{k[1]}": round(v / 1e6, 3) for k, v in sorted(costs.items())},
             "method": "static-order replay of the declared dispatch order on one GPU per "
                       "logical device, task costs = measured 1-GPU means (windows >= 1) plus the "
-                      "window Reduce/Broadcast collectives at 770 GB/s ((P-1)/P of the stage's fp32 "
-                      "bytes each), inter-device gap = activation bytes / 770 GB/s peer copy; bubble = "
+                      "window Reduce/Broadcast collectives (or the replicated Update's all-reduce) at "
+                      "770 GB/s ((P-1)/P of the stage's fp32 bytes per phase), inter-device gap = activation bytes / 770 GB/s peer copy; bubble = "
                       "reference bubble_ratio(tl, 1).  A projection, not a multi-GPU measurement."}
 
 
