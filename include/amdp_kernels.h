@@ -43,7 +43,12 @@ enum amdp_epilogue {
   AMDP_EPI_RESIDUAL = 2,   /* C bf16 = acc + aux (bf16 residual stream)             */
   AMDP_EPI_ACCUM_F32 = 3,  /* C f32 += acc (window gradient accumulation)           */
   AMDP_EPI_GELU_BWD = 4,   /* C bf16 = acc * gelu'(aux), aux = pre-activation       */
-  AMDP_EPI_STORE_F32 = 5   /* C f32 = acc                                           */
+  AMDP_EPI_STORE_F32 = 5,  /* C f32 = acc                                           */
+  AMDP_EPI_ROWDOT = 6      /* C bf16 = acc, and per row and rowdot_seg-column segment
+                              rowdot[(m / rowdot_seq) * (N / rowdot_seg) + n / rowdot_seg]
+                                    [m % rowdot_seq] = sum bf16(acc) * aux over the segment
+                              (attention backward's delta = rowsum(dO * O) per head, fused
+                              into the dO GEMM); A and B K-major, rowdot_seg a multiple of 64 */
 };
 
 typedef struct amdp_gemm_args {
@@ -62,6 +67,9 @@ typedef struct amdp_gemm_args {
   int ldc2;
   int epilogue;
   float alpha;
+  float* rowdot;     /* AMDP_EPI_ROWDOT only */
+  int rowdot_seg;
+  int rowdot_seq;
 } amdp_gemm_args;
 
 int amdp_gemm(const amdp_gemm_args* args, amdp_stream_t stream);
@@ -76,6 +84,13 @@ int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse, int batch
 /* dout: [batch*seq][H*D]; writes dqkv [batch*seq][3*H*D] (dq | dk | dv).
  * workspace: at least amdp_attention_bwd_workspace() bytes.                        */
 size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim);
+/* The same backward with delta[batch][H][seq] = rowsum(dout * out) per head supplied by the
+ * caller (e.g. from the dO GEMM's AMDP_EPI_ROWDOT epilogue); tcgen05 path only
+ * (amdp_attention_bwd_delta_supported), AMDP_ERR_UNSUPPORTED otherwise.             */
+int amdp_attention_bwd_delta_supported(int seq, int head_dim);
+int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse, const float* delta,
+                             uint16_t* dqkv, int batch, int seq, int heads, int head_dim, int causal,
+                             amdp_stream_t stream);
 int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                        const float* lse, uint16_t* dqkv, void* workspace, int batch, int seq,
                        int heads, int head_dim, int causal, amdp_stream_t stream);

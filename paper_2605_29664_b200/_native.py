@@ -30,7 +30,7 @@ def _load() -> ctypes.CDLL:
 lib = _load()
 
 # ------------------------------------------------------------------ kernels
-EPI_STORE_BF16, EPI_GELU, EPI_RESIDUAL, EPI_ACCUM_F32, EPI_GELU_BWD, EPI_STORE_F32 = range(6)
+EPI_STORE_BF16, EPI_GELU, EPI_RESIDUAL, EPI_ACCUM_F32, EPI_GELU_BWD, EPI_STORE_F32, EPI_ROWDOT = range(7)
 OPT_SGD, OPT_MOMENTUM, OPT_REF_ADAMTYPE, OPT_ADAMW = range(4)
 
 
@@ -41,7 +41,8 @@ class GemmArgs(Structure):
                 ("C", c_void_p), ("ldc", c_int),
                 ("aux", c_void_p), ("ld_aux", c_int),
                 ("C2", c_void_p), ("ldc2", c_int),
-                ("epilogue", c_int), ("alpha", c_float)]
+                ("epilogue", c_int), ("alpha", c_float),
+                ("rowdot", c_void_p), ("rowdot_seg", c_int), ("rowdot_seq", c_int)]
 
 
 class OptArgs(Structure):
@@ -63,6 +64,9 @@ _sig("amdp_attention_fwd", c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_int
 _sig("amdp_attention_bwd_workspace", c_size_t, [c_int, c_int, c_int, c_int])
 _sig("amdp_attention_bwd", c_int,
      [_P, _P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
+_sig("amdp_attention_bwd_delta_supported", c_int, [c_int, c_int])
+_sig("amdp_attention_bwd_delta", c_int,
+     [_P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
 _sig("amdp_layernorm_fwd", c_int, [_P, _P, _P, _P, _P, _P, c_int, c_int, c_float, _P])
 _sig("amdp_layernorm_bwd_workspace", c_size_t, [c_int, c_int])
 _sig("amdp_layernorm_bwd", c_int,

@@ -25,9 +25,10 @@ struct Carver {
 // when the executor's kernel timer is on.
 int gemm_t(KTimer* kt, int M, int N, int K, const void* A, int lda, bool amn, const void* B, int ldb,
            bool bmn, void* C, int ldc, int epi, cudaStream_t s, const void* aux = nullptr,
-           int ld_aux = 0, void* C2 = nullptr, int ldc2 = 0, int cls = -1) {
+           int ld_aux = 0, void* C2 = nullptr, int ldc2 = 0, int cls = -1, float* rowdot = nullptr,
+           int rowdot_seg = 0, int rowdot_seq = 0) {
   amdp_gemm_args a{M, N, K, A, lda, amn ? 1 : 0, B, ldb, bmn ? 1 : 0, C, ldc, aux, ld_aux, C2, ldc2,
-                   epi, 1.0f};
+                   epi, 1.0f, rowdot, rowdot_seg, rowdot_seq};
   if (cls < 0) cls = epi == AMDP_EPI_ACCUM_F32 ? K_GEMM_WGRAD : (bmn ? K_GEMM_DGRAD : K_GEMM_FWD);
   if (kt) kt->begin(cls, 2.0 * M * N * static_cast<double>(K), 0, s);
   const int rc = amdp_gemm(&a, reinterpret_cast<amdp_stream_t>(s));
@@ -297,6 +298,8 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
   const int T = d_.T, h = d_.h, F = d_.ffn;
   const Ws ws = carve_ws(d_, wsb);
   cudaStream_t sd = ss.side ? ss.side : s;
+  static const bool no_fuse = getenv("AMDP_NO_DELTA_FUSION") != nullptr;
+  const bool fuse_delta = !no_fuse && d_.hd % 64 == 0 && amdp_attention_bwd_delta_supported(d_.S, d_.hd);
   auto hand = [&](cudaEvent_t e, cudaStream_t from, cudaStream_t to) {
     if (from == to) return;
     cudaEventRecord(e, from);
@@ -340,11 +343,23 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     // hmid = x + o Wo^T
     AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_DH], sd);
-    AMDP_GEMM(gemm_t(kt, T, h, h, ws.dhmid, h, false, wt + P.o.off, h, false, ws.dtmp, h, AMDP_EPI_STORE_BF16, s,
-                     nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
+    // dO = dhmid Wo; its epilogue also forms the attention backward's delta = rowsum(dO * O)
+    // per head (AMDP_EPI_ROWDOT) instead of a separate pass over dO and O
+    if (fuse_delta) {
+      AMDP_GEMM(gemm_t(kt, T, h, h, ws.dhmid, h, false, wt + P.o.off, h, false, ws.dtmp, h, AMDP_EPI_ROWDOT, s,
+                       A.o, h, nullptr, 0, K_GEMM_DGRAD, ws.attn, d_.hd, d_.S), 1);
+    } else {
+      AMDP_GEMM(gemm_t(kt, T, h, h, ws.dhmid, h, false, wt + P.o.off, h, false, ws.dtmp, h, AMDP_EPI_STORE_BF16, s,
+                       nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
+    }
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DQ], 0);  // previous layer's dWqkv done with dqkv
-    AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
-                                d_.causal ? 1 : 0, st), 3);
+    if (fuse_delta) {
+      AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd_delta(A.qkv, ws.dtmp, A.lse, ws.attn, ws.dqkv, d_.B, d_.S,
+                                  d_.heads, d_.hd, d_.causal ? 1 : 0, st), 2);
+    } else {
+      AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
+                                  d_.causal ? 1 : 0, st), 3);
+    }
     hand(ss.ev[E_DQ], s, sd);
     // qkv = ln1 Wqkv^T
     AMDP_GEMM(gemm_t(kt, 3 * h, h, T, ws.dqkv, 3 * h, true, A.ln1, h, true, grad + P.qkv.off, h,

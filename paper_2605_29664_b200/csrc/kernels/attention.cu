@@ -599,6 +599,20 @@ extern "C" int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse
   return AMDP_ERR_UNSUPPORTED;
 }
 
+extern "C" int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse,
+                                        const float* delta, uint16_t* dqkv, int batch, int seq, int heads,
+                                        int head_dim, int causal, amdp_stream_t stream) {
+  if (batch <= 0 || seq <= 0 || heads <= 0 || !delta) return AMDP_ERR_INVALID;
+  if (!amdp_attention_bwd_delta_supported(seq, head_dim)) return AMDP_ERR_UNSUPPORTED;
+  return attention_bwd_tc(reinterpret_cast<const bf16*>(qkv), reinterpret_cast<const bf16*>(dout), lse,
+                          const_cast<float*>(delta), reinterpret_cast<bf16*>(dqkv), batch, seq, heads, head_dim,
+                          causal, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int amdp_attention_bwd_delta_supported(int seq, int head_dim) {
+  return (head_dim == 64 || head_dim == 80 || head_dim == 128) && seq > 0 && seq % 128 == 0;
+}
+
 extern "C" size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim) {
   (void)head_dim;
   return static_cast<size_t>(batch) * seq * heads * sizeof(float);

@@ -56,6 +56,8 @@ struct EpiParams {
   __nv_bfloat16* C2;
   int ldc2;
   float alpha;
+  float* rowdot;  // AMDP_EPI_ROWDOT: [M / seq][N / seg][seq] fp32
+  int seg, seq;
 };
 
 // tanh on the SFU (tanh.approx.f32, max rel. error ~2^-11): the GELU epilogues run once per
@@ -112,7 +114,8 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
   // aux_bar[b] / bit b of aux_phase: the residual / pre-activation block landing in staging
   // buffer b.  Block c+1's load is issued before block c's math (one block of prefetch).
   constexpr bool F32 = (EPI == AMDP_EPI_ACCUM_F32 || EPI == AMDP_EPI_STORE_F32);
-  constexpr bool AUX = (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD);
+  constexpr bool ROWDOT = EPI == AMDP_EPI_ROWDOT;
+  constexpr bool AUX = (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD || ROWDOT);
   if constexpr (F32) {
 #pragma unroll 1
     for (int cc = 0; cc < width; cc += 32) {
@@ -140,7 +143,8 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
     }
   } else {
     const int n_end = min(width, p.N - n0);
-    if constexpr (AUX) {  // block 0's residual / pre-activation
+    float dot = 0.f;  // ROWDOT: this row's partial sum over the current segment
+    if constexpr (AUX) {  // block 0's residual / pre-activation / dot operand
       if (lane == 0) {
         ptx::bulk_wait_read<1>();
         ptx::mbar_arrive_expect_tx(&aux_bar[bsel], 4096);
@@ -170,7 +174,7 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
       ptx::tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(raw[j]) * p.alpha;
-      if constexpr (AUX) {
+      if constexpr (AUX && !ROWDOT) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const uint4 q = *reinterpret_cast<const uint4*>(buf + sw_chunk(lane, j));
@@ -216,7 +220,33 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
         __nv_bfloat162* hq = reinterpret_cast<__nv_bfloat162*>(&q);
 #pragma unroll
         for (int e = 0; e < 4; ++e) hq[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+        if constexpr (ROWDOT) {  // dot of the stored (bf16) values with the aux chunk in place
+          const uint4 a = *reinterpret_cast<const uint4*>(buf + sw_chunk(lane, j));
+          const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 x = __bfloat1622float2(hq[e]), y = __bfloat1622float2(ha[e]);
+            dot = fmaf(x.x, y.x, dot);
+            dot = fmaf(x.y, y.y, dot);
+          }
+        }
         *reinterpret_cast<uint4*>(buf + sw_chunk(lane, j)) = q;
+      }
+      if constexpr (ROWDOT) {
+        const int col_end = n0 + cc + 64;  // segments end on 64-column block boundaries
+        if (col_end % p.seg == 0 || cc + 64 >= n_end) {
+          const int row = row0 + lane;
+          const int seg_lo = ((col_end - 1) / p.seg) * p.seg;
+          if (row < p.M) {
+            float* dst = p.rowdot + (static_cast<size_t>(row / p.seq) * (p.N / p.seg) + seg_lo / p.seg) * p.seq +
+                         row % p.seq;
+            // a segment split across two tiles (64-wide tail sub-tiles): two partial sums
+            // added to zero, exact in either order
+            if (seg_lo >= n0 && seg_lo + p.seg <= n0 + n_end) *dst = dot;
+            else atomicAdd(dst, dot);
+          }
+          dot = 0.f;
+        }
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
@@ -271,7 +301,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 3 && lane == 0) {
     ptx::tma_prefetch(&em.c);
     if (EPI == AMDP_EPI_GELU) ptx::tma_prefetch(&em.c2);
-    if (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD) ptx::tma_prefetch(&em.aux);
+    if (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD || EPI == AMDP_EPI_ROWDOT) ptx::tma_prefetch(&em.aux);
   }
   if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
   ptx::tc_fence_before();
@@ -470,7 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
   if (warp == 3 && lane == 0) {
     ptx::tma_prefetch(&em.c);
     if (EPI == AMDP_EPI_GELU) ptx::tma_prefetch(&em.c2);
-    if (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD) ptx::tma_prefetch(&em.aux);
+    if (EPI == AMDP_EPI_RESIDUAL || EPI == AMDP_EPI_GELU_BWD || EPI == AMDP_EPI_ROWDOT) ptx::tma_prefetch(&em.aux);
   }
   if (warp == 2) ptx::tmem_alloc_pair<C::TMEM>(tmem_slot);
   ptx::tc_fence_before();
@@ -736,6 +766,9 @@ int dispatch_epi(int mode, int epi, const CUtensorMap& ma, const CUtensorMap& mb
     case AMDP_EPI_ACCUM_F32: return launch<A_MN, B_MN, AMDP_EPI_ACCUM_F32>(mode, ma, mb, mbt, em, p, s);
     case AMDP_EPI_GELU_BWD: return launch<A_MN, B_MN, AMDP_EPI_GELU_BWD>(mode, ma, mb, mbt, em, p, s);
     case AMDP_EPI_STORE_F32: return launch<A_MN, B_MN, AMDP_EPI_STORE_F32>(mode, ma, mb, mbt, em, p, s);
+    case AMDP_EPI_ROWDOT:
+      if constexpr (!A_MN && !B_MN) return launch<A_MN, B_MN, AMDP_EPI_ROWDOT>(mode, ma, mb, mbt, em, p, s);
+      break;
   }
   return AMDP_ERR_INVALID;
 }
@@ -766,7 +799,11 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
   using namespace amdp;
   if (!a || a->M <= 0 || a->N <= 0 || a->K <= 0 || a->K % BK != 0) return AMDP_ERR_INVALID;
   if (a->N % 8 != 0 || a->ldc % 4 != 0) return AMDP_ERR_INVALID;
-  if (a->epilogue < 0 || a->epilogue > AMDP_EPI_STORE_F32) return AMDP_ERR_INVALID;
+  if (a->epilogue < 0 || a->epilogue > AMDP_EPI_ROWDOT) return AMDP_ERR_INVALID;
+  if (a->epilogue == AMDP_EPI_ROWDOT &&
+      (!a->aux || !a->rowdot || a->a_mn_major || a->b_mn_major || a->rowdot_seg <= 0 || a->rowdot_seg % 64 != 0 ||
+       a->N % a->rowdot_seg != 0 || a->rowdot_seq <= 0 || a->M % a->rowdot_seq != 0))
+    return AMDP_ERR_INVALID;
   if ((a->epilogue == AMDP_EPI_RESIDUAL || a->epilogue == AMDP_EPI_GELU_BWD) && !a->aux)
     return AMDP_ERR_INVALID;
   if (a->epilogue == AMDP_EPI_GELU && !a->C2) return AMDP_ERR_INVALID;
@@ -804,13 +841,23 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
     em.c2 = em.c;
     em.aux = em.c;
     if (ok && a->epilogue == AMDP_EPI_GELU) ok = make_map(&em.c2, a->C2, a->N, a->M, a->ldc2, 32);
-    if (ok && (a->epilogue == AMDP_EPI_RESIDUAL || a->epilogue == AMDP_EPI_GELU_BWD))
+    if (ok && (a->epilogue == AMDP_EPI_RESIDUAL || a->epilogue == AMDP_EPI_GELU_BWD || a->epilogue == AMDP_EPI_ROWDOT))
       ok = make_map(&em.aux, a->aux, a->N, a->M, a->ld_aux, 32);
     if (!ok) return AMDP_ERR_TMA;
   }
   EpiParams p{a->M, a->N, a->K, a->C, a->ldc,
               static_cast<const __nv_bfloat16*>(a->aux), a->ld_aux,
-              static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha};
+              static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha,
+              a->rowdot, a->rowdot_seg, a->rowdot_seq};
+  if (a->epilogue == AMDP_EPI_ROWDOT && mode != 0) {
+    // tail sub-tiles narrower than a segment split it between two CTAs (atomicAdd onto zero)
+    const PairSched sc = pair_schedule(a->M, a->N, false, gemm_pairs());
+    if (PBN / sc.tail_split < a->rowdot_seg) {
+      const cudaError_t e = cudaMemsetAsync(a->rowdot, 0, static_cast<size_t>(a->M) * (a->N / a->rowdot_seg) * sizeof(float),
+                                            reinterpret_cast<cudaStream_t>(stream));
+      if (e != cudaSuccess) return e;
+    }
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int am = a->a_mn_major ? 1 : 0, bm = a->b_mn_major ? 1 : 0;
   if (!am && !bm) return dispatch_epi<false, false>(mode, a->epilogue, ma, mb, mbt, em, p, s);

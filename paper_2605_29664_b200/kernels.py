@@ -21,7 +21,8 @@ def _p(t):
 
 
 def gemm(A, B, *, M, N_, K, a_mn=False, b_mn=False, lda=None, ldb=None, C=None, ldc=None,
-         epilogue=N.EPI_STORE_BF16, aux=None, ld_aux=0, C2=None, ldc2=0, alpha=1.0):
+         epilogue=N.EPI_STORE_BF16, aux=None, ld_aux=0, C2=None, ldc2=0, alpha=1.0,
+         rowdot=None, rowdot_seg=0, rowdot_seq=0):
     """C = epi(alpha * A(m,k) B(n,k)); see amdp_gemm for the operand conventions."""
     if lda is None:
         lda = M if a_mn else K
@@ -34,7 +35,8 @@ def gemm(A, B, *, M, N_, K, a_mn=False, b_mn=False, lda=None, ldb=None, C=None, 
         ldc = C.stride(0)
     args = N.GemmArgs(M, N_, K, A.data_ptr(), lda, int(a_mn), B.data_ptr(), ldb, int(b_mn),
                       C.data_ptr(), ldc, aux.data_ptr() if aux is not None else 0, ld_aux,
-                      C2.data_ptr() if C2 is not None else 0, ldc2, epilogue, alpha)
+                      C2.data_ptr() if C2 is not None else 0, ldc2, epilogue, alpha,
+                      rowdot.data_ptr() if rowdot is not None else 0, rowdot_seg, rowdot_seq)
     N.check(N.lib.amdp_gemm(ctypes.byref(args), _stream()), "amdp_gemm")
     return C
 
@@ -54,6 +56,14 @@ def attention_bwd(qkv, out, dout, lse, batch, seq, heads, head_dim, causal=True)
     N.check(N.lib.amdp_attention_bwd(_p(qkv), _p(out), _p(dout), _p(lse), _p(dqkv), _p(ws),
                                      batch, seq, heads, head_dim, int(causal), _stream()),
             "amdp_attention_bwd")
+    return dqkv
+
+
+def attention_bwd_delta(qkv, dout, lse, delta, batch, seq, heads, head_dim, causal=True):
+    """Backward with delta [batch][heads][seq] supplied (amdp_attention_bwd_delta)."""
+    dqkv = torch.empty_like(qkv)
+    N.check(N.lib.amdp_attention_bwd_delta(_p(qkv), _p(dout), _p(lse), _p(delta), _p(dqkv), batch, seq, heads,
+                                           head_dim, int(causal), _stream()), "amdp_attention_bwd_delta")
     return dqkv
 
 

@@ -150,6 +150,47 @@ def test_attention_fwd_bwd(K, B, S, H, D, causal):
         assert _rel(dqkv[:, part * hd:(part + 1) * hd], g[:, part * hd:(part + 1) * hd]) < 2e-2
 
 
+# (M, N, K, seg, seq): the 1.3B dO GEMM (8192x2048, 256 tiles -> tail split), a 350M-like
+# head_dim 64 case, a single-CTA M < 256 case and a 64-wide-tail case (segments split
+# between two CTAs: atomic sum of two partials onto zero).
+@pytest.mark.parametrize("M,N_,K_,seg,seq", [(8192, 2048, 256, 128, 2048), (4096, 1024, 128, 64, 1024),
+                                             (128, 512, 128, 128, 64), (2560, 2048, 128, 128, 512)])
+def test_gemm_rowdot(K, N, M, N_, K_, seg, seq):
+    """AMDP_EPI_ROWDOT: C = bf16(A B^T) and rowdot[b][h][s] = sum over the h-th seg-column
+    segment of bf16(C) * aux (attention backward's delta from the dO GEMM)."""
+    torch.manual_seed(5)
+    A = torch.randn(M, K_, device="cuda").bfloat16()
+    B = (torch.randn(N_, K_, device="cuda") / math.sqrt(K_)).bfloat16()
+    aux = torch.randn(M, N_, device="cuda").bfloat16()
+    rowdot = torch.full((M // seq, N_ // seg, seq), float("nan"), device="cuda")
+    C = K.gemm(A, B, M=M, N_=N_, K=K_, epilogue=N.EPI_ROWDOT, aux=aux, ld_aux=N_, rowdot=rowdot,
+               rowdot_seg=seg, rowdot_seq=seq)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T
+    assert (C.float() - ref).abs().max().item() < 0.02 * ref.abs().max().item()
+    want = (C.float() * aux.float()).view(M // seq, seq, N_ // seg, seg).sum(-1).permute(0, 2, 1)
+    assert torch.isfinite(rowdot).all()
+    assert _rel(rowdot, want) < 1e-5
+
+
+@pytest.mark.parametrize("B,S,H,D", [(2, 256, 3, 64), (4, 2048, 2, 128), (1, 512, 2, 80)])
+def test_attention_bwd_supplied_delta(K, B, S, H, D):
+    """amdp_attention_bwd_delta with delta = rowsum(dO * O) from the caller gives the same
+    gradients as the self-contained backward (torch fp32 reference as above)."""
+    torch.manual_seed(6)
+    qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
+    dout = torch.randn(B * S, H * D, device="cuda").bfloat16()
+    out, lse = K.attention_fwd(qkv, B, S, H, D, True)
+    delta = (dout.float() * out.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).contiguous()
+    dqkv = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, True)
+    x = qkv.float().requires_grad_()
+    _attn_ref(x, B, S, H, D, True).backward(dout.float())
+    torch.cuda.synchronize()
+    hd = H * D
+    for part in range(3):
+        assert _rel(dqkv[:, part * hd:(part + 1) * hd], x.grad[:, part * hd:(part + 1) * hd]) < 2e-2
+
+
 @pytest.mark.parametrize("rows,cols", [(256, 128), (1000, 1024), (4096, 2048), (512, 2560)])
 def test_layernorm(K, rows, cols):
     torch.manual_seed(4)

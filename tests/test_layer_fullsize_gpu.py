@@ -89,8 +89,10 @@ def test_layer_forward_backward_full_size(layer):
     dl2 = K.gemm(dU, wt["w1"], M=T, N_=h, K=F)
     dhm = K.layernorm_bwd(dl2, hm, ln["g2"], m2, r2, dy, gl["g2"], gl["b2"])
     K.gemm(dhm, o, M=h, N_=h, K=T, a_mn=True, b_mn=True, C=g["wo"], epilogue=N.EPI_ACCUM_F32)
-    do = K.gemm(dhm, wt["wo"], M=T, N_=h, K=h)
-    dqkv = K.attention_bwd(qkv, o, do, lse, B, S, H, D)
+    delta = torch.empty(B, H, S, device="cuda")  # dO GEMM epilogue forms delta = rowsum(dO * O)
+    do = K.gemm(dhm, wt["wo"], M=T, N_=h, K=h, epilogue=N.EPI_ROWDOT, aux=o, ld_aux=h, rowdot=delta,
+                rowdot_seg=D, rowdot_seq=S)
+    dqkv = K.attention_bwd_delta(qkv, do, lse, delta, B, S, H, D)
     K.gemm(dqkv, l1, M=3 * h, N_=h, K=T, a_mn=True, b_mn=True, C=g["wqkv"], epilogue=N.EPI_ACCUM_F32)
     dl1 = K.gemm(dqkv, wt["wqkv"], M=T, N_=h, K=3 * h)
     dx = K.layernorm_bwd(dl1, x, ln["g1"], m1, r1, dhm, gl["g1"], gl["b1"])
