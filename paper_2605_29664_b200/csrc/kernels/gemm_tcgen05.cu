@@ -89,7 +89,7 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   tn = r / gsz;
 }
 
-constexpr int EPI_DISCARD = 6;  // experiment only: drain TMEM, store nothing (AMDP_GEMM_DISCARD)
+constexpr int EPI_DISCARD = 99; // experiment only: drain TMEM, store nothing (AMDP_GEMM_DISCARD)
 
 // Output tensor maps of the pair kernel's TMA epilogue: C (bf16 box {64, 32} or f32 box
 // {32, 32}), C2 (GELU pre-activation), aux (residual / pre-activation input), SWIZZLE_128B.
