@@ -280,6 +280,17 @@ def main():
                               schedule=args.schedule, zero=zero).policy()
             projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
                                     stage_numel=numel, policy=pol)
+            if args.schedule == "AMDP" and zero:
+                # the same measured costs under AMDP's other update mode: replicated weights,
+                # window gradient all-reduced over the stage's devices, every replica stepping
+                # its own optimizer (an Update costs the measured fused optimizer step + the
+                # all-reduce), builder.hpp:306-336
+                alt = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=args.steps,
+                                  schedule="AMDP", zero=False).policy()
+                pa = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
+                                stage_numel=numel, policy=alt)
+                projection["allreduce_update_variant"] = {k: pa[k] for k in
+                                                          ("bubble", "bubble_without_collectives", "tokens_per_s")}
         except Exception as e:  # never let the projection break the bench line
             projection = {"error": str(e)[:200]}
 

@@ -106,6 +106,9 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
                                    zero_enabled=True)
     bubble_nc = None
     devices = depth // 2 if pol.policy == P.Policy.Interleaved1F1B else depth
+    for s in range(depth):  # an Update steps the optimizer: a ZeRO run measured that as Broadcast
+        if (P.Kind.Update, s) not in costs and (P.Kind.Broadcast, s) in costs:
+            costs[(P.Kind.Update, s)] = costs[(P.Kind.Broadcast, s)]
     if stage_numel is not None and replicas_of(pol) > 1:
         rep0 = static_order_replay(pol, depth, costs, gap_ns, devices=devices)
         bubble_nc = float(P.bubble_ratio(rep0, 1 if windows > 2 else 0))
