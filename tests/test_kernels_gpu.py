@@ -174,17 +174,18 @@ def test_gemm_rowdot(K, N, M, N_, K_, seg, seq):
 
 
 @pytest.mark.parametrize("B,S,H,D", [(2, 256, 3, 64), (4, 2048, 2, 128), (1, 512, 2, 80)])
-def test_attention_bwd_supplied_delta(K, B, S, H, D):
+@pytest.mark.parametrize("causal", [True, False])
+def test_attention_bwd_supplied_delta(K, B, S, H, D, causal):
     """amdp_attention_bwd_delta with delta = rowsum(dO * O) from the caller gives the same
     gradients as the self-contained backward (torch fp32 reference as above)."""
     torch.manual_seed(6)
     qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
     dout = torch.randn(B * S, H * D, device="cuda").bfloat16()
-    out, lse = K.attention_fwd(qkv, B, S, H, D, True)
+    out, lse = K.attention_fwd(qkv, B, S, H, D, causal)
     delta = (dout.float() * out.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).contiguous()
-    dqkv = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, True)
+    dqkv = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal)
     x = qkv.float().requires_grad_()
-    _attn_ref(x, B, S, H, D, True).backward(dout.float())
+    _attn_ref(x, B, S, H, D, causal).backward(dout.float())
     torch.cuda.synchronize()
     hd = H * D
     for part in range(3):
