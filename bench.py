@@ -353,6 +353,8 @@ def main():
             "bubble": {"physical_gpu": phys_bubble, "logical_devices_bubble_ratio_w1": logical_bubble,
                        f"projected_d{args.depth}_gpus": projection},
             "kernels": kernels,
+            "memory_gb": {k: (round(v / 1e9, 3) if not k.endswith(("_units", "_slots")) else v)
+                          for k, v in eng.plan()["memory"].items()},
             "clocks": clk.summary()}
     if rank == 0:
         if world == 1:

@@ -204,6 +204,8 @@ class Engine {
   cudaEvent_t run_begin_ = nullptr, run_end_ = nullptr;
   std::vector<cudaEvent_t> stage_ready_;      // weights of stage i usable (after bcast)
   size_t slot_total_ = 0;
+  int64_t measured_alloc_bytes_ = -1;  // cudaMemGetInfo delta across allocate() (-1: plan only)
+  std::string memory_json() const;
   bool plan_only_ = false;
   std::vector<float> loss_scale_;  // per minibatch: 1 / number of labelled tokens
   SideStream side_;                // weight-gradient GEMM stream + events
@@ -346,7 +348,12 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     }
   }
   make_plan();
+  size_t free0 = 0, free1 = 0, total = 0;
+  CUDA_OK(cudaMemGetInfo(&free0, &total));
   allocate();
+  CUDA_OK(cudaStreamSynchronize(cs_));
+  CUDA_OK(cudaMemGetInfo(&free1, &total));
+  measured_alloc_bytes_ = static_cast<int64_t>(free0) - static_cast<int64_t>(free1);
   init_weights();
 }
 
@@ -946,7 +953,8 @@ std::string Engine::plan_json() const {
            ",\"std\":" + std::to_string(ps[k].std) + "}";
     s += "]}";
   }
-  s += "],\"boundary_buffers\":" + std::to_string(nbuf) + ",\"activation_bytes\":" + std::to_string(slot_total_) +
+  s += "],\"memory\":" + memory_json();
+  s += ",\"boundary_buffers\":" + std::to_string(nbuf) + ",\"activation_bytes\":" + std::to_string(slot_total_) +
        ",\"workspace_bytes\":" + std::to_string(GptStage::workspace_bytes(dm)) + ",\"comm_ops\":[";
   bool first = true;
   for (size_t k = 0; k < comm_at_.size(); ++k)
@@ -957,6 +965,44 @@ std::string Engine::plan_json() const {
       first = false;
     }
   return s + "]}";
+}
+
+// What this rank allocates, by category (allocate() below, the same formulas), in the units of
+// the reference's memory model (H/analysis.hpp:226-330: stage replicas, gradient buffers,
+// optimizer-state multiples, live per-stage activations), plus the measured cudaMemGetInfo
+// delta across allocate().  Co-resident replicas of one stage share one set of buffers.
+std::string Engine::memory_json() const {
+  const int64_t T = dm.T, h = dm.h;
+  int64_t w = 0, wt = 0, wver = 0, master = 0, grad = 0, opt = 0, act = 0;
+  int hosted_n = 0, owned_n = 0, slots = 0;
+  for (int i = 0; i < depth_; ++i) {
+    if (!hosted[static_cast<size_t>(i)]) continue;
+    const int64_t n = stages[static_cast<size_t>(i)]->numel();
+    ++hosted_n;
+    w += 2 * n;
+    wt += 2 * n;
+    if (versioned_) wver += 4 * n;
+    master += 4 * n;
+    grad += 4 * n;
+    if (owned[static_cast<size_t>(i)]) {
+      opt += 8 * n;
+      ++owned_n;
+    }
+    slots += slots_per_stage[static_cast<size_t>(i)];
+    act += static_cast<int64_t>(slots_per_stage[static_cast<size_t>(i)]) *
+           static_cast<int64_t>(stages[static_cast<size_t>(i)]->slot_bytes());
+  }
+  const int64_t bounds = static_cast<int64_t>(nbuf) * T * h * 2;
+  const int64_t wsb = static_cast<int64_t>(GptStage::workspace_bytes(dm));
+  const int64_t io = static_cast<int64_t>(M_) * T * 8 + static_cast<int64_t>(M_) * 4;
+  const int64_t total = w + wt + wver + master + grad + opt + act + bounds + wsb + io;
+  auto kv = [](const char* k, int64_t v) { return std::string("\"") + k + "\":" + std::to_string(v); };
+  return "{" + kv("weights_bf16", w) + "," + kv("weights_transposed_bf16", wt) + "," + kv("weight_versions_bf16", wver) +
+         "," + kv("master_fp32", master) + "," + kv("gradient_fp32", grad) + "," + kv("optimizer_state_fp32", opt) +
+         "," + kv("activations", act) + "," + kv("boundary_buffers", bounds) + "," + kv("workspace", wsb) + "," +
+         kv("token_io", io) + "," + kv("total", total) + "," + kv("measured_device_bytes", measured_alloc_bytes_) +
+         "," + kv("weight_units", hosted_n) + "," + kv("gradient_units", hosted_n) + "," +
+         kv("optimizer_state_units", 2 * owned_n) + "," + kv("activation_slots", slots) + "}";
 }
 
 std::string Engine::version_csv() const {

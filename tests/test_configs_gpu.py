@@ -88,5 +88,9 @@ def test_baseline_config_runs(name):
         rep = eng.timeline().report(run.policy(), warmup=0)
         assert rep["causality_issues"] == [] and rep["overlap_issues"] == []
         assert rep["mismatch"]["max_overall"] <= 1
+        # the engine's memory accounting is what the device lost across allocate()
+        # (cudaMemGetInfo moves in 2 MiB pages; one page of slack per allocation)
+        mem = eng.plan()["memory"]
+        assert mem["total"] <= mem["measured_device_bytes"] <= mem["total"] * 1.01 + (256 << 20), mem
     finally:
         eng.close()

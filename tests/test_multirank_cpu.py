@@ -254,3 +254,26 @@ def test_unsupported_schedules_rejected():
         E.Engine(model, E.RunConfig(depth=4, threshold=8, windows=2, plan_only=True, schedule="ZeroBubble"))
     with pytest.raises(RuntimeError):  # AMDP needs an even depth (validate.hpp:60-73)
         E.Engine(model, E.RunConfig(depth=3, threshold=8, windows=2, plan_only=True))
+
+
+@pytest.mark.parametrize("zero", [True, False])
+def test_memory_accounting_matches_reference_model(zero):
+    """what each rank of the 8-GPU 1.3B run allocates, in the units of the
+    reference's memory_report (H/analysis.hpp:226-330) on the same schedule: stage replicas
+    (weights), gradient buffers, optimizer-state multiples (ZeRO: 2 x replicas x 2/d) and live
+    activations.  The executor frees an activation slot at its backward's position in the
+    dispatch order, so it never needs more than the reference's closed-interval peak."""
+    model = E.ModelConfig.gpt_1p3b()
+    for r in range(8):
+        run = E.RunConfig(depth=8, threshold=32, windows=2, world_size=8, rank=r, plan_only=True, zero=zero)
+        eng = E.Engine(model, run)
+        mem = eng.plan()["memory"]
+        ref = P.memory_report(eng.declared_timeline(), run.policy())["per_device"][r]
+        assert mem["weight_units"] == ref["weight"] == 4
+        assert mem["gradient_units"] == ref["gradient"]
+        # ZeRO: the owner's m, v for one stage = 4 replicas x 2 x 2/8; replicated: every replica
+        assert mem["optimizer_state_units"] == ref["optimizer_state"] == (2 if zero else 8)
+        assert 0 < mem["activation_slots"] <= ref["activation_peak"]
+        parts = [k for k in mem if k not in ("total", "measured_device_bytes") and not k.endswith(("_units", "_slots"))]
+        assert mem["total"] == sum(mem[k] for k in parts)
+        assert mem["total"] < 180e9  # fits one B200's HBM
