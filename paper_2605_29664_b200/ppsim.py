@@ -470,3 +470,54 @@ def version_trace_csv(t: Timeline) -> str:
 
 def timeline_json(t: Timeline) -> dict:
     return json.loads(t._text(2))
+
+
+_GANTT_COLOR = {Kind.Forward: "#3b7dd8", Kind.Backward: "#f0a030", Kind.Reduce: "#8a5cc2",
+                Kind.Broadcast: "#3fae7a", Kind.Update: "#d25050"}
+
+
+def gantt_svg(t: Timeline, title: str = "", window_from: Optional[int] = None,
+              window_to: Optional[int] = None) -> str:
+    """SVG Gantt chart of a timeline (the reference's gantt.hpp:36-100 view: one lane per
+    device, one bar per task coloured by kind, preloaded forwards outlined, idle time blank),
+    optionally cut to windows [window_from, window_to].  Deterministic for a given timeline;
+    measured (ns) and declared (rational) timelines render alike."""
+    evs = [e for e in t.flat() if (window_from is None or e.window >= window_from)
+           and (window_to is None or e.window <= window_to)]
+    if not evs:
+        return '<svg xmlns="http://www.w3.org/2000/svg" width="10" height="10"/>\n'
+    t0 = min(float(e.start) for e in evs)
+    t1 = max(float(e.finish()) for e in evs)
+    span = max(t1 - t0, 1e-12)
+    lane, gap, x0, y0, width = 22, 4, 58, 30, 1200
+    height = y0 + t.devices * (lane + gap) + 40
+    sx = width / span
+    out = [f'<svg xmlns="http://www.w3.org/2000/svg" width="{x0 + width + 12}" height="{height}" '
+           f'font-family="sans-serif" font-size="11">',
+           f'<rect x="0" y="0" width="{x0 + width + 12}" height="{height}" fill="white"/>',
+           f'<text x="{x0}" y="16">{title or t.policy.name} - {t.depth} stages on {t.devices} devices, '
+           f'span {span:.6g}</text>']
+    busy = [0.0] * t.devices
+    for e in sorted(evs, key=lambda e: (e.device, e.start, int(e.kind))):
+        d = float(e.duration)
+        if d <= 0:
+            continue
+        busy[e.device] += d
+        x = x0 + (float(e.start) - t0) * sx
+        y = y0 + e.device * (lane + gap)
+        stroke = ' stroke="black" stroke-dasharray="2,2"' if e.preloaded else ""
+        out.append(f'<rect x="{x:.2f}" y="{y}" width="{max(d * sx, 0.5):.2f}" height="{lane}" '
+                   f'fill="{_GANTT_COLOR[e.kind]}"{stroke}><title>{e.kind.name} stage {e.stage} mb '
+                   f'{e.minibatch} pipe {e.pipeline} window {e.window}</title></rect>')
+    for dv in range(t.devices):
+        y = y0 + dv * (lane + gap)
+        out.append(f'<text x="4" y="{y + 15}">dev {dv}</text>')
+        out.append(f'<text x="{x0 + width + 2}" y="{y + 15}" font-size="9">{100 * (1 - busy[dv] / span):.0f}%</text>')
+    lx = x0
+    for k, c in _GANTT_COLOR.items():
+        out.append(f'<rect x="{lx}" y="{height - 24}" width="10" height="10" fill="{c}"/>'
+                   f'<text x="{lx + 14}" y="{height - 15}">{k.name}</text>')
+        lx += 95
+    out.append(f'<text x="{lx + 10}" y="{height - 15}">right margin: idle share per device</text>')
+    out.append("</svg>")
+    return "\n".join(out) + "\n"

@@ -68,3 +68,16 @@ def test_collective_costs_follow_reduce_broadcast_cost():
     assert abs(c[(P.Kind.Reduce, 0)] - 0.75 * 4e6 / 1e12 * 1e9) < 1e-6
     assert c[(P.Kind.Broadcast, 1)] == 2 * c[(P.Kind.Broadcast, 0)]
     assert PR.collective_costs([5], 1) == {(P.Kind.Reduce, 0): 0.0, (P.Kind.Broadcast, 0): 0.0}
+
+
+def test_gantt_svg_renders_every_task():
+    """ppsim.gantt_svg (the gantt.hpp view): valid SVG, one bar per task of non-zero duration,
+    deterministic."""
+    import xml.etree.ElementTree as ET
+    cl = P.ClusterSpec.uniform(4, 4, 1, 2)
+    tl = P.simulate(P.build(P.PolicyConfig(P.Policy.AMDP, 2, 2, 8, 32, True), cl), cl)
+    svg = P.gantt_svg(tl)
+    assert svg == P.gantt_svg(tl)
+    root = ET.fromstring(svg)
+    bars = [r for r in root.iter("{http://www.w3.org/2000/svg}rect") if r.find("{http://www.w3.org/2000/svg}title") is not None]
+    assert len(bars) == sum(1 for e in tl.flat() if e.duration > 0)
