@@ -438,18 +438,41 @@ struct PairSched {
   int tiles_m, tiles_n;
   int full_tiles;   // tiles before the split tail (raster order)
   int tail_split;   // 1, 2 or 4
-  int num_work;     // full_tiles + tail_split * (tiles - full_tiles)
+  int num_work;     // full_tiles + tail_split * (tiles - full_tiles)  (ksplit: + 2 * tail)
   int group_m;      // raster: tile rows per group (L2 reuse of B across consecutive tiles)
+  // Weight-gradient tail (C += A B, fp32): the last partial wave's tiles split into two K
+  // halves, all first halves listed before all second halves.  A second half reduce-adds into
+  // C only after its first half's reduce-add has completed (flag = epoch per (tail tile,
+  // CTA, epilogue warp)), so the fp32 summation order is fixed: (C + P0) + P1.
+  int ksplit;       // 1 or 2
+  int* flags;       // [tail tiles][2][4]
+  int epoch;        // this launch's flag value
 };
 
-// Work item w -> output rows [m0, m0 + 256), columns [n0, n0 + width).
-__device__ __forceinline__ void pair_work(const PairSched& s, int w, int& m0, int& n0, int& width) {
+// Work item w -> output rows [m0, m0 + 256), columns [n0, n0 + width), K blocks [kb0, kb1);
+// khalf: -1 whole K, 0 / 1 first / second half of K-split tail tile `tail` (ksplit = 2).
+__device__ __forceinline__ void pair_work(const PairSched& s, int w, int num_kb, int& m0, int& n0, int& width,
+                                          int& kb0, int& kb1, int& khalf, int& tail) {
   int t = w, part = 0, split = 1;
+  kb0 = 0;
+  kb1 = num_kb;
+  khalf = -1;
+  tail = 0;
   if (w >= s.full_tiles) {
     const int u = w - s.full_tiles;
-    split = s.tail_split;
-    t = s.full_tiles + u / split;
-    part = u % split;
+    if (s.ksplit == 2) {
+      const int ntail = (s.num_work - s.full_tiles) / 2;
+      khalf = u >= ntail ? 1 : 0;
+      tail = u - khalf * ntail;
+      t = s.full_tiles + tail;
+      const int mid = num_kb / 2;
+      kb0 = khalf ? mid : 0;
+      kb1 = khalf ? num_kb : mid;
+    } else {
+      split = s.tail_split;
+      t = s.full_tiles + u / split;
+      part = u % split;
+    }
   }
   int tm, tn;
   tile_coords(t, s.tiles_m, s.tiles_n, tm, tn, s.group_m);
@@ -515,14 +538,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = cluster; w < sc.num_work; w += nclusters) {
-        int m0, n0, width;
-        pair_work(sc, w, m0, n0, width);
+        int m0, n0, width, kb0, kb1, khalf, tail;
+        pair_work(sc, w, num_kb, m0, n0, width, kb0, kb1, khalf, tail);
         const int ma = m0 + 128 * static_cast<int>(rank);
         const int half = width / 2;
         const int nb = n0 + half * static_cast<int>(rank);
         const uint32_t bytes = 2u * (C::A_BYTES + static_cast<uint32_t>(half) * BK * 2);
         const CUtensorMap* mb = (width == PBN || B_MN) ? &map_b : &map_b_tail;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t fb = ptx::mapa(ptx::smem_u32(&full_bar[stage]), 0);
           if (rank == 0) ptx::mbar_arrive_expect_tx_w(&full_bar[stage], bytes);
@@ -552,13 +575,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int w = cluster; w < sc.num_work; w += nclusters) {
-        int m0, n0, width;
-        pair_work(sc, w, m0, n0, width);
+        int m0, n0, width, kb0, kb1, khalf, tail;
+        pair_work(sc, w, num_kb, m0, n0, width, kb0, kb1, khalf, tail);
         const uint32_t idesc = ptx::idesc_bf16_f32(256, width, A_MN, B_MN);
         ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * PBN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
           const uint64_t a0 = ptx::umma_desc_sw128(ptx::smem_u32(smem_a + stage * C::A_BYTES),
@@ -568,7 +591,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             ptx::mma_bf16_ss_pair_w(d_tmem, a0 + ((A_MN ? k * 2048 : k * 32) >> 4),
-                                    b0 + ((B_MN ? k * 2048 : k * 32) >> 4), idesc, (kb | k) != 0 ? 1u : 0u);
+                                    b0 + ((B_MN ? k * 2048 : k * 32) >> 4), idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           ptx::mma_commit_pair_w(&empty_bar[stage], 0x3);
           if (++stage == C::NSTAGE) { stage = 0; phase ^= 1; }
         }
@@ -585,9 +608,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     int bsel = 0;
     uint8_t* stg = stg_all + q * 8192;
     for (int w = cluster; w < sc.num_work; w += nclusters) {
-      int m0, n0, width;
-      pair_work(sc, w, m0, n0, width);
+      int m0, n0, width, kb0, kb1, khalf, tail;
+      pair_work(sc, w, num_kb, m0, n0, width, kb0, kb1, khalf, tail);
       const int row0 = m0 + 128 * static_cast<int>(rank) + q * 32;
+      int* const flag = sc.flags + (tail * 2 + static_cast<int>(rank)) * 4 + q;
+      if (khalf == 1) {  // the first half's reduce-add into these rows has completed
+        if (lane == 0) {
+          while (ptx::ld_acquire_gpu(flag) != sc.epoch) __nanosleep(64);
+          ptx::fence_proxy_async_global();
+        }
+        __syncwarp();
+      }
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * PBN;
@@ -600,6 +631,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive_cluster(acc == 0 ? tempty_leader0 : tempty_leader1);
+      if (khalf == 0 && lane == 0) {  // publish: this warp's reduce-adds are complete
+        ptx::bulk_wait<0>();
+        ptx::fence_proxy_async_global();
+        ptx::st_release_gpu(flag, sc.epoch);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) ptx::bulk_wait<0>();
@@ -678,6 +714,9 @@ PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
   s.group_m = gm > 0 ? gm : GROUP_M;
   s.full_tiles = best == 1 ? T : T - R;
   s.num_work = s.full_tiles + best * (T - s.full_tiles);
+  s.ksplit = 1;
+  s.flags = nullptr;
+  s.epoch = 0;
   return s;
 }
 
@@ -723,7 +762,28 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr_set = true;
   }
   const int pairs = max_pairs<NST>();
-  const PairSched sc = pair_schedule(p.M, p.N, B_MN, pairs);
+  PairSched sc = pair_schedule(p.M, p.N, B_MN, pairs);
+  if constexpr (EPI == AMDP_EPI_ACCUM_F32) {
+    // K-split of a partial last wave that fits in one wave as halves (fc1 / fc2 / LM-head
+    // weight gradients at the 1.3B shapes); deterministic (see PairSched)
+    static const int ks_env = env_int("AMDP_GEMM_KSPLIT", 1);
+    const int T = sc.tiles_m * sc.tiles_n, R = T % pairs, num_kb = p.K / BK;
+    if (ks_env != 0 && sc.tail_split == 1 && T > pairs && R > 0 && 2 * R <= pairs && num_kb >= 8) {
+      static int* flags = nullptr;
+      static int epoch = 0;
+      if (!flags) {
+        if (cudaMalloc(&flags, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
+        if (cudaMemset(flags, 0, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
+      }
+      if (R <= 2048) {
+        sc.ksplit = 2;
+        sc.full_tiles = T - R;
+        sc.num_work = sc.full_tiles + 2 * R;
+        sc.flags = flags;
+        sc.epoch = ++epoch;
+      }
+    }
+  }
   const int grid = 2 * (sc.num_work < pairs ? sc.num_work : pairs);
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(PAIR_THREADS), PairCfg<NST>::SMEM, s, ma, mb, mbt, em, p, sc);
   return e != cudaSuccess ? e : cudaGetLastError();

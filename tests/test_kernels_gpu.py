@@ -74,6 +74,28 @@ def test_gemm_split_tail(K, N, M, N_, K_, a_mn, b_mn, accum):
     assert err < tol, f"max abs err {err}"
 
 
+# Weight-gradient shape with a partial last wave that fits in one wave as K halves (fc1 at
+# 1.3B: 256 tiles on 74 pairs -> 34 tail tiles split in two; LM-head-like 1576 tiles): every
+# element checked, and the fp32 result is bitwise reproducible (the second K half adds after
+# the first, in a fixed order).
+@pytest.mark.parametrize("M,N_,K_", [(8192, 2048, 1024), (2048, 50304, 512)])
+def test_gemm_accum_ksplit_tail_deterministic(K, N, M, N_, K_):
+    torch.manual_seed(9)
+    A = torch.randn(K_, M, device="cuda").bfloat16()   # MN-major (activation gradient^T)
+    B = torch.randn(K_, N_, device="cuda").bfloat16()  # MN-major (activations)
+    C0 = torch.randn(M, N_, device="cuda")
+    ref = C0.double() + (A.double().T @ B.double())
+    outs = []
+    for _ in range(3):
+        C = C0.clone()
+        K.gemm(A, B, M=M, N_=N_, K=K_, a_mn=True, b_mn=True, C=C, epilogue=N.EPI_ACCUM_F32)
+        torch.cuda.synchronize()
+        outs.append(C)
+    err = (outs[0].double() - ref).abs().max().item()
+    assert err < 1e-3 * ref.abs().max().item(), err
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, True)])
 def test_gemm_accum_f32(K, N, a_mn, b_mn):
     torch.manual_seed(1)
