@@ -701,7 +701,9 @@ PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
   const int P = pairs;
   const int R = T % P;
   int best = 1;
-  if (R != 0 && T > P && !b_mn) {
+  // GEMMs with fewer tiles than pairs (BERT-large / 350M shapes) split every tile along N too
+  static const int small_split = env_int("AMDP_GEMM_SMALL_SPLIT", 1);
+  if (R != 0 && (T > P || small_split) && !b_mn) {
     double best_len = 1.0;
     for (int cand = 2; cand <= 4; cand *= 2) {
       const double len = static_cast<double>((cand * R + P - 1) / P) / cand;
