@@ -770,7 +770,8 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     // weight gradients at the 1.3B shapes); deterministic (see PairSched)
     static const int ks_env = env_int("AMDP_GEMM_KSPLIT", 1);
     const int T = sc.tiles_m * sc.tiles_n, R = T % pairs, num_kb = p.K / BK;
-    if (ks_env != 0 && sc.tail_split == 1 && T > pairs && R > 0 && 2 * R <= pairs && num_kb >= 8) {
+    if (ks_env != 0 && sc.tail_split == 1 && (T > pairs || ks_env == 2) && R > 0 && 2 * R <= pairs &&
+        num_kb >= 8) {
       static int* flags = nullptr;
       static int epoch = 0;
       if (!flags) {
