@@ -25,7 +25,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
-LOSS_RTOL = 2e-3        # per-minibatch loss, relative
+LOSS_RTOL = 1e-3        # per-minibatch loss, relative (north_star: 1e-3 in bf16 compute, fp32 accumulation)
 # Final weights, per stage: ||theta_gpu - theta_cpu|| / ||theta_cpu||, and the stricter
 # ||theta_gpu - theta_cpu|| / ||theta_cpu - theta_init|| (error relative to the update).
 # Adam normalises each gradient, so parameters whose gradient is at the noise level of

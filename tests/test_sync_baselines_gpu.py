@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.join(os.path.dirname(HERE), "oracle"))
-LOSS_RTOL = 2e-3
+LOSS_RTOL = 1e-3  # north_star: 1e-3 in bf16 compute with fp32 accumulation
 
 
 def _golden_csv(cfg):
