@@ -47,7 +47,7 @@ def test_tiny_bert_mlm_parity():
     ol, _, seen = O.replay(trace, om, [1, 1, 1, 1], O.Opt("adamw", 1e-3, 0.9, 0.95, 1e-8, 0.0), 8, inputs,
                            labels)
     rel = np.abs(losses - ol) / np.abs(ol)
-    assert rel.max() < 2e-3, rel.max()
+    assert rel.max() < 1e-3, rel.max()  # north_star: 1e-3 (bf16 compute, fp32 accumulation)
     for r in eng.version_trace().strip().split("\n")[1:]:
         dev, kind, stage, mb, pipe, w, pre, ver = r.split(",")
         assert int(ver) == seen[(kind, int(stage), int(mb))]
