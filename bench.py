@@ -172,12 +172,15 @@ def main():
     ap.add_argument("--no-zero", action="store_true",
                     help="AMDP with replicated per-pipeline updates instead of ZeRO reduce/broadcast")
     ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--recompute", action="store_true",
+                    help="backward rebuilds f = gelu(u) and o = attention(qkv) (fits GPT-2.7B D=8 on one GPU)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     model = model_cfg(args.model)
+    model.recompute = bool(args.recompute)
     tok_step = args.threshold * model.tokens_per_minibatch
     npipe = {"AMDP": args.depth // 2, "Chimera": 2}.get(args.schedule, 1)
     zero = args.schedule == "AMDP" and not args.no_zero
@@ -187,7 +190,7 @@ def main():
            "model": ("bert-large" if args.model == "bert" else f"gpt-{args.model}"), "layers": model.layers, "hidden": model.hidden,
            "global_batch": args.threshold * model.seqs_per_minibatch, "seq_len": model.seq,
            "tokens_per_step": tok_step, "parallelism": f"{args.schedule.lower()}{'' if zero or args.schedule != 'AMDP' else '-replicated'}-d{args.depth}-p{npipe} folded on {args.gpus} GPU",
-           "declared_costs": "uniform fwd=1 bwd=1 (preload 1)", "l2": "working set >> L2 (no flush)"}
+           "declared_costs": "uniform fwd=1 bwd=1 (preload 1)", "recompute_f_and_o": bool(args.recompute), "l2": "working set >> L2 (no flush)"}
     metric = "tokens/s AMDP GPT-style training" if args.schedule == "AMDP" else f"tokens/s {args.schedule} GPT-style training"
 
     if args.impl == "reference":

@@ -41,6 +41,10 @@ typedef struct amdp_model_config {
   uint64_t seed;
   /* stage partition: layers_per_stage[depth] (NULL = balanced automatically) */
   const int* layers_per_stage;
+  /* 1 = keep neither f = gelu(u) nor the attention output o per minibatch: the backward
+   * recomputes both from u / qkv (weight-independent, so exact under AMDP's staleness);
+   * activation slots shrink by 5/16.  Weight-gradient GEMMs then run on the compute stream. */
+  int recompute;
 } amdp_model_config;
 
 typedef struct amdp_run_config {

@@ -98,6 +98,8 @@ int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const uint16_t*
 /* ---------------------------------------------------------------- LayerNorm
  * y = (x - mean) * rstd * gamma + beta over rows of width `cols` (bf16 in/out,
  * fp32 gamma/beta/statistics).  mean/rstd: [rows] fp32, saved for backward.        */
+/* f = gelu_tanh(u) elementwise, bf16 in / out (the GEMM GELU epilogue's formula). */
+int amdp_gelu_fwd(const uint16_t* u, uint16_t* f, int64_t n, amdp_stream_t stream);
 int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const float* beta, uint16_t* y,
                        float* mean, float* rstd, int rows, int cols, float eps,
                        amdp_stream_t stream);

@@ -65,6 +65,7 @@ _sig("amdp_attention_bwd_workspace", c_size_t, [c_int, c_int, c_int, c_int])
 _sig("amdp_attention_bwd", c_int,
      [_P, _P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
 _sig("amdp_attention_bwd_delta_supported", c_int, [c_int, c_int])
+_sig("amdp_gelu_fwd", c_int, [_P, _P, c_int64, _P])
 _sig("amdp_attention_bwd_delta", c_int,
      [_P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
 _sig("amdp_layernorm_fwd", c_int, [_P, _P, _P, _P, _P, _P, c_int, c_int, c_float, _P])

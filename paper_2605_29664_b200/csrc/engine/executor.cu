@@ -269,6 +269,7 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   dm.T = dm.B * dm.S;
   dm.causal = mc.causal != 0;
   dm.ln_eps = mc.ln_eps > 0 ? mc.ln_eps : 1e-5f;
+  dm.recompute = mc.recompute != 0;
   if (dm.h % dm.heads != 0) throw std::invalid_argument("engine: hidden must divide into heads");
 
   // schedule: build + order on the declared cost model
@@ -720,7 +721,9 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
       uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
       // the kernel-timing run serialises the streams so per-launch event spans are exact
-      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, ktimer_.enabled ? SideStream{} : side_, &rc);
+      // (recompute: o / f are rebuilt in the shared workspace, so the weight-gradient GEMMs that
+      // read them stay on the compute stream)
+      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, (ktimer_.enabled || dm.recompute) ? SideStream{} : side_, &rc);
     }
     stats.kernels_launched += launched;
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));

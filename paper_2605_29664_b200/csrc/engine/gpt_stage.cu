@@ -133,11 +133,11 @@ size_t GptStage::slot_bytes() const {
     if (l > l0_) c.take<uint16_t>(T * h);  // x
     c.take<uint16_t>(T * h);               // ln1
     c.take<uint16_t>(T * 3 * h);           // qkv
-    c.take<uint16_t>(T * h);               // o
+    if (!d_.recompute) c.take<uint16_t>(T * h);  // o
     c.take<uint16_t>(T * h);               // hmid
     c.take<uint16_t>(T * h);               // ln2
     c.take<uint16_t>(T * d_.ffn);          // u
-    c.take<uint16_t>(T * d_.ffn);          // f
+    if (!d_.recompute) c.take<uint16_t>(T * d_.ffn);  // f
     c.take<float>(T);
     c.take<float>(T);
     c.take<float>(T);
@@ -164,11 +164,11 @@ SlotActs GptStage::carve_slot(uint8_t* base) const {
     if (l > l0_) la.x = c.take<uint16_t>(T * h);
     la.ln1 = c.take<uint16_t>(T * h);
     la.qkv = c.take<uint16_t>(T * 3 * h);
-    la.o = c.take<uint16_t>(T * h);
+    la.o = d_.recompute ? nullptr : c.take<uint16_t>(T * h);
     la.hmid = c.take<uint16_t>(T * h);
     la.ln2 = c.take<uint16_t>(T * h);
     la.u = c.take<uint16_t>(T * d_.ffn);
-    la.f = c.take<uint16_t>(T * d_.ffn);
+    la.f = d_.recompute ? nullptr : c.take<uint16_t>(T * d_.ffn);
     la.ln1_mean = c.take<float>(T);
     la.ln1_rstd = c.take<float>(T);
     la.ln2_mean = c.take<float>(T);
@@ -191,6 +191,7 @@ struct Ws {
   uint16_t *g0, *g1, *dU, *dqkv, *dtmp, *dhmid;
   float* attn;
   uint8_t* ln;
+  uint16_t *rc_o = nullptr, *rc_f = nullptr;  // recompute: this layer's o and f
 };
 Ws carve_ws(const Dims& d, uint8_t* base) {
   Carver c{base};
@@ -204,6 +205,10 @@ Ws carve_ws(const Dims& d, uint8_t* base) {
   w.dhmid = c.take<uint16_t>(T * h);
   w.attn = c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
   w.ln = c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
+  if (d.recompute) {
+    w.rc_o = c.take<uint16_t>(T * h);
+    w.rc_f = c.take<uint16_t>(T * d.ffn);
+  }
   return w;
 }
 }  // namespace
@@ -219,6 +224,10 @@ size_t GptStage::workspace_bytes(const Dims& d) {
   c.take<uint16_t>(T * h);
   c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
   c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
+  if (d.recompute) {
+    c.take<uint16_t>(T * h);
+    c.take<uint16_t>(T * d.ffn);
+  }
   return c.used;
 }
 
@@ -245,8 +254,9 @@ size_t GptStage::workspace_bytes(const Dims& d) {
   } while (0)
 
 int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
-                      const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* /*ws*/,
+                      const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* wsb,
                       cudaStream_t s, int* rc) const {
+  const Ws ws = carve_ws(d_, wsb);
   int launched = 0;
   *rc = 0;
   auto st = reinterpret_cast<amdp_stream_t>(s);
@@ -258,7 +268,11 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
   }
   for (int li = 0; li < l1_ - l0_; ++li) {
     const LayerParams& P = layers_[static_cast<size_t>(li)];
-    const LayerActs& A = a.layers[static_cast<size_t>(li)];
+    LayerActs A = a.layers[static_cast<size_t>(li)];
+    if (d_.recompute) {  // o and f live in the workspace, rebuilt by the backward
+      A.o = ws.rc_o;
+      A.f = ws.rc_f;
+    }
     AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * h, amdp_layernorm_fwd(x, master + P.ln1_g.off, master + P.ln1_b.off, A.ln1, A.ln1_mean,
                                 A.ln1_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm_t(kt, T, 3 * h, h, A.ln1, h, false, w + P.qkv.off, h, false, A.qkv, 3 * h,
@@ -320,9 +334,15 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
   }
   for (int li = l1_ - l0_ - 1; li >= 0; --li) {
     const LayerParams& P = layers_[static_cast<size_t>(li)];
-    const LayerActs& A = a.layers[static_cast<size_t>(li)];
+    LayerActs A = a.layers[static_cast<size_t>(li)];
+    if (d_.recompute) {  // o and f live in the workspace, rebuilt by the backward
+      A.o = ws.rc_o;
+      A.f = ws.rc_f;
+    }
     const uint16_t* x = li > 0 ? A.x : (first() ? a.x0 : in);
     // y = hmid + f W2^T
+    if (d_.recompute)  // f = gelu(u): weight-independent, exact under staleness
+      AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * F, amdp_gelu_fwd(A.u, A.f, static_cast<int64_t>(T) * F, st), 1);
     hand(ss.ev[E_G], s, sd);
     AMDP_GEMM(gemm_t(kt, h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_G], sd);
@@ -341,6 +361,9 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
                                 grad + P.ln2_g.off, grad + P.ln2_b.off, ws.ln, T, h, st), 2);
     hand(ss.ev[E_DH], s, sd);
     // hmid = x + o Wo^T
+    if (d_.recompute)  // o = attention(qkv): deterministic, rewrites the same lse
+      AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd,
+                                                                   d_.causal ? 1 : 0, st), 1);
     AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_DH], sd);
     // dO = dhmid Wo; its epilogue also forms the attention backward's delta = rowsum(dO * O)

@@ -30,6 +30,7 @@ struct Dims {
   int L, h, heads, hd, ffn, V, S, B, T;  // T = B * S tokens per minibatch
   bool causal;
   float ln_eps;
+  bool recompute = false;  // f and o recomputed in the backward (amdp_model_config.recompute)
 };
 
 struct ParamRef {

@@ -475,6 +475,38 @@ static bool ln_row_group_form(int cols) {
   return !off && cols % 256 == 0 && cols >= 256 && cols / 8 <= 512;
 }
 
+namespace amdp {
+namespace {
+__global__ void gelu_fwd_kernel(const bf16* __restrict__ u, bf16* __restrict__ f, int64_t n8) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float v[8];
+    load8(u + i * 8, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float t;
+      const float x = v[e];
+      asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+      v[e] = 0.5f * x * (1.f + t);
+    }
+    store8(f + i * 8, v);
+  }
+}
+}  // namespace
+}  // namespace amdp
+
+extern "C" int amdp_gelu_fwd(const uint16_t* u, uint16_t* f, int64_t n, amdp_stream_t stream) {
+  using namespace amdp;
+  if (n <= 0 || n % 8 != 0) return AMDP_ERR_INVALID;
+  const int64_t n8 = n / 8;
+  const int blocks = static_cast<int>(std::min<int64_t>((n8 + 255) / 256, 8 * num_sms()));
+  launch_pdl(gelu_fwd_kernel, dim3(blocks), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream),
+             reinterpret_cast<const bf16*>(u), reinterpret_cast<bf16*>(f), n8);
+  return cudaGetLastError();
+}
+
 extern "C" int amdp_layernorm_fwd(const uint16_t* x, const float* gamma, const float* beta,
                                   uint16_t* y, float* mean, float* rstd, int rows, int cols,
                                   float eps, amdp_stream_t stream) {

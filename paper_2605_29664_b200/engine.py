@@ -29,7 +29,7 @@ class _Model(Structure):
     _fields_ = [("layers", c_int), ("hidden", c_int), ("heads", c_int), ("ffn", c_int),
                 ("vocab", c_int), ("seq", c_int), ("seqs_per_minibatch", c_int),
                 ("causal", c_int), ("init_std", c_float), ("ln_eps", c_float),
-                ("seed", c_uint64), ("layers_per_stage", POINTER(c_int))]
+                ("seed", c_uint64), ("layers_per_stage", POINTER(c_int)), ("recompute", c_int)]
 
 
 class _Run(Structure):
@@ -94,6 +94,7 @@ class ModelConfig:
     ln_eps: float = 1e-5
     seed: int = 1234
     layers_per_stage: Optional[List[int]] = None
+    recompute: bool = False  # backward rebuilds f = gelu(u) and o = attention(qkv) (amdp_model_config)
 
     @property
     def tokens_per_minibatch(self) -> int:
@@ -130,7 +131,7 @@ class ModelConfig:
             lps = (c_int * len(self.layers_per_stage))(*self.layers_per_stage)
         m = _Model(self.layers, self.hidden, self.heads, self.ffn, self.vocab, self.seq,
                    self.seqs_per_minibatch, int(self.causal), self.init_std, self.ln_eps,
-                   self.seed, lps)
+                   self.seed, lps, int(self.recompute))
         m._keep = lps
         return m
 

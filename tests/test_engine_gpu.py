@@ -140,3 +140,35 @@ def test_measured_timeline_audits(tiny_run):
     st = eng.stats()
     assert st["tasks_executed"] == len(tl.flat())
     assert st["kernels_launched"] > 0
+
+
+def test_recompute_matches_oracle():
+    """model.recompute: the backward rebuilds f = gelu(u) and the attention output from the
+    stored pre-activation / qkv (weight-independent, so exact under the one-step staleness);
+    same version trace, losses and final weights vs the oracle as the stored-activation run."""
+    import gpt_oracle as O
+    from paper_2605_29664_b200 import engine as E
+
+    model = E.ModelConfig.tiny()
+    model.layers_per_stage = [1, 1, 1, 1]
+    model.recompute = True
+    opt = E.OptimizerConfig(kind=3, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0)
+    run = E.RunConfig(depth=4, threshold=8, windows=4, optimizer=opt)
+    eng = E.Engine(model, run)
+    init = [eng.stage_params(i) for i in range(4)]
+    inputs, labels = E.synthetic_tokens(model, run.data_seed, 0, run.num_minibatches)
+    losses = eng.run(inputs, labels)
+    trace = _golden_csv(["AMDP", 4, 4, "1", "1", "0", "0", 2, 2, 8, 32, 1])
+    om = O.Model(4, 128, 4, 512, 1024, 64, 4, True, model.seed)
+    ol, omaster, seen = O.replay(trace, om, [1, 1, 1, 1], O.Opt("adamw", 1e-3, 0.9, 0.95, 1e-8, 0.0), 8, inputs, labels)
+    assert np.max(np.abs(losses - ol) / np.abs(ol)) < LOSS_RTOL
+    rows = eng.version_trace().strip().split("\n")[1:]
+    assert all(int(r.split(",")[-1]) == seen[(r.split(",")[1], int(r.split(",")[2]), int(r.split(",")[3]))] for r in rows)
+    plan = eng.plan()
+    for i in range(4):
+        st = plan["stages"][i]
+        ref = O.flat_stage(omaster[i], st["params"], st["numel"])
+        got = eng.stage_params(i).astype(np.float64)
+        err = np.linalg.norm(got - ref)
+        assert err / np.linalg.norm(ref) < WEIGHT_RTOL["adamw"]
+        assert err / np.linalg.norm(ref - init[i]) < UPDATE_RTOL["adamw"]

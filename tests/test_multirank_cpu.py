@@ -277,3 +277,14 @@ def test_memory_accounting_matches_reference_model(zero):
         parts = [k for k in mem if k not in ("total", "measured_device_bytes") and not k.endswith(("_units", "_slots"))]
         assert mem["total"] == sum(mem[k] for k in parts)
         assert mem["total"] < 180e9  # fits one B200's HBM
+
+
+def test_recompute_fits_2p7b_d8_on_one_gpu():
+    """GPT-2.7B D=8 folded on one GPU: 224 GB planned with stored activations, under the
+    B200's 180 GB once f and o are recomputed (5 of 16 h-widths per layer and slot)."""
+    m = E.ModelConfig.gpt_2p7b()
+    full = E.Engine(m, E.RunConfig(depth=8, threshold=32, windows=2, plan_only=True)).plan()["memory"]
+    m.recompute = True
+    rc = E.Engine(m, E.RunConfig(depth=8, threshold=32, windows=2, plan_only=True)).plan()["memory"]
+    assert full["total"] > 180e9 > rc["total"]
+    assert rc["activations"] < full["activations"] * 0.72
