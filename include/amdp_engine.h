@@ -43,7 +43,7 @@ typedef struct amdp_model_config {
   const int* layers_per_stage;
   /* 1 = keep neither f = gelu(u) nor the attention output o per minibatch: the backward
    * recomputes both from u / qkv (weight-independent, so exact under AMDP's staleness);
-   * activation slots shrink by 5/16.  Weight-gradient GEMMs then run on the compute stream. */
+   * activation slots shrink by 5/16 (the rebuilt o / f live in the shared workspace). */
   int recompute;
 } amdp_model_config;
 

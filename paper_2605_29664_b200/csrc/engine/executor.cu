@@ -721,9 +721,7 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
       uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
       // the kernel-timing run serialises the streams so per-launch event spans are exact
-      // (recompute: o / f are rebuilt in the shared workspace, so the weight-gradient GEMMs that
-      // read them stay on the compute stream)
-      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, (ktimer_.enabled || dm.recompute) ? SideStream{} : side_, &rc);
+      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, ktimer_.enabled ? SideStream{} : side_, &rc);
     }
     stats.kernels_launched += launched;
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));

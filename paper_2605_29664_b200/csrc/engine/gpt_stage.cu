@@ -341,8 +341,11 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     }
     const uint16_t* x = li > 0 ? A.x : (first() ? a.x0 : in);
     // y = hmid + f W2^T
-    if (d_.recompute)  // f = gelu(u): weight-independent, exact under staleness
+    if (d_.recompute) {  // f = gelu(u): weight-independent, exact under staleness
+      // the layer above's fc2 weight gradient (side stream) has finished reading the shared f
+      if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_G], 0);
       AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * F, amdp_gelu_fwd(A.u, A.f, static_cast<int64_t>(T) * F, st), 1);
+    }
     hand(ss.ev[E_G], s, sd);
     AMDP_GEMM(gemm_t(kt, h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_G], sd);
@@ -359,11 +362,14 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DH], 0);  // previous layer's dWo done with dhmid
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, A.hmid, master + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g, ws.dhmid,
                                 grad + P.ln2_g.off, grad + P.ln2_b.off, ws.ln, T, h, st), 2);
-    hand(ss.ev[E_DH], s, sd);
-    // hmid = x + o Wo^T
-    if (d_.recompute)  // o = attention(qkv): deterministic, rewrites the same lse
+    // o = attention(qkv) when recomputing: deterministic (rewrites the same lse), issued before
+    // the hand-off so the side stream's out-proj weight gradient reads the rebuilt o; its
+    // previous reader (the layer above's) finished before F_DH, waited for above
+    if (d_.recompute)
       AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd,
                                                                    d_.causal ? 1 : 0, st), 1);
+    hand(ss.ev[E_DH], s, sd);
+    // hmid = x + o Wo^T
     AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
     if (sd != s) cudaEventRecord(ss.ev[F_DH], sd);
     // dO = dhmid Wo; its epilogue also forms the attention backward's delta = rowsum(dO * O)
