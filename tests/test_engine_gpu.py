@@ -172,3 +172,33 @@ def test_recompute_matches_oracle():
         err = np.linalg.norm(got - ref)
         assert err / np.linalg.norm(ref) < WEIGHT_RTOL["adamw"]
         assert err / np.linalg.norm(ref - init[i]) < UPDATE_RTOL["adamw"]
+
+
+def test_recompute_side_stream_is_race_free(monkeypatch):
+    """With recomputation the rebuilt f / o share one workspace buffer between the compute
+    stream and the weight-gradient side stream; event waits order them.  A run with the side
+    stream must reproduce the serialised run (GPT-350M shapes, 2 windows) up to the
+    run-to-run noise of the atomically summed loss / embedding gradient (~1e-7): a read of a
+    half-rebuilt f or o would move the weight gradients by O(1).""" 
+    from paper_2605_29664_b200 import engine as E
+
+    def run_once(side):
+        if side:
+            monkeypatch.delenv("AMDP_NO_SIDE_STREAM", raising=False)
+        else:
+            monkeypatch.setenv("AMDP_NO_SIDE_STREAM", "1")
+        model = E.ModelConfig.gpt_350m()
+        model.recompute = True
+        run = E.RunConfig(depth=2, threshold=8, windows=2, optimizer=E.OptimizerConfig(lr=1e-4))
+        eng = E.Engine(model, run)
+        inputs, labels = E.synthetic_tokens(model, run.data_seed, 0, run.num_minibatches)
+        losses = eng.run(inputs, labels)
+        w = [eng.stage_params(i) for i in range(2)]
+        eng.close()
+        return losses, w
+
+    l0, w0 = run_once(False)
+    l1, w1 = run_once(True)
+    assert np.max(np.abs(l0 - l1) / np.abs(l0)) < 1e-5
+    for a, b in zip(w0, w1):
+        assert np.linalg.norm(a.astype(np.float64) - b) / np.linalg.norm(a) < 1e-4
