@@ -31,6 +31,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SPEC_BF16_TFLOPS = 2250.0  # dense bf16 tensor-core peak per B200 (spec sheet; 4.5 PF is 2:4 sparse)
 PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -43,10 +44,24 @@ def peaks():
         return dict(PEAK_FALLBACK), "fallback"
 
 
+# Model shapes (layers, hidden, heads, ffn, vocab, seq, causal) — the same as
+# paper_2605_29664_b200.engine.ModelConfig's factories, restated here so that the reference
+# arm (--impl reference) never imports the product package or loads libamdp.so.
+MODELS = {"1p3b": (24, 2048, 16, 8192, 50304, 2048, True), "350m": (24, 1024, 16, 4096, 50304, 1024, True),
+          "2p7b": (32, 2560, 32, 10240, 50304, 2048, True), "bert": (24, 1024, 16, 4096, 30528, 512, False),
+          "tiny": (4, 128, 4, 512, 1024, 64, True)}
+
+
+def flops_per_token(name):
+    """Training FLOPs per token, 6 L (4h^2 + 2 h ffn) + 12 L s h + 6 h V."""
+    L, h, _, f, V, s, _ = MODELS[name]
+    return 6 * L * (4 * h * h + 2 * h * f) + 12 * L * s * h + 6 * h * V
+
+
 def model_cfg(name):
     from paper_2605_29664_b200 import engine as E
-    return {"1p3b": E.ModelConfig.gpt_1p3b, "350m": E.ModelConfig.gpt_350m,
-            "2p7b": E.ModelConfig.gpt_2p7b, "bert": E.ModelConfig.bert_large, "tiny": E.ModelConfig.tiny}[name]()
+    L, h, H, f, V, s, causal = MODELS[name]
+    return E.ModelConfig(L, h, H, f, V, s, causal=causal)
 
 
 class ClockSampler:
@@ -100,41 +115,77 @@ class ClockSampler:
                 "reasons": [n for b, n in names.items() if bits & b and n != "gpu_idle"]}
 
 
-def cpu_port_baseline(model, seconds=12.0):
-    """The CPU restatement (oracle/gpt_oracle.py, numpy fp32, all host threads via BLAS) on a
-    bounded sample: forward + backward of ONE transformer layer of the model on ONE sequence
-    (seq tokens), repeated for ~`seconds`; tokens/s = sample FLOP rate / model FLOPs per token."""
+def _oracle():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
     import gpt_oracle as O
+    return O
 
-    om = O.Model(model.layers, model.hidden, model.heads, model.ffn, model.vocab, model.seq, 1,
-                 True, model.seed)
-    st = O.StageMath(om, 1, 3, 0, 1, emulate_bf16=False)
-    specs = O.stage_param_specs(om, 1, 3, 0, 1)
-    W = {k: v.astype(np.float32) for k, v in O.init_stage(om, specs).items()}
-    rng = np.random.default_rng(0)
-    x = rng.standard_normal((model.seq, model.hidden)).astype(np.float32)
-    g = rng.standard_normal((model.seq, model.hidden)).astype(np.float32) * 1e-3
-    grads = {k: np.zeros_like(v) for k, v in W.items()}
-    st.rb = lambda a: np.asarray(a, np.float32)
-    h, s, f = model.hidden, model.seq, model.ffn
-    flops = 3 * (2 * s * (4 * h * h + 2 * h * f) + 2 * s * s * h)  # fwd+bwd, one layer, one sequence
+
+class LayerSample:
+    """The CPU restatement (oracle/gpt_oracle.py, numpy fp32, all host threads through BLAS) on a
+    bounded sample of the workload: forward + backward of ONE transformer layer of the model on
+    ONE sequence.  Model-equivalent tokens/s = the sample's FLOP rate / the model's FLOPs per
+    token (an extrapolation: kind "port-extrapolated")."""
+
+    def __init__(self, name):
+        import numpy as np
+        O = _oracle()
+        L, h, H, f, V, s, causal = MODELS[name]
+        self.name, self.layers, self.seq = name, L, s
+        om = O.Model(L, h, H, f, V, s, 1, causal, 1234)
+        self.st = O.StageMath(om, 1, 3, 0, 1, emulate_bf16=False)
+        self.st.rb = lambda a: np.asarray(a, np.float32)
+        self.W = {k: v.astype(np.float32) for k, v in O.init_stage(om, O.stage_param_specs(om, 1, 3, 0, 1)).items()}
+        rng = np.random.default_rng(0)
+        self.x = rng.standard_normal((s, h)).astype(np.float32)
+        self.g = rng.standard_normal((s, h)).astype(np.float32) * 1e-3
+        self.grads = {k: np.zeros_like(v) for k, v in self.W.items()}
+        self.flops = 3 * (2 * s * (4 * h * h + 2 * h * f) + 2 * s * s * h)  # fwd+bwd, 1 layer, 1 seq
+
+    def step(self):
+        _, cache, _ = self.st.forward(self.W, self.x, None, None)
+        self.st.backward(self.W, cache, self.g, None, self.grads)
+
+    def describe(self, reps, secs):
+        return (f"numpy fp32 forward+backward of 1 of {self.layers} layers on 1 sequence of {self.seq} tokens "
+                f"x {reps} samples ({secs:.1f} s); model tokens/s = sample FLOP/s / model FLOPs per token "
+                f"({flops_per_token(self.name):.3e})")
+
+
+def cpu_port_baseline(name, seconds=12.0):
+    """Bounded 1-layer sample (LayerSample), repeated for ~`seconds`."""
+    smp = LayerSample(name)
     reps, t0 = 0, time.perf_counter()
     while True:
-        _, cache, _ = st.forward(W, x, None, None)
-        st.backward(W, cache, g, None, grads)
+        smp.step()
         reps += 1
         if time.perf_counter() - t0 > seconds or reps >= 50:
             break
     dt = time.perf_counter() - t0
-    rate = flops * reps / dt
-    return {"value": rate / model.flops_per_token(), "unit": "tokens/s", "cores": os.cpu_count(),
-            "kind": "port",
-            "sample": f"numpy fp32 forward+backward of 1 of {model.layers} layers on 1 sequence of "
-                      f"{model.seq} tokens x {reps} reps ({dt:.1f} s); tokens/s = measured FLOP/s / "
-                      f"model FLOPs per token ({model.flops_per_token():.3e})",
-            "cpu_gflops": rate / 1e9}
+    rate = smp.flops * reps / dt
+    return {"value": rate / flops_per_token(name), "unit": "tokens/s", "cores": os.cpu_count(),
+            "kind": "port-extrapolated", "sample": smp.describe(reps, dt), "cpu_gflops": rate / 1e9}
+
+
+def cpu_schedule_replay():
+    """A real timed run of the reference path on the CPU: the oracle replays the UNMODIFIED
+    reference's AMDP timeline (tests/golden fixture from oracle/_ref/ppsim_ref: tiny GPT,
+    D=4, 2 pipelines, 8 minibatches per window) with the reference's version semantics, every
+    stage forward/backward and the window optimizer steps, fp64 (numpy, all host threads)."""
+    O = _oracle()
+    cfg = ["AMDP", 4, 4, "1", "1", "0", "0", 2, 2, 8, 32, 1]
+    with open(os.path.join(ROOT, "tests", "golden", "sched_golden.json")) as f:
+        trace = next(e["csv"] for e in json.load(f) if e["config"] == cfg)
+    L, h, H, ff, V, s, causal = MODELS["tiny"]
+    om = O.Model(L, h, H, ff, V, s, 4, causal, 1234)
+    M = 8 * 4
+    inputs, labels = O.synthetic_tokens(s, 4, V, 1234, 0, M)
+    t0 = time.perf_counter()
+    O.replay(trace, om, [1, 1, 1, 1], O.Opt("adamw", 1e-3, 0.9, 0.95, 1e-8, 0.0), 8, inputs, labels)
+    dt = time.perf_counter() - t0
+    return {"value": M * om.T / dt, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+            "seconds": dt, "sample": f"oracle replay of the reference AMDP timeline, tiny GPT (L4 h128 seq64), "
+                                     f"D=4, 4 windows x 8 minibatches x {om.T} tokens, fp64, all {M} minibatches"}
 
 
 def schedule_baseline():
@@ -179,36 +230,55 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    model = model_cfg(args.model)
-    model.recompute = bool(args.recompute)
-    tok_step = args.threshold * model.tokens_per_minibatch
+    L, h, H, ffn, V, seq, causal = MODELS[args.model]
+    tokens_per_mb = 4 * seq
+    tok_step = args.threshold * tokens_per_mb
     npipe = {"AMDP": args.depth // 2, "Chimera": 2}.get(args.schedule, 1)
     zero = args.schedule == "AMDP" and not args.no_zero
     cfg = {"workload": f"GPT-style {args.model} {args.schedule} D={args.depth} ({npipe} pipelines), "
-                       f"seq {model.seq}, {model.seqs_per_minibatch} seqs/minibatch, "
-                       f"{args.threshold} minibatches/step",
-           "model": ("bert-large" if args.model == "bert" else f"gpt-{args.model}"), "layers": model.layers, "hidden": model.hidden,
-           "global_batch": args.threshold * model.seqs_per_minibatch, "seq_len": model.seq,
+                       f"seq {seq}, 4 seqs/minibatch, {args.threshold} minibatches/step",
+           "model": ("bert-large" if args.model == "bert" else f"gpt-{args.model}"), "layers": L, "hidden": h,
+           "global_batch": args.threshold * 4, "seq_len": seq,
            "tokens_per_step": tok_step, "parallelism": f"{args.schedule.lower()}{'' if zero or args.schedule != 'AMDP' else '-replicated'}-d{args.depth}-p{npipe} folded on {args.gpus} GPU",
            "declared_costs": "uniform fwd=1 bwd=1 (preload 1)", "recompute_f_and_o": bool(args.recompute), "l2": "working set >> L2 (no flush)"}
     metric = "tokens/s AMDP GPT-style training" if args.schedule == "AMDP" else f"tokens/s {args.schedule} GPT-style training"
 
     if args.impl == "reference":
+        # The reference (ppsim) is a CPU schedule simulator with no model arithmetic; its CPU
+        # path for this metric is the oracle port executing the same GPT stage math.  This arm
+        # imports neither torch nor the product package.
         if rank != 0:
             return
-        cb = cpu_port_baseline(model)
-        sched = schedule_baseline()
-        line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "tokens/s",
+        smp = LayerSample(args.model)
+        for _ in range(args.warmup):
+            smp.step()
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            smp.step()
+            times.append(time.perf_counter() - t0)
+        total = sum(times)
+        value = smp.flops * args.steps / total / flops_per_token(args.model)
+        replay = cpu_schedule_replay()
+        cb = {"value": value, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port-extrapolated",
+              "sample": smp.describe(args.steps, total)}
+        line = {"impl": "reference", "metric": metric, "value": value, "unit": "tokens/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * total / args.steps,
+                "step_definition": "one bounded sample (1 layer x 1 sequence forward+backward) of the workload",
                 "higher_is_better": True, "dtype": "f32", "data": "synthetic", "config": cfg,
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0},
-                "reference_schedule_path": sched,
+                "cpu_baseline": cb,
+                "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "full_schedule_replay": replay,
+                "reference_schedule_path": schedule_baseline(),
                 "note": "the reference (ppsim) has no model arithmetic; its CPU path for tokens/s is "
                         "the oracle port executing the same GPT stage math"}
+        assert "paper_2605_29664_b200" not in sys.modules  # the reference arm never loads libamdp.so
         print(json.dumps(line), flush=True)
         return
+
+    model = model_cfg(args.model)
+    model.recompute = bool(args.recompute)
 
     import numpy as np
     import torch
@@ -340,7 +410,10 @@ def main():
                    "tflops": round(v["flops"] / (v["ms"] / 1e3) / 1e12, 1) if v["flops"] and v["ms"] else None,
                    "gbs": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["bytes"] and v["ms"] else None}
                for k, v in kern.items()}
-    mfu = value * model.flops_per_token() / (args.gpus * peak * 1e12)
+    # MFU against the dense bf16 spec peak (2.25 PF/s per B200); the ratio to the measured,
+    # power-capped sustained cuBLAS rate on this box is reported beside it
+    mfu = value * model.flops_per_token() / (args.gpus * SPEC_BF16_TFLOPS * 1e12)
+    mfu_sustained = value * model.flops_per_token() / (args.gpus * peak * 1e12)
 
     line = {"metric": metric, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
@@ -353,6 +426,7 @@ def main():
             "host_issue_ms_per_step": host_issue_ms / args.steps,
             "roofline": roofline,
             "model_flops_utilization": mfu,
+            "model_flops_vs_measured_sustained_peak": mfu_sustained,
             "bubble": {"physical_gpu": phys_bubble, "logical_devices_bubble_ratio_w1": logical_bubble,
                        f"projected_d{args.depth}_gpus": projection},
             "kernels": kernels,
@@ -361,7 +435,8 @@ def main():
             "clocks": clk.summary()}
     if rank == 0:
         if world == 1:
-            line["cpu_baseline"] = {k: v for k, v in cpu_port_baseline(model).items() if k != "cpu_gflops"}
+            line["cpu_baseline"] = {k: v for k, v in cpu_port_baseline(args.model).items() if k != "cpu_gflops"}
+            line["cpu_baseline"]["full_schedule_replay"] = cpu_schedule_replay()
             sb = schedule_baseline()
             if sb:
                 line["reference_schedule_path"] = sb

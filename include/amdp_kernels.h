@@ -88,6 +88,11 @@ size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim)
  * caller (e.g. from the dO GEMM's AMDP_EPI_ROWDOT epilogue); tcgen05 path only
  * (amdp_attention_bwd_delta_supported), AMDP_ERR_UNSUPPORTED otherwise.             */
 int amdp_attention_bwd_delta_supported(int seq, int head_dim);
+/* Which implementation amdp_attention_fwd (backward = 0) / amdp_attention_bwd (1) dispatches
+ * to for this shape: AMDP_ATTN_IMPL_TCGEN05 (tcgen05/TMEM/TMA), AMDP_ATTN_IMPL_MMA_SYNC
+ * (head_dim 32 or sequence lengths the tensor-core tiles do not divide), -1 unsupported.   */
+enum { AMDP_ATTN_IMPL_MMA_SYNC = 0, AMDP_ATTN_IMPL_TCGEN05 = 1 };
+int amdp_attention_impl(int seq, int head_dim, int backward);
 int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse, const float* delta,
                              uint16_t* dqkv, int batch, int seq, int heads, int head_dim, int causal,
                              amdp_stream_t stream);

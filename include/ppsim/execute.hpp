@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "amdp_engine.h"
@@ -31,6 +32,9 @@ struct ExecuteResult {
   Timeline timeline;          // measured, this rank's logical devices
   std::vector<float> losses;  // per minibatch (valid on the rank hosting the last stage)
   amdp_run_stats stats{};
+  // per-logical-device F/B order with the parameter version each task read on the GPU
+  // (device,kind,stage,minibatch,pipeline,window,preloaded,version; = version_trace_csv)
+  std::string version_trace;
 };
 
 // Throws std::invalid_argument for configurations the executor does not run (non-AMDP

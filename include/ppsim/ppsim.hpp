@@ -161,6 +161,11 @@ struct CommVolume {
   Rat broadcast;
   Rat allreduce;
 };
+// types.hpp:204-207 — outcome of a property check
+struct Verdict {
+  bool pass = false;
+  std::string detail;
+};
 
 // ---- validate.hpp
 PPSIM_API std::vector<std::string> validate_cluster(const ClusterSpec& c);
@@ -189,10 +194,18 @@ PPSIM_API WindowReport window_mismatch(const Timeline& t, int depth);
 PPSIM_API MemoryReport memory_report(const Timeline& t, const PolicyConfig& policy,
                                      const MemoryModel& mem);
 PPSIM_API CommVolume reduce_broadcast_cost(int replicas, const Rat& bytes);
+// analysis.hpp:96-121: PipeDreamAsync steady staleness = min(n, depth - stage) - 1 per stage
+PPSIM_API Verdict verify_steady_mismatch(int depth, int injection_limit);
+// analysis.hpp:161-221: AMDP's one-step bound under random costs, comm gaps, node
+// partitions, device relabelings and ring reflections (deterministic in `seed`)
+PPSIM_API Verdict verify_topology_invariance(int depth, int trials, std::uint64_t seed);
 
-// ---- serialize.hpp (the trace wire format)
+// ---- serialize.hpp (the trace wire format; the nlohmann::ordered_json emitters of the
+// reference — timeline_json, mismatch_json, window_json, memory_json, rat_json — are in
+// ppsim/serialize.hpp, which needs nlohmann/json on the include path like the reference's)
 PPSIM_API std::string timeline_csv(const Timeline& t);
-PPSIM_API std::string timeline_json(const Timeline& t);
+// timeline_json(t).dump() of the reference, as text (no nlohmann dependency)
+PPSIM_API std::string timeline_json_text(const Timeline& t);
 // Version trace: timeline_csv with start/duration dropped and a `version` column
 // (parameter updates of the stage visible to the task) appended.  Byte-comparable
 // between the reference's simulated order and a measured GPU run.

@@ -25,12 +25,29 @@ from __future__ import annotations
 import csv
 import io
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 
 M64 = (1 << 64) - 1
+
+# Elementwise passes over [T, ffn] activations dominate the replay time; numpy ufuncs release
+# the GIL, so they run chunked over the host's cores (the matmuls are already threaded BLAS).
+_NT = max(1, min(32, os.cpu_count() or 1))
+_POOL = ThreadPoolExecutor(_NT) if _NT > 1 else None
+
+
+def _chunked(fn, x, *rest):
+    """fn applied to row chunks of x (and same-shaped arrays in rest); results concatenated."""
+    if _POOL is None or x.ndim == 0 or x.shape[0] < 2 * _NT or x.size < (1 << 16):
+        return fn(x, *rest)
+    edges = np.linspace(0, x.shape[0], _NT + 1).astype(int)
+    parts = list(_POOL.map(lambda k: fn(x[edges[k]:edges[k + 1]], *(r[edges[k]:edges[k + 1]] for r in rest)),
+                           range(_NT)))
+    return np.concatenate(parts, axis=0)
 
 
 # ------------------------------------------------------------------ counter-based RNG
@@ -96,12 +113,21 @@ def normal_init(n: int, seed: int, std: float) -> np.ndarray:
     return (float(np.float32(std)) * z).astype(np.float32)
 
 
+def _bf16(x):
+    a = np.array(x, np.float32, copy=True, order="C")
+    u = a.view(np.uint32)
+    r = (u >> np.uint32(16)) & np.uint32(1)
+    r += np.uint32(0x7FFF)
+    u += r
+    u &= np.uint32(0xFFFF0000)
+    return a
+
+
 def bf16(x):
-    """Round-to-nearest-even to bf16, returned as float32 values."""
-    a = np.ascontiguousarray(np.asarray(x, np.float32))
-    u = a.view(np.uint32).astype(np.uint64)
-    u = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
-    return u.view(np.float32)
+    """Round-to-nearest-even to bf16, returned as float32 values (uint32 arithmetic on a
+    float32 copy; NaN payloads are not preserved)."""
+    x = np.asarray(x)
+    return _chunked(_bf16, x) if x.ndim >= 1 else _bf16(x)
 
 
 # ------------------------------------------------------------------ model
@@ -157,13 +183,23 @@ def init_stage(m: Model, specs) -> Dict[str, np.ndarray]:
     return P
 
 
+def _gelu1(x):
+    x2 = x * x
+    return 0.5 * x * (1.0 + np.tanh(0.7978845608028654 * x * (1.0 + 0.044715 * x2)))
+
+
+def _gelu_grad1(x):
+    x2 = x * x
+    t = np.tanh(0.7978845608028654 * x * (1.0 + 0.044715 * x2))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x2)
+
+
 def _gelu(x):
-    return 0.5 * x * (1.0 + np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+    return _chunked(_gelu1, x)
 
 
 def _gelu_grad(x):
-    t = np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
-    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
+    return _chunked(_gelu_grad1, x)
 
 
 class StageMath:
@@ -185,29 +221,42 @@ class StageMath:
         dx = rstd * (dxh - dxh.mean(-1, keepdims=True) - xh * (dxh * xh).mean(-1, keepdims=True))
         return dx, (dy * xh).sum(0), dy.sum(0)
 
-    def _attn(self, qkv):
+    def _attn_seq(self, qkv):
+        """One sequence: qkv [S, 3hd] -> (o [S, h], p [H, S, S])."""
         m = self.m
-        B, S, H, D = m.seqs, m.seq, m.heads, m.hidden // m.heads
-        q, k, v = qkv.reshape(B, S, 3, H, D).transpose(2, 0, 3, 1, 4)
-        s = q @ k.transpose(0, 1, 3, 2) / math.sqrt(D)
+        S, H, D = m.seq, m.heads, m.hidden // m.heads
+        q, k, v = qkv.reshape(S, 3, H, D).transpose(1, 2, 0, 3)
+        s = q @ k.transpose(0, 2, 1) / math.sqrt(D)
         if m.causal:
             s = np.where(np.triu(np.ones((S, S), bool), 1), -np.inf, s)
         s = s - s.max(-1, keepdims=True)
         p = np.exp(s)
         p /= p.sum(-1, keepdims=True)
-        o = (p @ v).transpose(0, 2, 1, 3).reshape(B * S, H * D)
-        return o, p
+        return (p @ v).transpose(1, 0, 2).reshape(S, H * D), p
+
+    def _attn(self, qkv):
+        m = self.m
+        seqs = qkv.reshape(m.seqs, m.seq, -1)
+        res = list(_POOL.map(self._attn_seq, seqs)) if _POOL else [self._attn_seq(x) for x in seqs]
+        return np.concatenate([r[0] for r in res], 0), np.stack([r[1] for r in res], 0)
+
+    def _attn_bwd_seq(self, qkv, p, do):
+        m = self.m
+        S, H, D = m.seq, m.heads, m.hidden // m.heads
+        q, k, v = qkv.reshape(S, 3, H, D).transpose(1, 2, 0, 3)
+        dO = do.reshape(S, H, D).transpose(1, 0, 2)
+        dv = p.transpose(0, 2, 1) @ dO
+        dp = dO @ v.transpose(0, 2, 1)
+        ds = p * (dp - (dp * p).sum(-1, keepdims=True)) / math.sqrt(D)
+        dq, dk = ds @ k, ds.transpose(0, 2, 1) @ q
+        return np.stack([dq, dk, dv], 0).transpose(2, 0, 1, 3).reshape(S, 3 * H * D)
 
     def _attn_bwd(self, qkv, p, do):
         m = self.m
-        B, S, H, D = m.seqs, m.seq, m.heads, m.hidden // m.heads
-        q, k, v = qkv.reshape(B, S, 3, H, D).transpose(2, 0, 3, 1, 4)
-        dO = do.reshape(B, S, H, D).transpose(0, 2, 1, 3)
-        dv = p.transpose(0, 1, 3, 2) @ dO
-        dp = dO @ v.transpose(0, 1, 3, 2)
-        ds = p * (dp - (dp * p).sum(-1, keepdims=True)) / math.sqrt(D)
-        dq, dk = ds @ k, ds.transpose(0, 1, 3, 2) @ q
-        return np.stack([dq, dk, dv], 0).transpose(1, 3, 0, 2, 4).reshape(B * S, 3 * H * D)
+        args = list(zip(qkv.reshape(m.seqs, m.seq, -1), p, do.reshape(m.seqs, m.seq, -1)))
+        res = list(_POOL.map(lambda a: self._attn_bwd_seq(*a), args)) if _POOL else \
+            [self._attn_bwd_seq(*a) for a in args]
+        return np.concatenate(res, 0)
 
     def forward(self, W, x_in, tokens, labels):
         rb, m = self.rb, self.m

@@ -6,7 +6,7 @@
 //   ppsim_ref <policy> <depth> <devices> <fwd> <bwd> <update> <comm> <inj> <pipes> <thr> <M>
 //             <zero> <mode> [warmup]
 //   costs are "n" or "n/d" (uniform across stages; "a,b,c,..." gives per-stage costs)
-//   mode: csv | summary | bench <reps>
+//   mode: csv | summary | json | bench <reps>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -75,6 +75,13 @@ int main(int argc, char** argv) {
       j["causality_issues"] = validate_causality(tl, cl).size();
       j["overlap_issues"] = validate_non_overlap(tl).size();
       std::puts(j.dump().c_str());
+    } else if (mode == "json") {
+      // the reference's serialize.hpp emitters, one dump() per line
+      auto tl = simulate(build(cfg, cl), cl);
+      std::puts(timeline_json(tl).dump().c_str());
+      std::puts(mismatch_json(mismatch_report(tl)).dump().c_str());
+      std::puts(window_json(window_mismatch(tl, cl.depth)).dump().c_str());
+      std::puts(memory_json(memory_report(tl, cfg, MemoryModel{})).dump().c_str());
     } else if (mode == "bench") {
       // build + simulate + mismatch_report, single-threaded, as the reference runs
       const int reps = argc > 14 ? std::atoi(argv[14]) : 10;

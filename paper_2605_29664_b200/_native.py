@@ -32,6 +32,7 @@ lib = _load()
 # ------------------------------------------------------------------ kernels
 EPI_STORE_BF16, EPI_GELU, EPI_RESIDUAL, EPI_ACCUM_F32, EPI_GELU_BWD, EPI_STORE_F32, EPI_ROWDOT = range(7)
 OPT_SGD, OPT_MOMENTUM, OPT_REF_ADAMTYPE, OPT_ADAMW = range(4)
+ATTN_IMPL_MMA_SYNC, ATTN_IMPL_TCGEN05 = range(2)
 
 
 class GemmArgs(Structure):
@@ -65,6 +66,7 @@ _sig("amdp_attention_bwd_workspace", c_size_t, [c_int, c_int, c_int, c_int])
 _sig("amdp_attention_bwd", c_int,
      [_P, _P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
 _sig("amdp_attention_bwd_delta_supported", c_int, [c_int, c_int])
+_sig("amdp_attention_impl", c_int, [c_int, c_int, c_int])
 _sig("amdp_gelu_fwd", c_int, [_P, _P, c_int64, _P])
 _sig("amdp_attention_bwd_delta", c_int,
      [_P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])

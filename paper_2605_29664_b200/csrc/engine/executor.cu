@@ -1309,6 +1309,7 @@ ExecuteResult execute(const PolicyConfig& cfg, const ClusterSpec& declared, cons
   out.losses.assign(static_cast<std::size_t>(cfg.num_minibatches), 0.f);
   eng.run(inputs, labels, out.losses.data());
   out.stats = eng.stats;
+  out.version_trace = eng.version_csv();
   out.timeline.policy = cfg.policy;
   out.timeline.depth = declared.depth;
   out.timeline.devices = declared.devices;

@@ -609,6 +609,14 @@ extern "C" int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dou
                           causal, reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" int amdp_attention_impl(int seq, int head_dim, int backward) {
+  const bool tc_dim = head_dim == 64 || head_dim == 80 || head_dim == 128;
+  if (seq <= 0 || seq % 64 != 0) return -1;
+  if (tc_dim && seq % (backward ? 128 : 256) == 0) return AMDP_ATTN_IMPL_TCGEN05;
+  if (head_dim == 32 || tc_dim) return AMDP_ATTN_IMPL_MMA_SYNC;
+  return -1;
+}
+
 extern "C" int amdp_attention_bwd_delta_supported(int seq, int head_dim) {
   return (head_dim == 64 || head_dim == 80 || head_dim == 128) && seq > 0 && seq % 128 == 0;
 }

@@ -4,7 +4,10 @@
 // and the trace emitters (serialize.hpp:41-94).
 #include <algorithm>
 #include <map>
+#include <numeric>
+#include <random>
 #include <set>
+#include <sstream>
 #include <stdexcept>
 
 #include "ppsim/ppsim.hpp"
@@ -245,6 +248,83 @@ CommVolume reduce_broadcast_cost(int replicas, const Rat& bytes) {
 }
 
 // ------------------------------------------------------------------ emitters
+// Property check of analysis.hpp:96-121: a PipeDreamAsync pipeline (update after every
+// backward) with at most n minibatches in flight shows min(n, depth - i) - 1 parameter changes
+// between F(i, j) and B(i, j) for every steady minibatch j (ramp-up / drain: the first and last
+// `depth` minibatches, excluded).
+Verdict verify_steady_mismatch(int depth, int injection_limit) {
+  if (injection_limit < 1 || injection_limit > depth) return {false, "injection limit must lie in [1, depth]"};
+  const ClusterSpec cl = ClusterSpec::uniform(depth, depth, Rat(1), Rat(1));
+  PolicyConfig cfg;
+  cfg.policy = Policy::PipeDreamAsync;
+  cfg.injection_limit = injection_limit;
+  cfg.num_minibatches = 4 * depth;
+  const MismatchReport rep = mismatch_report(simulate(build(cfg, cl), cl));
+  for (int i = 0; i < depth; ++i) {
+    const int expect = std::min(injection_limit, depth - i) - 1;
+    for (int j = depth; j < 3 * depth; ++j) {
+      const auto it = rep.entries.find({i, j});
+      const std::string where = "stage " + std::to_string(i) + " minibatch " + std::to_string(j);
+      if (it == rep.entries.end()) return {false, "no measurement for " + where};
+      if (it->second != expect)
+        return {false, where + ": measured " + std::to_string(it->second) + ", predicted " + std::to_string(expect)};
+    }
+  }
+  return {true, "steady mismatch matches min(n, depth - stage) - 1 at every stage"};
+}
+
+// Property check of analysis.hpp:161-221: AMDP's one-step staleness bound comes from the
+// dependency edges alone, so it must hold for any declared costs, cross-device / cross-node
+// gaps, node partition, device relabeling and ring reflection.  Each trial draws all of them
+// from `seed` (std::mt19937_64) and re-simulates.
+Verdict verify_topology_invariance(int depth, int trials, std::uint64_t seed) {
+  if (depth < 2 || depth % 2 != 0) return {false, "depth must be even and at least 2"};
+  std::mt19937_64 rng(seed);
+  auto pick = [&](int lo, int hi) { return lo + static_cast<int>(rng() % static_cast<std::uint64_t>(hi - lo + 1)); };
+  auto shuffled = [&]() {
+    std::vector<int> v(static_cast<std::size_t>(depth));
+    std::iota(v.begin(), v.end(), 0);
+    for (std::size_t k = v.size(); k > 1; --k) std::swap(v[k - 1], v[rng() % k]);
+    return v;
+  };
+  for (int trial = 0; trial < trials; ++trial) {
+    ClusterSpec cl = ClusterSpec::uniform(depth, depth, Rat(1), Rat(1));
+    for (int i = 0; i < depth; ++i) {
+      cl.fwd_cost[static_cast<std::size_t>(i)] = Rat(pick(1, 4));
+      cl.bwd_cost[static_cast<std::size_t>(i)] = Rat(pick(1, 8));
+    }
+    cl.comm_cost = Rat(pick(1, 8), pick(1, 4));
+    cl.update_cost = Rat(pick(0, 2), 2);
+    const std::vector<int> order = shuffled();
+    const int nodes = pick(1, 4);
+    cl.nodes.assign(static_cast<std::size_t>(std::min(nodes, depth)), {});
+    for (std::size_t k = 0; k < order.size(); ++k) cl.nodes[k % cl.nodes.size()].push_back(order[k]);
+    cl.inter_node_cost = Rat(pick(1, 6), pick(1, 2));
+    PolicyConfig cfg;
+    cfg.policy = Policy::AMDP;
+    cfg.injection_limit = 2;
+    cfg.num_pipelines = depth / 2;
+    cfg.accumulation_threshold = depth;
+    cfg.num_minibatches = 3 * depth;
+    cfg.zero_enabled = rng() % 2 == 0;
+    TaskGraph g = build(cfg, cl);
+    const std::vector<int> perm = shuffled();
+    const bool reflect = rng() % 2 == 1;
+    for (Task& task : g.tasks)
+      task.device = perm[static_cast<std::size_t>(reflect ? depth - 1 - task.device : task.device)];
+    const MismatchReport rep = mismatch_report(simulate(g, cl));
+    if (rep.max_overall() > 1) {
+      std::ostringstream os;
+      os << "trial " << trial << " (seed " << seed << "): max mismatch " << rep.max_overall() << " with comm_cost "
+         << cl.comm_cost.str() << ", reflect " << reflect << ", zero " << cfg.zero_enabled << ", perm";
+      for (int v : perm) os << ' ' << v;
+      return {false, os.str()};
+    }
+    if (!rep.missing.empty()) return {false, "trial " + std::to_string(trial) + ": incomplete forward/backward pairs"};
+  }
+  return {true, std::to_string(trials) + " perturbed runs kept max mismatch <= 1"};
+}
+
 std::string timeline_csv(const Timeline& t) {
   std::string s = "device,kind,stage,minibatch,pipeline,window,preloaded,start,duration\n";
   s.reserve(64 * 1024);
@@ -282,7 +362,7 @@ namespace {
 std::string rat_j(const Rat& r) { return r.den() == 1 ? std::to_string(r.num()) : "\"" + r.str() + "\""; }
 }  // namespace
 
-std::string timeline_json(const Timeline& t) {
+std::string timeline_json_text(const Timeline& t) {
   std::string s = "{\"policy\":\"" + std::string(policy_name(t.policy)) +
                   "\",\"depth\":" + std::to_string(t.depth) + ",\"devices\":" + std::to_string(t.devices) +
                   ",\"threshold\":" + std::to_string(t.threshold) + ",\"makespan\":" + rat_j(t.makespan) +

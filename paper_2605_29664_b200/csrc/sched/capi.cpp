@@ -350,7 +350,7 @@ size_t amdp_schedule_text(const amdp_schedule* s, int which, char* buf, size_t l
   switch (which) {
     case AMDP_TEXT_TIMELINE_CSV: return put_text(timeline_csv(h->tl), buf, len);
     case AMDP_TEXT_VERSION_CSV: return put_text(version_trace_csv(h->tl), buf, len);
-    case AMDP_TEXT_TIMELINE_JSON: return put_text(timeline_json(h->tl), buf, len);
+    case AMDP_TEXT_TIMELINE_JSON: return put_text(timeline_json_text(h->tl), buf, len);
   }
   return put_text("", buf, len);
 }

@@ -46,6 +46,16 @@ CONFIGS += [
     ("Interleaved1F1B", 4, 2, "1", "1", "0", "0", 8, 1, 8, 32, 0),    # two chunks per device
     ("PipeDreamAsync", 4, 4, "1", "1", "0", "0", 4, 1, 8, 32, 0),     # update per backward
 ]
+# Production-shaped engine-vs-oracle parity runs (tests/test_parity_prod_gpu.py): the trace is
+# stored for each (declared 1:1 -> preload 1; declared 1:2 -> preload 2, the reference's
+# canonical manifests/amdp_d8.json cost model), ZeRO and replicated.
+PARITY = [
+    ("AMDP", 4, 4, "1", "1", "0", "0", 2, 2, 8, 24, 1),
+    ("AMDP", 4, 4, "1", "2", "0", "0", 2, 2, 8, 24, 0),
+    ("AMDP", 8, 8, "1", "2", "0", "0", 2, 4, 16, 32, 1),
+    ("AMDP", 8, 8, "1", "1", "0", "0", 2, 4, 16, 32, 0),
+]
+CONFIGS += PARITY
 
 
 def run(cfg, mode):
@@ -67,7 +77,7 @@ def main():
                  "mismatch_nonzero": [[e["stage"], e["minibatch"], e["updates_between"]]
                                       for e in summ["mismatch"]["entries"] if e["updates_between"]],
                  "windows": summ["windows"], "memory": summ["memory"]}
-        if cfg[1] <= 4 and cfg[10] <= 32:
+        if (cfg[1] <= 4 and cfg[10] <= 32) or cfg in PARITY:
             entry["csv"] = csv
         out.append(entry)
     with open(os.path.join(HERE, "sched_golden.json"), "w") as f:
