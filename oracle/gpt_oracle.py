@@ -279,7 +279,8 @@ class StageMath:
             a2, c["mu2"], c["r2"] = self._ln(hm, W[p + "ln2.gamma"], W[p + "ln2.beta"])
             c["ln2"] = a2 = rb(a2)
             u = a2 @ W[p + "mlp.fc1"].T
-            c["u"], c["f"] = rb(u), rb(_gelu(u))
+            c["u"] = rb(u)
+            c["f"] = rb(_gelu(c["u"]))  # of the stored (bf16) pre-activation, as the fc1 epilogue
             x = rb(hm + c["f"] @ W[p + "mlp.fc2"].T)
             cache["layers"].append(c)
         loss = None

@@ -344,7 +344,7 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     if (d_.recompute) {  // f = gelu(u): weight-independent, exact under staleness
       // the layer above's fc2 weight gradient (side stream) has finished reading the shared f
       if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_G], 0);
-      AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * F, amdp_gelu_fwd(A.u, A.f, static_cast<int64_t>(T) * F, st), 1);
+      AMDP_TRY(K_GELU, 0, 4.0 * T * F, amdp_gelu_fwd(A.u, A.f, static_cast<int64_t>(T) * F, st), 1);
     }
     hand(ss.ev[E_G], s, sd);
     AMDP_GEMM(gemm_t(kt, h, F, T, g, h, true, A.f, F, true, grad + P.fc2.off, F, AMDP_EPI_ACCUM_F32, sd), 1);

@@ -21,12 +21,13 @@ enum KClass : int {
   K_XENT,
   K_EMBED,
   K_OPTIM,
+  K_GELU,  // recompute runs only: f = gelu(u) rebuilt by the backward
   K_NUM
 };
 
 inline const char* kclass_name(int c) {
   static const char* n[] = {"gemm_fwd", "gemm_dgrad", "gemm_wgrad", "attn_fwd", "attn_bwd",
-                            "layernorm", "xent", "embedding", "optimizer"};
+                            "layernorm", "xent", "embedding", "optimizer", "gelu"};
   return c >= 0 && c < K_NUM ? n[c] : "?";
 }
 

@@ -680,14 +680,15 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
     return AMDP_ERR_TMA;
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
-  static bool attr = false;
+  static std::atomic<uint64_t> attr{0};
   const size_t smem_kv = KvSmem<D>::BYTES + 1024, smem_q = QSmem<D>::BYTES + 1024;
-  if (!attr) {
+  if (first_on_device(attr)) {
     int e = set_smem(fa_bwd_dkdv_kernel<D>, smem_kv);
-    if (e) return e;
-    e = set_smem(fa_bwd_dq_kernel<D>, smem_q);
-    if (e) return e;
-    attr = true;
+    if (!e) e = set_smem(fa_bwd_dq_kernel<D>, smem_q);
+    if (e) {
+      attr.store(0);
+      return e;
+    }
   }
   const int nt = S / 128;
   const int kv_grid = std::min(nt * H * B, num_sms());  // persistent

@@ -457,11 +457,13 @@ int launch_fa_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, i
     return AMDP_ERR_TMA;
   const size_t smem = FaSmem<D>::BYTES + 1024;
   auto k = fa_fwd_tc_kernel<D>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    attr = true;
+    if (e != cudaSuccess) {
+      attr.store(0);
+      return e;
+    }
   }
   const int n_qt = S / FA_BQ;
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));

@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <utility>
@@ -43,6 +44,19 @@ __device__ __forceinline__ void store8(bf16* p, const float (&f)[8]) {
   *reinterpret_cast<uint4*>(p) = q;
 }
 
+// tanh-GELU of the bf16-rounded pre-activation, with every operation spelled out (no FMA
+// contraction choices left to the compiler), shared by the fc1 GEMM epilogue and the
+// recompute kernel so that the recomputed f = gelu(u) is bit-identical to the stored one.
+// tanh on the SFU (tanh.approx.f32, max rel. error ~2^-11); the result is rounded to bf16.
+__device__ __forceinline__ float gelu_tanh_bf16in(float acc) {
+  const float x = __bfloat162float(__float2bfloat16_rn(acc));
+  const float x3 = __fmul_rn(__fmul_rn(x, x), x);
+  const float arg = __fmul_rn(0.7978845608028654f, __fmaf_rn(0.044715f, x3, x));
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(arg));
+  return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.f, t));
+}
+
 // splitmix64: the counter-based generator shared with the CPU oracle
 // (oracle/gpt_oracle.py restates it bit-for-bit).
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -77,6 +91,15 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Per-device one-time flag (function attributes are per device): true the first time it is
+// called for (key, current device).  key: a distinct static object per kernel instantiation.
+inline bool first_on_device(std::atomic<uint64_t>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  const uint64_t bit = 1ull << dev;
+  return (mask.fetch_or(bit) & bit) == 0;
 }
 
 inline int num_sms() {

@@ -23,9 +23,11 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "amdp_kernels.h"
 #include "common.cuh"
@@ -66,11 +68,6 @@ __device__ __forceinline__ float tanh_fast(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-__device__ __forceinline__ float gelu_tanh(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  float t = tanh_fast(k0 * (x + k1 * x * x * x));
-  return 0.5f * x * (1.f + t);
 }
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -212,7 +209,7 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
         if (lane == 0) ptx::bulk_wait_read<1>();
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 64; ++j) v[j] = gelu_tanh(v[j]);
+        for (int j = 0; j < 64; ++j) v[j] = gelu_tanh_bf16in(v[j]);  // of the stored u
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -682,6 +679,16 @@ bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer
 
 int g_num_sms = 0;
 
+// Launch state that is per device (function attributes, occupancy, the K-split flag buffer),
+// keyed by the current device ordinal; thread-safe.
+constexpr int kMaxDevices = 64;
+int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+std::mutex g_dev_mu;
+
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
@@ -726,7 +733,9 @@ PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
 // so this may be below #SMs / 2); the persistent grid never exceeds it.
 template <int NST>
 int max_pairs() {
-  static int pairs = 0;
+  static std::atomic<int> pairs_of[kMaxDevices];
+  std::atomic<int>& pairs_a = pairs_of[current_device()];
+  int pairs = pairs_a.load();
   if (pairs == 0) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr;
@@ -747,6 +756,7 @@ int max_pairs() {
       n = g_num_sms / 2;
     }
     pairs = n < g_num_sms / 2 ? n : g_num_sms / 2;
+    pairs_a.store(pairs);
     if (getenv("AMDP_GEMM_DEBUG")) fprintf(stderr, "amdp_gemm: %d co-resident CTA pairs (NST=%d)\n", pairs, NST);
   }
   return pairs;
@@ -756,12 +766,13 @@ template <bool A_MN, bool B_MN, int EPI, int NST>
 int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbt, const EpiMaps& em,
                 const EpiParams& p, cudaStream_t s) {
   auto kern = gemm_bf16_tc_pair<A_MN, B_MN, EPI, NST>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  const int dev = current_device();
+  static std::atomic<bool> attr_set[kMaxDevices];
+  if (!attr_set[dev].load()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(PairCfg<NST>::SMEM));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[dev].store(true);
   }
   const int pairs = max_pairs<NST>();
   PairSched sc = pair_schedule(p.M, p.N, B_MN, pairs);
@@ -772,18 +783,25 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     const int T = sc.tiles_m * sc.tiles_n, R = T % pairs, num_kb = p.K / BK;
     if (ks_env != 0 && sc.tail_split == 1 && (T > pairs || ks_env == 2) && R > 0 && 2 * R <= pairs &&
         num_kb >= 8) {
-      static int* flags = nullptr;
-      static int epoch = 0;
-      if (!flags) {
-        if (cudaMalloc(&flags, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
-        if (cudaMemset(flags, 0, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
+      // one flag buffer per device; K-split GEMMs of a device are issued on one stream (the
+      // executor's weight-gradient stream), so consecutive launches are ordered by the epoch
+      static int* flags_of[kMaxDevices];
+      static std::atomic<int> epoch_of[kMaxDevices];
+      int* flags;
+      {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        if (!flags_of[dev]) {
+          if (cudaMalloc(&flags_of[dev], 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
+          if (cudaMemset(flags_of[dev], 0, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
+        }
+        flags = flags_of[dev];
       }
       if (R <= 2048) {
         sc.ksplit = 2;
         sc.full_tiles = T - R;
         sc.num_work = sc.full_tiles + 2 * R;
         sc.flags = flags;
-        sc.epoch = ++epoch;
+        sc.epoch = ++epoch_of[dev];
       }
     }
   }
@@ -798,12 +816,13 @@ int launch(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
            const EpiParams& p, cudaStream_t s) {
   if (mode == 0) {
     auto kern = gemm_bf16_tcgen05<A_MN, B_MN, EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<bool> attr_set[kMaxDevices];
+    const int dev = current_device();
+    if (!attr_set[dev].load()) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(SMEM_BYTES));
       if (e != cudaSuccess) return e;
-      attr_set = true;
+      attr_set[dev].store(true);
     }
     const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
     const int grid = tiles < g_num_sms ? tiles : g_num_sms;

@@ -485,12 +485,7 @@ __global__ void gelu_fwd_kernel(const bf16* __restrict__ u, bf16* __restrict__ f
     float v[8];
     load8(u + i * 8, v);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      float t;
-      const float x = v[e];
-      asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.7978845608028654f * (x + 0.044715f * x * x * x)));
-      v[e] = 0.5f * x * (1.f + t);
-    }
+    for (int e = 0; e < 8; ++e) v[e] = gelu_tanh_bf16in(v[e]);  // same bits as the fc1 epilogue
     store8(f + i * 8, v);
   }
 }

@@ -47,6 +47,9 @@ __device__ __forceinline__ void opt_elem(const OptK& o, float& th, float& m, flo
   }
 }
 
+// USE_M / USE_V: whether the rule keeps momentum / second moment.  Unused state is neither
+// read nor written (its pointer may be null), so no buffer is ever aliased.
+template <bool USE_M, bool USE_V>
 __global__ void __launch_bounds__(256) opt_kernel(OptK o, float* __restrict__ theta,
                                                   float* __restrict__ m, float* __restrict__ v,
                                                   float* __restrict__ grad, bf16* __restrict__ w,
@@ -58,16 +61,16 @@ __global__ void __launch_bounds__(256) opt_kernel(OptK o, float* __restrict__ th
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += stride) {
     float4 t = reinterpret_cast<float4*>(theta)[i];
-    float4 mm = reinterpret_cast<float4*>(m)[i];
-    float4 vv = reinterpret_cast<float4*>(v)[i];
+    float4 mm = USE_M ? reinterpret_cast<float4*>(m)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 vv = USE_V ? reinterpret_cast<float4*>(v)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     float4 g = reinterpret_cast<float4*>(grad)[i];
     opt_elem(o, t.x, mm.x, vv.x, g.x);
     opt_elem(o, t.y, mm.y, vv.y, g.y);
     opt_elem(o, t.z, mm.z, vv.z, g.z);
     opt_elem(o, t.w, mm.w, vv.w, g.w);
     reinterpret_cast<float4*>(theta)[i] = t;
-    reinterpret_cast<float4*>(m)[i] = mm;
-    reinterpret_cast<float4*>(v)[i] = vv;
+    if (USE_M) reinterpret_cast<float4*>(m)[i] = mm;
+    if (USE_V) reinterpret_cast<float4*>(v)[i] = vv;
     reinterpret_cast<float4*>(grad)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __nv_bfloat162 lo = __floats2bfloat162_rn(t.x, t.y), hi = __floats2bfloat162_rn(t.z, t.w);
     uint2 packed;
@@ -78,11 +81,11 @@ __global__ void __launch_bounds__(256) opt_kernel(OptK o, float* __restrict__ th
   // tail
   for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += stride) {
-    float t = theta[i], mm = m[i], vv = v[i];
+    float t = theta[i], mm = USE_M ? m[i] : 0.f, vv = USE_V ? v[i] : 0.f;
     opt_elem(o, t, mm, vv, grad[i]);
     theta[i] = t;
-    m[i] = mm;
-    v[i] = vv;
+    if (USE_M) m[i] = mm;
+    if (USE_V) v[i] = vv;
     grad[i] = 0.f;
     w[i] = __float2bfloat16_rn(t);
   }
@@ -148,6 +151,8 @@ extern "C" int amdp_optimizer_step(const amdp_opt_args* a, float* master, float*
   if ((a->kind == AMDP_OPT_REF_ADAMTYPE || a->kind == AMDP_OPT_ADAMW) && !v)
     return AMDP_ERR_INVALID;
   if (n == 0) return 0;
+  if (a->kind == AMDP_OPT_SGD) m = nullptr;
+  if (a->kind == AMDP_OPT_SGD || a->kind == AMDP_OPT_MOMENTUM) v = nullptr;
   if ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(grad) |
        reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) % 16 != 0 ||
       reinterpret_cast<uintptr_t>(weight_bf16) % 8 != 0)
@@ -165,11 +170,15 @@ extern "C" int amdp_optimizer_step(const amdp_opt_args* a, float* master, float*
   const int step = a->step < 1 ? 1 : a->step;
   o.bc1 = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(a->beta1), step)));
   o.bc2 = static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(a->beta2), step)));
-  // SGD never touches m/v; keep the kernel branch-free on pointer validity.
-  float* mm = m ? m : grad;
-  float* vv = v ? v : grad;
-  launch_pdl(opt_kernel, dim3(grid_for(n / 4 + 1, 8)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), 
-      o, master, mm, vv, grad, reinterpret_cast<bf16*>(weight_bf16), n);
+  const dim3 grid(grid_for(n / 4 + 1, 8));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  bf16* w = reinterpret_cast<bf16*>(weight_bf16);
+  if (a->kind == AMDP_OPT_SGD)
+    launch_pdl(opt_kernel<false, false>, grid, dim3(256), 0, s, o, master, nullptr, nullptr, grad, w, n);
+  else if (a->kind == AMDP_OPT_MOMENTUM)
+    launch_pdl(opt_kernel<true, false>, grid, dim3(256), 0, s, o, master, m, nullptr, grad, w, n);
+  else
+    launch_pdl(opt_kernel<true, true>, grid, dim3(256), 0, s, o, master, m, v, grad, w, n);
   return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 Tolerances are stated per test: bf16 outputs carry ~2^-8 relative rounding, fp32
 accumulation order differs from torch's.
 """
+import ctypes
 import math
 
 import pytest
@@ -138,6 +139,26 @@ def test_gemm_gelu_residual_gelubwd(K, N):
     C = K.gemm(A, B, M=M, N_=N_, K=K_, epilogue=N.EPI_GELU_BWD, aux=U, ld_aux=N_)
     torch.cuda.synchronize()
     assert _rel(C, x.grad) < 1e-2
+
+
+@pytest.mark.parametrize("shape", [(512, 768, 256), (2048, 2048, 1024)])
+def test_recompute_gelu_bit_identical_to_epilogue(K, N, shape):
+    """The recompute path's f = gelu(u) (amdp_gelu_fwd on the stored bf16 pre-activation) is
+    bit-identical to the fc1 GEMM epilogue's f: both take gelu of the bf16-rounded u with the
+    same spelled-out operations, so recomputation changes no bit of the backward's inputs."""
+    torch.manual_seed(3)
+    M, N_, K_ = shape
+    A = (0.05 * torch.randn(M, K_, device="cuda")).bfloat16()
+    B = torch.randn(N_, K_, device="cuda").bfloat16()
+    u = torch.empty(M, N_, dtype=torch.bfloat16, device="cuda")
+    f_epi = K.gemm(A, B, M=M, N_=N_, K=K_, epilogue=N.EPI_GELU, C2=u, ldc2=N_)
+    f_re = torch.empty_like(f_epi)
+    N.check(N.lib.amdp_gelu_fwd(ctypes.c_void_p(u.data_ptr()), ctypes.c_void_p(f_re.data_ptr()),
+                                ctypes.c_int64(M * N_), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)),
+            "amdp_gelu_fwd")
+    torch.cuda.synchronize()
+    assert torch.equal(f_epi.view(torch.int16), f_re.view(torch.int16))
+    assert _rel(f_re, _gelu(u.float())) < 1e-2
 
 
 def _attn_ref(qkv, B, S, H, D, causal):
