@@ -223,6 +223,8 @@ def main():
     ap.add_argument("--no-zero", action="store_true",
                     help="AMDP with replicated per-pipeline updates instead of ZeRO reduce/broadcast")
     ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--comm", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1 data plane: this library's CUDA-IPC peer-memory backend or NCCL")
     ap.add_argument("--recompute", action="store_true",
                     help="backward rebuilds f = gelu(u) and o = attention(qkv) (fits GPT-2.7B D=8 on one GPU)")
     args = ap.parse_args()
@@ -289,9 +291,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [E.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        if args.comm == "nccl":
+            obj = [E.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
 
     def barrier():
         if dist is not None:
@@ -315,8 +318,8 @@ def main():
     windows = max(args.steps, args.warmup)
     opt = E.OptimizerConfig(lr=1e-4, weight_decay=0.0)
     run = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=windows, optimizer=opt, schedule=args.schedule,
-                      zero=zero, world_size=world, rank=rank)
-    eng = E.Engine(model, run, nccl_id)
+                      zero=zero, world_size=world, rank=rank, comm=args.comm)
+    eng = E.Engine(model, run, nccl_id, allgather=E.torch_allgather() if world > 1 else None)
     M = run.num_minibatches
     toks = E.PinnedTokens(M, model.tokens_per_minibatch)
     E.synthetic_tokens(model, run.data_seed, 0, M, out=toks)

@@ -60,7 +60,13 @@ typedef struct amdp_run_config {
   int depth;                   /* stages = devices; 0 = 2 x num_pipelines (AMDP).  */
                                /* Policies: AMDP (ZeRO on), or DAPPLE / GPipe with */
                                /* one pipeline and per-window Update tasks         */
+  int comm_backend;            /* world_size > 1: AMDP_COMM_IPC (default, this     */
+                               /* library's peer-memory data plane; also several   */
+                               /* ranks on one GPU) or AMDP_COMM_NCCL              */
 } amdp_run_config;
+
+#define AMDP_COMM_IPC 0
+#define AMDP_COMM_NCCL 1
 
 typedef struct amdp_engine amdp_engine;
 
@@ -73,6 +79,17 @@ int amdp_nccl_unique_id(uint8_t out[128]);
 amdp_engine* amdp_engine_create(const amdp_model_config* model, const amdp_run_config* run,
                                 const uint8_t* nccl_id, char* err, size_t errlen);
 void amdp_engine_destroy(amdp_engine* e);
+
+/* world_size > 1 with AMDP_COMM_IPC: after every rank created its engine, each exports a
+ * descriptor of the memory its peers may map (IPC handles of the boundary arena, of the
+ * per-stage gradient / weight buffers and of its flag array, plus its send table); the host
+ * all-gathers them (any transport: torch.distributed, MPI, files) and passes all world_size
+ * descriptors, in rank order, to amdp_engine_comm_connect.  Export returns the descriptor
+ * size (copies at most len bytes into buf; call with buf = NULL to size it).  No-ops for
+ * world_size 1 and for NCCL.                                                        */
+size_t amdp_engine_comm_export(amdp_engine* e, uint8_t* buf, size_t len);
+int amdp_engine_comm_connect(amdp_engine* e, const uint8_t* const* blobs, const size_t* lens,
+                             int count, char* err, size_t errlen);
 
 /* Pinned host memory for the token streams (host -> device copies overlap compute). */
 void* amdp_host_alloc(size_t bytes);

@@ -121,17 +121,21 @@ int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const float* gamma
  * x[t] = wte[tokens[t]] + wpe[t % seq]   (bf16 tables, bf16 out)                    */
 int amdp_embedding_fwd(const int32_t* tokens, const uint16_t* wte, const uint16_t* wpe,
                        uint16_t* x, int ntok, int seq, int hidden, amdp_stream_t stream);
-/* dwte[tokens[t]] += dx[t]; dwpe[p] += sum over sequences of dx[b*seq+p]  (fp32)   */
+/* dwte[tokens[t]] += dx[t]; dwpe[p] += sum over sequences of dx[b*seq+p]  (fp32).
+ * Deterministic (no atomics): the (token, position) keys are sorted on the device and every
+ * token's rows are summed in position order.  workspace: 4 * ntok bytes; ntok <= 16384,
+ * vocab < 2^18.                                                                     */
 int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, float* dwte, float* dwpe,
-                       int ntok, int seq, int hidden, amdp_stream_t stream);
+                       void* workspace, int ntok, int seq, int hidden, amdp_stream_t stream);
 
 /* ---------------------------------------------------------------- cross-entropy
  * Fused softmax cross-entropy over bf16 logits [ntok][vocab] (row stride ld):
- * loss_sum[0] += sum_t (lse_t - logit[t][label_t]) (fp32 atomic);
+ * row_loss[t] = lse_t - logit[t][label_t] (scratch, ntok floats), then
+ * loss_sum[0] += sum_t row_loss[t] in a fixed order (deterministic, no atomics);
  * logits are overwritten IN PLACE by d(loss * scale)/dlogits = scale*(softmax - onehot).
  * Labels < 0 are ignored (zero gradient, no loss).                                 */
-int amdp_xent_fwd_bwd(uint16_t* logits, const int32_t* labels, float* loss_sum, int ntok,
-                      int vocab, int ld, float scale, amdp_stream_t stream);
+int amdp_xent_fwd_bwd(uint16_t* logits, const int32_t* labels, float* loss_sum, float* row_loss,
+                      int ntok, int vocab, int ld, float scale, amdp_stream_t stream);
 
 /* ---------------------------------------------------------------- optimizer
  * One fused pass per parameter: g = grad (fp32, then zeroed), state update, fp32

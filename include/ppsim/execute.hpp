@@ -11,6 +11,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -24,7 +25,11 @@ struct ExecuteOptions {
   amdp_opt_args optimizer{AMDP_OPT_ADAMW, 3e-4f, 0.9f, 0.95f, 1e-8f, 0.f, 1e-8f, 1e6f, 1.f, 1};
   int world_size = 1;
   int rank = 0;
-  const uint8_t* nccl_id = nullptr;  // amdp_nccl_unique_id() from rank 0 when world_size > 1
+  int comm_backend = AMDP_COMM_IPC;   // world_size > 1: peer-memory data plane or NCCL
+  const uint8_t* nccl_id = nullptr;  // AMDP_COMM_NCCL: amdp_nccl_unique_id() from rank 0
+  // AMDP_COMM_IPC with world_size > 1: gathers this rank's descriptor from every rank and
+  // returns all of them in rank order (MPI_Allgather, torch.distributed, a shared file ...)
+  std::function<std::vector<std::string>(const std::string&)> allgather;
   uint64_t data_seed = 1234;
 };
 

@@ -75,8 +75,8 @@ _sig("amdp_layernorm_bwd_workspace", c_size_t, [c_int, c_int])
 _sig("amdp_layernorm_bwd", c_int,
      [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int, c_int, _P])
 _sig("amdp_embedding_fwd", c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P])
-_sig("amdp_embedding_bwd", c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P])
-_sig("amdp_xent_fwd_bwd", c_int, [_P, _P, _P, c_int, c_int, c_int, c_float, _P])
+_sig("amdp_embedding_bwd", c_int, [_P, _P, _P, _P, _P, c_int, c_int, c_int, _P])
+_sig("amdp_xent_fwd_bwd", c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_float, _P])
 _sig("amdp_optimizer_step", c_int, [POINTER(OptArgs), _P, _P, _P, _P, _P, c_int64, _P])
 _sig("amdp_sumsq", c_int, [_P, c_int64, _P, _P])
 _sig("amdp_fill_normal_bf16_f32", c_int, [_P, _P, c_int64, c_uint64, c_float, _P])

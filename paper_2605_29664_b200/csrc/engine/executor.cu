@@ -1,23 +1,34 @@
 // AMDP stage executor: replays the reference dispatch order (ppsim::simulate_with_order on
-// the declared ClusterSpec) on this process's GPU, one CUDA compute stream plus one NCCL
-// communication stream, and returns the measured Timeline.
+// the declared ClusterSpec) on this process's GPU and returns the measured Timeline.
 //
-//  * Planning (host, once): stage hosting per rank (logical devices folded contiguously,
-//    depth/world per GPU), activation-slot assignment per (stage, minibatch) from the
-//    order, boundary buffers for stage-to-stage activations/gradients with exact
-//    liveness, the communication program (send/recv at the producer's position in the
-//    global order on both ranks, so NCCL pairs match and no wait can form a cycle), and
-//    the replica groups of every stage (owner = logical device i, H/builder.hpp:273).
-//  * Execution: Forward/Backward -> GptStage task bodies; Reduce -> ncclReduce of the
-//    stage's fp32 window gradient to the owner (no-op when every replica is on this
-//    GPU: co-resident replicas accumulate into one buffer); Broadcast -> fused optimizer
-//    step on the owner + ncclBroadcast of the fp32 weights + bf16 refresh on replicas.
-//    Parameter versions are therefore exactly the trace's (F sees w - preloaded, B sees
-//    w): a device-side counter per stage records what each task actually read.
+//  * Planning (host, once): logical devices are folded onto ranks WITHIN replica groups
+//    (devices that share a stage land on the same rank first: AMDP D=8 on 2 GPUs puts
+//    {0,3,4,7} / {1,2,5,6} together, so every stage lives on one GPU and no collective is
+//    needed), activation slots per (stage, minibatch) from the order, boundary buffers for
+//    stage-to-stage activations/gradients with exact liveness, the communication program
+//    (send/recv at the producer's position in the global order on both ranks; message and
+//    collective ids numbered identically on every rank), and the replica groups of every
+//    stage (owner = the rank of logical device i, H/builder.hpp:273).
+//  * Streams: compute (stage kernels, in dispatch order), weight-gradient side stream,
+//    receive, send, collective and update streams.  Each wait names the one event it needs
+//    (a buffer's last compute use, a message's arrival, a stage's new weights), so a stage's
+//    window machinery never blocks the compute of other stages.
+//  * Window machinery (ZeRO, H/builder.hpp:272-304): Reduce -> the stage's fp32 window
+//    gradients summed onto the owner (collective stream; a no-op when every replica is on
+//    this GPU: co-resident replicas accumulate into one buffer); Broadcast -> on the update
+//    stream, after the compute that read the old weights: the owner's fused optimizer step,
+//    then the bf16 weights + fp32 LayerNorm parameters pulled by the other replicas (half of
+//    the fp32-master bytes), which refresh their transposed copies.  Only the tasks the
+//    reference gates on the Broadcast (BC(w-1,i) -> F / preloaded B, builder.hpp:289-304)
+//    wait for it.  Replicated updates (every other schedule): the first Update(w,i,.)
+//    all-reduces the window gradient over the stage's ranks and steps the optimizer.
+//  * Exchanges go through Comm (comm.hpp): this library's CUDA-IPC peer-memory data plane
+//    (default; also runs several ranks on ONE GPU) or NCCL.
+//    Parameter versions are exactly the trace's (F sees w - preloaded, B sees w): a
+//    device-side counter per stage records what each task actually read.
 #include <cuda_runtime.h>
 
 #include <chrono>
-#include <nccl.h>
 
 #include <algorithm>
 #include <array>
@@ -33,6 +44,7 @@
 #include "amdp_engine.h"
 #include "../kernels/common.cuh"
 #include "../sched/sched_handle.hpp"
+#include "comm.hpp"
 #include "gpt_stage.hpp"
 #include "ktimer.hpp"
 #include "ppsim/ppsim.hpp"
@@ -58,12 +70,6 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ src, bf16* __rest
     cudaError_t _e = (x);                                                          \
     if (_e != cudaSuccess)                                                         \
       throw std::runtime_error(std::string(#x) + ": " + cudaGetErrorString(_e));   \
-  } while (0)
-#define NCCL_OK(x)                                                                 \
-  do {                                                                             \
-    ncclResult_t _r = (x);                                                         \
-    if (_r != ncclSuccess)                                                         \
-      throw std::runtime_error(std::string(#x) + ": " + ncclGetErrorString(_r));   \
   } while (0)
 
 uint64_t tensor_seed(uint64_t model_seed, int gidx) {
@@ -112,8 +118,10 @@ std::vector<int> balance_layers(int L, int depth, int h, int V, int ffn, int seq
 
 struct BoundaryBuf {
   uint16_t* ptr = nullptr;
-  cudaEvent_t comm_done = nullptr;  // last communication use (send) of this buffer
+  cudaEvent_t comm_done = nullptr;  // last communication use (send / recv) of this buffer
   bool comm_pending = false;
+  cudaEvent_t used = nullptr;       // last compute use (a recv into it waits for this)
+  bool use_recorded = false;
 };
 
 struct TaskPlan {
@@ -127,12 +135,13 @@ struct TaskPlan {
   bool first_update = false;  // Update: the first of its (stage, window) -> the optimizer step
 };
 
-struct CommOp {           // executed on the comm stream at a position in the global order
+struct CommOp {           // issued at a position in the global order
   enum Kind { Send, Recv, Reduce, Bcast, Allreduce } kind;
   int peer = -1;          // send/recv peer rank
   int buf = -1;           // boundary buffer (send/recv)
   int stage = -1;         // reduce/bcast stage
   int after_task = -1;    // order position whose compute it must follow (send/reduce)
+  int id = -1;            // message id (send/recv) or collective id, same on every rank
 };
 
 }  // namespace
@@ -186,23 +195,34 @@ class Engine {
   std::vector<std::vector<int>> rep_buf_;                // per stage, pipeline
   float update_div_ = 1.f;                               // minibatches per optimizer step
   void use_replica_weights(int stage, int pipeline);
-  void optimizer_step(int stage, int step);
+  void optimizer_step(int stage, int step, cudaStream_t st);
+  int cur_pos_ = 0;  // order position being issued
+  int64_t comm_launches_seen_ = 0;
   std::vector<TaskPlan> plan_;               // per order position
   std::vector<std::vector<CommOp>> comm_at_; // per order position
   std::vector<std::vector<uint8_t*>> slot_mem_;
   std::vector<std::vector<SlotActs>> slot_acts_;
   std::vector<BoundaryBuf> bufs_;
   std::vector<std::vector<int>> group_ranks_; // per stage: ranks hosting it
-  std::vector<ncclComm_t> group_comm_;        // per stage (null if single-rank group)
-  ncclComm_t world_comm_ = nullptr;
-  cudaStream_t cs_ = nullptr, ms_ = nullptr;  // compute, communication
+  std::vector<int> dev_rank_;                 // logical device -> rank (fold within replica groups)
+  std::unique_ptr<Comm> comm_;                // world_size > 1
+  int nmsg_ = 0, ncoll_ = 0;                  // message / collective ids of the global plan
+  // compute, receive, send, collective, window-update streams (NCCL: one stream for all comm)
+  cudaStream_t cs_ = nullptr, rs_ = nullptr, ss_ = nullptr, ks_ = nullptr, us_ = nullptr;
+  std::vector<cudaEvent_t> wready_;   // per stage: new weights in place (update stream)
+  std::vector<char> wpending_;        // per stage: next F/B must wait wready_
+  std::vector<cudaEvent_t> reduced_;  // per stage: window gradient reduced (collective stream)
+  std::vector<cudaEvent_t> ev_pool_;  // cross-stream hand-offs (recycled round robin)
+  size_t ev_next_ = 0;
+  cudaEvent_t handoff(cudaStream_t from);  // event recorded on `from` now
+  uint16_t* bounds_arena_ = nullptr;
+  std::vector<std::pair<int, int>> planned_sends_;  // (message id, boundary buffer)
   uint8_t* ws_ = nullptr;
   int32_t *d_inputs_ = nullptr, *d_labels_ = nullptr;
   float* d_loss_ = nullptr;
   int *d_ver_ = nullptr, *d_trace_ = nullptr;
   std::vector<cudaEvent_t> ev_start_, ev_end_;
   cudaEvent_t run_begin_ = nullptr, run_end_ = nullptr;
-  std::vector<cudaEvent_t> stage_ready_;      // weights of stage i usable (after bcast)
   size_t slot_total_ = 0;
   int64_t measured_alloc_bytes_ = -1;  // cudaMemGetInfo delta across allocate() (-1: plan only)
   std::string memory_json() const;
@@ -210,7 +230,7 @@ class Engine {
   std::vector<float> loss_scale_;  // per minibatch: 1 / number of labelled tokens
   SideStream side_;                // weight-gradient GEMM stream + events
 
-  int rank_of_dev(int dev) const { return dev / per_rank_; }
+  int rank_of_dev(int dev) const { return dev_rank_[static_cast<size_t>(dev)]; }
   int owner_rank(int stage) const { return rank_of_dev(stage); }
   void make_plan();
   void allocate();
@@ -218,6 +238,13 @@ class Engine {
   void exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::vector<int>& window_tokens_loaded,
                  std::vector<int>& window_last_left, float* losses_out);
   void exec_comm(int pos);
+  void zero_broadcast(int stage, int window);
+
+ public:
+  std::string comm_export() { return comm_ ? comm_->export_blob() : std::string(); }
+  void comm_connect(const std::vector<std::string>& blobs) {
+    if (comm_) comm_->import_blobs(blobs);
+  }
 };
 
 Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uint8_t* nccl_id)
@@ -298,6 +325,38 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     l += part[static_cast<size_t>(i)];
   }
 
+  // fold logical devices onto ranks within replica groups: devices running a common stage
+  // form one component (union-find); devices ordered by (component's smallest device,
+  // device) are cut into world_ contiguous chunks of per_rank_.  AMDP D=8: components
+  // {0,3,4,7} and {1,2,5,6} (map_stage_to_device, H/builder.hpp:81-88), so N=2 needs no
+  // collective and N=4 pairs {0,3},{4,7},{1,2},{5,6}; DAPPLE / GPipe (stage i on device i)
+  // fold contiguously.
+  {
+    std::vector<int> up(static_cast<size_t>(devices_));
+    for (int d = 0; d < devices_; ++d) up[static_cast<size_t>(d)] = d;
+    auto find = [&](int d) {
+      while (up[static_cast<size_t>(d)] != d) d = up[static_cast<size_t>(d)] = up[static_cast<size_t>(up[static_cast<size_t>(d)])];
+      return d;
+    };
+    std::vector<int> first_dev(static_cast<size_t>(depth_), -1);
+    for (const auto& t : sched.g.tasks) {
+      if (t.kind != ppsim::Kind::Forward && t.kind != ppsim::Kind::Backward) continue;
+      int& f = first_dev[static_cast<size_t>(t.stage)];
+      if (f < 0) {
+        f = t.device;
+        continue;
+      }
+      const int a = find(f), b = find(t.device);
+      if (a != b) up[static_cast<size_t>(std::max(a, b))] = std::min(a, b);
+    }
+    std::vector<int> ord(static_cast<size_t>(devices_));
+    for (int d = 0; d < devices_; ++d) ord[static_cast<size_t>(d)] = d;
+    if (per_rank_ > 1)  // one device per rank: rank r runs logical device r
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return find(a) < find(b); });
+    dev_rank_.assign(static_cast<size_t>(devices_), 0);
+    for (int k = 0; k < devices_; ++k) dev_rank_[static_cast<size_t>(ord[static_cast<size_t>(k)])] = k / per_rank_;
+  }
+
   // hosting
   hosted.assign(static_cast<size_t>(depth_), false);
   owned.assign(static_cast<size_t>(depth_), false);
@@ -319,36 +378,33 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     owned[static_cast<size_t>(i)] = zero_ ? owner_rank(i) == rank_ : hosted[static_cast<size_t>(i)];
   }
 
+  make_plan();
   if (rc.plan_only) {  // host-side planning only (multi-rank consistency tests on CPU)
-    group_comm_.assign(static_cast<size_t>(depth_), nullptr);
-    make_plan();
     plan_only_ = true;
     return;
   }
   CUDA_OK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
-  CUDA_OK(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
+  CUDA_OK(cudaStreamCreateWithFlags(&us_, cudaStreamNonBlocking));
   if (!getenv("AMDP_NO_SIDE_STREAM")) {
     CUDA_OK(cudaStreamCreateWithFlags(&side_.side, cudaStreamNonBlocking));
     for (auto& e : side_.ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   if (world_ > 1) {
-    if (!nccl_id) throw std::invalid_argument("engine: nccl_id required when world_size > 1");
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
-    NCCL_OK(ncclCommInitRank(&world_comm_, world_, id, rank_));
-  }
-  group_comm_.assign(static_cast<size_t>(depth_), nullptr);
-  if (world_ > 1) {
-    for (int i = 0; i < depth_; ++i) {
-      const auto& gr = group_ranks_[static_cast<size_t>(i)];
-      const int color = hosted[static_cast<size_t>(i)] ? i : NCCL_SPLIT_NOCOLOR;
-      ncclComm_t c = nullptr;
-      NCCL_OK(ncclCommSplit(world_comm_, color, rank_, &c, nullptr));  // collective over all ranks
-      group_comm_[static_cast<size_t>(i)] = (gr.size() > 1 && hosted[static_cast<size_t>(i)]) ? c : nullptr;
-      if (c && !(gr.size() > 1 && hosted[static_cast<size_t>(i)])) ncclCommDestroy(c);
+    if (rc.comm_backend == AMDP_COMM_NCCL)
+      comm_ = make_nccl_comm(world_, rank_, nccl_id, group_ranks_);
+    else
+      comm_ = make_ipc_comm(world_, rank_, nmsg_, ncoll_);
+    if (comm_->single_stream()) {
+      CUDA_OK(cudaStreamCreateWithFlags(&rs_, cudaStreamNonBlocking));
+      ss_ = ks_ = rs_;
+    } else {
+      CUDA_OK(cudaStreamCreateWithFlags(&rs_, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithFlags(&ss_, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithFlags(&ks_, cudaStreamNonBlocking));
     }
   }
-  make_plan();
+  ev_pool_.resize(64);
+  for (auto& e : ev_pool_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   size_t free0 = 0, free1 = 0, total = 0;
   CUDA_OK(cudaMemGetInfo(&free0, &total));
   allocate();
@@ -358,10 +414,19 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   init_weights();
 }
 
+// An event recorded on `from` now, for an immediate cudaStreamWaitEvent (which binds the
+// event's record at call time, so recycling the small pool is safe).
+cudaEvent_t Engine::handoff(cudaStream_t from) {
+  cudaEvent_t e = ev_pool_[ev_next_++ % ev_pool_.size()];
+  CUDA_OK(cudaEventRecord(e, from));
+  return e;
+}
+
 Engine::~Engine() {
   if (plan_only_) return;
-  cudaStreamSynchronize(cs_);
-  cudaStreamSynchronize(ms_);
+  for (cudaStream_t st : {cs_, rs_, ss_, ks_, us_, side_.side})
+    if (st) cudaStreamSynchronize(st);
+  comm_.reset();  // unmaps peers' memory before our own buffers go away
   for (auto& s : stages) {
     cudaFree(s->master);
     cudaFree(s->m);
@@ -378,9 +443,10 @@ Engine::~Engine() {
   for (auto& v : slot_mem_)
     for (auto* p : v) cudaFree(p);
   for (auto& b : bufs_) {
-    cudaFree(b.ptr);
     if (b.comm_done) cudaEventDestroy(b.comm_done);
+    if (b.used) cudaEventDestroy(b.used);
   }
+  cudaFree(bounds_arena_);
   cudaFree(ws_);
   cudaFree(d_inputs_);
   cudaFree(d_labels_);
@@ -389,25 +455,28 @@ Engine::~Engine() {
   cudaFree(d_trace_);
   for (auto e : ev_start_) cudaEventDestroy(e);
   for (auto e : ev_end_) cudaEventDestroy(e);
-  for (auto e : stage_ready_) cudaEventDestroy(e);
+  for (auto e : wready_) cudaEventDestroy(e);
+  for (auto e : reduced_) cudaEventDestroy(e);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
   if (run_begin_) cudaEventDestroy(run_begin_);
   if (run_end_) cudaEventDestroy(run_end_);
-  for (auto c : group_comm_)
-    if (c) ncclCommDestroy(c);
-  if (world_comm_) ncclCommDestroy(world_comm_);
   if (side_.side) {
-    cudaStreamSynchronize(side_.side);
     for (auto e : side_.ev) cudaEventDestroy(e);
     cudaStreamDestroy(side_.side);
   }
+  if (ss_ && ss_ != rs_) cudaStreamDestroy(ss_);
+  if (ks_ && ks_ != rs_) cudaStreamDestroy(ks_);
+  if (rs_) cudaStreamDestroy(rs_);
+  cudaStreamDestroy(us_);
   cudaStreamDestroy(cs_);
-  cudaStreamDestroy(ms_);
 }
 
 void Engine::make_plan() {
   const auto& g = sched.g;
   const auto& order = sched.order;
   const int N = static_cast<int>(order.size());
+  nmsg_ = ncoll_ = 0;
+  planned_sends_.clear();
   plan_.assign(static_cast<size_t>(N), TaskPlan{});
   comm_at_.assign(static_cast<size_t>(N), {});
   std::vector<int> pos_of(g.tasks.size());
@@ -467,6 +536,7 @@ void Engine::make_plan() {
         const int cons = F.at({i + 1, j});
         const int cr = rank_of_task(cons);
         const int last_use = pos_of[static_cast<size_t>(B.at({i + 1, j}))];
+        const int msg = cr != me ? nmsg_++ : -1;  // numbered on every rank alike
         if (tp.local) {
           const int b = alloc_buf();
           tp.out_buf = b;
@@ -475,13 +545,14 @@ void Engine::make_plan() {
             release_at[static_cast<size_t>(last_use)].push_back(b);
           } else {
             tp.send_to = cr;
-            comm_at_[static_cast<size_t>(k)].push_back({CommOp::Send, cr, b, -1, k});
+            comm_at_[static_cast<size_t>(k)].push_back({CommOp::Send, cr, b, -1, k, msg});
+            planned_sends_.emplace_back(msg, b);
             release_at[static_cast<size_t>(k)].push_back(b);
           }
         } else if (cr == rank_) {
           const int b = alloc_buf();
           fbuf_recv[{i, j}] = b;
-          comm_at_[static_cast<size_t>(k)].push_back({CommOp::Recv, me, b, -1, -1});
+          comm_at_[static_cast<size_t>(k)].push_back({CommOp::Recv, me, b, -1, -1, msg});
           release_at[static_cast<size_t>(last_use)].push_back(b);
         }
       }
@@ -497,6 +568,7 @@ void Engine::make_plan() {
         const int cons = B.at({i - 1, j});
         const int cr = rank_of_task(cons);
         const int last_use = pos_of[static_cast<size_t>(cons)];
+        const int msg = cr != me ? nmsg_++ : -1;
         if (tp.local) {
           const int b = alloc_buf();
           tp.gout_buf = b;
@@ -505,25 +577,29 @@ void Engine::make_plan() {
             release_at[static_cast<size_t>(last_use)].push_back(b);
           } else {
             tp.send_to = cr;
-            comm_at_[static_cast<size_t>(k)].push_back({CommOp::Send, cr, b, -1, k});
+            comm_at_[static_cast<size_t>(k)].push_back({CommOp::Send, cr, b, -1, k, msg});
+            planned_sends_.emplace_back(msg, b);
             release_at[static_cast<size_t>(k)].push_back(b);
           }
         } else if (cr == rank_) {
           const int b = alloc_buf();
           bbuf_recv[{i - 1, j}] = b;
-          comm_at_[static_cast<size_t>(k)].push_back({CommOp::Recv, me, b, -1, -1});
+          comm_at_[static_cast<size_t>(k)].push_back({CommOp::Recv, me, b, -1, -1, msg});
           release_at[static_cast<size_t>(last_use)].push_back(b);
         }
       }
     } else if (task.kind == ppsim::Kind::Reduce) {
       const int i = task.stage;
-      if (hosted[static_cast<size_t>(i)] && group_comm_.size() > static_cast<size_t>(i) &&
-          group_ranks_[static_cast<size_t>(i)].size() > 1)
-        comm_at_[static_cast<size_t>(k)].push_back({CommOp::Reduce, -1, -1, i, k});
+      if (group_ranks_[static_cast<size_t>(i)].size() > 1) {
+        const int c = ncoll_++;
+        if (hosted[static_cast<size_t>(i)]) comm_at_[static_cast<size_t>(k)].push_back({CommOp::Reduce, -1, -1, i, k, c});
+      }
     } else if (task.kind == ppsim::Kind::Broadcast) {
       const int i = task.stage;
-      if (hosted[static_cast<size_t>(i)] && group_ranks_[static_cast<size_t>(i)].size() > 1)
-        comm_at_[static_cast<size_t>(k)].push_back({CommOp::Bcast, -1, -1, i, k});
+      if (group_ranks_[static_cast<size_t>(i)].size() > 1) {
+        const int c = ncoll_++;
+        if (hosted[static_cast<size_t>(i)]) comm_at_[static_cast<size_t>(k)].push_back({CommOp::Bcast, -1, -1, i, k, c});
+      }
     } else if (task.kind == ppsim::Kind::Update) {
       // Update(w, i, p) (minibatch field = w; PipeDreamAsync: = j).  The first one in the global
       // order steps the optimizer on every rank hosting stage i, after an all-reduce of the
@@ -531,8 +607,10 @@ void Engine::make_plan() {
       // barrier", builder.hpp:306-308): all of the window's backwards precede it.
       const int i = task.stage;
       tp.first_update = updates_seen[{i, task.minibatch}]++ == 0;
-      if (tp.first_update && hosted[static_cast<size_t>(i)] && group_ranks_[static_cast<size_t>(i)].size() > 1)
-        comm_at_[static_cast<size_t>(k)].push_back({CommOp::Allreduce, -1, -1, i, k});
+      if (tp.first_update && group_ranks_[static_cast<size_t>(i)].size() > 1) {
+        const int c = ncoll_++;
+        if (hosted[static_cast<size_t>(i)]) comm_at_[static_cast<size_t>(k)].push_back({CommOp::Allreduce, -1, -1, i, k, c});
+      }
     }
     for (int b : release_at[static_cast<size_t>(k)]) free_bufs.push_back(b);
   }
@@ -580,10 +658,14 @@ void Engine::allocate() {
       slot_acts_[static_cast<size_t>(i)].push_back(stages[static_cast<size_t>(i)]->carve_slot(p));
     }
   }
+  // boundary buffers: one arena (one IPC export), buffer b at b * T * h elements
   bufs_.resize(static_cast<size_t>(nbuf));
-  for (auto& b : bufs_) {
-    CUDA_OK(cudaMalloc(&b.ptr, T * h * sizeof(uint16_t)));
+  if (nbuf > 0) CUDA_OK(cudaMalloc(&bounds_arena_, static_cast<size_t>(nbuf) * T * h * sizeof(uint16_t)));
+  for (size_t k = 0; k < bufs_.size(); ++k) {
+    BoundaryBuf& b = bufs_[k];
+    b.ptr = bounds_arena_ + k * T * h;
     CUDA_OK(cudaEventCreateWithFlags(&b.comm_done, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&b.used, cudaEventDisableTiming));
   }
   CUDA_OK(cudaMalloc(&ws_, GptStage::workspace_bytes(dm)));
   CUDA_OK(cudaMalloc(&d_inputs_, static_cast<size_t>(M_) * T * sizeof(int32_t)));
@@ -591,8 +673,23 @@ void Engine::allocate() {
   CUDA_OK(cudaMalloc(&d_loss_, static_cast<size_t>(M_) * sizeof(float)));
   CUDA_OK(cudaMalloc(&d_ver_, static_cast<size_t>(depth_ * P_) * sizeof(int)));
   CUDA_OK(cudaMalloc(&d_trace_, sched.g.tasks.size() * sizeof(int)));
-  stage_ready_.resize(static_cast<size_t>(depth_));
-  for (auto& e : stage_ready_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  wready_.resize(static_cast<size_t>(depth_));
+  reduced_.resize(static_cast<size_t>(depth_));
+  wpending_.assign(static_cast<size_t>(depth_), 0);
+  for (auto& e : wready_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : reduced_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (comm_) {  // what peers may read: boundary arena, and per hosted stage grad / w / master
+    if (bounds_arena_) comm_->register_region(REG_BOUNDS, 0, bounds_arena_, static_cast<size_t>(nbuf) * T * h * 2);
+    for (const auto& [msg, b] : planned_sends_) comm_->plan_send(msg, static_cast<size_t>(b) * T * h * 2);
+    for (int i = 0; i < depth_; ++i) {
+      if (!hosted[static_cast<size_t>(i)] || group_ranks_[static_cast<size_t>(i)].size() < 2) continue;
+      GptStage& st = *stages[static_cast<size_t>(i)];
+      const size_t n = static_cast<size_t>(st.numel());
+      comm_->register_region(REG_GRAD, i, st.grad, n * 4);
+      comm_->register_region(REG_MASTER, i, st.master, n * 4);
+      comm_->register_region(REG_W, i, st.w, n * 2);
+    }
+  }
   CUDA_OK(cudaEventCreate(&run_begin_));
   CUDA_OK(cudaEventCreate(&run_end_));
 }
@@ -621,46 +718,37 @@ void Engine::init_weights() {
   CUDA_OK(cudaStreamSynchronize(cs_));
 }
 
+// Point-to-point ops placed at order position `pos`, and the Reduce of a window.  Sends run
+// on the send stream after this position's compute; a receive waits only for the last
+// compute use of its destination buffer (not for all earlier compute of the rank).
 void Engine::exec_comm(int pos) {
   for (const CommOp& op : comm_at_[static_cast<size_t>(pos)]) {
-    const size_t T = static_cast<size_t>(dm.T), h = static_cast<size_t>(dm.h);
+    const size_t bytes = static_cast<size_t>(dm.T) * static_cast<size_t>(dm.h) * 2;
     switch (op.kind) {
       case CommOp::Send: {
-        cudaEvent_t e;
-        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CUDA_OK(cudaEventRecord(e, cs_));
-        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
-        cudaEventDestroy(e);
-        NCCL_OK(ncclSend(bufs_[static_cast<size_t>(op.buf)].ptr, T * h, ncclBfloat16, op.peer, world_comm_, ms_));
-        CUDA_OK(cudaEventRecord(bufs_[static_cast<size_t>(op.buf)].comm_done, ms_));
-        bufs_[static_cast<size_t>(op.buf)].comm_pending = true;
-        stats.p2p_bytes_sent += static_cast<int64_t>(T * h * 2);
+        BoundaryBuf& b = bufs_[static_cast<size_t>(op.buf)];
+        CUDA_OK(cudaStreamWaitEvent(ss_, handoff(cs_), 0));
+        comm_->send(op.id, op.peer, b.ptr, bytes, ss_);
+        CUDA_OK(cudaEventRecord(b.comm_done, ss_));
+        b.comm_pending = true;
+        stats.p2p_bytes_sent += static_cast<int64_t>(bytes);
         break;
       }
       case CommOp::Recv: {
         BoundaryBuf& b = bufs_[static_cast<size_t>(op.buf)];
-        // the buffer's previous compute use must be finished before it is overwritten
-        cudaEvent_t e;
-        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CUDA_OK(cudaEventRecord(e, cs_));
-        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
-        cudaEventDestroy(e);
-        NCCL_OK(ncclRecv(b.ptr, T * h, ncclBfloat16, op.peer, world_comm_, ms_));
-        CUDA_OK(cudaEventRecord(b.comm_done, ms_));
+        if (b.use_recorded) CUDA_OK(cudaStreamWaitEvent(rs_, b.used, 0));
+        if (b.comm_pending) CUDA_OK(cudaStreamWaitEvent(rs_, b.comm_done, 0));  // NCCL: same stream
+        comm_->recv(op.id, op.peer, b.ptr, bytes, rs_);
+        CUDA_OK(cudaEventRecord(b.comm_done, rs_));
         b.comm_pending = true;
         break;
       }
       case CommOp::Reduce: {
         GptStage& st = *stages[static_cast<size_t>(op.stage)];
-        cudaEvent_t e;
-        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CUDA_OK(cudaEventRecord(e, cs_));
-        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
-        cudaEventDestroy(e);
-        const auto& gr = group_ranks_[static_cast<size_t>(op.stage)];
-        const int root = static_cast<int>(std::find(gr.begin(), gr.end(), owner_rank(op.stage)) - gr.begin());
-        NCCL_OK(ncclReduce(st.grad, st.grad, static_cast<size_t>(st.numel()), ncclFloat32, ncclSum, root,
-                           group_comm_[static_cast<size_t>(op.stage)], ms_));
+        CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));  // the window's backwards of this rank
+        comm_->reduce_f32(op.id, group_ranks_[static_cast<size_t>(op.stage)], owner_rank(op.stage), op.stage,
+                          st.grad, static_cast<size_t>(st.numel()), ks_);
+        CUDA_OK(cudaEventRecord(reduced_[static_cast<size_t>(op.stage)], ks_));
         stats.collective_bytes += st.numel() * 4;
         break;
       }
@@ -671,6 +759,53 @@ void Engine::exec_comm(int pos) {
   }
 }
 
+// ZeRO Broadcast(w, i) (H/builder.hpp:289-304) on the update stream, after this rank's compute
+// up to this order position (every read of the old weights and, through reduced_, the
+// reduced window gradient): the owner steps the optimizer (bf16 copy + transposed copy
+// rewritten, gradient zeroed); replicas on other ranks clear their gradient and pull the
+// owner's bf16 weights + fp32 LayerNorm parameters, then refresh their transposed copy.
+// The next F/B of stage i waits for wready_[i]; nothing else does.
+void Engine::zero_broadcast(int i, int window) {
+  GptStage& S = *stages[static_cast<size_t>(i)];
+  const auto& gr = group_ranks_[static_cast<size_t>(i)];
+  const bool multi = gr.size() > 1;
+  CUDA_OK(cudaStreamWaitEvent(us_, handoff(cs_), 0));
+  if (multi) CUDA_OK(cudaStreamWaitEvent(us_, reduced_[static_cast<size_t>(i)], 0));
+  // the measured Broadcast event is the update stream's interval (it overlaps other stages'
+  // compute on this GPU; projection.py models the update lane separately)
+  if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(cur_pos_)], us_));
+  cudaStream_t bs = us_;  // broadcast stream
+  if (multi && comm_->single_stream()) bs = ks_;
+  if (owned[static_cast<size_t>(i)]) {
+    optimizer_step(i, window + 1, us_);
+  } else {
+    CUDA_OK(cudaMemsetAsync(S.grad, 0, static_cast<size_t>(S.numel()) * sizeof(float), us_));
+  }
+  if (multi) {
+    int coll = -1;
+    for (const CommOp& op : comm_at_[static_cast<size_t>(cur_pos_)])
+      if (op.kind == CommOp::Bcast && op.stage == i) coll = op.id;
+    std::vector<Span> spans;
+    spans.push_back(Span{REG_W, i, 0, static_cast<size_t>(S.numel()) * 2});
+    for (const auto& p : S.params())
+      if (p.rows == 1) spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(p.off) * 4, static_cast<size_t>(p.numel()) * 4});
+    if (bs != us_) CUDA_OK(cudaStreamWaitEvent(bs, handoff(us_), 0));
+    comm_->broadcast(coll, gr, owner_rank(i), i, spans, bs);
+    if (bs != us_) CUDA_OK(cudaStreamWaitEvent(us_, handoff(bs), 0));
+    int64_t moved = 0;
+    for (const Span& sp : spans) moved += static_cast<int64_t>(sp.bytes);
+    stats.collective_bytes += moved;
+    if (!owned[static_cast<size_t>(i)]) {
+      const int nt = S.refresh_transposed(us_);
+      if (nt < 0) throw std::runtime_error("weight transpose failed");
+      stats.kernels_launched += nt;
+    }
+  }
+  CUDA_OK(cudaEventRecord(wready_[static_cast<size_t>(i)], us_));
+  if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(cur_pos_)], us_));
+  wpending_[static_cast<size_t>(i)] = 1;
+}
+
 void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::vector<int>& loaded,
                        std::vector<int>& last_left, float* losses_out) {
   const auto& g = sched.g;
@@ -678,8 +813,8 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
   const auto& task = g.tasks[static_cast<size_t>(t)];
   const TaskPlan& tp = plan_[static_cast<size_t>(pos)];
   const size_t T = static_cast<size_t>(dm.T);
-  auto st = reinterpret_cast<amdp_stream_t>(cs_);
   int rc = 0;
+  cur_pos_ = pos;
 
   if (task.kind == ppsim::Kind::Forward || task.kind == ppsim::Kind::Backward) {
     if (!tp.local) {
@@ -706,6 +841,10 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     wait_buf(tp.gin_buf);
     wait_buf(tp.out_buf);
     wait_buf(tp.gout_buf);
+    if (wpending_[static_cast<size_t>(i)]) {  // the stage's new weights (Broadcast, update stream)
+      CUDA_OK(cudaStreamWaitEvent(cs_, wready_[static_cast<size_t>(i)], 0));
+      wpending_[static_cast<size_t>(i)] = 0;
+    }
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
     record_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, d_trace_, t);
     use_replica_weights(i, task.pipeline);
@@ -727,6 +866,13 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
     stats.tasks_executed += 1;
+    if (comm_) {  // last compute use of the buffers this task touched (a later recv waits for it)
+      for (int b : {tp.in_buf, tp.gin_buf, tp.out_buf, tp.gout_buf})
+        if (b >= 0) {
+          CUDA_OK(cudaEventRecord(bufs_[static_cast<size_t>(b)].used, cs_));
+          bufs_[static_cast<size_t>(b)].use_recorded = true;
+        }
+    }
     exec_comm(pos);  // sends of this task's output, recvs placed at this position
     // D2H of a window's losses once its last-stage forwards are all issued
     if (task.kind == ppsim::Kind::Forward && S.last() && losses_out) {
@@ -747,16 +893,13 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
   }
   GptStage& S = *stages[static_cast<size_t>(i)];
   if (task.kind == ppsim::Kind::Reduce) {
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
-    exec_comm(pos);  // ncclReduce on the comm stream after this position's compute
-    if (group_ranks_[static_cast<size_t>(i)].size() > 1 && owned[static_cast<size_t>(i)]) {
-      cudaEvent_t e;
-      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CUDA_OK(cudaEventRecord(e, ms_));
-      CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
-      cudaEventDestroy(e);
-    }
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    // the reduction runs on the collective stream (its measured interval); the update stream's
+    // Broadcast waits for it
+    cudaStream_t rs = comm_at_[static_cast<size_t>(pos)].empty() ? cs_ : ks_;
+    if (rc_.record_events && rs == ks_) CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], rs));
+    exec_comm(pos);
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], rs));
     stats.tasks_executed += 1;
     return;
   }
@@ -764,18 +907,16 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
     if (tp.first_update) {
       if (group_ranks_[static_cast<size_t>(i)].size() > 1) {  // sum the replicas' window gradients
-        cudaEvent_t e;
-        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CUDA_OK(cudaEventRecord(e, cs_));
-        CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
-        NCCL_OK(ncclAllReduce(S.grad, S.grad, static_cast<size_t>(S.numel()), ncclFloat32, ncclSum,
-                              group_comm_[static_cast<size_t>(i)], ms_));
+        int coll = -1;
+        for (const CommOp& op : comm_at_[static_cast<size_t>(pos)])
+          if (op.kind == CommOp::Allreduce && op.stage == i) coll = op.id;
+        CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));
+        comm_->allreduce_f32(coll, group_ranks_[static_cast<size_t>(i)], i, S.grad, static_cast<size_t>(S.numel()),
+                             ks_);
         stats.collective_bytes += 2 * S.numel() * 4;
-        CUDA_OK(cudaEventRecord(e, ms_));
-        CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
-        cudaEventDestroy(e);
+        CUDA_OK(cudaStreamWaitEvent(cs_, handoff(ks_), 0));
       }
-      optimizer_step(i, task.minibatch + 1);  // Update's minibatch field: window (PipeDream: j)
+      optimizer_step(i, task.minibatch + 1, cs_);  // Update's minibatch field: window (PipeDream: j)
     }
     if (rank_of_dev(task.device) == rank_) {  // this replica now reads the newest weights
       if (versioned_) rep_buf_[static_cast<size_t>(i)][static_cast<size_t>(task.pipeline)] = cur_buf_[static_cast<size_t>(i)];
@@ -787,45 +928,10 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     return;
   }
   if (task.kind == ppsim::Kind::Broadcast) {
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
-    const bool multi = group_ranks_[static_cast<size_t>(i)].size() > 1;
-    if (owned[static_cast<size_t>(i)]) {
-      optimizer_step(i, task.minibatch + 1);  // Broadcast's minibatch field: the window
-    } else {
-      // the reduce on the comm stream read this replica's gradient: wait, then clear it
-      cudaEvent_t e;
-      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CUDA_OK(cudaEventRecord(e, ms_));
-      CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
-      cudaEventDestroy(e);
-      CUDA_OK(cudaMemsetAsync(S.grad, 0, static_cast<size_t>(S.numel()) * sizeof(float), cs_));
-    }
-    if (multi) {
-      cudaEvent_t e;
-      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CUDA_OK(cudaEventRecord(e, cs_));
-      CUDA_OK(cudaStreamWaitEvent(ms_, e, 0));
-      cudaEventDestroy(e);
-      const auto& gr = group_ranks_[static_cast<size_t>(i)];
-      const int root = static_cast<int>(std::find(gr.begin(), gr.end(), owner_rank(i)) - gr.begin());
-      NCCL_OK(ncclBroadcast(S.master, S.master, static_cast<size_t>(S.numel()), ncclFloat32, root,
-                            group_comm_[static_cast<size_t>(i)], ms_));
-      stats.collective_bytes += S.numel() * 4;
-      CUDA_OK(cudaEventRecord(stage_ready_[static_cast<size_t>(i)], ms_));
-      if (!owned[static_cast<size_t>(i)]) {
-        CUDA_OK(cudaStreamWaitEvent(cs_, stage_ready_[static_cast<size_t>(i)], 0));
-        const int64_t n = S.numel();
-        cast_f32_bf16_kernel<<<std::min<int64_t>((n + 255) / 256, 4 * 148), 256, 0, cs_>>>(
-            S.master, reinterpret_cast<bf16*>(S.w), n);
-        stats.kernels_launched += 1;
-        const int nt = S.refresh_transposed(cs_);
-        if (nt < 0) throw std::runtime_error("weight transpose failed");
-        stats.kernels_launched += nt;
-      }
-    }
-    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_, P_);  // every replica of stage i
+    zero_broadcast(i, task.minibatch);  // Broadcast's minibatch field: the window
+    // every replica of stage i reads the next version from its next task on (in order)
+    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_, P_);
     stats.kernels_launched += 1;
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
     stats.tasks_executed += 1;
     return;
   }
@@ -871,6 +977,14 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
     if (t.kind == ppsim::Kind::Forward && t.stage == depth_ - 1 && plan_[static_cast<size_t>(k)].local)
       ++last_left[static_cast<size_t>(t.window)];
   }
+  if (comm_) {
+    if (!comm_->connected())
+      throw std::runtime_error("engine: world_size > 1 needs the communication descriptors exchanged "
+                               "(amdp_engine_comm_export / amdp_engine_comm_connect) before run");
+    comm_->begin_run();
+  }
+  for (auto& b : bufs_) b.comm_pending = b.use_recorded = false;  // the previous run fully drained
+  std::fill(wpending_.begin(), wpending_.end(), 0);
   CUDA_OK(cudaEventRecord(run_begin_, cs_));
   const auto t_issue0 = std::chrono::steady_clock::now();
   for (int k = 0; k < N; ++k)
@@ -878,15 +992,14 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
       exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
   stats.host_issue_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_issue0).count();
-  {
-    cudaEvent_t e;
-    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CUDA_OK(cudaEventRecord(e, ms_));
-    CUDA_OK(cudaStreamWaitEvent(cs_, e, 0));
-    cudaEventDestroy(e);
-  }
+  for (cudaStream_t st : {rs_, ss_, ks_, us_})  // join every stream: the run ends when all are idle
+    if (st) CUDA_OK(cudaStreamWaitEvent(cs_, handoff(st), 0));
   CUDA_OK(cudaEventRecord(run_end_, cs_));
   CUDA_OK(cudaStreamSynchronize(cs_));
+  if (comm_) {
+    stats.kernels_launched += comm_->kernel_launches() - comm_launches_seen_;
+    comm_launches_seen_ = comm_->kernel_launches();
+  }
   float ms = 0.f;
   CUDA_OK(cudaEventElapsedTime(&ms, run_begin_, run_end_));
   stats.device_ms = ms;
@@ -933,7 +1046,11 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
 std::string Engine::plan_json() const {
   std::string s = "{\"depth\":" + std::to_string(depth_) + ",\"world_size\":" + std::to_string(world_) +
                   ",\"rank\":" + std::to_string(rank_) + ",\"tokens_per_minibatch\":" + std::to_string(dm.T) +
-                  ",\"partition\":[";
+                  ",\"comm_backend\":\"" + (world_ == 1 ? "none" : rc_.comm_backend == AMDP_COMM_NCCL ? "nccl" : "ipc") +
+                  "\",\"messages\":" + std::to_string(nmsg_) + ",\"collectives\":" + std::to_string(ncoll_) +
+                  ",\"device_rank\":[";
+  for (size_t d = 0; d < dev_rank_.size(); ++d) s += (d ? "," : "") + std::to_string(dev_rank_[d]);
+  s += "],\"partition\":[";
   for (size_t i = 0; i < part.size(); ++i) s += (i ? "," : "") + std::to_string(part[i]);
   s += "],\"stages\":[";
   for (int i = 0; i < depth_; ++i) {
@@ -962,7 +1079,7 @@ std::string Engine::plan_json() const {
     for (const CommOp& op : comm_at_[k]) {
       static const char* names[] = {"send", "recv", "reduce", "bcast", "allreduce"};
       s += std::string(first ? "[" : ",[") + std::to_string(k) + ",\"" + names[op.kind] + "\"," +
-           std::to_string(op.peer) + "," + std::to_string(op.stage) + "]";
+           std::to_string(op.peer) + "," + std::to_string(op.stage) + "," + std::to_string(op.id) + "]";
       first = false;
     }
   return s + "]}";
@@ -1039,7 +1156,7 @@ void Engine::use_replica_weights(int stage, int pipeline) {
 // The optimizer step of stage i (detail::apply_update H/optim.hpp:234-268 / AdamW) on this
 // rank's state: g / update_div -> master, m, v; bf16 working copy + transposed copy rewritten
 // (versioned: into the buffer no replica reads yet); the gradient is zeroed.
-void Engine::optimizer_step(int stage, int step) {
+void Engine::optimizer_step(int stage, int step, cudaStream_t st) {
   GptStage& S = *stages[static_cast<size_t>(stage)];
   if (versioned_) {
     int& cur = cur_buf_[static_cast<size_t>(stage)];
@@ -1050,11 +1167,11 @@ void Engine::optimizer_step(int stage, int step) {
   amdp_opt_args o = rc_.optimizer;
   o.step = step;
   o.grad_scale = rc_.optimizer.grad_scale * (1.0f / update_div_);
-  ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), cs_);
-  const int rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), reinterpret_cast<amdp_stream_t>(cs_));
-  ktimer_.end(cs_);
+  ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), st);
+  const int rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), reinterpret_cast<amdp_stream_t>(st));
+  ktimer_.end(st);
   if (rc != 0) throw std::runtime_error("optimizer step failed");
-  const int nt = S.refresh_transposed(cs_);
+  const int nt = S.refresh_transposed(st);
   if (nt < 0) throw std::runtime_error("weight transpose failed");
   stats.kernels_launched += 1 + nt;
 }
@@ -1103,12 +1220,6 @@ using amdp::Engine;
 
 extern "C" {
 
-int amdp_nccl_unique_id(uint8_t out[128]) {
-  ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return AMDP_ERR_CUDA;
-  std::memcpy(out, &id, sizeof(id));
-  return 0;
-}
 
 amdp_engine* amdp_engine_create(const amdp_model_config* model, const amdp_run_config* run,
                                 const uint8_t* nccl_id, char* err, size_t errlen) {
@@ -1121,6 +1232,30 @@ amdp_engine* amdp_engine_create(const amdp_model_config* model, const amdp_run_c
 }
 
 void amdp_engine_destroy(amdp_engine* e) { delete reinterpret_cast<Engine*>(e); }
+
+size_t amdp_engine_comm_export(amdp_engine* e, uint8_t* buf, size_t len) {
+  try {
+    const std::string b = reinterpret_cast<Engine*>(e)->comm_export();
+    if (buf) std::memcpy(buf, b.data(), std::min(len, b.size()));
+    return b.size();
+  } catch (...) {
+    return 0;
+  }
+}
+
+int amdp_engine_comm_connect(amdp_engine* e, const uint8_t* const* blobs, const size_t* lens, int count, char* err,
+                             size_t errlen) {
+  try {
+    std::vector<std::string> all;
+    for (int r = 0; r < count; ++r)
+      all.emplace_back(reinterpret_cast<const char*>(blobs[r]), lens[r]);
+    reinterpret_cast<Engine*>(e)->comm_connect(all);
+    return 0;
+  } catch (const std::exception& ex) {
+    put_err(err, errlen, ex.what());
+    return AMDP_ERR_CUDA;
+  }
+}
 
 void* amdp_host_alloc(size_t bytes) {
   void* p = nullptr;
@@ -1304,7 +1439,12 @@ ExecuteResult execute(const PolicyConfig& cfg, const ClusterSpec& declared, cons
   rc.record_events = 1;
   rc.data_seed = opt.data_seed;
   rc.depth = declared.depth;
+  rc.comm_backend = opt.comm_backend;
   amdp::Engine eng(opt.model, rc, opt.nccl_id);
+  if (opt.world_size > 1 && opt.comm_backend == AMDP_COMM_IPC) {
+    if (!opt.allgather) throw std::invalid_argument("execute: world_size > 1 needs ExecuteOptions::allgather");
+    eng.comm_connect(opt.allgather(eng.comm_export()));
+  }
   ExecuteResult out;
   out.losses.assign(static_cast<std::size_t>(cfg.num_minibatches), 0.f);
   eng.run(inputs, labels, out.losses.data());

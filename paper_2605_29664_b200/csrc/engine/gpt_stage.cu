@@ -192,6 +192,7 @@ struct Ws {
   float* attn;
   uint8_t* ln;
   uint16_t *rc_o = nullptr, *rc_f = nullptr;  // recompute: this layer's o and f
+  float* rows = nullptr;  // per-token scratch: CE row losses / sorted embedding keys
 };
 Ws carve_ws(const Dims& d, uint8_t* base) {
   Carver c{base};
@@ -205,6 +206,7 @@ Ws carve_ws(const Dims& d, uint8_t* base) {
   w.dhmid = c.take<uint16_t>(T * h);
   w.attn = c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
   w.ln = c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
+  w.rows = c.take<float>(T);
   if (d.recompute) {
     w.rc_o = c.take<uint16_t>(T * h);
     w.rc_f = c.take<uint16_t>(T * d.ffn);
@@ -224,6 +226,7 @@ size_t GptStage::workspace_bytes(const Dims& d) {
   c.take<uint16_t>(T * h);
   c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
   c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
+  c.take<float>(T);
   if (d.recompute) {
     c.take<uint16_t>(T * h);
     c.take<uint16_t>(T * d.ffn);
@@ -295,7 +298,7 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
                                 a.lnf_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm_t(kt, T, d_.V, h, a.lnf, h, false, w + head_.off, h, false, a.logits, d_.V,
                   AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(K_XENT, 0, 6.0 * T * d_.V, amdp_xent_fwd_bwd(a.logits, labels, loss_sum, T, d_.V, d_.V, loss_scale, st), 1);
+    AMDP_TRY(K_XENT, 0, 6.0 * T * d_.V, amdp_xent_fwd_bwd(a.logits, labels, loss_sum, ws.rows, T, d_.V, d_.V, loss_scale, st), 1);
   }
   return launched;
 }
@@ -402,7 +405,7 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
                                 grad + P.ln1_g.off, grad + P.ln1_b.off, ws.ln, T, h, st), 2);
     g = gn;
   }
-  if (first()) AMDP_TRY(K_EMBED, 0, 10.0 * T * h, amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, T, d_.S, h, st), 2);
+  if (first()) AMDP_TRY(K_EMBED, 0, 10.0 * T * h, amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, ws.rows, T, d_.S, h, st), 2);
   hand(ss.ev[F_END], sd, s);  // join: weight gradients complete before the task ends
   return launched;
 }

@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dx_kernel(
 constexpr int LN_DG_ROWS = 64;
 __global__ void __launch_bounds__(256) layernorm_bwd_dgb_kernel(
     const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ mean_in,
-    const float* __restrict__ rstd_in, float* dgamma, float* dbeta, int rows, int cols) {
+    const float* __restrict__ rstd_in, float* __restrict__ part, int rows, int cols) {
+  // per-(row block) partials [gridDim.y][2][cols], summed in a fixed order by
+  // layernorm_dgb_reduce_kernel: deterministic (no atomics)
   __shared__ float red[8][2][256];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 256 + lane * 8;
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_dgb_kernel(
 #pragma unroll
     for (int w = 0; w < 8; ++w) s += red[w][which][col];
     const int gc = blockIdx.x * 256 + col;
-    if (gc < cols) atomicAdd((which ? dbeta : dgamma) + gc, s);
+    if (gc < cols) part[(static_cast<size_t>(blockIdx.y) * 2 + which) * cols + gc] = s;
   }
 }
 
@@ -354,22 +356,65 @@ __global__ void embedding_fwd_kernel(const int32_t* __restrict__ tok, const bf16
   }
 }
 
-__global__ void embedding_bwd_tok_kernel(const int32_t* __restrict__ tok,
-                                         const bf16* __restrict__ dx, float* dwte, int ntok,
-                                         int hidden) {
+// Deterministic token-table gradient: the minibatch's (token, position) keys are sorted in
+// one CTA (bitonic, shared memory), then each run of equal tokens is summed in position order
+// by the single thread owning that (token, 8-column) slice and added to dwte without atomics.
+// The window gradient is therefore bitwise reproducible (and independent of how the stages are
+// spread over GPUs).  Key = token << 14 | position: ntok <= 16384, vocab < 2^18.
+constexpr int EMB_POS_BITS = 14;
+__global__ void __launch_bounds__(1024) embedding_sort_kernel(const int32_t* __restrict__ tok, int ntok,
+                                                              uint32_t* __restrict__ sorted) {
+  extern __shared__ uint32_t keys[];
+  grid_dep_wait();
+  grid_dep_trigger();
+  int n2 = 1;
+  while (n2 < ntok) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x)
+    keys[i] = i < ntok ? (static_cast<uint32_t>(tok[i]) << EMB_POS_BITS) | static_cast<uint32_t>(i) : 0xffffffffu;
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint32_t a = keys[lo], b = keys[hi];
+        if ((a > b) == up) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < ntok; i += blockDim.x) sorted[i] = keys[i];
+}
+
+__global__ void embedding_bwd_tok_kernel(const uint32_t* __restrict__ sorted, const bf16* __restrict__ dx,
+                                         float* __restrict__ dwte, int ntok, int hidden) {
   grid_dep_wait();  // PDL: predecessor's outputs visible from here
   grid_dep_trigger();
   const int vecs = hidden / 8;
   const int64_t total = static_cast<int64_t>(ntok) * vecs;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int t = static_cast<int>(i / vecs);
+    const int k = static_cast<int>(i / vecs);
     const int c = static_cast<int>(i % vecs) * 8;
-    float g[8];
-    load8(dx + static_cast<size_t>(t) * hidden + c, g);
-    float4* dst = reinterpret_cast<float4*>(dwte + static_cast<size_t>(tok[t]) * hidden + c);
-    atomicAdd(dst, make_float4(g[0], g[1], g[2], g[3]));
-    atomicAdd(dst + 1, make_float4(g[4], g[5], g[6], g[7]));
+    const uint32_t t = sorted[k] >> EMB_POS_BITS;
+    if (k > 0 && (sorted[k - 1] >> EMB_POS_BITS) == t) continue;  // not the run's first key
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int r = k;
+    while (r < ntok && (sorted[r] >> EMB_POS_BITS) == t) {
+      float g[8];
+      load8(dx + static_cast<size_t>(sorted[r] & ((1u << EMB_POS_BITS) - 1)) * hidden + c, g);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += g[e];
+      ++r;
+    }
+    float4* dst = reinterpret_cast<float4*>(dwte + static_cast<size_t>(t) * hidden + c);
+    float4 a = dst[0], b = dst[1];
+    a.x += acc[0]; a.y += acc[1]; a.z += acc[2]; a.w += acc[3];
+    b.x += acc[4]; b.y += acc[5]; b.z += acc[6]; b.w += acc[7];
+    dst[0] = a;
+    dst[1] = b;
   }
 }
 
@@ -400,7 +445,7 @@ __global__ void embedding_bwd_pos_kernel(const bf16* __restrict__ dx, float* dwp
 // One CTA per token row: pass 1 online max/sum-exp over the bf16 row, pass 2 writes
 // scale * (softmax - onehot) back in place.  The second read of the row hits L2.
 __global__ void __launch_bounds__(512) xent_kernel(bf16* logits, const int32_t* __restrict__ labels,
-                                                   float* loss_sum, int vocab, int ld,
+                                                   float* __restrict__ row_loss, int vocab, int ld,
                                                    float scale) {
   grid_dep_wait();  // PDL: predecessor's outputs visible from here
   grid_dep_trigger();
@@ -448,7 +493,7 @@ __global__ void __launch_bounds__(512) xent_kernel(bf16* logits, const int32_t* 
     }
     const float lse = M + __logf(S);
     row_lse = lse;
-    if (label >= 0) atomicAdd(loss_sum, lse - __bfloat162float(lr[label]));
+    row_loss[row] = label >= 0 ? lse - __bfloat162float(lr[label]) : 0.f;
   }
   __syncthreads();
   const float lse = row_lse;
@@ -461,6 +506,24 @@ __global__ void __launch_bounds__(512) xent_kernel(bf16* logits, const int32_t* 
       f[e] = (label >= 0) ? scale * (__expf(f[e] - lse) - (col == label ? 1.f : 0.f)) : 0.f;
     }
     store8(lr + v * 8, f);
+  }
+}
+
+// loss_sum[0] += sum of the rows' losses in a fixed order (one CTA): deterministic.
+__global__ void __launch_bounds__(1024) sum_rows_kernel(const float* __restrict__ row_loss, int n,
+                                                        float* loss_sum) {
+  grid_dep_wait();
+  grid_dep_trigger();
+  __shared__ float part[32];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += row_loss[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) loss_sum[0] += t;
   }
 }
 
@@ -532,7 +595,8 @@ static int ln_bwd_ctas(int rows) {
 
 extern "C" size_t amdp_layernorm_bwd_workspace(int rows, int cols) {
   if (rows <= 0 || cols <= 0) return 16;
-  return static_cast<size_t>(ln_bwd_ctas(rows)) * 2 * cols * sizeof(float) + 16;
+  const int parts = std::max(ln_bwd_ctas(rows), (rows + LN_DG_ROWS - 1) / LN_DG_ROWS);
+  return static_cast<size_t>(parts) * 2 * cols * sizeof(float) + 16;
 }
 
 extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const float* gamma,
@@ -542,8 +606,8 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
                                   amdp_stream_t stream) {
   if (rows <= 0 || cols <= 0 || cols % 8 != 0 || cols > LN_MAX_VEC * 256) return AMDP_ERR_INVALID;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!workspace) return AMDP_ERR_INVALID;
   if (ln_row_group_form(cols)) {
-    if (!workspace) return AMDP_ERR_INVALID;
     const int grid = ln_bwd_ctas(rows);
     float* part = static_cast<float*>(workspace);
     launch_pdl(layernorm_bwd_rows_kernel<2>, dim3(grid), dim3(cols / 8), 0, s, 
@@ -566,9 +630,11 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
     else layernorm_bwd_dx_kernel<LN_MAX_VEC><<<blocks, 256, 0, s>>>(dys, xs, gamma, mean, rstd, rs, dxs, rows, cols);
   }
   dim3 g((cols + 255) / 256, (rows + LN_DG_ROWS - 1) / LN_DG_ROWS);
+  float* part = static_cast<float*>(workspace);
   layernorm_bwd_dgb_kernel<<<g, 256, 0, s>>>(reinterpret_cast<const bf16*>(dy),
-                                             reinterpret_cast<const bf16*>(x), mean, rstd, dgamma,
-                                             dbeta, rows, cols);
+                                             reinterpret_cast<const bf16*>(x), mean, rstd, part, rows, cols);
+  launch_pdl(layernorm_dgb_reduce_kernel, dim3((2 * cols + 31) / 32), dim3(1024), 0, s, static_cast<const float*>(part),
+             static_cast<int>(g.y), cols, dgamma, dbeta);
   return cudaGetLastError();
 }
 
@@ -586,15 +652,30 @@ extern "C" int amdp_embedding_fwd(const int32_t* tokens, const uint16_t* wte, co
 }
 
 extern "C" int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, float* dwte,
-                                  float* dwpe, int ntok, int seq, int hidden,
+                                  float* dwpe, void* workspace, int ntok, int seq, int hidden,
                                   amdp_stream_t stream) {
-  if (ntok <= 0 || seq <= 0 || hidden % 8 != 0 || ntok % seq != 0) return AMDP_ERR_INVALID;
+  if (ntok <= 0 || seq <= 0 || hidden % 8 != 0 || ntok % seq != 0 || !workspace) return AMDP_ERR_INVALID;
+  if (ntok > (1 << EMB_POS_BITS)) return AMDP_ERR_INVALID;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int n2 = 1;
+  while (n2 < ntok) n2 <<= 1;
+  const size_t smem = static_cast<size_t>(n2) * sizeof(uint32_t);
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
+    cudaError_t e = cudaFuncSetAttribute(embedding_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sizeof(uint32_t) << EMB_POS_BITS));
+    if (e != cudaSuccess) {
+      attr.store(0);
+      return e;
+    }
+  }
+  uint32_t* sorted = static_cast<uint32_t*>(workspace);
+  launch_pdl(embedding_sort_kernel, dim3(1), dim3(1024), smem, s, tokens, ntok, sorted);
   const int64_t work = static_cast<int64_t>(ntok) * (hidden / 8);
   int blocks = static_cast<int>((work + 255) / 256);
   if (blocks > 16 * num_sms()) blocks = 16 * num_sms();
-  launch_pdl(embedding_bwd_tok_kernel, dim3(blocks), dim3(256), 0, s, tokens, reinterpret_cast<const bf16*>(dx), dwte,
-                                                  ntok, hidden);
+  launch_pdl(embedding_bwd_tok_kernel, dim3(blocks), dim3(256), 0, s, static_cast<const uint32_t*>(sorted),
+             reinterpret_cast<const bf16*>(dx), dwte, ntok, hidden);
   const int pwork = seq * (hidden / 8);
   launch_pdl(embedding_bwd_pos_kernel, dim3((pwork + 255) / 256), dim3(256), 0, s, reinterpret_cast<const bf16*>(dx),
                                                                dwpe, ntok, seq, hidden);
@@ -602,9 +683,12 @@ extern "C" int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, flo
 }
 
 extern "C" int amdp_xent_fwd_bwd(uint16_t* logits, const int32_t* labels, float* loss_sum,
-                                 int ntok, int vocab, int ld, float scale, amdp_stream_t stream) {
-  if (ntok <= 0 || vocab % 8 != 0 || ld % 8 != 0 || ld < vocab) return AMDP_ERR_INVALID;
-  launch_pdl(xent_kernel, dim3(ntok), dim3(512), 0, reinterpret_cast<cudaStream_t>(stream), 
-      reinterpret_cast<bf16*>(logits), labels, loss_sum, vocab, ld, scale);
+                                 float* row_loss, int ntok, int vocab, int ld, float scale,
+                                 amdp_stream_t stream) {
+  if (ntok <= 0 || vocab % 8 != 0 || ld % 8 != 0 || ld < vocab || !row_loss) return AMDP_ERR_INVALID;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  launch_pdl(xent_kernel, dim3(ntok), dim3(512), 0, s, reinterpret_cast<bf16*>(logits), labels, row_loss, vocab, ld,
+             scale);
+  launch_pdl(sum_rows_kernel, dim3(1), dim3(1024), 0, s, static_cast<const float*>(row_loss), ntok, loss_sum);
   return cudaGetLastError();
 }

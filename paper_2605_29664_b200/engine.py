@@ -36,7 +36,9 @@ class _Run(Structure):
     _fields_ = [("policy", P._Policy), ("declared_fwd", P._Rat), ("declared_bwd", P._Rat),
                 ("optimizer", N.OptArgs), ("world_size", c_int), ("rank", c_int),
                 ("record_events", c_int), ("data_seed", c_uint64), ("plan_only", c_int),
-                ("depth", c_int)]
+                ("depth", c_int), ("comm_backend", c_int)]
+
+COMM_IPC, COMM_NCCL = 0, 1
 
 
 class _Stats(Structure):
@@ -78,6 +80,8 @@ _sig("amdp_engine_stage_numel", c_int64, [c_void_p, c_int])
 _sig("amdp_engine_get_stage_params", c_int, [c_void_p, c_int, c_void_p, c_int64])
 _sig("amdp_engine_set_stage_params", c_int, [c_void_p, c_int, c_void_p, c_int64])
 _sig("amdp_engine_plan_json", c_size_t, [c_void_p, c_char_p, c_size_t])
+_sig("amdp_engine_comm_export", c_size_t, [c_void_p, c_void_p, c_size_t])
+_sig("amdp_engine_comm_connect", c_int, [c_void_p, POINTER(c_void_p), POINTER(c_size_t), c_int, c_char_p, c_size_t])
 
 
 @dataclass
@@ -173,6 +177,9 @@ class RunConfig:
     # builder.hpp:145-338 for each policy's tasks and dependencies.
     schedule: str = "AMDP"
     zero: bool = True
+    # world_size > 1: "ipc" (this library's CUDA-IPC peer-memory data plane; also runs
+    # several ranks on one GPU) or "nccl"
+    comm: str = "ipc"
 
     @property
     def num_minibatches(self) -> int:
@@ -201,7 +208,19 @@ class RunConfig:
     def _c(self):
         return _Run(self.policy()._c(), P._r(self.declared_fwd), P._r(self.declared_bwd),
                     self.optimizer._c(), self.world_size, self.rank, int(self.record_events),
-                    self.data_seed, int(self.plan_only), self.depth)
+                    self.data_seed, int(self.plan_only), self.depth,
+                    COMM_NCCL if self.comm == "nccl" else COMM_IPC)
+
+
+def torch_allgather(group=None):
+    """An `allgather` for Engine over an initialised torch.distributed process group."""
+    import torch.distributed as dist
+
+    def gather(blob: bytes):
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, blob, group=group)
+        return out
+    return gather
 
 
 def nccl_unique_id() -> bytes:
@@ -243,7 +262,12 @@ def synthetic_tokens(model: ModelConfig, data_seed: int, first: int, count: int,
 
 
 class Engine:
-    def __init__(self, model: ModelConfig, run: RunConfig, nccl_id: Optional[bytes] = None):
+    """One rank of the executor.  world_size > 1: pass `allgather` (bytes -> list of every
+    rank's bytes, in rank order; e.g. `torch_allgather` over torch.distributed) so the
+    ranks exchange their communication descriptors (IPC backend), or `nccl_id` for NCCL."""
+
+    def __init__(self, model: ModelConfig, run: RunConfig, nccl_id: Optional[bytes] = None,
+                 allgather=None):
         self.model, self.runcfg = model, run
         err = ctypes.create_string_buffer(4096)
         idb = (c_uint8 * 128)(*nccl_id) if nccl_id else None
@@ -252,6 +276,24 @@ class Engine:
         if not h:
             raise RuntimeError("amdp_engine_create: " + err.value.decode())
         self._h = h
+        if run.world_size > 1 and not run.plan_only and run.comm != "nccl":
+            if allgather is None:
+                raise ValueError("world_size > 1 with the IPC backend needs an allgather callable")
+            self.connect(allgather(self.comm_descriptor()))
+
+    def comm_descriptor(self) -> bytes:
+        n = lib.amdp_engine_comm_export(self._h, None, 0)
+        buf = ctypes.create_string_buffer(max(1, n))
+        lib.amdp_engine_comm_export(self._h, buf, n)
+        return buf.raw[:n]
+
+    def connect(self, descriptors: Sequence[bytes]) -> None:
+        bufs = [ctypes.create_string_buffer(bytes(d), max(1, len(d))) for d in descriptors]
+        ptrs = (c_void_p * len(bufs))(*[ctypes.cast(b, c_void_p) for b in bufs])
+        lens = (c_size_t * len(bufs))(*[len(d) for d in descriptors])
+        err = ctypes.create_string_buffer(4096)
+        if lib.amdp_engine_comm_connect(self._h, ptrs, lens, len(bufs), err, len(err)) != 0:
+            raise RuntimeError("amdp_engine_comm_connect: " + err.value.decode())
 
     def close(self):
         if getattr(self, "_h", None):

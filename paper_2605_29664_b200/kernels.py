@@ -98,13 +98,15 @@ def embedding_fwd(tokens, wte, wpe, seq):
 
 def embedding_bwd(tokens, dx, dwte, dwpe, seq):
     ntok, hidden = dx.shape
-    N.check(N.lib.amdp_embedding_bwd(_p(tokens), _p(dx), _p(dwte), _p(dwpe), ntok, seq, hidden,
+    ws = torch.empty(ntok, dtype=torch.int32, device=dx.device)
+    N.check(N.lib.amdp_embedding_bwd(_p(tokens), _p(dx), _p(dwte), _p(dwpe), _p(ws), ntok, seq, hidden,
                                      _stream()), "amdp_embedding_bwd")
 
 
 def xent_fwd_bwd(logits, labels, loss_sum, scale):
     ntok, vocab = logits.shape
-    N.check(N.lib.amdp_xent_fwd_bwd(_p(logits), _p(labels), _p(loss_sum), ntok, vocab,
+    rows = torch.empty(ntok, dtype=torch.float32, device=logits.device)
+    N.check(N.lib.amdp_xent_fwd_bwd(_p(logits), _p(labels), _p(loss_sum), _p(rows), ntok, vocab,
                                     logits.stride(0), scale, _stream()), "amdp_xent_fwd_bwd")
 
 

@@ -37,10 +37,20 @@ def measured_costs(tl: P.Timeline, min_window: int = 1) -> Dict[Tuple[P.Kind, in
 
 
 def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple[P.Kind, int], float],
-                        gap_ns: float, declared_fwd=1, declared_bwd=1, devices: int = 0) -> P.Timeline:
+                        gap_ns: float, declared_fwd=1, declared_bwd=1, devices: int = 0,
+                        update_lane: bool = False, lane_out: dict = None) -> P.Timeline:
     """Re-times the declared dispatch order of `policy` (depth stages on `devices`, default
     depth) with measured costs.  Update tasks (replicated-weight policies) cost what the
-    stage's measured Broadcast (fused optimizer step) cost."""
+    stage's measured Broadcast (fused optimizer step) cost.
+
+    update_lane: the executor's ZeRO window machinery — Reduce on a collective stream and
+    Broadcast (optimizer + weight broadcast) on an update stream.  Such a task starts once
+    its graph predecessors have finished AND the device's compute stream has reached its
+    position in the order (the executor hands the compute stream's progress to it), but it
+    does not hold the compute stream: only its graph successors (BC(w-1,i) -> F / preloaded
+    B, builder.hpp:289-304) wait for it.  In the returned timeline these tasks are
+    zero-length at their finish, so `bubble_ratio` measures compute-stream idle time; their
+    real intervals are appended to `lane_out["events"]` if given."""
     devices = devices or depth
     declared = P.ClusterSpec.uniform(depth, devices, declared_fwd, declared_bwd)
     g = P.build(policy, declared)
@@ -53,16 +63,26 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
     for a, b in g.deps:
         preds[b].append(a)
     free = [0] * devices
+    ufree = [0] * devices
     finish = [0] * len(g.tasks)
     gap = int(round(gap_ns))
     events = []
+    lane_kinds = (P.Kind.Reduce, P.Kind.Broadcast) if update_lane else ()
     for t in tl.order:
         task = g.tasks[t]
         dur = int(round(costs_ns.get((task.kind, task.stage), 0.0)))
-        start = free[task.device]
+        on_lane = task.kind in lane_kinds
+        start = max(free[task.device], ufree[task.device]) if on_lane else free[task.device]
         for p in preds[t]:
             start = max(start, finish[p] + (gap if g.tasks[p].device != task.device else 0))
         finish[t] = start + dur
+        if on_lane:
+            ufree[task.device] = finish[t]
+            if lane_out is not None:
+                lane_out.setdefault("events", []).append((task.kind, task.stage, task.device, start, dur))
+            events.append(P.TaskEvent(task.kind, task.stage, task.minibatch, task.pipeline, task.device,
+                                      Fraction(finish[t]), Fraction(0), task.preloaded, task.window))
+            continue
         free[task.device] = finish[t]
         events.append(P.TaskEvent(task.kind, task.stage, task.minibatch, task.pipeline, task.device,
                                   Fraction(start), Fraction(dur), task.preloaded, task.window))
@@ -72,17 +92,18 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
 def collective_costs(stage_numel, replicas: int, link_gbs: float = 770.0,
                      zero: bool = True) -> Dict[Tuple[P.Kind, int], float]:
     """Window-boundary communication a 1-GPU run does not perform: per stage, the ZeRO Reduce of
-    the fp32 window gradient to the owner and the Broadcast of the fp32 weights over the
-    stage's `replicas` devices, each moving (replicas-1)/replicas of the stage's bytes per
-    device (analysis.hpp:341-346 reduce_broadcast_cost) at the measured peer bandwidth; without
-    ZeRO, the all-reduce of the window gradient (reduce + broadcast volume) in every Update."""
+    the fp32 window gradient to the owner (4 B/param) and the Broadcast of the bf16 weights
+    (2 B/param; the LayerNorm parameters' fp32 copy is negligible) over the stage's `replicas`
+    devices, each moving (replicas-1)/replicas of those bytes per device
+    (analysis.hpp:341-346 reduce_broadcast_cost) at the measured peer bandwidth; without ZeRO,
+    the all-reduce of the fp32 window gradient (reduce + broadcast volume) in every Update."""
     f = (replicas - 1) / replicas if replicas > 1 else 0.0
     out = {}
     for s, n in enumerate(stage_numel):
         t = f * 4.0 * n / (link_gbs * 1e9) * 1e9
         if zero:
             out[(P.Kind.Reduce, s)] = t
-            out[(P.Kind.Broadcast, s)] = t
+            out[(P.Kind.Broadcast, s)] = t / 2
         else:
             out[(P.Kind.Update, s)] = 2 * t
     return out
@@ -109,13 +130,18 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
     for s in range(depth):  # an Update steps the optimizer: a ZeRO run measured that as Broadcast
         if (P.Kind.Update, s) not in costs and (P.Kind.Broadcast, s) in costs:
             costs[(P.Kind.Update, s)] = costs[(P.Kind.Broadcast, s)]
+    lane = bool(pol.zero_enabled)  # the executor's update / collective streams (ZeRO)
     if stage_numel is not None and replicas_of(pol) > 1:
-        rep0 = static_order_replay(pol, depth, costs, gap_ns, devices=devices)
+        rep0 = static_order_replay(pol, depth, costs, gap_ns, devices=devices, update_lane=lane)
         bubble_nc = float(P.bubble_ratio(rep0, 1 if windows > 2 else 0))
         for k, v in collective_costs(stage_numel, replicas_of(pol), zero=pol.zero_enabled).items():
             costs[k] = costs.get(k, 0.0) + v
-    rep = static_order_replay(pol, depth, costs, gap_ns, devices=devices)
+    lane_out = {}
+    rep = static_order_replay(pol, depth, costs, gap_ns, devices=devices, update_lane=lane, lane_out=lane_out)
     bubble = P.bubble_ratio(rep, 1 if windows > 2 else 0)
+    # the same costs with the window machinery serialised on the compute stream (round-1 executor)
+    serial = static_order_replay(pol, depth, costs, gap_ns, devices=devices) if lane else rep
+    bubble_serial = float(P.bubble_ratio(serial, 1 if windows > 2 else 0))
     # steady-state window period: first F of window w to first F of window w+1, averaged
     firsts = {}
     for ev in rep.flat():
@@ -124,14 +150,20 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
     ws = sorted(firsts)
     period = float(firsts[ws[-1]] - firsts[ws[1]]) / (len(ws) - 2) if len(ws) > 2 else None
     return {"gpus": devices, "bubble": float(bubble), "bubble_without_collectives": bubble_nc,
+            "bubble_window_machinery_serialised": bubble_serial,
+            "update_lane": "Reduce / Broadcast on the collective / update streams, off the compute stream"
+                           if lane else "Update tasks on the compute stream",
             "tokens_per_s": (threshold * tokens_per_minibatch / (period * 1e-9)) if period else None,
             "gap_us": gap_ns / 1e3,
             "stage_ms": {f"{KIND_TAG[k[0]]}{k[1]}": round(v / 1e6, 3) for k, v in sorted(costs.items())},
             "method": "static-order replay of the declared dispatch order on one GPU per "
                       "logical device, task costs = measured 1-GPU means (windows >= 1) plus the "
-                      "window Reduce/Broadcast collectives (or the replicated Update's all-reduce) at "
-                      "770 GB/s ((P-1)/P of the stage's fp32 bytes per phase), inter-device gap = activation bytes / 770 GB/s peer copy; bubble = "
-                      "reference bubble_ratio(tl, 1).  A projection, not a multi-GPU measurement."}
+                      "window Reduce (fp32) / Broadcast (bf16) collectives (or the replicated Update's "
+                      "all-reduce) at 770 GB/s ((P-1)/P of the stage's bytes per phase); ZeRO Reduce / "
+                      "Broadcast on the update lane (start when the compute stream reaches them, only "
+                      "their graph successors wait); inter-device gap = activation bytes / 770 GB/s peer "
+                      "copy; bubble = reference bubble_ratio(tl, 1) of the compute streams.  A projection, "
+                      "not a multi-GPU measurement."}
 
 
 # Schedules of the paper's comparison (reference builder.hpp policies) on the same D stages /

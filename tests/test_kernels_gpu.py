@@ -282,6 +282,41 @@ def test_embedding(K):
     assert _rel(dwpe, rpe) < 1e-5
 
 
+@pytest.mark.parametrize("ntok,S,V,Hd", [(2048, 512, 30528, 1024), (8192, 2048, 50304, 256), (16384, 2048, 50304, 64)])
+def test_embedding_bwd_deterministic(K, ntok, S, V, Hd):
+    """The token-table gradient has no atomics: heavily repeated tokens (a BERT [MASK]-like id on
+    15% of positions) give bitwise-identical results run to run and match the fp32 sum; the
+    largest supported minibatch (16384 tokens) works."""
+    torch.manual_seed(8)
+    tok = torch.randint(0, V, (ntok,), device="cuda", dtype=torch.int32)
+    tok[torch.rand(ntok, device="cuda") < 0.15] = V - 1
+    dx = torch.randn(ntok, Hd, device="cuda").bfloat16()
+    outs = []
+    for _ in range(3):
+        dwte = torch.full((V, Hd), 0.25, device="cuda")
+        dwpe = torch.zeros(S, Hd, device="cuda")
+        K.embedding_bwd(tok, dx, dwte, dwpe, S)
+        outs.append(dwte)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    rte = torch.full((V, Hd), 0.25, device="cuda", dtype=torch.float64).index_add_(0, tok.long(), dx.double())
+    assert _rel(outs[0], rte) < 1e-6
+
+
+def test_xent_loss_deterministic(K):
+    """The loss sum is a fixed-order reduction of per-row losses: bitwise repeatable."""
+    torch.manual_seed(9)
+    ntok, V = 4096, 50304
+    logits = (3 * torch.randn(ntok, V, device="cuda")).bfloat16()
+    labels = torch.randint(0, V, (ntok,), device="cuda", dtype=torch.int32)
+    vals = []
+    for _ in range(3):
+        loss = torch.zeros(1, device="cuda")
+        K.xent_fwd_bwd(logits.clone(), labels, loss, 1.0 / ntok)
+        vals.append(loss.item())
+    assert vals[0] == vals[1] == vals[2]
+
+
 @pytest.mark.parametrize("ntok,V", [(256, 1024), (512, 50304), (64, 30528)])
 def test_xent(K, ntok, V):
     torch.manual_seed(6)

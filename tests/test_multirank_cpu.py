@@ -26,46 +26,47 @@ def _plans(world, windows=2, depth=8, thr=32):
 
 def _check(plans, depth=8):
     world = len(plans)
-    per = depth // world
+    fold = plans[0]["device_rank"]
     for r, pl in enumerate(plans):
+        assert pl["device_rank"] == fold
         hosted = {s["stage"] for s in pl["stages"] if s["hosted"]}
         want = {i for i in range(depth) for p in range(depth // 2)
-                if P.map_stage_to_device(p, i, depth) // per == r}
+                if fold[P.map_stage_to_device(p, i, depth)] == r}
         assert hosted == want
         for s in pl["stages"]:
-            assert s["owner"] == (s["stage"] // per == r)
-            grp = sorted({P.map_stage_to_device(p, s["stage"], depth) // per for p in range(depth // 2)})
+            assert s["owner"] == (fold[s["stage"]] == r)  # ZeRO owner: the rank of device i
+            grp = sorted({fold[P.map_stage_to_device(p, s["stage"], depth)] for p in range(depth // 2)})
             assert s["group"] == grp
-    # p2p pairing
+    # p2p pairing (message ids agree), collectives issued by exactly the replica group
     ops = [[tuple(o) for o in pl["comm_ops"]] for pl in plans]
     for r in range(world):
-        for (k, kind, peer, stage) in ops[r]:
+        for (k, kind, peer, stage, mid) in ops[r]:
             if kind == "send":
-                assert (k, "recv", r, -1) in ops[peer], (r, k, peer)
+                assert (k, "recv", r, -1, mid) in ops[peer], (r, k, peer)
             elif kind == "recv":
-                assert (k, "send", r, -1) in ops[peer], (r, k, peer)
+                assert (k, "send", r, -1, mid) in ops[peer], (r, k, peer)
             else:
                 members = plans[r]["stages"][stage]["group"]
                 for m in members:
-                    assert (k, kind, -1, stage) in ops[m]
-    # rendezvous simulation of the joint program
+                    assert (k, kind, -1, stage, mid) in ops[m]
+    # rendezvous simulation of the joint program (NCCL backend: one stream per rank)
     pos = [0] * world
     while True:
         progressed = False
         for r in range(world):
             if pos[r] >= len(ops[r]):
                 continue
-            k, kind, peer, stage = ops[r][pos[r]]
+            k, kind, peer, stage, mid = ops[r][pos[r]]
             if kind in ("send", "recv"):
                 if pos[peer] < len(ops[peer]):
-                    k2, kind2, peer2, _ = ops[peer][pos[peer]]
-                    if k2 == k and peer2 == r and kind2 != kind:
+                    k2, kind2, peer2, _, mid2 = ops[peer][pos[peer]]
+                    if k2 == k and peer2 == r and kind2 != kind and mid2 == mid:
                         pos[r] += 1
                         pos[peer] += 1
                         progressed = True
             else:
                 members = plans[r]["stages"][stage]["group"]
-                if all(pos[m] < len(ops[m]) and ops[m][pos[m]] == (k, kind, -1, stage) for m in members):
+                if all(pos[m] < len(ops[m]) and ops[m][pos[m]] == (k, kind, -1, stage, mid) for m in members):
                     for m in members:
                         pos[m] += 1
                     progressed = True
@@ -78,18 +79,32 @@ def _check(plans, depth=8):
 def test_rank_plans_pair_and_cannot_deadlock(world):
     n = _check(_plans(world))
     if world == 1:
-        assert n == 0  # all replicas co-resident: no NCCL traffic at all
+        assert n == 0  # all replicas co-resident: no traffic at all
     else:
         assert n > 0
 
 
-def test_folding_within_replica_groups_shares_weights():
-    # world 4 folds devices {0,1},{2,3},{4,5},{6,7}: each rank hosts the stages of its two
-    # logical devices; co-resident replicas share one weight/grad buffer (ZeRO broadcast
-    # rewrites all replicas at once, H/builder.hpp:272-304)
-    plans = _plans(4)
-    for pl in plans:
-        assert sum(s["hosted"] for s in pl["stages"]) <= 8
+@pytest.mark.parametrize("world,fold,hosted,group_size", [
+    (1, [0] * 8, [set(range(8))], 1),
+    # components of map_stage_to_device at d=8: {0,3,4,7} and {1,2,5,6} (H/builder.hpp:81-88)
+    (2, [0, 1, 1, 0, 0, 1, 1, 0], [{0, 3, 4, 7}, {1, 2, 5, 6}], 1),
+    (4, [0, 2, 2, 0, 1, 3, 3, 1], [{0, 3, 4, 7}, {0, 3, 4, 7}, {1, 2, 5, 6}, {1, 2, 5, 6}], 2),
+    (8, list(range(8)), None, 4),
+])
+def test_fold_within_replica_groups(world, fold, hosted, group_size):
+    """Logical devices fold onto ranks within replica groups: at N=2 every stage lives on one
+    GPU (no collective at all), at N=4 every stage spans 2 ranks, at N=8 its 4 devices."""
+    plans = _plans(world)
+    assert plans[0]["device_rank"] == fold
+    for r, pl in enumerate(plans):
+        if hosted is not None:
+            assert {s["stage"] for s in pl["stages"] if s["hosted"]} == hosted[r]
+        for s in pl["stages"]:
+            assert len(s["group"]) == group_size
+        assert pl["collectives"] == (0 if group_size == 1 else 2 * 8 * 2)  # R + BC per stage per window
+        kinds = {o[1] for o in pl["comm_ops"]}
+        if world == 2:
+            assert kinds == {"send", "recv"}
 
 
 def _gloo_worker(rank, world, port, q):
@@ -142,6 +157,8 @@ def test_synchronous_baselines_plan(schedule, world):
                           schedule=schedule)
         plans.append(E.Engine(model, run).plan())
     per = 8 // world
+    fold = plans[0]["device_rank"]
+    assert fold == [d // per for d in range(8)]  # no shared stages: contiguous fold
     for r, pl in enumerate(plans):
         for s in pl["stages"]:
             assert s["hosted"] == (s["stage"] // per == r)
@@ -150,8 +167,8 @@ def test_synchronous_baselines_plan(schedule, world):
         assert all(o[1] in ("send", "recv") for o in pl["comm_ops"])
     ops = [[tuple(o) for o in pl["comm_ops"]] for pl in plans]
     for r in range(world):
-        for (k, kind, peer, stage) in ops[r]:
-            assert (k, "recv" if kind == "send" else "send", r, -1) in ops[peer]
+        for (k, kind, peer, stage, mid) in ops[r]:
+            assert (k, "recv" if kind == "send" else "send", r, -1, mid) in ops[peer]
 
 
 @pytest.mark.parametrize("schedule,zero", [("AMDP", False), ("Chimera", False)])
@@ -169,7 +186,7 @@ def test_replicated_update_plans(schedule, zero, world):
         run = E.RunConfig(depth=8, threshold=thr, windows=2, world_size=world, rank=r, plan_only=True,
                           schedule=schedule, zero=zero)
         plans.append(E.Engine(model, run).plan())
-    per = 8 // world
+    fold = plans[0]["device_rank"]
     if schedule == "Chimera":
         dev = lambda p, i: i if p == 0 else 7 - i  # noqa: E731  (builder.hpp:160)
         pipes = 2
@@ -178,7 +195,7 @@ def test_replicated_update_plans(schedule, zero, world):
         pipes = 4
     for r, pl in enumerate(plans):
         for s in pl["stages"]:
-            grp = sorted({dev(p, s["stage"]) // per for p in range(pipes)})
+            grp = sorted({fold[dev(p, s["stage"])] for p in range(pipes)})
             assert s["group"] == grp
             assert s["hosted"] == (r in grp)
             assert s["owner"] == s["hosted"]  # replicated optimizer state
@@ -199,27 +216,27 @@ def _check_joint(plans):
     world = len(plans)
     ops = [[tuple(o) for o in pl["comm_ops"]] for pl in plans]
     for r in range(world):
-        for (k, kind, peer, stage) in ops[r]:
+        for (k, kind, peer, stage, mid) in ops[r]:
             if kind in ("send", "recv"):
-                assert (k, "recv" if kind == "send" else "send", r, -1) in ops[peer]
+                assert (k, "recv" if kind == "send" else "send", r, -1, mid) in ops[peer]
             else:
                 for m in plans[r]["stages"][stage]["group"]:
-                    assert (k, kind, -1, stage) in ops[m]
+                    assert (k, kind, -1, stage, mid) in ops[m]
     pos = [0] * world
     while not all(pos[r] >= len(ops[r]) for r in range(world)):
         progressed = False
         for r in range(world):
             if pos[r] >= len(ops[r]):
                 continue
-            k, kind, peer, stage = ops[r][pos[r]]
+            k, kind, peer, stage, mid = ops[r][pos[r]]
             if kind in ("send", "recv"):
-                if pos[peer] < len(ops[peer]) and ops[peer][pos[peer]][:3] == (k, "recv" if kind == "send" else "send", r):
+                if pos[peer] < len(ops[peer]) and ops[peer][pos[peer]] == (k, "recv" if kind == "send" else "send", r, -1, mid):
                     pos[r] += 1
                     pos[peer] += 1
                     progressed = True
             else:
                 members = plans[r]["stages"][stage]["group"]
-                if all(pos[m] < len(ops[m]) and ops[m][pos[m]] == (k, kind, -1, stage) for m in members):
+                if all(pos[m] < len(ops[m]) and ops[m][pos[m]] == (k, kind, -1, stage, mid) for m in members):
                     for m in members:
                         pos[m] += 1
                     progressed = True

@@ -81,3 +81,37 @@ def test_gantt_svg_renders_every_task():
     root = ET.fromstring(svg)
     bars = [r for r in root.iter("{http://www.w3.org/2000/svg}rect") if r.find("{http://www.w3.org/2000/svg}title") is not None]
     assert len(bars) == sum(1 for e in tl.flat() if e.duration > 0)
+
+
+def test_update_lane_takes_window_machinery_off_the_compute_stream():
+    """ZeRO Reduce / Broadcast on the update lane (the executor's collective / update streams):
+    they start only after their graph predecessors and the device's compute up to their order
+    position, every successor (BC(w-1,i) -> F / preloaded B) still waits for them, and the
+    compute-stream bubble is no larger than with the machinery serialised on the compute stream."""
+    d, thr, windows = 8, 32, 4
+    pol = _pol(d, thr, windows)
+    costs = {}
+    for s in range(d):
+        costs[(P.Kind.Forward, s)] = 1000.0
+        costs[(P.Kind.Backward, s)] = 2000.0
+        costs[(P.Kind.Reduce, s)] = 400.0
+        costs[(P.Kind.Broadcast, s)] = 900.0
+    lane = {}
+    rep = PR.static_order_replay(pol, d, costs, 30.0, update_lane=True, lane_out=lane)
+    ser = PR.static_order_replay(pol, d, costs, 30.0)
+    assert P.bubble_ratio(rep, 1) <= P.bubble_ratio(ser, 1)
+    assert max(e.finish() for e in rep.flat()) <= max(e.finish() for e in ser.flat())
+    g = P.build(pol, P.ClusterSpec.uniform(d, d, 1, 1))
+    fin = {}
+    for e in rep.flat():
+        fin[(e.kind, e.stage, e.minibatch, e.pipeline)] = e.finish()
+    # lane tasks appear as zero-length events at their finish; their successors start after it
+    for a, b in g.deps:
+        ta, tb = g.tasks[a], g.tasks[b]
+        if ta.kind == P.Kind.Broadcast:
+            fa = fin[(ta.kind, ta.stage, ta.minibatch, ta.pipeline)]
+            sb = next(e.start for e in rep.flat() if (e.kind, e.stage, e.minibatch, e.pipeline) ==
+                      (tb.kind, tb.stage, tb.minibatch, tb.pipeline))
+            assert sb >= fa
+    assert len(lane["events"]) == 2 * d * windows
+    assert all(dur in (400, 900) for (_, _, _, _, dur) in lane["events"])
