@@ -354,8 +354,9 @@ def main():
             numel = [lib_numel(eng, i) for i in range(args.depth)]
             pol = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=args.steps,
                               schedule=args.schedule, zero=zero).policy()
+            lanes = eng.lane_events()
             projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
-                                    stage_numel=numel, policy=pol)
+                                    stage_numel=numel, policy=pol, lane_events=lanes)
             if args.schedule == "AMDP" and zero:
                 # the same measured costs under AMDP's other update mode: replicated weights,
                 # window gradient all-reduced over the stage's devices, every replica stepping
@@ -364,7 +365,7 @@ def main():
                 alt = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=args.steps,
                                   schedule="AMDP", zero=False).policy()
                 pa = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
-                                stage_numel=numel, policy=alt)
+                                stage_numel=numel, policy=alt, lane_events=lanes)
                 projection["allreduce_update_variant"] = {k: pa[k] for k in
                                                           ("bubble", "bubble_without_collectives", "tokens_per_s")}
         except Exception as e:  # never let the projection break the bench line

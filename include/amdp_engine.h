@@ -45,6 +45,11 @@ typedef struct amdp_model_config {
    * recomputes both from u / qkv (weight-independent, so exact under AMDP's staleness);
    * activation slots shrink by 5/16 (the rebuilt o / f live in the shared workspace). */
   int recompute;
+  /* 1 = fp32 validation mode: activations, weights and every product in fp32 on the CUDA
+   * cores (amdp_f32_* kernels) instead of the bf16 tcgen05 path, so that losses / weights
+   * match the fp64 CPU oracle at a tolerance far below bf16's (north_star).  Slow; for
+   * correctness runs, not throughput. */
+  int fp32_validation;
 } amdp_model_config;
 
 typedef struct amdp_run_config {
@@ -146,6 +151,12 @@ int amdp_engine_stats(const amdp_engine* e, amdp_run_stats* out);
  * logical devices hosted by this rank only.  Pass to amdp_timeline_new for analyses. */
 int amdp_engine_num_events(const amdp_engine* e);
 int amdp_engine_events(const amdp_engine* e, amdp_event* out, int cap);
+/* The window machinery's own intervals: ZeRO Reduce (collective stream) and Broadcast
+ * (optimizer step + weight broadcast on the update stream) run beside the compute stream;
+ * the Timeline above shows each where the compute stream passed it (the reference's
+ * one-task-per-device model, so its validators apply), these events their real extent. */
+int amdp_engine_num_lane_events(const amdp_engine* e);
+int amdp_engine_lane_events(const amdp_engine* e, amdp_event* out, int cap);
 /* Parameter version each Forward/Backward actually read on the GPU (device-side
  * counter per stage, bumped by the optimizer step), as version_trace_csv text. */
 size_t amdp_engine_version_trace(const amdp_engine* e, char* buf, size_t len);

@@ -137,6 +137,35 @@ int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, float* dwte, f
 int amdp_xent_fwd_bwd(uint16_t* logits, const int32_t* labels, float* loss_sum, float* row_loss,
                       int ntok, int vocab, int ld, float scale, amdp_stream_t stream);
 
+/* ---------------------------------------------------------------- fp32 validation mode
+ * The stage math in fp32 end to end on the CUDA cores (no bf16 storage, no tensor-core or SFU
+ * approximations), deterministic: the engine's fp32 validation mode
+ * (amdp_model_config.fp32_validation) runs these instead of the bf16 tcgen05 kernels so that
+ * losses / weights can be checked against the fp64 CPU oracle at a tight tolerance.  Same
+ * argument conventions as the bf16 kernels above with float tensors (GEMM: every epilogue
+ * except AMDP_EPI_ROWDOT; C, C2, aux are fp32).                                       */
+int amdp_f32_gemm(const amdp_gemm_args* args, amdp_stream_t stream);
+int amdp_f32_layernorm_fwd(const float* x, const float* gamma, const float* beta, float* y,
+                           float* mean, float* rstd, int rows, int cols, float eps,
+                           amdp_stream_t stream);
+int amdp_f32_layernorm_bwd(const float* dy, const float* x, const float* gamma,
+                           const float* mean, const float* rstd, const float* resid_grad,
+                           float* dx, float* dgamma, float* dbeta, int rows, int cols,
+                           amdp_stream_t stream);
+int amdp_f32_attention_fwd(const float* qkv, float* out, float* lse, int batch, int seq,
+                           int heads, int head_dim, int causal, amdp_stream_t stream);
+size_t amdp_f32_attention_bwd_workspace(int batch, int seq, int heads);
+int amdp_f32_attention_bwd(const float* qkv, const float* out, const float* dout,
+                           const float* lse, float* dqkv, float* workspace, int batch, int seq,
+                           int heads, int head_dim, int causal, amdp_stream_t stream);
+int amdp_f32_embedding_fwd(const int32_t* tokens, const float* wte, const float* wpe, float* x,
+                           int ntok, int seq, int hidden, amdp_stream_t stream);
+int amdp_f32_embedding_bwd(const int32_t* tokens, const float* dx, float* dwte, float* dwpe,
+                           void* workspace, int ntok, int seq, int hidden, amdp_stream_t stream);
+int amdp_f32_xent_fwd_bwd(float* logits, const int32_t* labels, float* loss_sum,
+                          float* row_loss, int ntok, int vocab, int ld, float scale,
+                          amdp_stream_t stream);
+
 /* ---------------------------------------------------------------- optimizer
  * One fused pass per parameter: g = grad (fp32, then zeroed), state update, fp32
  * master update, bf16 copy refresh.  Modes:

@@ -61,6 +61,7 @@ def _sig(name, restype, argtypes):
 
 _P = c_void_p
 _sig("amdp_gemm", c_int, [POINTER(GemmArgs), _P])
+_sig("amdp_f32_gemm", c_int, [POINTER(GemmArgs), _P])
 _sig("amdp_attention_fwd", c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
 _sig("amdp_attention_bwd_workspace", c_size_t, [c_int, c_int, c_int, c_int])
 _sig("amdp_attention_bwd", c_int,

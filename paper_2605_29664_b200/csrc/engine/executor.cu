@@ -166,6 +166,7 @@ class Engine {
   // results
   amdp_run_stats stats{};
   std::vector<ppsim::TaskEvent> events;  // measured, this rank's logical devices
+  std::vector<ppsim::TaskEvent> lane_events;  // Reduce / Broadcast on their own streams
   std::vector<int> version_seen;         // per task id (-1 if not local)
   SchedHandle sched;                     // declared graph + timeline + order
   std::vector<std::unique_ptr<GptStage>> stages;
@@ -222,6 +223,11 @@ class Engine {
   float* d_loss_ = nullptr;
   int *d_ver_ = nullptr, *d_trace_ = nullptr;
   std::vector<cudaEvent_t> ev_start_, ev_end_;
+  // window machinery's own intervals on the collective / update streams (Reduce, Broadcast);
+  // the Timeline shows those tasks where the compute stream passed them (the reference's
+  // one-task-at-a-time device model), lane_events their real extent
+  std::vector<cudaEvent_t> ev_lstart_, ev_lend_;
+  std::vector<char> lane_rec_;
   cudaEvent_t run_begin_ = nullptr, run_end_ = nullptr;
   size_t slot_total_ = 0;
   int64_t measured_alloc_bytes_ = -1;  // cudaMemGetInfo delta across allocate() (-1: plan only)
@@ -297,6 +303,8 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   dm.causal = mc.causal != 0;
   dm.ln_eps = mc.ln_eps > 0 ? mc.ln_eps : 1e-5f;
   dm.recompute = mc.recompute != 0;
+  dm.fp32 = mc.fp32_validation != 0;
+  if (dm.fp32 && dm.recompute) throw std::invalid_argument("engine: fp32 validation mode stores every activation (no recompute)");
   if (dm.h % dm.heads != 0) throw std::invalid_argument("engine: hidden must divide into heads");
 
   // schedule: build + order on the declared cost model
@@ -384,7 +392,15 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     return;
   }
   CUDA_OK(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
-  CUDA_OK(cudaStreamCreateWithFlags(&us_, cudaStreamNonBlocking));
+  // the window machinery and the data plane run at the highest stream priority: their few,
+  // short kernels (optimizer step, transposes, peer reductions, flag signals) then take SMs
+  // as the persistent stage GEMMs retire instead of queueing behind the next ones, which is
+  // what keeps a Broadcast's latency — the one the gated forwards wait for — short
+  int prio_lo = 0, prio_hi = 0;
+  CUDA_OK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  static const bool no_prio = getenv("AMDP_NO_UPDATE_PRIORITY") != nullptr;
+  const int hi = no_prio ? prio_lo : prio_hi;
+  CUDA_OK(cudaStreamCreateWithPriority(&us_, cudaStreamNonBlocking, hi));
   if (!getenv("AMDP_NO_SIDE_STREAM")) {
     CUDA_OK(cudaStreamCreateWithFlags(&side_.side, cudaStreamNonBlocking));
     for (auto& e : side_.ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -395,12 +411,12 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     else
       comm_ = make_ipc_comm(world_, rank_, nmsg_, ncoll_);
     if (comm_->single_stream()) {
-      CUDA_OK(cudaStreamCreateWithFlags(&rs_, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithPriority(&rs_, cudaStreamNonBlocking, hi));
       ss_ = ks_ = rs_;
     } else {
-      CUDA_OK(cudaStreamCreateWithFlags(&rs_, cudaStreamNonBlocking));
-      CUDA_OK(cudaStreamCreateWithFlags(&ss_, cudaStreamNonBlocking));
-      CUDA_OK(cudaStreamCreateWithFlags(&ks_, cudaStreamNonBlocking));
+      CUDA_OK(cudaStreamCreateWithPriority(&rs_, cudaStreamNonBlocking, hi));
+      CUDA_OK(cudaStreamCreateWithPriority(&ss_, cudaStreamNonBlocking, hi));
+      CUDA_OK(cudaStreamCreateWithPriority(&ks_, cudaStreamNonBlocking, hi));
     }
   }
   ev_pool_.resize(64);
@@ -455,6 +471,10 @@ Engine::~Engine() {
   cudaFree(d_trace_);
   for (auto e : ev_start_) cudaEventDestroy(e);
   for (auto e : ev_end_) cudaEventDestroy(e);
+  for (auto e : ev_lstart_)
+    if (e) cudaEventDestroy(e);
+  for (auto e : ev_lend_)
+    if (e) cudaEventDestroy(e);
   for (auto e : wready_) cudaEventDestroy(e);
   for (auto e : reduced_) cudaEventDestroy(e);
   for (auto e : ev_pool_) cudaEventDestroy(e);
@@ -660,10 +680,11 @@ void Engine::allocate() {
   }
   // boundary buffers: one arena (one IPC export), buffer b at b * T * h elements
   bufs_.resize(static_cast<size_t>(nbuf));
-  if (nbuf > 0) CUDA_OK(cudaMalloc(&bounds_arena_, static_cast<size_t>(nbuf) * T * h * sizeof(uint16_t)));
+  const size_t ab = dm.act_bytes();
+  if (nbuf > 0) CUDA_OK(cudaMalloc(&bounds_arena_, static_cast<size_t>(nbuf) * T * h * ab));
   for (size_t k = 0; k < bufs_.size(); ++k) {
     BoundaryBuf& b = bufs_[k];
-    b.ptr = bounds_arena_ + k * T * h;
+    b.ptr = bounds_arena_ + k * T * h * (ab / 2);
     CUDA_OK(cudaEventCreateWithFlags(&b.comm_done, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&b.used, cudaEventDisableTiming));
   }
@@ -679,8 +700,8 @@ void Engine::allocate() {
   for (auto& e : wready_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : reduced_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (comm_) {  // what peers may read: boundary arena, and per hosted stage grad / w / master
-    if (bounds_arena_) comm_->register_region(REG_BOUNDS, 0, bounds_arena_, static_cast<size_t>(nbuf) * T * h * 2);
-    for (const auto& [msg, b] : planned_sends_) comm_->plan_send(msg, static_cast<size_t>(b) * T * h * 2);
+    if (bounds_arena_) comm_->register_region(REG_BOUNDS, 0, bounds_arena_, static_cast<size_t>(nbuf) * T * h * ab);
+    for (const auto& [msg, b] : planned_sends_) comm_->plan_send(msg, static_cast<size_t>(b) * T * h * ab);
     for (int i = 0; i < depth_; ++i) {
       if (!hosted[static_cast<size_t>(i)] || group_ranks_[static_cast<size_t>(i)].size() < 2) continue;
       GptStage& st = *stages[static_cast<size_t>(i)];
@@ -723,7 +744,7 @@ void Engine::init_weights() {
 // compute use of its destination buffer (not for all earlier compute of the rank).
 void Engine::exec_comm(int pos) {
   for (const CommOp& op : comm_at_[static_cast<size_t>(pos)]) {
-    const size_t bytes = static_cast<size_t>(dm.T) * static_cast<size_t>(dm.h) * 2;
+    const size_t bytes = static_cast<size_t>(dm.T) * static_cast<size_t>(dm.h) * dm.act_bytes();
     switch (op.kind) {
       case CommOp::Send: {
         BoundaryBuf& b = bufs_[static_cast<size_t>(op.buf)];
@@ -771,9 +792,12 @@ void Engine::zero_broadcast(int i, int window) {
   const bool multi = gr.size() > 1;
   CUDA_OK(cudaStreamWaitEvent(us_, handoff(cs_), 0));
   if (multi) CUDA_OK(cudaStreamWaitEvent(us_, reduced_[static_cast<size_t>(i)], 0));
-  // the measured Broadcast event is the update stream's interval (it overlaps other stages'
+  // the update stream's interval of this Broadcast (a lane event: it overlaps other stages'
   // compute on this GPU; projection.py models the update lane separately)
-  if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(cur_pos_)], us_));
+  if (rc_.record_events) {
+    CUDA_OK(cudaEventRecord(ev_lstart_[static_cast<size_t>(cur_pos_)], us_));
+    lane_rec_[static_cast<size_t>(cur_pos_)] = 1;
+  }
   cudaStream_t bs = us_;  // broadcast stream
   if (multi && comm_->single_stream()) bs = ks_;
   if (owned[static_cast<size_t>(i)]) {
@@ -786,9 +810,13 @@ void Engine::zero_broadcast(int i, int window) {
     for (const CommOp& op : comm_at_[static_cast<size_t>(cur_pos_)])
       if (op.kind == CommOp::Bcast && op.stage == i) coll = op.id;
     std::vector<Span> spans;
-    spans.push_back(Span{REG_W, i, 0, static_cast<size_t>(S.numel()) * 2});
-    for (const auto& p : S.params())
-      if (p.rows == 1) spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(p.off) * 4, static_cast<size_t>(p.numel()) * 4});
+    if (dm.fp32) {  // fp32 validation mode: the kernels read the fp32 master itself
+      spans.push_back(Span{REG_MASTER, i, 0, static_cast<size_t>(S.numel()) * 4});
+    } else {  // bf16 working weights + the fp32 LayerNorm parameters the kernels read
+      spans.push_back(Span{REG_W, i, 0, static_cast<size_t>(S.numel()) * 2});
+      for (const auto& p : S.params())
+        if (p.rows == 1) spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(p.off) * 4, static_cast<size_t>(p.numel()) * 4});
+    }
     if (bs != us_) CUDA_OK(cudaStreamWaitEvent(bs, handoff(us_), 0));
     comm_->broadcast(coll, gr, owner_rank(i), i, spans, bs);
     if (bs != us_) CUDA_OK(cudaStreamWaitEvent(us_, handoff(bs), 0));
@@ -802,7 +830,7 @@ void Engine::zero_broadcast(int i, int window) {
     }
   }
   CUDA_OK(cudaEventRecord(wready_[static_cast<size_t>(i)], us_));
-  if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(cur_pos_)], us_));
+  if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_lend_[static_cast<size_t>(cur_pos_)], us_));
   wpending_[static_cast<size_t>(i)] = 1;
 }
 
@@ -895,11 +923,16 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
   if (task.kind == ppsim::Kind::Reduce) {
     // the reduction runs on the collective stream (its measured interval); the update stream's
     // Broadcast waits for it
-    cudaStream_t rs = comm_at_[static_cast<size_t>(pos)].empty() ? cs_ : ks_;
-    if (rc_.record_events && rs == ks_) CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], rs));
+    const bool lane = !comm_at_[static_cast<size_t>(pos)].empty();
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events && lane) {
+      CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));
+      CUDA_OK(cudaEventRecord(ev_lstart_[static_cast<size_t>(pos)], ks_));
+      lane_rec_[static_cast<size_t>(pos)] = 1;
+    }
     exec_comm(pos);
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], rs));
+    if (rc_.record_events && lane) CUDA_OK(cudaEventRecord(ev_lend_[static_cast<size_t>(pos)], ks_));
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
     stats.tasks_executed += 1;
     return;
   }
@@ -928,10 +961,12 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     return;
   }
   if (task.kind == ppsim::Kind::Broadcast) {
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
     zero_broadcast(i, task.minibatch);  // Broadcast's minibatch field: the window
     // every replica of stage i reads the next version from its next task on (in order)
     bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_, P_);
     stats.kernels_launched += 1;
+    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
     stats.tasks_executed += 1;
     return;
   }
@@ -963,9 +998,16 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
   if (rc_.record_events && ev_start_.empty()) {
     ev_start_.resize(static_cast<size_t>(N));
     ev_end_.resize(static_cast<size_t>(N));
+    ev_lstart_.assign(static_cast<size_t>(N), nullptr);
+    ev_lend_.assign(static_cast<size_t>(N), nullptr);
     for (int k = 0; k < N; ++k) {
       CUDA_OK(cudaEventCreate(&ev_start_[static_cast<size_t>(k)]));
       CUDA_OK(cudaEventCreate(&ev_end_[static_cast<size_t>(k)]));
+      const auto kind = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])].kind;
+      if (kind == ppsim::Kind::Reduce || kind == ppsim::Kind::Broadcast) {
+        CUDA_OK(cudaEventCreate(&ev_lstart_[static_cast<size_t>(k)]));
+        CUDA_OK(cudaEventCreate(&ev_lend_[static_cast<size_t>(k)]));
+      }
     }
   }
   CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_ * P_) * sizeof(int), cs_));
@@ -984,6 +1026,7 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
     comm_->begin_run();
   }
   for (auto& b : bufs_) b.comm_pending = b.use_recorded = false;  // the previous run fully drained
+  lane_rec_.assign(static_cast<size_t>(N), 0);
   std::fill(wpending_.begin(), wpending_.end(), 0);
   CUDA_OK(cudaEventRecord(run_begin_, cs_));
   const auto t_issue0 = std::chrono::steady_clock::now();
@@ -1012,6 +1055,7 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
   CUDA_OK(cudaMemcpy(trace.data(), d_trace_, trace.size() * sizeof(int), cudaMemcpyDeviceToHost));
   version_seen = trace;
   events.clear();
+  lane_events.clear();
   double busy = 0;
   if (rc_.record_events) {
     for (int k = 0; k < N; ++k) {
@@ -1038,6 +1082,15 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
       ev.duration = ppsim::Rat(e_ns - s_ns);
       busy += static_cast<double>(e_ns - s_ns) * 1e-6;
       events.push_back(ev);
+      if (lane_rec_[static_cast<size_t>(k)]) {  // the task's own interval on its stream
+        CUDA_OK(cudaEventElapsedTime(&a, run_begin_, ev_lstart_[static_cast<size_t>(k)]));
+        CUDA_OK(cudaEventElapsedTime(&b, run_begin_, ev_lend_[static_cast<size_t>(k)]));
+        const int64_t ls = std::llround(static_cast<double>(a) * 1e6);
+        const int64_t le = std::max(ls, static_cast<int64_t>(std::llround(static_cast<double>(b) * 1e6)));
+        ev.start = ppsim::Rat(ls);
+        ev.duration = ppsim::Rat(le - ls);
+        lane_events.push_back(ev);
+      }
     }
   }
   stats.busy_ms = busy;
@@ -1110,7 +1163,7 @@ std::string Engine::memory_json() const {
     act += static_cast<int64_t>(slots_per_stage[static_cast<size_t>(i)]) *
            static_cast<int64_t>(stages[static_cast<size_t>(i)]->slot_bytes());
   }
-  const int64_t bounds = static_cast<int64_t>(nbuf) * T * h * 2;
+  const int64_t bounds = static_cast<int64_t>(nbuf) * T * h * static_cast<int64_t>(dm.act_bytes());
   const int64_t wsb = static_cast<int64_t>(GptStage::workspace_bytes(dm));
   const int64_t io = static_cast<int64_t>(M_) * T * 8 + static_cast<int64_t>(M_) * 4;
   const int64_t total = w + wt + wver + master + grad + opt + act + bounds + wsb + io;
@@ -1359,6 +1412,22 @@ int amdp_engine_stats(const amdp_engine* e, amdp_run_stats* out) {
 
 int amdp_engine_num_events(const amdp_engine* e) {
   return static_cast<int>(reinterpret_cast<const Engine*>(e)->events.size());
+}
+
+int amdp_engine_num_lane_events(const amdp_engine* e) {
+  return static_cast<int>(reinterpret_cast<const Engine*>(e)->lane_events.size());
+}
+
+int amdp_engine_lane_events(const amdp_engine* e, amdp_event* out, int cap) {
+  const auto& ev = reinterpret_cast<const Engine*>(e)->lane_events;
+  const int n = std::min(cap, static_cast<int>(ev.size()));
+  for (int i = 0; i < n; ++i) {
+    const auto& x = ev[static_cast<size_t>(i)];
+    out[i] = amdp_event{static_cast<int>(x.kind), x.stage, x.minibatch, x.pipeline, x.device, x.window,
+                        x.preloaded ? 1 : 0, amdp_rat{x.start.num(), x.start.den()},
+                        amdp_rat{x.duration.num(), x.duration.den()}};
+  }
+  return n;
 }
 
 int amdp_engine_events(const amdp_engine* e, amdp_event* out, int cap) {

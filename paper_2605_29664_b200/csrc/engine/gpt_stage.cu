@@ -1,4 +1,5 @@
 // GPT stage forward/backward as kernel sequences (see gpt_stage.hpp).
+#include <algorithm>
 #include <cmath>
 
 #include "gpt_stage.hpp"
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(256) transpose_bf16_kernel(const uint16_t* __r
 }  // namespace
 
 int GptStage::refresh_transposed(cudaStream_t s) const {
-  if (!wt) return 0;
+  if (!wt || d_.fp32) return 0;  // fp32 mode reads `master` with MN-major operands
   int launched = 0;
   auto tr = [&](const ParamRef& p) {
     dim3 grid((p.cols + 63) / 64, (p.rows + 63) / 64);
@@ -128,16 +129,17 @@ size_t GptStage::slot_bytes() const {
   SlotActs a;
   (void)a;
   const size_t T = static_cast<size_t>(d_.T), h = static_cast<size_t>(d_.h);
-  if (first()) c.take<uint16_t>(T * h);
+  const size_t E = d_.act_bytes() / 2;  // uint16 units per activation element
+  if (first()) c.take<uint16_t>(E * T * h);
   for (int l = l0_; l < l1_; ++l) {
-    if (l > l0_) c.take<uint16_t>(T * h);  // x
-    c.take<uint16_t>(T * h);               // ln1
-    c.take<uint16_t>(T * 3 * h);           // qkv
-    if (!d_.recompute) c.take<uint16_t>(T * h);  // o
-    c.take<uint16_t>(T * h);               // hmid
-    c.take<uint16_t>(T * h);               // ln2
-    c.take<uint16_t>(T * d_.ffn);          // u
-    if (!d_.recompute) c.take<uint16_t>(T * d_.ffn);  // f
+    if (l > l0_) c.take<uint16_t>(E * T * h);  // x
+    c.take<uint16_t>(E * T * h);               // ln1
+    c.take<uint16_t>(E * T * 3 * h);           // qkv
+    if (!d_.recompute) c.take<uint16_t>(E * T * h);  // o
+    c.take<uint16_t>(E * T * h);               // hmid
+    c.take<uint16_t>(E * T * h);               // ln2
+    c.take<uint16_t>(E * T * d_.ffn);          // u
+    if (!d_.recompute) c.take<uint16_t>(E * T * d_.ffn);  // f
     c.take<float>(T);
     c.take<float>(T);
     c.take<float>(T);
@@ -145,11 +147,11 @@ size_t GptStage::slot_bytes() const {
     c.take<float>(static_cast<size_t>(d_.B) * d_.heads * d_.S);  // lse
   }
   if (last()) {
-    c.take<uint16_t>(T * h);
-    c.take<uint16_t>(T * h);
+    c.take<uint16_t>(E * T * h);
+    c.take<uint16_t>(E * T * h);
     c.take<float>(T);
     c.take<float>(T);
-    c.take<uint16_t>(T * static_cast<size_t>(d_.V));
+    c.take<uint16_t>(E * T * static_cast<size_t>(d_.V));
   }
   return c.used;
 }
@@ -158,17 +160,18 @@ SlotActs GptStage::carve_slot(uint8_t* base) const {
   Carver c{base};
   SlotActs a;
   const size_t T = static_cast<size_t>(d_.T), h = static_cast<size_t>(d_.h);
-  if (first()) a.x0 = c.take<uint16_t>(T * h);
+  const size_t E = d_.act_bytes() / 2;  // uint16 units per activation element
+  if (first()) a.x0 = c.take<uint16_t>(E * T * h);
   for (int l = l0_; l < l1_; ++l) {
     LayerActs la;
-    if (l > l0_) la.x = c.take<uint16_t>(T * h);
-    la.ln1 = c.take<uint16_t>(T * h);
-    la.qkv = c.take<uint16_t>(T * 3 * h);
-    la.o = d_.recompute ? nullptr : c.take<uint16_t>(T * h);
-    la.hmid = c.take<uint16_t>(T * h);
-    la.ln2 = c.take<uint16_t>(T * h);
-    la.u = c.take<uint16_t>(T * d_.ffn);
-    la.f = d_.recompute ? nullptr : c.take<uint16_t>(T * d_.ffn);
+    if (l > l0_) la.x = c.take<uint16_t>(E * T * h);
+    la.ln1 = c.take<uint16_t>(E * T * h);
+    la.qkv = c.take<uint16_t>(E * T * 3 * h);
+    la.o = d_.recompute ? nullptr : c.take<uint16_t>(E * T * h);
+    la.hmid = c.take<uint16_t>(E * T * h);
+    la.ln2 = c.take<uint16_t>(E * T * h);
+    la.u = c.take<uint16_t>(E * T * d_.ffn);
+    la.f = d_.recompute ? nullptr : c.take<uint16_t>(E * T * d_.ffn);
     la.ln1_mean = c.take<float>(T);
     la.ln1_rstd = c.take<float>(T);
     la.ln2_mean = c.take<float>(T);
@@ -177,11 +180,11 @@ SlotActs GptStage::carve_slot(uint8_t* base) const {
     a.layers.push_back(la);
   }
   if (last()) {
-    a.xf = c.take<uint16_t>(T * h);
-    a.lnf = c.take<uint16_t>(T * h);
+    a.xf = c.take<uint16_t>(E * T * h);
+    a.lnf = c.take<uint16_t>(E * T * h);
     a.lnf_mean = c.take<float>(T);
     a.lnf_rstd = c.take<float>(T);
-    a.logits = c.take<uint16_t>(T * static_cast<size_t>(d_.V));
+    a.logits = c.take<uint16_t>(E * T * static_cast<size_t>(d_.V));
   }
   return a;
 }
@@ -197,19 +200,21 @@ struct Ws {
 Ws carve_ws(const Dims& d, uint8_t* base) {
   Carver c{base};
   const size_t T = static_cast<size_t>(d.T), h = static_cast<size_t>(d.h);
+  const size_t E = d.act_bytes() / 2;  // uint16 units per activation element
   Ws w;
-  w.g0 = c.take<uint16_t>(T * h);
-  w.g1 = c.take<uint16_t>(T * h);
-  w.dU = c.take<uint16_t>(T * d.ffn);
-  w.dqkv = c.take<uint16_t>(T * 3 * h);
-  w.dtmp = c.take<uint16_t>(T * h);
-  w.dhmid = c.take<uint16_t>(T * h);
-  w.attn = c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
+  w.g0 = c.take<uint16_t>(E * T * h);
+  w.g1 = c.take<uint16_t>(E * T * h);
+  w.dU = c.take<uint16_t>(E * T * d.ffn);
+  w.dqkv = c.take<uint16_t>(E * T * 3 * h);
+  w.dtmp = c.take<uint16_t>(E * T * h);
+  w.dhmid = c.take<uint16_t>(E * T * h);
+  w.attn = c.take<float>(std::max(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd),
+                                 amdp_f32_attention_bwd_workspace(d.B, d.S, d.heads)) / sizeof(float) + 1);
   w.ln = c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
   w.rows = c.take<float>(T);
   if (d.recompute) {
-    w.rc_o = c.take<uint16_t>(T * h);
-    w.rc_f = c.take<uint16_t>(T * d.ffn);
+    w.rc_o = c.take<uint16_t>(E * T * h);
+    w.rc_f = c.take<uint16_t>(E * T * d.ffn);
   }
   return w;
 }
@@ -218,18 +223,20 @@ Ws carve_ws(const Dims& d, uint8_t* base) {
 size_t GptStage::workspace_bytes(const Dims& d) {
   Carver c{nullptr};
   const size_t T = static_cast<size_t>(d.T), h = static_cast<size_t>(d.h);
-  c.take<uint16_t>(T * h);
-  c.take<uint16_t>(T * h);
-  c.take<uint16_t>(T * d.ffn);
-  c.take<uint16_t>(T * 3 * h);
-  c.take<uint16_t>(T * h);
-  c.take<uint16_t>(T * h);
-  c.take<float>(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd) / sizeof(float) + 1);
+  const size_t E = d.act_bytes() / 2;  // uint16 units per activation element
+  c.take<uint16_t>(E * T * h);
+  c.take<uint16_t>(E * T * h);
+  c.take<uint16_t>(E * T * d.ffn);
+  c.take<uint16_t>(E * T * 3 * h);
+  c.take<uint16_t>(E * T * h);
+  c.take<uint16_t>(E * T * h);
+  c.take<float>(std::max(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd),
+                                 amdp_f32_attention_bwd_workspace(d.B, d.S, d.heads)) / sizeof(float) + 1);
   c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
   c.take<float>(T);
   if (d.recompute) {
-    c.take<uint16_t>(T * h);
-    c.take<uint16_t>(T * d.ffn);
+    c.take<uint16_t>(E * T * h);
+    c.take<uint16_t>(E * T * d.ffn);
   }
   return c.used;
 }
@@ -259,6 +266,9 @@ size_t GptStage::workspace_bytes(const Dims& d) {
 int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
                       const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* wsb,
                       cudaStream_t s, int* rc) const {
+  if (d_.fp32)
+    return forward_f32(a, tokens, labels, reinterpret_cast<const float*>(in), reinterpret_cast<float*>(out), loss_sum,
+                       loss_scale, wsb, s, rc);
   const Ws ws = carve_ws(d_, wsb);
   int launched = 0;
   *rc = 0;
@@ -309,6 +319,9 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
 // joined to `side`, so slot activations and gradient buffers are quiescent afterwards.
 int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in, const uint16_t* gin,
                        uint16_t* gout, uint8_t* wsb, cudaStream_t s, const SideStream& ss, int* rc) const {
+  if (d_.fp32)
+    return backward_f32(a, tokens, reinterpret_cast<const float*>(in), reinterpret_cast<const float*>(gin),
+                        reinterpret_cast<float*>(gout), wsb, s, rc);
   int launched = 0;
   *rc = 0;
   auto st = reinterpret_cast<amdp_stream_t>(s);
@@ -407,6 +420,117 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
   }
   if (first()) AMDP_TRY(K_EMBED, 0, 10.0 * T * h, amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, ws.rows, T, d_.S, h, st), 2);
   hand(ss.ev[F_END], sd, s);  // join: weight gradients complete before the task ends
+  return launched;
+}
+
+// ------------------------------------------------------------------ fp32 validation mode
+// The same stage math as forward() / backward() above on fp32 tensors (the slot and workspace
+// pointers address floats), weights read from the fp32 master, every kernel an amdp_f32_*
+// one, all on stream `s` in a fixed order (no side stream): bitwise reproducible.
+namespace {
+int gemm32(KTimer* kt, int M, int N, int K, const float* A, int lda, bool amn, const float* B, int ldb, bool bmn,
+           float* C, int ldc, int epi, cudaStream_t s, const float* aux = nullptr, int ld_aux = 0,
+           float* C2 = nullptr, int ldc2 = 0, int cls = -1) {
+  amdp_gemm_args a{M, N, K, A, lda, amn ? 1 : 0, B, ldb, bmn ? 1 : 0, C, ldc, aux, ld_aux, C2, ldc2,
+                   epi, 1.0f, nullptr, 0, 0};
+  if (cls < 0) cls = epi == AMDP_EPI_ACCUM_F32 ? K_GEMM_WGRAD : (bmn ? K_GEMM_DGRAD : K_GEMM_FWD);
+  if (kt) kt->begin(cls, 2.0 * M * N * static_cast<double>(K), 0, s);
+  const int rc = amdp_f32_gemm(&a, reinterpret_cast<amdp_stream_t>(s));
+  if (kt) kt->end(s);
+  return rc;
+}
+inline float* F(uint16_t* p) { return reinterpret_cast<float*>(p); }
+inline const float* F(const uint16_t* p) { return reinterpret_cast<const float*>(p); }
+}  // namespace
+
+int GptStage::forward_f32(const SlotActs& a, const int32_t* tokens, const int32_t* labels, const float* in,
+                          float* out, float* loss_sum, float loss_scale, uint8_t* wsb, cudaStream_t s, int* rc) const {
+  const Ws ws = carve_ws(d_, wsb);
+  int launched = 0;
+  *rc = 0;
+  auto st = reinterpret_cast<amdp_stream_t>(s);
+  const int T = d_.T, h = d_.h;
+  const float* W = master;
+  const float* x = in;
+  if (first()) {
+    AMDP_TRY(K_EMBED, 0, 12.0 * T * h, amdp_f32_embedding_fwd(tokens, W + wte_.off, W + wpe_.off, F(a.x0), T, d_.S, h, st), 1);
+    x = F(a.x0);
+  }
+  for (int li = 0; li < l1_ - l0_; ++li) {
+    const LayerParams& P = layers_[static_cast<size_t>(li)];
+    const LayerActs& A = a.layers[static_cast<size_t>(li)];
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_f32_layernorm_fwd(x, W + P.ln1_g.off, W + P.ln1_b.off, F(A.ln1), A.ln1_mean,
+                                                                A.ln1_rstd, T, h, d_.ln_eps, st), 1);
+    AMDP_GEMM(gemm32(kt, T, 3 * h, h, F(A.ln1), h, false, W + P.qkv.off, h, false, F(A.qkv), 3 * h, AMDP_EPI_STORE_F32, s), 1);
+    AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_f32_attention_fwd(F(A.qkv), F(A.o), A.lse, d_.B, d_.S, d_.heads, d_.hd,
+                                                                     d_.causal ? 1 : 0, st), 1);
+    AMDP_GEMM(gemm32(kt, T, h, h, F(A.o), h, false, W + P.o.off, h, false, F(A.hmid), h, AMDP_EPI_RESIDUAL, s, x, h), 1);
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_f32_layernorm_fwd(F(A.hmid), W + P.ln2_g.off, W + P.ln2_b.off, F(A.ln2),
+                                                                A.ln2_mean, A.ln2_rstd, T, h, d_.ln_eps, st), 1);
+    AMDP_GEMM(gemm32(kt, T, d_.ffn, h, F(A.ln2), h, false, W + P.fc1.off, h, false, F(A.f), d_.ffn, AMDP_EPI_GELU, s,
+                     nullptr, 0, F(A.u), d_.ffn), 1);
+    float* nx;
+    if (li + 1 < l1_ - l0_) nx = F(a.layers[static_cast<size_t>(li) + 1].x);
+    else nx = last() ? F(a.xf) : out;
+    AMDP_GEMM(gemm32(kt, T, h, d_.ffn, F(A.f), d_.ffn, false, W + P.fc2.off, d_.ffn, false, nx, h, AMDP_EPI_RESIDUAL, s,
+                     F(A.hmid), h), 1);
+    x = nx;
+  }
+  if (last()) {
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_f32_layernorm_fwd(F(a.xf), W + lnf_g_.off, W + lnf_b_.off, F(a.lnf),
+                                                                a.lnf_mean, a.lnf_rstd, T, h, d_.ln_eps, st), 1);
+    AMDP_GEMM(gemm32(kt, T, d_.V, h, F(a.lnf), h, false, W + head_.off, h, false, F(a.logits), d_.V, AMDP_EPI_STORE_F32, s), 1);
+    AMDP_TRY(K_XENT, 0, 12.0 * T * d_.V, amdp_f32_xent_fwd_bwd(F(a.logits), labels, loss_sum, ws.rows, T, d_.V, d_.V,
+                                                               loss_scale, st), 2);
+  }
+  return launched;
+}
+
+int GptStage::backward_f32(const SlotActs& a, const int32_t* tokens, const float* in, const float* gin, float* gout,
+                           uint8_t* wsb, cudaStream_t s, int* rc) const {
+  int launched = 0;
+  *rc = 0;
+  auto st = reinterpret_cast<amdp_stream_t>(s);
+  const int T = d_.T, h = d_.h, Fn = d_.ffn;
+  const Ws ws = carve_ws(d_, wsb);
+  const float* W = master;
+  float *g0 = F(ws.g0), *g1 = F(ws.g1), *dU = F(ws.dU), *dqkv = F(ws.dqkv), *dtmp = F(ws.dtmp), *dh = F(ws.dhmid);
+  const float* g = gin;
+  if (last()) {  // logits hold dloss/dlogits (written by the forward's cross-entropy)
+    AMDP_GEMM(gemm32(kt, d_.V, h, T, F(a.logits), d_.V, true, F(a.lnf), h, true, grad + head_.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_GEMM(gemm32(kt, T, h, d_.V, F(a.logits), d_.V, false, W + head_.off, h, true, dtmp, h, AMDP_EPI_STORE_F32, s), 1);
+    AMDP_TRY(K_LAYERNORM, 0, 16.0 * T * h, amdp_f32_layernorm_bwd(dtmp, F(a.xf), W + lnf_g_.off, a.lnf_mean, a.lnf_rstd,
+                                                                 nullptr, g0, grad + lnf_g_.off, grad + lnf_b_.off, T, h, st), 2);
+    g = g0;
+  }
+  for (int li = l1_ - l0_ - 1; li >= 0; --li) {
+    const LayerParams& P = layers_[static_cast<size_t>(li)];
+    const LayerActs& A = a.layers[static_cast<size_t>(li)];
+    const float* x = li > 0 ? F(A.x) : (first() ? F(a.x0) : in);
+    // y = hmid + f W2^T
+    AMDP_GEMM(gemm32(kt, h, Fn, T, g, h, true, F(A.f), Fn, true, grad + P.fc2.off, Fn, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_GEMM(gemm32(kt, T, Fn, h, g, h, false, W + P.fc2.off, Fn, true, dU, Fn, AMDP_EPI_GELU_BWD, s, F(A.u), Fn), 1);
+    // f = gelu(ln2 W1^T)
+    AMDP_GEMM(gemm32(kt, Fn, h, T, dU, Fn, true, F(A.ln2), h, true, grad + P.fc1.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_GEMM(gemm32(kt, T, h, Fn, dU, Fn, false, W + P.fc1.off, h, true, dtmp, h, AMDP_EPI_STORE_F32, s), 1);
+    AMDP_TRY(K_LAYERNORM, 0, 16.0 * T * h, amdp_f32_layernorm_bwd(dtmp, F(A.hmid), W + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g,
+                                                                 dh, grad + P.ln2_g.off, grad + P.ln2_b.off, T, h, st), 2);
+    // hmid = x + o Wo^T
+    AMDP_GEMM(gemm32(kt, h, h, T, dh, h, true, F(A.o), h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_GEMM(gemm32(kt, T, h, h, dh, h, false, W + P.o.off, h, true, dtmp, h, AMDP_EPI_STORE_F32, s), 1);
+    AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_f32_attention_bwd(F(A.qkv), F(A.o), dtmp, A.lse, dqkv, ws.attn, d_.B,
+                                                                           d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, st), 3);
+    // qkv = ln1 Wqkv^T
+    AMDP_GEMM(gemm32(kt, 3 * h, h, T, dqkv, 3 * h, true, F(A.ln1), h, true, grad + P.qkv.off, h, AMDP_EPI_ACCUM_F32, s), 1);
+    AMDP_GEMM(gemm32(kt, T, h, 3 * h, dqkv, 3 * h, false, W + P.qkv.off, h, true, dtmp, h, AMDP_EPI_STORE_F32, s), 1);
+    float* gn = (li == 0 && !first()) ? gout : (g == g0 ? g1 : g0);
+    AMDP_TRY(K_LAYERNORM, 0, 16.0 * T * h, amdp_f32_layernorm_bwd(dtmp, x, W + P.ln1_g.off, A.ln1_mean, A.ln1_rstd, dh, gn,
+                                                                 grad + P.ln1_g.off, grad + P.ln1_b.off, T, h, st), 2);
+    g = gn;
+  }
+  if (first())
+    AMDP_TRY(K_EMBED, 0, 20.0 * T * h, amdp_f32_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, ws.rows, T, d_.S,
+                                                              h, st), 3);
   return launched;
 }
 

@@ -31,6 +31,8 @@ struct Dims {
   bool causal;
   float ln_eps;
   bool recompute = false;  // f and o recomputed in the backward (amdp_model_config.recompute)
+  bool fp32 = false;       // fp32 validation mode: activations fp32, amdp_f32_* kernels
+  size_t act_bytes() const { return fp32 ? 4 : 2; }  // per activation element
 };
 
 struct ParamRef {
@@ -104,6 +106,12 @@ class GptStage {
   int backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in,
                const uint16_t* gin, uint16_t* gout, uint8_t* ws, cudaStream_t s,
                const SideStream& side, int* rc) const;
+  // fp32 validation mode bodies (gpt_stage_f32.cu): the same math on float tensors (the
+  // activation pointers then address fp32 data), weights read from `master`
+  int forward_f32(const SlotActs& a, const int32_t* tokens, const int32_t* labels, const float* in,
+                  float* out, float* loss_sum, float loss_scale, uint8_t* ws, cudaStream_t s, int* rc) const;
+  int backward_f32(const SlotActs& a, const int32_t* tokens, const float* in, const float* gin,
+                   float* gout, uint8_t* ws, cudaStream_t s, int* rc) const;
 
  private:
   Dims d_;

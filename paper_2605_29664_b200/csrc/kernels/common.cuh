@@ -102,6 +102,39 @@ inline bool first_on_device(std::atomic<uint64_t>& mask) {
   return (mask.fetch_or(bit) & bit) == 0;
 }
 
+// Sort of a minibatch's (token, position) keys for the deterministic token-table gradient
+// (bf16 and fp32 paths): one CTA, bitonic in shared memory.  Key = token << 14 | position,
+// so ntok <= 16384 and vocab < 2^18.
+namespace {
+constexpr int kEmbPosBits = 14;
+__global__ void __launch_bounds__(1024) embedding_sort_kernel(const int32_t* __restrict__ tok, int ntok,
+                                                              uint32_t* __restrict__ sorted) {
+  extern __shared__ uint32_t keys[];
+  grid_dep_wait();
+  grid_dep_trigger();
+  int n2 = 1;
+  while (n2 < ntok) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x)
+    keys[i] = i < ntok ? (static_cast<uint32_t>(tok[i]) << kEmbPosBits) | static_cast<uint32_t>(i) : 0xffffffffu;
+  __syncthreads();
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint32_t a = keys[lo], b = keys[hi];
+        if ((a > b) == up) {
+          keys[lo] = b;
+          keys[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < ntok; i += blockDim.x) sorted[i] = keys[i];
+}
+
+}  // namespace
+
 inline int num_sms() {
   static int n = 0;
   if (n == 0) {

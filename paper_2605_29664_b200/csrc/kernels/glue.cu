@@ -361,33 +361,6 @@ __global__ void embedding_fwd_kernel(const int32_t* __restrict__ tok, const bf16
 // by the single thread owning that (token, 8-column) slice and added to dwte without atomics.
 // The window gradient is therefore bitwise reproducible (and independent of how the stages are
 // spread over GPUs).  Key = token << 14 | position: ntok <= 16384, vocab < 2^18.
-constexpr int EMB_POS_BITS = 14;
-__global__ void __launch_bounds__(1024) embedding_sort_kernel(const int32_t* __restrict__ tok, int ntok,
-                                                              uint32_t* __restrict__ sorted) {
-  extern __shared__ uint32_t keys[];
-  grid_dep_wait();
-  grid_dep_trigger();
-  int n2 = 1;
-  while (n2 < ntok) n2 <<= 1;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x)
-    keys[i] = i < ntok ? (static_cast<uint32_t>(tok[i]) << EMB_POS_BITS) | static_cast<uint32_t>(i) : 0xffffffffu;
-  __syncthreads();
-  for (int size = 2; size <= n2; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const uint32_t a = keys[lo], b = keys[hi];
-        if ((a > b) == up) {
-          keys[lo] = b;
-          keys[hi] = a;
-        }
-      }
-      __syncthreads();
-    }
-  for (int i = threadIdx.x; i < ntok; i += blockDim.x) sorted[i] = keys[i];
-}
-
 __global__ void embedding_bwd_tok_kernel(const uint32_t* __restrict__ sorted, const bf16* __restrict__ dx,
                                          float* __restrict__ dwte, int ntok, int hidden) {
   grid_dep_wait();  // PDL: predecessor's outputs visible from here
@@ -398,13 +371,13 @@ __global__ void embedding_bwd_tok_kernel(const uint32_t* __restrict__ sorted, co
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int k = static_cast<int>(i / vecs);
     const int c = static_cast<int>(i % vecs) * 8;
-    const uint32_t t = sorted[k] >> EMB_POS_BITS;
-    if (k > 0 && (sorted[k - 1] >> EMB_POS_BITS) == t) continue;  // not the run's first key
+    const uint32_t t = sorted[k] >> kEmbPosBits;
+    if (k > 0 && (sorted[k - 1] >> kEmbPosBits) == t) continue;  // not the run's first key
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int r = k;
-    while (r < ntok && (sorted[r] >> EMB_POS_BITS) == t) {
+    while (r < ntok && (sorted[r] >> kEmbPosBits) == t) {
       float g[8];
-      load8(dx + static_cast<size_t>(sorted[r] & ((1u << EMB_POS_BITS) - 1)) * hidden + c, g);
+      load8(dx + static_cast<size_t>(sorted[r] & ((1u << kEmbPosBits) - 1)) * hidden + c, g);
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] += g[e];
       ++r;
@@ -655,7 +628,7 @@ extern "C" int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, flo
                                   float* dwpe, void* workspace, int ntok, int seq, int hidden,
                                   amdp_stream_t stream) {
   if (ntok <= 0 || seq <= 0 || hidden % 8 != 0 || ntok % seq != 0 || !workspace) return AMDP_ERR_INVALID;
-  if (ntok > (1 << EMB_POS_BITS)) return AMDP_ERR_INVALID;
+  if (ntok > (1 << kEmbPosBits)) return AMDP_ERR_INVALID;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int n2 = 1;
   while (n2 < ntok) n2 <<= 1;
@@ -663,7 +636,7 @@ extern "C" int amdp_embedding_bwd(const int32_t* tokens, const uint16_t* dx, flo
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     cudaError_t e = cudaFuncSetAttribute(embedding_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sizeof(uint32_t) << EMB_POS_BITS));
+                                         static_cast<int>(sizeof(uint32_t) << kEmbPosBits));
     if (e != cudaSuccess) {
       attr.store(0);
       return e;

@@ -29,7 +29,8 @@ class _Model(Structure):
     _fields_ = [("layers", c_int), ("hidden", c_int), ("heads", c_int), ("ffn", c_int),
                 ("vocab", c_int), ("seq", c_int), ("seqs_per_minibatch", c_int),
                 ("causal", c_int), ("init_std", c_float), ("ln_eps", c_float),
-                ("seed", c_uint64), ("layers_per_stage", POINTER(c_int)), ("recompute", c_int)]
+                ("seed", c_uint64), ("layers_per_stage", POINTER(c_int)), ("recompute", c_int),
+                ("fp32_validation", c_int)]
 
 
 class _Run(Structure):
@@ -74,6 +75,8 @@ class _KStat(Structure):
 _sig("amdp_engine_kernel_stats", c_int, [c_void_p, POINTER(_KStat), c_int])
 _sig("amdp_engine_num_events", c_int, [c_void_p])
 _sig("amdp_engine_events", c_int, [c_void_p, POINTER(P._Event), c_int])
+_sig("amdp_engine_num_lane_events", c_int, [c_void_p])
+_sig("amdp_engine_lane_events", c_int, [c_void_p, POINTER(P._Event), c_int])
 _sig("amdp_engine_version_trace", c_size_t, [c_void_p, c_char_p, c_size_t])
 _sig("amdp_engine_schedule", c_void_p, [c_void_p])
 _sig("amdp_engine_stage_numel", c_int64, [c_void_p, c_int])
@@ -99,6 +102,7 @@ class ModelConfig:
     seed: int = 1234
     layers_per_stage: Optional[List[int]] = None
     recompute: bool = False  # backward rebuilds f = gelu(u) and o = attention(qkv) (amdp_model_config)
+    fp32_validation: bool = False  # every tensor / product fp32 on the CUDA cores (amdp_f32_* kernels)
 
     @property
     def tokens_per_minibatch(self) -> int:
@@ -135,7 +139,7 @@ class ModelConfig:
             lps = (c_int * len(self.layers_per_stage))(*self.layers_per_stage)
         m = _Model(self.layers, self.hidden, self.heads, self.ffn, self.vocab, self.seq,
                    self.seqs_per_minibatch, int(self.causal), self.init_std, self.ln_eps,
-                   self.seed, lps, int(self.recompute))
+                   self.seed, lps, int(self.recompute), int(self.fp32_validation))
         m._keep = lps
         return m
 
@@ -353,6 +357,14 @@ class Engine:
         rc = self.runcfg
         return P.Timeline.from_events(evs, rc.policy().policy, rc.depth, rc.devices, rc.threshold,
                                       rc.declared_cluster())
+
+    def lane_events(self) -> list:
+        """Reduce / Broadcast intervals on the collective / update streams (see timeline())."""
+        n = lib.amdp_engine_num_lane_events(self._h)
+        arr = (P._Event * max(1, n))()
+        lib.amdp_engine_lane_events(self._h, arr, n)
+        return [P.TaskEvent(P.Kind(e.kind), e.stage, e.minibatch, e.pipeline, e.device,
+                            P._f(e.start), P._f(e.duration), bool(e.preloaded), e.window) for e in arr[:n]]
 
     def declared_timeline(self) -> P.Timeline:
         h = P._Handle(lib.amdp_engine_schedule(self._h))

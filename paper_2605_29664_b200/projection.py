@@ -24,13 +24,19 @@ KIND_TAG = {P.Kind.Forward: "F", P.Kind.Backward: "B", P.Kind.Reduce: "R", P.Kin
             P.Kind.Update: "U"}
 
 
-def measured_costs(tl: P.Timeline, min_window: int = 1) -> Dict[Tuple[P.Kind, int], float]:
+def measured_costs(tl: P.Timeline, min_window: int = 1, lane_events=None) -> Dict[Tuple[P.Kind, int], float]:
     """Mean measured duration (ns) per (kind, stage) over windows >= min_window.  Update tasks
     take the max: folded on one GPU only the first replica's Update of a window runs the
     optimizer (the others switch weight buffers), while on one GPU per device every replica
-    steps its own optimizer state."""
+    steps its own optimizer state.  `lane_events` (Engine.lane_events()): the Reduce /
+    Broadcast intervals on the executor's collective / update streams, which replace the
+    compute-stream markers of those tasks."""
     acc: Dict[Tuple[P.Kind, int], list] = {}
+    lane_kinds = {ev.kind for ev in lane_events} if lane_events else set()
     for ev in tl.flat():
+        if ev.window >= min_window and ev.kind not in lane_kinds:
+            acc.setdefault((ev.kind, ev.stage), []).append(float(ev.duration))
+    for ev in lane_events or []:
         if ev.window >= min_window:
             acc.setdefault((ev.kind, ev.stage), []).append(float(ev.duration))
     return {k: (max(v) if k[0] == P.Kind.Update else statistics.mean(v)) for k, v in acc.items()}
@@ -117,11 +123,11 @@ def replicas_of(policy: P.PolicyConfig) -> int:
 
 
 def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, tokens_per_minibatch: int,
-            gap_ns: float, stage_numel=None, policy: P.PolicyConfig = None) -> dict:
+            gap_ns: float, stage_numel=None, policy: P.PolicyConfig = None, lane_events=None) -> dict:
     """Projected d-GPU bubble and throughput of a measured run's schedule (default AMDP).  With
     `stage_numel`, the Reduce / Broadcast tasks also carry the NVLink collective time
     (collective_costs) on top of what was measured on one GPU (the fused optimizer)."""
-    costs = measured_costs(tl_measured)
+    costs = measured_costs(tl_measured, lane_events=lane_events)
     pol = policy or P.PolicyConfig(policy=P.Policy.AMDP, injection_limit=2, num_pipelines=depth // 2,
                                    accumulation_threshold=threshold, num_minibatches=windows * threshold,
                                    zero_enabled=True)
