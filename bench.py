@@ -355,8 +355,10 @@ def main():
             pol = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=args.steps,
                               schedule=args.schedule, zero=zero).policy()
             lanes = eng.lane_events()
+            part = eng.plan()["partition"]
+            segs = [part[i] + (i == 0) + (i == args.depth - 1) for i in range(args.depth)]
             projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
-                                    stage_numel=numel, policy=pol, lane_events=lanes)
+                                    stage_numel=numel, policy=pol, lane_events=lanes, segments=segs)
             if args.schedule == "AMDP" and zero:
                 # the same measured costs under AMDP's other update mode: replicated weights,
                 # window gradient all-reduced over the stage's devices, every replica stepping

@@ -60,9 +60,12 @@ class Comm {
   // ---- replica-group collectives (group = sorted ranks hosting the stage; root a rank id)
   virtual void reduce_f32(int coll, const std::vector<int>& group, int root, int stage, float* buf,
                           size_t n, cudaStream_t s) = 0;
-  // root's spans -> every member's same spans
+  // root's spans -> every member's same spans.  root_waits = false: the root only publishes
+  // (the call returns without waiting for the members' copies); it must then call
+  // broadcast_root_wait(coll, ...) before it next modifies the spans.
   virtual void broadcast(int coll, const std::vector<int>& group, int root, int stage,
-                         const std::vector<Span>& spans, cudaStream_t s) = 0;
+                         const std::vector<Span>& spans, cudaStream_t s, bool root_waits = true) = 0;
+  virtual void broadcast_root_wait(int coll, const std::vector<int>& group, int root, cudaStream_t s) = 0;
   virtual void allreduce_f32(int coll, const std::vector<int>& group, int stage, float* buf, size_t n,
                              cudaStream_t s) = 0;
 

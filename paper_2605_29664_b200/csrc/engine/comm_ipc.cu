@@ -224,7 +224,7 @@ class IpcComm final : public Comm {
   }
 
   void broadcast(int coll, const std::vector<int>& group, int root, int stage, const std::vector<Span>& spans,
-                 cudaStream_t s) override {
+                 cudaStream_t s, bool root_waits) override {
     (void)stage;
     const int base = coll_base(coll), me = index_in(group, rank_), ri = index_in(group, root);
     if (rank_ == root) {
@@ -232,8 +232,7 @@ class IpcComm final : public Comm {
       for (int j = 0; j < static_cast<int>(group.size()); ++j)
         if (j != me) t.push_back(flag_of(group[static_cast<size_t>(j)], base + ri));
       signal(s, t);
-      for (int j = 0; j < static_cast<int>(group.size()); ++j)
-        if (j != me) wait(s, base + 8 + j);
+      if (root_waits) broadcast_root_wait(coll, group, root, s);
     } else {
       wait(s, base + ri);
       for (const Span& sp : spans) {
@@ -244,6 +243,13 @@ class IpcComm final : public Comm {
       }
       signal(s, {flag_of(root, base + 8 + me)});
     }
+  }
+
+  void broadcast_root_wait(int coll, const std::vector<int>& group, int root, cudaStream_t s) override {
+    if (rank_ != root) return;
+    const int base = coll_base(coll), me = index_in(group, rank_);
+    for (int j = 0; j < static_cast<int>(group.size()); ++j)
+      if (j != me) wait(s, base + 8 + j);
   }
 
   void allreduce_f32(int coll, const std::vector<int>& group, int stage, float* buf, size_t n,

@@ -70,8 +70,9 @@ class NcclComm final : public Comm {
                   cudaStream_t s) override {
     NCCL_OK(ncclReduce(buf, buf, n, ncclFloat32, ncclSum, index_in(group, root), comm(stage), s));
   }
+  void broadcast_root_wait(int, const std::vector<int>&, int, cudaStream_t) override {}
   void broadcast(int, const std::vector<int>& group, int root, int stage, const std::vector<Span>& spans,
-                 cudaStream_t s) override {
+                 cudaStream_t s, bool) override {
     const int r = index_in(group, root);
     NCCL_OK(ncclGroupStart());
     for (const Span& sp : spans) {

@@ -196,7 +196,9 @@ class Engine {
   std::vector<std::vector<int>> rep_buf_;                // per stage, pipeline
   float update_div_ = 1.f;                               // minibatches per optimizer step
   void use_replica_weights(int stage, int pipeline);
-  void optimizer_step(int stage, int step, cudaStream_t st);
+  void optimizer_step(int stage, int step, cudaStream_t st);  // whole stage + transposed copies
+  void optimizer_range(int stage, int step, int64_t off, int64_t n, cudaStream_t st);
+  std::vector<int> pending_root_wait_;  // per stage: first collective id of an unconfirmed publication
   int cur_pos_ = 0;  // order position being issued
   int64_t comm_launches_seen_ = 0;
   std::vector<TaskPlan> plan_;               // per order position
@@ -211,7 +213,10 @@ class Engine {
   // compute, receive, send, collective, window-update streams (NCCL: one stream for all comm)
   cudaStream_t cs_ = nullptr, rs_ = nullptr, ss_ = nullptr, ks_ = nullptr, us_ = nullptr;
   std::vector<cudaEvent_t> wready_;   // per stage: new weights in place (update stream)
-  std::vector<char> wpending_;        // per stage: next F/B must wait wready_
+  std::vector<char> wpending_;        // per stage: next B must wait wready_
+  std::vector<char> fpending_;        // per stage: next F waits the per-segment events
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> segs_;  // per stage: GptStage::segments()
+  std::vector<std::vector<cudaEvent_t>> seg_ev_;               // per stage, segment: weights in place
   std::vector<cudaEvent_t> reduced_;  // per stage: window gradient reduced (collective stream)
   std::vector<cudaEvent_t> ev_pool_;  // cross-stream hand-offs (recycled round robin)
   size_t ev_next_ = 0;
@@ -477,6 +482,8 @@ Engine::~Engine() {
     if (e) cudaEventDestroy(e);
   for (auto e : wready_) cudaEventDestroy(e);
   for (auto e : reduced_) cudaEventDestroy(e);
+  for (auto& v : seg_ev_)
+    for (auto e : v) cudaEventDestroy(e);
   for (auto e : ev_pool_) cudaEventDestroy(e);
   if (run_begin_) cudaEventDestroy(run_begin_);
   if (run_end_) cudaEventDestroy(run_end_);
@@ -616,8 +623,9 @@ void Engine::make_plan() {
       }
     } else if (task.kind == ppsim::Kind::Broadcast) {
       const int i = task.stage;
-      if (group_ranks_[static_cast<size_t>(i)].size() > 1) {
-        const int c = ncoll_++;
+      if (group_ranks_[static_cast<size_t>(i)].size() > 1) {  // one collective per parameter segment
+        const int c = ncoll_;
+        ncoll_ += static_cast<int>(stages[static_cast<size_t>(i)]->segments().size());
         if (hosted[static_cast<size_t>(i)]) comm_at_[static_cast<size_t>(k)].push_back({CommOp::Bcast, -1, -1, i, k, c});
       }
     } else if (task.kind == ppsim::Kind::Update) {
@@ -697,6 +705,18 @@ void Engine::allocate() {
   wready_.resize(static_cast<size_t>(depth_));
   reduced_.resize(static_cast<size_t>(depth_));
   wpending_.assign(static_cast<size_t>(depth_), 0);
+  fpending_.assign(static_cast<size_t>(depth_), 0);
+  pending_root_wait_.assign(static_cast<size_t>(depth_), -1);
+  segs_.resize(static_cast<size_t>(depth_));
+  seg_ev_.resize(static_cast<size_t>(depth_));
+  for (int i = 0; i < depth_; ++i) {
+    segs_[static_cast<size_t>(i)] = stages[static_cast<size_t>(i)]->segments();
+    for (size_t k = 0; k < segs_[static_cast<size_t>(i)].size(); ++k) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      seg_ev_[static_cast<size_t>(i)].push_back(e);
+    }
+  }
   for (auto& e : wready_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : reduced_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (comm_) {  // what peers may read: boundary arena, and per hosted stage grad / w / master
@@ -790,6 +810,7 @@ void Engine::zero_broadcast(int i, int window) {
   GptStage& S = *stages[static_cast<size_t>(i)];
   const auto& gr = group_ranks_[static_cast<size_t>(i)];
   const bool multi = gr.size() > 1;
+  const bool own = owned[static_cast<size_t>(i)];
   CUDA_OK(cudaStreamWaitEvent(us_, handoff(cs_), 0));
   if (multi) CUDA_OK(cudaStreamWaitEvent(us_, reduced_[static_cast<size_t>(i)], 0));
   // the update stream's interval of this Broadcast (a lane event: it overlaps other stages'
@@ -798,40 +819,54 @@ void Engine::zero_broadcast(int i, int window) {
     CUDA_OK(cudaEventRecord(ev_lstart_[static_cast<size_t>(cur_pos_)], us_));
     lane_rec_[static_cast<size_t>(cur_pos_)] = 1;
   }
-  cudaStream_t bs = us_;  // broadcast stream
-  if (multi && comm_->single_stream()) bs = ks_;
-  if (owned[static_cast<size_t>(i)]) {
-    optimizer_step(i, window + 1, us_);
-  } else {
-    CUDA_OK(cudaMemsetAsync(S.grad, 0, static_cast<size_t>(S.numel()) * sizeof(float), us_));
+  int coll0 = -1;
+  for (const CommOp& op : comm_at_[static_cast<size_t>(cur_pos_)])
+    if (op.kind == CommOp::Bcast && op.stage == i) coll0 = op.id;
+  // NCCL: the collectives of one communicator must share its stream, so the whole Broadcast
+  // runs there; the peer-memory backend runs it on the update stream
+  cudaStream_t st = multi && comm_->single_stream() ? ks_ : us_;
+  if (st != us_) CUDA_OK(cudaStreamWaitEvent(st, handoff(us_), 0));
+  // the previous window's publication of these weights must have been copied by every replica
+  // before the optimizer overwrites them
+  if (pending_root_wait_[static_cast<size_t>(i)] >= 0) {
+    const int c0 = pending_root_wait_[static_cast<size_t>(i)];
+    for (size_t k = 0; k < segs_[static_cast<size_t>(i)].size(); ++k)
+      comm_->broadcast_root_wait(c0 + static_cast<int>(k), gr, owner_rank(i), st);
+    pending_root_wait_[static_cast<size_t>(i)] = -1;
   }
-  if (multi) {
-    int coll = -1;
-    for (const CommOp& op : comm_at_[static_cast<size_t>(cur_pos_)])
-      if (op.kind == CommOp::Bcast && op.stage == i) coll = op.id;
-    std::vector<Span> spans;
-    if (dm.fp32) {  // fp32 validation mode: the kernels read the fp32 master itself
-      spans.push_back(Span{REG_MASTER, i, 0, static_cast<size_t>(S.numel()) * 4});
-    } else {  // bf16 working weights + the fp32 LayerNorm parameters the kernels read
-      spans.push_back(Span{REG_W, i, 0, static_cast<size_t>(S.numel()) * 2});
-      for (const auto& p : S.params())
-        if (p.rows == 1) spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(p.off) * 4, static_cast<size_t>(p.numel()) * 4});
+  if (!own) CUDA_OK(cudaMemsetAsync(S.grad, 0, static_cast<size_t>(S.numel()) * sizeof(float), st));
+  // segment by segment in the forward's reading order (embeddings, layers, head): a gated
+  // Forward starts on the first layer while the optimizer still runs on the later ones
+  const auto& segs = segs_[static_cast<size_t>(i)];
+  int64_t moved = 0;
+  for (size_t k = 0; k < segs.size(); ++k) {
+    const int64_t off = segs[k].first, n = segs[k].second;
+    if (own) optimizer_range(i, window + 1, off, n, st);
+    if (multi) {
+      std::vector<Span> spans;
+      if (dm.fp32) {  // fp32 validation mode: the kernels read the fp32 master itself
+        spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(off) * 4, static_cast<size_t>(n) * 4});
+      } else {  // bf16 working weights + the fp32 LayerNorm parameters the kernels read
+        spans.push_back(Span{REG_W, i, static_cast<size_t>(off) * 2, static_cast<size_t>(n) * 2});
+        for (const auto& p : S.params())
+          if (p.rows == 1 && p.off >= off && p.off < off + n)
+            spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(p.off) * 4, static_cast<size_t>(p.numel()) * 4});
+      }
+      comm_->broadcast(coll0 + static_cast<int>(k), gr, owner_rank(i), i, spans, st, /*root_waits=*/false);
+      for (const Span& sp : spans) moved += static_cast<int64_t>(sp.bytes);
     }
-    if (bs != us_) CUDA_OK(cudaStreamWaitEvent(bs, handoff(us_), 0));
-    comm_->broadcast(coll, gr, owner_rank(i), i, spans, bs);
-    if (bs != us_) CUDA_OK(cudaStreamWaitEvent(us_, handoff(bs), 0));
-    int64_t moved = 0;
-    for (const Span& sp : spans) moved += static_cast<int64_t>(sp.bytes);
-    stats.collective_bytes += moved;
-    if (!owned[static_cast<size_t>(i)]) {
-      const int nt = S.refresh_transposed(us_);
-      if (nt < 0) throw std::runtime_error("weight transpose failed");
-      stats.kernels_launched += nt;
-    }
+    CUDA_OK(cudaEventRecord(seg_ev_[static_cast<size_t>(i)][k], st));
   }
+  if (multi && own) pending_root_wait_[static_cast<size_t>(i)] = coll0;
+  stats.collective_bytes += moved;
+  const int nt = S.refresh_transposed(st);  // the backward's K-major weight copies
+  if (nt < 0) throw std::runtime_error("weight transpose failed");
+  stats.kernels_launched += nt;
+  if (st != us_) CUDA_OK(cudaStreamWaitEvent(us_, handoff(st), 0));
   CUDA_OK(cudaEventRecord(wready_[static_cast<size_t>(i)], us_));
   if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_lend_[static_cast<size_t>(cur_pos_)], us_));
   wpending_[static_cast<size_t>(i)] = 1;
+  fpending_[static_cast<size_t>(i)] = 1;
 }
 
 void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::vector<int>& loaded,
@@ -869,9 +904,15 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     wait_buf(tp.gin_buf);
     wait_buf(tp.out_buf);
     wait_buf(tp.gout_buf);
-    if (wpending_[static_cast<size_t>(i)]) {  // the stage's new weights (Broadcast, update stream)
+    // the stage's new weights (Broadcast on the update stream): a Forward waits segment by
+    // segment inside its body, a Backward (transposed copies, cleared gradient) for all of it
+    const cudaEvent_t* seg_wait = nullptr;
+    if (task.kind == ppsim::Kind::Forward && fpending_[static_cast<size_t>(i)]) {
+      seg_wait = seg_ev_[static_cast<size_t>(i)].data();
+      fpending_[static_cast<size_t>(i)] = 0;
+    } else if (task.kind == ppsim::Kind::Backward && wpending_[static_cast<size_t>(i)]) {
       CUDA_OK(cudaStreamWaitEvent(cs_, wready_[static_cast<size_t>(i)], 0));
-      wpending_[static_cast<size_t>(i)] = 0;
+      wpending_[static_cast<size_t>(i)] = fpending_[static_cast<size_t>(i)] = 0;
     }
     if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
     record_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, d_trace_, t);
@@ -883,7 +924,8 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     int launched;
     if (task.kind == ppsim::Kind::Forward) {
       uint16_t* out = tp.out_buf >= 0 ? bufs_[static_cast<size_t>(tp.out_buf)].ptr : nullptr;
-      launched = S.forward(A, tok, lab, in, out, d_loss_ + j, loss_scale_[static_cast<size_t>(j)], ws_, cs_, &rc);
+      launched = S.forward(A, tok, lab, in, out, d_loss_ + j, loss_scale_[static_cast<size_t>(j)], ws_, cs_, &rc,
+                           seg_wait);
     } else {
       const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
       uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
@@ -1035,6 +1077,14 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
       exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
   stats.host_issue_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_issue0).count();
+  for (int i = 0; i < depth_; ++i)  // the last window's publications have been copied everywhere
+    if (pending_root_wait_[static_cast<size_t>(i)] >= 0) {
+      cudaStream_t st = comm_->single_stream() ? ks_ : us_;
+      for (size_t k = 0; k < segs_[static_cast<size_t>(i)].size(); ++k)
+        comm_->broadcast_root_wait(pending_root_wait_[static_cast<size_t>(i)] + static_cast<int>(k),
+                                   group_ranks_[static_cast<size_t>(i)], owner_rank(i), st);
+      pending_root_wait_[static_cast<size_t>(i)] = -1;
+    }
   for (cudaStream_t st : {rs_, ss_, ks_, us_})  // join every stream: the run ends when all are idle
     if (st) CUDA_OK(cudaStreamWaitEvent(cs_, handoff(st), 0));
   CUDA_OK(cudaEventRecord(run_end_, cs_));
@@ -1217,16 +1267,26 @@ void Engine::optimizer_step(int stage, int step, cudaStream_t st) {
     S.w = wbuf_[static_cast<size_t>(stage)][static_cast<size_t>(cur)];
     S.wt = wtbuf_[static_cast<size_t>(stage)][static_cast<size_t>(cur)];
   }
+  optimizer_range(stage, step, 0, S.numel(), st);
+  const int nt = S.refresh_transposed(st);
+  if (nt < 0) throw std::runtime_error("weight transpose failed");
+  stats.kernels_launched += nt;
+}
+
+// The optimizer step of parameters [off, off + n) of stage i (detail::apply_update
+// H/optim.hpp:234-268 / AdamW): g / update_div -> master, m, v; bf16 working copy; gradient
+// zeroed.  Elementwise, so any split into ranges gives the same bits as one call.
+void Engine::optimizer_range(int stage, int step, int64_t off, int64_t n, cudaStream_t st) {
+  GptStage& S = *stages[static_cast<size_t>(stage)];
   amdp_opt_args o = rc_.optimizer;
   o.step = step;
   o.grad_scale = rc_.optimizer.grad_scale * (1.0f / update_div_);
-  ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(S.numel()), st);
-  const int rc = amdp_optimizer_step(&o, S.master, S.m, S.v, S.grad, S.w, S.numel(), reinterpret_cast<amdp_stream_t>(st));
+  ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(n), st);
+  const int rc = amdp_optimizer_step(&o, S.master + off, S.m + off, S.v ? S.v + off : nullptr, S.grad + off,
+                                     S.w + off, n, reinterpret_cast<amdp_stream_t>(st));
   ktimer_.end(st);
   if (rc != 0) throw std::runtime_error("optimizer step failed");
-  const int nt = S.refresh_transposed(st);
-  if (nt < 0) throw std::runtime_error("weight transpose failed");
-  stats.kernels_launched += 1 + nt;
+  stats.kernels_launched += 1;
 }
 
 void Engine::copy_params(int stage, float* host, int64_t n, bool to_host) {

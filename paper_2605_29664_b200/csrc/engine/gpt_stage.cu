@@ -263,12 +263,28 @@ size_t GptStage::workspace_bytes(const Dims& d) {
     launched += (nk);         \
   } while (0)
 
+std::vector<std::pair<int64_t, int64_t>> GptStage::segments() const {
+  std::vector<int64_t> starts;
+  if (first()) starts.push_back(0);
+  for (const LayerParams& P : layers_) starts.push_back(P.ln1_g.off);
+  if (last()) starts.push_back(lnf_g_.off);
+  std::vector<std::pair<int64_t, int64_t>> out;
+  for (size_t k = 0; k < starts.size(); ++k)
+    out.emplace_back(starts[k], (k + 1 < starts.size() ? starts[k + 1] : numel_) - starts[k]);
+  return out;
+}
+
 int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
                       const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* wsb,
-                      cudaStream_t s, int* rc) const {
+                      cudaStream_t s, int* rc, const cudaEvent_t* seg_ready) const {
   if (d_.fp32)
     return forward_f32(a, tokens, labels, reinterpret_cast<const float*>(in), reinterpret_cast<float*>(out), loss_sum,
-                       loss_scale, wsb, s, rc);
+                       loss_scale, wsb, s, rc, seg_ready);
+  int seg = 0;  // next segment to wait for
+  auto wait_seg = [&]() {
+    if (seg_ready) cudaStreamWaitEvent(s, seg_ready[seg], 0);
+    ++seg;
+  };
   const Ws ws = carve_ws(d_, wsb);
   int launched = 0;
   *rc = 0;
@@ -276,6 +292,7 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
   const int T = d_.T, h = d_.h;
   const uint16_t* x = in;
   if (first()) {
+    wait_seg();
     AMDP_TRY(K_EMBED, 0, 6.0 * T * h, amdp_embedding_fwd(tokens, w + wte_.off, w + wpe_.off, a.x0, T, d_.S, h, st), 1);
     x = a.x0;
   }
@@ -286,6 +303,7 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
       A.o = ws.rc_o;
       A.f = ws.rc_f;
     }
+    wait_seg();
     AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * h, amdp_layernorm_fwd(x, master + P.ln1_g.off, master + P.ln1_b.off, A.ln1, A.ln1_mean,
                                 A.ln1_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm_t(kt, T, 3 * h, h, A.ln1, h, false, w + P.qkv.off, h, false, A.qkv, 3 * h,
@@ -304,6 +322,7 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
     x = nx;
   }
   if (last()) {
+    wait_seg();
     AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * h, amdp_layernorm_fwd(a.xf, master + lnf_g_.off, master + lnf_b_.off, a.lnf, a.lnf_mean,
                                 a.lnf_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm_t(kt, T, d_.V, h, a.lnf, h, false, w + head_.off, h, false, a.logits, d_.V,
@@ -444,7 +463,13 @@ inline const float* F(const uint16_t* p) { return reinterpret_cast<const float*>
 }  // namespace
 
 int GptStage::forward_f32(const SlotActs& a, const int32_t* tokens, const int32_t* labels, const float* in,
-                          float* out, float* loss_sum, float loss_scale, uint8_t* wsb, cudaStream_t s, int* rc) const {
+                          float* out, float* loss_sum, float loss_scale, uint8_t* wsb, cudaStream_t s, int* rc,
+                          const cudaEvent_t* seg_ready) const {
+  int seg = 0;
+  auto wait_seg = [&]() {
+    if (seg_ready) cudaStreamWaitEvent(s, seg_ready[seg], 0);
+    ++seg;
+  };
   const Ws ws = carve_ws(d_, wsb);
   int launched = 0;
   *rc = 0;
@@ -453,12 +478,14 @@ int GptStage::forward_f32(const SlotActs& a, const int32_t* tokens, const int32_
   const float* W = master;
   const float* x = in;
   if (first()) {
+    wait_seg();
     AMDP_TRY(K_EMBED, 0, 12.0 * T * h, amdp_f32_embedding_fwd(tokens, W + wte_.off, W + wpe_.off, F(a.x0), T, d_.S, h, st), 1);
     x = F(a.x0);
   }
   for (int li = 0; li < l1_ - l0_; ++li) {
     const LayerParams& P = layers_[static_cast<size_t>(li)];
     const LayerActs& A = a.layers[static_cast<size_t>(li)];
+    wait_seg();
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_f32_layernorm_fwd(x, W + P.ln1_g.off, W + P.ln1_b.off, F(A.ln1), A.ln1_mean,
                                                                 A.ln1_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm32(kt, T, 3 * h, h, F(A.ln1), h, false, W + P.qkv.off, h, false, F(A.qkv), 3 * h, AMDP_EPI_STORE_F32, s), 1);
@@ -477,6 +504,7 @@ int GptStage::forward_f32(const SlotActs& a, const int32_t* tokens, const int32_
     x = nx;
   }
   if (last()) {
+    wait_seg();
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_f32_layernorm_fwd(F(a.xf), W + lnf_g_.off, W + lnf_b_.off, F(a.lnf),
                                                                 a.lnf_mean, a.lnf_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm32(kt, T, d_.V, h, F(a.lnf), h, false, W + head_.off, h, false, F(a.logits), d_.V, AMDP_EPI_STORE_F32, s), 1);

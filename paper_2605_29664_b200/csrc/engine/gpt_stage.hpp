@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "amdp_kernels.h"
@@ -100,16 +101,23 @@ class GptStage {
   // output [T][h] (stages < depth-1).  Backward: `gin` incoming grad [T][h] (stages <
   // depth-1), `gout` grad w.r.t. the stage input (stages > 0).  Returns the number of
   // kernels launched (>= 0) or a negative/positive error code via `rc`.
+  // `seg_ready` (optional, one event per segments() entry): the forward waits for segment k's
+  // weights only right before its first use (an optimizer step still running on another
+  // stream overlaps the layers already updated).
   int forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
               const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* ws,
-              cudaStream_t s, int* rc) const;
+              cudaStream_t s, int* rc, const cudaEvent_t* seg_ready = nullptr) const;
+  // The stage's parameters as contiguous (offset, numel) segments in the order the forward
+  // reads them: [embeddings (stage 0)], one per layer, [final LayerNorm + head (last stage)].
+  std::vector<std::pair<int64_t, int64_t>> segments() const;
   int backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in,
                const uint16_t* gin, uint16_t* gout, uint8_t* ws, cudaStream_t s,
                const SideStream& side, int* rc) const;
   // fp32 validation mode bodies (gpt_stage_f32.cu): the same math on float tensors (the
   // activation pointers then address fp32 data), weights read from `master`
   int forward_f32(const SlotActs& a, const int32_t* tokens, const int32_t* labels, const float* in,
-                  float* out, float* loss_sum, float loss_scale, uint8_t* ws, cudaStream_t s, int* rc) const;
+                  float* out, float* loss_sum, float loss_scale, uint8_t* ws, cudaStream_t s, int* rc,
+                  const cudaEvent_t* seg_ready) const;
   int backward_f32(const SlotActs& a, const int32_t* tokens, const float* in, const float* gin,
                    float* gout, uint8_t* ws, cudaStream_t s, int* rc) const;
 

@@ -44,7 +44,7 @@ def measured_costs(tl: P.Timeline, min_window: int = 1, lane_events=None) -> Dic
 
 def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple[P.Kind, int], float],
                         gap_ns: float, declared_fwd=1, declared_bwd=1, devices: int = 0,
-                        update_lane: bool = False, lane_out: dict = None) -> P.Timeline:
+                        update_lane: bool = False, lane_out: dict = None, segments=None) -> P.Timeline:
     """Re-times the declared dispatch order of `policy` (depth stages on `devices`, default
     depth) with measured costs.  Update tasks (replicated-weight policies) cost what the
     stage's measured Broadcast (fused optimizer step) cost.
@@ -56,7 +56,13 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
     does not hold the compute stream: only its graph successors (BC(w-1,i) -> F / preloaded
     B, builder.hpp:289-304) wait for it.  In the returned timeline these tasks are
     zero-length at their finish, so `bubble_ratio` measures compute-stream idle time; their
-    real intervals are appended to `lane_out["events"]` if given."""
+    real intervals are appended to `lane_out["events"]` if given.
+
+    segments (per stage, with update_lane): the Broadcast steps the optimizer segment by
+    segment (embeddings, each layer, head) in the forward's reading order and a gated Forward
+    waits per segment: it may start once the first segment is stepped and cannot finish
+    earlier than one segment's share of its own cost after the last one (the optimizer part
+    taken as 90% of the Broadcast, the rest being the backward's transposed copies)."""
     devices = devices or depth
     declared = P.ClusterSpec.uniform(depth, devices, declared_fwd, declared_bwd)
     g = P.build(policy, declared)
@@ -71,6 +77,7 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
     free = [0] * devices
     ufree = [0] * devices
     finish = [0] * len(g.tasks)
+    bc_start = [0] * len(g.tasks)
     gap = int(round(gap_ns))
     events = []
     lane_kinds = (P.Kind.Reduce, P.Kind.Broadcast) if update_lane else ()
@@ -79,9 +86,18 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
         dur = int(round(costs_ns.get((task.kind, task.stage), 0.0)))
         on_lane = task.kind in lane_kinds
         start = max(free[task.device], ufree[task.device]) if on_lane else free[task.device]
+        min_finish = 0
         for p in preds[t]:
-            start = max(start, finish[p] + (gap if g.tasks[p].device != task.device else 0))
-        finish[t] = start + dur
+            ready = finish[p] + (gap if g.tasks[p].device != task.device else 0)
+            if segments and task.kind == P.Kind.Forward and g.tasks[p].kind == P.Kind.Broadcast:
+                nseg = segments[task.stage]
+                opt = 0.9 * (finish[p] - bc_start[p])
+                ready = bc_start[p] + opt / nseg
+                min_finish = max(min_finish, bc_start[p] + opt + dur / nseg)
+            start = max(start, ready)
+        finish[t] = max(start + dur, min_finish)
+        dur = finish[t] - start
+        bc_start[t] = start
         if on_lane:
             ufree[task.device] = finish[t]
             if lane_out is not None:
@@ -123,7 +139,8 @@ def replicas_of(policy: P.PolicyConfig) -> int:
 
 
 def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, tokens_per_minibatch: int,
-            gap_ns: float, stage_numel=None, policy: P.PolicyConfig = None, lane_events=None) -> dict:
+            gap_ns: float, stage_numel=None, policy: P.PolicyConfig = None, lane_events=None,
+            segments=None) -> dict:
     """Projected d-GPU bubble and throughput of a measured run's schedule (default AMDP).  With
     `stage_numel`, the Reduce / Broadcast tasks also carry the NVLink collective time
     (collective_costs) on top of what was measured on one GPU (the fused optimizer)."""
@@ -138,12 +155,14 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
             costs[(P.Kind.Update, s)] = costs[(P.Kind.Broadcast, s)]
     lane = bool(pol.zero_enabled)  # the executor's update / collective streams (ZeRO)
     if stage_numel is not None and replicas_of(pol) > 1:
-        rep0 = static_order_replay(pol, depth, costs, gap_ns, devices=devices, update_lane=lane)
+        rep0 = static_order_replay(pol, depth, costs, gap_ns, devices=devices, update_lane=lane,
+                                   segments=segments if lane else None)
         bubble_nc = float(P.bubble_ratio(rep0, 1 if windows > 2 else 0))
         for k, v in collective_costs(stage_numel, replicas_of(pol), zero=pol.zero_enabled).items():
             costs[k] = costs.get(k, 0.0) + v
     lane_out = {}
-    rep = static_order_replay(pol, depth, costs, gap_ns, devices=devices, update_lane=lane, lane_out=lane_out)
+    rep = static_order_replay(pol, depth, costs, gap_ns, devices=devices, update_lane=lane, lane_out=lane_out,
+                              segments=segments if lane else None)
     bubble = P.bubble_ratio(rep, 1 if windows > 2 else 0)
     # the same costs with the window machinery serialised on the compute stream (round-1 executor)
     serial = static_order_replay(pol, depth, costs, gap_ns, devices=devices) if lane else rep

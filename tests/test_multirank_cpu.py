@@ -101,7 +101,10 @@ def test_fold_within_replica_groups(world, fold, hosted, group_size):
             assert {s["stage"] for s in pl["stages"] if s["hosted"]} == hosted[r]
         for s in pl["stages"]:
             assert len(s["group"]) == group_size
-        assert pl["collectives"] == (0 if group_size == 1 else 2 * 8 * 2)  # R + BC per stage per window
+        # per stage and window: one Reduce + one Broadcast per parameter segment (embeddings /
+        # layer / head), 2 windows
+        segs = sum(1 + n + (s == 0) + (s == 7) for s, n in enumerate(pl["partition"]))
+        assert pl["collectives"] == (0 if group_size == 1 else 2 * segs)
         kinds = {o[1] for o in pl["comm_ops"]}
         if world == 2:
             assert kinds == {"send", "recv"}
