@@ -57,15 +57,20 @@ class Comm {
   virtual void send(int msg, int peer, const void* buf, size_t bytes, cudaStream_t s) = 0;
   virtual void recv(int msg, int peer, void* dst, size_t bytes, cudaStream_t s) = 0;
 
-  // ---- replica-group collectives (group = sorted ranks hosting the stage; root a rank id)
-  virtual void reduce_f32(int coll, const std::vector<int>& group, int root, int stage, float* buf,
-                          size_t n, cudaStream_t s) = 0;
-  // root's spans -> every member's same spans.  root_waits = false: the root only publishes
-  // (the call returns without waiting for the members' copies); it must then call
-  // broadcast_root_wait(coll, ...) before it next modifies the spans.
-  virtual void broadcast(int coll, const std::vector<int>& group, int root, int stage,
-                         const std::vector<Span>& spans, cudaStream_t s, bool root_waits = true) = 0;
-  virtual void broadcast_root_wait(int coll, const std::vector<int>& group, int root, cudaStream_t s) = 0;
+  // ---- replica-group collectives (group = sorted ranks hosting the stage; members indexed
+  // by their position in it).  ZeRO within the replica group: the window gradient is
+  // reduce-scattered (member j ends with the group sum over ranges[j]), each member steps the
+  // optimizer on its ranges, and the updated weights are all-gathered.
+  using Ranges = std::vector<std::pair<size_t, size_t>>;  // element [lo, hi)
+  virtual void reduce_scatter_f32(int coll, const std::vector<int>& group, int stage, float* buf,
+                                  const std::vector<Ranges>& ranges, cudaStream_t s) = 0;
+  // every member's spans[j] (its own, freshly written) -> all other members.  Returns once this
+  // rank has copied everyone's spans; before a member next modifies its own spans it calls
+  // allgather_wait(coll, ...) (every other member has copied them).
+  virtual void allgather(int coll, const std::vector<int>& group, int stage,
+                         const std::vector<std::vector<Span>>& spans, cudaStream_t s) = 0;
+  virtual void allgather_wait(int coll, const std::vector<int>& group, cudaStream_t s) = 0;
+  // replicated updates: the whole window gradient summed on every member
   virtual void allreduce_f32(int coll, const std::vector<int>& group, int stage, float* buf, size_t n,
                              cudaStream_t s) = 0;
 

@@ -3,10 +3,10 @@
 // Flag array of one rank (int32, waited on by that rank only, written by its peers):
 //   [0, M)                 READY(msg)   the producer's payload of message msg is complete
 //   [M, 2M)                ACK(msg)     the consumer has copied message msg out
-//   2M + 32 c + [0, 8)     collective c: phase-1 arrival of group member k
-//   2M + 32 c + [8, 16)    phase-2 arrival (broadcast: member done; all-reduce: chunk summed)
+//   2M + 32 c + [0, 8)     collective c: phase-1 arrival of group member k (its data ready)
+//   2M + 32 c + [8, 16)    phase-2 arrival (reduce-scatter / all-reduce: its ranges summed;
+//                          all-gather: it has copied every other member's spans)
 //   2M + 32 c + [16, 24)   phase-3 arrival (all-reduce: member gathered every chunk)
-//   2M + 32 c + 24         reduce: root has read every member's gradient
 // A flag holds the epoch (run counter) of its last signal; waits are "flag >= epoch", so no
 // flag is ever reset and consecutive runs cannot confuse each other.
 #include <cuda.h>
@@ -201,55 +201,48 @@ class IpcComm final : public Comm {
     bytes_in_ += static_cast<int64_t>(bytes);
   }
 
-  void reduce_f32(int coll, const std::vector<int>& group, int root, int stage, float* buf, size_t n,
-                  cudaStream_t s) override {
-    const int base = coll_base(coll), me = index_in(group, rank_), ri = index_in(group, root);
-    if (rank_ == root) {
-      for (int j = 0; j < static_cast<int>(group.size()); ++j)
-        if (j != me) wait(s, base + j);
+  void reduce_scatter_f32(int coll, const std::vector<int>& group, int stage, float* buf,
+                          const std::vector<Ranges>& ranges, cudaStream_t s) override {
+    const int G = static_cast<int>(group.size()), base = coll_base(coll), me = index_in(group, rank_);
+    // 1. every member's window gradient is complete
+    signal(s, to_others(group, base + me));
+    wait_others(group, base, s);
+    // 2. this member sums its ranges over the group (group order: deterministic)
+    for (const auto& [lo, hi] : ranges.at(static_cast<size_t>(me))) {
+      if (hi <= lo) continue;
       SumSrcs src{};
-      src.n = static_cast<int>(group.size());
-      for (int j = 0; j < src.n; ++j)
-        src.p[j] = j == me ? buf : static_cast<const float*>(region(group[static_cast<size_t>(j)], REG_GRAD, stage));
-      launch_sum(buf, src, n, s);
-      std::vector<int*> t;
-      for (int j = 0; j < static_cast<int>(group.size()); ++j)
-        if (j != me) t.push_back(flag_of(group[static_cast<size_t>(j)], base + 24));
-      signal(s, t);
-    } else {
-      signal(s, {flag_of(root, base + me)});
-      wait(s, base + 24);
+      src.n = G;
+      for (int j = 0; j < G; ++j)
+        src.p[j] = (j == me ? buf : static_cast<const float*>(region(group[static_cast<size_t>(j)], REG_GRAD, stage))) + lo;
+      launch_sum(buf + lo, src, hi - lo, s);
+      bytes_in_ += static_cast<int64_t>((G - 1) * (hi - lo) * sizeof(float));
     }
-    (void)ri;
+    // 3. nobody modifies its gradient before every member has read its ranges from it
+    signal(s, to_others(group, base + 8 + me));
+    wait_others(group, base + 8, s);
   }
 
-  void broadcast(int coll, const std::vector<int>& group, int root, int stage, const std::vector<Span>& spans,
-                 cudaStream_t s, bool root_waits) override {
+  void allgather(int coll, const std::vector<int>& group, int stage, const std::vector<std::vector<Span>>& spans,
+                 cudaStream_t s) override {
     (void)stage;
-    const int base = coll_base(coll), me = index_in(group, rank_), ri = index_in(group, root);
-    if (rank_ == root) {
-      std::vector<int*> t;
-      for (int j = 0; j < static_cast<int>(group.size()); ++j)
-        if (j != me) t.push_back(flag_of(group[static_cast<size_t>(j)], base + ri));
-      signal(s, t);
-      if (root_waits) broadcast_root_wait(coll, group, root, s);
-    } else {
-      wait(s, base + ri);
-      for (const Span& sp : spans) {
+    const int G = static_cast<int>(group.size()), base = coll_base(coll), me = index_in(group, rank_);
+    signal(s, to_others(group, base + me));  // my spans are written
+    for (int j = 0; j < G; ++j) {
+      if (j == me) continue;
+      wait(s, base + j);
+      for (const Span& sp : spans.at(static_cast<size_t>(j))) {
+        if (!sp.bytes) continue;
         char* dst = static_cast<char*>(local_region(sp.kind, sp.index)) + sp.offset;
-        const char* src = static_cast<const char*>(region(root, sp.kind, sp.index)) + sp.offset;
+        const char* src = static_cast<const char*>(region(group[static_cast<size_t>(j)], sp.kind, sp.index)) + sp.offset;
         IPC_OK(cudaMemcpyAsync(dst, src, sp.bytes, cudaMemcpyDeviceToDevice, s));
         bytes_in_ += static_cast<int64_t>(sp.bytes);
       }
-      signal(s, {flag_of(root, base + 8 + me)});
     }
+    signal(s, to_others(group, base + 8 + me));  // I have copied everyone's
   }
 
-  void broadcast_root_wait(int coll, const std::vector<int>& group, int root, cudaStream_t s) override {
-    if (rank_ != root) return;
-    const int base = coll_base(coll), me = index_in(group, rank_);
-    for (int j = 0; j < static_cast<int>(group.size()); ++j)
-      if (j != me) wait(s, base + 8 + j);
+  void allgather_wait(int coll, const std::vector<int>& group, cudaStream_t s) override {
+    wait_others(group, coll_base(coll) + 8, s);
   }
 
   void allreduce_f32(int coll, const std::vector<int>& group, int stage, float* buf, size_t n,
@@ -332,6 +325,18 @@ class IpcComm final : public Comm {
     return it->second;
   }
   int* flag_of(int peer, int idx) const { return peers_.at(static_cast<size_t>(peer)).flags + idx; }
+  // flag `idx` of every other group member / wait for flags base + j of every other member j
+  std::vector<int*> to_others(const std::vector<int>& group, int idx) const {
+    std::vector<int*> t;
+    for (int r : group)
+      if (r != rank_) t.push_back(flag_of(r, idx));
+    return t;
+  }
+  void wait_others(const std::vector<int>& group, int base, cudaStream_t s) {
+    const int me = index_in(group, rank_);
+    for (int j = 0; j < static_cast<int>(group.size()); ++j)
+      if (j != me) wait(s, base + j);
+  }
   int coll_base(int coll) const { return 2 * nmsg_ + kCollStride * coll; }
   static int index_in(const std::vector<int>& g, int r) {
     auto it = std::find(g.begin(), g.end(), r);

@@ -66,22 +66,28 @@ class NcclComm final : public Comm {
     NCCL_OK(ncclRecv(dst, bytes, ncclUint8, peer, world_comm_, s));
     bytes_in_ += static_cast<int64_t>(bytes);
   }
-  void reduce_f32(int, const std::vector<int>& group, int root, int stage, float* buf, size_t n,
-                  cudaStream_t s) override {
-    NCCL_OK(ncclReduce(buf, buf, n, ncclFloat32, ncclSum, index_in(group, root), comm(stage), s));
-  }
-  void broadcast_root_wait(int, const std::vector<int>&, int, cudaStream_t) override {}
-  void broadcast(int, const std::vector<int>& group, int root, int stage, const std::vector<Span>& spans,
-                 cudaStream_t s, bool) override {
-    const int r = index_in(group, root);
+  void reduce_scatter_f32(int, const std::vector<int>& group, int stage, float* buf, const std::vector<Ranges>& ranges,
+                          cudaStream_t s) override {
     NCCL_OK(ncclGroupStart());
-    for (const Span& sp : spans) {
-      char* p = static_cast<char*>(regions_.at({sp.kind, sp.index})) + sp.offset;
-      NCCL_OK(ncclBroadcast(p, p, sp.bytes, ncclUint8, r, comm(stage), s));
-      if (rank_ != root) bytes_in_ += static_cast<int64_t>(sp.bytes);
-    }
+    for (size_t j = 0; j < group.size(); ++j)
+      for (const auto& [lo, hi] : ranges[j])
+        if (hi > lo)
+          NCCL_OK(ncclReduce(buf + lo, buf + lo, hi - lo, ncclFloat32, ncclSum, static_cast<int>(j), comm(stage), s));
     NCCL_OK(ncclGroupEnd());
   }
+  void allgather(int, const std::vector<int>& group, int stage, const std::vector<std::vector<Span>>& spans,
+                 cudaStream_t s) override {
+    NCCL_OK(ncclGroupStart());
+    for (size_t j = 0; j < group.size(); ++j)
+      for (const Span& sp : spans[j]) {
+        if (!sp.bytes) continue;
+        char* p = static_cast<char*>(regions_.at({sp.kind, sp.index})) + sp.offset;
+        NCCL_OK(ncclBroadcast(p, p, sp.bytes, ncclUint8, static_cast<int>(j), comm(stage), s));
+        if (group[j] != rank_) bytes_in_ += static_cast<int64_t>(sp.bytes);
+      }
+    NCCL_OK(ncclGroupEnd());
+  }
+  void allgather_wait(int, const std::vector<int>&, cudaStream_t) override {}
   void allreduce_f32(int, const std::vector<int>&, int stage, float* buf, size_t n, cudaStream_t s) override {
     NCCL_OK(ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, comm(stage), s));
   }

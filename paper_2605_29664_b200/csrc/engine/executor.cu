@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -159,6 +160,13 @@ class Engine {
   }
   KTimer ktimer_;
   std::string plan_json() const;
+  std::string shard_json(int i) const {  // this rank's ZeRO ranges of stage i ([] if unsharded)
+    std::string r;
+    if (!sharded(i) || !hosted[static_cast<size_t>(i)]) return r;
+    for (const auto& [lo, hi] : shard_[static_cast<size_t>(i)][static_cast<size_t>(member(i))])
+      r += (r.empty() ? "[" : ",[") + std::to_string(lo) + "," + std::to_string(hi) + "]";
+    return r;
+  }
   std::string version_csv() const;
   int64_t stage_numel(int stage) const;
   void copy_params(int stage, float* host, int64_t n, bool to_host);
@@ -197,8 +205,20 @@ class Engine {
   float update_div_ = 1.f;                               // minibatches per optimizer step
   void use_replica_weights(int stage, int pipeline);
   void optimizer_step(int stage, int step, cudaStream_t st);  // whole stage + transposed copies
-  void optimizer_range(int stage, int step, int64_t off, int64_t n, cudaStream_t st);
-  std::vector<int> pending_root_wait_;  // per stage: first collective id of an unconfirmed publication
+  // m_off: where parameter `off`'s optimizer state lives in the stage's m / v (= off unless sharded)
+  void optimizer_range(int stage, int step, int64_t off, int64_t n, cudaStream_t st, int64_t m_off = -1);
+  std::vector<int> pending_ag_;  // per stage: first collective id of an all-gather not yet confirmed
+  // ZeRO within a multi-rank replica group: member j of stage i's group steps the optimizer on
+  // shard_[i][j] (its part of every parameter segment) and keeps m / v for those ranges only,
+  // packed (opt_off_[i][k]: packed offset of this rank's k-th range)
+  bool sharded(int i) const { return zero_ && group_ranks_[static_cast<size_t>(i)].size() > 1; }
+  int member(int i) const {
+    const auto& g = group_ranks_[static_cast<size_t>(i)];
+    return static_cast<int>(std::find(g.begin(), g.end(), rank_) - g.begin());
+  }
+  std::vector<std::vector<Comm::Ranges>> shard_;
+  std::vector<std::vector<int64_t>> opt_off_;
+  std::vector<int64_t> opt_numel_;  // per stage: optimizer-state elements on this rank
   int cur_pos_ = 0;  // order position being issued
   int64_t comm_launches_seen_ = 0;
   std::vector<TaskPlan> plan_;               // per order position
@@ -389,6 +409,37 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
     hosted[static_cast<size_t>(i)] = std::count(group_ranks_[static_cast<size_t>(i)].begin(),
                                                 group_ranks_[static_cast<size_t>(i)].end(), rank_) > 0;
     owned[static_cast<size_t>(i)] = zero_ ? owner_rank(i) == rank_ : hosted[static_cast<size_t>(i)];
+  }
+  // ZeRO shards: every parameter segment split over the replica group in 64-element-aligned
+  // parts, part j to member j (sharded(i) groups only; otherwise the owner holds everything)
+  shard_.assign(static_cast<size_t>(depth_), {});
+  opt_off_.assign(static_cast<size_t>(depth_), {});
+  opt_numel_.assign(static_cast<size_t>(depth_), 0);
+  for (int i = 0; i < depth_; ++i) {
+    const int64_t n = stages[static_cast<size_t>(i)]->numel();
+    if (!sharded(i)) {
+      if (owned[static_cast<size_t>(i)]) opt_numel_[static_cast<size_t>(i)] = n;
+      continue;
+    }
+    const size_t G = group_ranks_[static_cast<size_t>(i)].size();
+    auto& sh = shard_[static_cast<size_t>(i)];
+    sh.assign(G, {});
+    for (const auto& [off, len] : stages[static_cast<size_t>(i)]->segments()) {
+      const int64_t q = ((len + static_cast<int64_t>(G) - 1) / static_cast<int64_t>(G) + 63) / 64 * 64;
+      for (size_t j = 0; j < G; ++j) {
+        const int64_t lo = std::min(len, q * static_cast<int64_t>(j)), hi = std::min(len, lo + q);
+        sh[j].emplace_back(static_cast<size_t>(off + lo), static_cast<size_t>(off + hi));
+      }
+    }
+    owned[static_cast<size_t>(i)] = hosted[static_cast<size_t>(i)];
+    if (hosted[static_cast<size_t>(i)]) {
+      int64_t c = 0;
+      for (const auto& [lo, hi] : sh[static_cast<size_t>(member(i))]) {
+        opt_off_[static_cast<size_t>(i)].push_back(c);
+        c += static_cast<int64_t>(hi - lo);
+      }
+      opt_numel_[static_cast<size_t>(i)] = c;
+    }
   }
 
   make_plan();
@@ -667,11 +718,12 @@ void Engine::allocate() {
       CUDA_OK(cudaMalloc(&wb[1], n * sizeof(uint16_t)));
       CUDA_OK(cudaMalloc(&wtb[1], n * sizeof(uint16_t)));
     }
-    if (owned[static_cast<size_t>(i)]) {
-      CUDA_OK(cudaMalloc(&st.m, n * sizeof(float)));
-      CUDA_OK(cudaMalloc(&st.v, n * sizeof(float)));
-      CUDA_OK(cudaMemsetAsync(st.m, 0, n * sizeof(float), cs_));
-      CUDA_OK(cudaMemsetAsync(st.v, 0, n * sizeof(float), cs_));
+    if (owned[static_cast<size_t>(i)]) {  // the optimizer state this rank keeps (its shard under ZeRO)
+      const size_t no = static_cast<size_t>(std::max<int64_t>(opt_numel_[static_cast<size_t>(i)], 64));
+      CUDA_OK(cudaMalloc(&st.m, no * sizeof(float)));
+      CUDA_OK(cudaMalloc(&st.v, no * sizeof(float)));
+      CUDA_OK(cudaMemsetAsync(st.m, 0, no * sizeof(float), cs_));
+      CUDA_OK(cudaMemsetAsync(st.v, 0, no * sizeof(float), cs_));
     }
   }
   slot_mem_.assign(static_cast<size_t>(depth_), {});
@@ -706,7 +758,7 @@ void Engine::allocate() {
   reduced_.resize(static_cast<size_t>(depth_));
   wpending_.assign(static_cast<size_t>(depth_), 0);
   fpending_.assign(static_cast<size_t>(depth_), 0);
-  pending_root_wait_.assign(static_cast<size_t>(depth_), -1);
+  pending_ag_.assign(static_cast<size_t>(depth_), -1);
   segs_.resize(static_cast<size_t>(depth_));
   seg_ev_.resize(static_cast<size_t>(depth_));
   for (int i = 0; i < depth_; ++i) {
@@ -787,8 +839,9 @@ void Engine::exec_comm(int pos) {
       case CommOp::Reduce: {
         GptStage& st = *stages[static_cast<size_t>(op.stage)];
         CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));  // the window's backwards of this rank
-        comm_->reduce_f32(op.id, group_ranks_[static_cast<size_t>(op.stage)], owner_rank(op.stage), op.stage,
-                          st.grad, static_cast<size_t>(st.numel()), ks_);
+        // ZeRO within the group: member j ends with the group's sum over its shard
+        comm_->reduce_scatter_f32(op.id, group_ranks_[static_cast<size_t>(op.stage)], op.stage, st.grad,
+                                  shard_[static_cast<size_t>(op.stage)], ks_);
         CUDA_OK(cudaEventRecord(reduced_[static_cast<size_t>(op.stage)], ks_));
         stats.collective_bytes += st.numel() * 4;
         break;
@@ -809,8 +862,7 @@ void Engine::exec_comm(int pos) {
 void Engine::zero_broadcast(int i, int window) {
   GptStage& S = *stages[static_cast<size_t>(i)];
   const auto& gr = group_ranks_[static_cast<size_t>(i)];
-  const bool multi = gr.size() > 1;
-  const bool own = owned[static_cast<size_t>(i)];
+  const bool multi = sharded(i);
   CUDA_OK(cudaStreamWaitEvent(us_, handoff(cs_), 0));
   if (multi) CUDA_OK(cudaStreamWaitEvent(us_, reduced_[static_cast<size_t>(i)], 0));
   // the update stream's interval of this Broadcast (a lane event: it overlaps other stages'
@@ -819,50 +871,70 @@ void Engine::zero_broadcast(int i, int window) {
     CUDA_OK(cudaEventRecord(ev_lstart_[static_cast<size_t>(cur_pos_)], us_));
     lane_rec_[static_cast<size_t>(cur_pos_)] = 1;
   }
-  int coll0 = -1;
-  for (const CommOp& op : comm_at_[static_cast<size_t>(cur_pos_)])
-    if (op.kind == CommOp::Bcast && op.stage == i) coll0 = op.id;
-  // NCCL: the collectives of one communicator must share its stream, so the whole Broadcast
-  // runs there; the peer-memory backend runs it on the update stream
-  cudaStream_t st = multi && comm_->single_stream() ? ks_ : us_;
-  if (st != us_) CUDA_OK(cudaStreamWaitEvent(st, handoff(us_), 0));
-  // the previous window's publication of these weights must have been copied by every replica
-  // before the optimizer overwrites them
-  if (pending_root_wait_[static_cast<size_t>(i)] >= 0) {
-    const int c0 = pending_root_wait_[static_cast<size_t>(i)];
-    for (size_t k = 0; k < segs_[static_cast<size_t>(i)].size(); ++k)
-      comm_->broadcast_root_wait(c0 + static_cast<int>(k), gr, owner_rank(i), st);
-    pending_root_wait_[static_cast<size_t>(i)] = -1;
-  }
-  if (!own) CUDA_OK(cudaMemsetAsync(S.grad, 0, static_cast<size_t>(S.numel()) * sizeof(float), st));
-  // segment by segment in the forward's reading order (embeddings, layers, head): a gated
-  // Forward starts on the first layer while the optimizer still runs on the later ones
   const auto& segs = segs_[static_cast<size_t>(i)];
-  int64_t moved = 0;
-  for (size_t k = 0; k < segs.size(); ++k) {
-    const int64_t off = segs[k].first, n = segs[k].second;
-    if (own) optimizer_range(i, window + 1, off, n, st);
-    if (multi) {
-      std::vector<Span> spans;
-      if (dm.fp32) {  // fp32 validation mode: the kernels read the fp32 master itself
-        spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(off) * 4, static_cast<size_t>(n) * 4});
-      } else {  // bf16 working weights + the fp32 LayerNorm parameters the kernels read
-        spans.push_back(Span{REG_W, i, static_cast<size_t>(off) * 2, static_cast<size_t>(n) * 2});
-        for (const auto& p : S.params())
-          if (p.rows == 1 && p.off >= off && p.off < off + n)
-            spans.push_back(Span{REG_MASTER, i, static_cast<size_t>(p.off) * 4, static_cast<size_t>(p.numel()) * 4});
-      }
-      comm_->broadcast(coll0 + static_cast<int>(k), gr, owner_rank(i), i, spans, st, /*root_waits=*/false);
-      for (const Span& sp : spans) moved += static_cast<int64_t>(sp.bytes);
+  if (!multi) {
+    // every replica of stage i is on this GPU (they share one set of buffers): the owner
+    // steps segment by segment in the forward's reading order (embeddings, layers, head), so
+    // a gated Forward starts on its first layer while later layers are still being stepped
+    for (size_t k = 0; k < segs.size(); ++k) {
+      optimizer_range(i, window + 1, segs[k].first, segs[k].second, us_);
+      CUDA_OK(cudaEventRecord(seg_ev_[static_cast<size_t>(i)][k], us_));
     }
-    CUDA_OK(cudaEventRecord(seg_ev_[static_cast<size_t>(i)][k], st));
+  } else {
+    // ZeRO within the replica group: after the reduce-scatter (collective stream) each member
+    // steps its shard of every segment and the group all-gathers the bf16 weights + fp32
+    // LayerNorm parameters (fp32 validation mode: the fp32 master), segment by segment.
+    // NCCL: the collectives of one communicator share its stream, so this runs there.
+    int coll0 = -1;
+    for (const CommOp& op : comm_at_[static_cast<size_t>(cur_pos_)])
+      if (op.kind == CommOp::Bcast && op.stage == i) coll0 = op.id;
+    cudaStream_t st = comm_->single_stream() ? ks_ : us_;
+    if (st != us_) CUDA_OK(cudaStreamWaitEvent(st, handoff(us_), 0));
+    // the previous window's gather of these weights must be complete everywhere before the
+    // optimizer overwrites this rank's shard
+    if (pending_ag_[static_cast<size_t>(i)] >= 0) {
+      for (size_t k = 0; k < segs.size(); ++k)
+        comm_->allgather_wait(pending_ag_[static_cast<size_t>(i)] + static_cast<int>(k), gr, st);
+      pending_ag_[static_cast<size_t>(i)] = -1;
+    }
+    const auto& sh = shard_[static_cast<size_t>(i)];
+    const int me = member(i);
+    int64_t moved = 0;
+    for (size_t k = 0; k < segs.size(); ++k) {
+      const auto [lo, hi] = sh[static_cast<size_t>(me)][k];
+      if (hi > lo)
+        optimizer_range(i, window + 1, static_cast<int64_t>(lo), static_cast<int64_t>(hi - lo), st,
+                        opt_off_[static_cast<size_t>(i)][k]);
+      std::vector<std::vector<Span>> spans(gr.size());
+      for (size_t j = 0; j < gr.size(); ++j) {
+        const auto [a, b] = sh[j][k];
+        if (b <= a) continue;
+        if (dm.fp32) {  // fp32 validation mode: the kernels read the fp32 master itself
+          spans[j].push_back(Span{REG_MASTER, i, a * 4, (b - a) * 4});
+        } else {  // bf16 working weights + the fp32 LayerNorm parameters the kernels read
+          spans[j].push_back(Span{REG_W, i, a * 2, (b - a) * 2});
+          for (const auto& p : S.params()) {
+            const size_t p0 = static_cast<size_t>(p.off), p1 = p0 + static_cast<size_t>(p.numel());
+            if (p.rows == 1 && p1 > a && p0 < b)
+              spans[j].push_back(Span{REG_MASTER, i, std::max(p0, a) * 4, (std::min(p1, b) - std::max(p0, a)) * 4});
+          }
+        }
+        if (j != static_cast<size_t>(me))
+          for (const Span& sp : spans[j]) moved += static_cast<int64_t>(sp.bytes);
+      }
+      comm_->allgather(coll0 + static_cast<int>(k), gr, i, spans, st);
+      CUDA_OK(cudaEventRecord(seg_ev_[static_cast<size_t>(i)][k], st));
+    }
+    pending_ag_[static_cast<size_t>(i)] = coll0;
+    stats.collective_bytes += moved;
+    // the optimizer zeroed this rank's shard of the window gradient; the rest was consumed by
+    // the reduce-scatter
+    CUDA_OK(cudaMemsetAsync(S.grad, 0, static_cast<size_t>(S.numel()) * sizeof(float), st));
+    if (st != us_) CUDA_OK(cudaStreamWaitEvent(us_, handoff(st), 0));
   }
-  if (multi && own) pending_root_wait_[static_cast<size_t>(i)] = coll0;
-  stats.collective_bytes += moved;
-  const int nt = S.refresh_transposed(st);  // the backward's K-major weight copies
+  const int nt = S.refresh_transposed(us_);  // the backward's K-major weight copies
   if (nt < 0) throw std::runtime_error("weight transpose failed");
   stats.kernels_launched += nt;
-  if (st != us_) CUDA_OK(cudaStreamWaitEvent(us_, handoff(st), 0));
   CUDA_OK(cudaEventRecord(wready_[static_cast<size_t>(i)], us_));
   if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_lend_[static_cast<size_t>(cur_pos_)], us_));
   wpending_[static_cast<size_t>(i)] = 1;
@@ -1077,13 +1149,13 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
       exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
   stats.host_issue_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_issue0).count();
-  for (int i = 0; i < depth_; ++i)  // the last window's publications have been copied everywhere
-    if (pending_root_wait_[static_cast<size_t>(i)] >= 0) {
+  for (int i = 0; i < depth_; ++i)  // the last window's gathers have completed everywhere
+    if (pending_ag_[static_cast<size_t>(i)] >= 0) {
       cudaStream_t st = comm_->single_stream() ? ks_ : us_;
       for (size_t k = 0; k < segs_[static_cast<size_t>(i)].size(); ++k)
-        comm_->broadcast_root_wait(pending_root_wait_[static_cast<size_t>(i)] + static_cast<int>(k),
-                                   group_ranks_[static_cast<size_t>(i)], owner_rank(i), st);
-      pending_root_wait_[static_cast<size_t>(i)] = -1;
+        comm_->allgather_wait(pending_ag_[static_cast<size_t>(i)] + static_cast<int>(k), group_ranks_[static_cast<size_t>(i)],
+                              st);
+      pending_ag_[static_cast<size_t>(i)] = -1;
     }
   for (cudaStream_t st : {rs_, ss_, ks_, us_})  // join every stream: the run ends when all are idle
     if (st) CUDA_OK(cudaStreamWaitEvent(cs_, handoff(st), 0));
@@ -1161,6 +1233,8 @@ std::string Engine::plan_json() const {
     s += std::string(i ? ",{" : "{") + "\"stage\":" + std::to_string(i) + ",\"hosted\":" +
          (hosted[static_cast<size_t>(i)] ? "true" : "false") + ",\"owner\":" +
          (owned[static_cast<size_t>(i)] ? "true" : "false") + ",\"numel\":" + std::to_string(st.numel()) +
+         ",\"owner_rank\":" + std::to_string(owner_rank(i)) + ",\"opt_numel\":" +
+         std::to_string(opt_numel_[static_cast<size_t>(i)]) + ",\"shard\":[" + shard_json(i) + "]" +
          ",\"slots\":" + std::to_string(slots_per_stage[static_cast<size_t>(i)]) +
          ",\"slot_bytes\":" + std::to_string(st.slot_bytes()) + ",\"group\":[";
     const auto& gr = group_ranks_[static_cast<size_t>(i)];
@@ -1192,10 +1266,22 @@ std::string Engine::plan_json() const {
 // the reference's memory model (H/analysis.hpp:226-330: stage replicas, gradient buffers,
 // optimizer-state multiples, live per-stage activations), plus the measured cudaMemGetInfo
 // delta across allocate().  Co-resident replicas of one stage share one set of buffers.
+namespace {
+std::string fmt_units(double u) {  // shards of 64-aligned segments: round to 1e-3 of a stage
+  char b[32];
+  std::snprintf(b, sizeof(b), "%.3f", u);
+  std::string s(b);
+  while (!s.empty() && s.back() == '0') s.pop_back();
+  if (!s.empty() && s.back() == '.') s.pop_back();
+  return s;
+}
+}  // namespace
+
 std::string Engine::memory_json() const {
   const int64_t T = dm.T, h = dm.h;
   int64_t w = 0, wt = 0, wver = 0, master = 0, grad = 0, opt = 0, act = 0;
-  int hosted_n = 0, owned_n = 0, slots = 0;
+  int hosted_n = 0, slots = 0;
+  double owned_units = 0;  // optimizer state in stage-weight units (m + v = 2 per full stage)
   for (int i = 0; i < depth_; ++i) {
     if (!hosted[static_cast<size_t>(i)]) continue;
     const int64_t n = stages[static_cast<size_t>(i)]->numel();
@@ -1206,8 +1292,8 @@ std::string Engine::memory_json() const {
     master += 4 * n;
     grad += 4 * n;
     if (owned[static_cast<size_t>(i)]) {
-      opt += 8 * n;
-      ++owned_n;
+      opt += 8 * opt_numel_[static_cast<size_t>(i)];
+      owned_units += 2.0 * static_cast<double>(opt_numel_[static_cast<size_t>(i)]) / static_cast<double>(n);
     }
     slots += slots_per_stage[static_cast<size_t>(i)];
     act += static_cast<int64_t>(slots_per_stage[static_cast<size_t>(i)]) *
@@ -1223,7 +1309,7 @@ std::string Engine::memory_json() const {
          "," + kv("activations", act) + "," + kv("boundary_buffers", bounds) + "," + kv("workspace", wsb) + "," +
          kv("token_io", io) + "," + kv("total", total) + "," + kv("measured_device_bytes", measured_alloc_bytes_) +
          "," + kv("weight_units", hosted_n) + "," + kv("gradient_units", hosted_n) + "," +
-         kv("optimizer_state_units", 2 * owned_n) + "," + kv("activation_slots", slots) + "}";
+         "\"optimizer_state_units\":" + fmt_units(owned_units) + "," + kv("activation_slots", slots) + "}";
 }
 
 std::string Engine::version_csv() const {
@@ -1276,13 +1362,14 @@ void Engine::optimizer_step(int stage, int step, cudaStream_t st) {
 // The optimizer step of parameters [off, off + n) of stage i (detail::apply_update
 // H/optim.hpp:234-268 / AdamW): g / update_div -> master, m, v; bf16 working copy; gradient
 // zeroed.  Elementwise, so any split into ranges gives the same bits as one call.
-void Engine::optimizer_range(int stage, int step, int64_t off, int64_t n, cudaStream_t st) {
+void Engine::optimizer_range(int stage, int step, int64_t off, int64_t n, cudaStream_t st, int64_t m_off) {
   GptStage& S = *stages[static_cast<size_t>(stage)];
+  if (m_off < 0) m_off = off;
   amdp_opt_args o = rc_.optimizer;
   o.step = step;
   o.grad_scale = rc_.optimizer.grad_scale * (1.0f / update_div_);
   ktimer_.begin(K_OPTIM, 0, 34.0 * static_cast<double>(n), st);
-  const int rc = amdp_optimizer_step(&o, S.master + off, S.m + off, S.v ? S.v + off : nullptr, S.grad + off,
+  const int rc = amdp_optimizer_step(&o, S.master + off, S.m + m_off, S.v ? S.v + m_off : nullptr, S.grad + off,
                                      S.w + off, n, reinterpret_cast<amdp_stream_t>(st));
   ktimer_.end(st);
   if (rc != 0) throw std::runtime_error("optimizer step failed");

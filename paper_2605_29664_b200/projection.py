@@ -113,12 +113,13 @@ def static_order_replay(policy: P.PolicyConfig, depth: int, costs_ns: Dict[Tuple
 
 def collective_costs(stage_numel, replicas: int, link_gbs: float = 770.0,
                      zero: bool = True) -> Dict[Tuple[P.Kind, int], float]:
-    """Window-boundary communication a 1-GPU run does not perform: per stage, the ZeRO Reduce of
-    the fp32 window gradient to the owner (4 B/param) and the Broadcast of the bf16 weights
-    (2 B/param; the LayerNorm parameters' fp32 copy is negligible) over the stage's `replicas`
-    devices, each moving (replicas-1)/replicas of those bytes per device
-    (analysis.hpp:341-346 reduce_broadcast_cost) at the measured peer bandwidth; without ZeRO,
-    the all-reduce of the fp32 window gradient (reduce + broadcast volume) in every Update."""
+    """Window-boundary communication a 1-GPU run does not perform.  ZeRO (the executor's
+    peer-memory data plane): the Reduce is a reduce-scatter of the fp32 window gradient
+    (4 B/param) and the Broadcast an all-gather of the bf16 weights (2 B/param; the LayerNorm
+    parameters' fp32 copy is negligible) over the stage's `replicas` devices, each device
+    pulling (replicas-1)/replicas of those bytes (analysis.hpp:341-346 reduce_broadcast_cost)
+    at the measured peer bandwidth; without ZeRO, the all-reduce of the fp32 window gradient
+    (reduce-scatter + all-gather volume) in every Update."""
     f = (replicas - 1) / replicas if replicas > 1 else 0.0
     out = {}
     for s, n in enumerate(stage_numel):
@@ -154,6 +155,14 @@ def project(tl_measured: P.Timeline, depth: int, threshold: int, windows: int, t
         if (P.Kind.Update, s) not in costs and (P.Kind.Broadcast, s) in costs:
             costs[(P.Kind.Update, s)] = costs[(P.Kind.Broadcast, s)]
     lane = bool(pol.zero_enabled)  # the executor's update / collective streams (ZeRO)
+    if lane and replicas_of(pol) > 1:
+        # ZeRO within the replica group on d GPUs: each of the P replicas steps the optimizer on
+        # 1/P of the stage (the measured 1-GPU Broadcast stepped all of it); the transposed
+        # weight refresh (4 of the Broadcast's ~38 bytes per parameter, ~10%) stays whole
+        P_ = replicas_of(pol)
+        for s_ in range(depth):
+            if (P.Kind.Broadcast, s_) in costs:
+                costs[(P.Kind.Broadcast, s_)] *= 0.9 / P_ + 0.1
     if stage_numel is not None and replicas_of(pol) > 1:
         rep0 = static_order_replay(pol, depth, costs, gap_ns, devices=devices, update_lane=lane,
                                    segments=segments if lane else None)

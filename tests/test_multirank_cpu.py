@@ -34,9 +34,17 @@ def _check(plans, depth=8):
                 if fold[P.map_stage_to_device(p, i, depth)] == r}
         assert hosted == want
         for s in pl["stages"]:
-            assert s["owner"] == (fold[s["stage"]] == r)  # ZeRO owner: the rank of device i
+            assert s["owner_rank"] == fold[s["stage"]]  # the reference's owner: the rank of device i
             grp = sorted({fold[P.map_stage_to_device(p, s["stage"], depth)] for p in range(depth // 2)})
             assert s["group"] == grp
+            # ZeRO within a multi-rank replica group: every member keeps the optimizer state of
+            # its shard (1/|group| of every segment); a single-rank group's rank keeps all of it
+            if len(grp) > 1:
+                assert s["owner"] == s["hosted"]
+                if s["hosted"]:
+                    assert s["shard"] and abs(s["opt_numel"] * len(grp) / s["numel"] - 1) < 0.01
+            else:
+                assert s["owner"] == (fold[s["stage"]] == r) and s["shard"] == []
     # p2p pairing (message ids agree), collectives issued by exactly the replica group
     ops = [[tuple(o) for o in pl["comm_ops"]] for pl in plans]
     for r in range(world):

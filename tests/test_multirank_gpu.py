@@ -59,12 +59,17 @@ def _run_case(case, world, rank, allgather):
                       world_size=world, rank=rank,
                       optimizer=E.OptimizerConfig(kind=3, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.0))
     eng = E.Engine(model, run, allgather=allgather)
-    init = {s["stage"]: eng.stage_params(s["stage"]) for s in eng.plan()["stages"] if s["owner"]}
+    init = {s["stage"]: eng.stage_params(s["stage"]) for s in eng.plan()["stages"] if s["hosted"]}
     inputs, labels = E.synthetic_tokens(model, run.data_seed, 0, run.num_minibatches)
     l1 = eng.run(inputs, labels).copy()
     l2 = eng.run(inputs, labels).copy()  # continue training: second epoch of every flag
     plan = eng.plan()
-    owned = {s["stage"]: eng.stage_params(s["stage"]) for s in plan["stages"] if s["owner"]}
+    # fp32 masters this rank is authoritative for: a whole stage (single-rank group) or its
+    # ZeRO shard (ranges) of a stage shared by several ranks
+    owned = {}
+    for s in plan["stages"]:
+        if s["owner"]:
+            owned[s["stage"]] = (eng.stage_params(s["stage"]), s["shard"])
     rows = eng.version_trace().strip().split("\n")[1:]
     st = eng.stats()
     last = any(s["hosted"] and s["stage"] == depth - 1 for s in plan["stages"])
@@ -133,9 +138,20 @@ def _merge(results):
     # a minibatch's loss is reported by the rank that ran its last-stage forward (0 elsewhere)
     have = [r["losses"] for r in results if r["losses"] is not None]
     losses = tuple(np.sum([h[k] for h in have], axis=0) for k in (0, 1))
-    owned = {}
+    owned, covered = {}, {}
     for r in results:
-        owned.update(r["owned"])
+        for st, (vals, shard) in r["owned"].items():
+            if not shard:
+                owned[st] = vals
+                covered[st] = np.ones(vals.size, bool)
+                continue
+            dst = owned.setdefault(st, np.zeros_like(vals))
+            cov = covered.setdefault(st, np.zeros(vals.size, bool))
+            for lo, hi in shard:
+                dst[lo:hi] = vals[lo:hi]
+                cov[lo:hi] = True
+    for st, cov in covered.items():  # the shards tile the parameters (alignment padding aside)
+        assert cov.mean() > 0.99, (st, cov.mean())
     rows = sorted(row for r in results for row in r["rows"])
     return losses, owned, rows
 
@@ -168,7 +184,7 @@ def test_ranks_on_one_gpu_match_single_rank(case, world, exact, single_rank, tmp
             # different association of the fp32 window-gradient sum only (observed ~1e-6)
             assert np.max(np.abs(a - b) / np.abs(b)) < 1e-4
     for i in range(depth):
-        a, b = owned[i].astype(np.float64), ref["owned"][i].astype(np.float64)
+        a, b = owned[i].astype(np.float64), ref["owned"][i][0].astype(np.float64)
         if exact:
             assert np.array_equal(a, b), (i, np.max(np.abs(a - b)))
         else:
