@@ -132,6 +132,10 @@ typedef struct amdp_kernel_class_stats {
   double bytes; /* algorithmic HBM bytes (memory-bound classes) */
 } amdp_kernel_class_stats;
 int amdp_engine_set_kernel_timing(amdp_engine* e, int enable);
+/* CUDA graphs of whole runs (default on; one GPU only): a configuration's second run is
+ * captured and later runs replay it.  Host buffers must be pinned (amdp_host_alloc) or the
+ * run resident; otherwise, and with kernel timing on, runs are issued eagerly. */
+int amdp_engine_set_graphs(amdp_engine* e, int enable);
 int amdp_engine_kernel_stats(const amdp_engine* e, amdp_kernel_class_stats* out, int cap);
 
 /* Stats of the last run: device-timed milliseconds from the first task to the last,
@@ -144,6 +148,7 @@ typedef struct amdp_run_stats {
   int64_t p2p_bytes_sent, collective_bytes;
   double busy_ms; /* sum of measured task durations on this GPU (record_events) */
   double host_issue_ms; /* host wall time spent issuing the run (launches, events, NCCL) */
+  int64_t graph_replayed; /* 1: the run was one CUDA-graph launch (captured run, replayed) */
 } amdp_run_stats;
 int amdp_engine_stats(const amdp_engine* e, amdp_run_stats* out);
 

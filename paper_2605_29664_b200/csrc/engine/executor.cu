@@ -40,6 +40,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "amdp_engine.h"
@@ -241,6 +242,39 @@ class Engine {
   std::vector<cudaEvent_t> ev_pool_;  // cross-stream hand-offs (recycled round robin)
   size_t ev_next_ = 0;
   cudaEvent_t handoff(cudaStream_t from);  // event recorded on `from` now
+  // Timing records: under CUDA-graph capture they become event-record nodes (external), so a
+  // replay timestamps them like an eager run.
+  bool capturing_ = false;
+  void rec(cudaEvent_t e, cudaStream_t s) {
+    CUDA_OK(capturing_ ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s));
+  }
+  // CUDA graphs of whole runs (one GPU): a run is a fixed sequence of launches, so after one
+  // eager run (lazy initialisation) each new configuration is captured once (streams, events,
+  // PDL edges, copies) and replayed: one launch instead of ~17k host API calls per window.
+  struct GraphKey {
+    int max_window;
+    bool resident;
+    const void *in, *lab, *loss;
+    uint64_t scale_hash;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(max_window, resident, in, lab, loss, scale_hash) <
+             std::tie(o.max_window, o.resident, o.in, o.lab, o.loss, o.scale_hash);
+    }
+  };
+  struct GraphRun {
+    cudaGraphExec_t exec = nullptr;
+    amdp_run_stats stats{};
+    std::vector<char> lane_rec;
+  };
+  int eager_runs_ = 0;
+  std::string graph_error_;  // why capture was abandoned (plan_json "graph_error")
+  std::map<GraphKey, GraphRun> graphs_;
+
+ public:
+  bool graphs_enabled_ = true;
+
+ private:
+  void issue(int max_window, bool resident, const int32_t* h_in, const int32_t* h_lab, float* losses_out);
   uint16_t* bounds_arena_ = nullptr;
   std::vector<std::pair<int, int>> planned_sends_;  // (message id, boundary buffer)
   uint8_t* ws_ = nullptr;
@@ -499,6 +533,8 @@ Engine::~Engine() {
   for (cudaStream_t st : {cs_, rs_, ss_, ks_, us_, side_.side})
     if (st) cudaStreamSynchronize(st);
   comm_.reset();  // unmaps peers' memory before our own buffers go away
+  for (auto& [k, g] : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto& s : stages) {
     cudaFree(s->master);
     cudaFree(s->m);
@@ -868,7 +904,7 @@ void Engine::zero_broadcast(int i, int window) {
   // the update stream's interval of this Broadcast (a lane event: it overlaps other stages'
   // compute on this GPU; projection.py models the update lane separately)
   if (rc_.record_events) {
-    CUDA_OK(cudaEventRecord(ev_lstart_[static_cast<size_t>(cur_pos_)], us_));
+    rec(ev_lstart_[static_cast<size_t>(cur_pos_)], us_);
     lane_rec_[static_cast<size_t>(cur_pos_)] = 1;
   }
   const auto& segs = segs_[static_cast<size_t>(i)];
@@ -936,7 +972,7 @@ void Engine::zero_broadcast(int i, int window) {
   if (nt < 0) throw std::runtime_error("weight transpose failed");
   stats.kernels_launched += nt;
   CUDA_OK(cudaEventRecord(wready_[static_cast<size_t>(i)], us_));
-  if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_lend_[static_cast<size_t>(cur_pos_)], us_));
+  if (rc_.record_events) rec(ev_lend_[static_cast<size_t>(cur_pos_)], us_);
   wpending_[static_cast<size_t>(i)] = 1;
   fpending_[static_cast<size_t>(i)] = 1;
 }
@@ -986,7 +1022,7 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       CUDA_OK(cudaStreamWaitEvent(cs_, wready_[static_cast<size_t>(i)], 0));
       wpending_[static_cast<size_t>(i)] = fpending_[static_cast<size_t>(i)] = 0;
     }
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
     record_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, d_trace_, t);
     use_replica_weights(i, task.pipeline);
     stats.kernels_launched += 1;
@@ -1006,7 +1042,7 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     }
     stats.kernels_launched += launched;
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
     stats.tasks_executed += 1;
     if (comm_) {  // last compute use of the buffers this task touched (a later recv waits for it)
       for (int b : {tp.in_buf, tp.gin_buf, tp.out_buf, tp.gout_buf})
@@ -1038,20 +1074,20 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     // the reduction runs on the collective stream (its measured interval); the update stream's
     // Broadcast waits for it
     const bool lane = !comm_at_[static_cast<size_t>(pos)].empty();
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
     if (rc_.record_events && lane) {
       CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));
-      CUDA_OK(cudaEventRecord(ev_lstart_[static_cast<size_t>(pos)], ks_));
+      rec(ev_lstart_[static_cast<size_t>(pos)], ks_);
       lane_rec_[static_cast<size_t>(pos)] = 1;
     }
     exec_comm(pos);
-    if (rc_.record_events && lane) CUDA_OK(cudaEventRecord(ev_lend_[static_cast<size_t>(pos)], ks_));
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events && lane) rec(ev_lend_[static_cast<size_t>(pos)], ks_);
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
     stats.tasks_executed += 1;
     return;
   }
   if (task.kind == ppsim::Kind::Update) {  // replicated update (every schedule but ZeRO AMDP)
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
     if (tp.first_update) {
       if (group_ranks_[static_cast<size_t>(i)].size() > 1) {  // sum the replicas' window gradients
         int coll = -1;
@@ -1070,17 +1106,17 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, 1);
       stats.kernels_launched += 1;
     }
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
     stats.tasks_executed += 1;
     return;
   }
   if (task.kind == ppsim::Kind::Broadcast) {
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_start_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
     zero_broadcast(i, task.minibatch);  // Broadcast's minibatch field: the window
     // every replica of stage i reads the next version from its next task on (in order)
     bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_, P_);
     stats.kernels_launched += 1;
-    if (rc_.record_events) CUDA_OK(cudaEventRecord(ev_end_[static_cast<size_t>(pos)], cs_));
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
     stats.tasks_executed += 1;
     return;
   }
@@ -1091,6 +1127,40 @@ void Engine::stage_tokens(const int32_t* h_in, const int32_t* h_lab) {
   const size_t n = static_cast<size_t>(M_) * static_cast<size_t>(dm.T) * sizeof(int32_t);
   CUDA_OK(cudaMemcpy(d_inputs_, h_in, n, cudaMemcpyHostToDevice));
   CUDA_OK(cudaMemcpy(d_labels_, h_lab, n, cudaMemcpyHostToDevice));
+}
+
+// Everything a run puts on the GPU, in the global dispatch order (eager, or under capture).
+void Engine::issue(int max_window, bool resident, const int32_t* h_in, const int32_t* h_lab, float* losses_out) {
+  const int N = static_cast<int>(sched.order.size());
+  const auto& g = sched.g;
+  CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_ * P_) * sizeof(int), cs_));
+  CUDA_OK(cudaMemsetAsync(d_loss_, 0, static_cast<size_t>(M_) * sizeof(float), cs_));
+  CUDA_OK(cudaMemsetAsync(d_trace_, 0xff, g.tasks.size() * sizeof(int), cs_));
+  std::vector<int> loaded(static_cast<size_t>(W_), resident ? 1 : 0), last_left(static_cast<size_t>(W_), 0);
+  for (int k = 0; k < N; ++k) {
+    const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
+    if (t.kind == ppsim::Kind::Forward && t.stage == depth_ - 1 && plan_[static_cast<size_t>(k)].local)
+      ++last_left[static_cast<size_t>(t.window)];
+  }
+  for (auto& b : bufs_) b.comm_pending = b.use_recorded = false;  // the previous run fully drained
+  lane_rec_.assign(static_cast<size_t>(N), 0);
+  std::fill(wpending_.begin(), wpending_.end(), 0);
+  std::fill(fpending_.begin(), fpending_.end(), 0);
+  rec(run_begin_, cs_);
+  for (int k = 0; k < N; ++k)
+    if (g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])].window < max_window)
+      exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
+  for (int i = 0; i < depth_; ++i)  // the last window's gathers have completed everywhere
+    if (pending_ag_[static_cast<size_t>(i)] >= 0) {
+      cudaStream_t st = comm_ && comm_->single_stream() ? ks_ : us_;
+      for (size_t k = 0; k < segs_[static_cast<size_t>(i)].size(); ++k)
+        comm_->allgather_wait(pending_ag_[static_cast<size_t>(i)] + static_cast<int>(k), group_ranks_[static_cast<size_t>(i)],
+                              st);
+      pending_ag_[static_cast<size_t>(i)] = -1;
+    }
+  for (cudaStream_t st : {rs_, ss_, ks_, us_})  // join every stream: the run ends when all are idle
+    if (st) CUDA_OK(cudaStreamWaitEvent(cs_, handoff(st), 0));
+  rec(run_end_, cs_);
 }
 
 void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, int max_window, bool resident) {
@@ -1124,42 +1194,84 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
       }
     }
   }
-  CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_ * P_) * sizeof(int), cs_));
-  CUDA_OK(cudaMemsetAsync(d_loss_, 0, static_cast<size_t>(M_) * sizeof(float), cs_));
-  CUDA_OK(cudaMemsetAsync(d_trace_, 0xff, g.tasks.size() * sizeof(int), cs_));
-  std::vector<int> loaded(static_cast<size_t>(W_), resident ? 1 : 0), last_left(static_cast<size_t>(W_), 0);
-  for (int k = 0; k < N; ++k) {
-    const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
-    if (t.kind == ppsim::Kind::Forward && t.stage == depth_ - 1 && plan_[static_cast<size_t>(k)].local)
-      ++last_left[static_cast<size_t>(t.window)];
-  }
   if (comm_) {
     if (!comm_->connected())
       throw std::runtime_error("engine: world_size > 1 needs the communication descriptors exchanged "
                                "(amdp_engine_comm_export / amdp_engine_comm_connect) before run");
     comm_->begin_run();
   }
-  for (auto& b : bufs_) b.comm_pending = b.use_recorded = false;  // the previous run fully drained
-  lane_rec_.assign(static_cast<size_t>(N), 0);
-  std::fill(wpending_.begin(), wpending_.end(), 0);
-  CUDA_OK(cudaEventRecord(run_begin_, cs_));
+  // CUDA graph of the whole run: one GPU (peer flags carry a per-run epoch), no kernel timing,
+  // no replica weight versions (their buffer rotation is host state), pinned host buffers
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool can_graph = graphs_enabled_ && !comm_ && !ktimer_.enabled && !versioned_ &&
+                         (resident || (pinned(h_in) && pinned(h_lab))) && (!losses_out || pinned(losses_out));
+  uint64_t sh = 1469598103934665603ull;
+  for (float f : loss_scale_) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    sh = (sh ^ u) * 1099511628211ull;
+  }
+  const GraphKey key{max_window, resident, h_in, h_lab, losses_out, sh};
   const auto t_issue0 = std::chrono::steady_clock::now();
-  for (int k = 0; k < N; ++k)
-    if (g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])].window < max_window)
-      exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
+  auto it = can_graph ? graphs_.find(key) : graphs_.end();
+  if (it != graphs_.end()) {  // replay
+    CUDA_OK(cudaGraphLaunch(it->second.exec, cs_));
+    stats = it->second.stats;
+    lane_rec_ = it->second.lane_rec;
+    stats.graph_replayed = 1;
+  } else if (can_graph && eager_runs_ >= 1) {  // a new configuration after an eager run (which did
+                                                 // every lazy initialisation): capture
+    capturing_ = true;
+    cudaGraph_t graph = nullptr;
+    try {
+      CUDA_OK(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
+      const cudaEvent_t e0 = handoff(cs_);  // pull the other streams into the capture
+      for (cudaStream_t st : {us_, side_.side})
+        if (st) CUDA_OK(cudaStreamWaitEvent(st, e0, 0));
+      // the stage bodies wait on side-stream events recorded by the previous task; a wait on
+      // a record from outside the capture would invalidate it, so re-record them inside
+      if (side_.side)
+        for (cudaEvent_t e : side_.ev) CUDA_OK(cudaEventRecord(e, side_.side));
+      issue(max_window, resident, h_in, h_lab, losses_out);
+      CUDA_OK(cudaStreamEndCapture(cs_, &graph));
+      capturing_ = false;
+      GraphRun gr;
+      CUDA_OK(cudaGraphInstantiate(&gr.exec, graph, 0));
+      cudaGraphDestroy(graph);
+      gr.stats = stats;
+      gr.lane_rec = lane_rec_;
+      CUDA_OK(cudaGraphLaunch(gr.exec, cs_));
+      graphs_[key] = gr;
+      stats.graph_replayed = 1;
+    } catch (const std::exception& ex) {  // not capturable here: abandon graphs, run eagerly
+      graph_error_ = ex.what();
+      if (getenv("AMDP_GRAPH_DEBUG")) fprintf(stderr, "amdp: CUDA graph capture failed: %s\n", ex.what());
+      cudaStreamCaptureStatus cs;
+      if (cudaStreamIsCapturing(cs_, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t g2 = nullptr;
+        cudaStreamEndCapture(cs_, &g2);
+        if (g2) cudaGraphDestroy(g2);
+      }
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      capturing_ = false;
+      graphs_enabled_ = false;
+      stats = amdp_run_stats{};
+      issue(max_window, resident, h_in, h_lab, losses_out);
+    }
+  } else {
+    issue(max_window, resident, h_in, h_lab, losses_out);
+    ++eager_runs_;
+  }
   stats.host_issue_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_issue0).count();
-  for (int i = 0; i < depth_; ++i)  // the last window's gathers have completed everywhere
-    if (pending_ag_[static_cast<size_t>(i)] >= 0) {
-      cudaStream_t st = comm_->single_stream() ? ks_ : us_;
-      for (size_t k = 0; k < segs_[static_cast<size_t>(i)].size(); ++k)
-        comm_->allgather_wait(pending_ag_[static_cast<size_t>(i)] + static_cast<int>(k), group_ranks_[static_cast<size_t>(i)],
-                              st);
-      pending_ag_[static_cast<size_t>(i)] = -1;
-    }
-  for (cudaStream_t st : {rs_, ss_, ks_, us_})  // join every stream: the run ends when all are idle
-    if (st) CUDA_OK(cudaStreamWaitEvent(cs_, handoff(st), 0));
-  CUDA_OK(cudaEventRecord(run_end_, cs_));
   CUDA_OK(cudaStreamSynchronize(cs_));
   if (comm_) {
     stats.kernels_launched += comm_->kernel_launches() - comm_launches_seen_;
@@ -1218,11 +1330,30 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
   stats.busy_ms = busy;
 }
 
+namespace {
+std::string json_escape(const std::string& in) {
+  std::string o;
+  for (char c : in) {
+    if (c == '"' || c == '\\') o += '\\';
+    if (static_cast<unsigned char>(c) >= 0x20) o += c;
+  }
+  return o;
+}
+std::string fmt_units(double u) {  // shards of 64-aligned segments: round to 1e-3 of a stage
+  char b[32];
+  std::snprintf(b, sizeof(b), "%.3f", u);
+  std::string s(b);
+  while (!s.empty() && s.back() == '0') s.pop_back();
+  if (!s.empty() && s.back() == '.') s.pop_back();
+  return s;
+}
+}  // namespace
+
 std::string Engine::plan_json() const {
   std::string s = "{\"depth\":" + std::to_string(depth_) + ",\"world_size\":" + std::to_string(world_) +
                   ",\"rank\":" + std::to_string(rank_) + ",\"tokens_per_minibatch\":" + std::to_string(dm.T) +
                   ",\"comm_backend\":\"" + (world_ == 1 ? "none" : rc_.comm_backend == AMDP_COMM_NCCL ? "nccl" : "ipc") +
-                  "\",\"messages\":" + std::to_string(nmsg_) + ",\"collectives\":" + std::to_string(ncoll_) +
+                  "\",\"graph_error\":\"" + json_escape(graph_error_) + "\",\"messages\":" + std::to_string(nmsg_) + ",\"collectives\":" + std::to_string(ncoll_) +
                   ",\"device_rank\":[";
   for (size_t d = 0; d < dev_rank_.size(); ++d) s += (d ? "," : "") + std::to_string(dev_rank_[d]);
   s += "],\"partition\":[";
@@ -1266,16 +1397,6 @@ std::string Engine::plan_json() const {
 // the reference's memory model (H/analysis.hpp:226-330: stage replicas, gradient buffers,
 // optimizer-state multiples, live per-stage activations), plus the measured cudaMemGetInfo
 // delta across allocate().  Co-resident replicas of one stage share one set of buffers.
-namespace {
-std::string fmt_units(double u) {  // shards of 64-aligned segments: round to 1e-3 of a stage
-  char b[32];
-  std::snprintf(b, sizeof(b), "%.3f", u);
-  std::string s(b);
-  while (!s.empty() && s.back() == '0') s.pop_back();
-  if (!s.empty() && s.back() == '.') s.pop_back();
-  return s;
-}
-}  // namespace
 
 std::string Engine::memory_json() const {
   const int64_t T = dm.T, h = dm.h;
@@ -1535,6 +1656,11 @@ int amdp_engine_stage_tokens(amdp_engine* e, const int32_t* inputs, const int32_
 
 int amdp_engine_set_kernel_timing(amdp_engine* e, int enable) {
   reinterpret_cast<Engine*>(e)->set_kernel_timing(enable != 0);
+  return 0;
+}
+
+int amdp_engine_set_graphs(amdp_engine* e, int enable) {
+  reinterpret_cast<Engine*>(e)->graphs_enabled_ = enable != 0;
   return 0;
 }
 

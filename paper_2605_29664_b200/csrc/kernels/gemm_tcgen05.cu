@@ -612,6 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
       if (khalf == 1) {  // the first half's reduce-add into these rows has completed
         if (lane == 0) {
           while (ptx::ld_acquire_gpu(flag) != sc.epoch) __nanosleep(64);
+          *flag = 0;  // consumed: the next launch (or a CUDA-graph replay of this one) starts clean
           ptx::fence_proxy_async_global();
         }
         __syncwarp();

@@ -46,7 +46,7 @@ class _Stats(Structure):
     _fields_ = [("device_ms", c_double), ("tasks_executed", c_int64), ("kernels_launched", c_int64),
                 ("h2d_bytes", c_int64), ("d2h_bytes", c_int64), ("p2p_bytes_sent", c_int64),
                 ("collective_bytes", c_int64), ("busy_ms", c_double),
-                ("host_issue_ms", c_double)]
+                ("host_issue_ms", c_double), ("graph_replayed", c_int64)]
 
 
 def _sig(name, res, args):
@@ -65,6 +65,7 @@ _sig("amdp_engine_stats", c_int, [c_void_p, POINTER(_Stats)])
 _sig("amdp_engine_run_windows", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_char_p, c_size_t])
 _sig("amdp_engine_stage_tokens", c_int, [c_void_p, c_void_p, c_void_p])
 _sig("amdp_engine_set_kernel_timing", c_int, [c_void_p, c_int])
+_sig("amdp_engine_set_graphs", c_int, [c_void_p, c_int])
 
 
 class _KStat(Structure):
@@ -234,7 +235,8 @@ def nccl_unique_id() -> bytes:
 
 
 class PinnedTokens:
-    """Pinned host arrays inputs/labels [M][T] int32 (cudaHostAlloc through the C-ABI)."""
+    """Pinned host arrays inputs/labels [M][T] int32 and losses [M] float32 (cudaHostAlloc
+    through the C-ABI): copies overlap compute, and runs over them can be CUDA graphs."""
 
     def __init__(self, num_minibatches: int, tokens: int):
         n = num_minibatches * tokens * 4
@@ -244,11 +246,15 @@ class PinnedTokens:
             raise MemoryError("cudaHostAlloc failed")
         self.inputs = np.ctypeslib.as_array((ctypes.c_int32 * (num_minibatches * tokens)).from_address(self._pi)).reshape(num_minibatches, tokens)
         self.labels = np.ctypeslib.as_array((ctypes.c_int32 * (num_minibatches * tokens)).from_address(self._pl)).reshape(num_minibatches, tokens)
+        self._ps = lib.amdp_host_alloc(num_minibatches * 4)
+        if not self._ps:
+            raise MemoryError("cudaHostAlloc failed")
+        self.losses = np.ctypeslib.as_array((ctypes.c_float * num_minibatches).from_address(self._ps))
 
     def __del__(self):
         if lib is None:  # interpreter teardown: the process exit releases the pinned pages
             return
-        for p in (getattr(self, "_pi", None), getattr(self, "_pl", None)):
+        for p in (getattr(self, "_pi", None), getattr(self, "_pl", None), getattr(self, "_ps", None)):
             if p:
                 lib.amdp_host_free(p)
 
@@ -336,6 +342,10 @@ class Engine:
 
     def set_kernel_timing(self, on: bool) -> None:
         lib.amdp_engine_set_kernel_timing(self._h, int(on))
+
+    def set_graphs(self, on: bool) -> None:
+        """CUDA graphs of whole runs (default on, one GPU; needs pinned host buffers)."""
+        lib.amdp_engine_set_graphs(self._h, int(on))
 
     def kernel_stats(self) -> dict:
         arr = (_KStat * 16)()
