@@ -36,6 +36,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -234,8 +235,8 @@ class Engine {
   // compute, receive, send, collective, window-update streams (NCCL: one stream for all comm)
   cudaStream_t cs_ = nullptr, rs_ = nullptr, ss_ = nullptr, ks_ = nullptr, us_ = nullptr;
   std::vector<cudaEvent_t> wready_;   // per stage: new weights in place (update stream)
-  std::vector<char> wpending_;        // per stage: next B must wait wready_
-  std::vector<char> fpending_;        // per stage: next F waits the per-segment events
+  std::vector<char> wpending_;        // per (stage, compute stream): next B must wait wready_
+  std::vector<char> fpending_;        // per (stage, compute stream): next F waits the segment events
   std::vector<std::vector<std::pair<int64_t, int64_t>>> segs_;  // per stage: GptStage::segments()
   std::vector<std::vector<cudaEvent_t>> seg_ev_;               // per stage, segment: weights in place
   std::vector<cudaEvent_t> reduced_;  // per stage: window gradient reduced (collective stream)
@@ -278,6 +279,31 @@ class Engine {
   uint16_t* bounds_arena_ = nullptr;
   std::vector<std::pair<int, int>> planned_sends_;  // (message id, boundary buffer)
   uint8_t* ws_ = nullptr;
+  // Concurrent compute streams (one GPU, ZeRO AMDP): logical device d's Forward / Backward
+  // tasks run in dispatch order on compute stream dev_stream_[d] (cstreams_[0] = cs_), each
+  // with its own weight-gradient side stream and workspace, so tasks of different logical
+  // devices overlap on the SMs as they would on separate GPUs.  Every cross-stream hazard is
+  // an event wait computed at plan time from the resources the tasks touch (activation slots,
+  // boundary buffers, a stage's window gradient: B tasks of a stage keep their global order,
+  // so the fp32 sums - and the bits - are those of the serial run).
+  int nstreams_ = 1;
+  std::vector<cudaStream_t> cstreams_;
+  std::vector<SideStream> sides_;
+  std::vector<uint8_t*> wss_;
+  std::vector<int> dev_stream_;             // per logical device
+  std::vector<std::vector<int>> waits_;     // per position: earlier positions (other streams)
+  std::vector<std::vector<int>> stage_last_;  // per R / BC position: last local F/B of the stage per stream
+  std::vector<std::vector<int>> loss_tasks_;  // per window: local last-stage Forward positions
+  std::vector<cudaEvent_t> done_;           // per position: the F/B task complete on its stream
+  std::vector<int> tok_loader_;             // per window: position whose stream copied the tokens (run)
+  std::vector<char> issued_;                // per position: issued in the current run
+  int sidx(int pos) const {                 // compute-stream index of a local F/B position
+    if (ktimer_.enabled) return 0;          // kernel timing: everything serial on cs_
+    const auto& t = sched.g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(pos)])];
+    return dev_stream_[static_cast<size_t>(t.device)];
+  }
+  void plan_streams();
+  void wait_stage_tasks(int pos, cudaStream_t st);  // st waits for stage's earlier tasks
   int32_t *d_inputs_ = nullptr, *d_labels_ = nullptr;
   float* d_loss_ = nullptr;
   int *d_ver_ = nullptr, *d_trace_ = nullptr;
@@ -574,10 +600,23 @@ Engine::~Engine() {
   for (auto e : ev_pool_) cudaEventDestroy(e);
   if (run_begin_) cudaEventDestroy(run_begin_);
   if (run_end_) cudaEventDestroy(run_end_);
-  if (side_.side) {
+  for (size_t k = 0; k < sides_.size(); ++k) {  // sides_[0] is side_
+    if (sides_[k].side) {
+      cudaStreamSynchronize(sides_[k].side);
+      for (auto e : sides_[k].ev) cudaEventDestroy(e);
+      cudaStreamDestroy(sides_[k].side);
+    }
+  }
+  if (sides_.empty() && side_.side) {
     for (auto e : side_.ev) cudaEventDestroy(e);
     cudaStreamDestroy(side_.side);
   }
+  for (size_t k = 1; k < cstreams_.size(); ++k) {
+    cudaStreamSynchronize(cstreams_[k]);
+    cudaStreamDestroy(cstreams_[k]);
+  }
+  for (size_t k = 1; k < wss_.size(); ++k) cudaFree(wss_[k]);
+  for (auto e : done_) cudaEventDestroy(e);
   if (ss_ && ss_ != rs_) cudaStreamDestroy(ss_);
   if (ks_ && ks_ != rs_) cudaStreamDestroy(ks_);
   if (rs_) cudaStreamDestroy(rs_);
@@ -611,12 +650,26 @@ void Engine::make_plan() {
   // boundary buffers: interval allocation over positions on this rank
   std::vector<int> free_bufs;
   std::vector<std::vector<int>> release_at(static_cast<size_t>(N));  // buffers freed after position
+  // Reuse prefers a free buffer / slot whose last user ran on the same logical device: with
+  // concurrent compute streams (one per logical device) the reuse then needs no cross-stream
+  // wait; the counts are those of plain LIFO reuse (a free entry is always taken).
+  std::map<int, int> buf_dev;                      // buffer -> device of its last use
+  std::map<std::pair<int, int>, int> slot_dev;     // (stage, slot) -> device of its last use
+  auto take_pref = [](std::vector<int>& fl, const std::function<bool(int)>& same) {
+    for (size_t q = fl.size(); q-- > 0;)
+      if (same(fl[q])) {
+        const int v = fl[q];
+        fl.erase(fl.begin() + static_cast<std::ptrdiff_t>(q));
+        return v;
+      }
+    const int v = fl.back();
+    fl.pop_back();
+    return v;
+  };
+  int cur_dev = -1;  // device of the task being planned
   auto alloc_buf = [&]() {
-    if (!free_bufs.empty()) {
-      const int b = free_bufs.back();
-      free_bufs.pop_back();
-      return b;
-    }
+    if (!free_bufs.empty())
+      return take_pref(free_bufs, [&](int b) { auto it = buf_dev.find(b); return it != buf_dev.end() && it->second == cur_dev; });
     return nbuf++;
   };
   // F boundary (i -> i+1, j): receiver buffer lives [pos F(i,j), pos B(i+1,j)];
@@ -630,6 +683,7 @@ void Engine::make_plan() {
     TaskPlan& tp = plan_[static_cast<size_t>(k)];
     const int me = rank_of_task(t);
     tp.local = me == rank_;
+    cur_dev = task.device;
     // release buffers whose last use was an earlier position
     if (task.kind == ppsim::Kind::Forward) {
       const int i = task.stage, j = task.minibatch;
@@ -637,8 +691,7 @@ void Engine::make_plan() {
         auto& fl = free_slots[static_cast<size_t>(i)];
         int s;
         if (!fl.empty()) {
-          s = fl.back();
-          fl.pop_back();
+          s = take_pref(fl, [&](int x) { auto it = slot_dev.find({i, x}); return it != slot_dev.end() && it->second == cur_dev; });
         } else {
           s = slots_per_stage[static_cast<size_t>(i)]++;
         }
@@ -675,6 +728,7 @@ void Engine::make_plan() {
       if (tp.local) {
         tp.slot = slot_of.at({i, j});
         free_slots[static_cast<size_t>(i)].push_back(tp.slot);
+        slot_dev[{i, tp.slot}] = task.device;
         if (i > 0) tp.in_buf = fbuf_recv.at({i - 1, j});
         if (i + 1 < depth_) tp.gin_buf = bbuf_recv.at({i, j});
       }
@@ -727,8 +781,70 @@ void Engine::make_plan() {
         if (hosted[static_cast<size_t>(i)]) comm_at_[static_cast<size_t>(k)].push_back({CommOp::Allreduce, -1, -1, i, k, c});
       }
     }
-    for (int b : release_at[static_cast<size_t>(k)]) free_bufs.push_back(b);
+    for (int b : release_at[static_cast<size_t>(k)]) {
+      free_bufs.push_back(b);
+      buf_dev[b] = task.device;  // the buffer's last use: this position's task
+    }
   }
+}
+
+// Cross-stream hazards of the concurrent compute streams, from the resources each local F/B
+// task touches in dispatch order: its activation slot (stage, slot), its boundary buffers
+// (which also carries the producer -> consumer edge: F(i-1,j) -> F(i,j), B(i+1,j) -> B(i,j)),
+// and for a Backward its stage's fp32 window gradient (so the B tasks of a stage accumulate in
+// the global order: the same fp32 sums as one stream).  A task waits for the previous user of
+// each resource when that ran on another stream.  With one stream the lists only feed the
+// window machinery (stage_last_), which then waits for just that stage's last task.
+void Engine::plan_streams() {
+  const auto& g = sched.g;
+  const int N = static_cast<int>(sched.order.size());
+  dev_stream_.assign(static_cast<size_t>(devices_), 0);
+  {
+    int k = 0;
+    for (int d = 0; d < devices_; ++d)
+      if (rank_of_dev(d) == rank_) dev_stream_[static_cast<size_t>(d)] = (k++) % nstreams_;
+  }
+  waits_.assign(static_cast<size_t>(N), {});
+  stage_last_.assign(static_cast<size_t>(N), {});
+  loss_tasks_.assign(static_cast<size_t>(W_), {});
+  std::map<std::pair<int, int>, int> slot_last;  // (stage, slot) -> position
+  std::map<int, int> buf_last, grad_last;
+  std::vector<std::vector<int>> stage_stream_last(static_cast<size_t>(depth_), std::vector<int>(static_cast<size_t>(nstreams_), -1));
+  auto stream_at = [&](int q) {
+    return dev_stream_[static_cast<size_t>(g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(q)])].device)];
+  };
+  for (int k = 0; k < N; ++k) {
+    const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
+    const TaskPlan& tp = plan_[static_cast<size_t>(k)];
+    if (t.kind == ppsim::Kind::Reduce || t.kind == ppsim::Kind::Broadcast || t.kind == ppsim::Kind::Update) {
+      stage_last_[static_cast<size_t>(k)] = stage_stream_last[static_cast<size_t>(t.stage)];
+      continue;
+    }
+    if (!tp.local) continue;
+    const int me = stream_at(k);
+    auto use = [&](int& last) {
+      if (last >= 0 && stream_at(last) != me &&
+          std::find(waits_[static_cast<size_t>(k)].begin(), waits_[static_cast<size_t>(k)].end(), last) ==
+              waits_[static_cast<size_t>(k)].end())
+        waits_[static_cast<size_t>(k)].push_back(last);
+      last = k;
+    };
+    auto it = slot_last.emplace(std::make_pair(t.stage, tp.slot), -1).first;
+    use(it->second);
+    for (int b : {tp.in_buf, tp.out_buf, tp.gin_buf, tp.gout_buf})
+      if (b >= 0) use(buf_last.emplace(b, -1).first->second);
+    if (t.kind == ppsim::Kind::Backward) use(grad_last.emplace(t.stage, -1).first->second);
+    stage_stream_last[static_cast<size_t>(t.stage)][static_cast<size_t>(me)] = k;
+    if (t.kind == ppsim::Kind::Forward && t.stage == depth_ - 1) loss_tasks_[static_cast<size_t>(t.window)].push_back(k);
+  }
+}
+
+// `st` waits for every local Forward / Backward of the stage of the window task at `pos` that
+// precedes it in the dispatch order (the last one per compute stream): after them nothing
+// reads the stage's old weights or adds to its window gradient.
+void Engine::wait_stage_tasks(int pos, cudaStream_t st) {
+  for (int q : stage_last_[static_cast<size_t>(pos)])
+    if (q >= 0 && issued_[static_cast<size_t>(q)]) CUDA_OK(cudaStreamWaitEvent(st, done_[static_cast<size_t>(q)], 0));
 }
 
 void Engine::allocate() {
@@ -821,6 +937,38 @@ void Engine::allocate() {
   }
   CUDA_OK(cudaEventCreate(&run_begin_));
   CUDA_OK(cudaEventCreate(&run_end_));
+  // concurrent compute streams: as many as logical devices (one GPU, ZeRO AMDP), within what
+  // the extra workspaces leave of HBM (a 6 GiB margin); AMDP_STREAMS overrides the count
+  cstreams_.assign(1, cs_);
+  sides_.assign(1, side_);
+  wss_.assign(1, ws_);
+  nstreams_ = 1;
+  if (world_ == 1 && zero_ && devices_ > 1 && !getenv("AMDP_SINGLE_STREAM")) {
+    size_t fr = 0, tot = 0;
+    CUDA_OK(cudaMemGetInfo(&fr, &tot));
+    const size_t wsb = GptStage::workspace_bytes(dm);
+    int want = getenv("AMDP_STREAMS") ? std::max(1, atoi(getenv("AMDP_STREAMS"))) : devices_;
+    want = std::min(want, devices_);
+    while (want > 1 && static_cast<size_t>(want - 1) * wsb + (6ull << 30) > fr) --want;
+    for (int k = 1; k < want; ++k) {
+      cudaStream_t st;
+      CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      cstreams_.push_back(st);
+      SideStream sd;
+      if (side_.side) {
+        CUDA_OK(cudaStreamCreateWithFlags(&sd.side, cudaStreamNonBlocking));
+        for (auto& e : sd.ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      sides_.push_back(sd);
+      uint8_t* w = nullptr;
+      CUDA_OK(cudaMalloc(&w, wsb));
+      wss_.push_back(w);
+    }
+    nstreams_ = want;
+  }
+  wpending_.assign(static_cast<size_t>(depth_ * nstreams_), 0);
+  fpending_.assign(static_cast<size_t>(depth_ * nstreams_), 0);
+  plan_streams();
 }
 
 void Engine::init_weights() {
@@ -874,7 +1022,7 @@ void Engine::exec_comm(int pos) {
       }
       case CommOp::Reduce: {
         GptStage& st = *stages[static_cast<size_t>(op.stage)];
-        CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));  // the window's backwards of this rank
+        wait_stage_tasks(pos, ks_);  // the window's backwards of this stage on this rank
         // ZeRO within the group: member j ends with the group's sum over its shard
         comm_->reduce_scatter_f32(op.id, group_ranks_[static_cast<size_t>(op.stage)], op.stage, st.grad,
                                   shard_[static_cast<size_t>(op.stage)], ks_);
@@ -899,8 +1047,12 @@ void Engine::zero_broadcast(int i, int window) {
   GptStage& S = *stages[static_cast<size_t>(i)];
   const auto& gr = group_ranks_[static_cast<size_t>(i)];
   const bool multi = sharded(i);
-  CUDA_OK(cudaStreamWaitEvent(us_, handoff(cs_), 0));
+  wait_stage_tasks(cur_pos_, us_);  // every earlier reader of the old weights / window gradient
   if (multi) CUDA_OK(cudaStreamWaitEvent(us_, reduced_[static_cast<size_t>(i)], 0));
+  // every replica of stage i reads the next version from its next task on (those wait for
+  // this stream's segment events / wready_, recorded after this bump)
+  bump_version_kernel<<<1, 1, 0, us_>>>(d_ver_, i * P_, P_);
+  stats.kernels_launched += 1;
   // the update stream's interval of this Broadcast (a lane event: it overlaps other stages'
   // compute on this GPU; projection.py models the update lane separately)
   if (rc_.record_events) {
@@ -973,8 +1125,10 @@ void Engine::zero_broadcast(int i, int window) {
   stats.kernels_launched += nt;
   CUDA_OK(cudaEventRecord(wready_[static_cast<size_t>(i)], us_));
   if (rc_.record_events) rec(ev_lend_[static_cast<size_t>(cur_pos_)], us_);
-  wpending_[static_cast<size_t>(i)] = 1;
-  fpending_[static_cast<size_t>(i)] = 1;
+  for (int k = 0; k < nstreams_; ++k) {  // the first F / B of the stage on each compute stream waits
+    wpending_[static_cast<size_t>(i * nstreams_ + k)] = 1;
+    fpending_[static_cast<size_t>(i * nstreams_ + k)] = 1;
+  }
 }
 
 void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::vector<int>& loaded,
@@ -996,16 +1150,24 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     GptStage& S = *stages[static_cast<size_t>(i)];
     const SlotActs& A = slot_acts_[static_cast<size_t>(i)][static_cast<size_t>(tp.slot)];
     const int w = j / thr_;
+    const int si = sidx(pos);
+    cudaStream_t cs = cstreams_[static_cast<size_t>(si)];  // this task's compute stream
+    for (int q : waits_[static_cast<size_t>(pos)])      // hazards with other compute streams
+      if (issued_[static_cast<size_t>(q)]) CUDA_OK(cudaStreamWaitEvent(cs, done_[static_cast<size_t>(q)], 0));
     if (task.kind == ppsim::Kind::Forward && !loaded[static_cast<size_t>(w)]) {
       const size_t off = static_cast<size_t>(w) * thr_ * T;
-      CUDA_OK(cudaMemcpyAsync(d_inputs_ + off, h_in + off, thr_ * T * sizeof(int32_t), cudaMemcpyHostToDevice, cs_));
-      CUDA_OK(cudaMemcpyAsync(d_labels_ + off, h_lab + off, thr_ * T * sizeof(int32_t), cudaMemcpyHostToDevice, cs_));
+      CUDA_OK(cudaMemcpyAsync(d_inputs_ + off, h_in + off, thr_ * T * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
+      CUDA_OK(cudaMemcpyAsync(d_labels_ + off, h_lab + off, thr_ * T * sizeof(int32_t), cudaMemcpyHostToDevice, cs));
       stats.h2d_bytes += static_cast<int64_t>(2 * thr_ * T * sizeof(int32_t));
       loaded[static_cast<size_t>(w)] = 1;
+      tok_loader_[static_cast<size_t>(w)] = pos;
+    } else if (task.kind == ppsim::Kind::Forward && (S.first() || S.last()) && tok_loader_[static_cast<size_t>(w)] >= 0 &&
+               sidx(tok_loader_[static_cast<size_t>(w)]) != si) {  // tokens copied on another stream
+      CUDA_OK(cudaStreamWaitEvent(cs, done_[static_cast<size_t>(tok_loader_[static_cast<size_t>(w)])], 0));
     }
     auto wait_buf = [&](int b) {
       if (b >= 0 && bufs_[static_cast<size_t>(b)].comm_pending) {
-        CUDA_OK(cudaStreamWaitEvent(cs_, bufs_[static_cast<size_t>(b)].comm_done, 0));
+        CUDA_OK(cudaStreamWaitEvent(cs, bufs_[static_cast<size_t>(b)].comm_done, 0));
       }
     };
     wait_buf(tp.in_buf);
@@ -1015,15 +1177,19 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     // the stage's new weights (Broadcast on the update stream): a Forward waits segment by
     // segment inside its body, a Backward (transposed copies, cleared gradient) for all of it
     const cudaEvent_t* seg_wait = nullptr;
-    if (task.kind == ppsim::Kind::Forward && fpending_[static_cast<size_t>(i)]) {
+    const size_t pk = static_cast<size_t>(i * nstreams_ + si);  // (stage, compute stream)
+    if (task.kind == ppsim::Kind::Forward && fpending_[pk]) {
       seg_wait = seg_ev_[static_cast<size_t>(i)].data();
-      fpending_[static_cast<size_t>(i)] = 0;
-    } else if (task.kind == ppsim::Kind::Backward && wpending_[static_cast<size_t>(i)]) {
-      CUDA_OK(cudaStreamWaitEvent(cs_, wready_[static_cast<size_t>(i)], 0));
-      wpending_[static_cast<size_t>(i)] = fpending_[static_cast<size_t>(i)] = 0;
+      fpending_[pk] = 0;
+    } else if (task.kind == ppsim::Kind::Backward && wpending_[pk]) {
+      CUDA_OK(cudaStreamWaitEvent(cs, wready_[static_cast<size_t>(i)], 0));
+      wpending_[pk] = fpending_[pk] = 0;
     }
-    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
-    record_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, d_trace_, t);
+    // the version this task reads: after the Broadcast's counter bump, which precedes its first
+    // segment event (the body then waits for the later segments as it reaches them)
+    if (seg_wait) CUDA_OK(cudaStreamWaitEvent(cs, seg_wait[0], 0));
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs);
+    record_version_kernel<<<1, 1, 0, cs>>>(d_ver_, i * P_ + task.pipeline, d_trace_, t);
     use_replica_weights(i, task.pipeline);
     stats.kernels_launched += 1;
     const int32_t* tok = d_inputs_ + static_cast<size_t>(j) * T;
@@ -1032,22 +1198,25 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     int launched;
     if (task.kind == ppsim::Kind::Forward) {
       uint16_t* out = tp.out_buf >= 0 ? bufs_[static_cast<size_t>(tp.out_buf)].ptr : nullptr;
-      launched = S.forward(A, tok, lab, in, out, d_loss_ + j, loss_scale_[static_cast<size_t>(j)], ws_, cs_, &rc,
-                           seg_wait);
+      launched = S.forward(A, tok, lab, in, out, d_loss_ + j, loss_scale_[static_cast<size_t>(j)],
+                           wss_[static_cast<size_t>(si)], cs, &rc, seg_wait);
     } else {
       const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
       uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
       // the kernel-timing run serialises the streams so per-launch event spans are exact
-      launched = S.backward(A, tok, in, gin, gout, ws_, cs_, ktimer_.enabled ? SideStream{} : side_, &rc);
+      launched = S.backward(A, tok, in, gin, gout, wss_[static_cast<size_t>(si)], cs,
+                            ktimer_.enabled ? SideStream{} : sides_[static_cast<size_t>(si)], &rc);
     }
     stats.kernels_launched += launched;
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));
-    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs);
+    CUDA_OK(cudaEventRecord(done_[static_cast<size_t>(pos)], cs));
+    issued_[static_cast<size_t>(pos)] = 1;
     stats.tasks_executed += 1;
     if (comm_) {  // last compute use of the buffers this task touched (a later recv waits for it)
       for (int b : {tp.in_buf, tp.gin_buf, tp.out_buf, tp.gout_buf})
         if (b >= 0) {
-          CUDA_OK(cudaEventRecord(bufs_[static_cast<size_t>(b)].used, cs_));
+          CUDA_OK(cudaEventRecord(bufs_[static_cast<size_t>(b)].used, cs));
           bufs_[static_cast<size_t>(b)].use_recorded = true;
         }
     }
@@ -1055,8 +1224,11 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     // D2H of a window's losses once its last-stage forwards are all issued
     if (task.kind == ppsim::Kind::Forward && S.last() && losses_out) {
       if (--last_left[static_cast<size_t>(w)] == 0) {
+        for (int q : loss_tasks_[static_cast<size_t>(w)])  // the window's other last-stage forwards
+          if (q != pos && issued_[static_cast<size_t>(q)] && sidx(q) != si)
+            CUDA_OK(cudaStreamWaitEvent(cs, done_[static_cast<size_t>(q)], 0));
         CUDA_OK(cudaMemcpyAsync(losses_out + static_cast<size_t>(w) * thr_, d_loss_ + static_cast<size_t>(w) * thr_,
-                                thr_ * sizeof(float), cudaMemcpyDeviceToHost, cs_));
+                                thr_ * sizeof(float), cudaMemcpyDeviceToHost, cs));
         stats.d2h_bytes += thr_ * static_cast<int64_t>(sizeof(float));
       }
     }
@@ -1070,24 +1242,26 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     return;
   }
   GptStage& S = *stages[static_cast<size_t>(i)];
+  // the marker events of a window task: where its logical device's compute stream passed it
+  cudaStream_t ms = cstreams_[ktimer_.enabled ? 0 : static_cast<size_t>(dev_stream_[static_cast<size_t>(task.device)])];
   if (task.kind == ppsim::Kind::Reduce) {
     // the reduction runs on the collective stream (its measured interval); the update stream's
     // Broadcast waits for it
     const bool lane = !comm_at_[static_cast<size_t>(pos)].empty();
-    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], ms);
     if (rc_.record_events && lane) {
-      CUDA_OK(cudaStreamWaitEvent(ks_, handoff(cs_), 0));
+      wait_stage_tasks(pos, ks_);
       rec(ev_lstart_[static_cast<size_t>(pos)], ks_);
       lane_rec_[static_cast<size_t>(pos)] = 1;
     }
     exec_comm(pos);
     if (rc_.record_events && lane) rec(ev_lend_[static_cast<size_t>(pos)], ks_);
-    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], ms);
     stats.tasks_executed += 1;
     return;
   }
   if (task.kind == ppsim::Kind::Update) {  // replicated update (every schedule but ZeRO AMDP)
-    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], ms);
     if (tp.first_update) {
       if (group_ranks_[static_cast<size_t>(i)].size() > 1) {  // sum the replicas' window gradients
         int coll = -1;
@@ -1106,17 +1280,14 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_ + task.pipeline, 1);
       stats.kernels_launched += 1;
     }
-    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], ms);
     stats.tasks_executed += 1;
     return;
   }
   if (task.kind == ppsim::Kind::Broadcast) {
-    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], cs_);
+    if (rc_.record_events) rec(ev_start_[static_cast<size_t>(pos)], ms);
     zero_broadcast(i, task.minibatch);  // Broadcast's minibatch field: the window
-    // every replica of stage i reads the next version from its next task on (in order)
-    bump_version_kernel<<<1, 1, 0, cs_>>>(d_ver_, i * P_, P_);
-    stats.kernels_launched += 1;
-    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], cs_);
+    if (rc_.record_events) rec(ev_end_[static_cast<size_t>(pos)], ms);
     stats.tasks_executed += 1;
     return;
   }
@@ -1133,6 +1304,12 @@ void Engine::stage_tokens(const int32_t* h_in, const int32_t* h_lab) {
 void Engine::issue(int max_window, bool resident, const int32_t* h_in, const int32_t* h_lab, float* losses_out) {
   const int N = static_cast<int>(sched.order.size());
   const auto& g = sched.g;
+  if (done_.empty()) {
+    done_.resize(static_cast<size_t>(N));
+    for (auto& e : done_) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  issued_.assign(static_cast<size_t>(N), 0);
+  tok_loader_.assign(static_cast<size_t>(W_), -1);
   CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_ * P_) * sizeof(int), cs_));
   CUDA_OK(cudaMemsetAsync(d_loss_, 0, static_cast<size_t>(M_) * sizeof(float), cs_));
   CUDA_OK(cudaMemsetAsync(d_trace_, 0xff, g.tasks.size() * sizeof(int), cs_));
@@ -1147,6 +1324,11 @@ void Engine::issue(int max_window, bool resident, const int32_t* h_in, const int
   std::fill(wpending_.begin(), wpending_.end(), 0);
   std::fill(fpending_.begin(), fpending_.end(), 0);
   rec(run_begin_, cs_);
+  {  // every other stream starts after the run's initialisation (counters, losses, trace)
+    const cudaEvent_t e = handoff(cs_);
+    CUDA_OK(cudaStreamWaitEvent(us_, e, 0));
+    for (size_t k = 1; k < cstreams_.size(); ++k) CUDA_OK(cudaStreamWaitEvent(cstreams_[k], e, 0));
+  }
   for (int k = 0; k < N; ++k)
     if (g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])].window < max_window)
       exec_task(k, h_in, h_lab, loaded, last_left, losses_out);
@@ -1160,6 +1342,7 @@ void Engine::issue(int max_window, bool resident, const int32_t* h_in, const int
     }
   for (cudaStream_t st : {rs_, ss_, ks_, us_})  // join every stream: the run ends when all are idle
     if (st) CUDA_OK(cudaStreamWaitEvent(cs_, handoff(st), 0));
+  for (size_t k = 1; k < cstreams_.size(); ++k) CUDA_OK(cudaStreamWaitEvent(cs_, handoff(cstreams_[k]), 0));
   rec(run_end_, cs_);
 }
 
@@ -1233,12 +1416,16 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
     try {
       CUDA_OK(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
       const cudaEvent_t e0 = handoff(cs_);  // pull the other streams into the capture
-      for (cudaStream_t st : {us_, side_.side})
-        if (st) CUDA_OK(cudaStreamWaitEvent(st, e0, 0));
-      // the stage bodies wait on side-stream events recorded by the previous task; a wait on
-      // a record from outside the capture would invalidate it, so re-record them inside
-      if (side_.side)
-        for (cudaEvent_t e : side_.ev) CUDA_OK(cudaEventRecord(e, side_.side));
+      CUDA_OK(cudaStreamWaitEvent(us_, e0, 0));
+      for (size_t k = 0; k < cstreams_.size(); ++k) {
+        if (k) CUDA_OK(cudaStreamWaitEvent(cstreams_[k], e0, 0));
+        // the stage bodies wait on side-stream events recorded by the previous task; a wait on
+        // a record from outside the capture would invalidate it, so re-record them inside
+        if (sides_[k].side) {
+          CUDA_OK(cudaStreamWaitEvent(sides_[k].side, e0, 0));
+          for (cudaEvent_t e : sides_[k].ev) CUDA_OK(cudaEventRecord(e, sides_[k].side));
+        }
+      }
       issue(max_window, resident, h_in, h_lab, losses_out);
       CUDA_OK(cudaStreamEndCapture(cs_, &graph));
       capturing_ = false;
@@ -1354,7 +1541,7 @@ std::string Engine::plan_json() const {
                   ",\"rank\":" + std::to_string(rank_) + ",\"tokens_per_minibatch\":" + std::to_string(dm.T) +
                   ",\"comm_backend\":\"" + (world_ == 1 ? "none" : rc_.comm_backend == AMDP_COMM_NCCL ? "nccl" : "ipc") +
                   "\",\"graph_error\":\"" + json_escape(graph_error_) + "\",\"messages\":" + std::to_string(nmsg_) + ",\"collectives\":" + std::to_string(ncoll_) +
-                  ",\"device_rank\":[";
+                  ",\"compute_streams\":" + std::to_string(nstreams_) + ",\"device_rank\":[";
   for (size_t d = 0; d < dev_rank_.size(); ++d) s += (d ? "," : "") + std::to_string(dev_rank_[d]);
   s += "],\"partition\":[";
   for (size_t i = 0; i < part.size(); ++i) s += (i ? "," : "") + std::to_string(part[i]);
@@ -1421,7 +1608,7 @@ std::string Engine::memory_json() const {
            static_cast<int64_t>(stages[static_cast<size_t>(i)]->slot_bytes());
   }
   const int64_t bounds = static_cast<int64_t>(nbuf) * T * h * static_cast<int64_t>(dm.act_bytes());
-  const int64_t wsb = static_cast<int64_t>(GptStage::workspace_bytes(dm));
+  const int64_t wsb = static_cast<int64_t>(GptStage::workspace_bytes(dm)) * std::max(1, nstreams_);
   const int64_t io = static_cast<int64_t>(M_) * T * 8 + static_cast<int64_t>(M_) * 4;
   const int64_t total = w + wt + wver + master + grad + opt + act + bounds + wsb + io;
   auto kv = [](const char* k, int64_t v) { return std::string("\"") + k + "\":" + std::to_string(v); };

@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "amdp_kernels.h"
@@ -784,25 +785,28 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     const int T = sc.tiles_m * sc.tiles_n, R = T % pairs, num_kb = p.K / BK;
     if (ks_env != 0 && sc.tail_split == 1 && (T > pairs || ks_env == 2) && R > 0 && 2 * R <= pairs &&
         num_kb >= 8) {
-      // one flag buffer per device; K-split GEMMs of a device are issued on one stream (the
-      // executor's weight-gradient stream), so consecutive launches are ordered by the epoch
-      static int* flags_of[kMaxDevices];
-      static std::atomic<int> epoch_of[kMaxDevices];
+      // one flag buffer per (device, stream): launches on one stream are ordered, so the
+      // epoch tells consecutive ones apart; GEMMs on different streams (the executor's
+      // concurrent compute / weight-gradient streams) never share flags
+      static std::map<std::pair<int, cudaStream_t>, std::pair<int*, int>> flags_of;
       int* flags;
+      int epoch;
       {
         std::lock_guard<std::mutex> lk(g_dev_mu);
-        if (!flags_of[dev]) {
-          if (cudaMalloc(&flags_of[dev], 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
-          if (cudaMemset(flags_of[dev], 0, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
+        auto& slot = flags_of[{dev, s}];
+        if (!slot.first) {
+          if (cudaMalloc(&slot.first, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
+          if (cudaMemset(slot.first, 0, 2048 * 8 * sizeof(int)) != cudaSuccess) return AMDP_ERR_CUDA;
         }
-        flags = flags_of[dev];
+        flags = slot.first;
+        epoch = ++slot.second;
       }
       if (R <= 2048) {
         sc.ksplit = 2;
         sc.full_tiles = T - R;
         sc.num_work = sc.full_tiles + 2 * R;
         sc.flags = flags;
-        sc.epoch = ++epoch_of[dev];
+        sc.epoch = epoch;
       }
     }
   }
