@@ -701,7 +701,25 @@ int env_int(const char* name, int dflt) {
 // forward GEMMs, which run alone on the compute stream: the backward's activation- and
 // weight-gradient GEMMs (MN-major B) run concurrently on two streams and fill each other's
 // tails, where split sub-tiles measured slower (scripts/task_durations.py, B tasks).
-PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
+// Raster (tile rows per group, see tile_coords): L2 reuse of the operand that fits.  When one
+// operand is small enough to stay L2-resident (<= 48 MB of the 126 MB L2) and the other is
+// not, walk the tiles so the big one is streamed exactly once: row-major (group 1: a wave
+// covers ~tiles/row-length full rows, every A panel read once, all of B resident) or
+// column-major (group = tiles_m: every B panel read once, all of A resident).  fc1 / qkv /
+// LM-head weight gradients (A = the activation gradient^T, 100-824 MB; B = the layer input,
+// 34 MB) and the LM-head forward (B = 206 MB of head weights) are such shapes; otherwise
+// GROUP_M rows per group balance the two.
+int raster_group(int M, int N, int K, int tiles_m) {
+  static const int forced = env_int("AMDP_GEMM_GROUP_M", 0);
+  if (forced > 0) return forced;
+  const double a = 2.0 * M * static_cast<double>(K), b = 2.0 * N * static_cast<double>(K);
+  const double fits = 48.0 * 1024 * 1024;
+  if (b <= fits && a > 2 * b) return 1;
+  if (a <= fits && b > 2 * a) return tiles_m;
+  return GROUP_M;
+}
+
+PairSched pair_schedule(int M, int N, bool b_mn, int pairs, int K = 0) {
   PairSched s;
   s.tiles_m = (M + 255) / 256;
   s.tiles_n = (N + PBN - 1) / PBN;
@@ -721,8 +739,7 @@ PairSched pair_schedule(int M, int N, bool b_mn, int pairs) {
   }
   if (forced == 1 || ((forced == 2 || forced == 4) && !b_mn)) best = forced;
   s.tail_split = best;
-  static const int gm = env_int("AMDP_GEMM_GROUP_M", GROUP_M);
-  s.group_m = gm > 0 ? gm : GROUP_M;
+  s.group_m = K > 0 ? raster_group(M, N, K, s.tiles_m) : GROUP_M;
   s.full_tiles = best == 1 ? T : T - R;
   s.num_work = s.full_tiles + best * (T - s.full_tiles);
   s.ksplit = 1;
@@ -777,7 +794,7 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr_set[dev].store(true);
   }
   const int pairs = max_pairs<NST>();
-  PairSched sc = pair_schedule(p.M, p.N, B_MN, pairs);
+  PairSched sc = pair_schedule(p.M, p.N, B_MN, pairs, p.K);
   if constexpr (EPI == AMDP_EPI_ACCUM_F32) {
     // K-split of a partial last wave that fits in one wave as halves (fc1 / fc2 / LM-head
     // weight gradients at the 1.3B shapes); deterministic (see PairSched)
