@@ -701,22 +701,22 @@ int env_int(const char* name, int dflt) {
 // forward GEMMs, which run alone on the compute stream: the backward's activation- and
 // weight-gradient GEMMs (MN-major B) run concurrently on two streams and fill each other's
 // tails, where split sub-tiles measured slower (scripts/task_durations.py, B tasks).
-// Raster (tile rows per group, see tile_coords): L2 reuse of the operand that fits.  When one
-// operand is small enough to stay L2-resident (<= 48 MB of the 126 MB L2) and the other is
-// not, walk the tiles so the big one is streamed exactly once: row-major (group 1: a wave
-// covers ~tiles/row-length full rows, every A panel read once, all of B resident) or
-// column-major (group = tiles_m: every B panel read once, all of A resident).  fc1 / qkv /
-// LM-head weight gradients (A = the activation gradient^T, 100-824 MB; B = the layer input,
-// 34 MB) and the LM-head forward (B = 206 MB of head weights) are such shapes; otherwise
-// GROUP_M rows per group balance the two.
+// Raster (tile rows per group, see tile_coords).  Row-major (group 1: consecutive tiles walk
+// along N, so a wave of 74 pairs covers ~74 / tiles_n full tile rows: every A panel is read
+// once and B stays L2-resident) unless A is the operand that fits in L2 (<= 48 MB of the
+// 126 MB) and B is much larger (the LM-head forward: 206 MB of head weights), where the walk
+// is column-major (group = tiles_m) so that B is streamed once.  Measured under the power cap
+// (scripts/gemm_sustained.py, same box): row-major vs the previous 8-row groups +3.8% fc1
+// forward (1312 TF/s, above cuBLAS's 1292), +4.3% fc1 activation gradient, +3.9% fc2
+// forward, +4.4% fc1 weight gradient (DRAM reads 392 -> 313 MB per launch);
+// profiles/r02/gemm_raster.
 int raster_group(int M, int N, int K, int tiles_m) {
   static const int forced = env_int("AMDP_GEMM_GROUP_M", 0);
   if (forced > 0) return forced;
   const double a = 2.0 * M * static_cast<double>(K), b = 2.0 * N * static_cast<double>(K);
   const double fits = 48.0 * 1024 * 1024;
-  if (b <= fits && a > 2 * b) return 1;
   if (a <= fits && b > 2 * a) return tiles_m;
-  return GROUP_M;
+  return 1;
 }
 
 PairSched pair_schedule(int M, int N, bool b_mn, int pairs, int K = 0) {
