@@ -351,15 +351,32 @@ def main():
     except Exception:
         logical_bubble = None
     phys_bubble = max_over_ranks(1.0 - busy_frac) if busy_frac is not None else None
+    # e2e through the public API with pinned host buffers (its graph captured untimed first)
+    eng.run_windows(args.steps, toks.inputs, toks.labels, losses, resident=False)
+    barrier()
+    t0 = time.perf_counter()
+    eng.run_windows(args.steps, toks.inputs, toks.labels, losses, resident=False)
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    st2 = eng.stats()
+    e2e = args.steps * tok_step / e2e_s
+
     projection = None
     if world == 1 and args.steps > 2:
-        try:  # d-GPU projection of this measured run (static-order replay, reference bubble_ratio)
+        try:  # d-GPU projection (static-order replay, reference bubble_ratio) from per-task costs
+            # measured on the serial executor: with concurrent compute streams the tasks of
+            # different logical devices overlap, so their event spans are not their own costs
             from paper_2605_29664_b200 import projection as PR
+            ns = eng.plan()["compute_streams"]
+            eng.set_streams(1)
+            eng.run_windows(args.steps, toks.inputs, toks.labels, losses, resident=True)  # untimed
+            tl = eng.timeline()
+            lanes = eng.lane_events()
+            eng.set_streams(ns)
             gap_ns = model.tokens_per_minibatch * model.hidden * 2 / 770e9 * 1e9
             numel = [lib_numel(eng, i) for i in range(args.depth)]
             pol = E.RunConfig(depth=args.depth, threshold=args.threshold, windows=args.steps,
                               schedule=args.schedule, zero=zero).policy()
-            lanes = eng.lane_events()
             part = eng.plan()["partition"]
             segs = [part[i] + (i == 0) + (i == args.depth - 1) for i in range(args.depth)]
             projection = PR.project(tl, args.depth, args.threshold, args.steps, model.tokens_per_minibatch, gap_ns,
@@ -378,15 +395,6 @@ def main():
         except Exception as e:  # never let the projection break the bench line
             projection = {"error": str(e)[:200]}
 
-    # e2e through the public API with pinned host buffers (its graph captured untimed first)
-    eng.run_windows(args.steps, toks.inputs, toks.labels, losses, resident=False)
-    barrier()
-    t0 = time.perf_counter()
-    eng.run_windows(args.steps, toks.inputs, toks.labels, losses, resident=False)
-    barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    st2 = eng.stats()
-    e2e = args.steps * tok_step / e2e_s
 
     # per-kernel-class timing for the roofline
     kern = {}

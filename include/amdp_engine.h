@@ -136,6 +136,10 @@ int amdp_engine_set_kernel_timing(amdp_engine* e, int enable);
  * captured and later runs replay it.  Host buffers must be pinned (amdp_host_alloc) or the
  * run resident; otherwise, and with kernel timing on, runs are issued eagerly. */
 int amdp_engine_set_graphs(amdp_engine* e, int enable);
+/* Concurrent compute streams (one GPU, ZeRO AMDP; one per logical device by default, capped by
+ * free HBM): use the first n of them (1 = the serial executor, e.g. for isolated per-task
+ * times).  Returns the number in use. */
+int amdp_engine_set_streams(amdp_engine* e, int n);
 int amdp_engine_kernel_stats(const amdp_engine* e, amdp_kernel_class_stats* out, int cap);
 
 /* Stats of the last run: device-timed milliseconds from the first task to the last,

@@ -286,7 +286,8 @@ class Engine {
   // an event wait computed at plan time from the resources the tasks touch (activation slots,
   // boundary buffers, a stage's window gradient: B tasks of a stage keep their global order,
   // so the fp32 sums - and the bits - are those of the serial run).
-  int nstreams_ = 1;
+  int nstreams_ = 1;       // compute streams allocated (workspaces, side streams)
+  int active_streams_ = 1;  // compute streams the plan uses (<= nstreams_; amdp_engine_set_streams)
   std::vector<cudaStream_t> cstreams_;
   std::vector<SideStream> sides_;
   std::vector<uint8_t*> wss_;
@@ -333,6 +334,19 @@ class Engine {
 
  public:
   std::string comm_export() { return comm_ ? comm_->export_blob() : std::string(); }
+  // Use the first n allocated compute streams (1 = the serial executor: isolated per-task
+  // times, what the multi-GPU projection needs); recomputes the hazard plan and drops the
+  // captured graphs (they encode the previous stream assignment).
+  int set_streams(int n) {
+    if (plan_only_) return 0;
+    active_streams_ = std::max(1, std::min(n, nstreams_));
+    CUDA_OK(cudaDeviceSynchronize());
+    for (auto& kv : graphs_)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs_.clear();
+    plan_streams();
+    return active_streams_;
+  }
   void comm_connect(const std::vector<std::string>& blobs) {
     if (comm_) comm_->import_blobs(blobs);
   }
@@ -802,14 +816,14 @@ void Engine::plan_streams() {
   {
     int k = 0;
     for (int d = 0; d < devices_; ++d)
-      if (rank_of_dev(d) == rank_) dev_stream_[static_cast<size_t>(d)] = (k++) % nstreams_;
+      if (rank_of_dev(d) == rank_) dev_stream_[static_cast<size_t>(d)] = (k++) % active_streams_;
   }
   waits_.assign(static_cast<size_t>(N), {});
   stage_last_.assign(static_cast<size_t>(N), {});
   loss_tasks_.assign(static_cast<size_t>(W_), {});
   std::map<std::pair<int, int>, int> slot_last;  // (stage, slot) -> position
   std::map<int, int> buf_last, grad_last;
-  std::vector<std::vector<int>> stage_stream_last(static_cast<size_t>(depth_), std::vector<int>(static_cast<size_t>(nstreams_), -1));
+  std::vector<std::vector<int>> stage_stream_last(static_cast<size_t>(depth_), std::vector<int>(static_cast<size_t>(active_streams_), -1));
   auto stream_at = [&](int q) {
     return dev_stream_[static_cast<size_t>(g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(q)])].device)];
   };
@@ -968,6 +982,7 @@ void Engine::allocate() {
   }
   wpending_.assign(static_cast<size_t>(depth_ * nstreams_), 0);
   fpending_.assign(static_cast<size_t>(depth_ * nstreams_), 0);
+  active_streams_ = nstreams_;
   plan_streams();
 }
 
@@ -1541,7 +1556,8 @@ std::string Engine::plan_json() const {
                   ",\"rank\":" + std::to_string(rank_) + ",\"tokens_per_minibatch\":" + std::to_string(dm.T) +
                   ",\"comm_backend\":\"" + (world_ == 1 ? "none" : rc_.comm_backend == AMDP_COMM_NCCL ? "nccl" : "ipc") +
                   "\",\"graph_error\":\"" + json_escape(graph_error_) + "\",\"messages\":" + std::to_string(nmsg_) + ",\"collectives\":" + std::to_string(ncoll_) +
-                  ",\"compute_streams\":" + std::to_string(nstreams_) + ",\"device_rank\":[";
+                  ",\"compute_streams\":" + std::to_string(active_streams_) + ",\"compute_streams_allocated\":" +
+                  std::to_string(nstreams_) + ",\"device_rank\":[";
   for (size_t d = 0; d < dev_rank_.size(); ++d) s += (d ? "," : "") + std::to_string(dev_rank_[d]);
   s += "],\"partition\":[";
   for (size_t i = 0; i < part.size(); ++i) s += (i ? "," : "") + std::to_string(part[i]);
@@ -1844,6 +1860,14 @@ int amdp_engine_stage_tokens(amdp_engine* e, const int32_t* inputs, const int32_
 int amdp_engine_set_kernel_timing(amdp_engine* e, int enable) {
   reinterpret_cast<Engine*>(e)->set_kernel_timing(enable != 0);
   return 0;
+}
+
+int amdp_engine_set_streams(amdp_engine* e, int n) {
+  try {
+    return reinterpret_cast<Engine*>(e)->set_streams(n);
+  } catch (...) {
+    return AMDP_ERR_CUDA;
+  }
 }
 
 int amdp_engine_set_graphs(amdp_engine* e, int enable) {

@@ -66,6 +66,7 @@ _sig("amdp_engine_run_windows", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_v
 _sig("amdp_engine_stage_tokens", c_int, [c_void_p, c_void_p, c_void_p])
 _sig("amdp_engine_set_kernel_timing", c_int, [c_void_p, c_int])
 _sig("amdp_engine_set_graphs", c_int, [c_void_p, c_int])
+_sig("amdp_engine_set_streams", c_int, [c_void_p, c_int])
 
 
 class _KStat(Structure):
@@ -342,6 +343,13 @@ class Engine:
 
     def set_kernel_timing(self, on: bool) -> None:
         lib.amdp_engine_set_kernel_timing(self._h, int(on))
+
+    def set_streams(self, n: int) -> int:
+        """Concurrent compute streams in use (1 = serial executor); returns the count."""
+        r = lib.amdp_engine_set_streams(self._h, int(n))
+        if r < 0:
+            raise RuntimeError("amdp_engine_set_streams failed")
+        return r
 
     def set_graphs(self, on: bool) -> None:
         """CUDA graphs of whole runs (default on, one GPU; needs pinned host buffers)."""

@@ -23,6 +23,10 @@ def _run(kind, single, monkeypatch):
     elif kind == "hd64_d4":
         m, depth = E.ModelConfig(4, 512, 8, 2048, 2048, 256), 4
         m.layers_per_stage = [1, 1, 1, 1]
+    elif kind == "wide_d4":  # 1.3B-wide layers (h 2048, ffn 8192, head_dim 128): CTA-pair GEMMs with
+        # N-split tails and K-split weight-gradient tails (per-stream flag buffers), tcgen05 attention
+        m, depth = E.ModelConfig(4, 2048, 16, 8192, 4096, 512), 4
+        m.layers_per_stage = [1, 1, 1, 1]
     else:  # BERT-like, D=8: 8 concurrent streams, bidirectional MLM
         m, depth = E.ModelConfig(8, 256, 4, 1024, 2048, 128, causal=False), 8
         m.layers_per_stage = [1] * 8
@@ -42,7 +46,7 @@ def _run(kind, single, monkeypatch):
     return out, w, rep, streams
 
 
-@pytest.mark.parametrize("kind", ["tiny_d4", "hd64_d4", "bert_d8"])
+@pytest.mark.parametrize("kind", ["tiny_d4", "hd64_d4", "wide_d4", "bert_d8"])
 def test_concurrent_streams_bit_identical_to_single_stream(kind, monkeypatch):
     multi, wm, rep, ns = _run(kind, False, monkeypatch)
     single, ws, _, ns1 = _run(kind, True, monkeypatch)
