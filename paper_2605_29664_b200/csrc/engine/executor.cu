@@ -279,8 +279,8 @@ class Engine {
   uint16_t* bounds_arena_ = nullptr;
   std::vector<std::pair<int, int>> planned_sends_;  // (message id, boundary buffer)
   uint8_t* ws_ = nullptr;
-  // Concurrent compute streams (one GPU, ZeRO AMDP): logical device d's Forward / Backward
-  // tasks run in dispatch order on compute stream dev_stream_[d] (cstreams_[0] = cs_), each
+  // Concurrent compute streams (ZeRO AMDP, any rank hosting several logical devices): logical
+  // device d's Forward / Backward tasks run in dispatch order on compute stream dev_stream_[d] (cstreams_[0] = cs_), each
   // with its own weight-gradient side stream and workspace, so tasks of different logical
   // devices overlap on the SMs as they would on separate GPUs.  Every cross-stream hazard is
   // an event wait computed at plan time from the resources the tasks touch (activation slots,
@@ -951,18 +951,22 @@ void Engine::allocate() {
   }
   CUDA_OK(cudaEventCreate(&run_begin_));
   CUDA_OK(cudaEventCreate(&run_end_));
-  // concurrent compute streams: as many as logical devices (one GPU, ZeRO AMDP), within what
-  // the extra workspaces leave of HBM (a 6 GiB margin); AMDP_STREAMS overrides the count
+  // concurrent compute streams: as many as this rank's logical devices (ZeRO AMDP; the NCCL
+  // backend keeps one), within what the extra workspaces leave of HBM (a 6 GiB margin);
+  // AMDP_STREAMS overrides the count
   cstreams_.assign(1, cs_);
   sides_.assign(1, side_);
   wss_.assign(1, ws_);
   nstreams_ = 1;
-  if (world_ == 1 && zero_ && devices_ > 1 && !getenv("AMDP_SINGLE_STREAM")) {
+  int local_devices = 0;
+  for (int d = 0; d < devices_; ++d) local_devices += rank_of_dev(d) == rank_ ? 1 : 0;
+  const bool nccl = comm_ && comm_->single_stream();  // NCCL: one stream for all its ops
+  if (zero_ && local_devices > 1 && !nccl && !getenv("AMDP_SINGLE_STREAM")) {
     size_t fr = 0, tot = 0;
     CUDA_OK(cudaMemGetInfo(&fr, &tot));
     const size_t wsb = GptStage::workspace_bytes(dm);
-    int want = getenv("AMDP_STREAMS") ? std::max(1, atoi(getenv("AMDP_STREAMS"))) : devices_;
-    want = std::min(want, devices_);
+    int want = getenv("AMDP_STREAMS") ? std::max(1, atoi(getenv("AMDP_STREAMS"))) : local_devices;
+    want = std::min(want, local_devices);
     while (want > 1 && static_cast<size_t>(want - 1) * wsb + (6ull << 30) > fr) --want;
     for (int k = 1; k < want; ++k) {
       cudaStream_t st;
@@ -1019,7 +1023,8 @@ void Engine::exec_comm(int pos) {
     switch (op.kind) {
       case CommOp::Send: {
         BoundaryBuf& b = bufs_[static_cast<size_t>(op.buf)];
-        CUDA_OK(cudaStreamWaitEvent(ss_, handoff(cs_), 0));
+        // after the producing task (this position) on its compute stream
+        CUDA_OK(cudaStreamWaitEvent(ss_, issued_[static_cast<size_t>(pos)] ? done_[static_cast<size_t>(pos)] : handoff(cs_), 0));
         comm_->send(op.id, op.peer, b.ptr, bytes, ss_);
         CUDA_OK(cudaEventRecord(b.comm_done, ss_));
         b.comm_pending = true;
