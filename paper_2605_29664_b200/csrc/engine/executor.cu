@@ -280,8 +280,9 @@ class Engine {
   std::vector<std::pair<int, int>> planned_sends_;  // (message id, boundary buffer)
   uint8_t* ws_ = nullptr;
   // Concurrent compute streams (ZeRO AMDP, any rank hosting several logical devices): logical
-  // device d's Forward / Backward tasks run in dispatch order on compute stream dev_stream_[d] (cstreams_[0] = cs_), each
-  // with its own weight-gradient side stream and workspace, so tasks of different logical
+  // device d's Forward / Backward tasks run in dispatch order on compute stream
+  // dev_stream_[d] (cstreams_[0] = cs_), each with its own weight-gradient side stream and
+  // workspace, so tasks of different logical
   // devices overlap on the SMs as they would on separate GPUs.  Every cross-stream hazard is
   // an event wait computed at plan time from the resources the tasks touch (activation slots,
   // boundary buffers, a stage's window gradient: B tasks of a stage keep their global order,
