@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(384, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap qkv_map, const __grid_constant__ CUtensorMap do_map,
                      const bf16* __restrict__ qkv, const float* __restrict__ lse, const float* __restrict__ delta,
                      bf16* __restrict__ dqkv, int seq, int H, int n_qt, int BH, float scale_log2, float scale,
-                     int causal) {
+                     int causal, int early) {
   using L = QSmem<D>;
   constexpr int NSK = L::NSK, NSV = L::NSV;
   extern __shared__ uint8_t smem_raw[];
@@ -469,7 +469,12 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  ptx::pdl_wait();
+  // PDL: this kernel's predecessor is the dK/dV kernel, which it does not read (dQ and dK/dV
+  // are disjoint columns of dqkv); its inputs (qkv, dO, lse, delta) were complete when dK/dV
+  // passed its own griddepcontrol.wait, which precedes the trigger that let this grid launch.
+  // So dQ CTAs start on the SMs the dK/dV tail frees, and wait for dK/dV only before exiting
+  // (the next kernel's wait on this grid then also covers dK/dV).
+  if (!early) ptx::pdl_wait();
   ptx::pdl_trigger();
   // TMEM: S at 0, dP at 128, dQ at 256, dS (bf16 pairs, 64 columns) at 256 + 64 NB,
   // Q (bf16 pairs, D / 2 columns) at 320 + 64 NB
@@ -662,6 +667,7 @@ __global__ void __launch_bounds__(384, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
+  if (early) ptx::pdl_wait();  // the dK/dV grid has completed before this one does
 }
 
 template <class K>
@@ -696,8 +702,9 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
                              delta, dqkv, S, H, nt, H * B, scale_log2, scale, causal);
   if (e != cudaSuccess) return e;
   const int dq_grid = std::min(nt * H * B, num_sms());  // persistent
+  static const int early = getenv("AMDP_ATTN_DQ_EARLY") ? atoi(getenv("AMDP_ATTN_DQ_EARLY")) : 1;
   e = launch_pdl(fa_bwd_dq_kernel<D>, dim3(dq_grid), dim3(384), smem_q, st, q128, o128, qkv, lse, delta, dqkv, S, H,
-                 nt, H * B, scale_log2, scale, causal);
+                 nt, H * B, scale_log2, scale, causal, early);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
