@@ -884,15 +884,21 @@ int gemm_pairs() {
 
 // Tile shape per problem: CTA pairs with 256 x 256 tiles whenever M >= 256 (measured at the
 // 1.3B shapes, profiles/r01_gemm_modes.txt: +5-13% over single-CTA 128x256 tiles).
-int choose_mode(int M, int N, bool a_mn, bool b_mn) {
-  (void)N;
+int choose_mode(int M, int N, int K, bool a_mn, bool b_mn) {
   (void)a_mn;
   (void)b_mn;
   static const int forced = env_int("AMDP_GEMM_MODE", -1);
   if (forced == 0 || forced == 256) return forced;
-  // CTA pairs everywhere M allows.  (Weight-gradient GEMMs, A and B MN-major, issue four TMA
-  // boxes per stage and CTA; with a single-lane producer that issue loop starved the pair
-  // kernel, 1081 TF/s sustained vs 1136 on single-CTA tiles; warp-converged issue: 1189.)
+  // CTA pairs everywhere M allows, except small products (< 20 GFLOP: the BERT-large layer
+  // GEMMs at 2048 tokens, 350M's out-projection), which run as single-CTA 128x256 tiles: with
+  // the executor's concurrent streams a small GEMM then occupies half the SMs per tile and
+  // leaves the rest to other logical devices' kernels (BERT-large D8 +7%, same box A/B;
+  // GPT-1.3B's >= 69 GFLOP GEMMs stay on pairs, which are 6% faster there).  (Weight-gradient
+  // GEMMs, A and B MN-major, issue four TMA boxes per stage and CTA; with a single-lane
+  // producer that issue loop starved the pair kernel: 1081 TF/s sustained vs 1136 on
+  // single-CTA tiles; warp-converged issue: 1189.)
+  static const double small = env_int("AMDP_GEMM_SMALL_GFLOP", 20) * 1e9;
+  if (2.0 * M * static_cast<double>(N) * K < small) return 0;
   return M >= 256 ? 256 : 0;
 }
 
@@ -917,7 +923,7 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) return AMDP_ERR_CUDA;
   }
-  const int mode = choose_mode(a->M, a->N, a->a_mn_major != 0, a->b_mn_major != 0);
+  const int mode = choose_mode(a->M, a->N, a->K, a->a_mn_major != 0, a->b_mn_major != 0);
   CUtensorMap ma, mb, mbt;
   bool ok;
   if (a->a_mn_major)  // A stored [K][lda], M contiguous
