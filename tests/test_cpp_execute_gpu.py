@@ -45,3 +45,25 @@ def test_cpp_execute_matches_reference_and_oracle():
         assert int(ver) == seen[(kind, int(stage), int(mb))], row
     losses = np.array(r["losses"])
     assert np.max(np.abs(losses - ol) / np.abs(ol)) < 1e-3
+
+
+def test_cpp_execute_two_ranks_on_one_gpu(tmp_path):
+    """ppsim::execute with world_size 2 from C++ (ExecuteOptions::allgather over a shared
+    directory), both ranks on one GPU through the peer-memory data plane: the union of the
+    ranks' version traces and losses is the single-rank program's, to the bit (the fold puts
+    every stage of the tiny D=4 config on one rank, so only stage-boundary hops cross)."""
+    cpp = os.path.join(ROOT, "tests", "cpp")
+    subprocess.run(["make", "-C", cpp, "_build/execute_tiny", "_build/execute_multirank"], check=True,
+                   capture_output=True)
+    one = json.loads(subprocess.run([os.path.join(cpp, "_build", "execute_tiny")], capture_output=True, text=True,
+                                    timeout=600, check=True).stdout)
+    procs = [subprocess.Popen([os.path.join(cpp, "_build", "execute_multirank"), str(r), "2", str(tmp_path)],
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=600) for p in procs]
+    assert all(p.returncode == 0 for p in procs), [o[1][-2000:] for o in outs]
+    res = [json.loads(o[0]) for o in outs]
+    losses = np.sum([np.array(r["losses"]) for r in res], axis=0)
+    assert np.array_equal(losses.astype(np.float32), np.array(one["losses"], np.float32))
+    rows = sorted(x for r in res for x in r["version_trace"].strip().split("\n")[1:])
+    assert rows == sorted(one["version_trace"].strip().split("\n")[1:])
+    assert all(r["p2p_bytes_sent"] > 0 and r["overlap_issues"] == 0 for r in res)
