@@ -445,6 +445,9 @@ struct PairSched {
   int ksplit;       // 1 or 2
   int* flags;       // [tail tiles][2][4]
   int epoch;        // this launch's flag value
+  // L2 policy of the operand loads (see raster_group): 0 none, 1 A streamed once (evict_first)
+  // and B resident (evict_last), 2 the reverse
+  int l2hint;
 };
 
 // Work item w -> output rows [m0, m0 + 256), columns [n0, n0 + width), K blocks [kb0, kb1);
@@ -535,6 +538,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
     {  // TMA producer (warp-converged, elect.sync in the asm)
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pol_stream = ptx::l2_policy_evict_first(), pol_keep = ptx::l2_policy_evict_last();
+      const uint64_t pol_a = sc.l2hint == 1 ? pol_stream : pol_keep;
+      const uint64_t pol_b = sc.l2hint == 1 ? pol_keep : pol_stream;
       for (int w = cluster; w < sc.num_work; w += nclusters) {
         int m0, n0, width, kb0, kb1, khalf, tail;
         pair_work(sc, w, num_kb, m0, n0, width, kb0, kb1, khalf, tail);
@@ -550,17 +556,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PAIR_THREADS, 1)
           uint8_t* sa = smem_a + stage * C::A_BYTES;
           uint8_t* sb = smem_b + stage * C::B_BYTES;
           const int k0 = kb * BK;
-          if constexpr (A_MN) {
-            ptx::tma_load_2d_pair_w(sa, &map_a, fb, ma, k0);
-            ptx::tma_load_2d_pair_w(sa + 64 * BK * 2, &map_a, fb, ma + 64, k0);
+          if (sc.l2hint == 0) {
+            if constexpr (A_MN) {
+              ptx::tma_load_2d_pair_w(sa, &map_a, fb, ma, k0);
+              ptx::tma_load_2d_pair_w(sa + 64 * BK * 2, &map_a, fb, ma + 64, k0);
+            } else {
+              ptx::tma_load_2d_pair_w(sa, &map_a, fb, k0, ma);
+            }
+            if constexpr (B_MN) {
+              for (int i = 0; i < half / 64; ++i)
+                ptx::tma_load_2d_pair_w(sb + i * 64 * BK * 2, &map_b, fb, nb + 64 * i, k0);
+            } else {
+              ptx::tma_load_2d_pair_w(sb, mb, fb, k0, nb);
+            }
           } else {
-            ptx::tma_load_2d_pair_w(sa, &map_a, fb, k0, ma);
-          }
-          if constexpr (B_MN) {
-            for (int i = 0; i < half / 64; ++i)
-              ptx::tma_load_2d_pair_w(sb + i * 64 * BK * 2, &map_b, fb, nb + 64 * i, k0);
-          } else {
-            ptx::tma_load_2d_pair_w(sb, mb, fb, k0, nb);
+            if constexpr (A_MN) {
+              ptx::tma_load_2d_pair_hint_w(sa, &map_a, fb, ma, k0, pol_a);
+              ptx::tma_load_2d_pair_hint_w(sa + 64 * BK * 2, &map_a, fb, ma + 64, k0, pol_a);
+            } else {
+              ptx::tma_load_2d_pair_hint_w(sa, &map_a, fb, k0, ma, pol_a);
+            }
+            if constexpr (B_MN) {
+              for (int i = 0; i < half / 64; ++i)
+                ptx::tma_load_2d_pair_hint_w(sb + i * 64 * BK * 2, &map_b, fb, nb + 64 * i, k0, pol_b);
+            } else {
+              ptx::tma_load_2d_pair_hint_w(sb, mb, fb, k0, nb, pol_b);
+            }
           }
           if (++stage == C::NSTAGE) { stage = 0; phase ^= 1; }
         }
@@ -740,6 +761,19 @@ PairSched pair_schedule(int M, int N, bool b_mn, int pairs, int K = 0) {
   if (forced == 1 || ((forced == 2 || forced == 4) && !b_mn)) best = forced;
   s.tail_split = best;
   s.group_m = K > 0 ? raster_group(M, N, K, s.tiles_m) : GROUP_M;
+  s.l2hint = 0;
+  // L2 policies (AMDP_GEMM_L2HINT=1): the streamed operand evict_first, the resident one
+  // evict_last.  Isolated fc1 weight gradient: DRAM reads 317 -> 288 MB, writes 45 -> 24 MB
+  // (1.03x algorithmic), sustained +1-4%; but in the model the "streamed" operand (the
+  // activation gradient dU) is read again by the concurrent activation-gradient GEMM, which
+  // then misses: 1.3B window 1.3% slower.  Off by default.
+  if (K > 0) {
+    static const int hints = env_int("AMDP_GEMM_L2HINT", 0);
+    const double a = 2.0 * M * static_cast<double>(K), b = 2.0 * N * static_cast<double>(K);
+    const double fits = 48.0 * 1024 * 1024;
+    if (hints && s.group_m == 1 && b <= fits && a > 2 * b) s.l2hint = 1;
+    if (hints && s.group_m == s.tiles_m && s.tiles_m > 1 && a <= fits && b > 2 * a) s.l2hint = 2;
+  }
   s.full_tiles = best == 1 ? T : T - R;
   s.num_work = s.full_tiles + best * (T - s.full_tiles);
   s.ksplit = 1;
