@@ -50,6 +50,11 @@ typedef struct amdp_model_config {
    * match the fp64 CPU oracle at a tolerance far below bf16's (north_star).  Slow; for
    * correctness runs, not throughput. */
   int fp32_validation;
+  /* bidirectional (BERT) models: token id > 0 that marks padding (0 = no padding).  Each
+   * sequence's valid length is the position of its first pad token; attention gives padded
+   * keys no weight (their labels must be -1).  amdp_synthetic_tokens pads such models to a
+   * length drawn in [seq / 2, seq]. */
+  int pad_token;
 } amdp_model_config;
 
 typedef struct amdp_run_config {

@@ -78,9 +78,13 @@ int amdp_gemm(const amdp_gemm_args* args, amdp_stream_t stream);
  * Causal (or full) multi-head attention over `batch` sequences of `seq` tokens.
  * qkv: [batch*seq][3*H*D] bf16 rows holding q | k | v (head-major inside each);
  * out: [batch*seq][H*D] bf16; lse: [batch][H][seq] fp32 log-sum-exp (saved for bwd).
- * D in {32, 64, 80, 128}.                                                           */
+ * D in {32, 64, 80, 128}.  key_len (bidirectional models only; NULL = none): device int32
+ * [batch], the number of valid keys of each sequence — keys at positions >= key_len[b] are
+ * padding and get no attention weight (BERT padding mask); padded query rows still get an
+ * output (their loss is masked by the labels).                                       */
 int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse, int batch, int seq,
-                       int heads, int head_dim, int causal, amdp_stream_t stream);
+                       int heads, int head_dim, int causal, const int32_t* key_len,
+                       amdp_stream_t stream);
 /* dout: [batch*seq][H*D]; writes dqkv [batch*seq][3*H*D] (dq | dk | dv).
  * workspace: at least amdp_attention_bwd_workspace() bytes.                        */
 size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim);
@@ -95,10 +99,11 @@ enum { AMDP_ATTN_IMPL_MMA_SYNC = 0, AMDP_ATTN_IMPL_TCGEN05 = 1 };
 int amdp_attention_impl(int seq, int head_dim, int backward);
 int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse, const float* delta,
                              uint16_t* dqkv, int batch, int seq, int heads, int head_dim, int causal,
-                             amdp_stream_t stream);
+                             const int32_t* key_len, amdp_stream_t stream);
 int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                        const float* lse, uint16_t* dqkv, void* workspace, int batch, int seq,
-                       int heads, int head_dim, int causal, amdp_stream_t stream);
+                       int heads, int head_dim, int causal, const int32_t* key_len,
+                       amdp_stream_t stream);
 
 /* ---------------------------------------------------------------- LayerNorm
  * y = (x - mean) * rstd * gamma + beta over rows of width `cols` (bf16 in/out,
@@ -153,11 +158,13 @@ int amdp_f32_layernorm_bwd(const float* dy, const float* x, const float* gamma,
                            float* dx, float* dgamma, float* dbeta, int rows, int cols,
                            amdp_stream_t stream);
 int amdp_f32_attention_fwd(const float* qkv, float* out, float* lse, int batch, int seq,
-                           int heads, int head_dim, int causal, amdp_stream_t stream);
+                           int heads, int head_dim, int causal, const int32_t* key_len,
+                           amdp_stream_t stream);
 size_t amdp_f32_attention_bwd_workspace(int batch, int seq, int heads);
 int amdp_f32_attention_bwd(const float* qkv, const float* out, const float* dout,
                            const float* lse, float* dqkv, float* workspace, int batch, int seq,
-                           int heads, int head_dim, int causal, amdp_stream_t stream);
+                           int heads, int head_dim, int causal, const int32_t* key_len,
+                           amdp_stream_t stream);
 int amdp_f32_embedding_fwd(const int32_t* tokens, const float* wte, const float* wpe, float* x,
                            int ntok, int seq, int hidden, amdp_stream_t stream);
 int amdp_f32_embedding_bwd(const int32_t* tokens, const float* dx, float* dwte, float* dwpe,

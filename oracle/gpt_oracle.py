@@ -66,10 +66,12 @@ def _sm_int(x: int) -> int:
 
 
 def synthetic_tokens(seq: int, seqs: int, vocab: int, data_seed: int, first: int, count: int,
-                     causal: bool = True):
+                     causal: bool = True, pad_token: int = 0):
     """amdp_synthetic_tokens: arithmetic-progression token streams with 1/8 noise; causal ->
     next-token labels; otherwise BERT MLM (15% positions, 80/10/10 [MASK]/random/keep,
-    [MASK] = vocab - 1, label -1 elsewhere)."""
+    [MASK] = vocab - 1, label -1 elsewhere).  pad_token > 0 (bidirectional only): each sequence
+    keeps a length in [S/2, S] drawn from bits 40.. of its seed word; real tokens equal to the
+    pad id become (pad + 1) % V, positions past the length hold the pad id with label -1."""
     T = seq * seqs
     inputs = np.empty((count, T), np.int32)
     labels = np.empty((count, T), np.int32)
@@ -95,8 +97,14 @@ def synthetic_tokens(seq: int, seqs: int, vocab: int, data_seed: int, first: int
                 act = (hm >> np.uint64(8)) % np.uint64(10)
                 rnd = ((hm >> np.uint64(16)) % np.uint64(vocab)).astype(np.int64)
                 inp = np.where(masked & (act < 8), vocab - 1, np.where(masked & (act == 8), rnd, tok[:seq]))
+                lab = np.where(masked, tok[:seq], -1)
+                if pad_token > 0:
+                    n = seq // 2 + (r >> 40) % (seq - seq // 2 + 1)
+                    inp = np.where(inp == pad_token, (pad_token + 1) % vocab, inp)
+                    inp[n:] = pad_token
+                    lab[n:] = -1
                 inputs[j, sl] = inp
-                labels[j, sl] = np.where(masked, tok[:seq], -1)
+                labels[j, sl] = lab
     return inputs, labels
 
 
@@ -142,6 +150,7 @@ class Model:
     seqs: int = 4
     causal: bool = True
     seed: int = 1234
+    pad_token: int = 0  # > 0 (bidirectional): keys at/after a sequence's first pad id are masked
     ln_eps: float = 1e-5
     std: float = 0.02
 
@@ -221,23 +230,38 @@ class StageMath:
         dx = rstd * (dxh - dxh.mean(-1, keepdims=True) - xh * (dxh * xh).mean(-1, keepdims=True))
         return dx, (dy * xh).sum(0), dy.sum(0)
 
-    def _attn_seq(self, qkv):
-        """One sequence: qkv [S, 3hd] -> (o [S, h], p [H, S, S])."""
+    def _lens(self, tokens):
+        """Valid key length per sequence: the first pad position (executor.cu run(), >= 1)."""
+        m = self.m
+        if m.pad_token <= 0 or m.causal:
+            return [m.seq] * m.seqs
+        out = []
+        for sq in np.asarray(tokens).reshape(m.seqs, m.seq):
+            hit = np.nonzero(sq == m.pad_token)[0]
+            out.append(max(1, int(hit[0])) if hit.size else m.seq)
+        return out
+
+    def _attn_seq(self, qkv, klen=None):
+        """One sequence: qkv [S, 3hd] -> (o [S, h], p [H, S, S]); keys >= klen masked."""
         m = self.m
         S, H, D = m.seq, m.heads, m.hidden // m.heads
         q, k, v = qkv.reshape(S, 3, H, D).transpose(1, 2, 0, 3)
         s = q @ k.transpose(0, 2, 1) / math.sqrt(D)
         if m.causal:
             s = np.where(np.triu(np.ones((S, S), bool), 1), -np.inf, s)
+        if klen is not None and klen < S:
+            s[:, :, klen:] = -np.inf
         s = s - s.max(-1, keepdims=True)
         p = np.exp(s)
         p /= p.sum(-1, keepdims=True)
         return (p @ v).transpose(1, 0, 2).reshape(S, H * D), p
 
-    def _attn(self, qkv):
+    def _attn(self, qkv, lens=None):
         m = self.m
         seqs = qkv.reshape(m.seqs, m.seq, -1)
-        res = list(_POOL.map(self._attn_seq, seqs)) if _POOL else [self._attn_seq(x) for x in seqs]
+        lens = lens if lens is not None else [None] * m.seqs
+        res = list(_POOL.map(self._attn_seq, seqs, lens)) if _POOL else \
+            [self._attn_seq(x, n) for x, n in zip(seqs, lens)]
         return np.concatenate([r[0] for r in res], 0), np.stack([r[1] for r in res], 0)
 
     def _attn_bwd_seq(self, qkv, p, do):
@@ -260,7 +284,7 @@ class StageMath:
 
     def forward(self, W, x_in, tokens, labels):
         rb, m = self.rb, self.m
-        cache = {"x_in": x_in}
+        cache = {"x_in": x_in, "lens": self._lens(tokens)}
         if self.stage == 0:
             x = rb(W["wte"][tokens] + W["wpe"][np.arange(m.T) % m.seq])
             cache["x0"] = x
@@ -273,7 +297,7 @@ class StageMath:
             a, c["mu1"], c["r1"] = self._ln(x, W[p + "ln1.gamma"], W[p + "ln1.beta"])
             c["ln1"] = a = rb(a)
             c["qkv"] = qkv = rb(a @ W[p + "attn.qkv"].T)
-            o, c["p"] = self._attn(qkv)
+            o, c["p"] = self._attn(qkv, cache["lens"])
             c["o"] = o = rb(o)
             c["hmid"] = hm = rb(x + o @ W[p + "attn.out"].T)
             a2, c["mu2"], c["r2"] = self._ln(hm, W[p + "ln2.gamma"], W[p + "ln2.beta"])

@@ -62,15 +62,15 @@ def _sig(name, restype, argtypes):
 _P = c_void_p
 _sig("amdp_gemm", c_int, [POINTER(GemmArgs), _P])
 _sig("amdp_f32_gemm", c_int, [POINTER(GemmArgs), _P])
-_sig("amdp_attention_fwd", c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
+_sig("amdp_attention_fwd", c_int, [_P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P, _P])
 _sig("amdp_attention_bwd_workspace", c_size_t, [c_int, c_int, c_int, c_int])
 _sig("amdp_attention_bwd", c_int,
-     [_P, _P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
+     [_P, _P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P, _P])
 _sig("amdp_attention_bwd_delta_supported", c_int, [c_int, c_int])
 _sig("amdp_attention_impl", c_int, [c_int, c_int, c_int])
 _sig("amdp_gelu_fwd", c_int, [_P, _P, c_int64, _P])
 _sig("amdp_attention_bwd_delta", c_int,
-     [_P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P])
+     [_P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P, _P])
 _sig("amdp_layernorm_fwd", c_int, [_P, _P, _P, _P, _P, _P, c_int, c_int, c_float, _P])
 _sig("amdp_layernorm_bwd_workspace", c_size_t, [c_int, c_int])
 _sig("amdp_layernorm_bwd", c_int,

@@ -97,6 +97,14 @@ int amdp_synthetic_tokens(const amdp_model_config* m, uint64_t seed, int first, 
             if (act < 8) in = static_cast<int32_t>(UV - 1);  // [MASK] = last vocabulary id
             else if (act == 8) in = static_cast<int32_t>((hm >> 16) % UV);
           }
+          if (m->pad_token > 0) {  // padded to a length in [S/2, S]; no real token is the pad id
+            const int len = S / 2 + static_cast<int>((r >> 40) % static_cast<uint64_t>(S - S / 2 + 1));
+            if (in == m->pad_token) in = static_cast<int32_t>((m->pad_token + 1) % V);
+            if (p >= len) {
+              in = m->pad_token;
+              lab = -1;
+            }
+          }
           inputs[base + static_cast<size_t>(p)] = in;
           labels[base + static_cast<size_t>(p)] = lab;
         }

@@ -57,6 +57,8 @@ Engine::~Engine() {
   cudaFree(bounds_arena_);
   cudaFree(ws_);
   cudaFree(d_inputs_);
+  cudaFree(d_lens_);
+  if (h_lens_) cudaFreeHost(h_lens_);
   cudaFree(d_labels_);
   cudaFree(d_loss_);
   cudaFree(d_ver_);
@@ -164,6 +166,11 @@ void Engine::allocate() {
   CUDA_OK(cudaMalloc(&ws_, GptStage::workspace_bytes(dm)));
   CUDA_OK(cudaMalloc(&d_inputs_, static_cast<size_t>(M_) * T * sizeof(int32_t)));
   CUDA_OK(cudaMalloc(&d_labels_, static_cast<size_t>(M_) * T * sizeof(int32_t)));
+  if (dm.pad_token > 0) {
+    CUDA_OK(cudaMalloc(&d_lens_, static_cast<size_t>(M_) * dm.B * sizeof(int32_t)));
+    CUDA_OK(cudaHostAlloc(&h_lens_, static_cast<size_t>(M_) * dm.B * sizeof(int32_t), cudaHostAllocDefault));
+    std::fill(h_lens_, h_lens_ + static_cast<size_t>(M_) * dm.B, dm.S);
+  }
   CUDA_OK(cudaMalloc(&d_loss_, static_cast<size_t>(M_) * sizeof(float)));
   CUDA_OK(cudaMalloc(&d_ver_, static_cast<size_t>(depth_ * P_) * sizeof(int)));
   CUDA_OK(cudaMalloc(&d_trace_, sched.g.tasks.size() * sizeof(int)));
@@ -460,19 +467,20 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
     use_replica_weights(i, task.pipeline);
     stats.kernels_launched += 1;
     const int32_t* tok = d_inputs_ + static_cast<size_t>(j) * T;
+    const int32_t* klen = d_lens_ ? d_lens_ + static_cast<size_t>(j) * dm.B : nullptr;  // key padding
     const int32_t* lab = d_labels_ + static_cast<size_t>(j) * T;
     const uint16_t* in = tp.in_buf >= 0 ? bufs_[static_cast<size_t>(tp.in_buf)].ptr : nullptr;
     int launched;
     if (task.kind == ppsim::Kind::Forward) {
       uint16_t* out = tp.out_buf >= 0 ? bufs_[static_cast<size_t>(tp.out_buf)].ptr : nullptr;
       launched = S.forward(A, tok, lab, in, out, d_loss_ + j, loss_scale_[static_cast<size_t>(j)],
-                           wss_[static_cast<size_t>(si)], cs, &rc, seg_wait);
+                           wss_[static_cast<size_t>(si)], cs, &rc, seg_wait, klen);
     } else {
       const uint16_t* gin = tp.gin_buf >= 0 ? bufs_[static_cast<size_t>(tp.gin_buf)].ptr : nullptr;
       uint16_t* gout = tp.gout_buf >= 0 ? bufs_[static_cast<size_t>(tp.gout_buf)].ptr : nullptr;
       // the kernel-timing run serialises the streams so per-launch event spans are exact
       launched = S.backward(A, tok, in, gin, gout, wss_[static_cast<size_t>(si)], cs,
-                            ktimer_.enabled ? SideStream{} : sides_[static_cast<size_t>(si)], &rc);
+                            ktimer_.enabled ? SideStream{} : sides_[static_cast<size_t>(si)], &rc, klen);
     }
     stats.kernels_launched += launched;
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));
@@ -561,7 +569,24 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
   exec_comm(pos);
 }
 
+// key padding: each sequence's valid length = position of its first pad token (>= 1)
+void Engine::set_lengths(const int32_t* h_in) {
+  if (!h_lens_) return;
+  for (int j = 0; j < M_; ++j)
+    for (int b = 0; b < dm.B; ++b) {
+      const int32_t* sq = h_in + static_cast<size_t>(j) * dm.T + static_cast<size_t>(b) * dm.S;
+      int len = dm.S;
+      for (int p = 0; p < dm.S; ++p)
+        if (sq[p] == dm.pad_token) {
+          len = p;
+          break;
+        }
+      h_lens_[static_cast<size_t>(j) * dm.B + b] = std::max(1, len);
+    }
+}
+
 void Engine::stage_tokens(const int32_t* h_in, const int32_t* h_lab) {
+  set_lengths(h_in);
   const size_t n = static_cast<size_t>(M_) * static_cast<size_t>(dm.T) * sizeof(int32_t);
   CUDA_OK(cudaMemcpy(d_inputs_, h_in, n, cudaMemcpyHostToDevice));
   CUDA_OK(cudaMemcpy(d_labels_, h_lab, n, cudaMemcpyHostToDevice));
@@ -578,6 +603,9 @@ void Engine::issue(int max_window, bool resident, const int32_t* h_in, const int
   issued_.assign(static_cast<size_t>(N), 0);
   tok_loader_.assign(static_cast<size_t>(W_), -1);
   CUDA_OK(cudaMemsetAsync(d_ver_, 0, static_cast<size_t>(depth_ * P_) * sizeof(int), cs_));
+  if (d_lens_)  // the sequences' valid lengths (host-computed in run(), pinned: capturable)
+    CUDA_OK(cudaMemcpyAsync(d_lens_, h_lens_, static_cast<size_t>(M_) * dm.B * sizeof(int32_t), cudaMemcpyHostToDevice,
+                            cs_));
   CUDA_OK(cudaMemsetAsync(d_loss_, 0, static_cast<size_t>(M_) * sizeof(float), cs_));
   CUDA_OK(cudaMemsetAsync(d_trace_, 0xff, g.tasks.size() * sizeof(int), cs_));
   std::vector<int> loaded(static_cast<size_t>(W_), resident ? 1 : 0), last_left(static_cast<size_t>(W_), 0);
@@ -621,6 +649,7 @@ void Engine::run(const int32_t* h_in, const int32_t* h_lab, float* losses_out, i
   // loss = mean over the minibatch's labelled tokens (all of them for GPT; the masked
   // positions for MLM), so the CE gradient and the reported loss use 1 / count
   loss_scale_.assign(static_cast<size_t>(M_), 1.f / static_cast<float>(dm.T));
+  if (h_in) set_lengths(h_in);  // resident runs keep the lengths stage_tokens() set
   if (h_lab)
     for (int j = 0; j < M_; ++j) {
       int64_t cnt = 0;

@@ -260,6 +260,9 @@ class Engine {
   void plan_streams();
   void wait_stage_tasks(int pos, cudaStream_t st);  // st waits for stage's earlier tasks
   int32_t *d_inputs_ = nullptr, *d_labels_ = nullptr;
+  // key padding (dm.pad_token): valid length per (minibatch, sequence), pinned host -> device
+  int32_t *d_lens_ = nullptr, *h_lens_ = nullptr;
+  void set_lengths(const int32_t* h_in);
   float* d_loss_ = nullptr;
   int *d_ver_ = nullptr, *d_trace_ = nullptr;
   std::vector<cudaEvent_t> ev_start_, ev_end_;

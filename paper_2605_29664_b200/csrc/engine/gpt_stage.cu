@@ -276,10 +276,10 @@ std::vector<std::pair<int64_t, int64_t>> GptStage::segments() const {
 
 int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
                       const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* wsb,
-                      cudaStream_t s, int* rc, const cudaEvent_t* seg_ready) const {
+                      cudaStream_t s, int* rc, const cudaEvent_t* seg_ready, const int32_t* key_len) const {
   if (d_.fp32)
     return forward_f32(a, tokens, labels, reinterpret_cast<const float*>(in), reinterpret_cast<float*>(out), loss_sum,
-                       loss_scale, wsb, s, rc, seg_ready);
+                       loss_scale, wsb, s, rc, seg_ready, key_len);
   int seg = 0;  // next segment to wait for
   auto wait_seg = [&]() {
     if (seg_ready) cudaStreamWaitEvent(s, seg_ready[seg], 0);
@@ -308,7 +308,7 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
                                 A.ln1_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm_t(kt, T, 3 * h, h, A.ln1, h, false, w + P.qkv.off, h, false, A.qkv, 3 * h,
                   AMDP_EPI_STORE_BF16, s), 1);
-    AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, st), 1);
+    AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, key_len, st), 1);
     AMDP_GEMM(gemm_t(kt, T, h, h, A.o, h, false, w + P.o.off, h, false, A.hmid, h, AMDP_EPI_RESIDUAL, s, x, h), 1);
     AMDP_TRY(K_LAYERNORM, 0, 4.0 * T * h, amdp_layernorm_fwd(A.hmid, master + P.ln2_g.off, master + P.ln2_b.off, A.ln2, A.ln2_mean,
                                 A.ln2_rstd, T, h, d_.ln_eps, st), 1);
@@ -337,10 +337,11 @@ int GptStage::forward(const SlotActs& a, const int32_t* tokens, const int32_t* l
 // 256x256 pair tiles on 148 SMs).  Events order every hand-off; the task ends with `s`
 // joined to `side`, so slot activations and gradient buffers are quiescent afterwards.
 int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in, const uint16_t* gin,
-                       uint16_t* gout, uint8_t* wsb, cudaStream_t s, const SideStream& ss, int* rc) const {
+                       uint16_t* gout, uint8_t* wsb, cudaStream_t s, const SideStream& ss, int* rc,
+                       const int32_t* key_len) const {
   if (d_.fp32)
     return backward_f32(a, tokens, reinterpret_cast<const float*>(in), reinterpret_cast<const float*>(gin),
-                        reinterpret_cast<float*>(gout), wsb, s, rc);
+                        reinterpret_cast<float*>(gout), wsb, s, rc, key_len);
   int launched = 0;
   *rc = 0;
   auto st = reinterpret_cast<amdp_stream_t>(s);
@@ -402,7 +403,7 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     // previous reader (the layer above's) finished before F_DH, waited for above
     if (d_.recompute)
       AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_attention_fwd(A.qkv, A.o, A.lse, d_.B, d_.S, d_.heads, d_.hd,
-                                                                   d_.causal ? 1 : 0, st), 1);
+                                                                   d_.causal ? 1 : 0, key_len, st), 1);
     hand(ss.ev[E_DH], s, sd);
     // hmid = x + o Wo^T
     AMDP_GEMM(gemm_t(kt, h, h, T, ws.dhmid, h, true, A.o, h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, sd), 1);
@@ -419,10 +420,10 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DQ], 0);  // previous layer's dWqkv done with dqkv
     if (fuse_delta) {
       AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd_delta(A.qkv, ws.dtmp, A.lse, ws.attn, ws.dqkv, d_.B, d_.S,
-                                  d_.heads, d_.hd, d_.causal ? 1 : 0, st), 2);
+                                  d_.heads, d_.hd, d_.causal ? 1 : 0, key_len, st), 2);
     } else {
       AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
-                                  d_.causal ? 1 : 0, st), 3);
+                                  d_.causal ? 1 : 0, key_len, st), 3);
     }
     hand(ss.ev[E_DQ], s, sd);
     // qkv = ln1 Wqkv^T
@@ -464,7 +465,7 @@ inline const float* F(const uint16_t* p) { return reinterpret_cast<const float*>
 
 int GptStage::forward_f32(const SlotActs& a, const int32_t* tokens, const int32_t* labels, const float* in,
                           float* out, float* loss_sum, float loss_scale, uint8_t* wsb, cudaStream_t s, int* rc,
-                          const cudaEvent_t* seg_ready) const {
+                          const cudaEvent_t* seg_ready, const int32_t* key_len) const {
   int seg = 0;
   auto wait_seg = [&]() {
     if (seg_ready) cudaStreamWaitEvent(s, seg_ready[seg], 0);
@@ -490,7 +491,7 @@ int GptStage::forward_f32(const SlotActs& a, const int32_t* tokens, const int32_
                                                                 A.ln1_rstd, T, h, d_.ln_eps, st), 1);
     AMDP_GEMM(gemm32(kt, T, 3 * h, h, F(A.ln1), h, false, W + P.qkv.off, h, false, F(A.qkv), 3 * h, AMDP_EPI_STORE_F32, s), 1);
     AMDP_TRY(K_ATTN_FWD, attn_fwd_flops(), 0, amdp_f32_attention_fwd(F(A.qkv), F(A.o), A.lse, d_.B, d_.S, d_.heads, d_.hd,
-                                                                     d_.causal ? 1 : 0, st), 1);
+                                                                     d_.causal ? 1 : 0, key_len, st), 1);
     AMDP_GEMM(gemm32(kt, T, h, h, F(A.o), h, false, W + P.o.off, h, false, F(A.hmid), h, AMDP_EPI_RESIDUAL, s, x, h), 1);
     AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_f32_layernorm_fwd(F(A.hmid), W + P.ln2_g.off, W + P.ln2_b.off, F(A.ln2),
                                                                 A.ln2_mean, A.ln2_rstd, T, h, d_.ln_eps, st), 1);
@@ -515,7 +516,7 @@ int GptStage::forward_f32(const SlotActs& a, const int32_t* tokens, const int32_
 }
 
 int GptStage::backward_f32(const SlotActs& a, const int32_t* tokens, const float* in, const float* gin, float* gout,
-                           uint8_t* wsb, cudaStream_t s, int* rc) const {
+                           uint8_t* wsb, cudaStream_t s, int* rc, const int32_t* key_len) const {
   int launched = 0;
   *rc = 0;
   auto st = reinterpret_cast<amdp_stream_t>(s);
@@ -547,7 +548,7 @@ int GptStage::backward_f32(const SlotActs& a, const int32_t* tokens, const float
     AMDP_GEMM(gemm32(kt, h, h, T, dh, h, true, F(A.o), h, true, grad + P.o.off, h, AMDP_EPI_ACCUM_F32, s), 1);
     AMDP_GEMM(gemm32(kt, T, h, h, dh, h, false, W + P.o.off, h, true, dtmp, h, AMDP_EPI_STORE_F32, s), 1);
     AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_f32_attention_bwd(F(A.qkv), F(A.o), dtmp, A.lse, dqkv, ws.attn, d_.B,
-                                                                           d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, st), 3);
+                                                                           d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, key_len, st), 3);
     // qkv = ln1 Wqkv^T
     AMDP_GEMM(gemm32(kt, 3 * h, h, T, dqkv, 3 * h, true, F(A.ln1), h, true, grad + P.qkv.off, h, AMDP_EPI_ACCUM_F32, s), 1);
     AMDP_GEMM(gemm32(kt, T, h, 3 * h, dqkv, 3 * h, false, W + P.qkv.off, h, true, dtmp, h, AMDP_EPI_STORE_F32, s), 1);

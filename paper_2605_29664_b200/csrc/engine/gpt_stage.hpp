@@ -33,6 +33,7 @@ struct Dims {
   float ln_eps;
   bool recompute = false;  // f and o recomputed in the backward (amdp_model_config.recompute)
   bool fp32 = false;       // fp32 validation mode: activations fp32, amdp_f32_* kernels
+  int pad_token = 0;       // > 0: key padding of bidirectional models (amdp_model_config)
   size_t act_bytes() const { return fp32 ? 4 : 2; }  // per activation element
 };
 
@@ -106,20 +107,23 @@ class GptStage {
   // stream overlaps the layers already updated).
   int forward(const SlotActs& a, const int32_t* tokens, const int32_t* labels,
               const uint16_t* in, uint16_t* out, float* loss_sum, float loss_scale, uint8_t* ws,
-              cudaStream_t s, int* rc, const cudaEvent_t* seg_ready = nullptr) const;
+              cudaStream_t s, int* rc, const cudaEvent_t* seg_ready = nullptr,
+              const int32_t* key_len = nullptr) const;
   // The stage's parameters as contiguous (offset, numel) segments in the order the forward
   // reads them: [embeddings (stage 0)], one per layer, [final LayerNorm + head (last stage)].
   std::vector<std::pair<int64_t, int64_t>> segments() const;
+  // key_len: [seqs_per_minibatch] valid keys per sequence (key padding, bidirectional
+  // models), device memory, or null
   int backward(const SlotActs& a, const int32_t* tokens, const uint16_t* in,
                const uint16_t* gin, uint16_t* gout, uint8_t* ws, cudaStream_t s,
-               const SideStream& side, int* rc) const;
+               const SideStream& side, int* rc, const int32_t* key_len = nullptr) const;
   // fp32 validation mode bodies (gpt_stage_f32.cu): the same math on float tensors (the
   // activation pointers then address fp32 data), weights read from `master`
   int forward_f32(const SlotActs& a, const int32_t* tokens, const int32_t* labels, const float* in,
                   float* out, float* loss_sum, float loss_scale, uint8_t* ws, cudaStream_t s, int* rc,
-                  const cudaEvent_t* seg_ready) const;
+                  const cudaEvent_t* seg_ready, const int32_t* key_len) const;
   int backward_f32(const SlotActs& a, const int32_t* tokens, const float* in, const float* gin,
-                   float* gout, uint8_t* ws, cudaStream_t s, int* rc) const;
+                   float* gout, uint8_t* ws, cudaStream_t s, int* rc, const int32_t* key_len) const;
 
  private:
   Dims d_;

@@ -97,6 +97,8 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   dm.ln_eps = mc.ln_eps > 0 ? mc.ln_eps : 1e-5f;
   dm.recompute = mc.recompute != 0;
   dm.fp32 = mc.fp32_validation != 0;
+  dm.pad_token = dm.causal ? 0 : std::max(0, mc.pad_token);
+  if (mc.pad_token > 0 && dm.causal) throw std::invalid_argument("engine: pad_token is for bidirectional models");
   if (dm.fp32 && dm.recompute) throw std::invalid_argument("engine: fp32 validation mode stores every activation (no recompute)");
   if (dm.h % dm.heads != 0) throw std::invalid_argument("engine: hidden must divide into heads");
 

@@ -85,7 +85,8 @@ template <int D>
 __global__ void __launch_bounds__(128) attn_fwd_kernel(const bf16* __restrict__ qkv,
                                                        bf16* __restrict__ out,
                                                        float* __restrict__ lse, int seq, int H,
-                                                       float scale_log2, int causal) {
+                                                       float scale_log2, int causal,
+                                                       const int32_t* __restrict__ key_len) {
   constexpr int BQ = 64, BKV = 64, LDS = D + 8;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const bf16* __restrict__ 
   const bf16* gK = base + H * D + h * D;
   const bf16* gV = base + 2 * H * D + h * D;
   const int nkb = causal ? qb + 1 : seq / BKV;
+  const int klen = key_len ? key_len[b] : seq;  // key padding (bidirectional models)
 
   load_tile<D>(sQ, gQ, ld, BQ);
   load_tile<D>(sK, gK, ld, BKV);
@@ -142,18 +144,20 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const bf16* __restrict__ 
         mma16816(s[j], qf[d], r[0], r[1]);
         mma16816(s[j + 1], qf[d], r[2], r[3]);
       }
-    // scale (log2 domain) + causal mask on the diagonal block
+    // scale (log2 domain) + causal mask on the diagonal block, key-padding mask
     const bool diag = causal && kb == qb;
+    const bool lim = (kb + 1) * BKV > klen;
 #pragma unroll
     for (int j = 0; j < BKV / 8; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         float v = s[j][e] * scale_log2;
+        const int key = kb * BKV + j * 8 + 2 * t + (e & 1);
         if (diag) {
-          const int key = kb * BKV + j * 8 + 2 * t + (e & 1);
           const int qrow = q_row0 + ((e >> 1) << 3);
           if (key > qrow) v = -INFINITY;
         }
+        if (lim && key >= klen) v = -INFINITY;
         s[j][e] = v;
       }
     float mx0 = m0, mx1 = m1;
@@ -296,7 +300,7 @@ template <int D>
 __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
     const bf16* __restrict__ qkv, const bf16* __restrict__ dout, const float* __restrict__ lse,
     const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int H, float scale_log2,
-    float scale, int causal) {
+    float scale, int causal, const int32_t* __restrict__ key_len) {
   constexpr int BQ = 64, BKV = 64, LDS = D + 8;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
@@ -362,16 +366,16 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(
       }
     }
     const bool diag = causal && kb == qb;
+    const int klen = key_len ? key_len[b] : seq;
 #pragma unroll
     for (int j = 0; j < BKV / 8; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const bool hi = e >> 1;
         float p = exp2f(s[j][e] * scale_log2 - (hi ? lse1 : lse0));
-        if (diag) {
-          const int key = kb * BKV + j * 8 + 2 * t + (e & 1);
-          if (key > q_row0 + (hi ? 8 : 0)) p = 0.f;
-        }
+        const int key = kb * BKV + j * 8 + 2 * t + (e & 1);
+        if (diag && key > q_row0 + (hi ? 8 : 0)) p = 0.f;
+        if (key >= klen) p = 0.f;
         s[j][e] = p * (dp[j][e] - (hi ? dl1 : dl0));  // dS
       }
 #pragma unroll
@@ -405,7 +409,7 @@ template <int D, int BQ>
 __global__ void __launch_bounds__(128) attn_bwd_dkdv_kernel(
     const bf16* __restrict__ qkv, const bf16* __restrict__ dout, const float* __restrict__ lse,
     const float* __restrict__ delta, bf16* __restrict__ dqkv, int seq, int H, float scale_log2,
-    float scale, int causal) {
+    float scale, int causal, const int32_t* __restrict__ key_len) {
   constexpr int BKV = 64, LDS = D + 8;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   bf16* sK = reinterpret_cast<bf16*>(smem_raw);
@@ -491,6 +495,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dkdv_kernel(
         const int key = key0 + ((e >> 1) << 3);
         float p = exp2f(s[j][e] * scale_log2 - l_s[qc]);
         if (causal && qb * BQ + qc < key) p = 0.f;
+        if (key_len && key >= key_len[b]) p = 0.f;  // a padding key
         s[j][e] = p;
         dp[j][e] = p * (dp[j][e] - d_s[qc]);
       }
@@ -534,18 +539,18 @@ __global__ void __launch_bounds__(128) attn_bwd_dkdv_kernel(
 
 template <int D>
 int launch_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int causal,
-               cudaStream_t st) {
+               const int32_t* key_len, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(5) * 64 * (D + 8) * sizeof(bf16);
   auto k = attn_fwd_kernel<D>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(D));
-  k<<<dim3(S / 64, H, B), 128, smem, st>>>(qkv, out, lse, S, H, scale_log2, causal);
+  k<<<dim3(S / 64, H, B), 128, smem, st>>>(qkv, out, lse, S, H, scale_log2, causal, key_len);
   return cudaGetLastError();
 }
 
 template <int D>
 int launch_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* lse,
-               bf16* dqkv, float* delta, int B, int S, int H, int causal, cudaStream_t st) {
+               bf16* dqkv, float* delta, int B, int S, int H, int causal, const int32_t* key_len, cudaStream_t st) {
   const int ntok = B * S;
   attn_bwd_delta_kernel<<<(ntok * H + 7) / 8, 256, 0, st>>>(out, dout, delta, ntok, S, H, D);
   const float scale = 1.f / sqrtf(static_cast<float>(D));
@@ -555,7 +560,7 @@ int launch_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* 
     auto k = attn_bwd_dq_kernel<D>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k<<<dim3(S / 64, H, B), 128, smem, st>>>(qkv, dout, lse, delta, dqkv, S, H, scale_log2, scale,
-                                             causal);
+                                             causal, key_len);
   }
   {
     constexpr int BQ = D > 64 ? 32 : 64;
@@ -564,7 +569,7 @@ int launch_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* 
     auto k = attn_bwd_dkdv_kernel<D, BQ>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k<<<dim3(S / 64, H, B), 128, smem, st>>>(qkv, dout, lse, delta, dqkv, S, H, scale_log2,
-                                             scale, causal);
+                                             scale, causal, key_len);
   }
   return cudaGetLastError();
 }
@@ -574,39 +579,41 @@ int launch_bwd(const bf16* qkv, const bf16* out, const bf16* dout, const float* 
 
 namespace amdp {
 int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int D, int causal,
-                     cudaStream_t st);
+                     const int32_t* key_len, cudaStream_t st);
 int attention_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
-                     int S, int H, int D, int causal, cudaStream_t st);
+                     int S, int H, int D, int causal, const int32_t* key_len, cudaStream_t st);
 }
 
 using namespace amdp;
 
 extern "C" int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse, int batch,
-                                  int seq, int heads, int head_dim, int causal,
+                                  int seq, int heads, int head_dim, int causal, const int32_t* key_len,
                                   amdp_stream_t stream) {
   if (batch <= 0 || seq <= 0 || seq % 64 != 0 || heads <= 0) return AMDP_ERR_INVALID;
+  if (causal && key_len) return AMDP_ERR_UNSUPPORTED;  // key padding is for bidirectional models
   auto q = reinterpret_cast<const bf16*>(qkv);
   auto o = reinterpret_cast<bf16*>(out);
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if ((head_dim == 64 || head_dim == 80 || head_dim == 128) && seq % 256 == 0)  // tcgen05 path
-    return attention_fwd_tc(q, o, lse, batch, seq, heads, head_dim, causal, s);
+    return attention_fwd_tc(q, o, lse, batch, seq, heads, head_dim, causal, key_len, s);
   switch (head_dim) {
-    case 32: return launch_fwd<32>(q, o, lse, batch, seq, heads, causal, s);
-    case 64: return launch_fwd<64>(q, o, lse, batch, seq, heads, causal, s);
-    case 80: return launch_fwd<80>(q, o, lse, batch, seq, heads, causal, s);
-    case 128: return launch_fwd<128>(q, o, lse, batch, seq, heads, causal, s);
+    case 32: return launch_fwd<32>(q, o, lse, batch, seq, heads, causal, key_len, s);
+    case 64: return launch_fwd<64>(q, o, lse, batch, seq, heads, causal, key_len, s);
+    case 80: return launch_fwd<80>(q, o, lse, batch, seq, heads, causal, key_len, s);
+    case 128: return launch_fwd<128>(q, o, lse, batch, seq, heads, causal, key_len, s);
   }
   return AMDP_ERR_UNSUPPORTED;
 }
 
 extern "C" int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse,
                                         const float* delta, uint16_t* dqkv, int batch, int seq, int heads,
-                                        int head_dim, int causal, amdp_stream_t stream) {
+                                        int head_dim, int causal, const int32_t* key_len, amdp_stream_t stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || !delta) return AMDP_ERR_INVALID;
+  if (causal && key_len) return AMDP_ERR_UNSUPPORTED;
   if (!amdp_attention_bwd_delta_supported(seq, head_dim)) return AMDP_ERR_UNSUPPORTED;
   return attention_bwd_tc(reinterpret_cast<const bf16*>(qkv), reinterpret_cast<const bf16*>(dout), lse,
                           const_cast<float*>(delta), reinterpret_cast<bf16*>(dqkv), batch, seq, heads, head_dim,
-                          causal, reinterpret_cast<cudaStream_t>(stream));
+                          causal, key_len, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int amdp_attention_impl(int seq, int head_dim, int backward) {
@@ -628,9 +635,10 @@ extern "C" size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, in
 
 extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                                   const float* lse, uint16_t* dqkv, void* workspace, int batch,
-                                  int seq, int heads, int head_dim, int causal,
+                                  int seq, int heads, int head_dim, int causal, const int32_t* key_len,
                                   amdp_stream_t stream) {
   if (batch <= 0 || seq <= 0 || seq % 64 != 0 || heads <= 0 || !workspace) return AMDP_ERR_INVALID;
+  if (causal && key_len) return AMDP_ERR_UNSUPPORTED;
   auto q = reinterpret_cast<const bf16*>(qkv);
   auto o = reinterpret_cast<const bf16*>(out);
   auto d = reinterpret_cast<const bf16*>(dout);
@@ -649,13 +657,13 @@ extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, cons
     } else {
       launch_pdl(attn_bwd_delta_vec_kernel, dim3(static_cast<int>(blocks)), dim3(256), 0, s, o, d, w, ntok, seq, heads, head_dim);
     }
-    return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, s);
+    return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, key_len, s);
   }
   switch (head_dim) {
-    case 32: return launch_bwd<32>(q, o, d, lse, dq, w, batch, seq, heads, causal, s);
-    case 64: return launch_bwd<64>(q, o, d, lse, dq, w, batch, seq, heads, causal, s);
-    case 80: return launch_bwd<80>(q, o, d, lse, dq, w, batch, seq, heads, causal, s);
-    case 128: return launch_bwd<128>(q, o, d, lse, dq, w, batch, seq, heads, causal, s);
+    case 32: return launch_bwd<32>(q, o, d, lse, dq, w, batch, seq, heads, causal, key_len, s);
+    case 64: return launch_bwd<64>(q, o, d, lse, dq, w, batch, seq, heads, causal, key_len, s);
+    case 80: return launch_bwd<80>(q, o, d, lse, dq, w, batch, seq, heads, causal, key_len, s);
+    case 128: return launch_bwd<128>(q, o, d, lse, dq, w, batch, seq, heads, causal, key_len, s);
   }
   return AMDP_ERR_UNSUPPORTED;
 }

@@ -121,7 +121,8 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap kv_map, const __grid_constant__ CUtensorMap qkv_map,
                        const __grid_constant__ CUtensorMap do_map, const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
-                       int seq, int H, int n_kt, int BH, float scale_log2, float scale, int causal) {
+                       int seq, int H, int n_kt, int BH, float scale_log2, float scale, int causal,
+                       const int32_t* __restrict__ key_len) {
   using L = KvSmem<D>;
   constexpr int NU = L::NU;
   extern __shared__ uint8_t smem_raw[];
@@ -297,6 +298,7 @@ __global__ void __launch_bounds__(384, 1)
     Tile t;
     for (int it = 0, g0 = 0; tile_of(it, t); g0 += 2 * t.N, ++it) {
       const int key = t.kt * 128 + r;
+      const bool kpad = key_len && key >= key_len[t.b];  // a padding key: no P, no dS
       const float* lse_bh = lse + (static_cast<size_t>(t.b) * H + t.h) * seq;
       const float* del_bh = delta + (static_cast<size_t>(t.b) * H + t.h) * seq;
       for (int n = 0; n < t.N; ++n) {
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(384, 1)
             if (qbase + cc + 2 < key) p1.x = 0.f;
             if (qbase + cc + 3 < key) p1.y = 0.f;
           }
+          if (kpad) p0 = p1 = make_float2(0.f, 0.f);
           const float2 g0 = __fmul2_rn(
               __fadd2_rn(make_float2(__uint_as_float(d[cc]), __uint_as_float(d[cc + 1])), make_float2(-dq.x, -dq.y)), p0);
           const float2 g1 = __fmul2_rn(
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(384, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap qkv_map, const __grid_constant__ CUtensorMap do_map,
                      const bf16* __restrict__ qkv, const float* __restrict__ lse, const float* __restrict__ delta,
                      bf16* __restrict__ dqkv, int seq, int H, int n_qt, int BH, float scale_log2, float scale,
-                     int causal, int early) {
+                     int causal, int early, const int32_t* __restrict__ key_len) {
   using L = QSmem<D>;
   constexpr int NSK = L::NSK, NSV = L::NSV;
   extern __shared__ uint8_t smem_raw[];
@@ -608,9 +611,11 @@ __global__ void __launch_bounds__(384, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(q_full);
       }
+      const int klen = key_len ? key_len[b] : seq;  // key padding (bidirectional models)
       for (int n = 0; n < N; ++n) {
         const int g = g0 + n;
         const bool diag = causal && n == N - 1;
+        const bool lim = (n + 1) * 128 > klen;
         ptx::mbar_wait(s_full, g & 1);
         if (it == 0 && lane == 0 && q == 0 && wg == 0) BW_T(3, n);
         ptx::tc_fence_after();
@@ -635,6 +640,10 @@ __global__ void __launch_bounds__(384, 1)
             const int k0 = n * 128 + c0 + cc;
             if (k0 > qrow) g0f = 0.f;
             if (k0 + 1 > qrow) g1f = 0.f;
+          } else if (lim) {
+            const int k0 = n * 128 + c0 + cc;
+            if (k0 >= klen) g0f = 0.f;
+            if (k0 + 1 >= klen) g1f = 0.f;
           }
           gg[cc >> 1] = pack2(g0f, g1f);
         }
@@ -677,7 +686,7 @@ int set_smem(K k, size_t bytes) {
 
 template <int D>
 int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
-                  int S, int H, int causal, cudaStream_t st) {
+                  int S, int H, int causal, const int32_t* key_len, cudaStream_t st) {
   CUtensorMap q128, o128, q64, o64;
   const uint64_t ldq = static_cast<uint64_t>(3) * H * D, ldo = static_cast<uint64_t>(H) * D;
   const uint64_t rows = static_cast<uint64_t>(B) * S;
@@ -699,12 +708,12 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   const int nt = S / 128;
   const int kv_grid = std::min(nt * H * B, num_sms());  // persistent
   cudaError_t e = launch_pdl(fa_bwd_dkdv_kernel<D>, dim3(kv_grid), dim3(384), smem_kv, st, q128, q64, o64, lse,
-                             delta, dqkv, S, H, nt, H * B, scale_log2, scale, causal);
+                             delta, dqkv, S, H, nt, H * B, scale_log2, scale, causal, key_len);
   if (e != cudaSuccess) return e;
   const int dq_grid = std::min(nt * H * B, num_sms());  // persistent
   static const int early = getenv("AMDP_ATTN_DQ_EARLY") ? atoi(getenv("AMDP_ATTN_DQ_EARLY")) : 1;
   e = launch_pdl(fa_bwd_dq_kernel<D>, dim3(dq_grid), dim3(384), smem_q, st, q128, o128, qkv, lse, delta, dqkv, S, H,
-                 nt, H * B, scale_log2, scale, causal, early);
+                 nt, H * B, scale_log2, scale, causal, early, key_len);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -712,11 +721,11 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
 
 // Used by amdp_attention_bwd (after the delta pre-pass) when the tensor-core path applies.
 int attention_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
-                     int S, int H, int D, int causal, cudaStream_t st) {
+                     int S, int H, int D, int causal, const int32_t* key_len, cudaStream_t st) {
   if (S % 128 != 0) return AMDP_ERR_UNSUPPORTED;
-  if (D == 128) return launch_bwd_tc<128>(qkv, dout, lse, delta, dqkv, B, S, H, causal, st);
-  if (D == 64) return launch_bwd_tc<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, st);
-  if (D == 80) return launch_bwd_tc<80>(qkv, dout, lse, delta, dqkv, B, S, H, causal, st);
+  if (D == 128) return launch_bwd_tc<128>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, st);
+  if (D == 64) return launch_bwd_tc<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, st);
+  if (D == 80) return launch_bwd_tc<80>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, st);
   return AMDP_ERR_UNSUPPORTED;
 }
 

@@ -83,7 +83,9 @@ __device__ __forceinline__ float2 ex2_fma2(float2 x) {
 // P = 2^(S*scale - m) for one 128-column row held in registers, written as bf16 pairs over
 // the first 64 TMEM columns of the S tile; returns the row sum.  Packed f32x2 arithmetic and
 // one exponent pair in four on the FMA pipe keep issue slots and MUFU below the tensor time.
-template <bool DIAG>
+// MODE 0: every key; 1: causal diagonal block (key > qrow masked); 2: key padding (key >= qrow,
+// here the sequence's valid key count, masked).
+template <int MODE>
 __device__ __forceinline__ float softmax_p_row(const uint32_t (&v)[FA_BKV], float scale_log2, float nm, int kbase,
                                                int qrow, uint32_t ts) {
   const float2 sc = make_float2(scale_log2, scale_log2), sh = make_float2(nm, nm);
@@ -102,10 +104,14 @@ __device__ __forceinline__ float softmax_p_row(const uint32_t (&v)[FA_BKV], floa
         p.x = ex2(x.x);
         p.y = ex2(x.y);
       }
-      if (DIAG) {
+      if (MODE == 1) {
         const int k0 = kbase + c * 32 + e;
         if (k0 > qrow) p.x = 0.f;
         if (k0 + 1 > qrow) p.y = 0.f;
+      } else if (MODE == 2) {
+        const int k0 = kbase + c * 32 + e;
+        if (k0 >= qrow) p.x = 0.f;
+        if (k0 + 1 >= qrow) p.y = 0.f;
       }
       if ((e >> 1) & 1) acc1 = __fadd2_rn(acc1, p);
       else acc0 = __fadd2_rn(acc0, p);
@@ -148,7 +154,7 @@ template <int D>
 __global__ void __launch_bounds__(FA_THREADS, 1)
     fa_fwd_tc_kernel(const __grid_constant__ CUtensorMap qkv_map, bf16* __restrict__ out,
                      float* __restrict__ lse, int seq, int H, int BH, int n_qt, float scale_log2,
-                     int causal) {
+                     int causal, const int32_t* __restrict__ key_len) {
   using L = FaSmem<D>;
   constexpr int KVS = L::KVS;
   extern __shared__ uint8_t smem_raw[];
@@ -334,9 +340,11 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
       const FaTile T = fa_tile(idx, BH, H, n_qt, seq, causal);
       const int qrow = T.qp * FA_BQ + 128 * wg + r;
       const int nblk = wg == 0 ? T.last_a + 1 : T.nkv;
+      const int klen = key_len ? key_len[T.b] : seq;  // key padding (bidirectional models)
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < nblk; ++j) {
         const bool diag = causal && j == nblk - 1;
+        const bool lim = (j + 1) * FA_BKV > klen;  // keys >= klen in this block are padding
         ptx::mbar_wait(&s_full[wg], (nbase + j) & 1);  // also implies PV_wg(j-1) retired: O settled
         if (it == 0 && lane == 0 && q == 0) FA_T(5 + wg, j);
         ptx::tc_fence_after();
@@ -355,6 +363,10 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < FA_BKV; ++e)
               if (j * FA_BKV + e <= qrow) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(v[e]));
+          } else if (lim) {
+#pragma unroll
+            for (int e = 0; e < FA_BKV; ++e)
+              if (j * FA_BKV + e < klen) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(v[e]));
           } else {
 #pragma unroll
             for (int e = 0; e < FA_BKV; e += 16)
@@ -391,8 +403,9 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
           m_ref = m_new;
         }
         const float nm = -m_ref;
-        if (diag) l += softmax_p_row<true>(v, scale_log2, nm, j * FA_BKV, qrow, ts);
-        else l += softmax_p_row<false>(v, scale_log2, nm, j * FA_BKV, qrow, ts);
+        if (diag) l += softmax_p_row<1>(v, scale_log2, nm, j * FA_BKV, qrow, ts);
+        else if (lim) l += softmax_p_row<2>(v, scale_log2, nm, j * FA_BKV, klen, ts);
+        else l += softmax_p_row<0>(v, scale_log2, nm, j * FA_BKV, qrow, ts);
         if (it == 0 && lane == 0 && q == 0 && wg == 0) FA_T(13, j);
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
@@ -450,7 +463,8 @@ __global__ void __launch_bounds__(FA_THREADS, 1)
 }
 
 template <int D>
-int launch_fa_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int causal, cudaStream_t st) {
+int launch_fa_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int causal, const int32_t* key_len,
+                  cudaStream_t st) {
   CUtensorMap map;
   if (!tma_map_bf16_2d(&map, qkv, static_cast<uint64_t>(3) * H * D, static_cast<uint64_t>(B) * S,
                        static_cast<uint64_t>(3) * H * D, 64, 128))
@@ -469,7 +483,7 @@ int launch_fa_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, i
   const float scale_log2 = 1.4426950408889634f / sqrtf(static_cast<float>(D));
   const int grid = std::min(n_qt * H * B, num_sms());
   cudaError_t e = launch_pdl(k, dim3(grid), dim3(FA_THREADS), smem, st, map, out, lse, S, H, H * B, n_qt, scale_log2,
-                             causal);
+                             causal, key_len);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
@@ -477,11 +491,11 @@ int launch_fa_fwd(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, i
 
 // Used by amdp_attention_fwd when the tensor-core path applies (seq % 256 == 0).
 int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int D, int causal,
-                     cudaStream_t st) {
+                     const int32_t* key_len, cudaStream_t st) {
   if (S % FA_BQ != 0) return AMDP_ERR_UNSUPPORTED;
-  if (D == 128) return launch_fa_fwd<128>(qkv, out, lse, B, S, H, causal, st);
-  if (D == 64) return launch_fa_fwd<64>(qkv, out, lse, B, S, H, causal, st);
-  if (D == 80) return launch_fa_fwd<80>(qkv, out, lse, B, S, H, causal, st);
+  if (D == 128) return launch_fa_fwd<128>(qkv, out, lse, B, S, H, causal, key_len, st);
+  if (D == 64) return launch_fa_fwd<64>(qkv, out, lse, B, S, H, causal, key_len, st);
+  if (D == 80) return launch_fa_fwd<80>(qkv, out, lse, B, S, H, causal, key_len, st);
   return AMDP_ERR_UNSUPPORTED;
 }
 

@@ -170,6 +170,8 @@ struct Heads {
   const float* qkv;
   int S, H, D, causal;
   float scale;
+  const int32_t* key_len;  // per sequence valid key count (key padding), or null
+  __device__ int kend(int b, int qi) const { return causal ? qi + 1 : (key_len ? key_len[b] : S); }
   __device__ const float* q(int b, int s, int h) const { return qkv + (static_cast<size_t>(b) * S + s) * 3 * H * D + h * D; }
   __device__ const float* k(int b, int s, int h) const { return q(b, s, h) + H * D; }
   __device__ const float* v(int b, int s, int h) const { return q(b, s, h) + 2 * H * D; }
@@ -186,7 +188,7 @@ __global__ void f32_attn_fwd_kernel(Heads hd, float* __restrict__ o, float* __re
   if (gw >= B * H * S) return;
   const int qi = gw % S, h = (gw / S) % H, b = gw / (S * H);
   const float* q = hd.q(b, qi, h);
-  const int kend = hd.causal ? qi + 1 : S;
+  const int kend = hd.kend(b, qi);
   float m = -INFINITY;
   for (int k = 0; k < kend; ++k) m = fmaxf(m, hd.scale * dot_lanes(q, hd.k(b, k, h), D, lane));
   float l = 0.f, acc[FA_MAXV] = {0, 0, 0, 0};
@@ -229,7 +231,7 @@ __global__ void f32_attn_dq_kernel(Heads hd, const float* __restrict__ dout, con
   const int qi = gw % S, h = (gw / S) % H, b = gw / (S * H);
   const float* dO = dout + (static_cast<size_t>(b) * S + qi) * H * D + h * D;
   const float dl = delta[(static_cast<size_t>(b) * H + h) * S + qi];
-  const int kend = hd.causal ? qi + 1 : S;
+  const int kend = hd.kend(b, qi);
   float acc[FA_MAXV] = {0, 0, 0, 0};
   for (int k = 0; k < kend; ++k) {
     const float p = attn_p(hd, lse, b, h, qi, k, lane);
@@ -252,7 +254,8 @@ __global__ void f32_attn_dkdv_kernel(Heads hd, const float* __restrict__ dout, c
   if (gw >= B * H * S) return;
   const int ki = gw % S, h = (gw / S) % H, b = gw / (S * H);
   float dk[FA_MAXV] = {0, 0, 0, 0}, dv[FA_MAXV] = {0, 0, 0, 0};
-  for (int qi = hd.causal ? ki : 0; qi < S; ++qi) {
+  const bool pad = !hd.causal && hd.key_len && ki >= hd.key_len[b];  // a padding key: no gradient
+  for (int qi = hd.causal ? ki : 0; qi < S && !pad; ++qi) {
     const float p = attn_p(hd, lse, b, h, qi, ki, lane);
     const float* dO = dout + (static_cast<size_t>(b) * S + qi) * H * D + h * D;
     const float dl = delta[(static_cast<size_t>(b) * H + h) * S + qi];
@@ -398,9 +401,10 @@ extern "C" int amdp_f32_layernorm_bwd(const float* dy, const float* x, const flo
 }
 
 extern "C" int amdp_f32_attention_fwd(const float* qkv, float* out, float* lse, int batch, int seq, int heads,
-                                      int head_dim, int causal, amdp_stream_t stream) {
+                                      int head_dim, int causal, const int32_t* key_len, amdp_stream_t stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || head_dim <= 0 || head_dim > 32 * FA_MAXV) return AMDP_ERR_INVALID;
-  Heads hd{qkv, seq, heads, head_dim, causal, 1.f / sqrtf(static_cast<float>(head_dim))};
+  if (causal && key_len) return AMDP_ERR_UNSUPPORTED;
+  Heads hd{qkv, seq, heads, head_dim, causal, 1.f / sqrtf(static_cast<float>(head_dim)), key_len};
   f32_attn_fwd_kernel<<<warps_grid(static_cast<int64_t>(batch) * heads * seq), 256, 0,
                         reinterpret_cast<cudaStream_t>(stream)>>>(hd, out, lse, batch);
   return cudaGetLastError();
@@ -412,11 +416,12 @@ extern "C" size_t amdp_f32_attention_bwd_workspace(int batch, int seq, int heads
 
 extern "C" int amdp_f32_attention_bwd(const float* qkv, const float* out, const float* dout, const float* lse,
                                       float* dqkv, float* workspace, int batch, int seq, int heads, int head_dim,
-                                      int causal, amdp_stream_t stream) {
+                                      int causal, const int32_t* key_len, amdp_stream_t stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || head_dim <= 0 || head_dim > 32 * FA_MAXV || !workspace)
     return AMDP_ERR_INVALID;
+  if (causal && key_len) return AMDP_ERR_UNSUPPORTED;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Heads hd{qkv, seq, heads, head_dim, causal, 1.f / sqrtf(static_cast<float>(head_dim))};
+  Heads hd{qkv, seq, heads, head_dim, causal, 1.f / sqrtf(static_cast<float>(head_dim)), key_len};
   const int g = warps_grid(static_cast<int64_t>(batch) * heads * seq);
   f32_attn_delta_kernel<<<g, 256, 0, s>>>(out, dout, workspace, batch, seq, heads, head_dim);
   f32_attn_dq_kernel<<<g, 256, 0, s>>>(hd, dout, lse, workspace, dqkv, batch);

@@ -30,7 +30,7 @@ class _Model(Structure):
                 ("vocab", c_int), ("seq", c_int), ("seqs_per_minibatch", c_int),
                 ("causal", c_int), ("init_std", c_float), ("ln_eps", c_float),
                 ("seed", c_uint64), ("layers_per_stage", POINTER(c_int)), ("recompute", c_int),
-                ("fp32_validation", c_int)]
+                ("fp32_validation", c_int), ("pad_token", c_int)]
 
 
 class _Run(Structure):
@@ -105,6 +105,7 @@ class ModelConfig:
     layers_per_stage: Optional[List[int]] = None
     recompute: bool = False  # backward rebuilds f = gelu(u) and o = attention(qkv) (amdp_model_config)
     fp32_validation: bool = False  # every tensor / product fp32 on the CUDA cores (amdp_f32_* kernels)
+    pad_token: int = 0  # bidirectional models: token id (> 0) marking padding; 0 = no padding
 
     @property
     def tokens_per_minibatch(self) -> int:
@@ -141,7 +142,7 @@ class ModelConfig:
             lps = (c_int * len(self.layers_per_stage))(*self.layers_per_stage)
         m = _Model(self.layers, self.hidden, self.heads, self.ffn, self.vocab, self.seq,
                    self.seqs_per_minibatch, int(self.causal), self.init_std, self.ln_eps,
-                   self.seed, lps, int(self.recompute), int(self.fp32_validation))
+                   self.seed, lps, int(self.recompute), int(self.fp32_validation), int(self.pad_token))
         m._keep = lps
         return m
 

@@ -41,29 +41,29 @@ def gemm(A, B, *, M, N_, K, a_mn=False, b_mn=False, lda=None, ldb=None, C=None, 
     return C
 
 
-def attention_fwd(qkv, batch, seq, heads, head_dim, causal=True):
+def attention_fwd(qkv, batch, seq, heads, head_dim, causal=True, key_len=None):
     out = torch.empty(batch * seq, heads * head_dim, dtype=torch.bfloat16, device=qkv.device)
     lse = torch.empty(batch, heads, seq, dtype=torch.float32, device=qkv.device)
     N.check(N.lib.amdp_attention_fwd(_p(qkv), _p(out), _p(lse), batch, seq, heads, head_dim,
-                                     int(causal), _stream()), "amdp_attention_fwd")
+                                     int(causal), _p(key_len), _stream()), "amdp_attention_fwd")
     return out, lse
 
 
-def attention_bwd(qkv, out, dout, lse, batch, seq, heads, head_dim, causal=True):
+def attention_bwd(qkv, out, dout, lse, batch, seq, heads, head_dim, causal=True, key_len=None):
     dqkv = torch.empty_like(qkv)
     ws = torch.empty(N.lib.amdp_attention_bwd_workspace(batch, seq, heads, head_dim),
                      dtype=torch.uint8, device=qkv.device)
     N.check(N.lib.amdp_attention_bwd(_p(qkv), _p(out), _p(dout), _p(lse), _p(dqkv), _p(ws),
-                                     batch, seq, heads, head_dim, int(causal), _stream()),
+                                     batch, seq, heads, head_dim, int(causal), _p(key_len), _stream()),
             "amdp_attention_bwd")
     return dqkv
 
 
-def attention_bwd_delta(qkv, dout, lse, delta, batch, seq, heads, head_dim, causal=True):
+def attention_bwd_delta(qkv, dout, lse, delta, batch, seq, heads, head_dim, causal=True, key_len=None):
     """Backward with delta [batch][heads][seq] supplied (amdp_attention_bwd_delta)."""
     dqkv = torch.empty_like(qkv)
     N.check(N.lib.amdp_attention_bwd_delta(_p(qkv), _p(dout), _p(lse), _p(delta), _p(dqkv), batch, seq, heads,
-                                           head_dim, int(causal), _stream()), "amdp_attention_bwd_delta")
+                                           head_dim, int(causal), _p(key_len), _stream()), "amdp_attention_bwd_delta")
     return dqkv
 
 

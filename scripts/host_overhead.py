@@ -62,7 +62,7 @@ def main():
     lse = torch.empty(16 * 512, device="cuda")
     out["attention_fwd_s512"] = per_call(lambda: N.lib.amdp_attention_fwd(
         ctypes.c_void_p(qkv.data_ptr()), ctypes.c_void_p(o.data_ptr()), ctypes.c_void_p(lse.data_ptr()), 1, 512, 16, 64,
-        1, s), n=200)
+        1, None, s), n=200)
     ev = torch.cuda.Event()
     out["torch_event_record"] = per_call(lambda: ev.record())
     print(json.dumps({k: round(v, 2) for k, v in out.items()}))

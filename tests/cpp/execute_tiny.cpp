@@ -26,7 +26,7 @@ int main() {
 
   static const int parts[4] = {1, 1, 1, 1};
   ppsim::ExecuteOptions opt;
-  opt.model = amdp_model_config{4, 128, 4, 512, 1024, 64, 4, 1, 0.02f, 1e-5f, 1234, parts, 0, 0};
+  opt.model = amdp_model_config{4, 128, 4, 512, 1024, 64, 4, 1, 0.02f, 1e-5f, 1234, parts, 0, 0, 0};
   opt.optimizer = amdp_opt_args{AMDP_OPT_ADAMW, 1e-3f, 0.9f, 0.95f, 1e-8f, 0.f, 1e-8f, 1e6f, 1.f, 1};
   const int T = 4 * 64;
   std::vector<int32_t> inputs(static_cast<size_t>(cfg.num_minibatches) * T), labels(inputs.size());

@@ -29,20 +29,29 @@ def _golden_csv(cfg):
     raise KeyError(cfg)
 
 
-def test_tiny_bert_mlm_parity():
+@pytest.mark.parametrize("pad", [0, 7])
+def test_tiny_bert_mlm_parity(pad):
+    """pad > 0: every sequence is padded to a length in [S/2, S] with token id `pad`; keys at or
+    past the first pad are masked in attention (forward and backward) and padded positions
+    carry no label."""
     import gpt_oracle as O
     from paper_2605_29664_b200 import engine as E
 
     model = E.ModelConfig.tiny()
     model.causal = False
+    model.pad_token = pad
     model.layers_per_stage = [1, 1, 1, 1]
     opt = E.OptimizerConfig(kind=3, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8)
     run = E.RunConfig(depth=4, threshold=8, windows=4, optimizer=opt)
     eng = E.Engine(model, run)
     inputs, labels = E.synthetic_tokens(model, run.data_seed, 0, run.num_minibatches)
-    assert 0.1 < (labels >= 0).mean() < 0.2
+    oin, olab = O.synthetic_tokens(64, 4, 1024, run.data_seed, 0, run.num_minibatches, False, pad)
+    assert np.array_equal(inputs, oin) and np.array_equal(labels, olab)
+    assert (0.1 if pad == 0 else 0.05) < (labels >= 0).mean() < 0.2
+    if pad:
+        assert (inputs == pad).any() and ((inputs == pad) <= (labels < 0)).all()
     losses = eng.run(inputs, labels)
-    om = O.Model(4, 128, 4, 512, 1024, 64, 4, False, model.seed)
+    om = O.Model(4, 128, 4, 512, 1024, 64, 4, False, model.seed, pad_token=pad)
     trace = _golden_csv(["AMDP", 4, 4, "1", "1", "0", "0", 2, 2, 8, 32, 1])
     ol, _, seen = O.replay(trace, om, [1, 1, 1, 1], O.Opt("adamw", 1e-3, 0.9, 0.95, 1e-8, 0.0), 8, inputs,
                            labels)

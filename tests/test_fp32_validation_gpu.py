@@ -34,7 +34,9 @@ MODELS = {
     # name: (layers, hidden, heads, ffn, vocab, seq)
     "tiny": (4, 128, 4, 512, 1024, 64),
     "hd64": (4, 512, 8, 2048, 2048, 256),
+    "bert_pad": (4, 128, 4, 512, 1024, 64),  # bidirectional MLM, padded sequences (pad id 7)
 }
+PAD = {"bert_pad": 7}
 OPTS = {
     "adamw": (3, dict(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8), ("adamw", 1e-3, 0.9, 0.95, 1e-8, 0.0)),
     "adamtype": (2, dict(lr=2e-4, beta1=0.9, beta2=0.999, eps=1e-3), ("adamtype", 2e-4, 0.9, 0.999, 1e-3, 0.0)),
@@ -44,6 +46,7 @@ CASES = {
     "tiny_preload1_zero_adamw": ("tiny", 8, 3, 1, True, "adamw"),
     "tiny_preload2_replicated_adamtype": ("tiny", 8, 3, 2, False, "adamtype"),
     "hd64_preload1_zero_adamw": ("hd64", 8, 3, 1, True, "adamw"),
+    "bert_pad_preload1_zero_adamw": ("bert_pad", 8, 3, 1, True, "adamw"),
 }
 
 
@@ -62,7 +65,8 @@ def f32_run(request):
     from paper_2605_29664_b200 import engine as E
     mname, thr, windows, bwd, zero, oname = CASES[request.param]
     L, h, H, f, V, S = MODELS[mname]
-    model = E.ModelConfig(L, h, H, f, V, S)
+    pad = PAD.get(mname, 0)
+    model = E.ModelConfig(L, h, H, f, V, S, causal=not pad, pad_token=pad)
     model.layers_per_stage = [1, 1, 1, 1]
     model.fp32_validation = True
     kind, kw, okw = OPTS[oname]
@@ -74,7 +78,7 @@ def f32_run(request):
     losses = eng.run(inputs, labels)
     final = [eng.stage_params(i) for i in range(4)]
     trace = _golden_csv(["AMDP", 4, 4, "1", str(bwd), "0", "0", 2, 2, thr, thr * windows, int(zero)])
-    om = O.Model(L, h, H, f, V, S, 4, True, model.seed)
+    om = O.Model(L, h, H, f, V, S, 4, not pad, model.seed, pad_token=pad)
     ol, omaster, seen = O.replay(trace, om, [1, 1, 1, 1], O.Opt(*okw), thr, inputs, labels, emulate_bf16=False)
     out = dict(eng=eng, init=init, final=final, losses=losses, ol=ol, omaster=omaster, seen=seen, O=O)
     yield out

@@ -161,12 +161,15 @@ def test_recompute_gelu_bit_identical_to_epilogue(K, N, shape):
     assert _rel(f_re, _gelu(u.float())) < 1e-2
 
 
-def _attn_ref(qkv, B, S, H, D, causal):
+def _attn_ref(qkv, B, S, H, D, causal, key_len=None):
     q, k, v = qkv.float().view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
     s = q @ k.transpose(-1, -2) / math.sqrt(D)
     if causal:
         mask = torch.ones(S, S, dtype=torch.bool, device=qkv.device).triu(1)
         s = s.masked_fill(mask, float("-inf"))
+    if key_len is not None:  # [B] valid key count per sequence
+        kpad = torch.arange(S, device=qkv.device)[None, :] >= key_len[:, None].long()
+        s = s.masked_fill(kpad[:, None, None, :], float("-inf"))
     p = s.softmax(-1)
     o = p @ v  # B H S D
     return o.permute(0, 2, 1, 3).reshape(B * S, H * D)
@@ -191,6 +194,33 @@ def test_attention_fwd_bwd(K, B, S, H, D, causal):
     hd = H * D
     for part in range(3):
         assert _rel(dqkv[:, part * hd:(part + 1) * hd], g[:, part * hd:(part + 1) * hd]) < 2e-2
+
+
+@pytest.mark.parametrize("B,S,H,D", [(3, 128, 4, 32), (3, 256, 3, 64), (3, 512, 2, 128), (2, 192, 2, 80)])
+def test_attention_key_padding(K, B, S, H, D):
+    """Bidirectional attention with key_len[b] (BERT padding): keys >= key_len[b] get zero
+    probability; their dK / dV are exactly zero.  Lengths cover a full tile, a ragged tail
+    inside the first tile and a single valid key."""
+    torch.manual_seed(8)
+    qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
+    dout = torch.randn(B * S, H * D, device="cuda").bfloat16()
+    lens = [S, S // 2 + 37, 1, 100][:B]
+    key_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out, lse = K.attention_fwd(qkv, B, S, H, D, False, key_len=key_len)
+    x = qkv.float().requires_grad_()
+    ref = _attn_ref(x, B, S, H, D, False, key_len)
+    ref.backward(dout.float())
+    torch.cuda.synchronize()
+    assert _rel(out, ref) < 1e-2
+    dqkv = K.attention_bwd(qkv, out, dout, lse, B, S, H, D, False, key_len=key_len)
+    torch.cuda.synchronize()
+    hd = H * D
+    for part in range(3):
+        assert _rel(dqkv[:, part * hd:(part + 1) * hd], x.grad[:, part * hd:(part + 1) * hd]) < 2e-2
+    for b, n in enumerate(lens):  # padded keys: dK = dV = 0 exactly
+        assert not dqkv[b * S + n:(b + 1) * S, hd:].any()
+    with pytest.raises(RuntimeError):  # causal + key padding is not a supported combination
+        K.attention_fwd(qkv, B, S, H, D, True, key_len=key_len)
 
 
 # (M, N, K, seg, seq): the 1.3B dO GEMM (8192x2048, 256 tiles -> tail split), a 350M-like
