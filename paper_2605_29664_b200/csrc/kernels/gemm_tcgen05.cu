@@ -40,15 +40,21 @@ namespace {
 constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 64;
-constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KiB
-constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KiB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int NUM_THREADS = 256;
-constexpr int TMEM_COLS = 512;  // 2 accumulators x 256 fp32 columns
 constexpr int GROUP_M = 8;
 constexpr int STG_BYTES = 4 * 2 * 4096;  // TMA-store epilogue staging (4 warps x 2 x 4 KB)
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 256 /*barriers*/;
+
+// Single-CTA tile 128 x TBN: TBN = 256 (4-stage ring, 2 x 256 TMEM columns) or TBN = 128
+// (6-stage ring, 2 x 128 columns) for small products whose 128 x 256 tiles leave SMs idle.
+template <int TBN>
+struct SingleCfg {
+  static constexpr int B_STAGE_BYTES = TBN * BK * 2;
+  static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+  static constexpr int STAGES = TBN == 256 ? 4 : 6;
+  static constexpr uint32_t TMEM_COLS = 2 * TBN;
+  static constexpr size_t SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 256 /*barriers*/;
+};
 
 struct EpiParams {
   int M, N, K;
@@ -257,11 +263,14 @@ __device__ __forceinline__ void pair_epilogue(const EpiMaps& em, const EpiParams
   }
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, int TBN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const __grid_constant__ EpiMaps em,
                       const EpiParams p) {
+  using Cfg = SingleCfg<TBN>;
+  constexpr int STAGES = Cfg::STAGES, B_STAGE_BYTES = Cfg::B_STAGE_BYTES, STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr uint32_t TMEM_COLS = Cfg::TMEM_COLS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -278,7 +287,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int tiles_m = (p.M + BM - 1) / BM;
-  const int tiles_n = (p.N + BN - 1) / BN;
+  const int tiles_n = (p.N + TBN - 1) / TBN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = p.K / BK;
 
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int tm, tn;
         tile_coords(t, tiles_m, tiles_n, tm, tn);
-        const int m0 = tm * BM, n0 = tn * BN;
+        const int m0 = tm * BM, n0 = tn * TBN;
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem_a + stage * A_STAGE_BYTES;
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
+            for (int i = 0; i < TBN / 64; ++i)
               ptx::tma_load_2d_w(sb + i * (64 * BK * 2), &map_b, &full_bar[stage], n0 + 64 * i, k0);
           } else {
             ptx::tma_load_2d_w(sb, &map_b, &full_bar[stage], k0, n0);
@@ -343,7 +352,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     {  // ---------------- MMA issuer (warp-converged, elect.sync inside the asm)
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, TBN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         ptx::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * TBN;
         for (int kb = 0; kb < num_kb; ++kb) {
           ptx::mbar_wait(&full_bar[stage], phase);
           ptx::tc_fence_after();
@@ -382,13 +391,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_coords(t, tiles_m, tiles_n, tm, tn);
       ptx::mbar_wait(&tfull_bar[acc], acc_phase);
       ptx::tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * TBN;
       if constexpr (EPI == EPI_DISCARD) {
         uint32_t raw[32];
-        for (int c = 0; c < BN; c += 32) ptx::tmem_ld_32x32b_x32(t_row + c, raw);
+        for (int c = 0; c < TBN; c += 32) ptx::tmem_ld_32x32b_x32(t_row + c, raw);
         ptx::tmem_ld_wait();
       } else {
-        pair_epilogue<EPI>(em, p, t_row, BN, tn * BN, tm * BM + q * 32, stg, &aux_bar[2 * q], aux_phase, bsel,
+        pair_epilogue<EPI>(em, p, t_row, TBN, tn * TBN, tm * BM + q * 32, stg, &aux_bar[2 * q], aux_phase, bsel,
                            lane);
       }
       ptx::tc_fence_before();
@@ -866,25 +875,31 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// MODE 0: single-CTA 128x256 tiles; MODE 256: CTA-pair 256x256 tiles (+ split tail).
+template <bool A_MN, bool B_MN, int EPI, int TBN>
+int launch_single(const CUtensorMap& ma, const CUtensorMap& mb, const EpiMaps& em, const EpiParams& p,
+                  cudaStream_t s) {
+  auto kern = gemm_bf16_tcgen05<A_MN, B_MN, EPI, TBN>;
+  constexpr size_t smem = SingleCfg<TBN>::SMEM;
+  static std::atomic<bool> attr_set[kMaxDevices];
+  const int dev = current_device();
+  if (!attr_set[dev].load()) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr_set[dev].store(true);
+  }
+  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + TBN - 1) / TBN);
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), smem, s, ma, mb, em, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// MODE 0: single-CTA 128x256 tiles; MODE 128: single-CTA 128x128 tiles; MODE 256: CTA-pair
+// 256x256 tiles (+ split tail).
 template <bool A_MN, bool B_MN, int EPI>
 int launch(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mbt, const EpiMaps& em,
            const EpiParams& p, cudaStream_t s) {
-  if (mode == 0) {
-    auto kern = gemm_bf16_tcgen05<A_MN, B_MN, EPI>;
-    static std::atomic<bool> attr_set[kMaxDevices];
-    const int dev = current_device();
-    if (!attr_set[dev].load()) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(SMEM_BYTES));
-      if (e != cudaSuccess) return e;
-      attr_set[dev].store(true);
-    }
-    const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-    const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-    cudaError_t e = launch_pdl(kern, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, s, ma, mb, em, p);
-    return e != cudaSuccess ? e : cudaGetLastError();
-  }
+  if (mode == 0) return launch_single<A_MN, B_MN, EPI, 256>(ma, mb, em, p, s);
+  if (mode == 128) return launch_single<A_MN, B_MN, EPI, 128>(ma, mb, em, p, s);
   static const int nst = env_int("AMDP_GEMM_STAGES", 6);
   if (nst == 4) return launch_pair<A_MN, B_MN, EPI, 4>(ma, mb, mbt, em, p, s);
   return launch_pair<A_MN, B_MN, EPI, 6>(ma, mb, mbt, em, p, s);
@@ -922,7 +937,7 @@ int choose_mode(int M, int N, int K, bool a_mn, bool b_mn) {
   (void)a_mn;
   (void)b_mn;
   static const int forced = env_int("AMDP_GEMM_MODE", -1);
-  if (forced == 0 || forced == 256) return forced;
+  if (forced == 0 || forced == 128 || forced == 256) return forced;
   // CTA pairs everywhere M allows, except small products (< 20 GFLOP: the BERT-large layer
   // GEMMs at 2048 tokens, 350M's out-projection), which run as single-CTA 128x256 tiles: with
   // the executor's concurrent streams a small GEMM then occupies half the SMs per tile and
@@ -932,8 +947,22 @@ int choose_mode(int M, int N, int K, bool a_mn, bool b_mn) {
   // producer that issue loop starved the pair kernel: 1081 TF/s sustained vs 1136 on
   // single-CTA tiles; warp-converged issue: 1189.)
   static const double small = env_int("AMDP_GEMM_SMALL_GFLOP", 20) * 1e9;
-  if (2.0 * M * static_cast<double>(N) * K < small) return 0;
-  return M >= 256 ? 256 : 0;
+  if (M >= 256 && 2.0 * M * static_cast<double>(N) * K >= small) return 256;
+  // Single-CTA tiles of 128 x 128 (AMDP_GEMM_NARROW=1: where they take fewer tile-times than
+  // 128 x 256, waves(2T) / 2 < waves(T); =2 always).  In isolation they cut the BERT-large
+  // layer GEMMs from 210 to 184 us (fc2 forward 24.2 -> 15.2 us, fc1 activation gradient
+  // 22.9 -> 14.7, out-projection weight gradient 15.3 -> 9.9; cuBLAS 167 us for the set,
+  // scripts/gemm_small.py), but inside the folded BERT-large D=8 window, where 8 logical
+  // devices' kernels share the SMs, the wider tiles' lower per-tile overhead wins: 338k vs
+  // 325k tokens/s (same box, A/B twice).  Off by default.
+  static const int narrow = env_int("AMDP_GEMM_NARROW", 0);
+  if (narrow == 2) return 128;
+  if (narrow) {
+    const int tm = (M + BM - 1) / BM, t256 = tm * ((N + 255) / 256), t128 = tm * ((N + 127) / 128);
+    const int w256 = (t256 + g_num_sms - 1) / g_num_sms, w128 = (t128 + g_num_sms - 1) / g_num_sms;
+    if (w128 < 2 * w256) return 128;
+  }
+  return 0;
 }
 
 }  // namespace
@@ -968,9 +997,9 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
   if (a->b_mn_major) {
     ok = make_map(&mb, a->B, a->N, a->K, a->ldb, BK);
     mbt = mb;
-  } else {  // B rows per CTA: 256 (single) or 128 (pair); tail sub-tiles 128 / s
-    ok = make_map(&mb, a->B, a->K, a->N, a->ldb, mode == 0 ? BN : PBN / 2);
-    if (ok && mode != 0) {
+  } else {  // B rows per CTA: 256 / 128 (single) or 128 (pair); tail sub-tiles 128 / s
+    ok = make_map(&mb, a->B, a->K, a->N, a->ldb, mode == 0 ? BN : mode == 128 ? 128 : PBN / 2);
+    if (ok && mode == 256) {
       const PairSched sc = pair_schedule(a->M, a->N, false, gemm_pairs());
       ok = make_map(&mbt, a->B, a->K, a->N, a->ldb, PBN / 2 / sc.tail_split);
     } else {
@@ -993,10 +1022,11 @@ extern "C" int amdp_gemm(const amdp_gemm_args* a, amdp_stream_t stream) {
               static_cast<const __nv_bfloat16*>(a->aux), a->ld_aux,
               static_cast<__nv_bfloat16*>(a->C2), a->ldc2, a->alpha,
               a->rowdot, a->rowdot_seg, a->rowdot_seq};
-  if (a->epilogue == AMDP_EPI_ROWDOT && mode != 0) {
-    // tail sub-tiles narrower than a segment split it between two CTAs (atomicAdd onto zero)
-    const PairSched sc = pair_schedule(a->M, a->N, false, gemm_pairs());
-    if (PBN / sc.tail_split < a->rowdot_seg) {
+  if (a->epilogue == AMDP_EPI_ROWDOT) {
+    // tiles (or tail sub-tiles) narrower than a segment split it between two CTAs (atomicAdd
+    // onto zero)
+    const int width = mode == 256 ? PBN / pair_schedule(a->M, a->N, false, gemm_pairs()).tail_split : mode == 128 ? 128 : BN;
+    if (width < a->rowdot_seg) {
       const cudaError_t e = cudaMemsetAsync(a->rowdot, 0, static_cast<size_t>(a->M) * (a->N / a->rowdot_seg) * sizeof(float),
                                             reinterpret_cast<cudaStream_t>(stream));
       if (e != cudaSuccess) return e;

@@ -97,6 +97,76 @@ def test_gemm_accum_ksplit_tail_deterministic(K, N, M, N_, K_):
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
 
 
+# Small products on single-CTA tiles (BERT-large shapes, < 20 GFLOP): 128 x 256 by default,
+# 128 x 128 under AMDP_GEMM_NARROW (test_gemm_narrow_tiles_subprocess):
+# BERT-large shapes (fc2 forward: 64 tiles of 128 x 256 -> 128 tiles of 128 x 128; the
+# out-projection weight gradient, MN-major operands) and a ragged one (partial M and N tiles),
+# every epilogue, every element checked against torch fp32, and bitwise reproducible.
+SMALL_SHAPES = [(2048, 1024, 4096, False, False), (1024, 1024, 2048, True, True), (1000, 776, 1472, False, True)]
+
+
+@pytest.mark.parametrize("M,N_,K_,a_mn,b_mn", SMALL_SHAPES)
+@pytest.mark.parametrize("epi", ["store", "gelu", "residual", "gelu_bwd", "accum", "store_f32"])
+def test_gemm_small_tiles(K, N, M, N_, K_, a_mn, b_mn, epi):
+    torch.manual_seed(11)
+    A = torch.randn(M, K_, device="cuda").bfloat16()
+    B = (torch.randn(N_, K_, device="cuda") / math.sqrt(K_)).bfloat16()
+    As = A.T.contiguous() if a_mn else A
+    Bs = B.T.contiguous() if b_mn else B
+    prod = A.float() @ B.float().T
+    aux = torch.randn(M, N_, device="cuda").bfloat16()
+    outs = []
+    for _ in range(2):
+        kw = {}
+        if epi == "store":
+            kw = dict(epilogue=N.EPI_STORE_BF16)
+        elif epi == "gelu":
+            kw = dict(epilogue=N.EPI_GELU, C2=torch.empty(M, N_, dtype=torch.bfloat16, device="cuda"), ldc2=N_)
+        elif epi == "residual":
+            kw = dict(epilogue=N.EPI_RESIDUAL, aux=aux, ld_aux=N_)
+        elif epi == "gelu_bwd":
+            kw = dict(epilogue=N.EPI_GELU_BWD, aux=aux, ld_aux=N_)
+        elif epi == "accum":
+            kw = dict(epilogue=N.EPI_ACCUM_F32, C=torch.ones(M, N_, device="cuda"))
+        else:
+            kw = dict(epilogue=N.EPI_STORE_F32)
+        C = K.gemm(As, Bs, M=M, N_=N_, K=K_, a_mn=a_mn, b_mn=b_mn, **kw)
+        torch.cuda.synchronize()
+        outs.append((C.clone(), kw.get("C2")))
+    C, C2 = outs[0]
+    if epi == "gelu":
+        ref, ref2 = _gelu(C2.float()), prod
+        assert (C2.float() - ref2).abs().max().item() < 0.02 * ref2.abs().max().item()
+    elif epi == "residual":
+        ref = prod + aux.float()
+    elif epi == "gelu_bwd":
+        x = aux.float()
+        t = torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
+        ref = prod * (0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x))
+    elif epi == "accum":
+        ref = prod + 1.0
+    else:
+        ref = prod
+    tol = (1e-4 if epi in ("accum", "store_f32") else 0.02) * ref.abs().max().item()
+    err = (C.float() - ref).abs().max().item()
+    assert err < tol, f"max abs err {err} (tol {tol})"
+    assert torch.equal(outs[0][0], outs[1][0])
+
+
+def test_gemm_narrow_tiles_subprocess():
+    """AMDP_GEMM_NARROW=2 (128 x 128 single-CTA tiles everywhere below the pair threshold) is
+    read once per process: the small-tile and rowdot cases re-run in a child process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, AMDP_GEMM_NARROW="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_kernels_gpu.py"), "-k", "small_tiles or rowdot or gemm_store"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, True)])
 def test_gemm_accum_f32(K, N, a_mn, b_mn):
     torch.manual_seed(1)
@@ -227,7 +297,8 @@ def test_attention_key_padding(K, B, S, H, D):
 # head_dim 64 case, a single-CTA M < 256 case and a 64-wide-tail case (segments split
 # between two CTAs: atomic sum of two partials onto zero).
 @pytest.mark.parametrize("M,N_,K_,seg,seq", [(8192, 2048, 256, 128, 2048), (4096, 1024, 128, 64, 1024),
-                                             (128, 512, 128, 128, 64), (2560, 2048, 128, 128, 512)])
+                                             (128, 512, 128, 128, 64), (2560, 2048, 128, 128, 512),
+                                             (2048, 1024, 1024, 64, 512)])  # BERT-large dO: 128 x 128 tiles
 def test_gemm_rowdot(K, N, M, N_, K_, seg, seq):
     """AMDP_EPI_ROWDOT: C = bf16(A B^T) and rowdot[b][h][s] = sum over the h-th seg-column
     segment of bf16(C) * aux (attention backward's delta from the dO GEMM)."""
