@@ -121,6 +121,19 @@ int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const float* gamma
                        const float* mean, const float* rstd, const uint16_t* resid_grad,
                        uint16_t* dx, float* dgamma, float* dbeta, void* workspace, int rows,
                        int cols, amdp_stream_t stream);
+/* Deferred dgamma / dbeta (one column reduction per optimizer window instead of per call):
+ * amdp_layernorm_bwd_rows writes dx like amdp_layernorm_bwd and ADDS its per-CTA column
+ * partials into part[amdp_layernorm_bwd_parts(rows, cols)][2][cols] (zero-initialised by the
+ * caller, then kept between calls of the same rows / cols on one stream); the flush adds the
+ * column sums into dgamma / dbeta and zeroes part.  bwd_parts returns 0 (and bwd_rows
+ * AMDP_ERR_UNSUPPORTED) for widths the row-group kernel does not take (cols % 256 != 0 or
+ * cols > 4096): use amdp_layernorm_bwd there.                                          */
+int amdp_layernorm_bwd_parts(int rows, int cols);
+int amdp_layernorm_bwd_rows(const uint16_t* dy, const uint16_t* x, const float* gamma,
+                            const float* mean, const float* rstd, const uint16_t* resid_grad,
+                            uint16_t* dx, float* part, int rows, int cols, amdp_stream_t stream);
+int amdp_layernorm_dgb_flush(float* part, int nparts, int cols, float* dgamma, float* dbeta,
+                             amdp_stream_t stream);
 
 /* ---------------------------------------------------------------- embedding
  * x[t] = wte[tokens[t]] + wpe[t % seq]   (bf16 tables, bf16 out)                    */

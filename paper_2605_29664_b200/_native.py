@@ -75,6 +75,9 @@ _sig("amdp_layernorm_fwd", c_int, [_P, _P, _P, _P, _P, _P, c_int, c_int, c_float
 _sig("amdp_layernorm_bwd_workspace", c_size_t, [c_int, c_int])
 _sig("amdp_layernorm_bwd", c_int,
      [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, c_int, c_int, _P])
+_sig("amdp_layernorm_bwd_parts", c_int, [c_int, c_int])
+_sig("amdp_layernorm_bwd_rows", c_int, [_P, _P, _P, _P, _P, _P, _P, _P, c_int, c_int, _P])
+_sig("amdp_layernorm_dgb_flush", c_int, [_P, c_int, c_int, _P, _P, _P])
 _sig("amdp_embedding_fwd", c_int, [_P, _P, _P, _P, c_int, c_int, c_int, _P])
 _sig("amdp_embedding_bwd", c_int, [_P, _P, _P, _P, _P, c_int, c_int, c_int, _P])
 _sig("amdp_xent_fwd_bwd", c_int, [_P, _P, _P, _P, c_int, c_int, c_int, c_float, _P])

@@ -40,6 +40,7 @@ Engine::~Engine() {
     cudaFree(s->m);
     cudaFree(s->v);
     cudaFree(s->grad);
+    cudaFree(s->ln_part);
     cudaFree(s->w);
     cudaFree(s->wt);
   }
@@ -125,6 +126,12 @@ void Engine::allocate() {
     CUDA_OK(cudaMalloc(&st.w, n * sizeof(uint16_t)));
     CUDA_OK(cudaMalloc(&st.wt, n * sizeof(uint16_t)));
     CUDA_OK(cudaMemsetAsync(st.grad, 0, n * sizeof(float), cs_));
+    // deferred LayerNorm parameter gradients (bf16 path; AMDP_LN_DEFER=0 reduces per backward)
+    static const bool ln_defer = !getenv("AMDP_LN_DEFER") || atoi(getenv("AMDP_LN_DEFER")) != 0;
+    if (ln_defer && !dm.fp32 && st.ln_parts() > 0) {
+      CUDA_OK(cudaMalloc(&st.ln_part, st.ln_part_floats() * sizeof(float)));
+      CUDA_OK(cudaMemsetAsync(st.ln_part, 0, st.ln_part_floats() * sizeof(float), cs_));
+    }
     if (versioned_) {
       auto& wb = wbuf_[static_cast<size_t>(i)];
       auto& wtb = wtbuf_[static_cast<size_t>(i)];
@@ -481,6 +488,7 @@ void Engine::exec_task(int pos, const int32_t* h_in, const int32_t* h_lab, std::
       // the kernel-timing run serialises the streams so per-launch event spans are exact
       launched = S.backward(A, tok, in, gin, gout, wss_[static_cast<size_t>(si)], cs,
                             ktimer_.enabled ? SideStream{} : sides_[static_cast<size_t>(si)], &rc, klen);
+      if (rc == 0 && ln_flush_[static_cast<size_t>(pos)]) launched += S.flush_ln_grads(cs, &rc);
     }
     stats.kernels_launched += launched;
     if (rc != 0) throw std::runtime_error("stage kernel failed with code " + std::to_string(rc));

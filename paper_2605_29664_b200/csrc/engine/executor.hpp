@@ -249,6 +249,10 @@ class Engine {
   std::vector<std::vector<int>> waits_;     // per position: earlier positions (other streams)
   std::vector<std::vector<int>> stage_last_;  // per R / BC position: last local F/B of the stage per stream
   std::vector<std::vector<int>> loss_tasks_;  // per window: local last-stage Forward positions
+  // per position: 1 = a local Backward after which the stage's deferred LayerNorm gradients are
+  // folded into its window gradient (the last local Backward of the stage before each of its
+  // Reduce / Broadcast / Update tasks, and before the end of the run)
+  std::vector<char> ln_flush_;
   std::vector<cudaEvent_t> done_;           // per position: the F/B task complete on its stream
   std::vector<int> tok_loader_;             // per window: position whose stream copied the tokens (run)
   std::vector<char> issued_;                // per position: issued in the current run

@@ -263,6 +263,23 @@ size_t GptStage::workspace_bytes(const Dims& d) {
     launched += (nk);         \
   } while (0)
 
+int GptStage::flush_ln_grads(cudaStream_t s, int* rc) const {
+  int launched = 0;
+  *rc = 0;
+  if (!ln_part) return 0;
+  const int parts = ln_parts(), h = d_.h;
+  for (int k = 0; k < ln_count(); ++k) {
+    const bool fin = last() && k == ln_count() - 1;
+    const LayerParams* P = fin ? nullptr : &layers_[static_cast<size_t>(k / 2)];
+    const ParamRef& g = fin ? lnf_g_ : (k % 2 ? P->ln2_g : P->ln1_g);
+    const ParamRef& b = fin ? lnf_b_ : (k % 2 ? P->ln2_b : P->ln1_b);
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * parts * h, amdp_layernorm_dgb_flush(ln_part + static_cast<size_t>(k) * parts * 2 * h, parts,
+                                                                        h, grad + g.off, grad + b.off,
+                                                                        reinterpret_cast<amdp_stream_t>(s)), 1);
+  }
+  return launched;
+}
+
 std::vector<std::pair<int64_t, int64_t>> GptStage::segments() const {
   std::vector<int64_t> starts;
   if (first()) starts.push_back(0);
@@ -348,6 +365,17 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
   const int T = d_.T, h = d_.h, F = d_.ffn;
   const Ws ws = carve_ws(d_, wsb);
   cudaStream_t sd = ss.side ? ss.side : s;
+  // LayerNorm k's backward (k = 2 li / 2 li + 1 for a layer's ln1 / ln2, the last one for the
+  // final LayerNorm): deferred parameter gradients when ln_part is set
+  auto ln_bwd = [&](int k, const uint16_t* dy, const uint16_t* xin, const ParamRef& pg, const ParamRef& pb,
+                    const float* mean, const float* rstd, const uint16_t* resid, uint16_t* dx, void* lnws,
+                    amdp_stream_t stream) {
+    if (ln_part)
+      return amdp_layernorm_bwd_rows(dy, xin, master + pg.off, mean, rstd, resid, dx,
+                                     ln_part + static_cast<size_t>(k) * ln_parts() * 2 * h, T, h, stream);
+    return amdp_layernorm_bwd(dy, xin, master + pg.off, mean, rstd, resid, dx, grad + pg.off, grad + pb.off, lnws, T,
+                              h, stream);
+  };
   static const bool no_fuse = getenv("AMDP_NO_DELTA_FUSION") != nullptr;
   const bool fuse_delta = !no_fuse && d_.hd % 64 == 0 && amdp_attention_bwd_delta_supported(d_.S, d_.hd);
   auto hand = [&](cudaEvent_t e, cudaStream_t from, cudaStream_t to) {
@@ -364,8 +392,8 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
                      AMDP_EPI_ACCUM_F32, sd), 1);
     AMDP_GEMM(gemm_t(kt, T, h, d_.V, a.logits, d_.V, false, wt + head_.off, d_.V, false, ws.dtmp, h,
                      AMDP_EPI_STORE_BF16, s, nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
-    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, a.xf, master + lnf_g_.off, a.lnf_mean, a.lnf_rstd, nullptr, ws.g0,
-                                grad + lnf_g_.off, grad + lnf_b_.off, ws.ln, T, h, st), 2);
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, ln_bwd(ln_count() - 1, ws.dtmp, a.xf, lnf_g_, lnf_b_, a.lnf_mean, a.lnf_rstd,
+                                                 nullptr, ws.g0, ws.ln, st), ln_part ? 1 : 2);
     g = ws.g0;
   }
   for (int li = l1_ - l0_ - 1; li >= 0; --li) {
@@ -396,8 +424,8 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
                      nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
     // ln2 = LN(hmid); dhmid = g + LN'(dln2)
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DH], 0);  // previous layer's dWo done with dhmid
-    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, A.hmid, master + P.ln2_g.off, A.ln2_mean, A.ln2_rstd, g, ws.dhmid,
-                                grad + P.ln2_g.off, grad + P.ln2_b.off, ws.ln, T, h, st), 2);
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, ln_bwd(2 * li + 1, ws.dtmp, A.hmid, P.ln2_g, P.ln2_b, A.ln2_mean, A.ln2_rstd, g,
+                                                 ws.dhmid, ws.ln, st), ln_part ? 1 : 2);
     // o = attention(qkv) when recomputing: deterministic (rewrites the same lse), issued before
     // the hand-off so the side stream's out-proj weight gradient reads the rebuilt o; its
     // previous reader (the layer above's) finished before F_DH, waited for above
@@ -434,8 +462,8 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
                      AMDP_EPI_STORE_BF16, s, nullptr, 0, nullptr, 0, K_GEMM_DGRAD), 1);
     uint16_t* gn = (li == 0 && !first()) ? gout : (g == ws.g0 ? ws.g1 : ws.g0);
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_G], 0);  // dW2 of the layer that read gn's buffer
-    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, amdp_layernorm_bwd(ws.dtmp, x, master + P.ln1_g.off, A.ln1_mean, A.ln1_rstd, ws.dhmid, gn,
-                                grad + P.ln1_g.off, grad + P.ln1_b.off, ws.ln, T, h, st), 2);
+    AMDP_TRY(K_LAYERNORM, 0, 8.0 * T * h, ln_bwd(2 * li, ws.dtmp, x, P.ln1_g, P.ln1_b, A.ln1_mean, A.ln1_rstd, ws.dhmid, gn,
+                                                 ws.ln, st), ln_part ? 1 : 2);
     g = gn;
   }
   if (first()) AMDP_TRY(K_EMBED, 0, 10.0 * T * h, amdp_embedding_bwd(tokens, g, grad + wte_.off, grad + wpe_.off, ws.rows, T, d_.S, h, st), 2);

@@ -92,6 +92,14 @@ class GptStage {
   // forward GEMMs (refresh_transposed() after every write of `w`)
   uint16_t* wt = nullptr;
   int refresh_transposed(cudaStream_t s) const;
+  // Deferred LayerNorm parameter gradients (amdp_layernorm_bwd_rows): per-LayerNorm partial
+  // rows accumulated over the window's backwards, folded into `grad` by flush_ln_grads() once
+  // per window.  Null: every backward reduces its own (amdp_layernorm_bwd).
+  float* ln_part = nullptr;
+  int ln_count() const { return 2 * (l1_ - l0_) + (last() ? 1 : 0); }
+  int ln_parts() const { return amdp_layernorm_bwd_parts(d_.T, d_.h); }
+  size_t ln_part_floats() const { return static_cast<size_t>(ln_count()) * ln_parts() * 2 * d_.h; }
+  int flush_ln_grads(cudaStream_t s, int* rc) const;
   KTimer* kt = nullptr;     // optional per-kernel-class timing
   double attn_fwd_flops() const {  // algorithmic: QK^T + PV, causal half
     const double f = 4.0 * d_.B * d_.heads * static_cast<double>(d_.S) * d_.S * d_.hd;

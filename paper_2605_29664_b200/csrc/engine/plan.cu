@@ -469,6 +469,20 @@ void Engine::plan_streams() {
     stage_stream_last[static_cast<size_t>(t.stage)][static_cast<size_t>(me)] = k;
     if (t.kind == ppsim::Kind::Forward && t.stage == depth_ - 1) loss_tasks_[static_cast<size_t>(t.window)].push_back(k);
   }
+  ln_flush_.assign(static_cast<size_t>(N), 0);
+  std::vector<int> pending(static_cast<size_t>(depth_), -1);
+  for (int k = 0; k < N; ++k) {
+    const auto& t = g.tasks[static_cast<size_t>(sched.order[static_cast<size_t>(k)])];
+    int& p = pending[static_cast<size_t>(t.stage)];
+    if (t.kind == ppsim::Kind::Reduce || t.kind == ppsim::Kind::Broadcast || t.kind == ppsim::Kind::Update) {
+      if (p >= 0) ln_flush_[static_cast<size_t>(p)] = 1;
+      p = -1;
+    } else if (t.kind == ppsim::Kind::Backward && plan_[static_cast<size_t>(k)].local) {
+      p = k;
+    }
+  }
+  for (int p : pending)
+    if (p >= 0) ln_flush_[static_cast<size_t>(p)] = 1;
 }
 
 namespace {

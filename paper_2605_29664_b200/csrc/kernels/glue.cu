@@ -243,7 +243,7 @@ template <int RG>
 __global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
     const bf16* __restrict__ dy, const bf16* __restrict__ x, const float* __restrict__ gamma,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, const bf16* resid_grad, bf16* dx,
-    float* __restrict__ part, int rows, int cols) {
+    float* __restrict__ part, int rows, int cols, int accumulate) {
   grid_dep_wait();  // PDL: predecessor's outputs visible from here
   grid_dep_trigger();
   __shared__ float red[2][2 * RG * 32];
@@ -298,8 +298,17 @@ __global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
     }
     cur = nxt;
   }
-  // per-CTA column partials -> workspace row blockIdx.x: [dgamma cols | dbeta cols]
+  // per-CTA column partials -> workspace row blockIdx.x: [dgamma cols | dbeta cols]; with
+  // `accumulate` added to the row (the deferred form: one CTA index always owns one row, and
+  // the launches on a stream are ordered, so the sums are deterministic)
   float* wrow = part + static_cast<size_t>(blockIdx.x) * 2 * cols;
+  if (accumulate) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      ag[e] += wrow[c + e];
+      ab[e] += wrow[cols + c + e];
+    }
+  }
   *reinterpret_cast<float4*>(wrow + c) = make_float4(ag[0], ag[1], ag[2], ag[3]);
   *reinterpret_cast<float4*>(wrow + c + 4) = make_float4(ag[4], ag[5], ag[6], ag[7]);
   *reinterpret_cast<float4*>(wrow + cols + c) = make_float4(ab[0], ab[1], ab[2], ab[3]);
@@ -310,8 +319,9 @@ __global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
 // CTA = 32 columns x 32 row-lanes (each lane sums ~nparts/32 rows, all loads independent), a
 // fixed-order tree over the 32 lanes: deterministic, and short enough that the kernel is not
 // latency-bound (the 8-lane version spent ~9 us on 4.8 MB).
-__global__ void __launch_bounds__(1024) layernorm_dgb_reduce_kernel(const float* __restrict__ part, int nparts,
-                                                                    int cols, float* dgamma, float* dbeta) {
+__global__ void __launch_bounds__(1024) layernorm_dgb_reduce_kernel(float* __restrict__ part, int nparts,
+                                                                    int cols, float* dgamma, float* dbeta,
+                                                                    int clear) {
   grid_dep_wait();  // PDL: predecessor's outputs visible from here
   grid_dep_trigger();
   __shared__ float red[32][33];
@@ -321,6 +331,8 @@ __global__ void __launch_bounds__(1024) layernorm_dgb_reduce_kernel(const float*
   if (col < 2 * cols) {
 #pragma unroll 4
     for (int r = w; r < nparts; r += 32) s += part[static_cast<size_t>(r) * 2 * cols + col];
+    if (clear)  // deferred form: the partial rows start the next window at zero
+      for (int r = w; r < nparts; r += 32) part[static_cast<size_t>(r) * 2 * cols + col] = 0.f;
   }
   red[w][lane] = s;
   __syncthreads();
@@ -585,8 +597,8 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
     float* part = static_cast<float*>(workspace);
     launch_pdl(layernorm_bwd_rows_kernel<2>, dim3(grid), dim3(cols / 8), 0, s, 
         reinterpret_cast<const bf16*>(dy), reinterpret_cast<const bf16*>(x), gamma, mean, rstd,
-        reinterpret_cast<const bf16*>(resid_grad), reinterpret_cast<bf16*>(dx), part, rows, cols);
-    launch_pdl(layernorm_dgb_reduce_kernel, dim3((2 * cols + 31) / 32), dim3(1024), 0, s, part, grid, cols, dgamma, dbeta);
+        reinterpret_cast<const bf16*>(resid_grad), reinterpret_cast<bf16*>(dx), part, rows, cols, 0);
+    launch_pdl(layernorm_dgb_reduce_kernel, dim3((2 * cols + 31) / 32), dim3(1024), 0, s, part, grid, cols, dgamma, dbeta, 0);
     return cudaGetLastError();
   }
   int blocks = (rows + 7) / 8;
@@ -606,8 +618,36 @@ extern "C" int amdp_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const f
   float* part = static_cast<float*>(workspace);
   layernorm_bwd_dgb_kernel<<<g, 256, 0, s>>>(reinterpret_cast<const bf16*>(dy),
                                              reinterpret_cast<const bf16*>(x), mean, rstd, part, rows, cols);
-  launch_pdl(layernorm_dgb_reduce_kernel, dim3((2 * cols + 31) / 32), dim3(1024), 0, s, static_cast<const float*>(part),
-             static_cast<int>(g.y), cols, dgamma, dbeta);
+  launch_pdl(layernorm_dgb_reduce_kernel, dim3((2 * cols + 31) / 32), dim3(1024), 0, s, part,
+             static_cast<int>(g.y), cols, dgamma, dbeta, 0);
+  return cudaGetLastError();
+}
+
+// Deferred parameter gradients: the window's LayerNorm backwards accumulate per-CTA partial
+// rows (amdp_layernorm_bwd_rows) and one flush per window folds them into dgamma / dbeta —
+// one column-reduction launch per window instead of one per minibatch.
+extern "C" int amdp_layernorm_bwd_parts(int rows, int cols) {
+  if (rows <= 0 || !ln_row_group_form(cols)) return 0;
+  return ln_bwd_ctas(rows);
+}
+
+extern "C" int amdp_layernorm_bwd_rows(const uint16_t* dy, const uint16_t* x, const float* gamma, const float* mean,
+                                       const float* rstd, const uint16_t* resid_grad, uint16_t* dx, float* part,
+                                       int rows, int cols, amdp_stream_t stream) {
+  if (rows <= 0 || cols <= 0 || !part) return AMDP_ERR_INVALID;
+  if (!ln_row_group_form(cols)) return AMDP_ERR_UNSUPPORTED;
+  launch_pdl(layernorm_bwd_rows_kernel<2>, dim3(ln_bwd_ctas(rows)), dim3(cols / 8), 0,
+             reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<const bf16*>(dy),
+             reinterpret_cast<const bf16*>(x), gamma, mean, rstd, reinterpret_cast<const bf16*>(resid_grad),
+             reinterpret_cast<bf16*>(dx), part, rows, cols, 1);
+  return cudaGetLastError();
+}
+
+extern "C" int amdp_layernorm_dgb_flush(float* part, int nparts, int cols, float* dgamma, float* dbeta,
+                                        amdp_stream_t stream) {
+  if (!part || nparts <= 0 || cols <= 0) return AMDP_ERR_INVALID;
+  launch_pdl(layernorm_dgb_reduce_kernel, dim3((2 * cols + 31) / 32), dim3(1024), 0,
+             reinterpret_cast<cudaStream_t>(stream), part, nparts, cols, dgamma, dbeta, 1);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,24 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, resid_grad, dgamma, dbeta):
     return dx
 
 
+def layernorm_bwd_parts(rows, cols):
+    return N.lib.amdp_layernorm_bwd_parts(rows, cols)
+
+
+def layernorm_bwd_rows(dy, x, gamma, mean, rstd, resid_grad, part):
+    """dx, with the dgamma / dbeta column partials added into `part` (deferred form)."""
+    rows, cols = x.shape
+    dx = torch.empty_like(x)
+    N.check(N.lib.amdp_layernorm_bwd_rows(_p(dy), _p(x), _p(gamma), _p(mean), _p(rstd), _p(resid_grad), _p(dx),
+                                          _p(part), rows, cols, _stream()), "amdp_layernorm_bwd_rows")
+    return dx
+
+
+def layernorm_dgb_flush(part, nparts, cols, dgamma, dbeta):
+    N.check(N.lib.amdp_layernorm_dgb_flush(_p(part), nparts, cols, _p(dgamma), _p(dbeta), _stream()),
+            "amdp_layernorm_dgb_flush")
+
+
 def embedding_fwd(tokens, wte, wpe, seq):
     ntok, hidden = tokens.numel(), wte.shape[1]
     x = torch.empty(ntok, hidden, dtype=torch.bfloat16, device=wte.device)

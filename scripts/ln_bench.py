@@ -1,9 +1,9 @@
-"""LayerNorm fwd/bwd at the 1.3B shape (T=8192, h=2048), L2 flushed before every launch,
+"""LayerNorm fwd/bwd at the 1.3B shape (T=8192, h=2048; or argv T h), L2 flushed before every launch,
 next to a plain torch copy of the same bytes (the practical floor for this size)."""
 import sys, os, torch, json, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_29664_b200 import kernels as K
-T, h = 8192, 2048
+T, h = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (8192, 2048)
 x = torch.randn(T, h, device="cuda").bfloat16(); dy = torch.randn(T, h, device="cuda").bfloat16()
 rg = torch.randn(T, h, device="cuda").bfloat16()
 g = torch.ones(h, device="cuda"); b = torch.zeros(h, device="cuda")

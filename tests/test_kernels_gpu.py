@@ -361,6 +361,46 @@ def test_layernorm(K, rows, cols):
     assert _rel(db, b.grad) < 1e-3
 
 
+@pytest.mark.parametrize("rows,cols", [(2048, 1024), (8192, 2048), (1000, 512)])
+def test_layernorm_deferred_param_grads(K, rows, cols):
+    """amdp_layernorm_bwd_rows over 3 calls (a window of minibatches) + one flush: dx equals
+    amdp_layernorm_bwd's bit for bit, dgamma / dbeta equal the per-call reductions' sum
+    within fp32 reassociation (and torch's), the partial rows are zero again after the
+    flush, and the whole sequence is bitwise reproducible."""
+    torch.manual_seed(12)
+    parts = K.layernorm_bwd_parts(rows, cols)
+    assert parts > 0
+    gamma = 1 + 0.1 * torch.randn(cols, device="cuda")
+    beta = 0.1 * torch.randn(cols, device="cuda")
+    xs = [(torch.randn(rows, cols, device="cuda") * 2 + 0.5).bfloat16() for _ in range(3)]
+    dys = [torch.randn(rows, cols, device="cuda").bfloat16() for _ in range(3)]
+    resid = torch.randn(rows, cols, device="cuda").bfloat16()
+    stats = [K.layernorm_fwd(x, gamma, beta)[1:] for x in xs]
+
+    def deferred():
+        part = torch.zeros(parts, 2, cols, device="cuda")
+        dg = torch.full((cols,), 0.5, device="cuda")
+        db = torch.zeros(cols, device="cuda")
+        dxs = [K.layernorm_bwd_rows(dy, x, gamma, m, r, resid, part) for dy, x, (m, r) in zip(dys, xs, stats)]
+        K.layernorm_dgb_flush(part, parts, cols, dg, db)
+        torch.cuda.synchronize()
+        assert not part.any()
+        return dxs, dg, db
+
+    dxs, dg, db = deferred()
+    dg0 = torch.full((cols,), 0.5, device="cuda")
+    db0 = torch.zeros(cols, device="cuda")
+    for i, (dy, x, (m, r)) in enumerate(zip(dys, xs, stats)):
+        dx0 = K.layernorm_bwd(dy, x, gamma, m, r, resid, dg0, db0)
+        torch.cuda.synchronize()
+        assert torch.equal(dx0, dxs[i])
+    assert _rel(dg - 0.5, dg0 - 0.5) < 1e-5 and _rel(db, db0) < 1e-5
+    dg_ref = sum(((x.float() - m[:, None]) * r[:, None] * dy.float()).sum(0) for dy, x, (m, r) in zip(dys, xs, stats))
+    assert _rel(dg - 0.5, dg_ref) < 1e-4
+    dxs2, dg2, db2 = deferred()
+    assert torch.equal(dg, dg2) and torch.equal(db, db2)
+
+
 def test_embedding(K):
     torch.manual_seed(5)
     V, S, Bn, Hd = 1000, 64, 4, 256
