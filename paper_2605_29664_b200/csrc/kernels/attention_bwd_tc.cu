@@ -29,6 +29,9 @@ namespace amdp {
 namespace {
 
 constexpr uint32_t T128 = 16384;  // [128 rows][64 bf16] SW128 tile
+#ifndef FA_BWD_POLY_PAIRS
+#define FA_BWD_POLY_PAIRS 0  // dQ softmax: exponent pairs (of 4) on the FMA pipe; 0 measured best (MUFU is not the limit)
+#endif
 
 // Diagnostics (amdp_debug_attention_bwd_trace): CTA 0 of the dQ kernel records clock64().
 __device__ long long* g_bw_dbg = nullptr;
@@ -634,8 +637,13 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t gg[32];
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 2) {
-          float g0f = ex2(fmaf(__uint_as_float(s[cc]), scale_log2, nl)) * (__uint_as_float(d[cc]) - dl);
-          float g1f = ex2(fmaf(__uint_as_float(s[cc + 1]), scale_log2, nl)) * (__uint_as_float(d[cc + 1]) - dl);
+          // packed pairs; FA_BWD_POLY_PAIRS of every 4 exponent pairs on the FMA pipe
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[cc]), __uint_as_float(s[cc + 1])),
+                                      make_float2(scale_log2, scale_log2), make_float2(nl, nl));
+          const float2 p = ((cc >> 1) & 3) < FA_BWD_POLY_PAIRS ? ex2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
+          const float2 gv = __fmul2_rn(p, __fadd2_rn(make_float2(__uint_as_float(d[cc]), __uint_as_float(d[cc + 1])),
+                                                     make_float2(-dl, -dl)));
+          float g0f = gv.x, g1f = gv.y;
           if (diag) {
             const int k0 = n * 128 + c0 + cc;
             if (k0 > qrow) g0f = 0.f;

@@ -64,21 +64,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA pipe for a pair (round-to-nearest split, degree-3 fit of 2^f on [-1/2, 1/2],
-// rel. err 7.7e-5, far below the bf16 rounding of P): takes a quarter of the exponentials off
-// the 16/clk/SM MUFU unit, which otherwise matches the tensor time at head_dim 128.
-__device__ __forceinline__ float2 ex2_fma2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
-  // f = x - (t - M) = x + (M - t), both steps exact
-  const float2 f = __fadd2_rn(x, __ffma2_rn(t, make_float2(-1.f, -1.f), make_float2(12582912.f, 12582912.f)));
-  float2 p = __ffma2_rn(f, make_float2(0.05508868f, 0.05508868f), make_float2(0.24260405f, 0.24260405f));
-  p = __ffma2_rn(p, f, make_float2(0.69327623f, 0.69327623f));
-  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
 
 // P = 2^(S*scale - m) for one 128-column row held in registers, written as bf16 pairs over
 // the first 64 TMEM columns of the S tile; returns the row sum.  Packed f32x2 arithmetic and

@@ -67,6 +67,22 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 }
 
 // Device side of programmatic dependent launch (see sm100_ptx.cuh for the tcgen05 kernels).
+// 2^x on the FMA pipe for a pair (round-to-nearest split, degree-3 fit of 2^f on [-1/2, 1/2],
+// rel. err 7.7e-5, far below the bf16 rounding of P): takes part of the exponentials off the
+// 16/clk/SM MUFU unit (attention forward and backward softmax).
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  // f = x - (t - M) = x + (M - t), both steps exact
+  const float2 f = __fadd2_rn(x, __ffma2_rn(t, make_float2(-1.f, -1.f), make_float2(12582912.f, 12582912.f)));
+  float2 p = __ffma2_rn(f, make_float2(0.05508868f, 0.05508868f), make_float2(0.24260405f, 0.24260405f));
+  p = __ffma2_rn(p, f, make_float2(0.69327623f, 0.69327623f));
+  p = __ffma2_rn(p, f, make_float2(0.99992895f, 0.99992895f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
