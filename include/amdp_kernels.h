@@ -93,8 +93,11 @@ size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim)
  * (amdp_attention_bwd_delta_supported), AMDP_ERR_UNSUPPORTED otherwise.             */
 int amdp_attention_bwd_delta_supported(int seq, int head_dim);
 /* Which implementation amdp_attention_fwd (backward = 0) / amdp_attention_bwd (1) dispatches
- * to for this shape: AMDP_ATTN_IMPL_TCGEN05 (tcgen05/TMEM/TMA), AMDP_ATTN_IMPL_MMA_SYNC
- * (head_dim 32 or sequence lengths the tensor-core tiles do not divide), -1 unsupported.   */
+ * to for this shape: AMDP_ATTN_IMPL_TCGEN05 (tcgen05/TMEM/TMA: tiled kernels for head_dim
+ * 64 / 80 / 128 with seq % 256 == 0 forward, seq % 128 == 0 backward; one-tile kernels for
+ * seq <= 128 with head_dim 32 / 64), or -1 (unsupported: the calls return
+ * AMDP_ERR_UNSUPPORTED).  AMDP_ATTN_IMPL_MMA_SYNC is no longer returned (kept for ABI
+ * stability; round 1's warp-level fallback was removed).                                    */
 enum { AMDP_ATTN_IMPL_MMA_SYNC = 0, AMDP_ATTN_IMPL_TCGEN05 = 1 };
 int amdp_attention_impl(int seq, int head_dim, int backward);
 int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse, const float* delta,

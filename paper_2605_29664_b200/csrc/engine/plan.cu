@@ -101,6 +101,10 @@ Engine::Engine(const amdp_model_config& mc, const amdp_run_config& rc, const uin
   if (mc.pad_token > 0 && dm.causal) throw std::invalid_argument("engine: pad_token is for bidirectional models");
   if (dm.fp32 && dm.recompute) throw std::invalid_argument("engine: fp32 validation mode stores every activation (no recompute)");
   if (dm.h % dm.heads != 0) throw std::invalid_argument("engine: hidden must divide into heads");
+  if (!dm.fp32 && (amdp_attention_impl(dm.S, dm.hd, 0) < 0 || amdp_attention_impl(dm.S, dm.hd, 1) < 0))
+    throw std::invalid_argument("engine: no tensor-core attention kernel for seq " + std::to_string(dm.S) +
+                                ", head_dim " + std::to_string(dm.hd) +
+                                " (seq % 256 == 0 with head_dim 64 / 80 / 128, or seq <= 128 with head_dim 32 / 64)");
 
   // schedule: build + order on the declared cost model
   ppsim::ClusterSpec cl = ppsim::ClusterSpec::uniform(depth_, devices_, from_c(rc.declared_fwd),

@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_29664_b200 import kernels as K  # noqa: E402
 
-SHAPES = [(4, 512, 16, 64, False), (4, 2048, 16, 64, True), (4, 2048, 16, 128, True), (4, 2048, 32, 80, True)]
+SHAPES = [(4, 512, 16, 64, False), (4, 1024, 16, 64, True), (4, 2048, 16, 128, True), (4, 2048, 32, 80, True)]
 for B, S, H, D, causal in SHAPES:
     qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
     dout = torch.randn(B * S, H * D, device="cuda").bfloat16()

@@ -32,7 +32,7 @@ def per_call(fn, n=10, reps=20):
 
 SHAPES = [  # name, B, S, H, D, causal
     ("bert_large", 4, 512, 16, 64, False),
-    ("gpt_350m", 4, 2048, 16, 64, True),
+    ("gpt_350m", 4, 1024, 16, 64, True),
     ("gpt_1p3b", 4, 2048, 16, 128, True),
     ("gpt_2p7b", 4, 2048, 32, 80, True),
 ]

@@ -245,8 +245,8 @@ def _attn_ref(qkv, B, S, H, D, causal, key_len=None):
     return o.permute(0, 2, 1, 3).reshape(B * S, H * D)
 
 
-@pytest.mark.parametrize("B,S,H,D", [(2, 128, 4, 32), (2, 256, 3, 64), (1, 192, 2, 80), (2, 512, 3, 80), (1, 2048, 2, 80),
-                                     (2, 256, 2, 128), (4, 2048, 2, 128)])
+@pytest.mark.parametrize("B,S,H,D", [(2, 128, 4, 32), (4, 64, 4, 32), (3, 64, 2, 64), (2, 128, 3, 64), (2, 256, 3, 64),
+                                     (2, 512, 3, 80), (1, 2048, 2, 80), (2, 256, 2, 128), (4, 2048, 2, 128)])
 @pytest.mark.parametrize("causal", [True, False])
 def test_attention_fwd_bwd(K, B, S, H, D, causal):
     torch.manual_seed(3)
@@ -266,7 +266,8 @@ def test_attention_fwd_bwd(K, B, S, H, D, causal):
         assert _rel(dqkv[:, part * hd:(part + 1) * hd], g[:, part * hd:(part + 1) * hd]) < 2e-2
 
 
-@pytest.mark.parametrize("B,S,H,D", [(3, 128, 4, 32), (3, 256, 3, 64), (3, 512, 2, 128), (2, 192, 2, 80)])
+@pytest.mark.parametrize("B,S,H,D", [(3, 128, 4, 32), (3, 64, 4, 32), (3, 128, 2, 64), (3, 256, 3, 64), (3, 512, 2, 128),
+                                     (2, 512, 2, 80)])
 def test_attention_key_padding(K, B, S, H, D):
     """Bidirectional attention with key_len[b] (BERT padding): keys >= key_len[b] get zero
     probability; their dK / dV are exactly zero.  Lengths cover a full tile, a ragged tail
@@ -274,7 +275,7 @@ def test_attention_key_padding(K, B, S, H, D):
     torch.manual_seed(8)
     qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
     dout = torch.randn(B * S, H * D, device="cuda").bfloat16()
-    lens = [S, S // 2 + 37, 1, 100][:B]
+    lens = [S, S // 2 + 17, 1, 100][:B]
     key_len = torch.tensor(lens, dtype=torch.int32, device="cuda")
     out, lse = K.attention_fwd(qkv, B, S, H, D, False, key_len=key_len)
     x = qkv.float().requires_grad_()
@@ -291,6 +292,18 @@ def test_attention_key_padding(K, B, S, H, D):
         assert not dqkv[b * S + n:(b + 1) * S, hd:].any()
     with pytest.raises(RuntimeError):  # causal + key padding is not a supported combination
         K.attention_fwd(qkv, B, S, H, D, True, key_len=key_len)
+
+
+def test_attention_impl_report(K, N):
+    """Every BASELINE model shape (and the tiny configuration) runs a tcgen05 kernel; shapes
+    neither the tiled nor the one-tile kernels take are rejected (no fallback path)."""
+    T = N.ATTN_IMPL_TCGEN05
+    for S, D in [(64, 32), (128, 32), (64, 64), (128, 64), (512, 64), (1024, 64), (2048, 128), (2048, 80)]:
+        assert N.lib.amdp_attention_impl(S, D, 0) == T and N.lib.amdp_attention_impl(S, D, 1) == T, (S, D)
+    assert N.lib.amdp_attention_impl(192, 80, 0) == -1 and N.lib.amdp_attention_impl(128, 128, 1) == -1
+    qkv = torch.randn(192, 3 * 2 * 80, device="cuda").bfloat16()
+    with pytest.raises(RuntimeError):
+        K.attention_fwd(qkv, 1, 192, 2, 80, True)
 
 
 # (M, N, K, seg, seq): the 1.3B dO GEMM (8192x2048, 256 tiles -> tail split), a 350M-like
@@ -317,7 +330,7 @@ def test_gemm_rowdot(K, N, M, N_, K_, seg, seq):
     assert _rel(rowdot, want) < 1e-5
 
 
-@pytest.mark.parametrize("B,S,H,D", [(2, 256, 3, 64), (4, 2048, 2, 128), (1, 512, 2, 80)])
+@pytest.mark.parametrize("B,S,H,D", [(2, 256, 3, 64), (4, 2048, 2, 128), (1, 512, 2, 80), (4, 64, 4, 32), (2, 64, 3, 64)])
 @pytest.mark.parametrize("causal", [True, False])
 def test_attention_bwd_supplied_delta(K, B, S, H, D, causal):
     """amdp_attention_bwd_delta with delta = rowsum(dO * O) from the caller gives the same
