@@ -300,7 +300,7 @@ def test_attention_impl_report(K, N):
     T = N.ATTN_IMPL_TCGEN05
     for S, D in [(64, 32), (128, 32), (64, 64), (128, 64), (512, 64), (1024, 64), (2048, 128), (2048, 80)]:
         assert N.lib.amdp_attention_impl(S, D, 0) == T and N.lib.amdp_attention_impl(S, D, 1) == T, (S, D)
-    assert N.lib.amdp_attention_impl(192, 80, 0) == -1 and N.lib.amdp_attention_impl(128, 128, 1) == -1
+    assert N.lib.amdp_attention_impl(192, 80, 0) == -1 and N.lib.amdp_attention_impl(128, 128, 0) == -1
     qkv = torch.randn(192, 3 * 2 * 80, device="cuda").bfloat16()
     with pytest.raises(RuntimeError):
         K.attention_fwd(qkv, 1, 192, 2, 80, True)
