@@ -120,7 +120,7 @@ struct KvSmem {
   static constexpr uint32_t BYTES = BAR + 256;
 };
 
-template <int D>
+template <int D, bool KPAD>
 __global__ void __launch_bounds__(384, 1)
     fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap kv_map, const __grid_constant__ CUtensorMap qkv_map,
                        const __grid_constant__ CUtensorMap do_map, const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(384, 1)
     Tile t;
     for (int it = 0, g0 = 0; tile_of(it, t); g0 += 2 * t.N, ++it) {
       const int key = t.kt * 128 + r;
-      const bool kpad = key_len && key >= key_len[t.b];  // a padding key: no P, no dS
+      // a padding key (KPAD instances only: the unpadded kernel carries no mask code)
+      const bool kpad = KPAD && key >= key_len[t.b];
       const float* lse_bh = lse + (static_cast<size_t>(t.b) * H + t.h) * seq;
       const float* del_bh = delta + (static_cast<size_t>(t.b) * H + t.h) * seq;
       for (int n = 0; n < t.N; ++n) {
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(384, 1)
             if (qbase + cc + 2 < key) p1.x = 0.f;
             if (qbase + cc + 3 < key) p1.y = 0.f;
           }
-          if (kpad) p0 = p1 = make_float2(0.f, 0.f);
+          if (KPAD && kpad) p0 = p1 = make_float2(0.f, 0.f);
           const float2 g0 = __fmul2_rn(
               __fadd2_rn(make_float2(__uint_as_float(d[cc]), __uint_as_float(d[cc + 1])), make_float2(-dq.x, -dq.y)), p0);
           const float2 g1 = __fmul2_rn(
@@ -405,7 +406,7 @@ struct QSmem {
 // tiles, so the next tile's loads land during this tile's last blocks and epilogue instead of
 // behind a fresh CTA's prologue (the non-persistent version spent ~9k cycles before its
 // first MMA: profiles/r01_attn_traces.md).
-template <int D>
+template <int D, bool KPAD>
 __global__ void __launch_bounds__(384, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap qkv_map, const __grid_constant__ CUtensorMap do_map,
                      const bf16* __restrict__ qkv, const float* __restrict__ lse, const float* __restrict__ delta,
@@ -614,11 +615,11 @@ __global__ void __launch_bounds__(384, 1)
         ptx::tc_fence_before();
         ptx::mbar_arrive(q_full);
       }
-      const int klen = key_len ? key_len[b] : seq;  // key padding (bidirectional models)
+      const int klen = KPAD ? key_len[b] : seq;  // key padding (bidirectional models)
       for (int n = 0; n < N; ++n) {
         const int g = g0 + n;
         const bool diag = causal && n == N - 1;
-        const bool lim = (n + 1) * 128 > klen;
+        const bool lim = KPAD && (n + 1) * 128 > klen;
         ptx::mbar_wait(s_full, g & 1);
         if (it == 0 && lane == 0 && q == 0 && wg == 0) BW_T(3, n);
         ptx::tc_fence_after();
@@ -638,12 +639,17 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
         for (int cc = 0; cc < 64; cc += 2) {
           // packed pairs; FA_BWD_POLY_PAIRS of every 4 exponent pairs on the FMA pipe
+#ifdef FA_DQ_SCALAR
+          float g0f = ex2(fmaf(__uint_as_float(s[cc]), scale_log2, nl)) * (__uint_as_float(d[cc]) - dl);
+          float g1f = ex2(fmaf(__uint_as_float(s[cc + 1]), scale_log2, nl)) * (__uint_as_float(d[cc + 1]) - dl);
+#else
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[cc]), __uint_as_float(s[cc + 1])),
                                       make_float2(scale_log2, scale_log2), make_float2(nl, nl));
           const float2 p = ((cc >> 1) & 3) < FA_BWD_POLY_PAIRS ? ex2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
           const float2 gv = __fmul2_rn(p, __fadd2_rn(make_float2(__uint_as_float(d[cc]), __uint_as_float(d[cc + 1])),
                                                      make_float2(-dl, -dl)));
           float g0f = gv.x, g1f = gv.y;
+#endif
           if (diag) {
             const int k0 = n * 128 + c0 + cc;
             if (k0 > qrow) g0f = 0.f;
@@ -706,8 +712,10 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   static std::atomic<uint64_t> attr{0};
   const size_t smem_kv = KvSmem<D>::BYTES + 1024, smem_q = QSmem<D>::BYTES + 1024;
   if (first_on_device(attr)) {
-    int e = set_smem(fa_bwd_dkdv_kernel<D>, smem_kv);
-    if (!e) e = set_smem(fa_bwd_dq_kernel<D>, smem_q);
+    int e = set_smem(fa_bwd_dkdv_kernel<D, false>, smem_kv);
+    if (!e) e = set_smem(fa_bwd_dkdv_kernel<D, true>, smem_kv);
+    if (!e) e = set_smem(fa_bwd_dq_kernel<D, false>, smem_q);
+    if (!e) e = set_smem(fa_bwd_dq_kernel<D, true>, smem_q);
     if (e) {
       attr.store(0);
       return e;
@@ -715,13 +723,14 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   }
   const int nt = S / 128;
   const int kv_grid = std::min(nt * H * B, num_sms());  // persistent
-  cudaError_t e = launch_pdl(fa_bwd_dkdv_kernel<D>, dim3(kv_grid), dim3(384), smem_kv, st, q128, q64, o64, lse,
-                             delta, dqkv, S, H, nt, H * B, scale_log2, scale, causal, key_len);
+  cudaError_t e = launch_pdl(key_len ? fa_bwd_dkdv_kernel<D, true> : fa_bwd_dkdv_kernel<D, false>, dim3(kv_grid),
+                             dim3(384), smem_kv, st, q128, q64, o64, lse, delta, dqkv, S, H, nt, H * B, scale_log2,
+                             scale, causal, key_len);
   if (e != cudaSuccess) return e;
   const int dq_grid = std::min(nt * H * B, num_sms());  // persistent
   static const int early = getenv("AMDP_ATTN_DQ_EARLY") ? atoi(getenv("AMDP_ATTN_DQ_EARLY")) : 1;
-  e = launch_pdl(fa_bwd_dq_kernel<D>, dim3(dq_grid), dim3(384), smem_q, st, q128, o128, qkv, lse, delta, dqkv, S, H,
-                 nt, H * B, scale_log2, scale, causal, early, key_len);
+  e = launch_pdl(key_len ? fa_bwd_dq_kernel<D, true> : fa_bwd_dq_kernel<D, false>, dim3(dq_grid), dim3(384), smem_q,
+                 st, q128, o128, qkv, lse, delta, dqkv, S, H, nt, H * B, scale_log2, scale, causal, early, key_len);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
