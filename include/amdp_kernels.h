@@ -86,8 +86,14 @@ int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse, int batch
                        int heads, int head_dim, int causal, const int32_t* key_len,
                        amdp_stream_t stream);
 /* dout: [batch*seq][H*D]; writes dqkv [batch*seq][3*H*D] (dq | dk | dv).
- * workspace: at least amdp_attention_bwd_workspace() bytes.                        */
+ * workspace: at least amdp_attention_bwd_workspace() bytes (either causal value), or
+ * amdp_attention_bwd_workspace_causal() for the causal value passed: delta[batch][H][seq]
+ * (padded to 256 B), then the dS^T scratch of the tiled kernels
+ * (amdp_attention_bwd_scratch_bytes: the dK/dV kernel stores dS^T there and dQ = dS K reads
+ * it back instead of recomputing S, dP and the softmax).                             */
 size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim);
+size_t amdp_attention_bwd_workspace_causal(int batch, int seq, int heads, int head_dim, int causal);
+size_t amdp_attention_bwd_scratch_bytes(int batch, int seq, int heads, int head_dim, int causal);
 /* The same backward with delta[batch][H][seq] = rowsum(dout * out) per head supplied by the
  * caller (e.g. from the dO GEMM's AMDP_EPI_ROWDOT epilogue); tcgen05 path only
  * (amdp_attention_bwd_delta_supported), AMDP_ERR_UNSUPPORTED otherwise.             */
@@ -103,6 +109,11 @@ int amdp_attention_impl(int seq, int head_dim, int backward);
 int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse, const float* delta,
                              uint16_t* dqkv, int batch, int seq, int heads, int head_dim, int causal,
                              const int32_t* key_len, amdp_stream_t stream);
+/* amdp_attention_bwd_delta with the dS^T scratch (amdp_attention_bwd_scratch_bytes for this
+ * causal value; NULL = the dQ kernel that recomputes S / dP instead).                 */
+int amdp_attention_bwd_delta_ws(const uint16_t* qkv, const uint16_t* dout, const float* lse, const float* delta,
+                                uint16_t* dqkv, void* scratch, int batch, int seq, int heads, int head_dim,
+                                int causal, const int32_t* key_len, amdp_stream_t stream);
 int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                        const float* lse, uint16_t* dqkv, void* workspace, int batch, int seq,
                        int heads, int head_dim, int causal, const int32_t* key_len,

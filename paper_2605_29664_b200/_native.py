@@ -71,6 +71,10 @@ _sig("amdp_attention_impl", c_int, [c_int, c_int, c_int])
 _sig("amdp_gelu_fwd", c_int, [_P, _P, c_int64, _P])
 _sig("amdp_attention_bwd_delta", c_int,
      [_P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P, _P])
+_sig("amdp_attention_bwd_delta_ws", c_int,
+     [_P, _P, _P, _P, _P, _P, c_int, c_int, c_int, c_int, c_int, _P, _P])
+_sig("amdp_attention_bwd_workspace_causal", c_size_t, [c_int, c_int, c_int, c_int, c_int])
+_sig("amdp_attention_bwd_scratch_bytes", c_size_t, [c_int, c_int, c_int, c_int, c_int])
 _sig("amdp_layernorm_fwd", c_int, [_P, _P, _P, _P, _P, _P, c_int, c_int, c_float, _P])
 _sig("amdp_layernorm_bwd_workspace", c_size_t, [c_int, c_int])
 _sig("amdp_layernorm_bwd", c_int,

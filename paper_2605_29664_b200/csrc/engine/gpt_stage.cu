@@ -208,7 +208,7 @@ Ws carve_ws(const Dims& d, uint8_t* base) {
   w.dqkv = c.take<uint16_t>(E * T * 3 * h);
   w.dtmp = c.take<uint16_t>(E * T * h);
   w.dhmid = c.take<uint16_t>(E * T * h);
-  w.attn = c.take<float>(std::max(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd),
+  w.attn = c.take<float>(std::max(amdp_attention_bwd_workspace_causal(d.B, d.S, d.heads, d.hd, d.causal ? 1 : 0),
                                  amdp_f32_attention_bwd_workspace(d.B, d.S, d.heads)) / sizeof(float) + 1);
   w.ln = c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
   w.rows = c.take<float>(T);
@@ -230,7 +230,7 @@ size_t GptStage::workspace_bytes(const Dims& d) {
   c.take<uint16_t>(E * T * 3 * h);
   c.take<uint16_t>(E * T * h);
   c.take<uint16_t>(E * T * h);
-  c.take<float>(std::max(amdp_attention_bwd_workspace(d.B, d.S, d.heads, d.hd),
+  c.take<float>(std::max(amdp_attention_bwd_workspace_causal(d.B, d.S, d.heads, d.hd, d.causal ? 1 : 0),
                                  amdp_f32_attention_bwd_workspace(d.B, d.S, d.heads)) / sizeof(float) + 1);
   c.take<uint8_t>(amdp_layernorm_bwd_workspace(d.T, d.h));
   c.take<float>(T);
@@ -447,8 +447,11 @@ int GptStage::backward(const SlotActs& a, const int32_t* tokens, const uint16_t*
     }
     if (sd != s) cudaStreamWaitEvent(s, ss.ev[F_DQ], 0);  // previous layer's dWqkv done with dqkv
     if (fuse_delta) {
-      AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd_delta(A.qkv, ws.dtmp, A.lse, ws.attn, ws.dqkv, d_.B, d_.S,
-                                  d_.heads, d_.hd, d_.causal ? 1 : 0, key_len, st), 2);
+      // workspace layout of amdp_attention_bwd_workspace_causal: delta, then the dS^T scratch
+      uint8_t* scratch = reinterpret_cast<uint8_t*>(ws.attn) +
+                         ((static_cast<size_t>(d_.B) * d_.S * d_.heads * sizeof(float) + 255) & ~static_cast<size_t>(255));
+      AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd_delta_ws(A.qkv, ws.dtmp, A.lse, ws.attn, ws.dqkv,
+                                  scratch, d_.B, d_.S, d_.heads, d_.hd, d_.causal ? 1 : 0, key_len, st), 2);
     } else {
       AMDP_TRY(K_ATTN_BWD, 2.5 * attn_fwd_flops(), 0, amdp_attention_bwd(A.qkv, A.o, ws.dtmp, A.lse, ws.dqkv, ws.attn, d_.B, d_.S, d_.heads, d_.hd,
                                   d_.causal ? 1 : 0, key_len, st), 3);

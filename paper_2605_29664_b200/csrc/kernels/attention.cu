@@ -70,7 +70,8 @@ namespace amdp {
 int attention_fwd_tc(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int D, int causal,
                      const int32_t* key_len, cudaStream_t st);
 int attention_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
-                     int S, int H, int D, int causal, const int32_t* key_len, cudaStream_t st);
+                     int S, int H, int D, int causal, const int32_t* key_len, uint8_t* ds_ws, cudaStream_t st);
+size_t attention_bwd_ds_bytes(int B, int S, int H, int causal);
 // attention_short_tc.cu: seq <= 128, head_dim 32 / 64 (one 128 x 128 tile per sequence and head)
 bool attention_short_supported(int S, int D);
 int attention_fwd_short(const bf16* qkv, bf16* out, float* lse, int B, int S, int H, int D, int causal,
@@ -97,9 +98,31 @@ extern "C" int amdp_attention_fwd(const uint16_t* qkv, uint16_t* out, float* lse
   return AMDP_ERR_UNSUPPORTED;
 }
 
-extern "C" int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse,
-                                        const float* delta, uint16_t* dqkv, int batch, int seq, int heads,
-                                        int head_dim, int causal, const int32_t* key_len, amdp_stream_t stream) {
+namespace {
+// workspace = [delta: batch * heads * seq floats, padded to 256 B][dS^T scratch of the tiled path]
+size_t delta_bytes(int batch, int seq, int heads) {
+  return (static_cast<size_t>(batch) * seq * heads * sizeof(float) + 255) & ~static_cast<size_t>(255);
+}
+}  // namespace
+
+extern "C" size_t amdp_attention_bwd_scratch_bytes(int batch, int seq, int heads, int head_dim, int causal) {
+  if (batch <= 0 || seq <= 0 || heads <= 0 || !attention_tiled_bwd(seq, head_dim)) return 0;
+  return attention_bwd_ds_bytes(batch, seq, heads, causal ? 1 : 0);
+}
+
+extern "C" size_t amdp_attention_bwd_workspace_causal(int batch, int seq, int heads, int head_dim, int causal) {
+  return delta_bytes(batch, seq, heads) + amdp_attention_bwd_scratch_bytes(batch, seq, heads, head_dim, causal);
+}
+
+extern "C" size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim) {
+  // bidirectional scratch: an upper bound for either value of causal
+  return amdp_attention_bwd_workspace_causal(batch, seq, heads, head_dim, 0);
+}
+
+extern "C" int amdp_attention_bwd_delta_ws(const uint16_t* qkv, const uint16_t* dout, const float* lse,
+                                           const float* delta, uint16_t* dqkv, void* scratch, int batch, int seq,
+                                           int heads, int head_dim, int causal, const int32_t* key_len,
+                                           amdp_stream_t stream) {
   if (batch <= 0 || seq <= 0 || heads <= 0 || !delta) return AMDP_ERR_INVALID;
   if (causal && key_len) return AMDP_ERR_UNSUPPORTED;
   if (!amdp_attention_bwd_delta_supported(seq, head_dim)) return AMDP_ERR_UNSUPPORTED;
@@ -109,7 +132,14 @@ extern "C" int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dou
                                reinterpret_cast<cudaStream_t>(stream));
   return attention_bwd_tc(reinterpret_cast<const bf16*>(qkv), reinterpret_cast<const bf16*>(dout), lse,
                           const_cast<float*>(delta), reinterpret_cast<bf16*>(dqkv), batch, seq, heads, head_dim,
-                          causal, key_len, reinterpret_cast<cudaStream_t>(stream));
+                          causal, key_len, static_cast<uint8_t*>(scratch), reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int amdp_attention_bwd_delta(const uint16_t* qkv, const uint16_t* dout, const float* lse,
+                                        const float* delta, uint16_t* dqkv, int batch, int seq, int heads,
+                                        int head_dim, int causal, const int32_t* key_len, amdp_stream_t stream) {
+  return amdp_attention_bwd_delta_ws(qkv, dout, lse, delta, dqkv, nullptr, batch, seq, heads, head_dim, causal,
+                                     key_len, stream);
 }
 
 extern "C" int amdp_attention_impl(int seq, int head_dim, int backward) {
@@ -124,10 +154,7 @@ extern "C" int amdp_attention_bwd_delta_supported(int seq, int head_dim) {
   return attention_tiled_bwd(seq, head_dim) || attention_short_supported(seq, head_dim);
 }
 
-extern "C" size_t amdp_attention_bwd_workspace(int batch, int seq, int heads, int head_dim) {
-  (void)head_dim;
-  return static_cast<size_t>(batch) * seq * heads * sizeof(float);
-}
+
 
 extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, const uint16_t* dout,
                                   const float* lse, uint16_t* dqkv, void* workspace, int batch,
@@ -155,7 +182,8 @@ extern "C" int amdp_attention_bwd(const uint16_t* qkv, const uint16_t* out, cons
     }
     if (!attention_tiled_bwd(seq, head_dim))
       return attention_bwd_short(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, key_len, s);
-    return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, key_len, s);
+    return attention_bwd_tc(q, d, lse, w, dq, batch, seq, heads, head_dim, causal, key_len,
+                            static_cast<uint8_t*>(workspace) + delta_bytes(batch, seq, heads), s);
   }
   return AMDP_ERR_UNSUPPORTED;
 }

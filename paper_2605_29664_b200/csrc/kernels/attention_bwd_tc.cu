@@ -21,6 +21,8 @@
 // the N=64 / N=128 MMAs here (dQ kernel 166 -> 146 us).
 // lse / delta use the forward's log2-domain convention (softmax scale folded in);
 // delta = rowsum(dO * O) comes from attn_bwd_delta_vec_kernel (attention.cu).
+#include <cstring>
+
 #include "common.cuh"
 #include "sm100_ptx.cuh"
 #include "tma_host.hpp"
@@ -106,6 +108,21 @@ __device__ __forceinline__ void tmem_row_to_global(uint32_t src, bf16* dst, floa
 // half-block MMA groups ahead of its first use; lse / delta are read from L2 (broadcast).
 constexpr uint32_t T64 = 8192;  // [64 rows][64 bf16] SW128 tile
 
+// dS^T scratch for the dQ GEMM: per (sequence, head), one 16 KB chunk per (128-key tile kt,
+// 64-query half-block) the dK/dV kernel visits, holding dS [64 queries][128 keys] bf16 as two
+// 8 KB key halves, each [8 query groups][64 keys][8 queries] (16-byte unit of key r, queries
+// 8v..8v+7 at (r / 64) 8192 + v 1024 + (r % 64) 16).  That is the no-swizzle MN-major core-
+// matrix layout of the MMA operand (8 keys x 16 bytes contiguous), so the dQ kernel moves a key
+// half with one bulk copy and hands it to the MMA as is, and the dK/dV threads (thread = key)
+// store it coalesced: a warp's 16-byte stores of one query group cover 512 contiguous bytes.
+// Key tile kt's chunks are consecutive (causal: query blocks kt..nqb-1, else all), two per
+// 128-query block.
+constexpr uint32_t DS_CHUNK = 16384;
+__host__ __device__ inline int ds_chunks_per_head(int nqb, int causal) { return causal ? nqb * (nqb + 1) : 2 * nqb * nqb; }
+__host__ __device__ inline int ds_chunk_offset(int nqb, int kt, int causal) {
+  return causal ? kt * (2 * nqb - kt + 1) : 2 * kt * nqb;
+}
+
 // head_dim 80 uses the 128-wide layout (two SW128 boxes per row tile; see attention_tc.cu):
 // K-dim loops run D/16 steps, the D-wide outputs are N = D MMAs, TMEM keeps 128-column slots.
 template <int D>
@@ -125,7 +142,7 @@ __global__ void __launch_bounds__(384, 1)
     fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap kv_map, const __grid_constant__ CUtensorMap qkv_map,
                        const __grid_constant__ CUtensorMap do_map, const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv,
                        int seq, int H, int n_kt, int BH, float scale_log2, float scale, int causal,
-                       const int32_t* __restrict__ key_len) {
+                       const int32_t* __restrict__ key_len, uint8_t* __restrict__ ds_ws) {
   using L = KvSmem<D>;
   constexpr int NU = L::NU;
   extern __shared__ uint8_t smem_raw[];
@@ -305,6 +322,12 @@ __global__ void __launch_bounds__(384, 1)
       const bool kpad = KPAD && key >= key_len[t.b];
       const float* lse_bh = lse + (static_cast<size_t>(t.b) * H + t.h) * seq;
       const float* del_bh = delta + (static_cast<size_t>(t.b) * H + t.h) * seq;
+      // dS^T chunks of this tile (dQ GEMM operand, see DS_CHUNK): this thread's key in chunk
+      // (block n, half x)
+      uint8_t* ds_row = ds_ws == nullptr ? nullptr
+                                         : ds_ws + ((static_cast<size_t>(t.b) * H + t.h) * ds_chunks_per_head(nqb, causal) +
+                                                    ds_chunk_offset(nqb, t.kt, causal) + x) * DS_CHUNK +
+                                               (r >> 6) * 8192 + (r & 63) * 16;
       for (int n = 0; n < t.N; ++n) {
         const int u = g0 + 2 * n + x;
         const int qbase = (t.i0 + n) * 128 + 64 * x;
@@ -364,6 +387,14 @@ __global__ void __launch_bounds__(384, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_full[x]);
+        // dS^T for the dQ GEMM, after the hand-off (the arrive's release would otherwise wait
+        // for these global stores)
+        if (ds_row != nullptr) {
+          uint8_t* dst = ds_row + static_cast<size_t>(2 * n) * DS_CHUNK;
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            *reinterpret_cast<uint4*>(dst + v * 1024) = make_uint4(dd[4 * v], dd[4 * v + 1], dd[4 * v + 2], dd[4 * v + 3]);
+        }
         if (threadIdx.x == 128) BW_T(7, u);
       }
       ptx::mbar_wait(kv_done, it & 1);
@@ -693,6 +724,106 @@ __global__ void __launch_bounds__(384, 1)
   if (early) ptx::pdl_wait();  // the dK/dV grid has completed before this one does
 }
 
+// ==================================================================== dQ GEMM
+// dQ = scale * dS K per (128-query tile, head, sequence), from the dS^T chunks the dK/dV kernel
+// stored (DS_CHUNK): no second pass over S, dP and the softmax.  A plain K-loop over the
+// tile's keys, 64 per stage:  A = dS [128 queries][64 keys] (MN-major, no swizzle: the matching
+// 8 KB key halves of the block's two chunks, one bulk copy each), B = K [64 keys][D]
+// (MN-major, D/64 TMA boxes), fp32 accumulator [128 queries][D] in TMEM.  One warp loads, one
+// issues the MMAs, four drain TMEM; 64-72 KB of smem, so three CTAs share an SM.  Deterministic:
+// every dQ element sums its keys in one accumulator in a fixed order.
+template <int D, int NS_>
+struct DqgSmem {
+  static constexpr int NB = (D + 63) / 64;
+  static constexpr int NS = NS_;
+  static constexpr uint32_t A = 2 * T64;
+  static constexpr uint32_t STAGE = A + NB * T64;
+  static constexpr uint32_t BAR = NS * STAGE;
+  static constexpr uint32_t BYTES = BAR + 128;
+};
+
+template <int D, int NS_>
+__global__ void __launch_bounds__(192, 1)
+    fa_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap k64_map, const uint8_t* __restrict__ ds_ws,
+                          bf16* __restrict__ dqkv, int seq, int H, int n_qt, int BH, float scale, int causal) {
+  using L = DqgSmem<D, NS_>;
+  constexpr int NS = L::NS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::BAR);  // [NS]
+  uint64_t* empty = full + NS;                                   // [NS]
+  uint64_t* acc_full = empty + NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int idx = static_cast<int>(blockIdx.x);
+  const int qt = causal ? n_qt - 1 - idx / BH : idx / BH;  // causal: heavy tiles first
+  const int hb = idx % BH, h = hb % H, b = hb / H;
+  const int steps = 2 * (causal ? qt + 1 : n_qt);  // 64-key stages
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch(&k64_map);
+    for (int s = 0; s < NS; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(acc_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<128>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  ptx::pdl_wait();  // dS^T comes from the dK/dV grid
+  ptx::pdl_trigger();
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint8_t* ds_head = ds_ws + static_cast<size_t>(hb) * ds_chunks_per_head(n_qt, causal) * DS_CHUNK;
+      for (int j = 0; j < steps; ++j) {
+        const int s = j % NS, kt = j >> 1, hk = j & 1;
+        uint8_t* st = sm + s * L::STAGE;
+        ptx::mbar_wait(&empty[s], ((j / NS) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[s], L::STAGE);
+        const uint8_t* c0 = ds_head +
+                            static_cast<size_t>(ds_chunk_offset(n_qt, kt, causal) + 2 * (qt - (causal ? kt : 0))) * DS_CHUNK +
+                            hk * T64;
+        ptx::bulk_load(st, c0, T64, &full[s]);                  // queries [0, 64), keys 64 hk + [0, 64)
+        ptx::bulk_load(st + T64, c0 + DS_CHUNK, T64, &full[s]);  // queries [64, 128)
+        for (int c = 0; c < L::NB; ++c)
+          ptx::tma_load_2d(st + L::A + c * T64, &k64_map, &full[s], H * D + h * D + 64 * c, b * seq + kt * 128 + hk * 64);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id = ptx::idesc_bf16_f32(128, D, true, true);  // A, B MN-major
+    for (int j = 0; j < steps; ++j) {
+      const int s = j % NS;
+      ptx::mbar_wait(&full[s], (j / NS) & 1);
+      ptx::tc_fence_after();
+      // A: core matrices of 8 keys x 8 queries, 128 B apart along keys, 1024 B along queries
+      const uint64_t ad = ptx::umma_desc_noswz(ptx::smem_u32(sm + s * L::STAGE), 128, 1024);
+      const uint64_t bd = ptx::umma_desc_sw128(ptx::smem_u32(sm + s * L::STAGE + L::A), T64, 1024);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA: A +256 B, B +2048 B (16 SW128 rows)
+        ptx::mma_bf16_ss_w(tmem, ad + kk * 16, bd + kk * 128, id, (j > 0 || kk > 0) ? 1u : 0u);
+      ptx::mma_commit_w(&empty[s]);
+    }
+    ptx::mma_commit_w(acc_full);
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter of this warp (warps 2..5 -> 2, 3, 0, 1)
+    ptx::mbar_wait(acc_full, 0);
+    ptx::tc_fence_after();
+    const int row = q * 32 + lane;
+    bf16* dst = dqkv + (static_cast<size_t>(b) * seq + qt * 128 + row) * (static_cast<size_t>(3) * H * D) + h * D;
+    tmem_row_to_global<D>(tmem + (static_cast<uint32_t>(q * 32) << 16), dst, scale);
+    ptx::tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<128>(tmem);
+  }
+}
+
 template <class K>
 int set_smem(K k, size_t bytes) {
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
@@ -700,7 +831,7 @@ int set_smem(K k, size_t bytes) {
 
 template <int D>
 int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
-                  int S, int H, int causal, const int32_t* key_len, cudaStream_t st) {
+                  int S, int H, int causal, const int32_t* key_len, uint8_t* ds_ws, cudaStream_t st) {
   CUtensorMap q128, o128, q64, o64;
   const uint64_t ldq = static_cast<uint64_t>(3) * H * D, ldo = static_cast<uint64_t>(H) * D;
   const uint64_t rows = static_cast<uint64_t>(B) * S;
@@ -710,12 +841,20 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
   static std::atomic<uint64_t> attr{0};
+  // dQ GEMM ring depth (AMDP_ATTN_DQ_STAGES; measured best: head_dim 128 two stages = three CTAs per SM,
+  // head_dim 64 three = three CTAs per SM; scripts/attn_dq_probe.py)
+  static const int dq_stages = getenv("AMDP_ATTN_DQ_STAGES") ? atoi(getenv("AMDP_ATTN_DQ_STAGES")) : (D > 64 ? 2 : 3);
+  auto dq_gemm = dq_stages == 2 ? fa_bwd_dq_gemm_kernel<D, 2> : dq_stages == 3 ? fa_bwd_dq_gemm_kernel<D, 3>
+                                                                               : fa_bwd_dq_gemm_kernel<D, 4>;
+  const size_t smem_g = 1024 + (dq_stages == 2 ? DqgSmem<D, 2>::BYTES : dq_stages == 3 ? DqgSmem<D, 3>::BYTES
+                                                                                       : DqgSmem<D, 4>::BYTES);
   const size_t smem_kv = KvSmem<D>::BYTES + 1024, smem_q = QSmem<D>::BYTES + 1024;
   if (first_on_device(attr)) {
     int e = set_smem(fa_bwd_dkdv_kernel<D, false>, smem_kv);
     if (!e) e = set_smem(fa_bwd_dkdv_kernel<D, true>, smem_kv);
     if (!e) e = set_smem(fa_bwd_dq_kernel<D, false>, smem_q);
     if (!e) e = set_smem(fa_bwd_dq_kernel<D, true>, smem_q);
+    if (!e) e = set_smem(dq_gemm, smem_g);
     if (e) {
       attr.store(0);
       return e;
@@ -725,8 +864,13 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   const int kv_grid = std::min(nt * H * B, num_sms());  // persistent
   cudaError_t e = launch_pdl(key_len ? fa_bwd_dkdv_kernel<D, true> : fa_bwd_dkdv_kernel<D, false>, dim3(kv_grid),
                              dim3(384), smem_kv, st, q128, q64, o64, lse, delta, dqkv, S, H, nt, H * B, scale_log2,
-                             scale, causal, key_len);
+                             scale, causal, key_len, ds_ws);
   if (e != cudaSuccess) return e;
+  if (ds_ws != nullptr) {  // dQ = dS K from the stored dS^T
+    e = launch_pdl(dq_gemm, dim3(nt * H * B), dim3(192), smem_g, st, q64, ds_ws, dqkv, S, H, nt,
+                   H * B, scale, causal);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   const int dq_grid = std::min(nt * H * B, num_sms());  // persistent
   static const int early = getenv("AMDP_ATTN_DQ_EARLY") ? atoi(getenv("AMDP_ATTN_DQ_EARLY")) : 1;
   e = launch_pdl(key_len ? fa_bwd_dq_kernel<D, true> : fa_bwd_dq_kernel<D, false>, dim3(dq_grid), dim3(384), smem_q,
@@ -737,13 +881,21 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
 }  // namespace
 
 // Used by amdp_attention_bwd (after the delta pre-pass) when the tensor-core path applies.
+// ds_ws: dS^T scratch of attention_bwd_ds_bytes(); nullptr selects the dQ kernel that
+// recomputes S / dP (AMDP_ATTN_DQ=recompute; A/B only).
 int attention_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const float* delta, bf16* dqkv, int B,
-                     int S, int H, int D, int causal, const int32_t* key_len, cudaStream_t st) {
+                     int S, int H, int D, int causal, const int32_t* key_len, uint8_t* ds_ws, cudaStream_t st) {
   if (S % 128 != 0) return AMDP_ERR_UNSUPPORTED;
-  if (D == 128) return launch_bwd_tc<128>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, st);
-  if (D == 64) return launch_bwd_tc<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, st);
-  if (D == 80) return launch_bwd_tc<80>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, st);
+  static const bool recompute = getenv("AMDP_ATTN_DQ") && strcmp(getenv("AMDP_ATTN_DQ"), "recompute") == 0;
+  if (recompute || D == 80) ds_ws = nullptr;  // head_dim 80: storing dS^T costs the dK/dV kernel more than it saves
+  if (D == 128) return launch_bwd_tc<128>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, ds_ws, st);
+  if (D == 64) return launch_bwd_tc<64>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, ds_ws, st);
+  if (D == 80) return launch_bwd_tc<80>(qkv, dout, lse, delta, dqkv, B, S, H, causal, key_len, ds_ws, st);
   return AMDP_ERR_UNSUPPORTED;
+}
+
+size_t attention_bwd_ds_bytes(int B, int S, int H, int causal) {
+  return static_cast<size_t>(B) * H * ds_chunks_per_head(S / 128, causal) * DS_CHUNK;
 }
 
 }  // namespace amdp

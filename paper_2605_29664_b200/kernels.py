@@ -59,11 +59,21 @@ def attention_bwd(qkv, out, dout, lse, batch, seq, heads, head_dim, causal=True,
     return dqkv
 
 
-def attention_bwd_delta(qkv, dout, lse, delta, batch, seq, heads, head_dim, causal=True, key_len=None):
-    """Backward with delta [batch][heads][seq] supplied (amdp_attention_bwd_delta)."""
+def attention_bwd_delta(qkv, dout, lse, delta, batch, seq, heads, head_dim, causal=True, key_len=None,
+                        scratch=True):
+    """Backward with delta [batch][heads][seq] supplied.  scratch=True: amdp_attention_bwd_delta_ws
+    (dK/dV store dS^T, dQ = dS K; the engine's path); False: amdp_attention_bwd_delta (the dQ
+    kernel recomputes S / dP)."""
     dqkv = torch.empty_like(qkv)
-    N.check(N.lib.amdp_attention_bwd_delta(_p(qkv), _p(dout), _p(lse), _p(delta), _p(dqkv), batch, seq, heads,
-                                           head_dim, int(causal), _p(key_len), _stream()), "amdp_attention_bwd_delta")
+    if scratch:
+        ws = torch.empty(max(1, N.lib.amdp_attention_bwd_scratch_bytes(batch, seq, heads, head_dim, int(causal))),
+                         dtype=torch.uint8, device=qkv.device)
+        N.check(N.lib.amdp_attention_bwd_delta_ws(_p(qkv), _p(dout), _p(lse), _p(delta), _p(dqkv), _p(ws), batch, seq,
+                                                  heads, head_dim, int(causal), _p(key_len), _stream()),
+                "amdp_attention_bwd_delta_ws")
+    else:
+        N.check(N.lib.amdp_attention_bwd_delta(_p(qkv), _p(dout), _p(lse), _p(delta), _p(dqkv), batch, seq, heads,
+                                               head_dim, int(causal), _p(key_len), _stream()), "amdp_attention_bwd_delta")
     return dqkv
 
 

@@ -47,6 +47,10 @@ for name, B, S, H, D, causal in SHAPES:
     fl = 4.0 * B * H * S * S * D / (2 if causal else 1)
     f = per_call(lambda: K.attention_fwd(qkv, B, S, H, D, causal))
     b = per_call(lambda: K.attention_bwd(qkv, out, dout, lse, B, S, H, D, causal))
+    # the engine's call: delta supplied (dO GEMM epilogue); dQ from stored dS^T vs recomputed
+    delta = (dout.float() * out.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).contiguous()
+    bd = per_call(lambda: K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal))
+    br = per_call(lambda: K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal, scratch=False))
     q, k, v = [t.contiguous() for t in qkv.view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)]
     sd = per_call(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=causal))
     qq, kk, vv = [t.detach().clone().requires_grad_() for t in (q, k, v)]
@@ -56,4 +60,6 @@ for name, B, S, H, D, causal in SHAPES:
     print(json.dumps({"shape": name, "B": B, "S": S, "H": H, "D": D, "causal": causal,
                       "fwd_us": round(1e3 * f, 2), "fwd_tflops": round(fl / f / 1e9, 1),
                       "bwd_us": round(1e3 * b, 2), "bwd_tflops": round(2.5 * fl / b / 1e9, 1),
+                      "bwd_delta_us": round(1e3 * bd, 2), "bwd_delta_tflops": round(2.5 * fl / bd / 1e9, 1),
+                      "bwd_delta_recompute_dq_us": round(1e3 * br, 2),
                       "sdpa_fwd_us": round(1e3 * sd, 2), "sdpa_bwd_us": round(1e3 * sdb, 2)}), flush=True)

@@ -349,6 +349,38 @@ def test_attention_bwd_supplied_delta(K, B, S, H, D, causal):
         assert _rel(dqkv[:, part * hd:(part + 1) * hd], x.grad[:, part * hd:(part + 1) * hd]) < 2e-2
 
 
+@pytest.mark.parametrize("B,S,H,D,causal,padded", [(2, 256, 3, 64, True, False), (4, 2048, 2, 128, True, False),
+                                                    (1, 512, 2, 80, True, False), (2, 768, 2, 128, False, False),
+                                                    (4, 512, 3, 64, False, True), (3, 1024, 2, 64, True, False),
+                                                    (1, 256, 2, 128, True, False), (2, 2048, 2, 80, False, False)])
+def test_attention_bwd_ds_scratch(K, N, B, S, H, D, causal, padded):
+    """The engine's backward (dK/dV kernel stores dS^T chunks, dQ = dS K by fa_bwd_dq_gemm_kernel)
+    against torch fp32 and against the dQ kernel that recomputes S / dP: dK and dV come from the
+    same kernel (bit-identical), dQ agrees within bf16 rounding, and two runs are bit-identical
+    (no atomics).  Covers head_dim 64 / 80 / 128, causal and bidirectional, a single query tile,
+    a non-power-of-two tile count and BERT key padding."""
+    torch.manual_seed(11)
+    qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
+    dout = torch.randn(B * S, H * D, device="cuda").bfloat16()
+    key_len = torch.tensor([S, S // 2 + 17, 1, 100][:B], dtype=torch.int32, device="cuda") if padded else None
+    out, lse = K.attention_fwd(qkv, B, S, H, D, causal, key_len=key_len)
+    delta = (dout.float() * out.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).contiguous()
+    assert N.lib.amdp_attention_bwd_scratch_bytes(B, S, H, D, int(causal)) == B * H * 16384 * (
+        (S // 128) * (S // 128 + 1) if causal else 2 * (S // 128) ** 2)
+    d1 = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal, key_len=key_len)
+    d2 = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal, key_len=key_len)
+    d0 = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal, key_len=key_len, scratch=False)
+    x = qkv.float().requires_grad_()
+    _attn_ref(x, B, S, H, D, causal, key_len).backward(dout.float())
+    torch.cuda.synchronize()
+    hd = H * D
+    assert torch.equal(d1, d2)
+    assert torch.equal(d1[:, hd:], d0[:, hd:])
+    assert _rel(d1[:, :hd], d0[:, :hd]) < 5e-3
+    for part in range(3):
+        assert _rel(d1[:, part * hd:(part + 1) * hd], x.grad[:, part * hd:(part + 1) * hd]) < 2e-2
+
+
 @pytest.mark.parametrize("rows,cols", [(256, 128), (1000, 1024), (4096, 2048), (512, 2560)])
 def test_layernorm(K, rows, cols):
     torch.manual_seed(4)
