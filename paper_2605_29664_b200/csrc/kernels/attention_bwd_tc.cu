@@ -47,6 +47,11 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 16-byte global store that does not allocate in L1 (the dS^T stream would evict lse / delta)
+__device__ __forceinline__ void st_na_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&t);
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(384, 1)
           uint8_t* dst = ds_row + static_cast<size_t>(2 * n) * DS_CHUNK;
 #pragma unroll
           for (int v = 0; v < 8; ++v)
-            *reinterpret_cast<uint4*>(dst + v * 1024) = make_uint4(dd[4 * v], dd[4 * v + 1], dd[4 * v + 2], dd[4 * v + 3]);
+            st_na_v4(dst + v * 1024, dd[4 * v], dd[4 * v + 1], dd[4 * v + 2], dd[4 * v + 3]);
         }
         if (threadIdx.x == 128) BW_T(7, u);
       }
@@ -727,44 +732,53 @@ __global__ void __launch_bounds__(384, 1)
 // ==================================================================== dQ GEMM
 // dQ = scale * dS K per (128-query tile, head, sequence), from the dS^T chunks the dK/dV kernel
 // stored (DS_CHUNK): no second pass over S, dP and the softmax.  A plain K-loop over the
-// tile's keys, 64 per stage:  A = dS [128 queries][64 keys] (MN-major, no swizzle: the matching
+// tile's keys, 64 per step:  A = dS [128 queries][64 keys] (MN-major, no swizzle: the matching
 // 8 KB key halves of the block's two chunks, one bulk copy each), B = K [64 keys][D]
-// (MN-major, D/64 TMA boxes), fp32 accumulator [128 queries][D] in TMEM.  One warp loads, one
-// issues the MMAs, four drain TMEM; 64-72 KB of smem, so three CTAs share an SM.  Deterministic:
-// every dQ element sums its keys in one accumulator in a fixed order.
-template <int D, int NS_>
+// (MN-major, D/64 TMA boxes), fp32 accumulator [128 queries][D] in TMEM.  dS streams from HBM
+// once and K re-reads hit L2, so they have separate rings: a deep one for dS (bytes in flight
+// against DRAM latency) and a two-deep one for K, each with its own loading thread (warp 0 /
+// warp 2 lane 0); one warp issues the MMAs and four drain TMEM.  Deterministic: every dQ
+// element sums its keys in one accumulator in a fixed order.
+template <int D, int NA_, int NB_>
 struct DqgSmem {
   static constexpr int NB = (D + 63) / 64;
-  static constexpr int NS = NS_;
-  static constexpr uint32_t A = 2 * T64;
-  static constexpr uint32_t STAGE = A + NB * T64;
-  static constexpr uint32_t BAR = NS * STAGE;
+  static constexpr int NA = NA_, NK = NB_;  // dS / K ring depths
+  static constexpr uint32_t ASZ = 2 * T64, BSZ = NB * T64;
+  static constexpr uint32_t B0 = 0;                 // K ring first: SW128 boxes need 1024-B alignment
+  static constexpr uint32_t A0 = NK * BSZ;
+  static constexpr uint32_t BAR = A0 + NA * ASZ;
   static constexpr uint32_t BYTES = BAR + 128;
 };
 
-template <int D, int NS_>
+template <int D, int NA_, int NB_>
 __global__ void __launch_bounds__(192, 1)
     fa_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap k64_map, const uint8_t* __restrict__ ds_ws,
                           bf16* __restrict__ dqkv, int seq, int H, int n_qt, int BH, float scale, int causal) {
-  using L = DqgSmem<D, NS_>;
-  constexpr int NS = L::NS;
+  using L = DqgSmem<D, NA_, NB_>;
+  constexpr int NA = L::NA, NK = L::NK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + L::BAR);  // [NS]
-  uint64_t* empty = full + NS;                                   // [NS]
-  uint64_t* acc_full = empty + NS;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sm + L::BAR);  // [NA]
+  uint64_t* a_empty = a_full + NA;                                // [NA]
+  uint64_t* b_full = a_empty + NA;                                // [NK]
+  uint64_t* b_empty = b_full + NK;                                // [NK]
+  uint64_t* acc_full = b_empty + NK;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int idx = static_cast<int>(blockIdx.x);
   const int qt = causal ? n_qt - 1 - idx / BH : idx / BH;  // causal: heavy tiles first
   const int hb = idx % BH, h = hb % H, b = hb / H;
-  const int steps = 2 * (causal ? qt + 1 : n_qt);  // 64-key stages
+  const int steps = 2 * (causal ? qt + 1 : n_qt);  // 64-key steps
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&k64_map);
-    for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+    for (int s = 0; s < NA; ++s) {
+      ptx::mbar_init(&a_full[s], 1);
+      ptx::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < NK; ++s) {
+      ptx::mbar_init(&b_full[s], 1);
+      ptx::mbar_init(&b_empty[s], 1);
     }
     ptx::mbar_init(acc_full, 1);
     ptx::fence_mbar_init();
@@ -777,38 +791,49 @@ __global__ void __launch_bounds__(192, 1)
   ptx::pdl_wait();  // dS^T comes from the dK/dV grid
   ptx::pdl_trigger();
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0) {  // dS ring
       const uint8_t* ds_head = ds_ws + static_cast<size_t>(hb) * ds_chunks_per_head(n_qt, causal) * DS_CHUNK;
       for (int j = 0; j < steps; ++j) {
-        const int s = j % NS, kt = j >> 1, hk = j & 1;
-        uint8_t* st = sm + s * L::STAGE;
-        ptx::mbar_wait(&empty[s], ((j / NS) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], L::STAGE);
+        const int s = j % NA, kt = j >> 1, hk = j & 1;
+        uint8_t* st = sm + L::A0 + s * L::ASZ;
+        ptx::mbar_wait(&a_empty[s], ((j / NA) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&a_full[s], L::ASZ);
         const uint8_t* c0 = ds_head +
                             static_cast<size_t>(ds_chunk_offset(n_qt, kt, causal) + 2 * (qt - (causal ? kt : 0))) * DS_CHUNK +
                             hk * T64;
-        ptx::bulk_load(st, c0, T64, &full[s]);                  // queries [0, 64), keys 64 hk + [0, 64)
-        ptx::bulk_load(st + T64, c0 + DS_CHUNK, T64, &full[s]);  // queries [64, 128)
-        for (int c = 0; c < L::NB; ++c)
-          ptx::tma_load_2d(st + L::A + c * T64, &k64_map, &full[s], H * D + h * D + 64 * c, b * seq + kt * 128 + hk * 64);
+        ptx::bulk_load(st, c0, T64, &a_full[s]);                  // queries [0, 64), keys 64 hk + [0, 64)
+        ptx::bulk_load(st + T64, c0 + DS_CHUNK, T64, &a_full[s]);  // queries [64, 128)
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t id = ptx::idesc_bf16_f32(128, D, true, true);  // A, B MN-major
     for (int j = 0; j < steps; ++j) {
-      const int s = j % NS;
-      ptx::mbar_wait(&full[s], (j / NS) & 1);
+      const int sa = j % NA, sb = j % NK;
+      ptx::mbar_wait(&a_full[sa], (j / NA) & 1);
+      ptx::mbar_wait(&b_full[sb], (j / NK) & 1);
       ptx::tc_fence_after();
       // A: core matrices of 8 keys x 8 queries, 128 B apart along keys, 1024 B along queries
-      const uint64_t ad = ptx::umma_desc_noswz(ptx::smem_u32(sm + s * L::STAGE), 128, 1024);
-      const uint64_t bd = ptx::umma_desc_sw128(ptx::smem_u32(sm + s * L::STAGE + L::A), T64, 1024);
+      const uint64_t ad = ptx::umma_desc_noswz(ptx::smem_u32(sm + L::A0 + sa * L::ASZ), 128, 1024);
+      const uint64_t bd = ptx::umma_desc_sw128(ptx::smem_u32(sm + L::B0 + sb * L::BSZ), T64, 1024);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)  // 16 keys per MMA: A +256 B, B +2048 B (16 SW128 rows)
         ptx::mma_bf16_ss_w(tmem, ad + kk * 16, bd + kk * 128, id, (j > 0 || kk > 0) ? 1u : 0u);
-      ptx::mma_commit_w(&empty[s]);
+      ptx::mma_commit_w(&a_empty[sa]);
+      ptx::mma_commit_w(&b_empty[sb]);
     }
     ptx::mma_commit_w(acc_full);
   } else {
+    if (warp == 2 && lane == 0) {  // K ring (L2-resident re-reads)
+      for (int j = 0; j < steps; ++j) {
+        const int s = j % NK, kt = j >> 1, hk = j & 1;
+        uint8_t* st = sm + L::B0 + s * L::BSZ;
+        ptx::mbar_wait(&b_empty[s], ((j / NK) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&b_full[s], L::BSZ);
+        for (int c = 0; c < L::NB; ++c)
+          ptx::tma_load_2d(st + c * T64, &k64_map, &b_full[s], H * D + h * D + 64 * c, b * seq + kt * 128 + hk * 64);
+      }
+    }
+    __syncwarp();
     const int q = warp & 3;  // TMEM lane quarter of this warp (warps 2..5 -> 2, 3, 0, 1)
     ptx::mbar_wait(acc_full, 0);
     ptx::tc_fence_after();
@@ -841,13 +866,14 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = 1.4426950408889634f * scale;
   static std::atomic<uint64_t> attr{0};
-  // dQ GEMM ring depth (AMDP_ATTN_DQ_STAGES; measured best: head_dim 128 two stages = three CTAs per SM,
-  // head_dim 64 three = three CTAs per SM; scripts/attn_dq_probe.py)
+  // dQ GEMM dS ring depth (AMDP_ATTN_DQ_STAGES; the K ring is two deep).  Measured best: two
+  // (head_dim 128, 64 KB: three CTAs per SM) / three (head_dim 64, 64 KB); deeper rings with
+  // fewer CTAs per SM were slower (profiles/r02/dq_gemm)
   static const int dq_stages = getenv("AMDP_ATTN_DQ_STAGES") ? atoi(getenv("AMDP_ATTN_DQ_STAGES")) : (D > 64 ? 2 : 3);
-  auto dq_gemm = dq_stages == 2 ? fa_bwd_dq_gemm_kernel<D, 2> : dq_stages == 3 ? fa_bwd_dq_gemm_kernel<D, 3>
-                                                                               : fa_bwd_dq_gemm_kernel<D, 4>;
-  const size_t smem_g = 1024 + (dq_stages == 2 ? DqgSmem<D, 2>::BYTES : dq_stages == 3 ? DqgSmem<D, 3>::BYTES
-                                                                                       : DqgSmem<D, 4>::BYTES);
+  auto dq_gemm = dq_stages == 2 ? fa_bwd_dq_gemm_kernel<D, 2, 2> : dq_stages == 3 ? fa_bwd_dq_gemm_kernel<D, 3, 2>
+               : dq_stages == 4 ? fa_bwd_dq_gemm_kernel<D, 4, 2> : fa_bwd_dq_gemm_kernel<D, 5, 2>;
+  const size_t smem_g = 1024 + (dq_stages == 2 ? DqgSmem<D, 2, 2>::BYTES : dq_stages == 3 ? DqgSmem<D, 3, 2>::BYTES
+                                : dq_stages == 4 ? DqgSmem<D, 4, 2>::BYTES : DqgSmem<D, 5, 2>::BYTES);
   const size_t smem_kv = KvSmem<D>::BYTES + 1024, smem_q = QSmem<D>::BYTES + 1024;
   if (first_on_device(attr)) {
     int e = set_smem(fa_bwd_dkdv_kernel<D, false>, smem_kv);
