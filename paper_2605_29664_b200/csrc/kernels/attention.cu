@@ -106,7 +106,8 @@ size_t delta_bytes(int batch, int seq, int heads) {
 }  // namespace
 
 extern "C" size_t amdp_attention_bwd_scratch_bytes(int batch, int seq, int heads, int head_dim, int causal) {
-  if (batch <= 0 || seq <= 0 || heads <= 0 || !attention_tiled_bwd(seq, head_dim)) return 0;
+  // head_dim 80 keeps the dQ kernel that recomputes S / dP (attention_bwd_tc): no scratch
+  if (batch <= 0 || seq <= 0 || heads <= 0 || !attention_tiled_bwd(seq, head_dim) || head_dim == 80) return 0;
   return attention_bwd_ds_bytes(batch, seq, heads, causal ? 1 : 0);
 }
 

@@ -10,6 +10,8 @@ for f in sorted(glob.glob(os.path.join(sys.argv[1], "*.json"))):
         d = json.loads([x for x in open(f) if x.startswith("{")][-1])
     except Exception:  # noqa: BLE001
         continue
+    if d.get("impl") == "reference":
+        continue
     c = d["config"]
     pr = next((v for k, v in d["bubble"].items() if k.startswith("projected_")), None) or {}
     alt = pr.get("allreduce_update_variant") or {}
@@ -21,3 +23,25 @@ print("| run | model | parallelism | tokens/s (1 GPU) | e2e | MFU (spec / sustai
       "projected bubble (all-reduce updates) | projected tokens/s at D GPUs | SM MHz | memory GB |")
 print("|---|---|---|---|---|---|---|---|---|---|---|")
 print("\n".join(rows))
+
+# in-step kernel classes (present when the sweep ran with kernel timing: scripts/sweep_kt.sh)
+krows = []
+for f in sorted(glob.glob(os.path.join(sys.argv[1], "*.json"))):
+    try:
+        d = json.loads([x for x in open(f) if x.startswith("{")][-1])
+    except Exception:  # noqa: BLE001
+        continue
+    k = d.get("kernels") or {}
+    if not k:
+        continue
+    g = lambda n, f_="tflops": (k.get(n) or {}).get(f_) or "-"  # noqa: E731
+    tot = sum(v["ms"] for v in k.values()) or 1
+    share = lambda n: f"{100 * (k.get(n) or {}).get('ms', 0) / tot:.1f}%"  # noqa: E731
+    krows.append(f"| {os.path.basename(f)[:-5]} | {g('gemm_fwd')} | {g('gemm_dgrad')} | {g('gemm_wgrad')} | "
+                 f"{g('attn_fwd')} ({share('attn_fwd')}) | {g('attn_bwd')} ({share('attn_bwd')}) | "
+                 f"{g('layernorm', 'gbs')} ({share('layernorm')}) |")
+if krows:
+    print()
+    print("| run | GEMM fwd TF/s | dgrad TF/s | wgrad TF/s | attention fwd TF/s (share) | attention bwd TF/s (share) | LayerNorm GB/s (share) |")
+    print("|---|---|---|---|---|---|---|")
+    print("\n".join(krows))

@@ -44,9 +44,9 @@ def test_attention_workspace_sizes():
     256 B, then the dS^T scratch of the tiled kernels (one 16 KB chunk per 128-key tile and
     64-query half-block visited: causal n(n+1), bidirectional 2n^2 per sequence and head);
     the causal-agnostic size is the bidirectional upper bound; seq <= 128 (one-tile kernels)
-    needs no scratch."""
+    and head_dim 80 (dQ kernel recomputing S / dP) need no scratch."""
     L = _native.lib
-    for B, S, H, D in [(4, 2048, 16, 128), (4, 1024, 16, 64), (4, 512, 16, 64), (2, 768, 3, 80)]:
+    for B, S, H, D in [(4, 2048, 16, 128), (4, 1024, 16, 64), (4, 512, 16, 64), (2, 768, 3, 128)]:
         n = S // 128
         delta = (B * S * H * 4 + 255) // 256 * 256
         assert L.amdp_attention_bwd_scratch_bytes(B, S, H, D, 1) == B * H * n * (n + 1) * 16384
@@ -54,4 +54,5 @@ def test_attention_workspace_sizes():
         assert L.amdp_attention_bwd_workspace_causal(B, S, H, D, 1) == delta + B * H * n * (n + 1) * 16384
         assert L.amdp_attention_bwd_workspace(B, S, H, D) == L.amdp_attention_bwd_workspace_causal(B, S, H, D, 0)
     assert L.amdp_attention_bwd_scratch_bytes(4, 64, 4, 32, 1) == 0
+    assert L.amdp_attention_bwd_scratch_bytes(4, 2048, 32, 80, 1) == 0  # head_dim 80: recompute dQ kernel
     assert L.amdp_attention_bwd_workspace(4, 64, 4, 32) == 4 * 64 * 4 * 4

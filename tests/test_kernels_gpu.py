@@ -365,8 +365,8 @@ def test_attention_bwd_ds_scratch(K, N, B, S, H, D, causal, padded):
     key_len = torch.tensor([S, S // 2 + 17, 1, 100][:B], dtype=torch.int32, device="cuda") if padded else None
     out, lse = K.attention_fwd(qkv, B, S, H, D, causal, key_len=key_len)
     delta = (dout.float() * out.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).contiguous()
-    assert N.lib.amdp_attention_bwd_scratch_bytes(B, S, H, D, int(causal)) == B * H * 16384 * (
-        (S // 128) * (S // 128 + 1) if causal else 2 * (S // 128) ** 2)
+    assert N.lib.amdp_attention_bwd_scratch_bytes(B, S, H, D, int(causal)) == (0 if D == 80 else B * H * 16384 * (
+        (S // 128) * (S // 128 + 1) if causal else 2 * (S // 128) ** 2))
     d1 = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal, key_len=key_len)
     d2 = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal, key_len=key_len)
     d0 = K.attention_bwd_delta(qkv, dout, lse, delta, B, S, H, D, causal, key_len=key_len, scratch=False)
