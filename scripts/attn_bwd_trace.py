@@ -1,4 +1,5 @@
-"""Per-phase clock64 trace of CTA 0 (heaviest query tile) of the tcgen05 dQ kernel."""
+"""Per-phase clock64 trace of CTA 0 of the tcgen05 dQ kernel (AMDP_ATTN_DQ=recompute) and of
+the dK/dV kernel (times relative to its first recorded event)."""
 import sys, os, ctypes, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_29664_b200 import kernels as K, _native as N
@@ -19,6 +20,8 @@ print("n  " + " ".join(f"{x:>12s}" for i, x in enumerate(names) if i != 7))
 for n in range(32):
     print(f"{n:2d} " + " ".join(f"{int(t[s, n]) - t0 if t[s, n] else -1:12d}" for s in range(10) if s != 7))
 
+d = t[16:24, :]
+t0 = int(d[d > 0].min()) if (d > 0).any() else t0
 names = ["mma:u_full", "mma:S issued", "mma:p_full", "mma:dVdK issued", "wgA:s_full", "wgA:computed", "prod:u_empty", "wgA:arrived"]
 print("dK/dV kernel CTA 0 (kt = 0), per 64-query half unit u (softmax columns: warpgroup A only)")
 print("n  " + " ".join(f"{x:>14s}" for x in names))
