@@ -752,9 +752,12 @@ struct DqgSmem {
 
 template <int D, int NA_, int NB_>
 __global__ void __launch_bounds__(192, 1)
-    fa_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap k64_map, const uint8_t* __restrict__ ds_ws,
-                          bf16* __restrict__ dqkv, int seq, int H, int n_qt, int BH, float scale, int causal) {
+    fa_bwd_dq_gemm_kernel(const __grid_constant__ CUtensorMap k64_map, const __grid_constant__ CUtensorMap dq_map,
+                          const uint8_t* __restrict__ ds_ws, bf16* __restrict__ dqkv, int seq, int H, int n_qt, int BH,
+                          float scale, int causal) {
   using L = DqgSmem<D, NA_, NB_>;
+  static_assert(D % 64 == 0, "the TMA-store epilogue writes 64-column boxes");
+  static_assert(NA_ * 2 * T64 >= 4 * (D / 64) * 4096, "dQ staging reuses the dS ring");
   constexpr int NA = L::NA, NK = L::NK;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -797,6 +800,10 @@ __global__ void __launch_bounds__(192, 1)
         const int s = j % NA, kt = j >> 1, hk = j & 1;
         uint8_t* st = sm + L::A0 + s * L::ASZ;
         ptx::mbar_wait(&a_empty[s], ((j / NA) & 1) ^ 1);
+#ifdef FA_DQG_NODS  // ablation: no dS^T loads
+        ptx::mbar_arrive(&a_full[s]);
+        continue;
+#endif
         ptx::mbar_arrive_expect_tx(&a_full[s], L::ASZ);
         const uint8_t* c0 = ds_head +
                             static_cast<size_t>(ds_chunk_offset(n_qt, kt, causal) + 2 * (qt - (causal ? kt : 0))) * DS_CHUNK +
@@ -828,6 +835,10 @@ __global__ void __launch_bounds__(192, 1)
         const int s = j % NK, kt = j >> 1, hk = j & 1;
         uint8_t* st = sm + L::B0 + s * L::BSZ;
         ptx::mbar_wait(&b_empty[s], ((j / NK) & 1) ^ 1);
+#ifdef FA_DQG_NOK  // ablation: no K loads
+        ptx::mbar_arrive(&b_full[s]);
+        continue;
+#endif
         ptx::mbar_arrive_expect_tx(&b_full[s], L::BSZ);
         for (int c = 0; c < L::NB; ++c)
           ptx::tma_load_2d(st + c * T64, &k64_map, &b_full[s], H * D + h * D + 64 * c, b * seq + kt * 128 + hk * 64);
@@ -837,9 +848,40 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;  // TMEM lane quarter of this warp (warps 2..5 -> 2, 3, 0, 1)
     ptx::mbar_wait(acc_full, 0);
     ptx::tc_fence_after();
-    const int row = q * 32 + lane;
-    bf16* dst = dqkv + (static_cast<size_t>(b) * seq + qt * 128 + row) * (static_cast<size_t>(3) * H * D) + h * D;
-    tmem_row_to_global<D>(tmem + (static_cast<uint32_t>(q * 32) << 16), dst, scale);
+    // Epilogue: bf16(scale * dQ) rows -> this warp's SW128 staging blocks (the dS ring is free
+    // once every MMA retired: 32 rows x 64 columns, 16-byte unit v of row r at v ^ (r & 7),
+    // conflict-free) -> one TMA store per 64-column block (the per-row 16-byte stores this
+    // replaces were a quarter of the kernel: 70 -> 53 us without them at the 1.3B shape)
+    uint8_t* stg = sm + L::A0 + q * (D / 64) * 4096;
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t lo[32], hi[32];
+      const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + 64 * c;
+      ptx::tmem_ld_32x32b_x32(ta, lo);
+      ptx::tmem_ld_32x32b_x32(ta + 32, hi);
+      ptx::tmem_ld_wait();
+      uint8_t* rowp = stg + c * 4096 + lane * 128;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const uint32_t* src = v < 4 ? lo + 8 * v : hi + 8 * (v - 4);
+        uint4 pk;
+        pk.x = pack2(__uint_as_float(src[0]) * scale, __uint_as_float(src[1]) * scale);
+        pk.y = pack2(__uint_as_float(src[2]) * scale, __uint_as_float(src[3]) * scale);
+        pk.z = pack2(__uint_as_float(src[4]) * scale, __uint_as_float(src[5]) * scale);
+        pk.w = pack2(__uint_as_float(src[6]) * scale, __uint_as_float(src[7]) * scale);
+        *reinterpret_cast<uint4*>(rowp + ((v ^ (lane & 7)) << 4)) = pk;
+      }
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+#ifndef FA_DQG_NOEPI  // ablation: no dQ stores
+    if (lane == 0) {
+      for (int c = 0; c < D / 64; ++c)
+        ptx::tma_store_2d(&dq_map, stg + c * 4096, h * D + 64 * c, b * seq + qt * 128 + q * 32);
+      ptx::bulk_commit();
+      ptx::bulk_wait<0>();  // stores complete before the CTA exits (as the GEMM epilogue does)
+    }
+#endif
     ptx::tc_fence_before();
   }
   __syncthreads();
@@ -868,19 +910,21 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
   static std::atomic<uint64_t> attr{0};
   // dQ GEMM dS ring depth (AMDP_ATTN_DQ_STAGES; the K ring is two deep).  Measured best: two
   // (head_dim 128, 64 KB: three CTAs per SM) / three (head_dim 64, 64 KB); deeper rings with
-  // fewer CTAs per SM were slower (profiles/r02/dq_gemm)
+  // fewer CTAs per SM were slower (profiles/r02/dq_gemm).  head_dim 80 has no dQ GEMM.
+  constexpr int DG = D % 64 == 0 ? D : 64;
   static const int dq_stages = getenv("AMDP_ATTN_DQ_STAGES") ? atoi(getenv("AMDP_ATTN_DQ_STAGES")) : (D > 64 ? 2 : 3);
-  auto dq_gemm = dq_stages == 2 ? fa_bwd_dq_gemm_kernel<D, 2, 2> : dq_stages == 3 ? fa_bwd_dq_gemm_kernel<D, 3, 2>
-               : dq_stages == 4 ? fa_bwd_dq_gemm_kernel<D, 4, 2> : fa_bwd_dq_gemm_kernel<D, 5, 2>;
-  const size_t smem_g = 1024 + (dq_stages == 2 ? DqgSmem<D, 2, 2>::BYTES : dq_stages == 3 ? DqgSmem<D, 3, 2>::BYTES
-                                : dq_stages == 4 ? DqgSmem<D, 4, 2>::BYTES : DqgSmem<D, 5, 2>::BYTES);
+  auto dq_gemm = dq_stages == 2 ? fa_bwd_dq_gemm_kernel<DG, 2, 2> : dq_stages == 3 ? fa_bwd_dq_gemm_kernel<DG, 3, 2>
+               : dq_stages == 4 ? fa_bwd_dq_gemm_kernel<DG, 4, 2> : fa_bwd_dq_gemm_kernel<DG, 5, 2>;
+  const size_t smem_g = 1024 + (dq_stages == 2 ? DqgSmem<DG, 2, 2>::BYTES : dq_stages == 3 ? DqgSmem<DG, 3, 2>::BYTES
+                                : dq_stages == 4 ? DqgSmem<DG, 4, 2>::BYTES : DqgSmem<DG, 5, 2>::BYTES);
+  if (D != DG) ds_ws = nullptr;
   const size_t smem_kv = KvSmem<D>::BYTES + 1024, smem_q = QSmem<D>::BYTES + 1024;
   if (first_on_device(attr)) {
     int e = set_smem(fa_bwd_dkdv_kernel<D, false>, smem_kv);
     if (!e) e = set_smem(fa_bwd_dkdv_kernel<D, true>, smem_kv);
     if (!e) e = set_smem(fa_bwd_dq_kernel<D, false>, smem_q);
     if (!e) e = set_smem(fa_bwd_dq_kernel<D, true>, smem_q);
-    if (!e) e = set_smem(dq_gemm, smem_g);
+    if (!e && D == DG) e = set_smem(dq_gemm, smem_g);
     if (e) {
       attr.store(0);
       return e;
@@ -893,7 +937,9 @@ int launch_bwd_tc(const bf16* qkv, const bf16* dout, const float* lse, const flo
                              scale, causal, key_len, ds_ws);
   if (e != cudaSuccess) return e;
   if (ds_ws != nullptr) {  // dQ = dS K from the stored dS^T
-    e = launch_pdl(dq_gemm, dim3(nt * H * B), dim3(192), smem_g, st, q64, ds_ws, dqkv, S, H, nt,
+    CUtensorMap dq_out;  // dq columns of dqkv, 64 x 32 boxes (the epilogue's TMA stores)
+    if (!tma_map_bf16_2d(&dq_out, dqkv, ldq, rows, ldq, 64, 32)) return AMDP_ERR_TMA;
+    e = launch_pdl(dq_gemm, dim3(nt * H * B), dim3(192), smem_g, st, q64, dq_out, ds_ws, dqkv, S, H, nt,
                    H * B, scale, causal);
     return e != cudaSuccess ? e : cudaGetLastError();
   }
