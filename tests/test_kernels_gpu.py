@@ -489,6 +489,32 @@ def test_embedding_bwd_deterministic(K, ntok, S, V, Hd):
     assert _rel(outs[0], rte) < 1e-6
 
 
+def test_embedding_bwd_sequential_order(K):
+    """Each token's rows are summed in position order starting from zero, then added to the
+    table: bit-identical to that sequential fp32 sum (numpy), also for a run of several hundred
+    rows (a BERT padding-token run; the kernel batches its row loads) and runs of every length
+    around the 8-row batching boundary."""
+    import numpy as np
+    torch.manual_seed(10)
+    ntok, S, V, Hd = 2048, 512, 64, 64
+    tok = torch.randint(1, V, (ntok,), device="cuda", dtype=torch.int32)
+    tok[torch.rand(ntok, device="cuda") < 0.3] = 0  # one long run
+    for n in range(1, 18):  # tokens 40 + n: runs of exactly n rows
+        tok[(n * 97) % 1500:(n * 97) % 1500 + n] = 40 + n
+    dx = torch.randn(ntok, Hd, device="cuda").bfloat16()
+    dwte = torch.full((V, Hd), 0.25, device="cuda")
+    dwpe = torch.zeros(S, Hd, device="cuda")
+    K.embedding_bwd(tok, dx, dwte, dwpe, S)
+    torch.cuda.synchronize()
+    t = tok.cpu().numpy()
+    x = dx.float().cpu().numpy()
+    acc = np.zeros((V, Hd), dtype=np.float32)
+    for p in range(ntok):  # position order within every token's run
+        acc[t[p]] += x[p]
+    want = np.float32(0.25) + acc
+    assert np.array_equal(dwte.cpu().numpy(), want)
+
+
 def test_xent_loss_deterministic(K):
     """The loss sum is a fixed-order reduction of per-row losses: bitwise repeatable."""
     torch.manual_seed(9)
