@@ -1,6 +1,10 @@
 // Flash-attention backward on the 5th-generation tensor cores (sm_100a).
 //
-// Two deterministic kernels (no atomics), each with its accumulators in TMEM:
+// Default (head_dim 64 / 128): the dK/dV kernel below also stores dS^T (DS_CHUNK layout) and
+// fa_bwd_dq_gemm_kernel computes dQ = scale * dS K from it — five GEMM units and one softmax
+// pass.  The dQ kernel described second recomputes S, dP and the softmax instead; it serves
+// head_dim 80 and AMDP_ATTN_DQ=recompute (A/B).
+// Deterministic kernels (no atomics), each with its accumulators in TMEM:
 //   dK/dV : one CTA per (128-key tile, head, sequence), looping over 64-query halves:
 //           S^T = K Q_i^T, dP^T = V dO_i^T                    (SS, M=128 keys, N=64 queries)
 //           P^T = 2^(S^T c - lse), dS^T = P^T (dP^T - delta)  (thread = key, one warpgroup
